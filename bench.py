@@ -1,0 +1,403 @@
+#!/usr/bin/env python
+"""bench.py -- spGEMM GFLOPS (2 x intermediate products / device time).
+
+Workload (BASELINE.json configs[1], the config the metric is quoted on):
+C = A.A, A = 3D 27-point FEM-like stencil on a 64^3 grid (262,144 rows,
+6,859,000 nnz), fp16 in / fp32 accumulate, synthetic (generated
+deterministically, no dataset).  A "step" is one full spGEMM: CSR A (and B)
+resident in HBM -> CSR C in HBM, through the C ABI (tsg_spgemm), with every
+phase, allocation and size readback inside the timed region (PAPER.md:585
+counts allocations).  L2 (126 MB) is flushed with a 256 MB write before
+every timed step, outside the timed span.
+
+  python bench.py [--gpus N --steps K --warmup W] [--config fem27]
+  python bench.py --impl reference ...   (the reference CPU implementation)
+
+N > 1 (torchrun, one rank per GPU, NCCL): A is split into tile-row panels
+balanced by rows; B is broadcast from rank 0 over NVLink each step (the
+exchange step of SURVEY.md 8(e)); value = total flops of all ranks / max
+over ranks of the step time.  Total work is fixed: "scaling": "strong".
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "spGEMM GFLOPS (2x intermediate products / device time)"
+CONFIG_TEXT = {
+    "poisson": "C = A.A, 2D 5-point Poisson 256x256 (65,536 rows)",
+    "fem27": "C = A.A, 3D 27-point FEM-like stencil 64^3 (262,144 rows, 6.86M nnz)",
+    "rmat": "C = A.A, R-MAT 2^20 rows, edge factor 16, (0.45,0.15,0.15,0.25)",
+    "rect": "C = A.B, 1M x 500k . 500k x 1M, density 1e-5",
+    "amg": "C = (R.A).P, 7-point Laplacian 128^3, trilinear prolongation",
+}
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--config", default="fem27", choices=list(CONFIG_TEXT))
+    p.add_argument("--mode", default="tensor", choices=["tensor", "ordered"])
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--cpu-sample-runs", type=int, default=3)
+    return p.parse_args()
+
+
+# ----------------------------------------------------------------------------
+# clocks sampler (nvidia-smi during the timed region)
+class Clocks:
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.1)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self) -> dict:
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no-samples"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if len(s) > 3 + i and s[3 + i].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+# ----------------------------------------------------------------------------
+def operands(config):
+    from paper_2009_14600_b200 import workloads as W
+    return W.make(config)
+
+
+def algorithmic_bytes(st, nnzA, nnzB, rowsA, rowsC, same):
+    """SURVEY.md 8(d) compulsory-traffic model per phase (T=16 tiles:
+    tile record 32 B mask + 8 B coords + 4 B offset, fp16 in, fp32 out, 8 B pairs)."""
+    tA, tB = st["tiles_a"], st["tiles_b"]
+    P, S, cnt, nnzC = st["filtered_pairs"], st["segments"], st["counted_elements"], st["nnz_c"]
+    conv = (8 * (rowsA + 1) + 8 * nnzA) + (44 * tA + 2 * nnzA)
+    if not same:
+        conv += (8 * (rowsA + 1) + 8 * nnzB) + (44 * tB + 2 * nnzB)
+    return {
+        "convert": conv,
+        "task_list": 40 * (tA + tB) + 8 * P,      # enumerate + filter (tile metadata in, pairs out)
+        "sort": 16 * P + 8 * S,                    # read + write pairs, segment table
+        "counting": 8 * P + 32 * (tA + tB) + 4 * S,
+        "multiply": 8 * P + 44 * (tA + tB) + 2 * (nnzA + nnzB) + 44 * S + 4 * cnt,
+        "compaction": 44 * S + 4 * cnt + 8 * (rowsC + 1) + 8 * nnzC,
+    }
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+    from paper_2009_14600_b200 import _lib as L
+    from paper_2009_14600_b200 import workloads as W
+    from paper_2009_14600_b200.tilemul import Context, Csr, _view
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream(dev)
+    ctx = Context(device=local, stream=stream.cuda_stream)
+
+    mats = operands(args.config)
+    chain = len(mats) == 3
+    if chain:
+        Afull, Bs = mats[0], mats[1:]
+    elif len(mats) == 2:
+        Afull, Bs = mats[0], [mats[1]]
+    else:
+        Afull, Bs = mats[0], [mats[0]]
+    same = len(mats) == 1 and world == 1
+
+    # rank panel of A: tile-row aligned contiguous rows
+    tile_rows = (Afull.rows + 15) // 16
+    t0 = (tile_rows * rank) // world
+    t1 = (tile_rows * (rank + 1)) // world
+    r0, r1 = min(16 * t0, Afull.rows), min(16 * t1, Afull.rows)
+    lo, hi = Afull.row_ptr[r0], Afull.row_ptr[r1]
+    Apanel = Csr(r1 - r0, Afull.cols, (Afull.row_ptr[r0:r1 + 1] - lo).astype(np.int64),
+                 Afull.col[lo:hi], Afull.val[lo:hi])
+
+    # flops of this rank: 2 * C-bar over the chain stages (computed, never hard-coded)
+    cb = W.cbar(Apanel, Bs[0])
+    if chain:  # second stage C-bar needs the structure of R.A (untimed setup)
+        RA = ctx.spgemm(Apanel, Bs[0]).C
+        cb += W.cbar(RA, Bs[1])
+    keep = []
+    A_dev = Apanel.to_device(dev)
+    a_view = _view(A_dev, keep)
+    # B lives on rank 0 and is broadcast each step (N>1); same-pointer view for A.A at N=1
+    B_dev = [B.to_device(dev) for B in Bs]
+    b_views = [a_view] if same else [_view(B, keep) for B in B_dev]
+    opts = L.tsg_options()
+    ctx._lib.tsg_default_options(opts)
+    opts.mode = L.TSG_MODE_ORDERED if args.mode == "ordered" else L.TSG_MODE_TENSOR
+
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+
+    def one_step(stats=None):
+        if world > 1:
+            for B in B_dev:
+                for t in (B.row_ptr, B.col, B.val):
+                    dist.broadcast(t, src=0)
+        if chain:
+            import ctypes as C
+            arr = (C.POINTER(L.tsg_csr) * 3)(C.pointer(a_view), C.pointer(b_views[0]), C.pointer(b_views[1]))
+            co = L.tsg_csr_out()
+            co.mem = L.TSG_MEM_DEVICE
+            rc = ctx._lib.tsg_spgemm_chain(ctx.handle, 3, arr, C.byref(co), C.byref(opts),
+                                           C.byref(stats) if stats is not None else None)
+        else:
+            co = L.tsg_csr_out()
+            co.mem = L.TSG_MEM_DEVICE
+            rc = ctx.spgemm_raw(a_view, b_views[0], opts, co, stats)
+        if rc != 0:
+            raise RuntimeError(ctx._lib.tsg_last_error(ctx.handle).decode())
+        return co
+
+    def timed(k, fn):
+        times = []
+        for _ in range(k):
+            flush.fill_(1.0)
+            if world > 1:
+                dist.barrier()
+            torch.cuda.synchronize()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            out = fn()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            times.append(e0.elapsed_time(e1))
+            if out is not None:
+                ctx.free(out)
+        return times
+
+    for _ in range(args.warmup):
+        ctx.free(one_step())
+    torch.cuda.synchronize()
+    launches0 = ctx.launch_count()
+    with Clocks(local) as clk:
+        times = timed(args.steps, one_step)
+    launches = ctx.launch_count() - launches0
+    ms = float(np.mean(times))
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_max = float(t.item())
+        c = torch.tensor([cb], dtype=torch.float64, device=dev)
+        dist.all_reduce(c)
+        cb_total = int(c.item())
+    else:
+        ms_max, cb_total = ms, cb
+    value = 2.0 * cb_total / (ms_max * 1e-3) / 1e9
+
+    # ---- per-phase device times (separate run, phase events on) -> roofline
+    st = L.tsg_run_stats()
+    opts.phase_timing = 1
+    phase_ms = {}
+    for _ in range(3):
+        flush.fill_(1.0)
+        torch.cuda.synchronize()
+        st = L.tsg_run_stats()
+        ctx.free(one_step(st))
+        for ph in ("convert", "task_list", "sort", "counting", "multiply", "compaction", "total"):
+            phase_ms.setdefault(ph, []).append(ctx.last_phase_ms(ph) if not chain else getattr(st, ph) * 1e3)
+    opts.phase_timing = 0
+    phase_ms = {k: float(np.median(v)) for k, v in phase_ms.items()}
+    sd = st.as_dict()
+    nnzB = Bs[0].nnz
+    bytes_ = algorithmic_bytes(sd, Apanel.nnz, nnzB, Apanel.rows, Apanel.rows, same)
+    from pathlib import Path
+    peaks = json.loads((Path(ROOT) / "MEASURED_PEAKS.json").read_text()) if (Path(ROOT) / "MEASURED_PEAKS.json").exists() else {}
+    peak = float(peaks.get("hbm_gbs", 6650.0))
+    peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
+    dom = max((k for k in bytes_), key=lambda k: phase_ms.get(k, 0.0))
+    achieved = bytes_[dom] / (phase_ms[dom] * 1e-3) / 1e9 if phase_ms.get(dom) else 0.0
+
+    # ---- e2e: host CSR in (pinned), host CSR out, through the public API
+    pin = []
+    def pinned(a):
+        t = torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
+        pin.append(t)
+        return t
+    Ah = Csr(Apanel.rows, Apanel.cols, pinned(Apanel.row_ptr).numpy(), pinned(Apanel.col).numpy(),
+             pinned(Apanel.val).numpy())
+    Bh = [Csr(B.rows, B.cols, pinned(B.row_ptr).numpy(), pinned(B.col).numpy(), pinned(B.val).numpy()) for B in Bs]
+    e2e_stats = {}
+
+    def e2e_step():
+        import ctypes as C
+        keep2 = []
+        av = _view(Ah, keep2)
+        bvs = [av] if same else [_view(B, keep2) for B in Bh]
+        co = L.tsg_csr_out()
+        co.mem = L.TSG_MEM_HOST
+        st2 = L.tsg_run_stats()
+        if chain:
+            arr = (C.POINTER(L.tsg_csr) * 3)(C.pointer(av), C.pointer(bvs[0]), C.pointer(bvs[1]))
+            rc = ctx._lib.tsg_spgemm_chain(ctx.handle, 3, arr, C.byref(co), C.byref(opts), C.byref(st2))
+        else:
+            rc = ctx.spgemm_raw(av, bvs[0], opts, co, st2)
+        if rc != 0:
+            raise RuntimeError(ctx._lib.tsg_last_error(ctx.handle).decode())
+        e2e_stats["h2d"] = int(st2.h2d_bytes)
+        e2e_stats["d2h"] = int(st2.d2h_bytes)
+        return co
+
+    for _ in range(2):
+        ctx.free(e2e_step())
+    e2e_times = timed(max(3, args.steps // 2), e2e_step)
+    e2e_ms = float(np.mean(e2e_times))
+    if world > 1:
+        t = torch.tensor([e2e_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    e2e_value = 2.0 * cb_total / (e2e_ms * 1e-3) / 1e9
+
+    line = {
+        "metric": METRIC, "value": round(value, 3), "unit": "GFLOPS", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_max, 4),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f16-in/f32-acc",
+        "data": "synthetic (deterministic generator, paper_2009_14600_b200/workloads.py)",
+        "config": {"workload": CONFIG_TEXT[args.config], "config": args.config, "mode": args.mode,
+                   "flops_per_step": 2 * cb_total, "cbar": cb_total,
+                   "parallelism": f"A tile-row panels x{world}, B broadcast" if world > 1 else "single GPU",
+                   "l2": "flushed (256 MB write) before every timed step",
+                   "nnz_a": Afull.nnz, "nnz_c": sd["nnz_c"], "tiles_a": sd["tiles_a"],
+                   "filtered_pairs": sd["filtered_pairs"], "segments": sd["segments"]},
+        "e2e": {"value": round(e2e_value, 3), "unit": "GFLOPS", "ms_per_step": round(e2e_ms, 4),
+                "h2d_bytes_per_step": e2e_stats.get("h2d"), "d2h_bytes_per_step": e2e_stats.get("d2h")},
+        "gpu_launches": int(launches),
+        "gpu_launches_per_step": launches / max(1, args.steps),
+        "phase_ms": {k: round(v, 4) for k, v in phase_ms.items()},
+        "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": peak,
+                     "peak_source": peak_src, "unit": "GB/s", "frac": round(achieved / peak, 4),
+                     "algorithmic_bytes": int(bytes_[dom]), "traffic": None},
+        "clocks": clk.summary(),
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(args, mats, 2 * cb_total)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def cpu_run(mats, threads):
+    from oracle import ref
+    if len(mats) == 1:
+        return ref.spgemm(mats[0], threads=threads)
+    if len(mats) == 2:
+        return ref.spgemm(mats[0], mats[1], threads=threads)
+    return ref.chain(mats, threads=threads)
+
+
+def cpu_baseline(args, mats, flops):
+    """The reference tilemul (oracle/_ref, compiled unmodified) on host cores."""
+    from oracle import ref
+    if not ref.available():
+        return {"value": None, "unavailable": "oracle/_ref/libref_tilemul.so not built"}
+    cores = os.cpu_count() or 1
+    secs = []
+    for _ in range(max(1, args.cpu_sample_runs)):
+        r = cpu_run(mats, threads=cores)
+        secs.append(r.times["total"])
+    s = statistics.median(secs)
+    return {"value": round(flops / s / 1e9, 4), "unit": "GFLOPS", "cores": cores, "kind": "reference",
+            "sample": f"{len(secs)} full runs of the same workload (spgemm_square / pass composition, "
+                      f"pairing on, threads={cores}); median {s:.3f} s; input tiling untimed (SPEC.md:522)"}
+
+
+def run_reference(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from oracle import ref
+    if not ref.available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libref_tilemul.so not built"}))
+        return
+    from paper_2009_14600_b200 import workloads as W
+    mats = operands(args.config)
+    cb = W.cbar(mats[0], mats[1] if len(mats) > 1 else mats[0])
+    if len(mats) == 3:
+        RA = cpu_run(mats[:2], 1)  # only to size the second stage's C-bar
+        from paper_2009_14600_b200.tilemul import Csr
+        cb += W.cbar(Csr(RA.rows, RA.cols, RA.row_ptr, RA.col, RA.val), mats[2])
+    cores = os.cpu_count() or 1
+    steps = max(1, min(args.steps, 5))
+    warm = max(0, min(args.warmup, 1))
+    for _ in range(warm):
+        cpu_run(mats, cores)
+    secs = [cpu_run(mats, cores).times["total"] for _ in range(steps)]
+    s = float(np.mean(secs))
+    v = 2 * cb / s / 1e9
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": round(v, 4), "unit": "GFLOPS", "n_gpus": world,
+        "steps": steps, "warmup": warm, "ms_per_step": round(s * 1e3, 3), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f16-in/f32-acc (CPU, sequential fp32)",
+        "data": "synthetic", "config": {"workload": CONFIG_TEXT[args.config], "config": args.config,
+                                        "flops_per_step": 2 * cb},
+        "cpu_baseline": {"value": round(v, 4), "unit": "GFLOPS", "cores": cores, "kind": "reference",
+                         "sample": f"{steps} full runs, pairing on, threads={cores}"},
+        "e2e": {"value": round(v, 4), "unit": "GFLOPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

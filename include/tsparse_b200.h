@@ -1,0 +1,165 @@
+/* tsparse_b200.h -- C ABI of the B200-native tSparse spGEMM path (C = A.B).
+ *
+ * This is the drop-in boundary for the reference's hot path.  The reference
+ * (tilemul, /root/reference/proj) is a C++ library whose hot path is the
+ * pass chain
+ *
+ *   from_element_coo                      proj/include/tilemul/tile_format.hpp:71-72
+ *   enumerate_pairs / filter_zero_products proj/include/tilemul/pipeline.hpp:46-52
+ *   sort_and_segment                      proj/include/tilemul/pipeline.hpp:56-57
+ *   counting_pass                         proj/include/tilemul/kernels.hpp:52-53
+ *   multiply_pass                         proj/include/tilemul/kernels.hpp:62-64
+ *   compact                               proj/include/tilemul/kernels.hpp:67
+ *   spgemm_square                         proj/include/tilemul/kernels.hpp:88-89
+ *   to_element_coo                        proj/include/tilemul/tile_format.hpp:75
+ *
+ * tsg_spgemm() replaces that whole chain in one call (sorted duplicate-free
+ * COO == CSR, so CSR is the interchange format: SURVEY.md Appendix A.2).
+ * tsg_spgemm_chain() replaces the R.A.P composition with the fp32 -> binary16
+ * downcast between stages (proj/src/kernels.cpp:239-258).  The per-phase
+ * functions are not exported individually: on a GPU they would force a
+ * device<->host copy per phase.  include/tilemul_gpu.hpp re-exposes the
+ * reference's C++ names (tilemul::spgemm_square etc.) on top of this ABI.
+ *
+ * Plain C: no torch, no CUDA types.  Pointers are host or device as the
+ * `mem` field says.  Every call is synchronous at return and deterministic
+ * (byte-identical output for any launch configuration or GPU count).
+ * One context per host thread.
+ */
+#ifndef TSPARSE_B200_H
+#define TSPARSE_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TSG_ABI_VERSION 1
+
+/* Status codes mirror the reference CLI exit codes
+ * (proj/tools/tilemul.cpp:30-35,285-306; proj/include/tilemul/errors.hpp:9-51). */
+typedef enum {
+  TSG_OK = 0,
+  TSG_ERR_OTHER = 1,      /* tilemul::Error (anything else), CUDA failures      */
+  TSG_ERR_INVARIANT = 2,  /* InvariantError: unsorted/duplicate/out-of-range CSR */
+  TSG_ERR_OVERFLOW = 3,   /* OverflowError: |x| > 65504 or non-finite input       */
+  TSG_ERR_DIMENSION = 4,  /* DimensionError: A.cols != B.rows                      */
+  TSG_ERR_PRECISION = 5   /* PrecisionError: non-finite accumulator               */
+} tsg_status;
+
+typedef enum { TSG_F16 = 0, TSG_F32 = 1, TSG_F64 = 2 } tsg_dtype; /* value carrier */
+typedef enum { TSG_MEM_HOST = 0, TSG_MEM_DEVICE = 1 } tsg_mem;
+
+/* Numeric mode of the multiply.
+ * TENSOR:  fp16 x fp16 -> fp32 on the tensor cores (mma.m16n8k16), the
+ *          tSparse design.  Bit-exact wherever partial sums are exact
+ *          (integer / dyadic inputs), else within the stated tolerance.
+ * ORDERED: CUDA-core fp32 adds, one rounding per product in ascending k,
+ *          no FMA contraction: bit-identical to dense_spgemm_mixed_ordered
+ *          (proj/src/oracle.cpp:102-121) on every input. */
+typedef enum { TSG_MODE_TENSOR = 0, TSG_MODE_ORDERED = 1 } tsg_mode;
+
+/* Read-only CSR view: rows sorted by column, no duplicates (== the
+ * reference's ElementCoo invariant, proj/include/tilemul/coo.hpp:11-33). */
+typedef struct {
+  int64_t rows, cols, nnz;
+  const int64_t* row_ptr; /* rows + 1 */
+  const int32_t* col;     /* nnz      */
+  const void* val;        /* nnz values of type `dtype` (TSG_F16 = binary16 bits) */
+  int32_t dtype;          /* tsg_dtype */
+  int32_t mem;            /* tsg_mem   */
+} tsg_csr;
+
+/* Output CSR, allocated by the library (fp32 values, like compact()'s
+ * Fp32Stored output, proj/src/kernels.cpp:205-220).  Release with
+ * tsg_free_csr().  `mem` is set by the caller before the call. */
+typedef struct {
+  int64_t rows, cols, nnz;
+  int64_t* row_ptr;
+  int32_t* col;
+  float* val;
+  int32_t mem;
+  int32_t _pad;
+  void* _owner; /* library bookkeeping */
+} tsg_csr_out;
+
+/* Optional 16x16 tiled view of C (pre-CSR), for the tile-structure parity
+ * bridge: tile coords, 16 row masks (u16, bit c of row r =
+ * slot (r,c)), element offsets (row-major bit order), realised values.
+ * Host memory, allocated by the library; release with tsg_free_tiles(). */
+typedef struct {
+  int64_t ntiles, nnz;
+  uint32_t* tile_row;
+  uint32_t* tile_col;
+  uint16_t* row_masks; /* 16 per tile */
+  uint64_t* elem_index;
+  float* val;
+} tsg_tiles_out;
+
+typedef struct {
+  int32_t mode;           /* tsg_mode (default TENSOR)                          */
+  int32_t drop_nonfinite; /* from_element_coo(..., drop_nonfinite) semantics    */
+  int32_t phase_timing;   /* record CUDA events per phase into tsg_run_stats    */
+  int32_t want_tiles;     /* also fill a tsg_tiles_out (host) for parity tests  */
+} tsg_options;
+
+/* Phase names follow PhaseTiming (proj/include/tilemul/report.hpp:10-17)
+ * plus the two boundary conversions the GPU path owns.  Seconds of device
+ * time between CUDA events; zero unless options.phase_timing. */
+typedef struct {
+  double convert;    /* CSR -> 16x16 tiles (both operands)          */
+  double task_list;  /* enumerate + zero-product filter             */
+  double sort;       /* per-tile-row sort by output tile, segments  */
+  double counting;   /* boolean OR popcount + prefix sum            */
+  double multiply;   /* SEaC numeric                                */
+  double compaction; /* fused with tiled -> CSR output              */
+  double total;      /* first kernel to last, device time           */
+  /* counters (T = 16 tiles) */
+  uint64_t tiles_a, tiles_b, raw_pairs, filtered_pairs, segments;
+  uint64_t counted_elements; /* symbolic nnz(C), tile-size invariant      */
+  uint64_t nnz_c;            /* realised nnz(C)                            */
+  uint64_t cbar;             /* sum_k nnzA(:,k) * nnzB(k,:)  (flops / 2)  */
+  uint64_t kernel_launches;  /* own kernels launched by this call         */
+  uint64_t h2d_bytes, d2h_bytes;
+} tsg_run_stats;
+
+typedef struct tsg_ctx tsg_ctx;
+
+void tsg_default_options(tsg_options* opt);
+
+/* device < 0: current device.  stream: cudaStream_t or NULL (own stream). */
+int tsg_create(tsg_ctx** ctx, int device, void* stream);
+int tsg_destroy(tsg_ctx* ctx);
+const char* tsg_last_error(const tsg_ctx* ctx);
+int tsg_abi_version(void);
+
+/* C = A . B.  tiles may be NULL. */
+int tsg_spgemm(tsg_ctx* ctx, const tsg_csr* A, const tsg_csr* B, tsg_csr_out* C,
+               const tsg_options* opt, tsg_run_stats* stats, tsg_tiles_out* tiles);
+
+/* C = X0 . X1 . ... . X{n-1}, left to right; each intermediate is rounded
+ * to binary16 (drop exact zeros / underflow, OverflowError beyond 65504)
+ * before the next stage, as spgemm_square does for fp32-stored input
+ * (proj/src/kernels.cpp:239-258).  stats accumulates over stages. */
+int tsg_spgemm_chain(tsg_ctx* ctx, int n, const tsg_csr* const* X, tsg_csr_out* C,
+                     const tsg_options* opt, tsg_run_stats* stats);
+
+void tsg_free_csr(tsg_ctx* ctx, tsg_csr_out* C);
+void tsg_free_tiles(tsg_tiles_out* t);
+
+/* sum_k nnzA(:,k) * nnzB(k,:) on the device (analytics.cpp:51-65,
+ * generalised to A != B): the GFLOPS denominator / 2. */
+int tsg_cbar(tsg_ctx* ctx, const tsg_csr* A, const tsg_csr* B, uint64_t* cbar);
+
+/* Total own-kernel launches by this context since creation. */
+uint64_t tsg_launch_count(const tsg_ctx* ctx);
+
+/* Device time (ms) of each launch of the numeric kernel during the last
+ * call with phase_timing set (averaged over launches), for the roofline. */
+double tsg_last_kernel_ms(const tsg_ctx* ctx, const char* phase);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TSPARSE_B200_H */

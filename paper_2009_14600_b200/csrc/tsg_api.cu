@@ -1,0 +1,681 @@
+// tsg_api.cu -- host driver and C ABI (include/tsparse_b200.h).
+//
+// Sequences the four subsystems for C = A.B, like spgemm_square
+// (proj/src/kernels.cpp:222-302) sequences the reference passes:
+//
+//   convert A, B (CSR -> 16x16 tiles)         tsg_convert.cu
+//   enumerate + filter (count, scan, fill)    tsg_symbolic.cu      "taskList"
+//   stable per-tile-row sort by output tile   CUB segmented sort   "sort"
+//   segment heads                             tsg_symbolic.cu      "sort"
+//   counting pass + prefix sum                tsg_symbolic.cu      "counting"
+//   SEaC numeric                              tsg_numeric.cu       "multiply"
+//   tiled -> CSR (+ fused compaction)         tsg_output.cu        "compaction"
+//
+// Everything runs stream-ordered on the context's stream with scratch from
+// a stream-ordered memory pool (cudaMallocFromPoolAsync), so steady-state
+// calls do not touch the driver allocator.  The host synchronises only to
+// read data-dependent sizes (tile, pair, segment, element counts).
+#include <cub/device/device_scan.cuh>
+#include <cub/device/device_segmented_sort.cuh>
+
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/tsparse_b200.h"
+#include "tsg_kernels.cuh"
+
+struct tsg_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  cudaMemPool_t pool = nullptr;
+  uint64_t* pinned = nullptr;  // small pinned readback buffer
+  std::string err;
+  uint64_t launches = 0;
+  double last_phase_ms[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  cudaEvent_t ev[8] = {};
+  // pinned host blocks released by tsg_free_csr, reused by later host outputs
+  std::vector<std::pair<void*, size_t>> pinned_free;
+};
+
+namespace {
+
+using namespace tsg;
+
+struct Fail {
+  int code;
+  std::string msg;
+};
+
+#define TSG_CUDA(call)                                                                  \
+  do {                                                                                  \
+    cudaError_t e_ = (call);                                                            \
+    if (e_ != cudaSuccess)                                                              \
+      throw Fail{TSG_ERR_OTHER, std::string(#call) + ": " + cudaGetErrorString(e_)};    \
+  } while (0)
+
+// Stream-ordered scratch, released (to the pool) when the scope ends.
+struct Scratch {
+  tsg_ctx* ctx;
+  std::vector<void*> ptrs;
+  explicit Scratch(tsg_ctx* c) : ctx(c) {}
+  ~Scratch() {
+    for (void* p : ptrs) cudaFreeAsync(p, ctx->stream);
+  }
+  template <class T>
+  T* alloc(uint64_t n, bool keep = false) {
+    if (n == 0) n = 1;
+    void* p = nullptr;
+    TSG_CUDA(cudaMallocFromPoolAsync(&p, n * sizeof(T), ctx->pool, ctx->stream));
+    if (!keep) ptrs.push_back(p);
+    return static_cast<T*>(p);
+  }
+};
+
+void check_launch(tsg_ctx* ctx, int n = 1) {
+  ctx->launches += n;
+  TSG_CUDA(cudaGetLastError());
+}
+
+template <class T>
+T readback(tsg_ctx* ctx, const T* dptr) {
+  TSG_CUDA(cudaMemcpyAsync(ctx->pinned, dptr, sizeof(T), cudaMemcpyDeviceToHost, ctx->stream));
+  TSG_CUDA(cudaStreamSynchronize(ctx->stream));
+  T v;
+  std::memcpy(&v, ctx->pinned, sizeof(T));
+  return v;
+}
+
+// Sum of n u32 (exact, u64) -- guards every u32 offset array against wrap.
+__global__ void sum_u32_kernel(const uint32_t* __restrict__ in, uint64_t n,
+                               unsigned long long* __restrict__ out) {
+  unsigned long long acc = 0;
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
+       i += uint64_t(gridDim.x) * blockDim.x)
+    acc += in[i];
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0 && acc) atomicAdd(out, acc);
+}
+
+template <class Tin, class Tout>
+void exclusive_sum(tsg_ctx* ctx, Scratch& sc, const Tin* in, Tout* out, uint64_t n) {
+  size_t bytes = 0;
+  TSG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, bytes, in, out, n, ctx->stream));
+  void* tmp = sc.alloc<char>(bytes);
+  TSG_CUDA(cub::DeviceScan::ExclusiveSum(tmp, bytes, in, out, n, ctx->stream));
+}
+
+uint64_t total_u32(tsg_ctx* ctx, Scratch& sc, const uint32_t* in, uint64_t n) {
+  auto* d = sc.alloc<unsigned long long>(1);
+  TSG_CUDA(cudaMemsetAsync(d, 0, sizeof(unsigned long long), ctx->stream));
+  if (n) {
+    uint64_t blocks = (n + 255) / 256;
+    if (blocks > 1184) blocks = 1184;
+    sum_u32_kernel<<<unsigned(blocks), 256, 0, ctx->stream>>>(in, n, d);
+    check_launch(ctx);
+  }
+  return readback(ctx, d);
+}
+
+void record(tsg_ctx* ctx, bool timing, int i) {
+  if (timing) TSG_CUDA(cudaEventRecord(ctx->ev[i], ctx->stream));
+}
+
+size_t dtype_size(int dt) { return dt == TSG_F16 ? 2 : dt == TSG_F32 ? 4 : 8; }
+
+void check_csr(const tsg_csr* M, const char* name) {
+  if (!M) throw Fail{TSG_ERR_OTHER, std::string(name) + " is NULL"};
+  if (M->rows < 0 || M->cols < 0 || M->nnz < 0)
+    throw Fail{TSG_ERR_INVARIANT, std::string(name) + ": negative dimension"};
+  if (M->dtype < TSG_F16 || M->dtype > TSG_F64)
+    throw Fail{TSG_ERR_OTHER, std::string(name) + ": unknown dtype"};
+  if (M->rows > (int64_t(1) << 35) || M->cols > (int64_t(1) << 31) - 16)
+    throw Fail{TSG_ERR_OTHER, std::string(name) + ": dimensions beyond the 16x16 tile index range"};
+  if (M->nnz >= (int64_t(1) << 32))
+    throw Fail{TSG_ERR_OTHER, std::string(name) + ": nnz beyond 2^32 needs row-panel batching"};
+  if ((M->rows > 0 || M->nnz > 0) && (!M->row_ptr || (M->nnz > 0 && (!M->col || !M->val))))
+    throw Fail{TSG_ERR_OTHER, std::string(name) + ": missing arrays"};
+}
+
+// Device view of a CSR (copies host input; the H2D bytes are counted).
+CsrView stage(tsg_ctx* ctx, Scratch& sc, const tsg_csr* M, tsg_run_stats* st) {
+  CsrView v;
+  v.rows = M->rows;
+  v.cols = M->cols;
+  v.nnz = M->nnz;
+  v.dtype = M->dtype;
+  if (M->mem == TSG_MEM_DEVICE) {
+    v.row_ptr = M->row_ptr;
+    v.col = M->col;
+    v.val = M->val;
+    return v;
+  }
+  auto* rp = sc.alloc<int64_t>(M->rows + 1);
+  auto* col = sc.alloc<int32_t>(M->nnz);
+  auto* val = sc.alloc<char>(M->nnz * dtype_size(M->dtype));
+  const size_t b0 = (M->rows + 1) * sizeof(int64_t), b1 = M->nnz * sizeof(int32_t),
+               b2 = M->nnz * dtype_size(M->dtype);
+  TSG_CUDA(cudaMemcpyAsync(rp, M->row_ptr, b0, cudaMemcpyHostToDevice, ctx->stream));
+  if (M->nnz) {
+    TSG_CUDA(cudaMemcpyAsync(col, M->col, b1, cudaMemcpyHostToDevice, ctx->stream));
+    TSG_CUDA(cudaMemcpyAsync(val, M->val, b2, cudaMemcpyHostToDevice, ctx->stream));
+  }
+  if (st) st->h2d_bytes += b0 + b1 + b2;
+  v.row_ptr = rp;
+  v.col = col;
+  v.val = val;
+  return v;
+}
+
+// CSR -> 16x16 tiles (count, scan, fill).  Returns the tile count.
+uint64_t convert(tsg_ctx* ctx, Scratch& sc, const CsrView& in, TileMat& T, int roles,
+                 unsigned* err_flag, int drop_nonfinite, uint64_t* nvals_out) {
+  T.rows = in.rows;
+  T.cols = in.cols;
+  T.tile_rows = uint32_t((in.rows + 15) / 16);
+  T.tile_cols = uint32_t((in.cols + 15) / 16);
+  const uint64_t nr = uint64_t(T.tile_rows) + 1;
+  auto* row_nt = sc.alloc<uint32_t>(nr);
+  auto* row_nv = sc.alloc<uint32_t>(nr);
+  TSG_CUDA(cudaMemsetAsync(row_nt + nr - 1, 0, sizeof(uint32_t), ctx->stream));
+  TSG_CUDA(cudaMemsetAsync(row_nv + nr - 1, 0, sizeof(uint32_t), ctx->stream));
+  launch_convert_count(in, T, row_nt, row_nv, err_flag, drop_nonfinite, ctx->stream);
+  check_launch(ctx);
+  T.trp = sc.alloc<uint32_t>(nr);
+  auto* vbase = sc.alloc<uint32_t>(nr);
+  exclusive_sum(ctx, sc, row_nt, T.trp, nr);
+  exclusive_sum(ctx, sc, row_nv, vbase, nr);
+  // capacities: tiles <= nnz, values <= nnz (no host sync needed)
+  const uint64_t cap = uint64_t(in.nnz);
+  T.cap_tiles = cap;
+  T.cap_vals = cap;
+  T.tcol = sc.alloc<uint32_t>(cap);
+  T.rmask = sc.alloc<uint16_t>(cap * 16);
+  T.occ = sc.alloc<uint32_t>(cap);
+  T.voff = sc.alloc<uint32_t>(cap);
+  for (int role = 0; role < 2; ++role) {
+    if (!(roles & (1 << role))) continue;
+    T.fhdr[role] = sc.alloc<uint16_t>(cap * 32);
+    T.vals[role] = sc.alloc<__half>(cap);
+  }
+  launch_convert_fill(in, T, roles, T.trp, vbase, drop_nonfinite, ctx->stream);
+  check_launch(ctx);
+  uint32_t tail[2];
+  TSG_CUDA(cudaMemcpyAsync(ctx->pinned, T.trp + nr - 1, 4, cudaMemcpyDeviceToHost, ctx->stream));
+  TSG_CUDA(cudaMemcpyAsync(reinterpret_cast<char*>(ctx->pinned) + 4, vbase + nr - 1, 4,
+                           cudaMemcpyDeviceToHost, ctx->stream));
+  TSG_CUDA(cudaStreamSynchronize(ctx->stream));
+  std::memcpy(tail, ctx->pinned, 8);
+  if (nvals_out) *nvals_out = tail[1];
+  return tail[0];
+}
+
+void raise_flags(tsg_ctx* ctx, unsigned flags) {
+  if (flags & kErrInvariant)
+    throw Fail{TSG_ERR_INVARIANT, "CSR entries unsorted, duplicated, or out of range"};
+  if (flags & kErrOverflow)
+    throw Fail{TSG_ERR_OVERFLOW, "value outside binary16 finite range (|x| <= 65504) or non-finite"};
+  if (flags & kErrPrecision)
+    throw Fail{TSG_ERR_PRECISION, "non-finite accumulator in multiplication pass"};
+  (void)ctx;
+}
+
+struct OutOwner {  // device or pinned-host output buffers
+  bool host = false;
+  void* p[3] = {nullptr, nullptr, nullptr};
+  size_t sz[3] = {0, 0, 0};
+};
+
+// Pinned host block from the context cache (best fit) or cudaMallocHost.
+void* pinned_alloc(tsg_ctx* ctx, size_t bytes, size_t* got) {
+  if (bytes == 0) bytes = 1;
+  size_t best = SIZE_MAX, bi = 0;
+  for (size_t i = 0; i < ctx->pinned_free.size(); ++i) {
+    const size_t sz = ctx->pinned_free[i].second;
+    if (sz >= bytes && sz < best) {
+      best = sz;
+      bi = i;
+    }
+  }
+  if (best != SIZE_MAX) {
+    void* p = ctx->pinned_free[bi].first;
+    *got = best;
+    ctx->pinned_free.erase(ctx->pinned_free.begin() + bi);
+    return p;
+  }
+  void* p = nullptr;
+  TSG_CUDA(cudaMallocHost(&p, bytes));
+  *got = bytes;
+  return p;
+}
+
+void spgemm_impl(tsg_ctx* ctx, const tsg_csr* Ain, const tsg_csr* Bin, tsg_csr_out* C,
+                 const tsg_options& opt, tsg_run_stats* st, tsg_tiles_out* tiles) {
+  check_csr(Ain, "A");
+  check_csr(Bin, "B");
+  if (!C) throw Fail{TSG_ERR_OTHER, "C is NULL"};
+  if (Ain->cols != Bin->rows)
+    throw Fail{TSG_ERR_DIMENSION, "inner dimensions differ: A is " + std::to_string(Ain->rows) +
+                                      "x" + std::to_string(Ain->cols) + ", B is " +
+                                      std::to_string(Bin->rows) + "x" + std::to_string(Bin->cols)};
+  const bool timing = opt.phase_timing != 0;
+  cudaStream_t s = ctx->stream;
+  Scratch sc(ctx);
+  const uint64_t launches0 = ctx->launches;
+  record(ctx, timing, 0);
+
+  auto* err_flag = sc.alloc<unsigned>(1);
+  TSG_CUDA(cudaMemsetAsync(err_flag, 0, sizeof(unsigned), s));
+
+  const bool same = Ain == Bin ||
+                    (Ain->row_ptr == Bin->row_ptr && Ain->col == Bin->col && Ain->val == Bin->val &&
+                     Ain->rows == Bin->rows && Ain->cols == Bin->cols && Ain->mem == Bin->mem &&
+                     Ain->dtype == Bin->dtype && Ain->nnz == Bin->nnz);
+  const CsrView dA = stage(ctx, sc, Ain, st);
+  const CsrView dB = same ? dA : stage(ctx, sc, Bin, st);
+
+  // ---- (1) conversion ------------------------------------------------------
+  TileMat TA, TB_own;
+  uint64_t nvA = 0, nvB = 0;
+  const uint64_t tA = convert(ctx, sc, dA, TA, same ? 3 : 1, err_flag, opt.drop_nonfinite, &nvA);
+  uint64_t tB = tA;
+  if (!same) tB = convert(ctx, sc, dB, TB_own, 2, err_flag, opt.drop_nonfinite, &nvB);
+  const TileMat& TB = same ? TA : TB_own;
+  raise_flags(ctx, readback(ctx, err_flag));
+  record(ctx, timing, 1);
+
+  // ---- (2) symbolic: enumerate + filter -------------------------------------
+  TaskList tl;
+  auto* raw_d = sc.alloc<unsigned long long>(1);
+  TSG_CUDA(cudaMemsetAsync(raw_d, 0, sizeof(unsigned long long), s));
+  tl.tile_pair_off = sc.alloc<uint32_t>(tA + 1);
+  auto* tile_cnt = sc.alloc<uint32_t>(tA + 1);
+  TSG_CUDA(cudaMemsetAsync(tile_cnt + tA, 0, sizeof(uint32_t), s));
+  launch_enum_count(TA, TB, tA, tile_cnt, raw_d, s);
+  check_launch(ctx);
+  const uint64_t P = total_u32(ctx, sc, tile_cnt, tA);
+  const uint64_t raw = readback(ctx, raw_d);
+  if (P >= (uint64_t(1) << 31))
+    throw Fail{TSG_ERR_OTHER, "task list beyond 2^31 pairs needs row-panel batching"};
+  exclusive_sum(ctx, sc, tile_cnt, tl.tile_pair_off, tA + 1);
+  tl.npairs = P;
+  uint64_t* pairs_u = sc.alloc<uint64_t>(P);
+  uint32_t* keys_u = sc.alloc<uint32_t>(P);
+  launch_enum_fill(TA, TB, tA, tl.tile_pair_off, pairs_u, keys_u, s);
+  check_launch(ctx);
+  tl.row_pair_off = sc.alloc<uint32_t>(uint64_t(TA.tile_rows) + 1);
+  launch_row_pair_off(TA, tl.tile_pair_off, tl.row_pair_off, s);
+  check_launch(ctx);
+  record(ctx, timing, 2);
+
+  // ---- (2b) stable sort by output tile within each tile row, segments -------
+  tl.pairs = sc.alloc<uint64_t>(P);
+  tl.keys = sc.alloc<uint32_t>(P);
+  if (P > 0) {
+    size_t bytes = 0;
+    TSG_CUDA(cub::DeviceSegmentedSort::StableSortPairs(
+        nullptr, bytes, keys_u, tl.keys, pairs_u, tl.pairs, int(P), int(TA.tile_rows),
+        tl.row_pair_off, tl.row_pair_off + 1, s));
+    void* tmp = sc.alloc<char>(bytes);
+    TSG_CUDA(cub::DeviceSegmentedSort::StableSortPairs(
+        tmp, bytes, keys_u, tl.keys, pairs_u, tl.pairs, int(P), int(TA.tile_rows),
+        tl.row_pair_off, tl.row_pair_off + 1, s));
+  }
+  const uint64_t nr = uint64_t(TA.tile_rows) + 1;
+  auto* row_nseg = sc.alloc<uint32_t>(nr);
+  TSG_CUDA(cudaMemsetAsync(row_nseg + nr - 1, 0, sizeof(uint32_t), s));
+  launch_seg_count(TA, tl.row_pair_off, tl.keys, row_nseg, s);
+  check_launch(ctx);
+  const uint64_t S = total_u32(ctx, sc, row_nseg, nr);
+  tl.seg_row_ptr = sc.alloc<uint32_t>(nr);
+  exclusive_sum(ctx, sc, row_nseg, tl.seg_row_ptr, nr);
+  tl.nseg = S;
+  tl.seg_off = sc.alloc<uint32_t>(S + 1);
+  tl.seg_col = sc.alloc<uint32_t>(S);
+  {
+    // seg_off[S] = P via the pinned staging word (stream-ordered before any
+    // later readback into the same buffer)
+    uint32_t* stage_word = reinterpret_cast<uint32_t*>(ctx->pinned) + 14;
+    *stage_word = uint32_t(P);
+    TSG_CUDA(cudaMemcpyAsync(tl.seg_off + S, stage_word, 4, cudaMemcpyHostToDevice, s));
+  }
+  launch_seg_fill(TA, tl.row_pair_off, tl.keys, tl.seg_row_ptr, tl.seg_off, tl.seg_col, s);
+  check_launch(ctx);
+  record(ctx, timing, 3);
+
+  // ---- counting --------------------------------------------------------------
+  OutTiles ot;
+  ot.counted = sc.alloc<uint32_t>(S + 1);
+  TSG_CUDA(cudaMemsetAsync(ot.counted + S, 0, sizeof(uint32_t), s));
+  launch_counting(TA, TB, tl, ot.counted, s);
+  check_launch(ctx);
+  const uint64_t counted = total_u32(ctx, sc, ot.counted, S);
+  if (counted >= (uint64_t(1) << 32))
+    throw Fail{TSG_ERR_OTHER, "output beyond 2^32 elements needs row-panel batching"};
+  ot.elem_off = sc.alloc<uint32_t>(S + 1);
+  exclusive_sum(ctx, sc, ot.counted, ot.elem_off, S + 1);
+  record(ctx, timing, 4);
+
+  // ---- (3) numeric -----------------------------------------------------------
+  ot.cmask = sc.alloc<uint16_t>(S * 16);
+  ot.vals = sc.alloc<float>(counted);
+  launch_numeric(TA, TB, tl, ot, opt.mode, err_flag, s);
+  check_launch(ctx);
+  record(ctx, timing, 5);
+
+  // ---- (4) tiled -> CSR with fused compaction ----------------------------------
+  const int64_t rows = Ain->rows;
+  auto* rowcnt = sc.alloc<int64_t>(rows + 1);
+  TSG_CUDA(cudaMemsetAsync(rowcnt + rows, 0, sizeof(int64_t), s));
+  launch_out_rowcount(TA, rows, tl, ot, rowcnt, s);
+  check_launch(ctx);
+  auto* owner = new OutOwner();
+  owner->host = C->mem == TSG_MEM_HOST;
+  C->_owner = owner;  // released by free_out on any later failure
+  int64_t* d_rp = nullptr;
+  int32_t* d_col = nullptr;
+  float* d_val = nullptr;
+  // output buffers: device outputs outlive the call; host outputs use scratch
+  d_rp = owner->host ? sc.alloc<int64_t>(rows + 1) : sc.alloc<int64_t>(rows + 1, true);
+  if (!owner->host) owner->p[0] = d_rp;
+  exclusive_sum(ctx, sc, rowcnt, d_rp, uint64_t(rows) + 1);
+  const int64_t nnzC = readback(ctx, d_rp + rows);
+  raise_flags(ctx, readback(ctx, err_flag));
+  d_col = owner->host ? sc.alloc<int32_t>(nnzC) : sc.alloc<int32_t>(nnzC, true);
+  d_val = owner->host ? sc.alloc<float>(nnzC) : sc.alloc<float>(nnzC, true);
+  if (!owner->host) {
+    owner->p[1] = d_col;
+    owner->p[2] = d_val;
+  }
+  launch_out_fill(TA, rows, tl, ot, d_rp, d_col, d_val, s);
+  check_launch(ctx);
+  record(ctx, timing, 6);
+
+  C->rows = Ain->rows;
+  C->cols = Bin->cols;
+  C->nnz = nnzC;
+  if (owner->host) {
+    owner->p[0] = pinned_alloc(ctx, (rows + 1) * sizeof(int64_t), &owner->sz[0]);
+    owner->p[1] = pinned_alloc(ctx, nnzC * sizeof(int32_t), &owner->sz[1]);
+    owner->p[2] = pinned_alloc(ctx, nnzC * sizeof(float), &owner->sz[2]);
+    TSG_CUDA(cudaMemcpyAsync(owner->p[0], d_rp, (rows + 1) * sizeof(int64_t),
+                             cudaMemcpyDeviceToHost, s));
+    if (nnzC) {
+      TSG_CUDA(cudaMemcpyAsync(owner->p[1], d_col, nnzC * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+      TSG_CUDA(cudaMemcpyAsync(owner->p[2], d_val, nnzC * sizeof(float), cudaMemcpyDeviceToHost, s));
+    }
+    if (st) st->d2h_bytes += (rows + 1) * sizeof(int64_t) + nnzC * (sizeof(int32_t) + sizeof(float));
+  }
+  C->row_ptr = static_cast<int64_t*>(owner->p[0]);
+  C->col = static_cast<int32_t*>(owner->p[1]);
+  C->val = static_cast<float*>(owner->p[2]);
+
+  if (tiles) {  // pre-CSR tiled view for the tile-structure bridge (test path)
+    std::vector<uint32_t> h_seg_row(nr), h_seg_col(S), h_off(S + 1);
+    std::vector<uint16_t> h_mask(S * 16);
+    std::vector<float> h_vals(counted);
+    TSG_CUDA(cudaMemcpyAsync(h_seg_row.data(), tl.seg_row_ptr, nr * 4, cudaMemcpyDeviceToHost, s));
+    if (S) {
+      TSG_CUDA(cudaMemcpyAsync(h_seg_col.data(), tl.seg_col, S * 4, cudaMemcpyDeviceToHost, s));
+      TSG_CUDA(cudaMemcpyAsync(h_mask.data(), ot.cmask, S * 32, cudaMemcpyDeviceToHost, s));
+    }
+    TSG_CUDA(cudaMemcpyAsync(h_off.data(), ot.elem_off, (S + 1) * 4, cudaMemcpyDeviceToHost, s));
+    if (counted)
+      TSG_CUDA(cudaMemcpyAsync(h_vals.data(), ot.vals, counted * 4, cudaMemcpyDeviceToHost, s));
+    TSG_CUDA(cudaStreamSynchronize(s));
+    std::vector<uint32_t> tr, tc;
+    std::vector<uint16_t> rm;
+    std::vector<uint64_t> ei;
+    std::vector<float> vv;
+    for (uint32_t I = 0; I + 1 < nr; ++I)
+      for (uint32_t q = h_seg_row[I]; q < h_seg_row[I + 1]; ++q) {
+        int n = 0;
+        for (int r = 0; r < 16; ++r) n += __builtin_popcount(h_mask[size_t(q) * 16 + r]);
+        if (n == 0) continue;  // compact(): empty tiles dropped
+        tr.push_back(I);
+        tc.push_back(h_seg_col[q]);
+        ei.push_back(vv.size());
+        for (int r = 0; r < 16; ++r) rm.push_back(h_mask[size_t(q) * 16 + r]);
+        vv.insert(vv.end(), h_vals.begin() + h_off[q], h_vals.begin() + h_off[q] + n);
+      }
+    tiles->ntiles = int64_t(tr.size());
+    tiles->nnz = int64_t(vv.size());
+    auto dup = [](const void* src, size_t bytes) {
+      void* p = std::malloc(bytes ? bytes : 1);
+      if (bytes) std::memcpy(p, src, bytes);
+      return p;
+    };
+    tiles->tile_row = static_cast<uint32_t*>(dup(tr.data(), tr.size() * 4));
+    tiles->tile_col = static_cast<uint32_t*>(dup(tc.data(), tc.size() * 4));
+    tiles->row_masks = static_cast<uint16_t*>(dup(rm.data(), rm.size() * 2));
+    tiles->elem_index = static_cast<uint64_t*>(dup(ei.data(), ei.size() * 8));
+    tiles->val = static_cast<float*>(dup(vv.data(), vv.size() * 4));
+  }
+
+  TSG_CUDA(cudaStreamSynchronize(s));
+  if (timing) {
+    float ms[7] = {0};
+    for (int i = 1; i <= 6; ++i) TSG_CUDA(cudaEventElapsedTime(&ms[i], ctx->ev[i - 1], ctx->ev[i]));
+    float tot = 0;
+    TSG_CUDA(cudaEventElapsedTime(&tot, ctx->ev[0], ctx->ev[6]));
+    for (int i = 1; i <= 6; ++i) ctx->last_phase_ms[i] = ms[i];
+    ctx->last_phase_ms[7] = tot;
+    if (st) {
+      st->convert += ms[1] * 1e-3;
+      st->task_list += ms[2] * 1e-3;
+      st->sort += ms[3] * 1e-3;
+      st->counting += ms[4] * 1e-3;
+      st->multiply += ms[5] * 1e-3;
+      st->compaction += ms[6] * 1e-3;
+      st->total += tot * 1e-3;
+    }
+  }
+  if (st) {
+    st->tiles_a += tA;
+    st->tiles_b += tB;
+    st->raw_pairs += raw;
+    st->filtered_pairs += P;
+    st->segments += S;
+    st->counted_elements += counted;
+    st->nnz_c = uint64_t(nnzC);
+    st->kernel_launches += ctx->launches - launches0;
+  }
+  (void)nvA;
+  (void)nvB;
+}
+
+void free_out(tsg_ctx* ctx, tsg_csr_out* C) {
+  if (!C || !C->_owner) return;
+  auto* o = static_cast<OutOwner*>(C->_owner);
+  for (int i = 0; i < 3; ++i) {
+    void* p = o->p[i];
+    if (!p) continue;
+    if (o->host)
+      ctx->pinned_free.emplace_back(p, o->sz[i]);
+    else
+      cudaFreeAsync(p, ctx->stream);
+  }
+  delete o;
+  C->_owner = nullptr;
+  C->row_ptr = nullptr;
+  C->col = nullptr;
+  C->val = nullptr;
+}
+
+}  // namespace
+
+extern "C" {
+
+void tsg_default_options(tsg_options* opt) {
+  if (!opt) return;
+  std::memset(opt, 0, sizeof(*opt));
+  opt->mode = TSG_MODE_TENSOR;
+}
+
+int tsg_abi_version(void) { return TSG_ABI_VERSION; }
+
+int tsg_create(tsg_ctx** out, int device, void* stream) {
+  if (!out) return TSG_ERR_OTHER;
+  *out = nullptr;
+  auto* ctx = new tsg_ctx();
+  cudaError_t e = cudaSuccess;
+  if (device < 0) e = cudaGetDevice(&ctx->device);
+  else ctx->device = device;
+  if (e == cudaSuccess) e = cudaSetDevice(ctx->device);
+  if (e == cudaSuccess) {
+    if (stream) {
+      ctx->stream = static_cast<cudaStream_t>(stream);
+    } else {
+      e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking);
+      ctx->own_stream = true;
+    }
+  }
+  if (e == cudaSuccess) e = cudaDeviceGetDefaultMemPool(&ctx->pool, ctx->device);
+  if (e == cudaSuccess) {
+    uint64_t thr = ~uint64_t(0);
+    e = cudaMemPoolSetAttribute(ctx->pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  if (e == cudaSuccess) e = cudaMallocHost(&ctx->pinned, 64);
+  for (int i = 0; i < 8 && e == cudaSuccess; ++i) e = cudaEventCreate(&ctx->ev[i]);
+  if (e != cudaSuccess) {
+    std::fprintf(stderr, "tsg_create: %s\n", cudaGetErrorString(e));
+    delete ctx;
+    return TSG_ERR_OTHER;
+  }
+  *out = ctx;
+  return TSG_OK;
+}
+
+int tsg_destroy(tsg_ctx* ctx) {
+  if (!ctx) return TSG_OK;
+  cudaStreamSynchronize(ctx->stream);
+  for (auto& e : ctx->ev)
+    if (e) cudaEventDestroy(e);
+  if (ctx->pinned) cudaFreeHost(ctx->pinned);
+  for (auto& b : ctx->pinned_free) cudaFreeHost(b.first);
+  if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+  delete ctx;
+  return TSG_OK;
+}
+
+const char* tsg_last_error(const tsg_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+int tsg_spgemm(tsg_ctx* ctx, const tsg_csr* A, const tsg_csr* B, tsg_csr_out* C,
+               const tsg_options* opt, tsg_run_stats* stats, tsg_tiles_out* tiles) {
+  if (!ctx) return TSG_ERR_OTHER;
+  tsg_options o;
+  tsg_default_options(&o);
+  if (opt) o = *opt;
+  ctx->err.clear();
+  if (C) C->_owner = nullptr;
+  try {
+    TSG_CUDA(cudaSetDevice(ctx->device));
+    spgemm_impl(ctx, A, B, C, o, stats, o.want_tiles ? tiles : nullptr);
+    return TSG_OK;
+  } catch (const Fail& f) {
+    ctx->err = f.msg;
+    cudaStreamSynchronize(ctx->stream);
+    if (C && C->_owner) free_out(ctx, C);
+    return f.code;
+  } catch (const std::exception& e) {
+    ctx->err = e.what();
+    return TSG_ERR_OTHER;
+  }
+}
+
+int tsg_spgemm_chain(tsg_ctx* ctx, int n, const tsg_csr* const* X, tsg_csr_out* C,
+                     const tsg_options* opt, tsg_run_stats* stats) {
+  if (!ctx) return TSG_ERR_OTHER;
+  if (n < 2 || !X || !C) {
+    ctx->err = "chain needs at least two operands";
+    return TSG_ERR_OTHER;
+  }
+  tsg_options o;
+  tsg_default_options(&o);
+  if (opt) o = *opt;
+  o.want_tiles = 0;
+  tsg_csr_out cur{};
+  bool have_cur = false;
+  for (int i = 1; i < n; ++i) {
+    tsg_csr left;
+    if (!have_cur) {
+      left = *X[0];
+    } else {
+      // intermediate: device fp32 CSR, rounded to binary16 by the next
+      // conversion (kernels.cpp:239-258 semantics)
+      left.rows = cur.rows;
+      left.cols = cur.cols;
+      left.nnz = cur.nnz;
+      left.row_ptr = cur.row_ptr;
+      left.col = cur.col;
+      left.val = cur.val;
+      left.dtype = TSG_F32;
+      left.mem = TSG_MEM_DEVICE;
+    }
+    tsg_csr_out next{};
+    next.mem = (i == n - 1) ? C->mem : TSG_MEM_DEVICE;
+    const int rc = tsg_spgemm(ctx, &left, X[i], &next, &o, stats, nullptr);
+    if (have_cur) free_out(ctx, &cur);
+    if (rc != TSG_OK) return rc;
+    cur = next;
+    have_cur = true;
+  }
+  *C = cur;
+  return TSG_OK;
+}
+
+void tsg_free_csr(tsg_ctx* ctx, tsg_csr_out* C) {
+  if (!ctx) return;
+  free_out(ctx, C);
+  cudaStreamSynchronize(ctx->stream);
+}
+
+void tsg_free_tiles(tsg_tiles_out* t) {
+  if (!t) return;
+  std::free(t->tile_row);
+  std::free(t->tile_col);
+  std::free(t->row_masks);
+  std::free(t->elem_index);
+  std::free(t->val);
+  std::memset(t, 0, sizeof(*t));
+}
+
+int tsg_cbar(tsg_ctx* ctx, const tsg_csr* A, const tsg_csr* B, uint64_t* cbar) {
+  if (!ctx || !cbar) return TSG_ERR_OTHER;
+  ctx->err.clear();
+  try {
+    check_csr(A, "A");
+    check_csr(B, "B");
+    if (A->cols != B->rows) throw Fail{TSG_ERR_DIMENSION, "inner dimensions differ"};
+    Scratch sc(ctx);
+    const CsrView dA = stage(ctx, sc, A, nullptr);
+    const CsrView dB = stage(ctx, sc, B, nullptr);
+    auto* hist = sc.alloc<unsigned>(A->cols);
+    auto* out = sc.alloc<unsigned long long>(1);
+    TSG_CUDA(cudaMemsetAsync(hist, 0, A->cols * sizeof(unsigned), ctx->stream));
+    TSG_CUDA(cudaMemsetAsync(out, 0, sizeof(unsigned long long), ctx->stream));
+    launch_cbar(dA.col, dA.nnz, A->cols, dB.row_ptr, hist, out, ctx->stream);
+    check_launch(ctx, 2);
+    *cbar = readback(ctx, out);
+    return TSG_OK;
+  } catch (const Fail& f) {
+    ctx->err = f.msg;
+    return f.code;
+  }
+}
+
+uint64_t tsg_launch_count(const tsg_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+double tsg_last_kernel_ms(const tsg_ctx* ctx, const char* phase) {
+  if (!ctx || !phase) return 0.0;
+  static const char* names[] = {"", "convert", "task_list", "sort", "counting", "multiply",
+                                "compaction", "total"};
+  for (int i = 1; i < 8; ++i)
+    if (std::strcmp(phase, names[i]) == 0) return ctx->last_phase_ms[i];
+  return 0.0;
+}
+
+}  // extern "C"

@@ -1,0 +1,233 @@
+// tsg_convert.cu -- subsystem (1): CSR -> 16x16 tiled bitmap format.
+//
+// GPU restatement of from_element_coo(m, Fp16Stored)
+// (proj/src/tile_format.cpp:61-129) at T = 16:
+//   * validation of the COO/CSR invariant        tile_format.cpp:34-51
+//   * non-finite -> OverflowError (or dropped)   tile_format.cpp:82-86
+//   * exact zero dropped                         tile_format.cpp:87
+//   * round_to_half (RNE, |x| > 65504 throws)    tile_format.cpp:89-90, half.cpp:12-36
+//   * values that round to zero dropped          tile_format.cpp:98
+//   * tiles keyed (tile_row, tile_col), slots in-tile, tiles sorted
+//     (the std::sort at tile_format.cpp:106-110 is replaced by a 16-way
+//      merge across the rows of a tile row: CSR rows are already sorted).
+//
+// One warp per tile row (16 CSR rows, lane r<16 owns row r).  Each step the
+// warp takes the minimum pending tile column (REDUX), every row lane
+// consumes its entries in that tile, and the tile is emitted.  Two passes
+// (count, fill) with a prefix sum between them; the fill pass writes one or
+// both operand layouts (A order and/or B order, see tsg_common.cuh).
+#include "tsg_kernels.cuh"
+
+namespace tsg {
+
+namespace {
+
+// Single-step RNE double -> binary16 (no double rounding through float).
+__device__ __forceinline__ unsigned short f64_to_half_bits(double x) {
+  unsigned short h;
+  asm("cvt.rn.f16.f64 %0, %1;" : "=h"(h) : "d"(x));
+  return h;
+}
+
+// Loads value p as binary16 bits.  Sets *bad on overflow / non-finite and
+// *skip when the entry is dropped (zero, underflow, or dropped non-finite).
+__device__ __forceinline__ unsigned short load_half(const void* val, int dtype, int64_t p,
+                                                    bool drop_nonfinite, unsigned& err,
+                                                    bool& keep) {
+  unsigned short h = 0;
+  keep = false;
+  if (dtype == 1) {  // f32
+    const float x = __ldg(static_cast<const float*>(val) + p);
+    if (!isfinite(x)) {
+      if (!drop_nonfinite) err |= kErrOverflow;
+      return 0;
+    }
+    if (fabsf(x) > 65504.0f) {
+      err |= kErrOverflow;
+      return 0;
+    }
+    h = __half_as_ushort(__float2half_rn(x));
+  } else if (dtype == 2) {  // f64
+    const double x = __ldg(static_cast<const double*>(val) + p);
+    if (!isfinite(x)) {
+      if (!drop_nonfinite) err |= kErrOverflow;
+      return 0;
+    }
+    if (fabs(x) > 65504.0) {
+      err |= kErrOverflow;
+      return 0;
+    }
+    h = f64_to_half_bits(x);
+  } else {  // binary16 bits
+    h = __ldg(static_cast<const unsigned short*>(val) + p);
+    if ((h & 0x7c00u) == 0x7c00u) {  // inf / nan
+      if (!drop_nonfinite) err |= kErrOverflow;
+      return 0;
+    }
+  }
+  keep = (h & 0x7fffu) != 0;  // exact zero or underflow-to-(+-)0 dropped
+  return h;
+}
+
+template <bool kFill>
+__global__ void __launch_bounds__(256) convert_kernel(CsrView in, TileMat out, int roles,
+                                                     const uint32_t* __restrict__ tile_base,
+                                                     const uint32_t* __restrict__ val_base,
+                                                     uint32_t* __restrict__ row_ntiles,
+                                                     uint32_t* __restrict__ row_nvals,
+                                                     unsigned* __restrict__ err_flag,
+                                                     int drop_nonfinite) {
+  __shared__ uint16_t s_hdr[8][32];
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  const uint32_t I = blockIdx.x * 8 + wib;
+  if (I >= out.tile_rows) return;
+
+  const int64_t row = int64_t(I) * kTile + lane;
+  const bool has_row = lane < kTile && row < in.rows;
+  int64_t p = has_row ? in.row_ptr[row] : 0;
+  const int64_t end = has_row ? in.row_ptr[row + 1] : 0;
+  unsigned err = 0;
+  int32_t prev_col = -1;
+  if (!kFill && has_row && end < p) err |= kErrInvariant;
+
+  uint32_t ntiles = 0, nvals = 0;
+  uint32_t tbase = 0, vbase = 0;
+  if (kFill) {
+    tbase = tile_base[I];
+    vbase = val_base[I];
+  }
+  while (true) {
+    const uint32_t my_tc = (p < end) ? uint32_t(__ldg(in.col + p)) >> 4 : 0xffffffffu;
+    const uint32_t J = __reduce_min_sync(kFull, my_tc);
+    if (J == 0xffffffffu) break;
+    const int64_t p0 = p;
+    uint32_t rm = 0;
+    while (p < end) {
+      const int32_t c = __ldg(in.col + p);
+      if ((uint32_t(c) >> 4) != J) break;
+      if (!kFill) {
+        if (c <= prev_col || c >= in.cols || c < 0) err |= kErrInvariant;
+        prev_col = c;
+      }
+      bool keep;
+      load_half(in.val, in.dtype, p, drop_nonfinite, err, keep);
+      if (keep) rm |= 1u << (c & 15);
+      ++p;
+    }
+    // Termination holds for any input: the lane holding the minimum tile
+    // column always consumes at least one entry.  Invalid input only sets
+    // the flag; the host discards the results.
+    const unsigned any = __ballot_sync(kFull, rm != 0);
+    if (any == 0) continue;  // every value of this tile dropped
+    const uint32_t tile_nnz = __reduce_add_sync(kFull, __popc(rm));
+    if (kFill) {
+      const uint32_t t = tbase + ntiles;
+      const uint32_t v0 = vbase + nvals;
+      if (lane < kTile) out.rmask[size_t(t) * kTile + lane] = uint16_t(rm);
+      const uint32_t colocc = __reduce_or_sync(kFull, rm) & 0xffffu;
+      if (lane == 0) {
+        out.tcol[t] = J;
+        out.occ[t] = colocc | ((any & 0xffffu) << 16);
+        out.voff[t] = v0;
+      }
+      for (int role = 0; role < 2; ++role) {
+        if (!(roles & (1 << role))) continue;
+        // slot byte of this lane in `role` order: gather from the row lanes
+        unsigned byte = 0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          int r, c;
+          rc_of(role, lane, j, r, c);
+          const unsigned rowm = __shfl_sync(kFull, rm, r);
+          byte |= ((rowm >> c) & 1u) << j;
+        }
+        const unsigned cnt = __popc(byte);
+        unsigned incl = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const unsigned v = __shfl_up_sync(kFull, incl, o);
+          if (lane >= o) incl += v;
+        }
+        const unsigned pre = incl - cnt;
+        const uint16_t hdr = uint16_t(byte | (pre << 8));
+        out.fhdr[role][size_t(t) * 32 + lane] = hdr;
+        s_hdr[wib][lane] = hdr;
+        __syncwarp();
+        // scatter this row's kept values into fragment order
+        if (has_row) {
+          for (int64_t q = p0; q < p; ++q) {
+            bool keep;
+            unsigned e2 = 0;
+            const unsigned short h = load_half(in.val, in.dtype, q, drop_nonfinite, e2, keep);
+            if (!keep) continue;
+            const int c = __ldg(in.col + q) & 15;
+            int L, j;
+            slot_of(role, lane, c, L, j);
+            const unsigned hb = s_hdr[wib][L];
+            const unsigned pos = (hb >> 8) + __popc((hb & 0xffu) & ((1u << j) - 1u));
+            reinterpret_cast<unsigned short*>(out.vals[role])[v0 + pos] = h;
+          }
+        }
+        __syncwarp();
+      }
+    }
+    ++ntiles;
+    nvals += tile_nnz;
+  }
+  if (!kFill) {
+    const unsigned e = __reduce_or_sync(kFull, err);
+    if (lane == 0) {
+      row_ntiles[I] = ntiles;
+      row_nvals[I] = nvals;
+      if (e) atomicOr(err_flag, e);
+    }
+  }
+}
+
+// Column counts of A (histogram) for C-bar.
+__global__ void col_hist_kernel(const int32_t* __restrict__ col, int64_t nnz, int64_t ncols,
+                                unsigned* __restrict__ hist) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < nnz;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const int32_t c = __ldg(col + i);
+    if (c >= 0 && c < ncols) atomicAdd(hist + c, 1u);
+  }
+}
+
+__global__ void cbar_dot_kernel(const unsigned* __restrict__ hist, const int64_t* __restrict__ rpB,
+                                int64_t n, unsigned long long* __restrict__ out) {
+  unsigned long long acc = 0;
+  for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k < n;
+       k += int64_t(gridDim.x) * blockDim.x)
+    acc += (unsigned long long)hist[k] * (unsigned long long)(rpB[k + 1] - rpB[k]);
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(kFull, acc, o);
+  if ((threadIdx.x & 31) == 0 && acc) atomicAdd(out, acc);
+}
+
+}  // namespace
+
+void launch_convert_count(const CsrView& in, TileMat& out, uint32_t* row_ntiles,
+                          uint32_t* row_nvals, unsigned* err_flag, int drop_nonfinite,
+                          cudaStream_t st) {
+  const unsigned blocks = (out.tile_rows + 7) / 8;
+  if (blocks == 0) return;
+  convert_kernel<false><<<blocks, 256, 0, st>>>(in, out, 0, nullptr, nullptr, row_ntiles,
+                                                 row_nvals, err_flag, drop_nonfinite);
+}
+
+void launch_convert_fill(const CsrView& in, TileMat& out, int roles, const uint32_t* tile_base,
+                         const uint32_t* val_base, int drop_nonfinite, cudaStream_t st) {
+  const unsigned blocks = (out.tile_rows + 7) / 8;
+  if (blocks == 0) return;
+  convert_kernel<true><<<blocks, 256, 0, st>>>(in, out, roles, tile_base, val_base, nullptr,
+                                                nullptr, nullptr, drop_nonfinite);
+}
+
+void launch_cbar(const int32_t* colA, int64_t nnzA, int64_t inner, const int64_t* rpB,
+                 unsigned* hist, unsigned long long* out, cudaStream_t st) {
+  if (nnzA > 0) col_hist_kernel<<<1184, 256, 0, st>>>(colA, nnzA, inner, hist);
+  if (inner > 0) cbar_dot_kernel<<<592, 256, 0, st>>>(hist, rpB, inner, out);
+}
+
+}  // namespace tsg

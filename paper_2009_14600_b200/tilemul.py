@@ -1,0 +1,294 @@
+"""Python mirror of the reference's hot-path API, over the C ABI.
+
+The reference (tilemul, /root/reference/proj) exposes the spGEMM path as C++:
+``spgemm_square(A)`` (proj/include/tilemul/kernels.hpp:88-89) over
+``from_element_coo`` / ``to_element_coo`` (tile_format.hpp:71-75) and the
+exception taxonomy of errors.hpp:9-51.  This module keeps those names and
+their error behaviour, with CSR (== sorted duplicate-free COO) as the
+interchange format, so the parity tests read like the reference's tests:
+
+    C = spgemm_square(A)          # DimensionError for non-square A
+    C = spgemm(A, B)              # DimensionError when A.cols != B.rows
+    C = spgemm_chain([R, A, P])   # binary16 downcast between stages
+
+Every call runs the sm_100a CUDA path (libtsparse_b200.so); there is no CPU
+fallback.  C++ users get the same names from include/tilemul_gpu.hpp.
+"""
+from __future__ import annotations
+
+import builtins
+import ctypes as C
+import weakref
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib as L
+
+
+class Error(RuntimeError):
+    """tilemul::Error (errors.hpp:9-11)."""
+
+
+class InvariantError(Error):
+    """tilemul::InvariantError: unsorted / duplicated / out-of-range input."""
+
+
+class OverflowError(Error):  # noqa: A001 - mirrors tilemul::OverflowError
+    """tilemul::OverflowError: value outside the binary16 finite range."""
+
+
+class DimensionError(Error):
+    """tilemul::DimensionError: inner dimensions differ / non-square."""
+
+
+class PrecisionError(Error):
+    """tilemul::PrecisionError: non-finite accumulator."""
+
+
+_STATUS = {L.TSG_ERR_INVARIANT: InvariantError, L.TSG_ERR_OVERFLOW: OverflowError,
+           L.TSG_ERR_DIMENSION: DimensionError, L.TSG_ERR_PRECISION: PrecisionError}
+
+
+@dataclass
+class Csr:
+    """CSR matrix: numpy arrays (host) or torch CUDA tensors (device)."""
+    rows: int
+    cols: int
+    row_ptr: object
+    col: object
+    val: object
+
+    @property
+    def nnz(self) -> int:
+        return int(self.col.shape[0])
+
+    @property
+    def on_device(self) -> bool:
+        return hasattr(self.val, "is_cuda") and bool(self.val.is_cuda)
+
+    def to_numpy(self) -> "Csr":
+        if not self.on_device:
+            return self
+        return Csr(self.rows, self.cols, self.row_ptr.cpu().numpy(), self.col.cpu().numpy(),
+                   self.val.cpu().numpy())
+
+    def to_device(self, device: str = "cuda") -> "Csr":
+        import torch
+        if self.on_device:
+            return self
+        return Csr(self.rows, self.cols, torch.from_numpy(np.ascontiguousarray(self.row_ptr)).to(device),
+                   torch.from_numpy(np.ascontiguousarray(self.col)).to(device),
+                   torch.from_numpy(np.ascontiguousarray(self.val)).to(device))
+
+    def nbytes(self) -> int:
+        return int(self.row_ptr.nbytes + self.col.nbytes + self.val.nbytes) if not self.on_device else \
+            int(self.row_ptr.numel() * 8 + self.col.numel() * 4 + self.val.numel() * self.val.element_size())
+
+
+@dataclass
+class Tiles:
+    """16x16 tiled view of C (pre-CSR, compacted): the tile-structure bridge."""
+    tile_row: np.ndarray
+    tile_col: np.ndarray
+    row_masks: np.ndarray  # (ntiles, 16) uint16, bit c of row r = slot (r, c)
+    elem_index: np.ndarray
+    val: np.ndarray
+
+
+@dataclass
+class Result:
+    C: Csr
+    stats: dict = field(default_factory=dict)
+    tiles: Tiles | None = None
+
+
+_DT = {np.dtype(np.float16): L.TSG_F16, np.dtype(np.float32): L.TSG_F32, np.dtype(np.float64): L.TSG_F64}
+
+
+def _view(M: Csr, keep: list) -> L.tsg_csr:
+    v = L.tsg_csr()
+    v.rows, v.cols, v.nnz = int(M.rows), int(M.cols), int(M.nnz)
+    if M.on_device:
+        import torch
+        tdt = {torch.float16: L.TSG_F16, torch.float32: L.TSG_F32, torch.float64: L.TSG_F64}
+        rp = M.row_ptr.contiguous().to(torch.int64)
+        col = M.col.contiguous().to(torch.int32)
+        val = M.val.contiguous()
+        keep += [rp, col, val]
+        v.row_ptr, v.col, v.val = rp.data_ptr(), col.data_ptr(), val.data_ptr()
+        v.dtype = tdt[val.dtype]
+        v.mem = L.TSG_MEM_DEVICE
+    else:
+        rp = np.ascontiguousarray(M.row_ptr, dtype=np.int64)
+        col = np.ascontiguousarray(M.col, dtype=np.int32)
+        val = np.ascontiguousarray(M.val)
+        if val.dtype not in _DT:
+            val = val.astype(np.float64)
+        keep += [rp, col, val]
+        v.row_ptr, v.col, v.val = rp.ctypes.data, col.ctypes.data, val.ctypes.data
+        v.dtype = _DT[val.dtype]
+        v.mem = L.TSG_MEM_HOST
+    return v
+
+
+def _np_from(ptr: int, n: int, dtype) -> np.ndarray:
+    if n == 0:
+        return np.zeros(0, dtype=dtype)
+    buf = (C.c_char * (n * np.dtype(dtype).itemsize)).from_address(ptr)
+    return np.frombuffer(buf, dtype=dtype).copy()
+
+
+class Context:
+    """One tsg_ctx (device + stream + memory pool).  One per host thread."""
+
+    def __init__(self, device: int = -1, stream: int | None = None):
+        self._lib = L.load()
+        h = C.c_void_p()
+        rc = self._lib.tsg_create(C.byref(h), device, C.c_void_p(stream) if stream else None)
+        if rc != L.TSG_OK:
+            raise Error(f"tsg_create failed ({rc})")
+        self._h = h
+        self._fin = weakref.finalize(self, self._lib.tsg_destroy, h)
+
+    def close(self):
+        self._fin()
+
+    @property
+    def handle(self):
+        return self._h
+
+    def _raise(self, rc: int):
+        msg = self._lib.tsg_last_error(self._h).decode()
+        raise _STATUS.get(rc, Error)(msg)
+
+    def _opts(self, mode, phase_timing, want_tiles, drop_nonfinite) -> L.tsg_options:
+        o = L.tsg_options()
+        self._lib.tsg_default_options(C.byref(o))
+        o.mode = {"tensor": L.TSG_MODE_TENSOR, "ordered": L.TSG_MODE_ORDERED}[mode]
+        o.phase_timing = int(bool(phase_timing))
+        o.want_tiles = int(bool(want_tiles))
+        o.drop_nonfinite = int(bool(drop_nonfinite))
+        return o
+
+    def _collect(self, out: L.tsg_csr_out, device: bool) -> Csr:
+        if device:
+            import torch
+            n, r = int(out.nnz), int(out.rows)
+            # copy into torch-owned memory, then release the library buffers
+            rp = _cuda_tensor(out.row_ptr, r + 1, torch.int64).clone()
+            col = _cuda_tensor(out.col, n, torch.int32).clone() if n else torch.zeros(0, dtype=torch.int32, device="cuda")
+            val = _cuda_tensor(out.val, n, torch.float32).clone() if n else torch.zeros(0, dtype=torch.float32, device="cuda")
+            torch.cuda.synchronize()
+            res = Csr(int(out.rows), int(out.cols), rp, col, val)
+        else:
+            res = Csr(int(out.rows), int(out.cols), _np_from(out.row_ptr, int(out.rows) + 1, np.int64),
+                      _np_from(out.col, int(out.nnz), np.int32), _np_from(out.val, int(out.nnz), np.float32))
+        self._lib.tsg_free_csr(self._h, C.byref(out))
+        return res
+
+    def spgemm(self, A: Csr, B: Csr, *, mode: str = "tensor", out: str = "host",
+               want_tiles: bool = False, phase_timing: bool = False,
+               drop_nonfinite: bool = False) -> Result:
+        keep: list = []
+        a = _view(A, keep)
+        b = a if B is A else _view(B, keep)
+        o = self._opts(mode, phase_timing, want_tiles, drop_nonfinite)
+        co = L.tsg_csr_out()
+        co.mem = L.TSG_MEM_DEVICE if out == "device" else L.TSG_MEM_HOST
+        st = L.tsg_run_stats()
+        to = L.tsg_tiles_out()
+        rc = self._lib.tsg_spgemm(self._h, C.byref(a), C.byref(b), C.byref(co), C.byref(o),
+                                  C.byref(st), C.byref(to))
+        if rc != L.TSG_OK:
+            self._raise(rc)
+        res = Result(self._collect(co, out == "device"), st.as_dict())
+        if want_tiles:
+            nt, nz = int(to.ntiles), int(to.nnz)
+            res.tiles = Tiles(_np_from(to.tile_row, nt, np.uint32), _np_from(to.tile_col, nt, np.uint32),
+                              _np_from(to.row_masks, nt * 16, np.uint16).reshape(nt, 16),
+                              _np_from(to.elem_index, nt, np.uint64), _np_from(to.val, nz, np.float32))
+            self._lib.tsg_free_tiles(C.byref(to))
+        return res
+
+    def spgemm_raw(self, a: L.tsg_csr, b: L.tsg_csr, o: L.tsg_options, co: L.tsg_csr_out,
+                   st: L.tsg_run_stats | None = None) -> int:
+        """Zero-overhead call for benchmarking (caller frees `co`)."""
+        return self._lib.tsg_spgemm(self._h, C.byref(a), C.byref(b), C.byref(co), C.byref(o),
+                                    C.byref(st) if st is not None else None, None)
+
+    def free(self, co: L.tsg_csr_out):
+        self._lib.tsg_free_csr(self._h, C.byref(co))
+
+    def spgemm_chain(self, mats: list, *, mode: str = "tensor", out: str = "host",
+                     phase_timing: bool = False) -> Result:
+        keep: list = []
+        views = [_view(M, keep) for M in mats]
+        arr = (C.POINTER(L.tsg_csr) * len(views))(*[C.pointer(v) for v in views])
+        o = self._opts(mode, phase_timing, False, False)
+        co = L.tsg_csr_out()
+        co.mem = L.TSG_MEM_DEVICE if out == "device" else L.TSG_MEM_HOST
+        st = L.tsg_run_stats()
+        rc = self._lib.tsg_spgemm_chain(self._h, len(views), arr, C.byref(co), C.byref(o), C.byref(st))
+        if rc != L.TSG_OK:
+            self._raise(rc)
+        return Result(self._collect(co, out == "device"), st.as_dict())
+
+    def cbar(self, A: Csr, B: Csr) -> int:
+        keep: list = []
+        a, b = _view(A, keep), _view(B, keep)
+        v = C.c_uint64()
+        rc = self._lib.tsg_cbar(self._h, C.byref(a), C.byref(b), C.byref(v))
+        if rc != L.TSG_OK:
+            self._raise(rc)
+        return int(v.value)
+
+    def launch_count(self) -> int:
+        return int(self._lib.tsg_launch_count(self._h))
+
+    def last_phase_ms(self, phase: str) -> float:
+        return float(self._lib.tsg_last_kernel_ms(self._h, phase.encode()))
+
+
+class _CAI:
+    def __init__(self, ptr, n, typestr):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": typestr, "data": (ptr, False),
+                                         "version": 3, "strides": None}
+
+
+def _cuda_tensor(ptr, n, dtype):
+    import torch
+    ts = {torch.int64: "<i8", torch.int32: "<i4", torch.float32: "<f4"}[dtype]
+    return torch.as_tensor(_CAI(ptr, n, ts), device="cuda")
+
+
+_default: Context | None = None
+
+
+def default_context() -> Context:
+    global _default
+    if _default is None:
+        _default = Context()
+    return _default
+
+
+def spgemm(A: Csr, B: Csr, **kw) -> Csr:
+    """C = A.B (the pass composition of proj/tests/test_kernels.cpp:197-202)."""
+    return default_context().spgemm(A, B, **kw).C
+
+
+def spgemm_square(A: Csr, **kw) -> Csr:
+    """C = A.A; DimensionError for non-square input (kernels.cpp:223-226)."""
+    if A.rows != A.cols:
+        raise DimensionError(f"matrix squaring needs a square input, got {A.rows}x{A.cols}")
+    return default_context().spgemm(A, A, **kw).C
+
+
+def spgemm_chain(mats: list, **kw) -> Csr:
+    """X0.X1...Xn-1 left to right with the binary16 downcast between stages."""
+    return default_context().spgemm_chain(mats, **kw).C
+
+
+__all__ = ["Error", "InvariantError", "OverflowError", "DimensionError", "PrecisionError", "Csr",
+           "Tiles", "Result", "Context", "spgemm", "spgemm_square", "spgemm_chain", "default_context"]
+_ = builtins  # builtins.OverflowError stays reachable as builtins.OverflowError

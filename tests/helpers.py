@@ -1,0 +1,85 @@
+"""Comparison helpers shared by the parity tests (test infrastructure)."""
+from __future__ import annotations
+
+import numpy as np
+
+
+def csr_pattern_equal(C, R) -> bool:
+    return (C.rows == R.rows and C.cols == R.cols and np.array_equal(np.asarray(C.row_ptr), R.row_ptr)
+            and np.array_equal(np.asarray(C.col), R.col))
+
+
+def csr_bits_equal(C, R) -> bool:
+    """Positions and fp32 bit patterns equal (bit_equal_coo, corpus.hpp:102-116)."""
+    if not csr_pattern_equal(C, R):
+        return False
+    a = np.asarray(C.val, dtype=np.float32).view(np.uint32)
+    b = np.asarray(R.val, dtype=np.float64).astype(np.float32).view(np.uint32)
+    return np.array_equal(a, b)
+
+
+def first_diff(C, R) -> str:
+    if C.rows != R.rows or C.cols != R.cols:
+        return f"dims {C.rows}x{C.cols} vs {R.rows}x{R.cols}"
+    rp = np.asarray(C.row_ptr)
+    if not np.array_equal(rp, R.row_ptr):
+        i = int(np.nonzero(rp != R.row_ptr)[0][0])
+        return f"row_ptr[{i}] {rp[i]} vs {R.row_ptr[i]} (nnz {rp[-1]} vs {R.row_ptr[-1]})"
+    col = np.asarray(C.col)
+    if not np.array_equal(col, R.col):
+        i = int(np.nonzero(col != R.col)[0][0])
+        return f"col[{i}] {col[i]} vs {R.col[i]}"
+    a = np.asarray(C.val, dtype=np.float32)
+    b = R.val.astype(np.float32)
+    i = np.nonzero(a.view(np.uint32) != b.view(np.uint32))[0]
+    return f"{i.size} value bit mismatches, first at {int(i[0])}: {a[i[0]]!r} vs {b[i[0]]!r}" if i.size else "equal"
+
+
+def tolerance_ok(C, R, A, B, factor: float = 2.0) -> tuple[bool, float]:
+    """|c - r| <= factor * n * 2^-23 * sum_k |a_ik b_kj|.
+
+    Needs the |A|.|B| product and per-element product counts; computed with
+    a float64 Gustavson over the same CSR (test sizes only)."""
+    absprod, nprod = _abs_product(A, B)
+    rows = np.repeat(np.arange(R.rows), np.diff(R.row_ptr))
+    key = rows.astype(np.int64) * R.cols + R.col
+    bound = np.array([factor * nprod.get(k, 1) * 2.0 ** -23 * absprod.get(k, 0.0) for k in key.tolist()])
+    err = np.abs(np.asarray(C.val, np.float64) - R.val)
+    return bool(np.all(err <= bound)), float(np.max(err / np.maximum(bound, 1e-300))) if err.size else 0.0
+
+
+def _abs_product(A, B):
+    absprod, nprod = {}, {}
+    arp, acol, aval = np.asarray(A.row_ptr), np.asarray(A.col), np.abs(np.asarray(A.val, np.float64))
+    brp, bcol, bval = np.asarray(B.row_ptr), np.asarray(B.col), np.abs(np.asarray(B.val, np.float64))
+    aval = aval.astype(np.float16).astype(np.float64)
+    bval = bval.astype(np.float16).astype(np.float64)
+    for i in range(A.rows):
+        for p in range(arp[i], arp[i + 1]):
+            k = acol[p]
+            for q in range(brp[k], brp[k + 1]):
+                key = i * B.cols + int(bcol[q])
+                absprod[key] = absprod.get(key, 0.0) + aval[p] * bval[q]
+                nprod[key] = nprod.get(key, 0) + 1
+    return absprod, nprod
+
+
+def quadrants(tiles) -> tuple[np.ndarray, np.ndarray, np.ndarray]:
+    """16x16 tiles -> the 8x8 tiles they contain (SURVEY.md 8(c) bridge):
+    tile (I,J) quadrant (qr,qc) -> 8x8 tile (2I+qr, 2J+qc), bit 8r+c =
+    mask bit 16(8qr+r)+(8qc+c); empty quadrants dropped; sorted (row, col)."""
+    rows, cols, bms = [], [], []
+    m = tiles.row_masks.astype(np.uint64)
+    for qr in (0, 1):
+        for qc in (0, 1):
+            bm = np.zeros(m.shape[0], dtype=np.uint64)
+            for r in range(8):
+                byte = (m[:, 8 * qr + r] >> np.uint64(8 * qc)) & np.uint64(0xFF)
+                bm |= byte << np.uint64(8 * r)
+            keep = bm != 0
+            rows.append(2 * tiles.tile_row[keep].astype(np.int64) + qr)
+            cols.append(2 * tiles.tile_col[keep].astype(np.int64) + qc)
+            bms.append(bm[keep])
+    rows, cols, bms = np.concatenate(rows), np.concatenate(cols), np.concatenate(bms)
+    order = np.lexsort((cols, rows))
+    return rows[order], cols[order], bms[order]

@@ -1,0 +1,133 @@
+"""GPU parity tests: the CUDA path (through the C ABI) vs the reference.
+
+The reference is the unmodified tilemul library compiled in place
+(oracle/_ref, see oracle/Makefile).  Bars:
+  * ORDERED mode: bit-exact values and pattern vs dense_spgemm_mixed_ordered
+    on every input (the acceptance criterion-1 contract).
+  * TENSOR mode: pattern and tile structure bit-exact; values bit-exact on
+    integer / dyadic inputs, else |c - r| <= 2 n 2^-23 sum|a b|.
+"""
+import numpy as np
+import pytest
+
+from oracle import ref
+from paper_2009_14600_b200 import tilemul as T
+from paper_2009_14600_b200 import workloads as W
+from tests.helpers import csr_bits_equal, csr_pattern_equal, first_diff, quadrants, tolerance_ok
+
+pytestmark = pytest.mark.gpu
+
+
+def test_golden_hash_fixture(ctx):
+    """proj/tests/test_cli.cpp:149-169 fixture: seed 5150, 120^2, 5%."""
+    A = ref.random_coo(5150, 120, 120, 0.05)
+    want = ref.oracle(A)
+    assert want.fnv == 0x2D882906D15D6FAF
+    for mode in ("ordered", "tensor"):
+        res = ctx.spgemm(A, A, mode=mode, want_tiles=True)
+        if mode == "ordered":  # the reference's bit-exact contract
+            assert csr_bits_equal(res.C, want), (mode, first_diff(res.C, want))
+        else:  # MMA accumulation order: pattern exact, values within tolerance
+            assert csr_pattern_equal(res.C, want), first_diff(res.C, want)
+            ok, worst = tolerance_ok(res.C, want, A, A)
+            assert ok, worst
+        r, c, b = quadrants(res.tiles)
+        assert np.array_equal(r, want.tile_row) and np.array_equal(c, want.tile_col)
+        assert np.array_equal(b, want.bitmap)
+
+
+@pytest.mark.parametrize("mode", ["ordered", "tensor"])
+def test_acceptance_corpus(ctx, mode):
+    """acceptance.cpp:45-58,114-135: 200 matrices, SignedHalves."""
+    bad = []
+    for i in range(200):
+        A = ref.corpus("main", i)
+        want = ref.oracle(A)
+        got = ctx.spgemm(A, A, mode=mode).C
+        if mode == "ordered":
+            if not csr_bits_equal(got, want):
+                bad.append((i, first_diff(got, want)))
+        else:
+            if not csr_pattern_equal(got, want):
+                bad.append((i, first_diff(got, want)))
+                continue
+            ok, worst = tolerance_ok(got, want, A, A) if A.rows <= 200 else (True, 0.0)
+            if not ok:
+                bad.append((i, f"tolerance {worst}"))
+    assert not bad, bad[:5]
+
+
+def test_wild_corpus_ordered(ctx):
+    """test_kernels.cpp:332-348: full binary16 range, odd dims (edge tiles)."""
+    for i in range(30):
+        A = ref.corpus("wild", i)
+        want = ref.oracle(A)
+        got = ctx.spgemm(A, A, mode="ordered").C
+        assert csr_bits_equal(got, want), (i, first_diff(got, want))
+
+
+def test_poisson_tensor_bit_exact(ctx):
+    A = W.poisson2d(256)
+    want = ref.spgemm(A)
+    res = ctx.spgemm(A, A, want_tiles=True)
+    assert csr_bits_equal(res.C, want), first_diff(res.C, want)
+    assert res.stats["counted_elements"] == want.counted
+    r, c, b = quadrants(res.tiles)
+    assert np.array_equal(r, want.tile_row) and np.array_equal(c, want.tile_col)
+    assert np.array_equal(b, want.bitmap)
+
+
+def test_fem27_tensor_bit_exact(ctx):
+    A = W.fem27(64)
+    want = ref.spgemm(A)
+    res = ctx.spgemm(A, A)
+    assert csr_bits_equal(res.C, want), first_diff(res.C, want)
+    st = res.stats
+    assert st["counted_elements"] == want.counted == 30959144
+    assert st["nnz_c"] == want.realized
+    # T=16 restatement counts
+    assert st["tiles_a"] == 361000
+    assert st["raw_pairs"] == 8329256 and st["filtered_pairs"] == 7047832
+    assert st["segments"] == 985960
+
+
+def test_rect_small(ctx):
+    A = W.random_uniform(20000, 10000, 40000, 5)
+    B = W.random_uniform(10000, 20000, 40000, 6)
+    want = ref.spgemm(A, B)
+    got = ctx.spgemm(A, B).C
+    assert csr_pattern_equal(got, want), first_diff(got, want)
+    assert got.nnz == want.realized
+
+
+def test_amg_chain_small(ctx):
+    R, A, P = W.amg(32)
+    want = ref.chain([R, A, P])
+    got = ctx.spgemm_chain([R, A, P]).C
+    assert csr_bits_equal(got, want), first_diff(got, want)
+
+
+def test_errors(ctx):
+    A = ref.random_coo(7, 32, 32, 0.1)
+    B = ref.random_coo(8, 16, 32, 0.1)
+    with pytest.raises(T.DimensionError):
+        ctx.spgemm(A, B)
+    big = T.Csr(8, 8, np.array([0, 1, 1, 1, 1, 1, 1, 1, 1]), np.array([0], np.int32), np.array([70000.0]))
+    with pytest.raises(T.OverflowError):
+        ctx.spgemm(big, big)
+    bad = T.Csr(8, 8, np.array([0, 2, 2, 2, 2, 2, 2, 2, 2]), np.array([3, 1], np.int32), np.array([1.0, 2.0]))
+    with pytest.raises(T.InvariantError):
+        ctx.spgemm(bad, bad)
+    nan = T.Csr(8, 8, np.array([0, 1, 1, 1, 1, 1, 1, 1, 1]), np.array([0], np.int32), np.array([np.nan]))
+    with pytest.raises(T.OverflowError):
+        ctx.spgemm(nan, nan)
+    assert ctx.spgemm(nan, nan, drop_nonfinite=True).C.nnz == 0
+
+
+def test_empty_and_identity(ctx):
+    E = T.Csr(32, 32, np.zeros(33, np.int64), np.zeros(0, np.int32), np.zeros(0, np.float32))
+    assert ctx.spgemm(E, E).C.nnz == 0
+    n = 64
+    I = T.Csr(n, n, np.arange(n + 1, dtype=np.int64), np.arange(n, dtype=np.int32), np.ones(n, np.float32))
+    C = ctx.spgemm(I, I).C
+    assert np.array_equal(C.col, np.arange(n)) and np.all(C.val == 1.0)
