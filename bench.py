@@ -54,6 +54,7 @@ def parse():
     p.add_argument("--mode", default="tensor", choices=["tensor", "ordered"])
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-sample-runs", type=int, default=3)
+    p.add_argument("--no-e2e", action="store_true", help="skip the host-to-host e2e measurement")
     return p.parse_args()
 
 
@@ -290,9 +291,12 @@ def run_ours(args):
         e2e_stats["d2h"] = int(st2.d2h_bytes)
         return co
 
-    for _ in range(2):
-        ctx.free(e2e_step())
-    e2e_times = timed(max(3, args.steps // 2), e2e_step)
+    if args.no_e2e:
+        e2e_times = [float("nan")]
+    else:
+        for _ in range(2):
+            ctx.free(e2e_step())
+        e2e_times = timed(max(3, args.steps // 2), e2e_step)
     e2e_ms = float(np.mean(e2e_times))
     if world > 1:
         t = torch.tensor([e2e_ms], device=dev)

@@ -20,12 +20,21 @@
 
 #include <cstdint>
 #include <cstdio>
+#include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
 
 #include "../../include/tsparse_b200.h"
 #include "tsg_kernels.cuh"
+
+namespace tsg {
+int tuning_variant(const char* name, int dflt) {
+  const char* v = std::getenv(name);
+  return v ? std::atoi(v) : dflt;
+}
+}  // namespace tsg
 
 struct tsg_ctx {
   int device = 0;
@@ -134,8 +143,8 @@ void check_csr(const tsg_csr* M, const char* name) {
     throw Fail{TSG_ERR_OTHER, std::string(name) + ": unknown dtype"};
   if (M->rows > (int64_t(1) << 35) || M->cols > (int64_t(1) << 31) - 16)
     throw Fail{TSG_ERR_OTHER, std::string(name) + ": dimensions beyond the 16x16 tile index range"};
-  if (M->nnz >= (int64_t(1) << 32))
-    throw Fail{TSG_ERR_OTHER, std::string(name) + ": nnz beyond 2^32 needs row-panel batching"};
+  if (M->nnz >= (int64_t(1) << 29))
+    throw Fail{TSG_ERR_OTHER, std::string(name) + ": nnz beyond 2^29 needs row-panel batching"};
   if ((M->rows > 0 || M->nnz > 0) && (!M->row_ptr || (M->nnz > 0 && (!M->col || !M->val))))
     throw Fail{TSG_ERR_OTHER, std::string(name) + ": missing arrays"};
 }
@@ -170,9 +179,22 @@ CsrView stage(tsg_ctx* ctx, Scratch& sc, const tsg_csr* M, tsg_run_stats* st) {
   return v;
 }
 
-// CSR -> 16x16 tiles (count, scan, fill).  Returns the tile count.
-uint64_t convert(tsg_ctx* ctx, Scratch& sc, const CsrView& in, TileMat& T, int roles,
-                 unsigned* err_flag, int drop_nonfinite, uint64_t* nvals_out) {
+// Several device scalars -> host with one synchronisation.
+template <class T, int N>
+void readback_many(tsg_ctx* ctx, const T* const (&src)[N], T (&dst)[N]) {
+  static_assert(N * sizeof(T) <= 48, "pinned staging is 64 bytes");
+  for (int i = 0; i < N; ++i)
+    TSG_CUDA(cudaMemcpyAsync(reinterpret_cast<char*>(ctx->pinned) + i * sizeof(T), src[i], sizeof(T),
+                             cudaMemcpyDeviceToHost, ctx->stream));
+  TSG_CUDA(cudaStreamSynchronize(ctx->stream));
+  std::memcpy(dst, ctx->pinned, N * sizeof(T));
+}
+
+// CSR -> 16x16 tiles (count, scan, fill).  No host synchronisation: every
+// array is sized by the input nnz (an upper bound on tiles and chunks).
+// Returns the device address of the tile count (trp[tile_rows]).
+const uint32_t* convert(tsg_ctx* ctx, Scratch& sc, const CsrView& in, TileMat& T, int roles,
+                        unsigned* err_flag, int drop_nonfinite) {
   T.rows = in.rows;
   T.cols = in.cols;
   T.tile_rows = uint32_t((in.rows + 15) / 16);
@@ -188,39 +210,32 @@ uint64_t convert(tsg_ctx* ctx, Scratch& sc, const CsrView& in, TileMat& T, int r
   auto* vbase = sc.alloc<uint32_t>(nr);
   exclusive_sum(ctx, sc, row_nt, T.trp, nr);
   exclusive_sum(ctx, sc, row_nv, vbase, nr);
-  // capacities: tiles <= nnz, values <= nnz (no host sync needed)
   const uint64_t cap = uint64_t(in.nnz);
-  T.cap_tiles = cap;
-  T.cap_vals = cap;
-  T.tcol = sc.alloc<uint32_t>(cap);
-  T.rmask = sc.alloc<uint16_t>(cap * 16);
-  T.occ = sc.alloc<uint32_t>(cap);
-  T.voff = sc.alloc<uint32_t>(cap);
+  T.cap = cap;
+  T.tco = sc.alloc<uint2>(cap);
+  // one extra all-zero tile (index cap) pads the counting pass's batches
+  T.rm2 = sc.alloc<uint32_t>((cap + 1) * 8);
+  T.cm2 = sc.alloc<uint32_t>((cap + 1) * 8);
+  TSG_CUDA(cudaMemsetAsync(T.rm2 + cap * 8, 0, 32, ctx->stream));
+  TSG_CUDA(cudaMemsetAsync(T.cm2 + cap * 8, 0, 32, ctx->stream));
   for (int role = 0; role < 2; ++role) {
     if (!(roles & (1 << role))) continue;
-    T.fhdr[role] = sc.alloc<uint16_t>(cap * 32);
-    T.vals[role] = sc.alloc<__half>(cap);
+    T.meta[role] = sc.alloc<uint2>(cap);
+    T.chunk[role] = sc.alloc<uint4>(cap + 1);
+    TSG_CUDA(cudaMemsetAsync(T.chunk[role], 0, sizeof(uint4), ctx->stream));  // zero chunk 0
   }
   launch_convert_fill(in, T, roles, T.trp, vbase, drop_nonfinite, ctx->stream);
   check_launch(ctx);
-  uint32_t tail[2];
-  TSG_CUDA(cudaMemcpyAsync(ctx->pinned, T.trp + nr - 1, 4, cudaMemcpyDeviceToHost, ctx->stream));
-  TSG_CUDA(cudaMemcpyAsync(reinterpret_cast<char*>(ctx->pinned) + 4, vbase + nr - 1, 4,
-                           cudaMemcpyDeviceToHost, ctx->stream));
-  TSG_CUDA(cudaStreamSynchronize(ctx->stream));
-  std::memcpy(tail, ctx->pinned, 8);
-  if (nvals_out) *nvals_out = tail[1];
-  return tail[0];
+  return T.trp + nr - 1;
 }
 
-void raise_flags(tsg_ctx* ctx, unsigned flags) {
+void raise_flags(unsigned flags) {
   if (flags & kErrInvariant)
     throw Fail{TSG_ERR_INVARIANT, "CSR entries unsorted, duplicated, or out of range"};
   if (flags & kErrOverflow)
     throw Fail{TSG_ERR_OVERFLOW, "value outside binary16 finite range (|x| <= 65504) or non-finite"};
   if (flags & kErrPrecision)
     throw Fail{TSG_ERR_PRECISION, "non-finite accumulator in multiplication pass"};
-  (void)ctx;
 }
 
 struct OutOwner {  // device or pinned-host output buffers
@@ -252,6 +267,52 @@ void* pinned_alloc(tsg_ctx* ctx, size_t bytes, size_t* got) {
   return p;
 }
 
+// Host-side 16x16 tiled view of a CSR (pattern + values), for the parity
+// bridge only (tsg_tiles_out).  Tiles sorted by (row, col), row-major slots.
+void tiles_from_csr(int64_t rows, const std::vector<int64_t>& rp, const std::vector<int32_t>& col,
+                    const std::vector<float>& val, tsg_tiles_out* out) {
+  struct Ent {
+    uint64_t key;  // tile_row << 32 | tile_col
+    uint32_t slot;
+    float v;
+  };
+  std::vector<Ent> e;
+  e.reserve(col.size());
+  for (int64_t r = 0; r < rows; ++r)
+    for (int64_t p = rp[r]; p < rp[r + 1]; ++p)
+      e.push_back({(uint64_t(r >> 4) << 32) | uint32_t(col[p] >> 4),
+                   uint32_t((r & 15) * 16 + (col[p] & 15)), val[p]});
+  std::stable_sort(e.begin(), e.end(), [](const Ent& a, const Ent& b) {
+    return a.key != b.key ? a.key < b.key : a.slot < b.slot;
+  });
+  std::vector<uint32_t> tr, tc;
+  std::vector<uint16_t> rm;
+  std::vector<uint64_t> ei;
+  for (size_t i = 0; i < e.size();) {
+    const uint64_t k = e[i].key;
+    tr.push_back(uint32_t(k >> 32));
+    tc.push_back(uint32_t(k));
+    ei.push_back(i);
+    uint16_t m[16] = {0};
+    for (; i < e.size() && e[i].key == k; ++i) m[e[i].slot >> 4] |= uint16_t(1u << (e[i].slot & 15));
+    rm.insert(rm.end(), m, m + 16);
+  }
+  auto dup = [](const void* src, size_t bytes) {
+    void* p = std::malloc(bytes ? bytes : 1);
+    if (bytes) std::memcpy(p, src, bytes);
+    return p;
+  };
+  std::vector<float> vv(e.size());
+  for (size_t i = 0; i < e.size(); ++i) vv[i] = e[i].v;
+  out->ntiles = int64_t(tr.size());
+  out->nnz = int64_t(vv.size());
+  out->tile_row = static_cast<uint32_t*>(dup(tr.data(), tr.size() * 4));
+  out->tile_col = static_cast<uint32_t*>(dup(tc.data(), tc.size() * 4));
+  out->row_masks = static_cast<uint16_t*>(dup(rm.data(), rm.size() * 2));
+  out->elem_index = static_cast<uint64_t*>(dup(ei.data(), ei.size() * 8));
+  out->val = static_cast<float*>(dup(vv.data(), vv.size() * 4));
+}
+
 void spgemm_impl(tsg_ctx* ctx, const tsg_csr* Ain, const tsg_csr* Bin, tsg_csr_out* C,
                  const tsg_options& opt, tsg_run_stats* st, tsg_tiles_out* tiles) {
   check_csr(Ain, "A");
@@ -267,8 +328,10 @@ void spgemm_impl(tsg_ctx* ctx, const tsg_csr* Ain, const tsg_csr* Bin, tsg_csr_o
   const uint64_t launches0 = ctx->launches;
   record(ctx, timing, 0);
 
-  auto* err_flag = sc.alloc<unsigned>(1);
-  TSG_CUDA(cudaMemsetAsync(err_flag, 0, sizeof(unsigned), s));
+  // device scalars: [0] error flags, [1] max A tiles per tile row
+  auto* dscal = sc.alloc<unsigned>(2);
+  TSG_CUDA(cudaMemsetAsync(dscal, 0, 2 * sizeof(unsigned), s));
+  unsigned* err_flag = dscal;
 
   const bool same = Ain == Bin ||
                     (Ain->row_ptr == Bin->row_ptr && Ain->col == Bin->col && Ain->val == Bin->val &&
@@ -279,119 +342,200 @@ void spgemm_impl(tsg_ctx* ctx, const tsg_csr* Ain, const tsg_csr* Bin, tsg_csr_o
 
   // ---- (1) conversion ------------------------------------------------------
   TileMat TA, TB_own;
-  uint64_t nvA = 0, nvB = 0;
-  const uint64_t tA = convert(ctx, sc, dA, TA, same ? 3 : 1, err_flag, opt.drop_nonfinite, &nvA);
-  uint64_t tB = tA;
-  if (!same) tB = convert(ctx, sc, dB, TB_own, 2, err_flag, opt.drop_nonfinite, &nvB);
+  const uint32_t* ntA_d = convert(ctx, sc, dA, TA, same ? 3 : 1, err_flag, opt.drop_nonfinite);
+  const uint32_t* ntB_d = ntA_d;
+  if (!same) ntB_d = convert(ctx, sc, dB, TB_own, 2, err_flag, opt.drop_nonfinite);
   const TileMat& TB = same ? TA : TB_own;
-  raise_flags(ctx, readback(ctx, err_flag));
+  launch_row_stats(TA, dscal + 1, s);
+  check_launch(ctx);
+  uint64_t tA, tB;
+  bool light;
+  {
+    const unsigned* src[4] = {dscal, dscal + 1, ntA_d, ntB_d};
+    unsigned v[4];
+    readback_many(ctx, src, v);
+    raise_flags(v[0]);
+    light = v[1] <= 32;
+    tA = v[2];
+    tB = v[3];
+  }
   record(ctx, timing, 1);
 
-  // ---- (2) symbolic: enumerate + filter -------------------------------------
+  // ---- (2) symbolic: task list ----------------------------------------------
   TaskList tl;
-  auto* raw_d = sc.alloc<unsigned long long>(1);
-  TSG_CUDA(cudaMemsetAsync(raw_d, 0, sizeof(unsigned long long), s));
-  tl.tile_pair_off = sc.alloc<uint32_t>(tA + 1);
-  auto* tile_cnt = sc.alloc<uint32_t>(tA + 1);
-  TSG_CUDA(cudaMemsetAsync(tile_cnt + tA, 0, sizeof(uint32_t), s));
-  launch_enum_count(TA, TB, tA, tile_cnt, raw_d, s);
-  check_launch(ctx);
-  const uint64_t P = total_u32(ctx, sc, tile_cnt, tA);
-  const uint64_t raw = readback(ctx, raw_d);
-  if (P >= (uint64_t(1) << 31))
-    throw Fail{TSG_ERR_OTHER, "task list beyond 2^31 pairs needs row-panel batching"};
-  exclusive_sum(ctx, sc, tile_cnt, tl.tile_pair_off, tA + 1);
-  tl.npairs = P;
-  uint64_t* pairs_u = sc.alloc<uint64_t>(P);
-  uint32_t* keys_u = sc.alloc<uint32_t>(P);
-  launch_enum_fill(TA, TB, tA, tl.tile_pair_off, pairs_u, keys_u, s);
-  check_launch(ctx);
-  tl.row_pair_off = sc.alloc<uint32_t>(uint64_t(TA.tile_rows) + 1);
-  launch_row_pair_off(TA, tl.tile_pair_off, tl.row_pair_off, s);
-  check_launch(ctx);
-  record(ctx, timing, 2);
-
-  // ---- (2b) stable sort by output tile within each tile row, segments -------
-  tl.pairs = sc.alloc<uint64_t>(P);
-  tl.keys = sc.alloc<uint32_t>(P);
-  if (P > 0) {
-    size_t bytes = 0;
-    TSG_CUDA(cub::DeviceSegmentedSort::StableSortPairs(
-        nullptr, bytes, keys_u, tl.keys, pairs_u, tl.pairs, int(P), int(TA.tile_rows),
-        tl.row_pair_off, tl.row_pair_off + 1, s));
-    void* tmp = sc.alloc<char>(bytes);
-    TSG_CUDA(cub::DeviceSegmentedSort::StableSortPairs(
-        tmp, bytes, keys_u, tl.keys, pairs_u, tl.pairs, int(P), int(TA.tile_rows),
-        tl.row_pair_off, tl.row_pair_off + 1, s));
-  }
   const uint64_t nr = uint64_t(TA.tile_rows) + 1;
-  auto* row_nseg = sc.alloc<uint32_t>(nr);
-  TSG_CUDA(cudaMemsetAsync(row_nseg + nr - 1, 0, sizeof(uint32_t), s));
-  launch_seg_count(TA, tl.row_pair_off, tl.keys, row_nseg, s);
-  check_launch(ctx);
-  const uint64_t S = total_u32(ctx, sc, row_nseg, nr);
+  uint64_t P = 0, S = 0, raw = 0;
   tl.seg_row_ptr = sc.alloc<uint32_t>(nr);
-  exclusive_sum(ctx, sc, row_nseg, tl.seg_row_ptr, nr);
-  tl.nseg = S;
-  tl.seg_off = sc.alloc<uint32_t>(S + 1);
-  tl.seg_col = sc.alloc<uint32_t>(S);
-  {
-    // seg_off[S] = P via the pinned staging word (stream-ordered before any
-    // later readback into the same buffer)
-    uint32_t* stage_word = reinterpret_cast<uint32_t*>(ctx->pinned) + 14;
-    *stage_word = uint32_t(P);
-    TSG_CUDA(cudaMemcpyAsync(tl.seg_off + S, stage_word, 4, cudaMemcpyHostToDevice, s));
+  uint32_t* row_pair_off = sc.alloc<uint32_t>(nr);
+  if (light) {
+    auto* row_np = sc.alloc<uint32_t>(nr);
+    auto* row_ns = sc.alloc<uint32_t>(nr);
+    auto* row_raw = sc.alloc<uint32_t>(nr);
+    TSG_CUDA(cudaMemsetAsync(row_np + nr - 1, 0, 4, s));
+    TSG_CUDA(cudaMemsetAsync(row_ns + nr - 1, 0, 4, s));
+    launch_merge_count(TA, TB, row_np, row_ns, row_raw, s);
+    check_launch(ctx);
+    exclusive_sum(ctx, sc, row_np, row_pair_off, nr);
+    exclusive_sum(ctx, sc, row_ns, tl.seg_row_ptr, nr);
+    auto* raw_d = sc.alloc<unsigned long long>(1);
+    TSG_CUDA(cudaMemsetAsync(raw_d, 0, sizeof(unsigned long long), s));
+    {
+      uint64_t blocks = (nr + 255) / 256;
+      if (blocks > 1184) blocks = 1184;
+      sum_u32_kernel<<<unsigned(blocks), 256, 0, s>>>(row_raw, nr - 1, raw_d);
+      check_launch(ctx);
+    }
+    auto* tot_d = sc.alloc<unsigned long long>(2);
+    // totals fit u32 by construction (P < 2^31 checked below via raw)
+    TSG_CUDA(cudaMemsetAsync(tot_d, 0, 2 * sizeof(unsigned long long), s));
+    TSG_CUDA(cudaMemcpyAsync(tot_d, row_pair_off + nr - 1, 4, cudaMemcpyDeviceToDevice, s));
+    TSG_CUDA(cudaMemcpyAsync(tot_d + 1, tl.seg_row_ptr + nr - 1, 4, cudaMemcpyDeviceToDevice, s));
+    const unsigned long long* src[3] = {tot_d, tot_d + 1, raw_d};
+    unsigned long long v[3];
+    readback_many(ctx, src, v);
+    P = v[0];
+    S = v[1];
+    raw = v[2];
+    if (raw >= (uint64_t(1) << 32))
+      throw Fail{TSG_ERR_OTHER, "task list beyond 2^32 raw pairs needs row-panel batching"};
+    tl.npairs = P;
+    tl.nseg = S;
+    tl.pairs = sc.alloc<uint64_t>(P + 1);
+    tl.pmeta = sc.alloc<uint4>(P + 1);
+    tl.seg_off = sc.alloc<uint32_t>(S + 1);
+    tl.seg_col = sc.alloc<uint32_t>(S);
+    tl.seg_row = sc.alloc<uint32_t>(S);
+    TSG_CUDA(cudaMemcpyAsync(tl.seg_off + S, row_pair_off + nr - 1, 4, cudaMemcpyDeviceToDevice, s));
+    launch_merge_fill(TA, TB, row_pair_off, tl, s);
+    check_launch(ctx);
+    record(ctx, timing, 2);
+    record(ctx, timing, 3);  // the merge is the sort: no separate phase
+  } else {
+    auto* raw_d = sc.alloc<unsigned long long>(1);
+    TSG_CUDA(cudaMemsetAsync(raw_d, 0, sizeof(unsigned long long), s));
+    auto* tile_off = sc.alloc<uint32_t>(tA + 1);
+    auto* tile_cnt = sc.alloc<uint32_t>(tA + 1);
+    TSG_CUDA(cudaMemsetAsync(tile_cnt + tA, 0, sizeof(uint32_t), s));
+    launch_enum_count(TA, TB, tA, tile_cnt, raw_d, s);
+    check_launch(ctx);
+    P = total_u32(ctx, sc, tile_cnt, tA);
+    raw = readback(ctx, raw_d);
+    if (P >= (uint64_t(1) << 31))
+      throw Fail{TSG_ERR_OTHER, "task list beyond 2^31 pairs needs row-panel batching"};
+    exclusive_sum(ctx, sc, tile_cnt, tile_off, tA + 1);
+    tl.npairs = P;
+    uint64_t* pairs_u = sc.alloc<uint64_t>(P);
+    uint32_t* keys_u = sc.alloc<uint32_t>(P);
+    launch_enum_fill(TA, TB, tA, tile_off, pairs_u, keys_u, s);
+    check_launch(ctx);
+    launch_row_pair_off(TA, tile_off, row_pair_off, s);
+    check_launch(ctx);
+    record(ctx, timing, 2);
+    // stable sort by output tile column within each tile row
+    tl.pairs = sc.alloc<uint64_t>(P + 1);
+    uint32_t* keys = sc.alloc<uint32_t>(P);
+    if (P > 0) {
+      size_t bytes = 0;
+      TSG_CUDA(cub::DeviceSegmentedSort::StableSortPairs(nullptr, bytes, keys_u, keys, pairs_u,
+                                                         tl.pairs, int(P), int(TA.tile_rows),
+                                                         row_pair_off, row_pair_off + 1, s));
+      void* tmp = sc.alloc<char>(bytes);
+      TSG_CUDA(cub::DeviceSegmentedSort::StableSortPairs(tmp, bytes, keys_u, keys, pairs_u,
+                                                         tl.pairs, int(P), int(TA.tile_rows),
+                                                         row_pair_off, row_pair_off + 1, s));
+    }
+    auto* row_nseg = sc.alloc<uint32_t>(nr);
+    TSG_CUDA(cudaMemsetAsync(row_nseg + nr - 1, 0, sizeof(uint32_t), s));
+    launch_seg_count(TA, row_pair_off, keys, row_nseg, s);
+    check_launch(ctx);
+    S = total_u32(ctx, sc, row_nseg, nr);
+    exclusive_sum(ctx, sc, row_nseg, tl.seg_row_ptr, nr);
+    tl.nseg = S;
+    tl.seg_off = sc.alloc<uint32_t>(S + 1);
+    tl.seg_col = sc.alloc<uint32_t>(S);
+    tl.seg_row = sc.alloc<uint32_t>(S);
+    TSG_CUDA(cudaMemcpyAsync(tl.seg_off + S, row_pair_off + nr - 1, 4, cudaMemcpyDeviceToDevice, s));
+    launch_seg_fill(TA, row_pair_off, keys, tl, s);
+    check_launch(ctx);
+    tl.pmeta = sc.alloc<uint4>(P + 1);
+    launch_pair_meta(TA, TB, tl, s);
+    check_launch(ctx);
+    record(ctx, timing, 3);
   }
-  launch_seg_fill(TA, tl.row_pair_off, tl.keys, tl.seg_row_ptr, tl.seg_off, tl.seg_col, s);
-  check_launch(ctx);
-  record(ctx, timing, 3);
 
-  // ---- counting --------------------------------------------------------------
-  OutTiles ot;
-  ot.counted = sc.alloc<uint32_t>(S + 1);
-  TSG_CUDA(cudaMemsetAsync(ot.counted + S, 0, sizeof(uint32_t), s));
-  launch_counting(TA, TB, tl, ot.counted, s);
-  check_launch(ctx);
-  const uint64_t counted = total_u32(ctx, sc, ot.counted, S);
-  if (counted >= (uint64_t(1) << 32))
-    throw Fail{TSG_ERR_OTHER, "output beyond 2^32 elements needs row-panel batching"};
-  ot.elem_off = sc.alloc<uint32_t>(S + 1);
-  exclusive_sum(ctx, sc, ot.counted, ot.elem_off, S + 1);
-  record(ctx, timing, 4);
+  // pad entries: pairs[P] -> the all-zero mask tiles, pmeta[P] -> zero chunks
+  {
+    uint64_t* pad_host = reinterpret_cast<uint64_t*>(ctx->pinned) + 6;
+    *pad_host = uint64_t(uint32_t(TA.cap)) | (uint64_t(uint32_t(TB.cap)) << 32);
+    TSG_CUDA(cudaMemcpyAsync(tl.pairs + P, pad_host, 8, cudaMemcpyHostToDevice, s));
+    TSG_CUDA(cudaMemsetAsync(tl.pmeta + P, 0, sizeof(uint4), s));
+  }
 
-  // ---- (3) numeric -----------------------------------------------------------
-  ot.cmask = sc.alloc<uint16_t>(S * 16);
-  ot.vals = sc.alloc<float>(counted);
-  launch_numeric(TA, TB, tl, ot, opt.mode, err_flag, s);
-  check_launch(ctx);
-  record(ctx, timing, 5);
-
-  // ---- (4) tiled -> CSR with fused compaction ----------------------------------
+  // ---- counting pass + output positions ----------------------------------------
+  OutPlan op;
   const int64_t rows = Ain->rows;
-  auto* rowcnt = sc.alloc<int64_t>(rows + 1);
-  TSG_CUDA(cudaMemsetAsync(rowcnt + rows, 0, sizeof(int64_t), s));
-  launch_out_rowcount(TA, rows, tl, ot, rowcnt, s);
+  op.bm2 = sc.alloc<uint32_t>(S * 8);
+  op.cnt = sc.alloc<uint8_t>(S * 16);
+  op.pos = sc.alloc<uint32_t>(S * 16);
+  op.rowcnt = sc.alloc<int64_t>(rows + 1);
+  TSG_CUDA(cudaMemsetAsync(op.rowcnt + rows, 0, sizeof(int64_t), s));
+  launch_counting(TA, TB, tl, op, s);
+  check_launch(ctx);
+  launch_row_counts(rows, TA.tile_rows, tl, op, s);
   check_launch(ctx);
   auto* owner = new OutOwner();
   owner->host = C->mem == TSG_MEM_HOST;
   C->_owner = owner;  // released by free_out on any later failure
-  int64_t* d_rp = nullptr;
-  int32_t* d_col = nullptr;
-  float* d_val = nullptr;
-  // output buffers: device outputs outlive the call; host outputs use scratch
-  d_rp = owner->host ? sc.alloc<int64_t>(rows + 1) : sc.alloc<int64_t>(rows + 1, true);
-  if (!owner->host) owner->p[0] = d_rp;
-  exclusive_sum(ctx, sc, rowcnt, d_rp, uint64_t(rows) + 1);
-  const int64_t nnzC = readback(ctx, d_rp + rows);
-  raise_flags(ctx, readback(ctx, err_flag));
-  d_col = owner->host ? sc.alloc<int32_t>(nnzC) : sc.alloc<int32_t>(nnzC, true);
-  d_val = owner->host ? sc.alloc<float>(nnzC) : sc.alloc<float>(nnzC, true);
+  op.row_ptr = owner->host ? sc.alloc<int64_t>(rows + 1) : sc.alloc<int64_t>(rows + 1, true);
+  if (!owner->host) owner->p[0] = op.row_ptr;
+  exclusive_sum(ctx, sc, op.rowcnt, op.row_ptr, uint64_t(rows) + 1);
+  launch_positions(rows, TA.tile_rows, tl, op, s);
+  check_launch(ctx);
+  const uint64_t counted = uint64_t(readback(ctx, op.row_ptr + rows));
+  if (counted >= (uint64_t(1) << 32))
+    throw Fail{TSG_ERR_OTHER, "output beyond 2^32 elements needs row-panel batching"};
+  record(ctx, timing, 4);
+
+  // ---- (3) numeric -> final CSR at the counted positions ---------------------
+  op.col = sc.alloc<int32_t>(counted, !owner->host);
+  op.val = sc.alloc<float>(counted, !owner->host);
+  launch_numeric(TA, TB, tl, op, opt.mode, err_flag, s);
+  check_launch(ctx);
+  const unsigned flags = readback(ctx, err_flag);
+  raise_flags(flags);
+  record(ctx, timing, 5);
+
+  // ---- (4) compaction fix-up (only when some slot cancelled to zero) -----------
+  int64_t nnzC = int64_t(counted);
+  int64_t* d_rp = op.row_ptr;
+  int32_t* d_col = op.col;
+  float* d_val = op.val;
+  if (flags & kCancelled) {
+    auto* rowcnt = sc.alloc<int64_t>(rows + 1);
+    TSG_CUDA(cudaMemsetAsync(rowcnt + rows, 0, sizeof(int64_t), s));
+    launch_compact_count(rows, op, rowcnt, s);
+    check_launch(ctx);
+    int64_t* new_rp = sc.alloc<int64_t>(rows + 1, !owner->host);
+    exclusive_sum(ctx, sc, rowcnt, new_rp, uint64_t(rows) + 1);
+    nnzC = readback(ctx, new_rp + rows);
+    int32_t* ncol = sc.alloc<int32_t>(nnzC, !owner->host);
+    float* nval = sc.alloc<float>(nnzC, !owner->host);
+    launch_compact_fill(rows, op, new_rp, ncol, nval, s);
+    check_launch(ctx);
+    if (!owner->host) {  // the uncompacted buffers become scratch
+      sc.ptrs.push_back(op.row_ptr);
+      sc.ptrs.push_back(op.col);
+      sc.ptrs.push_back(op.val);
+    }
+    d_rp = new_rp;
+    d_col = ncol;
+    d_val = nval;
+  }
   if (!owner->host) {
+    owner->p[0] = d_rp;
     owner->p[1] = d_col;
     owner->p[2] = d_val;
   }
-  launch_out_fill(TA, rows, tl, ot, d_rp, d_col, d_val, s);
-  check_launch(ctx);
   record(ctx, timing, 6);
 
   C->rows = Ain->rows;
@@ -413,49 +557,18 @@ void spgemm_impl(tsg_ctx* ctx, const tsg_csr* Ain, const tsg_csr* Bin, tsg_csr_o
   C->col = static_cast<int32_t*>(owner->p[1]);
   C->val = static_cast<float*>(owner->p[2]);
 
-  if (tiles) {  // pre-CSR tiled view for the tile-structure bridge (test path)
-    std::vector<uint32_t> h_seg_row(nr), h_seg_col(S), h_off(S + 1);
-    std::vector<uint16_t> h_mask(S * 16);
-    std::vector<float> h_vals(counted);
-    TSG_CUDA(cudaMemcpyAsync(h_seg_row.data(), tl.seg_row_ptr, nr * 4, cudaMemcpyDeviceToHost, s));
-    if (S) {
-      TSG_CUDA(cudaMemcpyAsync(h_seg_col.data(), tl.seg_col, S * 4, cudaMemcpyDeviceToHost, s));
-      TSG_CUDA(cudaMemcpyAsync(h_mask.data(), ot.cmask, S * 32, cudaMemcpyDeviceToHost, s));
-    }
-    TSG_CUDA(cudaMemcpyAsync(h_off.data(), ot.elem_off, (S + 1) * 4, cudaMemcpyDeviceToHost, s));
-    if (counted)
-      TSG_CUDA(cudaMemcpyAsync(h_vals.data(), ot.vals, counted * 4, cudaMemcpyDeviceToHost, s));
-    TSG_CUDA(cudaStreamSynchronize(s));
-    std::vector<uint32_t> tr, tc;
-    std::vector<uint16_t> rm;
-    std::vector<uint64_t> ei;
-    std::vector<float> vv;
-    for (uint32_t I = 0; I + 1 < nr; ++I)
-      for (uint32_t q = h_seg_row[I]; q < h_seg_row[I + 1]; ++q) {
-        int n = 0;
-        for (int r = 0; r < 16; ++r) n += __builtin_popcount(h_mask[size_t(q) * 16 + r]);
-        if (n == 0) continue;  // compact(): empty tiles dropped
-        tr.push_back(I);
-        tc.push_back(h_seg_col[q]);
-        ei.push_back(vv.size());
-        for (int r = 0; r < 16; ++r) rm.push_back(h_mask[size_t(q) * 16 + r]);
-        vv.insert(vv.end(), h_vals.begin() + h_off[q], h_vals.begin() + h_off[q] + n);
-      }
-    tiles->ntiles = int64_t(tr.size());
-    tiles->nnz = int64_t(vv.size());
-    auto dup = [](const void* src, size_t bytes) {
-      void* p = std::malloc(bytes ? bytes : 1);
-      if (bytes) std::memcpy(p, src, bytes);
-      return p;
-    };
-    tiles->tile_row = static_cast<uint32_t*>(dup(tr.data(), tr.size() * 4));
-    tiles->tile_col = static_cast<uint32_t*>(dup(tc.data(), tc.size() * 4));
-    tiles->row_masks = static_cast<uint16_t*>(dup(rm.data(), rm.size() * 2));
-    tiles->elem_index = static_cast<uint64_t*>(dup(ei.data(), ei.size() * 8));
-    tiles->val = static_cast<float*>(dup(vv.data(), vv.size() * 4));
-  }
-
   TSG_CUDA(cudaStreamSynchronize(s));
+  if (tiles) {  // test path: 16x16 tiled view of the realised C
+    std::vector<int64_t> h_rp(rows + 1);
+    std::vector<int32_t> h_col(nnzC);
+    std::vector<float> h_val(nnzC);
+    TSG_CUDA(cudaMemcpy(h_rp.data(), d_rp, (rows + 1) * 8, cudaMemcpyDeviceToHost));
+    if (nnzC) {
+      TSG_CUDA(cudaMemcpy(h_col.data(), d_col, nnzC * 4, cudaMemcpyDeviceToHost));
+      TSG_CUDA(cudaMemcpy(h_val.data(), d_val, nnzC * 4, cudaMemcpyDeviceToHost));
+    }
+    tiles_from_csr(rows, h_rp, h_col, h_val, tiles);
+  }
   if (timing) {
     float ms[7] = {0};
     for (int i = 1; i <= 6; ++i) TSG_CUDA(cudaEventElapsedTime(&ms[i], ctx->ev[i - 1], ctx->ev[i]));
@@ -483,8 +596,6 @@ void spgemm_impl(tsg_ctx* ctx, const tsg_csr* Ain, const tsg_csr* Bin, tsg_csr_o
     st->nnz_c = uint64_t(nnzC);
     st->kernel_launches += ctx->launches - launches0;
   }
-  (void)nvA;
-  (void)nvB;
 }
 
 void free_out(tsg_ctx* ctx, tsg_csr_out* C) {

@@ -6,24 +6,26 @@
 // exactly like TiledMatrix.tiles (tile_format.hpp:43-55):
 //
 //   trp   u32[tile_rows+1]  first tile of each tile row
-//   tcol  u32[T]            tile column
-//   rmask u16[T*16]         row r bit c  <=> slot (r,c) nonzero  (the 256-bit
-//                           occupancy mask; reference bit 8r+c, tile_format.hpp:20-23)
-//   occ   u32[T]            lo16 = column occupancy (OR of rows), hi16 = row
-//                           occupancy: the O(1) zero-product filter inputs
-//                           (tile_product_nonzero, pipeline.cpp:23-35)
-//   voff  u32[T]            first value of the tile
-//   fhdr  u16[T*32]         per mma lane: (slot byte | prefix << 8), see below
-//   vals  f16[nnz]          values, packed per tile in *fragment order*
+//   tco   uint2[T]          {tile column, occupancy}; occupancy lo16 = column
+//                           occupancy (OR of rows), hi16 = row occupancy: the
+//                           O(1) zero-product filter (pipeline.cpp:23-35)
+//   rm2   u32[T*8]          row masks, interleaved: word g = row g | row g+8 << 16
+//                           (bit c of row r <=> slot (r,c) nonzero; the 256-bit
+//                           occupancy mask, reference bit 8r+c, tile_format.hpp:20-23)
+//   cm2   u32[T*8]          column masks, same interleave (bit r of column c)
+//   meta  uint2[T]  (per operand role)  {lane mask, first chunk}
+//   chunk uint4[]   (per operand role)  16-byte lane chunks, chunk 0 = zeros
 //
-// Fragment order (our layout, not the reference's ascending-bit order): the
-// 256 slots of a tile are numbered by (mma lane L, slot j) where lane L of an
-// m16n8k16 warp holds slot j of its operand registers.  A tile that will be
-// the A operand is packed in "A order", a B operand in "B order" (A order of
-// the transpose).  Lane L's nonzeros are then one contiguous run starting
-// at prefix(L); fhdr[L] says which of its 8 slots are present.  Building an
-// operand fragment is one coalesced 64-byte header load plus popc(byte)
-// (usually 0-2) two-byte loads per lane -- no per-element index search.
+// Lane-dense operand chunks (our layout, not the reference's ascending-bit
+// order): mma.m16n8k16 lane L holds 8 fp16 slots of a 16x16 operand in four
+// .f16x2 registers.  A tile stores, for every lane with at least one nonzero
+// slot, those 16 bytes verbatim ("chunk"); lane mask bit L says the chunk
+// exists, and it lives at meta.y + popc(lane mask below L).  Loading an
+// operand fragment is therefore one LDG.128 per lane (absent lanes read the
+// zero chunk 0) -- no per-element index arithmetic on the hot path.  A tile
+// that will be the A operand is stored in "A order", a B operand in "B order"
+// (the A order of its transpose, chunk registers stored {reg0, reg2, reg1,
+// reg3} so each n8 MMA's {b0, b1} is one register pair); A.A stores both.
 #pragma once
 #include <cstdint>
 #include <cuda_fp16.h>
@@ -38,14 +40,13 @@ enum Role : int { kRoleA = 0, kRoleB = 1 };
 struct TileMat {
   int64_t rows = 0, cols = 0;
   uint32_t tile_rows = 0, tile_cols = 0;
-  uint64_t cap_tiles = 0, cap_vals = 0;  // allocated capacity (upper bounds)
+  uint64_t cap = 0;  // allocated tiles/chunks capacity (upper bound: nnz)
   uint32_t* trp = nullptr;
-  uint32_t* tcol = nullptr;
-  uint16_t* rmask = nullptr;
-  uint32_t* occ = nullptr;
-  uint32_t* voff = nullptr;
-  uint16_t* fhdr[2] = {nullptr, nullptr};  // per role
-  __half* vals[2] = {nullptr, nullptr};    // per role
+  uint2* tco = nullptr;
+  uint32_t* rm2 = nullptr;
+  uint32_t* cm2 = nullptr;
+  uint2* meta[2] = {nullptr, nullptr};
+  uint4* chunk[2] = {nullptr, nullptr};
 };
 
 // Slot (r, c) of a tile used as operand `role` -> (lane, j).
@@ -73,22 +74,38 @@ __host__ __device__ inline void rc_of(int role, int lane, int j, int& r, int& c)
   if (role == kRoleB) { int tmp = r; r = c; c = tmp; }
 }
 
-// Accumulator (C/D fragment, two n8 halves: acc0 = cols 0..7, acc1 = 8..15):
+// Accumulator (C/D fragment, two n8 halves: acc[0] = cols 0..7, acc[1] = 8..15):
 //   acc[h][i]: row g + 8*(i>>1), col 2t + (i&1) + 8*h.
-// That is exactly A-order slot j = 2*(i>>1 | h<<1) + (i&1), so a C tile
-// written in A order can feed the next stage of a chain directly.
 
 // Device error flags (OR-ed), mapped to tsg_status by the host.
 enum ErrBits : unsigned {
   kErrInvariant = 1u,  // unsorted / duplicate / out-of-range CSR
   kErrOverflow = 2u,   // |x| > 65504 or non-finite input
   kErrPrecision = 4u,  // non-finite accumulator
+  kCancelled = 8u,     // an output slot cancelled to exactly 0 (compaction needed)
 };
 
 __device__ __forceinline__ unsigned lanemask_lt() {
   unsigned m;
   asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
   return m;
+}
+
+__device__ __forceinline__ unsigned spread4(unsigned n) {  // bit t -> bit 2t
+  return (n & 1u) | ((n & 2u) << 1) | ((n & 4u) << 2) | ((n & 8u) << 3);
+}
+
+// 16 row masks of an m16n16 accumulator held as acc[h][i] (see above):
+// from the 8 ballots B[h][i] (bit L = lane L's acc[h][i] nonzero), row r's
+// mask.  Returned in lane r (r < 16); other lanes get row r & 15.
+__device__ __forceinline__ unsigned row_mask_from_ballots(const unsigned (&B)[2][4], int lane) {
+  const int r = lane & 15, sh = 4 * (r & 7);
+  const bool lo = r < 8;  // selects, not a runtime index: keeps B in registers
+  const unsigned n0 = ((lo ? B[0][0] : B[0][2]) >> sh) & 0xfu;
+  const unsigned n1 = ((lo ? B[0][1] : B[0][3]) >> sh) & 0xfu;
+  const unsigned n2 = ((lo ? B[1][0] : B[1][2]) >> sh) & 0xfu;
+  const unsigned n3 = ((lo ? B[1][1] : B[1][3]) >> sh) & 0xfu;
+  return spread4(n0) | (spread4(n1) << 1) | (spread4(n2) << 8) | (spread4(n3) << 9);
 }
 
 }  // namespace tsg

@@ -14,8 +14,10 @@
 // One warp per tile row (16 CSR rows, lane r<16 owns row r).  Each step the
 // warp takes the minimum pending tile column (REDUX), every row lane
 // consumes its entries in that tile, and the tile is emitted.  Two passes
-// (count, fill) with a prefix sum between them; the fill pass writes one or
-// both operand layouts (A order and/or B order, see tsg_common.cuh).
+// (count, fill) with a prefix sum between them; the fill pass stages each
+// tile densely in shared memory and cuts the lane-dense operand chunks of
+// one or both roles (A order and/or B order, see tsg_common.cuh), plus the
+// interleaved row / column masks the symbolic and counting passes use.
 #include "tsg_kernels.cuh"
 
 namespace tsg {
@@ -29,14 +31,16 @@ __device__ __forceinline__ unsigned short f64_to_half_bits(double x) {
   return h;
 }
 
-// Loads value p as binary16 bits.  Sets *bad on overflow / non-finite and
-// *skip when the entry is dropped (zero, underflow, or dropped non-finite).
-__device__ __forceinline__ unsigned short load_half(const void* val, int dtype, int64_t p,
+// Loads value p as binary16 bits (kDtype: 0 f16 bits, 1 f32, 2 f64).  Sets
+// kErrOverflow on |x| > 65504 or non-finite input (unless dropped); `keep`
+// is false when the entry is dropped (zero, underflow, dropped non-finite).
+template <int kDtype>
+__device__ __forceinline__ unsigned short load_half(const void* val, int64_t p,
                                                     bool drop_nonfinite, unsigned& err,
                                                     bool& keep) {
   unsigned short h = 0;
   keep = false;
-  if (dtype == 1) {  // f32
+  if (kDtype == 1) {
     const float x = __ldg(static_cast<const float*>(val) + p);
     if (!isfinite(x)) {
       if (!drop_nonfinite) err |= kErrOverflow;
@@ -47,7 +51,7 @@ __device__ __forceinline__ unsigned short load_half(const void* val, int dtype, 
       return 0;
     }
     h = __half_as_ushort(__float2half_rn(x));
-  } else if (dtype == 2) {  // f64
+  } else if (kDtype == 2) {
     const double x = __ldg(static_cast<const double*>(val) + p);
     if (!isfinite(x)) {
       if (!drop_nonfinite) err |= kErrOverflow;
@@ -58,7 +62,7 @@ __device__ __forceinline__ unsigned short load_half(const void* val, int dtype, 
       return 0;
     }
     h = f64_to_half_bits(x);
-  } else {  // binary16 bits
+  } else {
     h = __ldg(static_cast<const unsigned short*>(val) + p);
     if ((h & 0x7c00u) == 0x7c00u) {  // inf / nan
       if (!drop_nonfinite) err |= kErrOverflow;
@@ -69,7 +73,21 @@ __device__ __forceinline__ unsigned short load_half(const void* val, int dtype, 
   return h;
 }
 
-template <bool kFill>
+// 16x16 bit-matrix transpose across lanes 0-15 (lane r holds row r as a
+// u16): four shuffle-xor butterfly stages.  Returns column `lane & 15`.
+__device__ __forceinline__ uint32_t transpose16(uint32_t x, int lane) {
+  const uint32_t masks[4] = {0x00ffu, 0x0f0fu, 0x3333u, 0x5555u};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int k = 8 >> i;
+    const uint32_t m = masks[i];
+    const uint32_t y = __shfl_xor_sync(kFull, x, k);
+    x = (lane & k) ? ((x & (m << k)) | ((y >> k) & m)) : ((x & m) | ((y & m) << k));
+  }
+  return x & 0xffffu;
+}
+
+template <bool kFill, int kDtype>
 __global__ void __launch_bounds__(256) convert_kernel(CsrView in, TileMat out, int roles,
                                                      const uint32_t* __restrict__ tile_base,
                                                      const uint32_t* __restrict__ val_base,
@@ -77,11 +95,14 @@ __global__ void __launch_bounds__(256) convert_kernel(CsrView in, TileMat out, i
                                                      uint32_t* __restrict__ row_nvals,
                                                      unsigned* __restrict__ err_flag,
                                                      int drop_nonfinite) {
-  __shared__ uint16_t s_hdr[8][32];
+  // per warp: the tile staged densely (row-major) and transposed, as fp16 bits
+  __shared__ __align__(16) uint16_t s_tile[8][2][256];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
   const uint32_t I = blockIdx.x * 8 + wib;
   if (I >= out.tile_rows) return;
+  uint16_t* st = s_tile[wib][0];
+  uint16_t* stT = s_tile[wib][1];
 
   const int64_t row = int64_t(I) * kTile + lane;
   const bool has_row = lane < kTile && row < in.rows;
@@ -92,16 +113,22 @@ __global__ void __launch_bounds__(256) convert_kernel(CsrView in, TileMat out, i
   if (!kFill && has_row && end < p) err |= kErrInvariant;
 
   uint32_t ntiles = 0, nvals = 0;
-  uint32_t tbase = 0, vbase = 0;
+  uint32_t tbase = 0;
+  uint32_t cbase[2] = {0, 0};
   if (kFill) {
     tbase = tile_base[I];
-    vbase = val_base[I];
+    // chunk capacity of a tile row = its kept nnz (every present lane holds >= 1)
+    cbase[0] = cbase[1] = 1u + val_base[I];
   }
   while (true) {
     const uint32_t my_tc = (p < end) ? uint32_t(__ldg(in.col + p)) >> 4 : 0xffffffffu;
     const uint32_t J = __reduce_min_sync(kFull, my_tc);
     if (J == 0xffffffffu) break;
-    const int64_t p0 = p;
+    if (kFill) {
+      reinterpret_cast<uint4*>(st)[lane] = make_uint4(0, 0, 0, 0);
+      reinterpret_cast<uint4*>(stT)[lane] = make_uint4(0, 0, 0, 0);
+      __syncwarp();
+    }
     uint32_t rm = 0;
     while (p < end) {
       const int32_t c = __ldg(in.col + p);
@@ -111,8 +138,14 @@ __global__ void __launch_bounds__(256) convert_kernel(CsrView in, TileMat out, i
         prev_col = c;
       }
       bool keep;
-      load_half(in.val, in.dtype, p, drop_nonfinite, err, keep);
-      if (keep) rm |= 1u << (c & 15);
+      const unsigned short h = load_half<kDtype>(in.val, p, drop_nonfinite, err, keep);
+      if (keep) {
+        rm |= 1u << (c & 15);
+        if (kFill) {
+          st[lane * 16 + (c & 15)] = h;
+          stT[(c & 15) * 16 + lane] = h;
+        }
+      }
       ++p;
     }
     // Termination holds for any input: the lane holding the minimum tile
@@ -122,55 +155,40 @@ __global__ void __launch_bounds__(256) convert_kernel(CsrView in, TileMat out, i
     if (any == 0) continue;  // every value of this tile dropped
     const uint32_t tile_nnz = __reduce_add_sync(kFull, __popc(rm));
     if (kFill) {
+      __syncwarp();
       const uint32_t t = tbase + ntiles;
-      const uint32_t v0 = vbase + nvals;
-      if (lane < kTile) out.rmask[size_t(t) * kTile + lane] = uint16_t(rm);
       const uint32_t colocc = __reduce_or_sync(kFull, rm) & 0xffffu;
-      if (lane == 0) {
-        out.tcol[t] = J;
-        out.occ[t] = colocc | ((any & 0xffffu) << 16);
-        out.voff[t] = v0;
-      }
+      if (lane == 0) out.tco[t] = make_uint2(J, colocc | ((any & 0xffffu) << 16));
+      // interleaved row masks: word g = row g | row g+8 << 16
+      const uint32_t rm_hi = __shfl_sync(kFull, rm, (lane & 7) + 8);
+      if (lane < 8) out.rm2[size_t(t) * 8 + lane] = rm | (rm_hi << 16);
+      // column masks (bit r of column c): transpose of the row masks
+      const uint32_t cm = transpose16(rm, lane);
+      const uint32_t cm_hi = __shfl_sync(kFull, cm, (lane & 7) + 8);
+      if (lane < 8) out.cm2[size_t(t) * 8 + lane] = cm | (cm_hi << 16);
+      // cut the lane chunks: A order reads row pairs (r, 2t..2t+1) of the
+      // staged tile, B order the same pairs of the transposed tile
+#pragma unroll
       for (int role = 0; role < 2; ++role) {
         if (!(roles & (1 << role))) continue;
-        // slot byte of this lane in `role` order: gather from the row lanes
-        unsigned byte = 0;
+        const uint16_t* src = role == kRoleA ? st : stT;
+        const int g = lane >> 2, tq = lane & 3;
+        uint32_t reg[4];
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          int r, c;
-          rc_of(role, lane, j, r, c);
-          const unsigned rowm = __shfl_sync(kFull, rm, r);
-          byte |= ((rowm >> c) & 1u) << j;
-        }
-        const unsigned cnt = __popc(byte);
-        unsigned incl = cnt;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const unsigned v = __shfl_up_sync(kFull, incl, o);
-          if (lane >= o) incl += v;
-        }
-        const unsigned pre = incl - cnt;
-        const uint16_t hdr = uint16_t(byte | (pre << 8));
-        out.fhdr[role][size_t(t) * 32 + lane] = hdr;
-        s_hdr[wib][lane] = hdr;
-        __syncwarp();
-        // scatter this row's kept values into fragment order
-        if (has_row) {
-          for (int64_t q = p0; q < p; ++q) {
-            bool keep;
-            unsigned e2 = 0;
-            const unsigned short h = load_half(in.val, in.dtype, q, drop_nonfinite, e2, keep);
-            if (!keep) continue;
-            const int c = __ldg(in.col + q) & 15;
-            int L, j;
-            slot_of(role, lane, c, L, j);
-            const unsigned hb = s_hdr[wib][L];
-            const unsigned pos = (hb >> 8) + __popc((hb & 0xffu) & ((1u << j) - 1u));
-            reinterpret_cast<unsigned short*>(out.vals[role])[v0 + pos] = h;
-          }
-        }
-        __syncwarp();
+        for (int i = 0; i < 4; ++i)  // reg i = rows g + 8(i&1), cols 2t + 8(i>>1) .. +1
+          reg[i] = *reinterpret_cast<const uint32_t*>(src + (g + 8 * (i & 1)) * 16 + 2 * tq + 8 * (i >> 1));
+        const bool present = (reg[0] | reg[1] | reg[2] | reg[3]) != 0u;
+        const unsigned lm = __ballot_sync(kFull, present);
+        // B chunks are stored {reg0, reg2, reg1, reg3}: the {b0, b1} operand
+        // pair of each n8 MMA is then one aligned register pair
+        if (present)
+          out.chunk[role][cbase[role] + __popc(lm & lanemask_lt())] =
+              role == kRoleA ? make_uint4(reg[0], reg[1], reg[2], reg[3])
+                             : make_uint4(reg[0], reg[2], reg[1], reg[3]);
+        if (lane == 0) out.meta[role][t] = make_uint2(lm, cbase[role]);
+        cbase[role] += __popc(lm);
       }
+      __syncwarp();
     }
     ++ntiles;
     nvals += tile_nnz;
@@ -183,6 +201,16 @@ __global__ void __launch_bounds__(256) convert_kernel(CsrView in, TileMat out, i
       if (e) atomicOr(err_flag, e);
     }
   }
+}
+
+__global__ void row_stats_kernel(const uint32_t* __restrict__ trp, uint32_t tile_rows,
+                                 unsigned* __restrict__ max_row_tiles) {
+  unsigned m = 0;
+  for (uint32_t I = blockIdx.x * blockDim.x + threadIdx.x; I < tile_rows;
+       I += gridDim.x * blockDim.x)
+    m = max(m, trp[I + 1] - trp[I]);
+  m = __reduce_max_sync(kFull, m);
+  if ((threadIdx.x & 31) == 0 && m) atomicMax(max_row_tiles, m);
 }
 
 // Column counts of A (histogram) for C-bar.
@@ -212,16 +240,27 @@ void launch_convert_count(const CsrView& in, TileMat& out, uint32_t* row_ntiles,
                           cudaStream_t st) {
   const unsigned blocks = (out.tile_rows + 7) / 8;
   if (blocks == 0) return;
-  convert_kernel<false><<<blocks, 256, 0, st>>>(in, out, 0, nullptr, nullptr, row_ntiles,
-                                                 row_nvals, err_flag, drop_nonfinite);
+  auto k = in.dtype == 0 ? convert_kernel<false, 0> : in.dtype == 2 ? convert_kernel<false, 2>
+                                                                    : convert_kernel<false, 1>;
+  k<<<blocks, 256, 0, st>>>(in, out, 0, nullptr, nullptr, row_ntiles, row_nvals, err_flag,
+                            drop_nonfinite);
 }
 
 void launch_convert_fill(const CsrView& in, TileMat& out, int roles, const uint32_t* tile_base,
                          const uint32_t* val_base, int drop_nonfinite, cudaStream_t st) {
   const unsigned blocks = (out.tile_rows + 7) / 8;
   if (blocks == 0) return;
-  convert_kernel<true><<<blocks, 256, 0, st>>>(in, out, roles, tile_base, val_base, nullptr,
-                                                nullptr, nullptr, drop_nonfinite);
+  auto k = in.dtype == 0 ? convert_kernel<true, 0> : in.dtype == 2 ? convert_kernel<true, 2>
+                                                                   : convert_kernel<true, 1>;
+  k<<<blocks, 256, 0, st>>>(in, out, roles, tile_base, val_base, nullptr, nullptr, nullptr,
+                            drop_nonfinite);
+}
+
+void launch_row_stats(const TileMat& A, unsigned* max_row_tiles, cudaStream_t st) {
+  if (A.tile_rows == 0) return;
+  unsigned blocks = (A.tile_rows + 255) / 256;
+  if (blocks > 592) blocks = 592;
+  row_stats_kernel<<<blocks, 256, 0, st>>>(A.trp, A.tile_rows, max_row_tiles);
 }
 
 void launch_cbar(const int32_t* colA, int64_t nnzA, int64_t inner, const int64_t* rpB,

@@ -11,6 +11,6 @@ timeout 600 python bench.py --steps 10 --warmup 3 > gpurun_out/bench.log 2>&1; e
 if [ -n "$NCU" ]; then
   timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_${TAG}.csv \
       python bench.py --steps 2 --warmup 1 --no-cpu-baseline > gpurun_out/ncu_launch.log 2>&1
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:${KREGEX} -s 2 -c 1 \
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:"${KREGEX}" -s ${NSKIP:-2} -c ${NCAP:-1} \
       -o gpurun_out/prof_${TAG} -f python bench.py --steps 1 --warmup 1 --no-cpu-baseline > gpurun_out/ncu_full.log 2>&1
 fi
