@@ -37,6 +37,14 @@ extern "C" {
 
 #define TSG_ABI_VERSION 1
 
+/* Only the functions below are exported (the library builds with
+ * -fvisibility=hidden). */
+#if defined(__GNUC__)
+#define TSG_API __attribute__((visibility("default")))
+#else
+#define TSG_API
+#endif
+
 /* Status codes mirror the reference CLI exit codes
  * (proj/tools/tilemul.cpp:30-35,285-306; proj/include/tilemul/errors.hpp:9-51). */
 typedef enum {
@@ -126,38 +134,38 @@ typedef struct {
 
 typedef struct tsg_ctx tsg_ctx;
 
-void tsg_default_options(tsg_options* opt);
+TSG_API void tsg_default_options(tsg_options* opt);
 
 /* device < 0: current device.  stream: cudaStream_t or NULL (own stream). */
-int tsg_create(tsg_ctx** ctx, int device, void* stream);
-int tsg_destroy(tsg_ctx* ctx);
-const char* tsg_last_error(const tsg_ctx* ctx);
-int tsg_abi_version(void);
+TSG_API int tsg_create(tsg_ctx** ctx, int device, void* stream);
+TSG_API int tsg_destroy(tsg_ctx* ctx);
+TSG_API const char* tsg_last_error(const tsg_ctx* ctx);
+TSG_API int tsg_abi_version(void);
 
 /* C = A . B.  tiles may be NULL. */
-int tsg_spgemm(tsg_ctx* ctx, const tsg_csr* A, const tsg_csr* B, tsg_csr_out* C,
+TSG_API int tsg_spgemm(tsg_ctx* ctx, const tsg_csr* A, const tsg_csr* B, tsg_csr_out* C,
                const tsg_options* opt, tsg_run_stats* stats, tsg_tiles_out* tiles);
 
 /* C = X0 . X1 . ... . X{n-1}, left to right; each intermediate is rounded
  * to binary16 (drop exact zeros / underflow, OverflowError beyond 65504)
  * before the next stage, as spgemm_square does for fp32-stored input
  * (proj/src/kernels.cpp:239-258).  stats accumulates over stages. */
-int tsg_spgemm_chain(tsg_ctx* ctx, int n, const tsg_csr* const* X, tsg_csr_out* C,
+TSG_API int tsg_spgemm_chain(tsg_ctx* ctx, int n, const tsg_csr* const* X, tsg_csr_out* C,
                      const tsg_options* opt, tsg_run_stats* stats);
 
-void tsg_free_csr(tsg_ctx* ctx, tsg_csr_out* C);
-void tsg_free_tiles(tsg_tiles_out* t);
+TSG_API void tsg_free_csr(tsg_ctx* ctx, tsg_csr_out* C);
+TSG_API void tsg_free_tiles(tsg_tiles_out* t);
 
 /* sum_k nnzA(:,k) * nnzB(k,:) on the device (analytics.cpp:51-65,
  * generalised to A != B): the GFLOPS denominator / 2. */
-int tsg_cbar(tsg_ctx* ctx, const tsg_csr* A, const tsg_csr* B, uint64_t* cbar);
+TSG_API int tsg_cbar(tsg_ctx* ctx, const tsg_csr* A, const tsg_csr* B, uint64_t* cbar);
 
 /* Total own-kernel launches by this context since creation. */
-uint64_t tsg_launch_count(const tsg_ctx* ctx);
+TSG_API uint64_t tsg_launch_count(const tsg_ctx* ctx);
 
 /* Device time (ms) of each launch of the numeric kernel during the last
  * call with phase_timing set (averaged over launches), for the roofline. */
-double tsg_last_kernel_ms(const tsg_ctx* ctx, const char* phase);
+TSG_API double tsg_last_kernel_ms(const tsg_ctx* ctx, const char* phase);
 
 #ifdef __cplusplus
 }

@@ -20,6 +20,7 @@ SOURCES = ["tsg_convert.cu", "tsg_symbolic.cu", "tsg_numeric.cu", "tsg_output.cu
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-O2",
+         "-Xcompiler", "-fvisibility=hidden",
          "--expt-relaxed-constexpr", "-I", str(ROOT / "include"), "-I", str(CSRC)]
 
 

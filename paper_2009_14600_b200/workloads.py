@@ -199,6 +199,21 @@ CONFIGS = {
 }
 
 
+def make_small(name: str):
+    """Test-size members of each config family (same generators)."""
+    if name == "poisson":
+        return [poisson2d(48)]
+    if name == "fem27":
+        return [fem27(12)]
+    if name == "rmat":
+        return [rmat(scale=11, edge_factor=8)]
+    if name == "rect":
+        return list(rect(m=4000, k=2000, nnz=16000))
+    if name == "amg":
+        return list(amg(16))
+    raise KeyError(name)
+
+
 def make(name: str):
     """Operand list for a config: [A] for squares, [A, B], or [R, A, P]."""
     if name == "poisson":

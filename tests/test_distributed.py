@@ -1,0 +1,78 @@
+"""CPU, world_size 2 over gloo: the multi-GPU host logic (panel partition,
+B broadcast, global offsets, assembly) reproduces the single-process
+product byte for byte.  The per-rank compute here is the C restatement
+(test stand-in for the GPU call each rank makes on the B200 box)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+from oracle import port
+from paper_2009_14600_b200 import distributed as D
+from paper_2009_14600_b200 import workloads as W
+
+pytestmark = pytest.mark.skipif(not port.available(), reason="C restatement not built")
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port_no, name, q):
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port_no))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        mats = W.make_small(name)
+        A, B = mats[0], mats[1] if len(mats) > 1 else mats[0]
+        Bb = D.broadcast_csr(B if rank == 0 else None, 0, "cpu", dist)  # torch CPU tensors
+        Bh = type(B)(Bb.rows, Bb.cols, Bb.row_ptr.numpy(), Bb.col.numpy(), Bb.val.numpy())
+        bounds = D.panel_bounds(A, Bh, world)
+        r0, r1 = bounds[rank]
+        Cp = port.spgemm_mixed(D.take_rows(A, r0, r1), Bh)
+        off, total = D.global_offsets(Cp.nnz, "cpu", dist)
+        q.put((rank, bounds, off, total, Cp.row_ptr, Cp.col, Cp.val))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("name", ["fem27", "rect", "rmat"])
+def test_two_rank_panels_reassemble_exactly(name):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port_no = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port_no, name, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in range(2))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    mats = W.make_small(name)
+    A, B = mats[0], mats[1] if len(mats) > 1 else mats[0]
+    full = port.spgemm_mixed(A, B)
+    bounds = res[0][1]
+    assert bounds == res[1][1] and bounds[0][0] == 0 and bounds[-1][1] == A.rows
+    assert all(b[0] % 16 == 0 for b in bounds)
+    assert res[0][2] == 0 and res[1][2] == len(res[0][5]) and res[0][3] == full.nnz
+    from paper_2009_14600_b200.tilemul import Csr
+    panels = [Csr(bounds[r][1] - bounds[r][0], B.cols, res[r][4], res[r][5], res[r][6]) for r in range(2)]
+    C = D.assemble(panels, B.cols)
+    assert np.array_equal(C.row_ptr, full.row_ptr) and np.array_equal(C.col, full.col)
+    assert np.array_equal(C.val.view(np.uint32), full.val.view(np.uint32))
+
+
+def test_panel_bounds_balance_skewed_rows():
+    A = W.make_small("rmat")[0]
+    b = D.panel_bounds(A, A, 4)
+    work = D.row_work(A, A)
+    per = [int(work[r0:r1].sum()) for r0, r1 in b]
+    assert b[0][0] == 0 and b[-1][1] == A.rows
+    assert max(per) <= 1.5 * (sum(per) / 4) + int(work.max()) * 16
