@@ -29,6 +29,8 @@ import sys
 import threading
 import time
 
+from pathlib import Path
+
 import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
@@ -61,27 +63,47 @@ def parse():
 # ----------------------------------------------------------------------------
 # clocks sampler (nvidia-smi during the timed region)
 class Clocks:
-    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
-         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-         "clocks_event_reasons.sw_power_cap")
+    """SM clock and clock-event reasons sampled every ~2 ms during the timed
+    region through NVML (nvidia-smi's ~100 ms per query is too coarse for a
+    region of a few tens of ms); falls back to nvidia-smi."""
+
+    REASONS = {  # NVML clocks-event-reason bits
+        "hw_slowdown": 0x0000000000000008, "sw_thermal_slowdown": 0x0000000000000020,
+        "hw_thermal_slowdown": 0x0000000000000040, "sw_power_cap": 0x0000000000000004,
+    }
 
     def __init__(self, index: int):
         self.index = index
         self.samples = []
         self._stop = threading.Event()
         self._t = None
+        self._nvml = None
 
     def _run(self):
-        while not self._stop.is_set():
-            try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
-                                     timeout=5).stdout.strip()
-                if out:
-                    self.samples.append([x.strip() for x in out.split(",")])
-            except Exception:
-                pass
-            self._stop.wait(0.1)
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+            while not self._stop.is_set():
+                sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                rs = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                self.samples.append((sm, mx, rs))
+                self._stop.wait(0.002)
+            self._nvml = True
+        except Exception:
+            self._nvml = False
+            while not self._stop.is_set():
+                try:
+                    out = subprocess.run(["nvidia-smi", "-i", str(self.index),
+                                          "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active",
+                                          "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                         timeout=5).stdout.strip()
+                    sm, mx, rs = [x.strip() for x in out.split(",")]
+                    self.samples.append((float(sm), float(mx), int(rs, 16)))
+                except Exception:
+                    pass
+                self._stop.wait(0.05)
 
     def __enter__(self):
         self._t = threading.Thread(target=self._run, daemon=True)
@@ -95,13 +117,10 @@ class Clocks:
     def summary(self) -> dict:
         if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no-samples"]}
-        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for s in self.samples for i in range(4)
-                          if len(s) > 3 + i and s[3 + i].lower().startswith("active")})
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.samples)}
+        sm = [x[0] for x in self.samples]
+        reasons = sorted({n for x in self.samples for n, b in self.REASONS.items() if x[2] & b})
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(x[1] for x in self.samples),
+                "reasons": reasons, "samples": len(self.samples), "source": "nvml" if self._nvml else "nvidia-smi"}
 
 
 # ----------------------------------------------------------------------------
@@ -123,7 +142,9 @@ def algorithmic_bytes(st, nnzA, nnzB, rowsA, rowsC, same):
         "task_list": 40 * (tA + tB) + 8 * P,      # enumerate + filter (tile metadata in, pairs out)
         "sort": 16 * P + 8 * S,                    # read + write pairs, segment table
         "counting": 8 * P + 32 * (tA + tB) + 4 * S,
-        "multiply": 8 * P + 44 * (tA + tB) + 2 * (nnzA + nnzB) + 44 * S + 4 * cnt,
+        # SURVEY numeric bytes, plus the 4-byte column index per output: this
+        # kernel stores the final CSR directly (the survey books that in "output")
+        "multiply": 8 * P + 44 * (tA + tB) + 2 * (nnzA + nnzB) + 44 * S + 8 * cnt,
         "compaction": 44 * S + 4 * cnt + 8 * (rowsC + 1) + 8 * nnzC,
     }
 
@@ -155,14 +176,11 @@ def run_ours(args):
         Afull, Bs = mats[0], [mats[0]]
     same = len(mats) == 1 and world == 1
 
-    # rank panel of A: tile-row aligned contiguous rows
-    tile_rows = (Afull.rows + 15) // 16
-    t0 = (tile_rows * rank) // world
-    t1 = (tile_rows * (rank + 1)) // world
-    r0, r1 = min(16 * t0, Afull.rows), min(16 * t1, Afull.rows)
-    lo, hi = Afull.row_ptr[r0], Afull.row_ptr[r1]
-    Apanel = Csr(r1 - r0, Afull.cols, (Afull.row_ptr[r0:r1 + 1] - lo).astype(np.int64),
-                 Afull.col[lo:hi], Afull.val[lo:hi])
+    # rank panel of A: tile-row aligned row ranges balanced by work
+    # (paper_2009_14600_b200/distributed.py)
+    from paper_2009_14600_b200 import distributed as D
+    r0, r1 = D.panel_bounds(Afull, Bs[0], world)[rank]
+    Apanel = D.take_rows(Afull, r0, r1)
 
     # flops of this rank: 2 * C-bar over the chain stages (computed, never hard-coded)
     cb = W.cbar(Apanel, Bs[0])
@@ -249,17 +267,28 @@ def run_ours(args):
         ctx.free(one_step(st))
         for ph in ("convert", "task_list", "sort", "counting", "multiply", "compaction", "total"):
             phase_ms.setdefault(ph, []).append(ctx.last_phase_ms(ph) if not chain else getattr(st, ph) * 1e3)
+        phase_ms.setdefault("numeric_kernel", []).append(ctx.last_phase_ms("numeric_kernel"))
+        phase_ms.setdefault("counting_kernel", []).append(ctx.last_phase_ms("counting_kernel"))
     opts.phase_timing = 0
     phase_ms = {k: float(np.median(v)) for k, v in phase_ms.items()}
     sd = st.as_dict()
     nnzB = Bs[0].nnz
     bytes_ = algorithmic_bytes(sd, Apanel.nnz, nnzB, Apanel.rows, Apanel.rows, same)
-    from pathlib import Path
     peaks = json.loads((Path(ROOT) / "MEASURED_PEAKS.json").read_text()) if (Path(ROOT) / "MEASURED_PEAKS.json").exists() else {}
     peak = float(peaks.get("hbm_gbs", 6650.0))
     peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
-    dom = max((k for k in bytes_), key=lambda k: phase_ms.get(k, 0.0))
-    achieved = bytes_[dom] / (phase_ms[dom] * 1e-3) / 1e9 if phase_ms.get(dom) else 0.0
+    # dominant kernel: the SEaC numeric kernel (largest single launch); its
+    # algorithmic bytes over its own CUDA-event duration
+    dom = "multiply"
+    kms = phase_ms.get("numeric_kernel") or phase_ms.get(dom)
+    achieved = bytes_[dom] / (kms * 1e-3) / 1e9 if kms else 0.0
+    traffic = None
+    prof = Path(ROOT) / "profiles" / "r01_ncu_full_fem27.json"
+    if args.config == "fem27" and world == 1 and prof.exists():
+        kk = json.loads(prof.read_text())["kernels"]
+        for name, k in kk.items():
+            if name.startswith("numeric_tc_kernel"):
+                traffic = int(k["dram_read_bytes"] + k["dram_write_bytes"])
 
     # ---- e2e: host CSR in (pinned), host CSR out, through the public API
     pin = []
@@ -320,9 +349,11 @@ def run_ours(args):
         "gpu_launches": int(launches),
         "gpu_launches_per_step": launches / max(1, args.steps),
         "phase_ms": {k: round(v, 4) for k, v in phase_ms.items()},
-        "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": peak,
-                     "peak_source": peak_src, "unit": "GB/s", "frac": round(achieved / peak, 4),
-                     "algorithmic_bytes": int(bytes_[dom]), "traffic": None},
+        "roofline": {"bound": "hbm", "kernel": "numeric_tc_kernel (SEaC multiply)", "achieved": round(achieved, 1),
+                     "peak": peak, "peak_source": peak_src, "unit": "GB/s", "frac": round(achieved / peak, 4),
+                     "kernel_ms": round(kms, 4) if kms else None, "algorithmic_bytes": int(bytes_[dom]),
+                     "traffic": traffic, "traffic_source": "profiles/r01_ncu_full_fem27.json (ncu --set full)"
+                     if traffic else None},
         "clocks": clk.summary(),
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

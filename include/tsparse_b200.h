@@ -163,8 +163,10 @@ TSG_API int tsg_cbar(tsg_ctx* ctx, const tsg_csr* A, const tsg_csr* B, uint64_t*
 /* Total own-kernel launches by this context since creation. */
 TSG_API uint64_t tsg_launch_count(const tsg_ctx* ctx);
 
-/* Device time (ms) of each launch of the numeric kernel during the last
- * call with phase_timing set (averaged over launches), for the roofline. */
+/* Device time (ms) of a phase ("convert", "task_list", "sort", "counting",
+ * "multiply", "compaction", "total") or of a single kernel launch
+ * ("numeric_kernel", "counting_kernel") during the last call made with
+ * phase_timing set -- CUDA events on the context's stream. */
 TSG_API double tsg_last_kernel_ms(const tsg_ctx* ctx, const char* phase);
 
 #ifdef __cplusplus

@@ -45,7 +45,9 @@ struct tsg_ctx {
   std::string err;
   uint64_t launches = 0;
   double last_phase_ms[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  double last_numeric_kernel_ms = 0, last_counting_kernel_ms = 0;
   cudaEvent_t ev[8] = {};
+  cudaEvent_t kev[4] = {};  // bracket the numeric and counting kernels alone
   // pinned host blocks released by tsg_free_csr, reused by later host outputs
   std::vector<std::pair<void*, size_t>> pinned_free;
 };
@@ -479,8 +481,10 @@ void spgemm_impl(tsg_ctx* ctx, const tsg_csr* Ain, const tsg_csr* Bin, tsg_csr_o
   op.pos = sc.alloc<uint32_t>(S * 16);
   op.rowcnt = sc.alloc<int64_t>(rows + 1);
   TSG_CUDA(cudaMemsetAsync(op.rowcnt + rows, 0, sizeof(int64_t), s));
+  if (timing) TSG_CUDA(cudaEventRecord(ctx->kev[2], s));
   launch_counting(TA, TB, tl, op, s);
   check_launch(ctx);
+  if (timing) TSG_CUDA(cudaEventRecord(ctx->kev[3], s));
   launch_row_counts(rows, TA.tile_rows, tl, op, s);
   check_launch(ctx);
   auto* owner = new OutOwner();
@@ -499,8 +503,10 @@ void spgemm_impl(tsg_ctx* ctx, const tsg_csr* Ain, const tsg_csr* Bin, tsg_csr_o
   // ---- (3) numeric -> final CSR at the counted positions ---------------------
   op.col = sc.alloc<int32_t>(counted, !owner->host);
   op.val = sc.alloc<float>(counted, !owner->host);
+  if (timing) TSG_CUDA(cudaEventRecord(ctx->kev[0], s));
   launch_numeric(TA, TB, tl, op, opt.mode, err_flag, s);
   check_launch(ctx);
+  if (timing) TSG_CUDA(cudaEventRecord(ctx->kev[1], s));
   const unsigned flags = readback(ctx, err_flag);
   raise_flags(flags);
   record(ctx, timing, 5);
@@ -576,6 +582,11 @@ void spgemm_impl(tsg_ctx* ctx, const tsg_csr* Ain, const tsg_csr* Bin, tsg_csr_o
     TSG_CUDA(cudaEventElapsedTime(&tot, ctx->ev[0], ctx->ev[6]));
     for (int i = 1; i <= 6; ++i) ctx->last_phase_ms[i] = ms[i];
     ctx->last_phase_ms[7] = tot;
+    float kn = 0, kc = 0;
+    TSG_CUDA(cudaEventElapsedTime(&kn, ctx->kev[0], ctx->kev[1]));
+    TSG_CUDA(cudaEventElapsedTime(&kc, ctx->kev[2], ctx->kev[3]));
+    ctx->last_numeric_kernel_ms = kn;
+    ctx->last_counting_kernel_ms = kc;
     if (st) {
       st->convert += ms[1] * 1e-3;
       st->task_list += ms[2] * 1e-3;
@@ -651,6 +662,7 @@ int tsg_create(tsg_ctx** out, int device, void* stream) {
   }
   if (e == cudaSuccess) e = cudaMallocHost(&ctx->pinned, 64);
   for (int i = 0; i < 8 && e == cudaSuccess; ++i) e = cudaEventCreate(&ctx->ev[i]);
+  for (int i = 0; i < 4 && e == cudaSuccess; ++i) e = cudaEventCreate(&ctx->kev[i]);
   if (e != cudaSuccess) {
     std::fprintf(stderr, "tsg_create: %s\n", cudaGetErrorString(e));
     delete ctx;
@@ -664,6 +676,8 @@ int tsg_destroy(tsg_ctx* ctx) {
   if (!ctx) return TSG_OK;
   cudaStreamSynchronize(ctx->stream);
   for (auto& e : ctx->ev)
+    if (e) cudaEventDestroy(e);
+  for (auto& e : ctx->kev)
     if (e) cudaEventDestroy(e);
   if (ctx->pinned) cudaFreeHost(ctx->pinned);
   for (auto& b : ctx->pinned_free) cudaFreeHost(b.first);
@@ -782,6 +796,8 @@ uint64_t tsg_launch_count(const tsg_ctx* ctx) { return ctx ? ctx->launches : 0; 
 
 double tsg_last_kernel_ms(const tsg_ctx* ctx, const char* phase) {
   if (!ctx || !phase) return 0.0;
+  if (std::strcmp(phase, "numeric_kernel") == 0) return ctx->last_numeric_kernel_ms;
+  if (std::strcmp(phase, "counting_kernel") == 0) return ctx->last_counting_kernel_ms;
   static const char* names[] = {"", "convert", "task_list", "sort", "counting", "multiply",
                                 "compaction", "total"};
   for (int i = 1; i < 8; ++i)

@@ -58,10 +58,10 @@ __device__ __forceinline__ TileDest tile_dest(uint64_t s, const TaskList& tl, co
                                               int lane) {
   const uint32_t J = tl.seg_col[s];
   const int r = lane & 15;
-  const uint32_t w = op.bm2[uint32_t(s) * 8 + (r & 7)];  // counted rows (r&7) | +8 << 16
+  const uint32_t w = op.bm2[s * 8 + (r & 7)];  // counted rows (r&7) | +8 << 16
   TileDest d;
   d.rowm = (r >> 3) ? (w >> 16) : (w & 0xffffu);
-  d.pos = op.pos[uint32_t(s) * 16 + r];  // 64 contiguous bytes per segment
+  d.pos = op.pos[s * 16 + r];  // 64 contiguous bytes per segment (64-bit index: 16S > 2^32)
   d.cbase = int32_t(J * 16);
   return d;
 }

@@ -322,8 +322,9 @@ __global__ void __launch_bounds__(256) counting_kernel(TileMat A, TileMat B, Tas
     for (int i = 0; i < 4; ++i) bal[h][i] = __ballot_sync(kFull, d[h][i] != 0);
   const unsigned rmask = row_mask_from_ballots(bal, lane);  // row lane & 15
   const unsigned hi = __shfl_sync(kFull, rmask, (lane & 7) + 8);
-  if (lane < 8) op.bm2[uint32_t(s) * 8 + lane] = rmask | (hi << 16);
-  if (lane < 16) op.cnt[uint32_t(s) * 16 + lane] = uint8_t(__popc(rmask));
+  // 64-bit: segments * 16 passes 2^32 on R-MAT (403M segments)
+  if (lane < 8) op.bm2[s * 8 + lane] = rmask | (hi << 16);
+  if (lane < 16) op.cnt[s * 16 + lane] = uint8_t(__popc(rmask));
 }
 
 // Counted entries per CSR row: warp per tile row, lanes over its segments
