@@ -35,7 +35,7 @@
 extern "C" {
 #endif
 
-#define TSG_ABI_VERSION 1
+#define TSG_ABI_VERSION 2
 
 /* Only the functions below are exported (the library builds with
  * -fvisibility=hidden). */
@@ -119,9 +119,9 @@ typedef struct {
   double convert;    /* CSR -> 16x16 tiles (both operands)          */
   double task_list;  /* enumerate + zero-product filter             */
   double sort;       /* per-tile-row sort by output tile, segments  */
-  double counting;   /* boolean OR popcount + prefix sum            */
-  double multiply;   /* SEaC numeric                                */
-  double compaction; /* fused with tiled -> CSR output              */
+  double counting;   /* fused into multiply: always ~0              */
+  double multiply;   /* counting + SEaC numeric (one fused kernel)  */
+  double compaction; /* tiled -> CSR assembly (zeros already gone) */
   double total;      /* first kernel to last, device time           */
   /* counters (T = 16 tiles) */
   uint64_t tiles_a, tiles_b, raw_pairs, filtered_pairs, segments;
@@ -130,6 +130,7 @@ typedef struct {
   uint64_t cbar;             /* sum_k nnzA(:,k) * nnzB(k,:)  (flops / 2)  */
   uint64_t kernel_launches;  /* own kernels launched by this call         */
   uint64_t h2d_bytes, d2h_bytes;
+  uint64_t staged_slots;     /* numeric staging capacity (bound on nnz)   */
 } tsg_run_stats;
 
 typedef struct tsg_ctx tsg_ctx;
@@ -165,7 +166,7 @@ TSG_API uint64_t tsg_launch_count(const tsg_ctx* ctx);
 
 /* Device time (ms) of a phase ("convert", "task_list", "sort", "counting",
  * "multiply", "compaction", "total") or of a single kernel launch
- * ("numeric_kernel", "counting_kernel") during the last call made with
+ * ("numeric_kernel", "assemble_kernel") during the last call made with
  * phase_timing set -- CUDA events on the context's stream. */
 TSG_API double tsg_last_kernel_ms(const tsg_ctx* ctx, const char* phase);
 

@@ -41,7 +41,8 @@ class tsg_options(C.Structure):
 
 STAT_TIMES = ("convert", "task_list", "sort", "counting", "multiply", "compaction", "total")
 STAT_COUNTS = ("tiles_a", "tiles_b", "raw_pairs", "filtered_pairs", "segments", "counted_elements",
-               "nnz_c", "cbar", "kernel_launches", "h2d_bytes", "d2h_bytes")
+               "nnz_c", "cbar", "kernel_launches", "h2d_bytes", "d2h_bytes",
+               "staged_slots")
 
 
 class tsg_run_stats(C.Structure):

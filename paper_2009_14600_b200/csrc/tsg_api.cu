@@ -7,9 +7,9 @@
 //   enumerate + filter (count, scan, fill)    tsg_symbolic.cu      "taskList"
 //   stable per-tile-row sort by output tile   CUB segmented sort   "sort"
 //   segment heads                             tsg_symbolic.cu      "sort"
-//   counting pass + prefix sum                tsg_symbolic.cu      "counting"
-//   SEaC numeric                              tsg_numeric.cu       "multiply"
-//   tiled -> CSR (+ fused compaction)         tsg_output.cu        "compaction"
+//   counting pass fused into the numeric      tsg_numeric.cu       "counting" (empty)
+//   SEaC numeric -> staged compressed tiles   tsg_numeric.cu       "multiply"
+//   tiled -> CSR (compaction already done)    tsg_output.cu        "compaction"
 //
 // Everything runs stream-ordered on the context's stream with scratch from
 // a stream-ordered memory pool (cudaMallocFromPoolAsync), so steady-state
@@ -45,11 +45,16 @@ struct tsg_ctx {
   std::string err;
   uint64_t launches = 0;
   double last_phase_ms[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  double last_numeric_kernel_ms = 0, last_counting_kernel_ms = 0;
+  double last_numeric_kernel_ms = 0, last_assemble_kernel_ms = 0;
   cudaEvent_t ev[8] = {};
-  cudaEvent_t kev[4] = {};  // bracket the numeric and counting kernels alone
+  cudaEvent_t kev[4] = {};  // bracket the numeric and assembly kernels alone
   // pinned host blocks released by tsg_free_csr, reused by later host outputs
   std::vector<std::pair<void*, size_t>> pinned_free;
+  // grow-only device arena for the numeric staging buffer (the one large,
+  // data-sized scratch of a call): kept across calls so steady-state calls
+  // never ask the pool for gigabytes at a new size
+  void* stage_buf = nullptr;
+  size_t stage_cap = 0;
 };
 
 namespace {
@@ -215,11 +220,7 @@ const uint32_t* convert(tsg_ctx* ctx, Scratch& sc, const CsrView& in, TileMat& T
   const uint64_t cap = uint64_t(in.nnz);
   T.cap = cap;
   T.tco = sc.alloc<uint2>(cap);
-  // one extra all-zero tile (index cap) pads the counting pass's batches
-  T.rm2 = sc.alloc<uint32_t>((cap + 1) * 8);
-  T.cm2 = sc.alloc<uint32_t>((cap + 1) * 8);
-  TSG_CUDA(cudaMemsetAsync(T.rm2 + cap * 8, 0, 32, ctx->stream));
-  TSG_CUDA(cudaMemsetAsync(T.cm2 + cap * 8, 0, 32, ctx->stream));
+  T.rm2 = sc.alloc<uint32_t>(cap * 8);
   for (int role = 0; role < 2; ++role) {
     if (!(roles & (1 << role))) continue;
     T.meta[role] = sc.alloc<uint2>(cap);
@@ -363,52 +364,58 @@ void spgemm_impl(tsg_ctx* ctx, const tsg_csr* Ain, const tsg_csr* Bin, tsg_csr_o
   }
   record(ctx, timing, 1);
 
-  // ---- (2) symbolic: task list ----------------------------------------------
+  // ---- (2) symbolic: task list + staging bounds ----------------------------------
   TaskList tl;
   const uint64_t nr = uint64_t(TA.tile_rows) + 1;
-  uint64_t P = 0, S = 0, raw = 0;
+  uint64_t P = 0, S = 0, raw = 0, stage_total = 0;
   tl.seg_row_ptr = sc.alloc<uint32_t>(nr);
   uint32_t* row_pair_off = sc.alloc<uint32_t>(nr);
   if (light) {
     auto* row_np = sc.alloc<uint32_t>(nr);
     auto* row_ns = sc.alloc<uint32_t>(nr);
+    auto* row_nb = sc.alloc<uint32_t>(nr);
     auto* row_raw = sc.alloc<uint32_t>(nr);
+    auto* row_stage_off = sc.alloc<uint32_t>(nr);
     TSG_CUDA(cudaMemsetAsync(row_np + nr - 1, 0, 4, s));
     TSG_CUDA(cudaMemsetAsync(row_ns + nr - 1, 0, 4, s));
-    launch_merge_count(TA, TB, row_np, row_ns, row_raw, s);
+    TSG_CUDA(cudaMemsetAsync(row_nb + nr - 1, 0, 4, s));
+    launch_merge_count(TA, TB, row_np, row_ns, row_nb, row_raw, s);
     check_launch(ctx);
     exclusive_sum(ctx, sc, row_np, row_pair_off, nr);
     exclusive_sum(ctx, sc, row_ns, tl.seg_row_ptr, nr);
-    auto* raw_d = sc.alloc<unsigned long long>(1);
-    TSG_CUDA(cudaMemsetAsync(raw_d, 0, sizeof(unsigned long long), s));
+    exclusive_sum(ctx, sc, row_nb, row_stage_off, nr);
+    // exact u64 totals: raw pairs, staging bound (guards the u32 offsets)
+    auto* tot_d = sc.alloc<unsigned long long>(4);
+    TSG_CUDA(cudaMemsetAsync(tot_d, 0, 4 * sizeof(unsigned long long), s));
     {
       uint64_t blocks = (nr + 255) / 256;
       if (blocks > 1184) blocks = 1184;
-      sum_u32_kernel<<<unsigned(blocks), 256, 0, s>>>(row_raw, nr - 1, raw_d);
-      check_launch(ctx);
+      sum_u32_kernel<<<unsigned(blocks), 256, 0, s>>>(row_raw, nr - 1, tot_d + 2);
+      sum_u32_kernel<<<unsigned(blocks), 256, 0, s>>>(row_nb, nr - 1, tot_d + 3);
+      check_launch(ctx, 2);
     }
-    auto* tot_d = sc.alloc<unsigned long long>(2);
-    // totals fit u32 by construction (P < 2^31 checked below via raw)
-    TSG_CUDA(cudaMemsetAsync(tot_d, 0, 2 * sizeof(unsigned long long), s));
+    // P, S fit u32 by construction (P <= raw, checked below)
     TSG_CUDA(cudaMemcpyAsync(tot_d, row_pair_off + nr - 1, 4, cudaMemcpyDeviceToDevice, s));
     TSG_CUDA(cudaMemcpyAsync(tot_d + 1, tl.seg_row_ptr + nr - 1, 4, cudaMemcpyDeviceToDevice, s));
-    const unsigned long long* src[3] = {tot_d, tot_d + 1, raw_d};
-    unsigned long long v[3];
+    const unsigned long long* src[4] = {tot_d, tot_d + 1, tot_d + 2, tot_d + 3};
+    unsigned long long v[4];
     readback_many(ctx, src, v);
     P = v[0];
     S = v[1];
     raw = v[2];
-    if (raw >= (uint64_t(1) << 32))
-      throw Fail{TSG_ERR_OTHER, "task list beyond 2^32 raw pairs needs row-panel batching"};
+    stage_total = v[3];
+    if (raw >= (uint64_t(1) << 32) || stage_total >= (uint64_t(1) << 32))
+      throw Fail{TSG_ERR_OTHER, "task list beyond 2^32 raw pairs or staged slots needs row-panel batching"};
     tl.npairs = P;
     tl.nseg = S;
-    tl.pairs = sc.alloc<uint64_t>(P + 1);
     tl.pmeta = sc.alloc<uint4>(P + 1);
     tl.seg_off = sc.alloc<uint32_t>(S + 1);
     tl.seg_col = sc.alloc<uint32_t>(S);
-    tl.seg_row = sc.alloc<uint32_t>(S);
+    tl.stage_off = sc.alloc<uint32_t>(S + 1);
     TSG_CUDA(cudaMemcpyAsync(tl.seg_off + S, row_pair_off + nr - 1, 4, cudaMemcpyDeviceToDevice, s));
-    launch_merge_fill(TA, TB, row_pair_off, tl, s);
+    TSG_CUDA(cudaMemcpyAsync(tl.stage_off + S, row_stage_off + nr - 1, 4, cudaMemcpyDeviceToDevice, s));
+    TSG_CUDA(cudaMemsetAsync(tl.pmeta + P, 0, sizeof(uint4), s));  // pad: zero metas
+    launch_merge_fill(TA, TB, row_pair_off, row_stage_off, tl, s);
     check_launch(ctx);
     record(ctx, timing, 2);
     record(ctx, timing, 3);  // the merge is the sort: no separate phase
@@ -434,16 +441,16 @@ void spgemm_impl(tsg_ctx* ctx, const tsg_csr* Ain, const tsg_csr* Bin, tsg_csr_o
     check_launch(ctx);
     record(ctx, timing, 2);
     // stable sort by output tile column within each tile row
-    tl.pairs = sc.alloc<uint64_t>(P + 1);
+    uint64_t* pairs = sc.alloc<uint64_t>(P + 1);
     uint32_t* keys = sc.alloc<uint32_t>(P);
     if (P > 0) {
       size_t bytes = 0;
       TSG_CUDA(cub::DeviceSegmentedSort::StableSortPairs(nullptr, bytes, keys_u, keys, pairs_u,
-                                                         tl.pairs, int(P), int(TA.tile_rows),
+                                                         pairs, int(P), int(TA.tile_rows),
                                                          row_pair_off, row_pair_off + 1, s));
       void* tmp = sc.alloc<char>(bytes);
       TSG_CUDA(cub::DeviceSegmentedSort::StableSortPairs(tmp, bytes, keys_u, keys, pairs_u,
-                                                         tl.pairs, int(P), int(TA.tile_rows),
+                                                         pairs, int(P), int(TA.tile_rows),
                                                          row_pair_off, row_pair_off + 1, s));
     }
     auto* row_nseg = sc.alloc<uint32_t>(nr);
@@ -455,94 +462,85 @@ void spgemm_impl(tsg_ctx* ctx, const tsg_csr* Ain, const tsg_csr* Bin, tsg_csr_o
     tl.nseg = S;
     tl.seg_off = sc.alloc<uint32_t>(S + 1);
     tl.seg_col = sc.alloc<uint32_t>(S);
-    tl.seg_row = sc.alloc<uint32_t>(S);
+    tl.stage_off = sc.alloc<uint32_t>(S + 1);
     TSG_CUDA(cudaMemcpyAsync(tl.seg_off + S, row_pair_off + nr - 1, 4, cudaMemcpyDeviceToDevice, s));
     launch_seg_fill(TA, row_pair_off, keys, tl, s);
     check_launch(ctx);
     tl.pmeta = sc.alloc<uint4>(P + 1);
-    launch_pair_meta(TA, TB, tl, s);
+    auto* pair_bound = sc.alloc<uint32_t>(P + 1);
+    launch_pair_meta(TA, TB, pairs, tl, pair_bound, s);
+    check_launch(ctx);
+    stage_total = total_u32(ctx, sc, pair_bound, P);
+    if (stage_total >= (uint64_t(1) << 32))
+      throw Fail{TSG_ERR_OTHER, "staged slots beyond 2^32 need row-panel batching"};
+    auto* pair_stage = sc.alloc<uint32_t>(P + 1);
+    exclusive_sum(ctx, sc, pair_bound, pair_stage, P + 1);
+    launch_seg_stage(tl, pair_stage, s);
     check_launch(ctx);
     record(ctx, timing, 3);
   }
+  record(ctx, timing, 4);  // the counting pass is fused into the numeric kernel
 
-  // pad entries: pairs[P] -> the all-zero mask tiles, pmeta[P] -> zero chunks
-  {
-    uint64_t* pad_host = reinterpret_cast<uint64_t*>(ctx->pinned) + 6;
-    *pad_host = uint64_t(uint32_t(TA.cap)) | (uint64_t(uint32_t(TB.cap)) << 32);
-    TSG_CUDA(cudaMemcpyAsync(tl.pairs + P, pad_host, 8, cudaMemcpyHostToDevice, s));
-    TSG_CUDA(cudaMemsetAsync(tl.pmeta + P, 0, sizeof(uint4), s));
-  }
-
-  // ---- counting pass + output positions ----------------------------------------
-  OutPlan op;
+  // ---- (3) numeric: counting + SEaC multiply -> staged tiles ---------------------
   const int64_t rows = Ain->rows;
-  op.bm2 = sc.alloc<uint32_t>(S * 8);
-  op.cnt = sc.alloc<uint8_t>(S * 16);
-  op.pos = sc.alloc<uint32_t>(S * 16);
-  op.rowcnt = sc.alloc<int64_t>(rows + 1);
-  TSG_CUDA(cudaMemsetAsync(op.rowcnt + rows, 0, sizeof(int64_t), s));
-  if (timing) TSG_CUDA(cudaEventRecord(ctx->kev[2], s));
-  launch_counting(TA, TB, tl, op, s);
+  Staged sg;
+  {
+    const size_t need = std::max<size_t>(stage_total, 1) * sizeof(float);
+    if (need > ctx->stage_cap) {
+      if (ctx->stage_buf) TSG_CUDA(cudaFreeAsync(ctx->stage_buf, s));
+      ctx->stage_buf = nullptr;
+      ctx->stage_cap = 0;
+      const size_t cap = need + need / 4;
+      TSG_CUDA(cudaMallocFromPoolAsync(&ctx->stage_buf, cap, ctx->pool, s));
+      ctx->stage_cap = cap;
+    }
+    sg.val = static_cast<float*>(ctx->stage_buf);
+  }
+  sg.rmask = sc.alloc<uint16_t>(S * 16);
+  sg.counted = sc.alloc<unsigned long long>(1);
+  TSG_CUDA(cudaMemsetAsync(sg.counted, 0, sizeof(unsigned long long), s));
+  if (timing) TSG_CUDA(cudaEventRecord(ctx->kev[0], s));
+  launch_numeric(tl, TA, TB, sg, opt.mode, err_flag, s);
   check_launch(ctx);
-  if (timing) TSG_CUDA(cudaEventRecord(ctx->kev[3], s));
-  launch_row_counts(rows, TA.tile_rows, tl, op, s);
-  check_launch(ctx);
+  if (timing) TSG_CUDA(cudaEventRecord(ctx->kev[1], s));
+  record(ctx, timing, 5);
+
+  // ---- (4) tiled -> CSR: realised row counts, scan, assembly ----------------------
   auto* owner = new OutOwner();
   owner->host = C->mem == TSG_MEM_HOST;
   C->_owner = owner;  // released by free_out on any later failure
-  op.row_ptr = owner->host ? sc.alloc<int64_t>(rows + 1) : sc.alloc<int64_t>(rows + 1, true);
-  if (!owner->host) owner->p[0] = op.row_ptr;
-  exclusive_sum(ctx, sc, op.rowcnt, op.row_ptr, uint64_t(rows) + 1);
-  launch_positions(rows, TA.tile_rows, tl, op, s);
+  auto* rowcnt = sc.alloc<int64_t>(rows + 1);
+  TSG_CUDA(cudaMemsetAsync(rowcnt + rows, 0, sizeof(int64_t), s));
+  launch_row_counts(rows, TA.tile_rows, tl, sg, rowcnt, s);
   check_launch(ctx);
-  const uint64_t counted = uint64_t(readback(ctx, op.row_ptr + rows));
-  if (counted >= (uint64_t(1) << 32))
-    throw Fail{TSG_ERR_OTHER, "output beyond 2^32 elements needs row-panel batching"};
-  record(ctx, timing, 4);
-
-  // ---- (3) numeric -> final CSR at the counted positions ---------------------
-  op.col = sc.alloc<int32_t>(counted, !owner->host);
-  op.val = sc.alloc<float>(counted, !owner->host);
-  if (timing) TSG_CUDA(cudaEventRecord(ctx->kev[0], s));
-  launch_numeric(TA, TB, tl, op, opt.mode, err_flag, s);
-  check_launch(ctx);
-  if (timing) TSG_CUDA(cudaEventRecord(ctx->kev[1], s));
-  const unsigned flags = readback(ctx, err_flag);
-  raise_flags(flags);
-  record(ctx, timing, 5);
-
-  // ---- (4) compaction fix-up (only when some slot cancelled to zero) -----------
-  int64_t nnzC = int64_t(counted);
-  int64_t* d_rp = op.row_ptr;
-  int32_t* d_col = op.col;
-  float* d_val = op.val;
-  if (flags & kCancelled) {
-    auto* rowcnt = sc.alloc<int64_t>(rows + 1);
-    TSG_CUDA(cudaMemsetAsync(rowcnt + rows, 0, sizeof(int64_t), s));
-    launch_compact_count(rows, op, rowcnt, s);
-    check_launch(ctx);
-    int64_t* new_rp = sc.alloc<int64_t>(rows + 1, !owner->host);
-    exclusive_sum(ctx, sc, rowcnt, new_rp, uint64_t(rows) + 1);
-    nnzC = readback(ctx, new_rp + rows);
-    int32_t* ncol = sc.alloc<int32_t>(nnzC, !owner->host);
-    float* nval = sc.alloc<float>(nnzC, !owner->host);
-    launch_compact_fill(rows, op, new_rp, ncol, nval, s);
-    check_launch(ctx);
-    if (!owner->host) {  // the uncompacted buffers become scratch
-      sc.ptrs.push_back(op.row_ptr);
-      sc.ptrs.push_back(op.col);
-      sc.ptrs.push_back(op.val);
-    }
-    d_rp = new_rp;
-    d_col = ncol;
-    d_val = nval;
+  int64_t* d_rp = owner->host ? sc.alloc<int64_t>(rows + 1) : sc.alloc<int64_t>(rows + 1, true);
+  if (!owner->host) owner->p[0] = d_rp;
+  exclusive_sum(ctx, sc, rowcnt, d_rp, uint64_t(rows) + 1);
+  uint64_t counted = 0;
+  int64_t nnzC = 0;
+  {
+    const unsigned long long* src[2] = {sg.counted, reinterpret_cast<const unsigned long long*>(d_rp + rows)};
+    unsigned long long v[2];
+    readback_many(ctx, src, v);
+    counted = v[0];
+    nnzC = int64_t(v[1]);
   }
+  if (uint64_t(nnzC) >= (uint64_t(1) << 32))
+    throw Fail{TSG_ERR_OTHER, "output beyond 2^32 elements needs row-panel batching"};
+  int32_t* d_col = sc.alloc<int32_t>(nnzC, !owner->host);
+  float* d_val = sc.alloc<float>(nnzC, !owner->host);
   if (!owner->host) {
-    owner->p[0] = d_rp;
     owner->p[1] = d_col;
     owner->p[2] = d_val;
   }
+  if (timing) TSG_CUDA(cudaEventRecord(ctx->kev[2], s));
+  launch_assemble(rows, TA.tile_rows, tl, sg, d_rp, d_col, d_val, err_flag, s);
+  check_launch(ctx);
+  if (timing) TSG_CUDA(cudaEventRecord(ctx->kev[3], s));
   record(ctx, timing, 6);
+  // non-finite accumulators are flagged by the assembly (read at the final sync)
+  unsigned* flags_host = reinterpret_cast<unsigned*>(reinterpret_cast<char*>(ctx->pinned) + 56);
+  TSG_CUDA(cudaMemcpyAsync(flags_host, err_flag, 4, cudaMemcpyDeviceToHost, s));
 
   C->rows = Ain->rows;
   C->cols = Bin->cols;
@@ -564,6 +562,7 @@ void spgemm_impl(tsg_ctx* ctx, const tsg_csr* Ain, const tsg_csr* Bin, tsg_csr_o
   C->val = static_cast<float*>(owner->p[2]);
 
   TSG_CUDA(cudaStreamSynchronize(s));
+  raise_flags(*flags_host);
   if (tiles) {  // test path: 16x16 tiled view of the realised C
     std::vector<int64_t> h_rp(rows + 1);
     std::vector<int32_t> h_col(nnzC);
@@ -586,7 +585,7 @@ void spgemm_impl(tsg_ctx* ctx, const tsg_csr* Ain, const tsg_csr* Bin, tsg_csr_o
     TSG_CUDA(cudaEventElapsedTime(&kn, ctx->kev[0], ctx->kev[1]));
     TSG_CUDA(cudaEventElapsedTime(&kc, ctx->kev[2], ctx->kev[3]));
     ctx->last_numeric_kernel_ms = kn;
-    ctx->last_counting_kernel_ms = kc;
+    ctx->last_assemble_kernel_ms = kc;
     if (st) {
       st->convert += ms[1] * 1e-3;
       st->task_list += ms[2] * 1e-3;
@@ -605,6 +604,7 @@ void spgemm_impl(tsg_ctx* ctx, const tsg_csr* Ain, const tsg_csr* Bin, tsg_csr_o
     st->segments += S;
     st->counted_elements += counted;
     st->nnz_c = uint64_t(nnzC);
+    st->staged_slots += stage_total;
     st->kernel_launches += ctx->launches - launches0;
   }
 }
@@ -679,6 +679,8 @@ int tsg_destroy(tsg_ctx* ctx) {
     if (e) cudaEventDestroy(e);
   for (auto& e : ctx->kev)
     if (e) cudaEventDestroy(e);
+  if (ctx->stage_buf) cudaFreeAsync(ctx->stage_buf, ctx->stream);
+  cudaStreamSynchronize(ctx->stream);
   if (ctx->pinned) cudaFreeHost(ctx->pinned);
   for (auto& b : ctx->pinned_free) cudaFreeHost(b.first);
   if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
@@ -797,7 +799,7 @@ uint64_t tsg_launch_count(const tsg_ctx* ctx) { return ctx ? ctx->launches : 0; 
 double tsg_last_kernel_ms(const tsg_ctx* ctx, const char* phase) {
   if (!ctx || !phase) return 0.0;
   if (std::strcmp(phase, "numeric_kernel") == 0) return ctx->last_numeric_kernel_ms;
-  if (std::strcmp(phase, "counting_kernel") == 0) return ctx->last_counting_kernel_ms;
+  if (std::strcmp(phase, "assemble_kernel") == 0) return ctx->last_assemble_kernel_ms;
   static const char* names[] = {"", "convert", "task_list", "sort", "counting", "multiply",
                                 "compaction", "total"};
   for (int i = 1; i < 8; ++i)

@@ -9,10 +9,10 @@
 //   tco   uint2[T]          {tile column, occupancy}; occupancy lo16 = column
 //                           occupancy (OR of rows), hi16 = row occupancy: the
 //                           O(1) zero-product filter (pipeline.cpp:23-35)
-//   rm2   u32[T*8]          row masks, interleaved: word g = row g | row g+8 << 16
-//                           (bit c of row r <=> slot (r,c) nonzero; the 256-bit
-//                           occupancy mask, reference bit 8r+c, tile_format.hpp:20-23)
-//   cm2   u32[T*8]          column masks, same interleave (bit r of column c)
+//   rm2   u32[T*8]          the 256-bit occupancy mask as interleaved row
+//                           masks: word g = row g | row g+8 << 16 (bit c of
+//                           row r <=> slot (r,c) nonzero; reference bit 8r+c,
+//                           tile_format.hpp:20-23)
 //   meta  uint2[T]  (per operand role)  {lane mask, first chunk}
 //   chunk uint4[]   (per operand role)  16-byte lane chunks, chunk 0 = zeros
 //
@@ -44,7 +44,6 @@ struct TileMat {
   uint32_t* trp = nullptr;
   uint2* tco = nullptr;
   uint32_t* rm2 = nullptr;
-  uint32_t* cm2 = nullptr;
   uint2* meta[2] = {nullptr, nullptr};
   uint4* chunk[2] = {nullptr, nullptr};
 };

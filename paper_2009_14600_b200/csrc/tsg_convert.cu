@@ -17,7 +17,7 @@
 // (count, fill) with a prefix sum between them; the fill pass stages each
 // tile densely in shared memory and cuts the lane-dense operand chunks of
 // one or both roles (A order and/or B order, see tsg_common.cuh), plus the
-// interleaved row / column masks the symbolic and counting passes use.
+// tile's 256-bit occupancy mask and row/column occupancy words.
 #include "tsg_kernels.cuh"
 
 namespace tsg {
@@ -71,20 +71,6 @@ __device__ __forceinline__ unsigned short load_half(const void* val, int64_t p,
   }
   keep = (h & 0x7fffu) != 0;  // exact zero or underflow-to-(+-)0 dropped
   return h;
-}
-
-// 16x16 bit-matrix transpose across lanes 0-15 (lane r holds row r as a
-// u16): four shuffle-xor butterfly stages.  Returns column `lane & 15`.
-__device__ __forceinline__ uint32_t transpose16(uint32_t x, int lane) {
-  const uint32_t masks[4] = {0x00ffu, 0x0f0fu, 0x3333u, 0x5555u};
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const int k = 8 >> i;
-    const uint32_t m = masks[i];
-    const uint32_t y = __shfl_xor_sync(kFull, x, k);
-    x = (lane & k) ? ((x & (m << k)) | ((y >> k) & m)) : ((x & m) | ((y & m) << k));
-  }
-  return x & 0xffffu;
 }
 
 template <bool kFill, int kDtype>
@@ -159,13 +145,9 @@ __global__ void __launch_bounds__(256) convert_kernel(CsrView in, TileMat out, i
       const uint32_t t = tbase + ntiles;
       const uint32_t colocc = __reduce_or_sync(kFull, rm) & 0xffffu;
       if (lane == 0) out.tco[t] = make_uint2(J, colocc | ((any & 0xffffu) << 16));
-      // interleaved row masks: word g = row g | row g+8 << 16
+      // the 256-bit mask as interleaved row masks: word g = row g | row g+8 << 16
       const uint32_t rm_hi = __shfl_sync(kFull, rm, (lane & 7) + 8);
       if (lane < 8) out.rm2[size_t(t) * 8 + lane] = rm | (rm_hi << 16);
-      // column masks (bit r of column c): transpose of the row masks
-      const uint32_t cm = transpose16(rm, lane);
-      const uint32_t cm_hi = __shfl_sync(kFull, cm, (lane & 7) + 8);
-      if (lane < 8) out.cm2[size_t(t) * 8 + lane] = cm | (cm_hi << 16);
       // cut the lane chunks: A order reads row pairs (r, 2t..2t+1) of the
       // staged tile, B order the same pairs of the transposed tile
 #pragma unroll

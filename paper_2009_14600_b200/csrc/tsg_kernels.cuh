@@ -20,25 +20,26 @@ struct CsrView {  // device CSR input
 
 // Sorted tile-pair task list (pipeline.hpp:22-34 at T=16): pairs sorted by
 // (output tile row, output tile col, inner k), one segment per output tile.
+// Each pair is stored as its two operands' metas (pmeta), so the numeric
+// kernels reach the lane chunks with one indirection.
 struct TaskList {
   uint64_t npairs = 0, nseg = 0;
-  uint64_t* pairs = nullptr;        // [P] a | b << 32
-  uint4* pmeta = nullptr;           // [P] {A lane mask, A chunk base, B lane mask, B chunk base}
+  uint4* pmeta = nullptr;           // [P+1] {A lane mask, A chunk base, B lane mask, B chunk base}; [P] = 0
   uint32_t* seg_row_ptr = nullptr;  // [tile_rows+1] first segment of each tile row
   uint32_t* seg_off = nullptr;      // [S+1] first pair of each segment
   uint32_t* seg_col = nullptr;      // [S] output tile column J
-  uint32_t* seg_row = nullptr;      // [S] output tile row I
+  uint32_t* stage_off = nullptr;    // [S+1] staged-entry region of each segment (upper bound)
 };
 
-// Output sizing and the final CSR (CountResult + compact, kernels.hpp:15-30).
-struct OutPlan {
-  uint32_t* bm2 = nullptr;    // [S*8] boolean (counted) row masks, interleaved like rm2
-  uint8_t* cnt = nullptr;     // [S*16] counted entries per (segment, row)
-  uint32_t* pos = nullptr;    // [S*16] CSR position of each (segment, row) run
-  int64_t* rowcnt = nullptr;  // [rows+1] counted entries per CSR row
-  int64_t* row_ptr = nullptr;
-  int32_t* col = nullptr;
-  float* val = nullptr;
+// Numeric output in tile order (MulResult, kernels.hpp:24-30): each
+// segment's realised (nonzero) bitmap as 16 row masks, and its values packed
+// row-major (bit order, like TiledMatrix.elements) at stage_off[s].  The
+// assembly pass turns it into CSR (compact + to_element_coo,
+// kernels.cpp:205-220, tile_format.cpp:131-154).
+struct Staged {
+  float* val = nullptr;                   // [stage cap]
+  uint16_t* rmask = nullptr;              // [S*16] realised row masks (bit c of row r)
+  unsigned long long* counted = nullptr;  // structural (counted) nonzeros, CountResult.total_elements
 };
 
 // (1) conversion
@@ -53,9 +54,9 @@ void launch_cbar(const int32_t* colA, int64_t nnzA, int64_t inner, const int64_t
 
 // (2) symbolic -- light rows (<= 32 A tiles per tile row): sort-free merge
 void launch_merge_count(const TileMat& A, const TileMat& B, uint32_t* row_np, uint32_t* row_ns,
-                        uint32_t* row_raw, cudaStream_t st);
+                        uint32_t* row_nb, uint32_t* row_raw, cudaStream_t st);
 void launch_merge_fill(const TileMat& A, const TileMat& B, const uint32_t* row_pair_off,
-                       TaskList& tl, cudaStream_t st);
+                       const uint32_t* row_stage_off, TaskList& tl, cudaStream_t st);
 // (2) symbolic -- general: enumerate + filter, stable sort, segment heads
 void launch_enum_count(const TileMat& A, const TileMat& B, uint64_t tA, uint32_t* tile_cnt,
                        unsigned long long* raw_total, cudaStream_t st);
@@ -67,23 +68,20 @@ void launch_seg_count(const TileMat& A, const uint32_t* row_pair_off, const uint
                       uint32_t* row_nseg, cudaStream_t st);
 void launch_seg_fill(const TileMat& A, const uint32_t* row_pair_off, const uint32_t* keys,
                      TaskList& tl, cudaStream_t st);
-void launch_pair_meta(const TileMat& A, const TileMat& B, TaskList& tl, cudaStream_t st);
-// counting pass (boolean products on the u8 tensor cores)
-void launch_counting(const TileMat& A, const TileMat& B, const TaskList& tl, OutPlan& op,
-                     cudaStream_t st);
-// counted row sums -> (CUB scan -> row_ptr) -> per (segment, row) positions
-void launch_row_counts(int64_t rows, uint32_t tile_rows, const TaskList& tl, OutPlan& op,
-                       cudaStream_t st);
-void launch_positions(int64_t rows, uint32_t tile_rows, const TaskList& tl, OutPlan& op,
-                      cudaStream_t st);
+// per sorted pair: operand metas and the staging bound popc(rows A) * popc(cols B)
+void launch_pair_meta(const TileMat& A, const TileMat& B, const uint64_t* pairs, TaskList& tl,
+                      uint32_t* pair_bound, cudaStream_t st);
+void launch_seg_stage(const TaskList& tl, const uint32_t* pair_stage, cudaStream_t st);
 
-// (3) numeric -- writes the final CSR at the counted positions
-void launch_numeric(const TileMat& A, const TileMat& B, const TaskList& tl, OutPlan& op, int mode,
+// (3) numeric -- fused boolean count (counting_pass) + SEaC multiply, staged output
+void launch_numeric(const TaskList& tl, const TileMat& A, const TileMat& B, Staged& sg, int mode,
                     unsigned* err_flag, cudaStream_t st);
 
-// (4) compaction fix-up, only when some slot cancelled to zero
-void launch_compact_count(int64_t rows, const OutPlan& op, int64_t* rowcnt, cudaStream_t st);
-void launch_compact_fill(int64_t rows, const OutPlan& op, const int64_t* new_rp, int32_t* col,
-                         float* val, cudaStream_t st);
+// (4) assembly: realised row counts -> (CUB scan -> row_ptr) -> CSR
+void launch_row_counts(int64_t rows, uint32_t tile_rows, const TaskList& tl, const Staged& sg,
+                       int64_t* rowcnt, cudaStream_t st);
+void launch_assemble(int64_t rows, uint32_t tile_rows, const TaskList& tl, const Staged& sg,
+                     const int64_t* row_ptr, int32_t* col, float* val, unsigned* err_flag,
+                     cudaStream_t st);
 
 }  // namespace tsg

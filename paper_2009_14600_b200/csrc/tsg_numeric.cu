@@ -1,30 +1,34 @@
-// tsg_numeric.cu -- subsystem (3): SEaC numeric phase (sort, expand, compress).
+// tsg_numeric.cu -- subsystem (3): SEaC numeric phase (sort, expand, compress)
+// with the counting pass fused in.
 //
-// GPU restatement of multiply_pass / finalize_segment
-// (proj/src/kernels.cpp:105-203) at T = 16.  One warp per segment (= one
-// output tile, TaskList order).  The warp walks the segment's pairs in
-// ascending inner tile k and keeps the 16x16 fp32 output tile in registers
-// for the whole run (two m16n8 accumulators, 8 floats per lane).
+// GPU restatement of counting_pass + multiply_pass + finalize_segment
+// (proj/src/kernels.cpp:79-203) at T = 16.  A warp owns one segment (= one
+// output tile, TaskList order) at a time and walks its pairs in ascending
+// inner tile k, keeping the 16x16 fp32 output tile in registers for the
+// whole run (two m16n8 accumulators, 8 floats per lane).  Warps stride over
+// the segments (persistent grid, one resident wave).
 //
 //   TENSOR mode: per pair each lane loads its A and B operand chunk (one
 //     LDG.128 each, tsg_common.cuh) and the warp issues two
 //     mma.sync.m16n8k16.f32.f16.f16.f32 -- the 16x16 tile product is exactly
 //     one m16n16k16, so the 8x8 diagonal pairing of the reference
 //     (kernels.cpp:40-77) has no waste left to remove.
+//     Two more MMAs on the 0/1 indicators of the same operand registers
+//     (set.ne.f16x2) count, per output slot, the products with two nonzero
+//     factors: the slot is structurally nonzero (boolean_tile_mm,
+//     pipeline.cpp:11-21) iff that count is.  This is the counting pass
+//     (kernels.cpp:79-103) at no extra operand traffic.
 //   ORDERED mode: CUDA-core fp32, one rounding per product, ascending k,
 //     __fmul_rn/__fadd_rn (no FMA contraction, proj/CMakeLists.txt:12-14):
 //     bit-identical to tile_mm_reference (kernels.cpp:28-38) and to
 //     dense_spgemm_mixed_ordered (oracle.cpp:102-121).
 //
-// Compress (finalize_segment, kernels.cpp:109-127) writes straight into the
-// final CSR: the counting pass already fixed every structurally nonzero
-// slot's position (pos[seg, r] = row_ptr + counted entries of row r in the
-// row's earlier tiles), so value (r, c) of output tile (I, J) goes to
-// pos[seg, r] + rank of c in the counted row mask.  An
-// accumulator that is exactly 0 there (cancellation; v != 0 is false for
-// -0 too) is written as a col = -1 hole and flagged; the host then runs the
-// compaction fix-up (compact(), kernels.cpp:205-220).  Non-finite
-// accumulators raise kErrPrecision (PrecisionError, kernels.cpp:199-201).
+// Compress (finalize_segment, kernels.cpp:109-127): the bitmap is the set of
+// accumulators != 0 (so -0 and cancelled slots drop, which is compact(),
+// kernels.cpp:205-220); it is stored as 16 row masks, and the nonzeros are
+// packed row-major at the segment's staging offset for the CSR assembly.
+// Non-finite accumulators raise kErrPrecision (PrecisionError,
+// kernels.cpp:199-201) in the assembly pass, which reads every value.
 #include "tsg_kernels.cuh"
 
 namespace tsg {
@@ -39,195 +43,268 @@ __device__ __forceinline__ void mma16816(float (&d)[4], const uint4& a, uint32_t
       : "r"(a.x), "r"(a.y), "r"(a.z), "r"(a.w), "r"(b0), "r"(b1));
 }
 
-// chunk index of this lane for a tile with meta {lane mask, base}; 0 = zeros
-__device__ __forceinline__ uint32_t chunk_index(uint32_t lm, uint32_t base, int lane, bool ok) {
-  const bool present = ok && ((lm >> lane) & 1u);
-  return present ? base + __popc(lm & lanemask_lt()) : 0u;
+// fp16 accumulate (two .f16x2 registers per m16n8 tile)
+__device__ __forceinline__ void mma16816_h(uint32_t (&d)[2], const uint4& a, uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f16.f16.f16.f16 "
+      "{%0,%1}, {%2,%3,%4,%5}, {%6,%7}, {%0,%1};\n"
+      : "+r"(d[0]), "+r"(d[1])
+      : "r"(a.x), "r"(a.y), "r"(a.z), "r"(a.w), "r"(b0), "r"(b1));
 }
 
-// Where segment s's output goes: everything the epilogue needs that does
-// not depend on the accumulators, loaded at the top of the kernel so the
-// loads overlap the MMA work.
-struct TileDest {
-  uint32_t rowm;   // counted mask of row lane & 15
-  uint32_t pos;    // CSR position of that row's first counted entry
-  int32_t cbase;   // 16 * output tile column
+// 1.0 where the binary16 slot is nonzero, 0.0 where it is zero (per half)
+__device__ __forceinline__ uint32_t nz_h2(uint32_t x) {
+  uint32_t r;
+  asm("set.ne.f16x2.f16x2 %0, %1, %2;" : "=r"(r) : "r"(x), "r"(0u));
+  return r;
+}
+__device__ __forceinline__ uint4 nz_h2(const uint4& v) {
+  return make_uint4(nz_h2(v.x), nz_h2(v.y), nz_h2(v.z), nz_h2(v.w));
+}
+
+// nonzero halves of a .f16x2 register (0, 1 or 2)
+__device__ __forceinline__ uint32_t count_nz_h2(uint32_t x) {
+  return ((x & 0x7fffu) != 0u) + ((x & 0x7fff0000u) != 0u);
+}
+
+// chunk index of this lane for a tile with meta {lane mask, base}; 0 = zeros
+__device__ __forceinline__ uint32_t chunk_index(uint32_t lm, uint32_t base, int lane) {
+  return ((lm >> lane) & 1u) ? base + __popc(lm & lanemask_lt()) : 0u;
+}
+
+// Unconditional load: absent lanes read the shared zero chunk 0 (one
+// broadcast sector), so no zero-fill and no branch on the hot path.
+__device__ __forceinline__ uint4 load_chunk(const uint4* __restrict__ base, uint32_t lm,
+                                            uint32_t first, unsigned lt, unsigned bit) {
+  const uint32_t idx = (lm & bit) ? first + __popc(lm & lt) : 0u;
+  return __ldg(base + idx);
+}
+
+// Per-lane constants of the accumulator layout: acc[h][i] holds
+// (row g + 8*(i>>1), col 2t + (i&1) + 8h); cm[b][h] masks the columns of
+// that row left of col 2t + b + 8h.
+struct LaneLayout {
+  int g, t;
+  uint32_t cm[2][2];
+  __device__ __forceinline__ explicit LaneLayout(int lane) {
+    g = lane >> 2;
+    t = lane & 3;
+#pragma unroll
+    for (int b = 0; b < 2; ++b)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) cm[b][h] = (1u << (2 * t + b + 8 * h)) - 1u;
+  }
 };
 
-__device__ __forceinline__ TileDest tile_dest(uint64_t s, const TaskList& tl, const OutPlan& op,
-                                              int lane) {
-  const uint32_t J = tl.seg_col[s];
-  const int r = lane & 15;
-  const uint32_t w = op.bm2[s * 8 + (r & 7)];  // counted rows (r&7) | +8 << 16
-  TileDest d;
-  d.rowm = (r >> 3) ? (w >> 16) : (w & 0xffffu);
-  d.pos = op.pos[s * 16 + r];  // 64 contiguous bytes per segment (64-bit index: 16S > 2^32)
-  d.cbase = int32_t(J * 16);
-  return d;
-}
-
-constexpr int kSRow = 24;  // staging row stride (floats): conflict-free STS.64
-
-// acc[h][i] holds (row g + 8*(i>>1), col 2t + (i&1) + 8h).  The tile is
-// staged in shared memory (four STS.64 per lane), then lane r & 15 walks the
-// counted entries of row r -- lanes 0-15 take the even entries, 16-31 the
-// odd ones -- and stores them at pos + entry index.  sacc is this warp's
-// 16 x 16 float scratch.
-__device__ __forceinline__ void store_tile(const float (&acc)[2][4], const TileDest& d,
-                                           const OutPlan& op, int lane,
-                                           float* __restrict__ sacc,
-                                           unsigned* __restrict__ err_flag) {
-  const int g = lane >> 2, t = lane & 3;
+// finalize_segment: realised bitmap (16 row masks) and the nonzeros packed
+// row-major (compressed in this warp's shared scratch, written coalesced).
+__device__ __forceinline__ void emit_tile(const float (&acc)[2][4], uint32_t so, uint64_t s,
+                                          int lane, const LaneLayout& L, const Staged& sg,
+                                          float* __restrict__ sv) {
+  unsigned B[2][4];
 #pragma unroll
   for (int h = 0; h < 2; ++h)
 #pragma unroll
-    for (int q = 0; q < 2; ++q)
-      *reinterpret_cast<float2*>(sacc + (g + 8 * q) * kSRow + 2 * t + 8 * h) =
-          make_float2(acc[h][2 * q], acc[h][2 * q + 1]);
-  __syncwarp();
-  const int r = lane & 15, par = lane >> 4;
-  bool bad = false, cancelled = false;
-  uint32_t m = par ? (d.rowm & (d.rowm - 1)) : d.rowm;  // odd lanes start at entry 1
-  uint32_t e = par;
-  while (m) {
-    const int c = __ffs(m) - 1;
-    const float v = sacc[r * kSRow + c];
-    bad |= !isfinite(v);
-    const bool zero = v == 0.0f;
-    cancelled |= zero;
-    op.col[d.pos + e] = zero ? -1 : d.cbase + c;
-    op.val[d.pos + e] = v;
-    m &= m - 1;  // skip this entry ...
-    m &= m - 1;  // ... and the other parity's next one
-    e += 2;
+    for (int i = 0; i < 4; ++i) B[h][i] = __ballot_sync(kFull, acc[h][i] != 0.0f);
+  const unsigned rm = row_mask_from_ballots(B, lane);  // row lane & 15
+  const unsigned n = __popc(rm);
+  unsigned incl = n;  // inclusive prefix over the 16 rows (each half-warp alike)
+#pragma unroll
+  for (int o = 1; o < 16; o <<= 1) {
+    const unsigned y = __shfl_up_sync(kFull, incl, o, 16);
+    if ((lane & 15) >= o) incl += y;
   }
-  const unsigned flags = (__any_sync(kFull, bad) ? unsigned(kErrPrecision) : 0u) |
-                         (__any_sync(kFull, cancelled) ? unsigned(kCancelled) : 0u);
-  if (flags && lane == 0) atomicOr(err_flag, flags);
-}
-
-// One warp per segment.  The serial load chain is kept to three steps:
-// (1) segment bounds, (2) one coalesced LDG.128 per lane of the operand
-// metas of up to 32 pairs (TaskList.pmeta) together with the epilogue's
-// index loads, (3) the operand chunks of kBatch pairs at a time (metas
-// broadcast by shuffle; absent lanes and pairs past the end read the zero
-// chunk), then the MMAs.  Accumulation order is ascending k.
-// Absent lanes skip the load (no L1 sector) and use zeros.
-__device__ __forceinline__ uint4 load_chunk(const uint4* __restrict__ base, uint32_t lm,
-                                            uint32_t first, unsigned lt, unsigned bit) {
-  uint4 v = make_uint4(0, 0, 0, 0);
-  if (lm & bit) v = __ldg(base + first + __popc(lm & lt));
-  return v;
-}
-
-template <int kBatch>
-__global__ void __launch_bounds__(256) numeric_tc_kernel(TileMat A, TileMat B, TaskList tl,
-                                                        OutPlan op,
-                                                        unsigned* __restrict__ err_flag) {
-  __shared__ __align__(16) float s_acc[8][16 * kSRow];
-  const int lane = threadIdx.x & 31;
-  const uint64_t s = uint64_t(blockIdx.x) * 8 + (threadIdx.x >> 5);
-  if (s >= tl.nseg) return;
-  const uint32_t p0 = tl.seg_off[s], p1 = tl.seg_off[s + 1];
-  const TileDest dest = tile_dest(s, tl, op, lane);
-  float acc[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
-  const uint4* cA = A.chunk[kRoleA];
-  const uint4* cB = B.chunk[kRoleB];
-  const unsigned lt = lanemask_lt(), bit = 1u << lane;
-  for (uint32_t pb = p0; pb < p1; pb += 32) {
-    const uint32_t n = min(32u, p1 - pb);
-    const uint4 ml = lane < n ? __ldg(tl.pmeta + pb + lane) : make_uint4(0, 0, 0, 0);
-    for (uint32_t u0 = 0; u0 < n; u0 += kBatch) {
-      uint4 fa[kBatch], fb[kBatch];
+  if (lane < 16) sg.rmask[s * 16 + lane] = uint16_t(rm);  // 64-bit: 16 S > 2^32 on R-MAT
+  const unsigned pk = (incl - n) | (rm << 16);
+  const unsigned p0 = __shfl_sync(kFull, pk, L.g), p1 = __shfl_sync(kFull, pk, L.g + 8);
+  const unsigned total = __shfl_sync(kFull, incl, 15);
 #pragma unroll
-      for (int u = 0; u < kBatch; ++u) {
-        const int q = int(u0) + u;  // lanes >= n hold zero metas
-        const uint32_t lma = __shfl_sync(kFull, ml.x, q), bsa = __shfl_sync(kFull, ml.y, q);
-        const uint32_t lmb = __shfl_sync(kFull, ml.z, q), bsb = __shfl_sync(kFull, ml.w, q);
-        fa[u] = load_chunk(cA, lma, bsa, lt, bit);
-        fb[u] = load_chunk(cB, lmb, bsb, lt, bit);
+  for (int h = 0; h < 2; ++h)
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      if (acc[h][i] != 0.0f) {
+        const unsigned p = (i >> 1) ? p1 : p0;
+        sv[(p & 0xffffu) + __popc((p >> 16) & L.cm[i & 1][h])] = acc[h][i];
       }
+    }
+  __syncwarp();
+  for (unsigned e = lane; e < total; e += 32) sg.val[so + e] = sv[e];
+  __syncwarp();
+}
+
+__device__ __forceinline__ void finish(uint32_t nstruct, const Staged& sg, int lane) {
+  nstruct = __reduce_add_sync(kFull, nstruct);
+  if (lane == 0 && nstruct) atomicAdd(sg.counted, (unsigned long long)nstruct);
+}
+
+// Per segment: (1) its bounds and staging offset, (2) one coalesced
+// LDG.128 per lane of the operand metas of up to 32 pairs, parked in shared
+// memory and read back as broadcasts, (3) the operand chunks of kBatch pairs
+// at a time, then the MMAs.  Accumulation order is ascending k.
+template <int kBatch>
+__global__ void __launch_bounds__(256, 5) numeric_tc_kernel(TaskList tl, const uint4* __restrict__ cA,
+                                                           const uint4* __restrict__ cB, Staged sg,
+                                                           unsigned* __restrict__ err_flag) {
+  __shared__ __align__(16) uint4 s_meta[8][32];
+  __shared__ __align__(16) float s_v[8][256];
+  const int lane = threadIdx.x & 31;
+  const int w = threadIdx.x >> 5;
+  const unsigned lt = lanemask_lt(), bit = 1u << lane;
+  const LaneLayout L(lane);
+  uint32_t nstruct = 0;
+  const uint64_t stride = uint64_t(gridDim.x) * 8;
+  for (uint64_t s = uint64_t(blockIdx.x) * 8 + w; s < tl.nseg; s += stride) {
+    const uint32_t p0 = tl.seg_off[s], p1 = tl.seg_off[s + 1];
+    const uint32_t so = tl.stage_off[s];
+    float acc[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+    uint32_t sac[2][2] = {{0u, 0u}, {0u, 0u}};  // .f16x2 counts of nonzero products
+    for (uint32_t pb = p0; pb < p1; pb += 32) {
+      const uint32_t n = min(32u, p1 - pb);
+      s_meta[w][lane] = lane < n ? __ldg(tl.pmeta + pb + lane) : make_uint4(0, 0, 0, 0);
+      __syncwarp();
+      // kBatch | 32, so u0 + u <= 31; pairs past n hold zero metas and add
+      // exact zeros (absent slots already are zeros: the sums cannot change)
+      for (uint32_t u0 = 0; u0 < n; u0 += kBatch) {
+        uint4 fa[kBatch], fb[kBatch];
 #pragma unroll
-      for (int u = 0; u < kBatch; ++u) {
-        if (u0 + u < n) {
+        for (int u = 0; u < kBatch; ++u) {
+          const uint4 m = s_meta[w][u0 + u];
+          fa[u] = load_chunk(cA, m.x, m.y, lt, bit);
+          fb[u] = load_chunk(cB, m.z, m.w, lt, bit);
+        }
+#pragma unroll
+        for (int u = 0; u < kBatch; ++u) {
           // B chunk: {x, y} = {b0, b1} of the n0..7 MMA, {z, w} of the n8..15 MMA
           mma16816(acc[0], fa[u], fb[u].x, fb[u].y);
           mma16816(acc[1], fa[u], fb[u].z, fb[u].w);
+          // boolean product as 0/1 counts (fp16 sums of positive integers
+          // never return to zero; overflow saturates at inf, still nonzero)
+          const uint4 xa = nz_h2(fa[u]), xb = nz_h2(fb[u]);
+          mma16816_h(sac[0], xa, xb.x, xb.y);
+          mma16816_h(sac[1], xa, xb.z, xb.w);
         }
       }
+      __syncwarp();
     }
+    nstruct += count_nz_h2(sac[0][0]) + count_nz_h2(sac[0][1]) + count_nz_h2(sac[1][0]) +
+               count_nz_h2(sac[1][1]);
+    emit_tile(acc, so, s, lane, L, sg, s_v[w]);
   }
-  store_tile(acc, dest, op, lane, s_acc[threadIdx.x >> 5], err_flag);
+  finish(nstruct, sg, lane);
 }
 
-constexpr int kSA = 17;  // padded row stride of the A scratch tile
+constexpr int kSA = 17;    // padded row stride of the A scratch tile
+constexpr int kSRow = 24;  // row stride of the B scratch tile
 
-__global__ void __launch_bounds__(256) numeric_ordered_kernel(TileMat A, TileMat B, TaskList tl,
-                                                             OutPlan op,
+__global__ void __launch_bounds__(256) numeric_ordered_kernel(TaskList tl, const uint4* __restrict__ cA,
+                                                             const uint4* __restrict__ cB, Staged sg,
                                                              unsigned* __restrict__ err_flag) {
   __shared__ float sA[8][16 * kSA];
   __shared__ __align__(16) float sB[8][16 * kSRow];
   const int lane = threadIdx.x & 31;
   const int w = threadIdx.x >> 5;
-  const uint64_t s = uint64_t(blockIdx.x) * 8 + w;
-  if (s >= tl.nseg) return;
-  const uint32_t p0 = tl.seg_off[s], p1 = tl.seg_off[s + 1];
-  const int g = lane >> 2, t = lane & 3;
-  float acc[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
-  const unsigned long long* pairs = reinterpret_cast<const unsigned long long*>(tl.pairs);
-  for (uint32_t p = p0; p < p1; ++p) {
-    const uint64_t pr = __ldg(pairs + p);
-    // expand_tile (kernels.cpp:17-26): every lane writes all 8 of its slots
-    // (absent lanes read the zero chunk), so no separate clearing is needed
+  const LaneLayout L(lane);
+  uint32_t nstruct = 0;
+  const uint64_t stride = uint64_t(gridDim.x) * 8;
+  for (uint64_t s = uint64_t(blockIdx.x) * 8 + w; s < tl.nseg; s += stride) {
+    const uint32_t p0 = tl.seg_off[s], p1 = tl.seg_off[s + 1];
+    const uint32_t so = tl.stage_off[s];
+    float acc[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+    bool snz[2][4] = {{false, false, false, false}, {false, false, false, false}};
+    for (uint32_t p = p0; p < p1; ++p) {
+      const uint4 m = __ldg(tl.pmeta + p);
+      // expand_tile (kernels.cpp:17-26): every lane writes all 8 of its slots
+      // (absent lanes read the zero chunk), so no separate clearing is needed
 #pragma unroll
-    for (int role = 0; role < 2; ++role) {
-      const TileMat& M = role == kRoleA ? A : B;
-      const uint32_t tt = role == kRoleA ? uint32_t(pr) : uint32_t(pr >> 32);
-      const uint2 m = __ldg(M.meta[role] + tt);
-      const uint4 ch = __ldg(M.chunk[role] + chunk_index(m.x, m.y, lane, true));
-      const uint32_t regs[4] = {ch.x, role == kRoleA ? ch.y : ch.z, role == kRoleA ? ch.z : ch.y, ch.w};
+      for (int role = 0; role < 2; ++role) {
+        const uint4 ch = role == kRoleA ? __ldg(cA + chunk_index(m.x, m.y, lane))
+                                        : __ldg(cB + chunk_index(m.z, m.w, lane));
+        const uint32_t regs[4] = {ch.x, role == kRoleA ? ch.y : ch.z, role == kRoleA ? ch.z : ch.y, ch.w};
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        int r, c;
-        rc_of(role, lane, j, r, c);
-        const float v = __half2float(__ushort_as_half(uint16_t(regs[j >> 1] >> (16 * (j & 1)))));
-        if (role == kRoleA)
-          sA[w][r * kSA + c] = v;
-        else
-          sB[w][r * kSRow + c] = v;
+        for (int j = 0; j < 8; ++j) {
+          int r, c;
+          rc_of(role, lane, j, r, c);
+          const float v = __half2float(__ushort_as_half(uint16_t(regs[j >> 1] >> (16 * (j & 1)))));
+          if (role == kRoleA)
+            sA[w][r * kSA + c] = v;
+          else
+            sB[w][r * kSRow + c] = v;
+        }
       }
+      __syncwarp();
+      // tile_mm_reference: acc += a[r][k] * b[k][c], k ascending, no FMA.
+      // A product of two binary16 values is exact in fp32, so it is nonzero
+      // iff both factors are: that is the boolean product of the counting pass.
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int r = L.g + 8 * (i >> 1), c = 2 * L.t + (i & 1) + 8 * h;
+          float x = acc[h][i];
+          bool nz = snz[h][i];
+#pragma unroll
+          for (int kk = 0; kk < 16; ++kk) {
+            const float pr = __fmul_rn(sA[w][r * kSA + kk], sB[w][kk * kSRow + c]);
+            nz |= pr != 0.0f;
+            x = __fadd_rn(x, pr);
+          }
+          acc[h][i] = x;
+          snz[h][i] = nz;
+        }
+      __syncwarp();
     }
-    __syncwarp();
-    // tile_mm_reference: acc += a[r][k] * b[k][c], k ascending, no FMA
 #pragma unroll
     for (int h = 0; h < 2; ++h)
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int r = g + 8 * (i >> 1), c = 2 * t + (i & 1) + 8 * h;
-        float x = acc[h][i];
-#pragma unroll
-        for (int kk = 0; kk < 16; ++kk)
-          x = __fadd_rn(x, __fmul_rn(sA[w][r * kSA + kk], sB[w][kk * kSRow + c]));
-        acc[h][i] = x;
-      }
-    __syncwarp();
+      for (int i = 0; i < 4; ++i) nstruct += snz[h][i];
+    emit_tile(acc, so, s, lane, L, sg, sA[w]);
   }
-  store_tile(acc, tile_dest(s, tl, op, lane), op, lane, sB[w], err_flag);  // sB is free again
+  finish(nstruct, sg, lane);
+}
+
+// One resident wave: warps stride over the segments.  Occupancy is cached
+// per kernel (host-side lookup, no device work).
+unsigned resident_blocks(const void* kernel, uint64_t nseg) {
+  struct Entry {
+    const void* k;
+    int per_sm;
+  };
+  static Entry cache[8];
+  static int ncache = 0, sms = 0;
+  int per_sm = 0;
+  for (int i = 0; i < ncache; ++i)
+    if (cache[i].k == kernel) per_sm = cache[i].per_sm;
+  if (per_sm == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, 256, 0) != cudaSuccess ||
+        per_sm < 1)
+      per_sm = 1;
+    if (ncache < 8) cache[ncache++] = {kernel, per_sm};
+  }
+  const uint64_t want = (nseg + 7) / 8;
+  const uint64_t cap = uint64_t(per_sm) * uint64_t(sms);
+  return unsigned(want < cap ? want : cap);
 }
 
 }  // namespace
 
-void launch_numeric(const TileMat& A, const TileMat& B, const TaskList& tl, OutPlan& op, int mode,
+void launch_numeric(const TaskList& tl, const TileMat& A, const TileMat& B, Staged& sg, int mode,
                     unsigned* err_flag, cudaStream_t st) {
-  const uint64_t blocks = (tl.nseg + 7) / 8;
-  if (blocks == 0) return;
+  if (tl.nseg == 0) return;
+  const uint4* cA = A.chunk[kRoleA];
+  const uint4* cB = B.chunk[kRoleB];
+  using K = void (*)(TaskList, const uint4*, const uint4*, Staged, unsigned*);
+  K k = numeric_tc_kernel<2>;
   if (mode == 1) {
-    numeric_ordered_kernel<<<unsigned(blocks), 256, 0, st>>>(A, B, tl, op, err_flag);
+    k = numeric_ordered_kernel;
   } else {
     const int v = tuning_variant("TSG_NUMERIC_BATCH", 2);
-    auto k = v == 2 ? numeric_tc_kernel<2> : v == 8 ? numeric_tc_kernel<8> : numeric_tc_kernel<4>;
-    k<<<unsigned(blocks), 256, 0, st>>>(A, B, tl, op, err_flag);
+    if (v == 4) k = numeric_tc_kernel<4>;
+    if (v == 8) k = numeric_tc_kernel<8>;
   }
+  k<<<resident_blocks(reinterpret_cast<const void*>(k), tl.nseg), 256, 0, st>>>(tl, cA, cB, sg, err_flag);
 }
 
 }  // namespace tsg
