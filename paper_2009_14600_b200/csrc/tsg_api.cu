@@ -17,6 +17,8 @@
 // read data-dependent sizes (tile, pair, segment, element counts).
 #include <cub/device/device_scan.cuh>
 #include <cub/device/device_segmented_sort.cuh>
+#include <cub/device/device_select.cuh>
+#include <cub/iterator/counting_input_iterator.cuh>
 
 #include <cstdint>
 #include <cstdio>
@@ -368,6 +370,7 @@ void spgemm_impl(tsg_ctx* ctx, const tsg_csr* Ain, const tsg_csr* Bin, tsg_csr_o
   TaskList tl;
   const uint64_t nr = uint64_t(TA.tile_rows) + 1;
   uint64_t P = 0, S = 0, raw = 0, stage_total = 0;
+  const uint64_t* sorted_pairs = nullptr;  // general path: tile ids of the sorted pairs
   tl.seg_row_ptr = sc.alloc<uint32_t>(nr);
   uint32_t* row_pair_off = sc.alloc<uint32_t>(nr);
   if (light) {
@@ -477,6 +480,7 @@ void spgemm_impl(tsg_ctx* ctx, const tsg_csr* Ain, const tsg_csr* Bin, tsg_csr_o
     exclusive_sum(ctx, sc, pair_bound, pair_stage, P + 1);
     launch_seg_stage(tl, pair_stage, s);
     check_launch(ctx);
+    sorted_pairs = pairs;
     record(ctx, timing, 3);
   }
   record(ctx, timing, 4);  // the counting pass is fused into the numeric kernel
@@ -500,7 +504,24 @@ void spgemm_impl(tsg_ctx* ctx, const tsg_csr* Ain, const tsg_csr* Bin, tsg_csr_o
   sg.counted = sc.alloc<unsigned long long>(1);
   TSG_CUDA(cudaMemsetAsync(sg.counted, 0, sizeof(unsigned long long), s));
   if (timing) TSG_CUDA(cudaEventRecord(ctx->kev[0], s));
-  launch_numeric(tl, TA, TB, sg, opt.mode, err_flag, s);
+  if (sorted_pairs) {
+    // thin segments: thread each; the rest: warp each, from a compacted list
+    auto* heavy = sc.alloc<uint8_t>(S);
+    auto* list = sc.alloc<uint32_t>(S);
+    auto* list_len = sc.alloc<uint32_t>(1);
+    launch_numeric_thin(tl, sorted_pairs, TA, TB, sg, heavy, s);
+    check_launch(ctx);
+    if (S > 0) {
+      cub::CountingInputIterator<uint32_t> ids(0);
+      size_t bytes = 0;
+      TSG_CUDA(cub::DeviceSelect::Flagged(nullptr, bytes, ids, heavy, list, list_len, int64_t(S), s));
+      void* tmp = sc.alloc<char>(bytes);
+      TSG_CUDA(cub::DeviceSelect::Flagged(tmp, bytes, ids, heavy, list, list_len, int64_t(S), s));
+    }
+    launch_numeric(tl, TA, TB, sg, opt.mode, list, list_len, s);
+  } else {
+    launch_numeric(tl, TA, TB, sg, opt.mode, nullptr, nullptr, s);
+  }
   check_launch(ctx);
   if (timing) TSG_CUDA(cudaEventRecord(ctx->kev[1], s));
   record(ctx, timing, 5);

@@ -73,9 +73,14 @@ void launch_pair_meta(const TileMat& A, const TileMat& B, const uint64_t* pairs,
                       uint32_t* pair_bound, cudaStream_t st);
 void launch_seg_stage(const TaskList& tl, const uint32_t* pair_stage, cudaStream_t st);
 
-// (3) numeric -- fused boolean count (counting_pass) + SEaC multiply, staged output
+// (3) numeric -- fused boolean count (counting_pass) + SEaC multiply, staged output.
+// Thin segments (tiny staging bound): thread per segment, sequential fp32;
+// flags the others in `heavy` (general path, where the tile pairs exist).
+void launch_numeric_thin(const TaskList& tl, const uint64_t* pairs, const TileMat& A, const TileMat& B,
+                         Staged& sg, uint8_t* heavy, cudaStream_t st);
+// warp per segment over all segments, or over list[0 .. *list_len) when list != null
 void launch_numeric(const TaskList& tl, const TileMat& A, const TileMat& B, Staged& sg, int mode,
-                    unsigned* err_flag, cudaStream_t st);
+                    const uint32_t* list, const uint32_t* list_len, cudaStream_t st);
 
 // (4) assembly: realised row counts -> (CUB scan -> row_ptr) -> CSR
 void launch_row_counts(int64_t rows, uint32_t tile_rows, const TaskList& tl, const Staged& sg,

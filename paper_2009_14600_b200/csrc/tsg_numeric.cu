@@ -144,7 +144,8 @@ __device__ __forceinline__ void finish(uint32_t nstruct, const Staged& sg, int l
 template <int kBatch>
 __global__ void __launch_bounds__(256, 5) numeric_tc_kernel(TaskList tl, const uint4* __restrict__ cA,
                                                            const uint4* __restrict__ cB, Staged sg,
-                                                           unsigned* __restrict__ err_flag) {
+                                                           const uint32_t* __restrict__ list,
+                                                           const uint32_t* __restrict__ list_len) {
   __shared__ __align__(16) uint4 s_meta[8][32];
   __shared__ __align__(16) float s_v[8][256];
   const int lane = threadIdx.x & 31;
@@ -153,7 +154,9 @@ __global__ void __launch_bounds__(256, 5) numeric_tc_kernel(TaskList tl, const u
   const LaneLayout L(lane);
   uint32_t nstruct = 0;
   const uint64_t stride = uint64_t(gridDim.x) * 8;
-  for (uint64_t s = uint64_t(blockIdx.x) * 8 + w; s < tl.nseg; s += stride) {
+  const uint64_t nwork = list ? uint64_t(*list_len) : tl.nseg;
+  for (uint64_t i = uint64_t(blockIdx.x) * 8 + w; i < nwork; i += stride) {
+    const uint64_t s = list ? uint64_t(__ldg(list + i)) : i;
     const uint32_t p0 = tl.seg_off[s], p1 = tl.seg_off[s + 1];
     const uint32_t so = tl.stage_off[s];
     float acc[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
@@ -198,7 +201,8 @@ constexpr int kSRow = 24;  // row stride of the B scratch tile
 
 __global__ void __launch_bounds__(256) numeric_ordered_kernel(TaskList tl, const uint4* __restrict__ cA,
                                                              const uint4* __restrict__ cB, Staged sg,
-                                                             unsigned* __restrict__ err_flag) {
+                                                             const uint32_t* __restrict__ list,
+                                                             const uint32_t* __restrict__ list_len) {
   __shared__ float sA[8][16 * kSA];
   __shared__ __align__(16) float sB[8][16 * kSRow];
   const int lane = threadIdx.x & 31;
@@ -206,7 +210,9 @@ __global__ void __launch_bounds__(256) numeric_ordered_kernel(TaskList tl, const
   const LaneLayout L(lane);
   uint32_t nstruct = 0;
   const uint64_t stride = uint64_t(gridDim.x) * 8;
-  for (uint64_t s = uint64_t(blockIdx.x) * 8 + w; s < tl.nseg; s += stride) {
+  const uint64_t nwork = list ? uint64_t(*list_len) : tl.nseg;
+  for (uint64_t i = uint64_t(blockIdx.x) * 8 + w; i < nwork; i += stride) {
+    const uint64_t s = list ? uint64_t(__ldg(list + i)) : i;
     const uint32_t p0 = tl.seg_off[s], p1 = tl.seg_off[s + 1];
     const uint32_t so = tl.stage_off[s];
     float acc[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
@@ -262,6 +268,125 @@ __global__ void __launch_bounds__(256) numeric_ordered_kernel(TaskList tl, const
   finish(nstruct, sg, lane);
 }
 
+// ------------------------------------------------------------------ thin
+// Segments whose staging bound is at most kThin slots (ultra-sparse tiles:
+// R-MAT, the rectangular uniform product -- about one nonzero per tile and
+// one pair per segment) get one thread each instead of one warp: the
+// thread walks its pairs, and per pair the common inner slots k
+// (A column occupancy & B row occupancy, pipeline.cpp:23-35), and
+// accumulates every product a[r][k]*b[k][c] in sequential fp32 (k
+// ascending, pairs in segment order, no FMA: tile_mm_reference,
+// kernels.cpp:28-38) into a <= kThin-entry slot list -- bit-identical to
+// the reference in both modes.  Heavier segments are flagged for the warp
+// kernels.
+constexpr int kThin = 8;
+
+// binary16 value of slot (r, c) of a tile stored in `role` order
+__device__ __forceinline__ float tile_value(const uint4* __restrict__ chunks, uint2 meta, int role,
+                                            int r, int c) {
+  int lane, j;
+  slot_of(role, r, c, lane, j);
+  if (!((meta.x >> lane) & 1u)) return 0.0f;
+  const uint4 ch = __ldg(chunks + meta.y + __popc(meta.x & ((1u << lane) - 1u)));
+  const int reg = j >> 1;
+  // B chunks store the fragment registers as {reg0, reg2, reg1, reg3}
+  const int at = role == kRoleB ? ((reg & 1) << 1 | (reg >> 1)) : reg;
+  const uint32_t word = at == 0 ? ch.x : at == 1 ? ch.y : at == 2 ? ch.z : ch.w;
+  return __half2float(__ushort_as_half(uint16_t(word >> (16 * (j & 1)))));
+}
+
+__global__ void __launch_bounds__(256) numeric_thin_kernel(TaskList tl, const uint64_t* __restrict__ pairs,
+                                                          TileMat A, TileMat B, Staged sg,
+                                                          uint8_t* __restrict__ heavy) {
+  const uint64_t s = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
+  uint32_t nstruct = 0;
+  if (s < tl.nseg) {
+    const uint32_t so = tl.stage_off[s];
+    const bool thin = tl.stage_off[s + 1] - so <= uint32_t(kThin);
+    heavy[s] = !thin;
+    if (thin) {
+      uint32_t slot[kThin];
+      float acc[kThin];
+#pragma unroll
+      for (int i = 0; i < kThin; ++i) {
+        slot[i] = 0xffffu;
+        acc[i] = 0.0f;
+      }
+      int n = 0;
+      const uint32_t p0 = tl.seg_off[s], p1 = tl.seg_off[s + 1];
+      for (uint32_t p = p0; p < p1; ++p) {
+        const uint64_t pr = __ldg(reinterpret_cast<const unsigned long long*>(pairs) + p);
+        const uint32_t ta = uint32_t(pr), tb = uint32_t(pr >> 32);
+        const uint32_t oa = __ldg(&A.tco[ta].y), ob = __ldg(&B.tco[tb].y);
+        const uint2 ma = __ldg(A.meta[kRoleA] + ta), mb = __ldg(B.meta[kRoleB] + tb);
+        for (uint32_t km = (oa & 0xffffu) & (ob >> 16); km; km &= km - 1) {
+          const int k = __ffs(km) - 1;
+          for (uint32_t rm = oa >> 16; rm; rm &= rm - 1) {
+            const int r = __ffs(rm) - 1;
+            const float a = tile_value(A.chunk[kRoleA], ma, kRoleA, r, k);
+            if (a == 0.0f) continue;
+            for (uint32_t cmk = ob & 0xffffu; cmk; cmk &= cmk - 1) {
+              const int c = __ffs(cmk) - 1;
+              const float b = tile_value(B.chunk[kRoleB], mb, kRoleB, k, c);
+              if (b == 0.0f) continue;
+              const uint32_t want = uint32_t(r << 4 | c);
+              const float pr2 = __fmul_rn(a, b);
+              bool hit = false;
+#pragma unroll
+              for (int i = 0; i < kThin; ++i)
+                if (slot[i] == want) {
+                  acc[i] = __fadd_rn(acc[i], pr2);
+                  hit = true;
+                }
+              if (!hit) {  // new structural slot (n < kThin: the bound holds it)
+#pragma unroll
+                for (int i = 0; i < kThin; ++i)
+                  if (i == n) {
+                    slot[i] = want;
+                    acc[i] = __fadd_rn(0.0f, pr2);
+                  }
+                ++n;
+              }
+            }
+          }
+        }
+      }
+      nstruct = uint32_t(n);
+      // row-major order: sorting network on (slot, value), empty slots (0xffff) last
+#pragma unroll
+      for (int i = 0; i < kThin; ++i)
+#pragma unroll
+        for (int j = 0; j + 1 < kThin - i; ++j)
+          if (slot[j] > slot[j + 1]) {
+            const uint32_t t = slot[j];
+            slot[j] = slot[j + 1];
+            slot[j + 1] = t;
+            const float v = acc[j];
+            acc[j] = acc[j + 1];
+            acc[j + 1] = v;
+          }
+      uint32_t w[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // row masks, rows 2q | 2q+1 << 16
+      uint32_t e = 0;
+#pragma unroll
+      for (int i = 0; i < kThin; ++i) {
+        if (i < n && acc[i] != 0.0f) {  // realised (cancelled slots drop: compact())
+          const uint32_t r = slot[i] >> 4, bitpos = (slot[i] & 15u) + 16u * (r & 1u);
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            if (uint32_t(q) == (r >> 1)) w[q] |= 1u << bitpos;
+          sg.val[so + e] = acc[i];
+          ++e;
+        }
+      }
+      uint4* rec = reinterpret_cast<uint4*>(sg.rmask) + 2 * s;
+      rec[0] = make_uint4(w[0], w[1], w[2], w[3]);
+      rec[1] = make_uint4(w[4], w[5], w[6], w[7]);
+    }
+  }
+  nstruct = __reduce_add_sync(kFull, nstruct);
+  if ((threadIdx.x & 31) == 0 && nstruct) atomicAdd(sg.counted, (unsigned long long)nstruct);
+}
+
 // One resident wave: warps stride over the segments.  Occupancy is cached
 // per kernel (host-side lookup, no device work).
 unsigned resident_blocks(const void* kernel, uint64_t nseg) {
@@ -290,12 +415,19 @@ unsigned resident_blocks(const void* kernel, uint64_t nseg) {
 
 }  // namespace
 
+void launch_numeric_thin(const TaskList& tl, const uint64_t* pairs, const TileMat& A, const TileMat& B,
+                         Staged& sg, uint8_t* heavy, cudaStream_t st) {
+  if (tl.nseg == 0) return;
+  const uint64_t blocks = (tl.nseg + 255) / 256;
+  numeric_thin_kernel<<<unsigned(blocks), 256, 0, st>>>(tl, pairs, A, B, sg, heavy);
+}
+
 void launch_numeric(const TaskList& tl, const TileMat& A, const TileMat& B, Staged& sg, int mode,
-                    unsigned* err_flag, cudaStream_t st) {
+                    const uint32_t* list, const uint32_t* list_len, cudaStream_t st) {
   if (tl.nseg == 0) return;
   const uint4* cA = A.chunk[kRoleA];
   const uint4* cB = B.chunk[kRoleB];
-  using K = void (*)(TaskList, const uint4*, const uint4*, Staged, unsigned*);
+  using K = void (*)(TaskList, const uint4*, const uint4*, Staged, const uint32_t*, const uint32_t*);
   K k = numeric_tc_kernel<2>;
   if (mode == 1) {
     k = numeric_ordered_kernel;
@@ -304,7 +436,7 @@ void launch_numeric(const TaskList& tl, const TileMat& A, const TileMat& B, Stag
     if (v == 4) k = numeric_tc_kernel<4>;
     if (v == 8) k = numeric_tc_kernel<8>;
   }
-  k<<<resident_blocks(reinterpret_cast<const void*>(k), tl.nseg), 256, 0, st>>>(tl, cA, cB, sg, err_flag);
+  k<<<resident_blocks(reinterpret_cast<const void*>(k), tl.nseg), 256, 0, st>>>(tl, cA, cB, sg, list, list_len);
 }
 
 }  // namespace tsg

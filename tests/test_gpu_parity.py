@@ -131,3 +131,42 @@ def test_empty_and_identity(ctx):
     I = T.Csr(n, n, np.arange(n + 1, dtype=np.int64), np.arange(n, dtype=np.int32), np.ones(n, np.float32))
     C = ctx.spgemm(I, I).C
     assert np.array_equal(C.col, np.arange(n)) and np.all(C.val == 1.0)
+
+
+def _signed_wide(rows, cols, nnz, seed, values):
+    """Random pattern with tile rows wider than 32 tiles (the general
+    enumerate + sort path) and sign-mixed values."""
+    M = W.random_uniform(rows, cols, nnz, seed)
+    u = W.uniform(seed + 7, M.nnz)
+    if values == "unit":  # +-1: exact sums, frequent exact cancellation
+        M.val = np.where(u < 0.5, -1.0, 1.0).astype(np.float32)
+    else:  # SignedHalves [-4, 4] (proj/tests/support/corpus.hpp:52-56)
+        M.val = W._round_half(-4.0 + 8.0 * u)
+    return M
+
+
+@pytest.mark.parametrize("density", [0.0005, 0.004, 0.03])
+def test_general_path_thin_and_heavy(ctx, density):
+    """General path (> 32 A tiles per tile row) with thin (thread) and heavy
+    (warp) segments mixed: ORDERED bit-exact on SignedHalves; TENSOR
+    bit-exact on +-1 values, whose cancellations exercise compaction."""
+    from oracle import port
+    m, k = 300, 6000
+    nnz = int(m * k * density)
+    A = _signed_wide(m, k, nnz, 21, "signed")
+    B = _signed_wide(k, 400, int(k * 400 * density), 22, "signed")
+    want = port.spgemm_mixed(A, B)
+    got = ctx.spgemm(A, B, mode="ordered")
+    assert csr_bits_equal(got.C, want), first_diff(got.C, want)
+    assert got.stats["counted_elements"] == port.tile_stats(A, B, 16)["counted_elements"]
+    ten = ctx.spgemm(A, B, mode="tensor")
+    assert csr_pattern_equal(ten.C, want), first_diff(ten.C, want)
+    ok, worst = tolerance_ok(ten.C, want, A, B)
+    assert ok, worst
+    Au = _signed_wide(m, k, nnz, 23, "unit")
+    Bu = _signed_wide(k, 400, int(k * 400 * density), 24, "unit")
+    want = port.spgemm_mixed(Au, Bu)
+    for mode in ("tensor", "ordered"):
+        got = ctx.spgemm(Au, Bu, mode=mode)
+        assert csr_bits_equal(got.C, want), (mode, first_diff(got.C, want))
+        assert got.stats["counted_elements"] == port.tile_stats(Au, Bu, 16)["counted_elements"]
