@@ -366,40 +366,75 @@ void spgemm_impl(tsg_ctx* ctx, const tsg_csr* Ain, const tsg_csr* Bin, tsg_csr_o
   }
   record(ctx, timing, 1);
 
-  // ---- (2) symbolic: task list + staging bounds ----------------------------------
-  TaskList tl;
+  const int64_t rows = Ain->rows;
   const uint64_t nr = uint64_t(TA.tile_rows) + 1;
-  uint64_t P = 0, S = 0, raw = 0, stage_total = 0;
-  const uint64_t* sorted_pairs = nullptr;  // general path: tile ids of the sorted pairs
-  tl.seg_row_ptr = sc.alloc<uint32_t>(nr);
-  uint32_t* row_pair_off = sc.alloc<uint32_t>(nr);
+  uint64_t P = 0, S = 0, raw = 0, stage_total = 0, counted = 0;
+  int64_t nnzC = 0;
+  auto* owner = new OutOwner();
+  owner->host = C->mem == TSG_MEM_HOST;
+  C->_owner = owner;  // released by free_out on any later failure
+  int64_t* d_rp = owner->host ? sc.alloc<int64_t>(rows + 1) : sc.alloc<int64_t>(rows + 1, true);
+  if (!owner->host) owner->p[0] = d_rp;
+  int32_t* d_col = nullptr;
+  float* d_val = nullptr;
+  auto* counted_d = sc.alloc<unsigned long long>(1);
+  TSG_CUDA(cudaMemsetAsync(counted_d, 0, sizeof(unsigned long long), s));
+  auto* rowcnt = sc.alloc<int64_t>(rows + 1);  // realised entries per CSR row
+  TSG_CUDA(cudaMemsetAsync(rowcnt + rows, 0, sizeof(int64_t), s));
+  // the realised row counts -> row_ptr, nnz(C) and counted elements to the host
+  auto finish_rows = [&]() {
+    exclusive_sum(ctx, sc, rowcnt, d_rp, uint64_t(rows) + 1);
+    const unsigned long long* src[2] = {counted_d, reinterpret_cast<const unsigned long long*>(d_rp + rows)};
+    unsigned long long v[2];
+    readback_many(ctx, src, v);
+    counted = v[0];
+    nnzC = int64_t(v[1]);
+    if (uint64_t(nnzC) >= (uint64_t(1) << 32))
+      throw Fail{TSG_ERR_OTHER, "output beyond 2^32 elements needs row-panel batching"};
+    d_col = sc.alloc<int32_t>(nnzC, !owner->host);
+    d_val = sc.alloc<float>(nnzC, !owner->host);
+    if (!owner->host) {
+      owner->p[1] = d_col;
+      owner->p[2] = d_val;
+    }
+  };
+  // grow-only staging arena (bytes)
+  auto arena = [&](size_t need) -> void* {
+    need = std::max<size_t>(need, 16);
+    if (need > ctx->stage_cap) {
+      if (ctx->stage_buf) TSG_CUDA(cudaFreeAsync(ctx->stage_buf, s));
+      ctx->stage_buf = nullptr;
+      ctx->stage_cap = 0;
+      const size_t cap = need + need / 4;
+      TSG_CUDA(cudaMallocFromPoolAsync(&ctx->stage_buf, cap, ctx->pool, s));
+      ctx->stage_cap = cap;
+    }
+    return ctx->stage_buf;
+  };
+
   if (light) {
+    // ---- light rows: one fused pass per tile row (tsg_panel.cu) -----------------
     auto* row_np = sc.alloc<uint32_t>(nr);
     auto* row_ns = sc.alloc<uint32_t>(nr);
-    auto* row_nb = sc.alloc<uint32_t>(nr);
     auto* row_raw = sc.alloc<uint32_t>(nr);
-    auto* row_stage_off = sc.alloc<uint32_t>(nr);
-    TSG_CUDA(cudaMemsetAsync(row_np + nr - 1, 0, 4, s));
-    TSG_CUDA(cudaMemsetAsync(row_ns + nr - 1, 0, 4, s));
-    TSG_CUDA(cudaMemsetAsync(row_nb + nr - 1, 0, 4, s));
-    launch_merge_count(TA, TB, row_np, row_ns, row_nb, row_raw, s);
+    auto* row_bound = sc.alloc<uint32_t>(rows + 1);
+    auto* row_stage = sc.alloc<uint32_t>(rows + 1);
+    TSG_CUDA(cudaMemsetAsync(row_bound + rows, 0, 4, s));
+    launch_panel_count(TA, TB, rows, row_np, row_ns, row_raw, row_bound, s);
     check_launch(ctx);
-    exclusive_sum(ctx, sc, row_np, row_pair_off, nr);
-    exclusive_sum(ctx, sc, row_ns, tl.seg_row_ptr, nr);
-    exclusive_sum(ctx, sc, row_nb, row_stage_off, nr);
-    // exact u64 totals: raw pairs, staging bound (guards the u32 offsets)
+    exclusive_sum(ctx, sc, row_bound, row_stage, uint64_t(rows) + 1);
+    // exact u64 totals (guard the u32 staging offsets)
     auto* tot_d = sc.alloc<unsigned long long>(4);
     TSG_CUDA(cudaMemsetAsync(tot_d, 0, 4 * sizeof(unsigned long long), s));
     {
-      uint64_t blocks = (nr + 255) / 256;
-      if (blocks > 1184) blocks = 1184;
-      sum_u32_kernel<<<unsigned(blocks), 256, 0, s>>>(row_raw, nr - 1, tot_d + 2);
-      sum_u32_kernel<<<unsigned(blocks), 256, 0, s>>>(row_nb, nr - 1, tot_d + 3);
-      check_launch(ctx, 2);
+      const uint64_t n = std::max<uint64_t>(nr, uint64_t(rows) + 1);
+      const unsigned blocks = unsigned(std::min<uint64_t>((n + 255) / 256, 1184));
+      sum_u32_kernel<<<blocks, 256, 0, s>>>(row_np, nr - 1, tot_d);
+      sum_u32_kernel<<<blocks, 256, 0, s>>>(row_ns, nr - 1, tot_d + 1);
+      sum_u32_kernel<<<blocks, 256, 0, s>>>(row_raw, nr - 1, tot_d + 2);
+      sum_u32_kernel<<<blocks, 256, 0, s>>>(row_bound, uint64_t(rows), tot_d + 3);
+      check_launch(ctx, 4);
     }
-    // P, S fit u32 by construction (P <= raw, checked below)
-    TSG_CUDA(cudaMemcpyAsync(tot_d, row_pair_off + nr - 1, 4, cudaMemcpyDeviceToDevice, s));
-    TSG_CUDA(cudaMemcpyAsync(tot_d + 1, tl.seg_row_ptr + nr - 1, 4, cudaMemcpyDeviceToDevice, s));
     const unsigned long long* src[4] = {tot_d, tot_d + 1, tot_d + 2, tot_d + 3};
     unsigned long long v[4];
     readback_many(ctx, src, v);
@@ -407,22 +442,29 @@ void spgemm_impl(tsg_ctx* ctx, const tsg_csr* Ain, const tsg_csr* Bin, tsg_csr_o
     S = v[1];
     raw = v[2];
     stage_total = v[3];
-    if (raw >= (uint64_t(1) << 32) || stage_total >= (uint64_t(1) << 32))
-      throw Fail{TSG_ERR_OTHER, "task list beyond 2^32 raw pairs or staged slots needs row-panel batching"};
-    tl.npairs = P;
-    tl.nseg = S;
-    tl.pmeta = sc.alloc<uint4>(P + 1);
-    tl.seg_off = sc.alloc<uint32_t>(S + 1);
-    tl.seg_col = sc.alloc<uint32_t>(S);
-    tl.stage_off = sc.alloc<uint32_t>(S + 1);
-    TSG_CUDA(cudaMemcpyAsync(tl.seg_off + S, row_pair_off + nr - 1, 4, cudaMemcpyDeviceToDevice, s));
-    TSG_CUDA(cudaMemcpyAsync(tl.stage_off + S, row_stage_off + nr - 1, 4, cudaMemcpyDeviceToDevice, s));
-    TSG_CUDA(cudaMemsetAsync(tl.pmeta + P, 0, sizeof(uint4), s));  // pad: zero metas
-    launch_merge_fill(TA, TB, row_pair_off, row_stage_off, tl, s);
-    check_launch(ctx);
+    if (stage_total >= (uint64_t(1) << 32))
+      throw Fail{TSG_ERR_OTHER, "staged slots beyond 2^32 need row-panel batching"};
     record(ctx, timing, 2);
     record(ctx, timing, 3);  // the merge is the sort: no separate phase
+    record(ctx, timing, 4);  // the counting pass is fused into the numeric pass
+    float* sval = static_cast<float*>(arena(stage_total * 8));
+    int32_t* scol = reinterpret_cast<int32_t*>(sval + stage_total);
+    if (timing) TSG_CUDA(cudaEventRecord(ctx->kev[0], s));
+    launch_panel_numeric(TA, TB, rows, row_stage, sval, scol, rowcnt, counted_d, opt.mode, s);
+    check_launch(ctx);
+    if (timing) TSG_CUDA(cudaEventRecord(ctx->kev[1], s));
+    record(ctx, timing, 5);
+    finish_rows();
+    if (timing) TSG_CUDA(cudaEventRecord(ctx->kev[2], s));
+    launch_panel_copy(rows, TA.tile_rows, row_stage, d_rp, sval, scol, d_col, d_val, err_flag, s);
+    check_launch(ctx);
+    if (timing) TSG_CUDA(cudaEventRecord(ctx->kev[3], s));
+    record(ctx, timing, 6);
   } else {
+    // ---- general rows: task list, sort, numeric, assembly --------------------------
+    TaskList tl;
+    tl.seg_row_ptr = sc.alloc<uint32_t>(nr);
+    uint32_t* row_pair_off = sc.alloc<uint32_t>(nr);
     auto* raw_d = sc.alloc<unsigned long long>(1);
     TSG_CUDA(cudaMemsetAsync(raw_d, 0, sizeof(unsigned long long), s));
     auto* tile_off = sc.alloc<uint32_t>(tA + 1);
@@ -480,36 +522,21 @@ void spgemm_impl(tsg_ctx* ctx, const tsg_csr* Ain, const tsg_csr* Bin, tsg_csr_o
     exclusive_sum(ctx, sc, pair_bound, pair_stage, P + 1);
     launch_seg_stage(tl, pair_stage, s);
     check_launch(ctx);
-    sorted_pairs = pairs;
     record(ctx, timing, 3);
-  }
-  record(ctx, timing, 4);  // the counting pass is fused into the numeric kernel
+    record(ctx, timing, 4);  // the counting pass is fused into the numeric kernels
 
-  // ---- (3) numeric: counting + SEaC multiply -> staged tiles ---------------------
-  const int64_t rows = Ain->rows;
-  Staged sg;
-  {
-    const size_t need = std::max<size_t>(stage_total, 1) * sizeof(float);
-    if (need > ctx->stage_cap) {
-      if (ctx->stage_buf) TSG_CUDA(cudaFreeAsync(ctx->stage_buf, s));
-      ctx->stage_buf = nullptr;
-      ctx->stage_cap = 0;
-      const size_t cap = need + need / 4;
-      TSG_CUDA(cudaMallocFromPoolAsync(&ctx->stage_buf, cap, ctx->pool, s));
-      ctx->stage_cap = cap;
-    }
-    sg.val = static_cast<float*>(ctx->stage_buf);
-  }
-  sg.rmask = sc.alloc<uint16_t>(S * 16);
-  sg.counted = sc.alloc<unsigned long long>(1);
-  TSG_CUDA(cudaMemsetAsync(sg.counted, 0, sizeof(unsigned long long), s));
-  if (timing) TSG_CUDA(cudaEventRecord(ctx->kev[0], s));
-  if (sorted_pairs) {
+    // numeric: counting + SEaC multiply -> staged tiles
+    Staged sg;
+    sg.val = static_cast<float*>(arena(stage_total * sizeof(float)));
+    sg.rmask = sc.alloc<uint16_t>(S * 16);
+    sg.counted = counted_d;
+    if (timing) TSG_CUDA(cudaEventRecord(ctx->kev[0], s));
     // thin segments: thread each; the rest: warp each, from a compacted list
     auto* heavy = sc.alloc<uint8_t>(S);
     auto* list = sc.alloc<uint32_t>(S);
     auto* list_len = sc.alloc<uint32_t>(1);
-    launch_numeric_thin(tl, sorted_pairs, TA, TB, sg, heavy, s);
+    TSG_CUDA(cudaMemsetAsync(list_len, 0, sizeof(uint32_t), s));
+    launch_numeric_thin(tl, pairs, TA, TB, sg, heavy, s);
     check_launch(ctx);
     if (S > 0) {
       cub::CountingInputIterator<uint32_t> ids(0);
@@ -519,46 +546,20 @@ void spgemm_impl(tsg_ctx* ctx, const tsg_csr* Ain, const tsg_csr* Bin, tsg_csr_o
       TSG_CUDA(cub::DeviceSelect::Flagged(tmp, bytes, ids, heavy, list, list_len, int64_t(S), s));
     }
     launch_numeric(tl, TA, TB, sg, opt.mode, list, list_len, s);
-  } else {
-    launch_numeric(tl, TA, TB, sg, opt.mode, nullptr, nullptr, s);
-  }
-  check_launch(ctx);
-  if (timing) TSG_CUDA(cudaEventRecord(ctx->kev[1], s));
-  record(ctx, timing, 5);
+    check_launch(ctx);
+    if (timing) TSG_CUDA(cudaEventRecord(ctx->kev[1], s));
+    record(ctx, timing, 5);
 
-  // ---- (4) tiled -> CSR: realised row counts, scan, assembly ----------------------
-  auto* owner = new OutOwner();
-  owner->host = C->mem == TSG_MEM_HOST;
-  C->_owner = owner;  // released by free_out on any later failure
-  auto* rowcnt = sc.alloc<int64_t>(rows + 1);
-  TSG_CUDA(cudaMemsetAsync(rowcnt + rows, 0, sizeof(int64_t), s));
-  launch_row_counts(rows, TA.tile_rows, tl, sg, rowcnt, s);
-  check_launch(ctx);
-  int64_t* d_rp = owner->host ? sc.alloc<int64_t>(rows + 1) : sc.alloc<int64_t>(rows + 1, true);
-  if (!owner->host) owner->p[0] = d_rp;
-  exclusive_sum(ctx, sc, rowcnt, d_rp, uint64_t(rows) + 1);
-  uint64_t counted = 0;
-  int64_t nnzC = 0;
-  {
-    const unsigned long long* src[2] = {sg.counted, reinterpret_cast<const unsigned long long*>(d_rp + rows)};
-    unsigned long long v[2];
-    readback_many(ctx, src, v);
-    counted = v[0];
-    nnzC = int64_t(v[1]);
+    // tiled -> CSR: realised row counts, scan, assembly
+    launch_row_counts(rows, TA.tile_rows, tl, sg, rowcnt, s);
+    check_launch(ctx);
+    finish_rows();
+    if (timing) TSG_CUDA(cudaEventRecord(ctx->kev[2], s));
+    launch_assemble(rows, TA.tile_rows, tl, sg, d_rp, d_col, d_val, err_flag, s);
+    check_launch(ctx);
+    if (timing) TSG_CUDA(cudaEventRecord(ctx->kev[3], s));
+    record(ctx, timing, 6);
   }
-  if (uint64_t(nnzC) >= (uint64_t(1) << 32))
-    throw Fail{TSG_ERR_OTHER, "output beyond 2^32 elements needs row-panel batching"};
-  int32_t* d_col = sc.alloc<int32_t>(nnzC, !owner->host);
-  float* d_val = sc.alloc<float>(nnzC, !owner->host);
-  if (!owner->host) {
-    owner->p[1] = d_col;
-    owner->p[2] = d_val;
-  }
-  if (timing) TSG_CUDA(cudaEventRecord(ctx->kev[2], s));
-  launch_assemble(rows, TA.tile_rows, tl, sg, d_rp, d_col, d_val, err_flag, s);
-  check_launch(ctx);
-  if (timing) TSG_CUDA(cudaEventRecord(ctx->kev[3], s));
-  record(ctx, timing, 6);
   // non-finite accumulators are flagged by the assembly (read at the final sync)
   unsigned* flags_host = reinterpret_cast<unsigned*>(reinterpret_cast<char*>(ctx->pinned) + 56);
   TSG_CUDA(cudaMemcpyAsync(flags_host, err_flag, 4, cudaMemcpyDeviceToHost, s));

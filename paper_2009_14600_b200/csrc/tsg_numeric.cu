@@ -30,71 +30,11 @@
 // Non-finite accumulators raise kErrPrecision (PrecisionError,
 // kernels.cpp:199-201) in the assembly pass, which reads every value.
 #include "tsg_kernels.cuh"
+#include "tsg_mma.cuh"
 
 namespace tsg {
 
 namespace {
-
-__device__ __forceinline__ void mma16816(float (&d)[4], const uint4& a, uint32_t b0, uint32_t b1) {
-  asm volatile(
-      "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 "
-      "{%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};\n"
-      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
-      : "r"(a.x), "r"(a.y), "r"(a.z), "r"(a.w), "r"(b0), "r"(b1));
-}
-
-// fp16 accumulate (two .f16x2 registers per m16n8 tile)
-__device__ __forceinline__ void mma16816_h(uint32_t (&d)[2], const uint4& a, uint32_t b0, uint32_t b1) {
-  asm volatile(
-      "mma.sync.aligned.m16n8k16.row.col.f16.f16.f16.f16 "
-      "{%0,%1}, {%2,%3,%4,%5}, {%6,%7}, {%0,%1};\n"
-      : "+r"(d[0]), "+r"(d[1])
-      : "r"(a.x), "r"(a.y), "r"(a.z), "r"(a.w), "r"(b0), "r"(b1));
-}
-
-// 1.0 where the binary16 slot is nonzero, 0.0 where it is zero (per half)
-__device__ __forceinline__ uint32_t nz_h2(uint32_t x) {
-  uint32_t r;
-  asm("set.ne.f16x2.f16x2 %0, %1, %2;" : "=r"(r) : "r"(x), "r"(0u));
-  return r;
-}
-__device__ __forceinline__ uint4 nz_h2(const uint4& v) {
-  return make_uint4(nz_h2(v.x), nz_h2(v.y), nz_h2(v.z), nz_h2(v.w));
-}
-
-// nonzero halves of a .f16x2 register (0, 1 or 2)
-__device__ __forceinline__ uint32_t count_nz_h2(uint32_t x) {
-  return ((x & 0x7fffu) != 0u) + ((x & 0x7fff0000u) != 0u);
-}
-
-// chunk index of this lane for a tile with meta {lane mask, base}; 0 = zeros
-__device__ __forceinline__ uint32_t chunk_index(uint32_t lm, uint32_t base, int lane) {
-  return ((lm >> lane) & 1u) ? base + __popc(lm & lanemask_lt()) : 0u;
-}
-
-// Unconditional load: absent lanes read the shared zero chunk 0 (one
-// broadcast sector), so no zero-fill and no branch on the hot path.
-__device__ __forceinline__ uint4 load_chunk(const uint4* __restrict__ base, uint32_t lm,
-                                            uint32_t first, unsigned lt, unsigned bit) {
-  const uint32_t idx = (lm & bit) ? first + __popc(lm & lt) : 0u;
-  return __ldg(base + idx);
-}
-
-// Per-lane constants of the accumulator layout: acc[h][i] holds
-// (row g + 8*(i>>1), col 2t + (i&1) + 8h); cm[b][h] masks the columns of
-// that row left of col 2t + b + 8h.
-struct LaneLayout {
-  int g, t;
-  uint32_t cm[2][2];
-  __device__ __forceinline__ explicit LaneLayout(int lane) {
-    g = lane >> 2;
-    t = lane & 3;
-#pragma unroll
-    for (int b = 0; b < 2; ++b)
-#pragma unroll
-      for (int h = 0; h < 2; ++h) cm[b][h] = (1u << (2 * t + b + 8 * h)) - 1u;
-  }
-};
 
 // finalize_segment: realised bitmap (16 row masks) and the nonzeros packed
 // row-major (compressed in this warp's shared scratch, written coalesced).
@@ -118,17 +58,26 @@ __device__ __forceinline__ void emit_tile(const float (&acc)[2][4], uint32_t so,
   const unsigned pk = (incl - n) | (rm << 16);
   const unsigned p0 = __shfl_sync(kFull, pk, L.g), p1 = __shfl_sync(kFull, pk, L.g + 8);
   const unsigned total = __shfl_sync(kFull, incl, 15);
+  // entry index of (row, col 2t + 8h) = row prefix + nonzeros left of it in
+  // the row; its odd neighbour follows directly when it is nonzero itself
 #pragma unroll
-  for (int h = 0; h < 2; ++h)
+  for (int q = 0; q < 2; ++q) {
+    const unsigned p = q ? p1 : p0;
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      if (acc[h][i] != 0.0f) {
-        const unsigned p = (i >> 1) ? p1 : p0;
-        sv[(p & 0xffffu) + __popc((p >> 16) & L.cm[i & 1][h])] = acc[h][i];
-      }
+    for (int h = 0; h < 2; ++h) {
+      const float v0 = acc[h][2 * q], v1 = acc[h][2 * q + 1];
+      const unsigned e0 = (p & 0xffffu) + __popc((p >> 16) & L.cm[h]);
+      if (v0 != 0.0f) sv[e0] = v0;
+      if (v1 != 0.0f) sv[e0 + (v0 != 0.0f)] = v1;
     }
+  }
   __syncwarp();
-  for (unsigned e = lane; e < total; e += 32) sg.val[so + e] = sv[e];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {  // total <= 256
+    if (32u * k >= total) break;
+    const unsigned e = lane + 32u * k;
+    if (e < total) sg.val[so + e] = sv[e];
+  }
   __syncwarp();
 }
 
@@ -141,8 +90,8 @@ __device__ __forceinline__ void finish(uint32_t nstruct, const Staged& sg, int l
 // LDG.128 per lane of the operand metas of up to 32 pairs, parked in shared
 // memory and read back as broadcasts, (3) the operand chunks of kBatch pairs
 // at a time, then the MMAs.  Accumulation order is ascending k.
-template <int kBatch>
-__global__ void __launch_bounds__(256, 5) numeric_tc_kernel(TaskList tl, const uint4* __restrict__ cA,
+template <int kBatch, int kMinBlocks>
+__global__ void __launch_bounds__(256, kMinBlocks) numeric_tc_kernel(TaskList tl, const uint4* __restrict__ cA,
                                                            const uint4* __restrict__ cB, Staged sg,
                                                            const uint32_t* __restrict__ list,
                                                            const uint32_t* __restrict__ list_len) {
@@ -428,13 +377,15 @@ void launch_numeric(const TaskList& tl, const TileMat& A, const TileMat& B, Stag
   const uint4* cA = A.chunk[kRoleA];
   const uint4* cB = B.chunk[kRoleB];
   using K = void (*)(TaskList, const uint4*, const uint4*, Staged, const uint32_t*, const uint32_t*);
-  K k = numeric_tc_kernel<2>;
+  K k = numeric_tc_kernel<2, 4>;
   if (mode == 1) {
     k = numeric_ordered_kernel;
   } else {
     const int v = tuning_variant("TSG_NUMERIC_BATCH", 2);
-    if (v == 4) k = numeric_tc_kernel<4>;
-    if (v == 8) k = numeric_tc_kernel<8>;
+    const int mb = tuning_variant("TSG_NUMERIC_MINB", 4);
+    if (v == 1) k = mb == 6 ? numeric_tc_kernel<1, 6> : numeric_tc_kernel<1, 5>;
+    if (v == 2) k = mb == 4 ? numeric_tc_kernel<2, 4> : mb == 6 ? numeric_tc_kernel<2, 6> : numeric_tc_kernel<2, 5>;
+    if (v == 4) k = mb == 3 ? numeric_tc_kernel<4, 3> : numeric_tc_kernel<4, 4>;
   }
   k<<<resident_blocks(reinterpret_cast<const void*>(k), tl.nseg), 256, 0, st>>>(tl, cA, cB, sg, list, list_len);
 }

@@ -82,33 +82,43 @@ __device__ __forceinline__ uint32_t kth_bit(uint32_t m, uint32_t k) {
   return c;
 }
 
-constexpr uint32_t kAsmW = 1024;  // staged values per warp batch (shared memory)
+constexpr uint32_t kAsmW = 512;  // staged values per warp batch (shared memory)
 
-// Warp per tile row.  Segments are taken in batches of up to 32 whose
-// staged values fit kAsmW: (1) the batch's staged runs are copied into
-// shared memory (flattened over the segments, contiguous per segment);
-// (2) for each row r of the tile row, the runs of row r of the batch's
-// segments are consecutive in the CSR (segments are in column order), so
-// the copy is flattened over them: lane q of an iteration writes CSR
-// position base_r + q -- every store instruction is one contiguous,
-// coalesced range -- taking its value from shared memory and its column
-// from the owning segment's row mask.  Non-finite values raise
-// kErrPrecision here (finalize_segment's check, kernels.cpp:115-127).
+// Warp per tile row.  Segments are taken in batches of up to 32 (lane j =
+// segment j of the batch) whose staged values fit kAsmW.  Every entry of a
+// batch goes to row r's CSR range at an offset = entries of row r in
+// earlier segments of the tile row (segments are in column order) -- a
+// stable partition of the batch's entries by r:
+//   (1) scatter: lanes over the batch's staged entries (contiguous per
+//       segment, so the global reads coalesce); entry e of segment j finds
+//       its row from the segment's 16 row-prefix bytes and its column from
+//       the row mask, ranks itself among the lanes holding the same row
+//       (match.any) and lands in shared memory at the batch's row-r offset;
+//   (2) copy out: lanes over the batch's entries in row order; each store
+//       instruction covers at most a few contiguous CSR ranges.
+// Non-finite values raise kErrPrecision here (finalize_segment's check,
+// kernels.cpp:115-127).
 __global__ void __launch_bounds__(256) assemble_kernel(int64_t rows, uint32_t tile_rows, TaskList tl,
                                                       Staged sg, const int64_t* __restrict__ row_ptr,
                                                       int32_t* __restrict__ col,
                                                       float* __restrict__ val,
                                                       unsigned* __restrict__ err_flag) {
   __shared__ float s_val[8][kAsmW];
+  __shared__ int32_t s_col[8][kAsmW];
+  __shared__ uint4 s_pre[8][32];   // per batch segment: 16 exclusive row-prefix bytes
+  __shared__ uint4 s_msk[8][64];   // per batch segment: 16 row masks (two uint4)
+  __shared__ uint32_t s_ctr[8][16];
   const int lane = threadIdx.x & 31;
   const int w = threadIdx.x >> 5;
   const uint32_t I = blockIdx.x * 8 + w;
   if (I >= tile_rows) return;
   float* sv = s_val[w];
+  int32_t* sc = s_col[w];
   const uint32_t s0 = tl.seg_row_ptr[I], s1 = tl.seg_row_ptr[I + 1];
   const int64_t row = int64_t(I) * 16 + (lane & 15);
   uint32_t carry = (lane < 16 && row < rows) ? uint32_t(row_ptr[row]) : 0u;  // lane r: row r
   const uint4* rec = reinterpret_cast<const uint4*>(sg.rmask);
+  const unsigned lt = lanemask_lt();
   bool bad = false;
   for (uint32_t sb = s0; sb < s1;) {
     const uint32_t s = sb + lane;
@@ -117,63 +127,110 @@ __global__ void __launch_bounds__(256) assemble_kernel(int64_t rows, uint32_t ti
       lo = __ldg(rec + 2 * uint64_t(s));
       hi = __ldg(rec + 2 * uint64_t(s) + 1);
     }
-    uint32_t m2[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};  // rows 2i | 2i+1 << 16
+    const uint32_t m2[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};  // rows 2i | 2i+1 << 16
+    uint32_t pc[16];
     uint32_t tot = 0;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) tot += __popc(m2[i]);
+    for (int r = 0; r < 16; ++r) {
+      pc[r] = __popc((m2[r >> 1] >> (16 * (r & 1))) & 0xffffu);
+      tot += pc[r];
+    }
     uint32_t incl = warp_incl_scan(tot, lane);
     // batch = the longest prefix of segments whose values fit (>= 1: tot <= 256)
-    const unsigned fit = __ballot_sync(kFull, s < s1 && incl <= kAsmW);
-    const uint32_t nb = __popc(fit);
+    const uint32_t nb = __popc(__ballot_sync(kFull, s < s1 && incl <= kAsmW));
     const uint32_t T = __shfl_sync(kFull, incl, nb - 1);
-    if (uint32_t(lane) >= nb) {  // not in this batch
+    const bool in = uint32_t(lane) < nb;
+    if (!in) {
 #pragma unroll
-      for (int i = 0; i < 8; ++i) m2[i] = 0;
+      for (int r = 0; r < 16; ++r) pc[r] = 0;
       tot = 0;
       incl = T;
     }
-    const uint32_t so = (uint32_t(lane) < nb) ? __ldg(tl.stage_off + s) : 0u;
-    const uint32_t cbase = (uint32_t(lane) < nb) ? __ldg(tl.seg_col + s) * 16u : 0u;
-    // (1) staged runs -> shared memory
-    {
-      const uint32_t from = so - (incl - tot);
-      for (uint32_t q0 = 0; q0 < T; q0 += 32) {
-        const uint32_t q = q0 + lane;
-        const int j = owner_of(incl, q);
-        const uint32_t f = __shfl_sync(kFull, from, j);
-        if (q < T) sv[q] = __ldg(sg.val + f + q);
-      }
-    }
-    __syncwarp();
-    // (2) row by row, CSR order
-    uint32_t src = incl - tot;  // shared-memory start of this segment's row r
+    const uint32_t so = in ? __ldg(tl.stage_off + s) : 0u;
+    const uint32_t cbase = in ? __ldg(tl.seg_col + s) * 16u : 0u;
+    // per-segment row prefixes (bytes: <= 240 before row 15) and masks
+    uint32_t pw[4] = {0, 0, 0, 0}, run = 0;
 #pragma unroll
     for (int r = 0; r < 16; ++r) {
-      const uint32_t m = (m2[r >> 1] >> (16 * (r & 1))) & 0xffffu;
-      const uint32_t v = __popc(m);
-      const uint32_t ri = warp_incl_scan(v, lane);
-      const uint32_t rt = __shfl_sync(kFull, ri, 31);
-      if (rt) {
-        const uint32_t base = __shfl_sync(kFull, carry, r);
-        const uint32_t from = src - (ri - v);
-        for (uint32_t q0 = 0; q0 < rt; q0 += 32) {
-          const uint32_t q = q0 + lane;
-          const int j = owner_of(ri, q);
-          const uint32_t f = __shfl_sync(kFull, from, j);
-          const uint32_t mj = __shfl_sync(kFull, m, j);
-          const uint32_t ej = __shfl_sync(kFull, ri - v, j);
-          const uint32_t cb = __shfl_sync(kFull, cbase, j);
-          if (q < rt) {
-            const float x = sv[f + q];
-            bad |= !isfinite(x);
-            col[base + q] = int32_t(cb + kth_bit(mj, q - ej));
-            val[base + q] = x;
-          }
-        }
-        if (lane == r) carry += rt;
-      }
-      src += v;
+      pw[r >> 2] |= run << (8 * (r & 3));
+      run += pc[r];
     }
+    s_pre[w][lane] = make_uint4(pw[0], pw[1], pw[2], pw[3]);
+    s_msk[w][2 * lane] = in ? lo : make_uint4(0, 0, 0, 0);
+    s_msk[w][2 * lane + 1] = in ? hi : make_uint4(0, 0, 0, 0);
+    // batch row totals -> row offsets in shared memory (lane r holds row r)
+    uint32_t ro = 0, rt_mine = 0, acc = 0;
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+      const uint32_t t = __reduce_add_sync(kFull, pc[r]);
+      if (lane == r) {
+        ro = acc;
+        rt_mine = t;
+      }
+      acc += t;
+    }
+    if (lane < 16) s_ctr[w][lane] = 0;
+    __syncwarp();
+    // (1) scatter into row order
+    const uint32_t excl = incl - tot;
+    for (uint32_t q0 = 0; q0 < T; q0 += 32) {
+      const uint32_t q = q0 + lane;
+      const int j = owner_of(incl, q);
+      const uint32_t ej = __shfl_sync(kFull, excl, j);
+      const uint32_t soj = __shfl_sync(kFull, so, j);
+      const uint32_t cbj = __shfl_sync(kFull, cbase, j);
+      const bool act = q < T;
+      const uint32_t e = q - ej;
+      uint32_t r = 16;  // sentinel for inactive lanes
+      float x = 0.0f;
+      int32_t c = 0;
+      if (act) {
+        x = __ldg(sg.val + soj + e);
+        const uint4 pv = s_pre[w][j];
+        const uint32_t pb[4] = {pv.x, pv.y, pv.z, pv.w};
+        r = 0;  // last row whose prefix is <= e (prefixes are non-decreasing)
+#pragma unroll
+        for (int b = 8; b > 0; b >>= 1) {
+          const uint32_t rr = r + b;
+          const uint32_t pre = (pb[rr >> 2] >> (8 * (rr & 3))) & 0xffu;
+          if (pre <= e) r = rr;
+        }
+        const uint32_t pre_r = (pb[r >> 2] >> (8 * (r & 3))) & 0xffu;
+        const uint32_t m = reinterpret_cast<const uint16_t*>(&s_msk[w][2 * j])[r];
+        c = int32_t(cbj + kth_bit(m, e - pre_r));
+      }
+      const unsigned grp = __match_any_sync(kFull, r);
+      const uint32_t ro_r = __shfl_sync(kFull, ro, r & 15);
+      if (act) {
+        const uint32_t d = ro_r + s_ctr[w][r] + __popc(grp & lt);
+        sv[d] = x;
+        sc[d] = c;
+      }
+      __syncwarp();
+      if (act && (grp >> lane) == 1u) s_ctr[w][r] += __popc(grp);  // highest lane of the group
+      __syncwarp();
+    }
+    // (2) copy out in row order: position q -> row r (lane r holds ro, rt)
+    for (uint32_t q0 = 0; q0 < T; q0 += 32) {
+      const uint32_t q = q0 + lane;
+      int r = 0;
+#pragma unroll
+      for (int b = 8; b > 0; b >>= 1) {
+        const uint32_t v = __shfl_sync(kFull, ro, r + b);
+        if (v <= q) r += b;
+      }
+      // rows with no entries share their offset with the next row: the search
+      // lands on the last such row, whose offset is still ro_r <= q
+      const uint32_t ro_r = __shfl_sync(kFull, ro, r), base = __shfl_sync(kFull, carry, r);
+      if (q < T) {
+        const float x = sv[q];
+        bad |= !isfinite(x);
+        const uint32_t dst = base + (q - ro_r);
+        col[dst] = sc[q];
+        val[dst] = x;
+      }
+    }
+    if (lane < 16) carry += rt_mine;
     __syncwarp();
     sb += nb;
   }

@@ -1,0 +1,331 @@
+// tsg_panel.cu -- the light-row pipeline: task list, counting, SEaC numeric
+// and compaction of one tile row (a 16-row panel of A) fused in one warp.
+//
+// Applies when every tile row of A has at most 32 tiles (FEM27, Poisson,
+// the R.A stage of AMG).  Restates, per tile row I:
+//   enumerate_pairs / filter_zero_products   pipeline.cpp:37-70
+//   sort_and_segment                          pipeline.cpp:72-109
+//   counting_pass                             kernels.cpp:79-103
+//   multiply_pass / finalize_segment          kernels.cpp:105-203
+//   compact                                   kernels.cpp:205-220
+// Lane l owns A tile (I, k_l) and walks B tile row k_l (sorted by J).  Each
+// step takes the minimum pending output column J (REDUX): the lanes holding
+// it are exactly output tile (I, J)'s pairs, already in ascending k (lane
+// order) -- the sort happens in registers, the segment is the step.  The
+// warp multiplies the step's pairs right there (mma.sync, fp32 accumulators
+// in registers; or sequential CUDA-core fp32 in ORDERED mode), counts its
+// structural nonzeros (0/1-indicator MMA, see tsg_numeric.cu) and appends
+// the realised entries of each of its 16 rows to that CSR row's staging
+// region.  Because the warp visits the row's output tiles in column order,
+// every staging row fills in final CSR order; no task list, segment table or
+// position pass ever reaches HBM.
+//
+//   panel_count_kernel    raw / filtered pairs, segments (stats) and a
+//                         staging bound per CSR row
+//   CUB scan              -> staging row offsets                (tsg_api.cu)
+//   panel_numeric_kernel  the fused pass above; realised count per row
+//   CUB scan              -> row_ptr                            (tsg_api.cu)
+//   panel_copy_kernel     staging rows -> CSR (contiguous copies), the
+//                         non-finite check of finalize_segment
+#include "tsg_kernels.cuh"
+#include "tsg_mma.cuh"
+
+namespace tsg {
+
+namespace {
+
+constexpr uint32_t kInf = 0xffffffffu;
+
+// Warp state of the 32-way merge over tile row I.
+struct Merge {
+  uint32_t colocc = 0, rowocc = 0, cur = 0, end = 0;
+  uint2 bt, bn;
+  __device__ __forceinline__ void start(const TileMat& A, const TileMat& B, uint32_t I, int lane,
+                                        uint32_t& a) {
+    const uint32_t a0 = A.trp[I];
+    const uint32_t na = A.trp[I + 1] - a0;  // <= 32 on this path
+    a = a0 + lane;
+    if (uint32_t(lane) < na) {
+      const uint2 ac = __ldg(A.tco + a);
+      colocc = ac.y & 0xffffu;
+      rowocc = ac.y >> 16;
+      cur = __ldg(B.trp + ac.x);
+      end = __ldg(B.trp + ac.x + 1);
+    }
+    bt = cur < end ? __ldg(B.tco + cur) : make_uint2(kInf, 0);
+    bn = cur + 1 < end ? __ldg(B.tco + cur + 1) : make_uint2(kInf, 0);
+  }
+  __device__ __forceinline__ void advance(const TileMat& B) {
+    ++cur;
+    bt = bn;
+    bn = cur + 1 < end ? __ldg(B.tco + cur + 1) : make_uint2(kInf, 0);
+  }
+};
+
+// Counts per tile row (raw pairs, filtered pairs, segments) and, per CSR
+// row r of the panel, a staging bound: the sum over the row's output tiles
+// that cover row r (OR of the run's A row occupancy) of the run's column
+// span (OR of its B column occupancy).
+__global__ void __launch_bounds__(256) panel_count_kernel(TileMat A, TileMat B, int64_t rows,
+                                                         uint32_t* __restrict__ row_np,
+                                                         uint32_t* __restrict__ row_ns,
+                                                         uint32_t* __restrict__ row_raw,
+                                                         uint32_t* __restrict__ row_bound) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t I = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (I >= A.tile_rows) return;
+  Merge m;
+  uint32_t a;
+  m.start(A, B, I, lane, a);
+  const uint32_t raw_len = m.end - m.cur;  // raw pairs of this A tile (pipeline.cpp:52-58)
+  uint32_t np = 0, ns = 0, bound = 0;
+  while (true) {
+    const uint32_t J = __reduce_min_sync(kFull, m.bt.x);
+    if (J == kInf) break;
+    const bool take = m.bt.x == J;
+    const bool pass = take && (m.colocc & (m.bt.y >> 16)) != 0u;
+    const unsigned pb = __ballot_sync(kFull, pass);
+    if (pb) {
+      const uint32_t ro = __reduce_or_sync(kFull, pass ? m.rowocc : 0u);
+      const uint32_t co = __reduce_or_sync(kFull, pass ? (m.bt.y & 0xffffu) : 0u);
+      bound += ((ro >> (lane & 15)) & 1u) * __popc(co);  // lane r: row r
+      np += __popc(pb);
+      ++ns;
+    }
+    if (take) m.advance(B);
+  }
+  const uint32_t rw = __reduce_add_sync(kFull, raw_len);
+  if (lane == 0) {
+    row_np[I] = np;
+    row_ns[I] = ns;
+    row_raw[I] = rw;
+  }
+  const int64_t row = int64_t(I) * 16 + lane;
+  if (lane < 16 && row < rows) row_bound[row] = bound;
+}
+
+constexpr int kSA = 17;    // padded row stride of the ordered A scratch tile
+constexpr int kSRow = 24;  // row stride of the ordered B scratch tile
+
+template <bool kOrdered>
+__global__ void __launch_bounds__(256, 4) panel_numeric_kernel(TileMat A, TileMat B, int64_t rows,
+                                                              const uint32_t* __restrict__ row_stage,
+                                                              float* __restrict__ sval,
+                                                              int32_t* __restrict__ scol,
+                                                              int64_t* __restrict__ rowcnt,
+                                                              unsigned long long* __restrict__ counted) {
+  __shared__ __align__(16) uint4 s_meta[8][32];
+  __shared__ float sA[kOrdered ? 8 : 1][16 * kSA];
+  __shared__ float sB[kOrdered ? 8 : 1][16 * kSRow];
+  const int lane = threadIdx.x & 31;
+  const int w = threadIdx.x >> 5;
+  const uint32_t I = blockIdx.x * 8 + w;
+  if (I >= A.tile_rows) return;
+  const uint4* cA = A.chunk[kRoleA];
+  const uint4* cB = B.chunk[kRoleB];
+  const unsigned lt = lanemask_lt(), bit = 1u << lane;
+  const LaneLayout L(lane);
+  Merge m;
+  uint32_t a;
+  m.start(A, B, I, lane, a);
+  const uint2 am = m.cur < m.end ? __ldg(A.meta[kRoleA] + a) : make_uint2(0, 0);
+  const int64_t row = int64_t(I) * 16 + (lane & 15);
+  const bool row_ok = lane < 16 && row < rows;
+  uint32_t wpos = row_ok ? __ldg(row_stage + row) : 0u;  // lane r: next staging slot of row r
+  const uint32_t wstart = wpos;
+  uint32_t nstruct = 0;
+  while (true) {
+    const uint32_t J = __reduce_min_sync(kFull, m.bt.x);
+    if (J == kInf) break;
+    const bool take = m.bt.x == J;
+    const bool pass = take && (m.colocc & (m.bt.y >> 16)) != 0u;
+    const unsigned pb = __ballot_sync(kFull, pass);
+    if (pb) {
+      // the run's operand metas, in ascending k (lane) order
+      if (pass) {
+        const uint2 bm = __ldg(B.meta[kRoleB] + m.cur);
+        s_meta[w][__popc(pb & lt)] = make_uint4(am.x, am.y, bm.x, bm.y);
+      }
+      const uint32_t n = __popc(pb);
+      if (n & 1u) s_meta[w][n] = make_uint4(0, 0, 0, 0);  // pad the last pair of two
+      __syncwarp();
+      float acc[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+      if (!kOrdered) {
+        uint32_t sac[2][2] = {{0u, 0u}, {0u, 0u}};
+        for (uint32_t u = 0; u < n; u += 2) {  // the zero pad adds exact zeros
+          const uint4 m0 = s_meta[w][u], m1 = s_meta[w][u + 1];
+          const uint4 fa0 = load_chunk(cA, m0.x, m0.y, lt, bit), fb0 = load_chunk(cB, m0.z, m0.w, lt, bit);
+          const uint4 fa1 = load_chunk(cA, m1.x, m1.y, lt, bit), fb1 = load_chunk(cB, m1.z, m1.w, lt, bit);
+          mma16816(acc[0], fa0, fb0.x, fb0.y);
+          mma16816(acc[1], fa0, fb0.z, fb0.w);
+          const uint4 xa0 = nz_h2(fa0), xb0 = nz_h2(fb0);
+          mma16816_h(sac[0], xa0, xb0.x, xb0.y);
+          mma16816_h(sac[1], xa0, xb0.z, xb0.w);
+          mma16816(acc[0], fa1, fb1.x, fb1.y);
+          mma16816(acc[1], fa1, fb1.z, fb1.w);
+          const uint4 xa1 = nz_h2(fa1), xb1 = nz_h2(fb1);
+          mma16816_h(sac[0], xa1, xb1.x, xb1.y);
+          mma16816_h(sac[1], xa1, xb1.z, xb1.w);
+        }
+        nstruct += count_nz_h2(sac[0][0]) + count_nz_h2(sac[0][1]) + count_nz_h2(sac[1][0]) +
+                   count_nz_h2(sac[1][1]);
+      } else {
+        bool snz[2][4] = {{false, false, false, false}, {false, false, false, false}};
+        for (uint32_t u = 0; u < n; ++u) {
+          const uint4 mt = s_meta[w][u];
+          // expand_tile (kernels.cpp:17-26): every lane writes all 8 of its slots
+#pragma unroll
+          for (int role = 0; role < 2; ++role) {
+            const uint4 ch = role == kRoleA ? load_chunk(cA, mt.x, mt.y, lt, bit)
+                                            : load_chunk(cB, mt.z, mt.w, lt, bit);
+            const uint32_t regs[4] = {ch.x, role == kRoleA ? ch.y : ch.z, role == kRoleA ? ch.z : ch.y, ch.w};
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              int r, c;
+              rc_of(role, lane, j, r, c);
+              const float v = __half2float(__ushort_as_half(uint16_t(regs[j >> 1] >> (16 * (j & 1)))));
+              if (role == kRoleA)
+                sA[w][r * kSA + c] = v;
+              else
+                sB[w][r * kSRow + c] = v;
+            }
+          }
+          __syncwarp();
+          // tile_mm_reference (kernels.cpp:28-38): k ascending, no FMA; an
+          // exact binary16 x binary16 product is nonzero iff both factors are
+#pragma unroll
+          for (int h = 0; h < 2; ++h)
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const int r = L.g + 8 * (i >> 1), c = 2 * L.t + (i & 1) + 8 * h;
+              float x = acc[h][i];
+              bool nz = snz[h][i];
+#pragma unroll
+              for (int kk = 0; kk < 16; ++kk) {
+                const float pr = __fmul_rn(sA[w][r * kSA + kk], sB[w][kk * kSRow + c]);
+                nz |= pr != 0.0f;
+                x = __fadd_rn(x, pr);
+              }
+              acc[h][i] = x;
+              snz[h][i] = nz;
+            }
+          __syncwarp();
+        }
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+          for (int i = 0; i < 4; ++i) nstruct += snz[h][i];
+      }
+      // finalize_segment: bitmap = accumulators != 0 (cancelled slots and -0
+      // drop: compact()); row r's entries append to row r's staging region
+      unsigned Bal[2][4];
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) Bal[h][i] = __ballot_sync(kFull, acc[h][i] != 0.0f);
+      const unsigned rm = row_mask_from_ballots(Bal, lane);  // row lane & 15
+      const uint32_t pg = __shfl_sync(kFull, wpos, L.g), pg8 = __shfl_sync(kFull, wpos, L.g + 8);
+      const uint32_t mg = __shfl_sync(kFull, rm, L.g), mg8 = __shfl_sync(kFull, rm, L.g + 8);
+      const int32_t cj = int32_t(J * 16u) + 2 * L.t;
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const uint32_t p = q ? pg8 : pg, mr = q ? mg8 : mg;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const float v0 = acc[h][2 * q], v1 = acc[h][2 * q + 1];
+          const uint32_t e0 = p + __popc(mr & L.cm[h]);
+          if (v0 != 0.0f) {
+            sval[e0] = v0;
+            scol[e0] = cj + 8 * h;
+          }
+          if (v1 != 0.0f) {
+            const uint32_t e1 = e0 + (v0 != 0.0f);
+            sval[e1] = v1;
+            scol[e1] = cj + 8 * h + 1;
+          }
+        }
+      }
+      if (lane < 16) wpos += __popc(rm);
+      __syncwarp();  // s_meta is rewritten by the next run
+    }
+    if (take) m.advance(B);
+  }
+  if (row_ok) rowcnt[row] = int64_t(wpos - wstart);
+  nstruct = __reduce_add_sync(kFull, nstruct);
+  if (lane == 0 && nstruct) atomicAdd(counted, (unsigned long long)nstruct);
+}
+
+// Staging rows -> CSR: warp per panel, lanes over the panel's output
+// positions (the 16 rows are consecutive in the CSR), each taken from its
+// row's staging region.  Non-finite values raise kErrPrecision
+// (finalize_segment, kernels.cpp:115-127).
+__global__ void __launch_bounds__(256) panel_copy_kernel(int64_t rows, uint32_t tile_rows,
+                                                        const uint32_t* __restrict__ row_stage,
+                                                        const int64_t* __restrict__ row_ptr,
+                                                        const float* __restrict__ sval,
+                                                        const int32_t* __restrict__ scol,
+                                                        int32_t* __restrict__ col,
+                                                        float* __restrict__ val,
+                                                        unsigned* __restrict__ err_flag) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t I = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (I >= tile_rows) return;
+  const int64_t r0 = int64_t(I) * 16;
+  const int64_t r1 = r0 + 16 < rows ? r0 + 16 : rows;
+  const int64_t base = row_ptr[r0];
+  const uint32_t T = uint32_t(row_ptr[r1] - base);
+  const int64_t row = r0 + (lane & 15);
+  // lane r: offset of row r within the panel (rows past the end: T)
+  const uint32_t off = row < r1 ? uint32_t(row_ptr[row] - base) : T;
+  const uint32_t src0 = row < r1 ? row_stage[row] : 0u;
+  bool bad = false;
+  for (uint32_t q0 = 0; q0 < T; q0 += 32) {
+    const uint32_t q = q0 + lane;
+    int r = 0;  // last row whose offset is <= q (empty rows resolve to the next one)
+#pragma unroll
+    for (int b = 8; b > 0; b >>= 1) {
+      const uint32_t v = __shfl_sync(kFull, off, r + b);
+      if (v <= q) r += b;
+    }
+    const uint32_t o = __shfl_sync(kFull, off, r), sr = __shfl_sync(kFull, src0, r);
+    if (q < T) {
+      const uint32_t k = sr + (q - o);
+      const float x = __ldg(sval + k);
+      bad |= !isfinite(x);
+      col[base + q] = __ldg(scol + k);
+      val[base + q] = x;
+    }
+  }
+  if (__any_sync(kFull, bad) && lane == 0) atomicOr(err_flag, unsigned(kErrPrecision));
+}
+
+}  // namespace
+
+void launch_panel_count(const TileMat& A, const TileMat& B, int64_t rows, uint32_t* row_np,
+                        uint32_t* row_ns, uint32_t* row_raw, uint32_t* row_bound, cudaStream_t st) {
+  const unsigned blocks = (A.tile_rows + 7) / 8;
+  if (blocks == 0) return;
+  panel_count_kernel<<<blocks, 256, 0, st>>>(A, B, rows, row_np, row_ns, row_raw, row_bound);
+}
+
+void launch_panel_numeric(const TileMat& A, const TileMat& B, int64_t rows, const uint32_t* row_stage,
+                          float* sval, int32_t* scol, int64_t* rowcnt, unsigned long long* counted,
+                          int mode, cudaStream_t st) {
+  const unsigned blocks = (A.tile_rows + 7) / 8;
+  if (blocks == 0) return;
+  if (mode == 1)
+    panel_numeric_kernel<true><<<blocks, 256, 0, st>>>(A, B, rows, row_stage, sval, scol, rowcnt, counted);
+  else
+    panel_numeric_kernel<false><<<blocks, 256, 0, st>>>(A, B, rows, row_stage, sval, scol, rowcnt, counted);
+}
+
+void launch_panel_copy(int64_t rows, uint32_t tile_rows, const uint32_t* row_stage, const int64_t* row_ptr,
+                       const float* sval, const int32_t* scol, int32_t* col, float* val,
+                       unsigned* err_flag, cudaStream_t st) {
+  const unsigned blocks = (tile_rows + 7) / 8;
+  if (blocks == 0) return;
+  panel_copy_kernel<<<blocks, 256, 0, st>>>(rows, tile_rows, row_stage, row_ptr, sval, scol, col, val,
+                                            err_flag);
+}
+
+}  // namespace tsg

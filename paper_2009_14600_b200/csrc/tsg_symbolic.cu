@@ -10,24 +10,14 @@
 // popc(OR of A row occupancy) * popc(OR of B column occupancy) -- every
 // realised output slot of the segment lies in that rectangle.
 //
-// Two ways to build the task list; both yield the identical TaskList (pairs
-// sorted by (out row, out col, k), one segment per output tile):
-//
-//  * light rows (every A tile row has <= 32 tiles -- FEM27, Poisson, AMG):
-//    one warp per tile row, lane l owns A tile (I, k_l) and walks B tile row
-//    k_l (sorted by J).  Each step takes the minimum pending J (REDUX): the
-//    lanes holding it are exactly that output tile's pairs, already in
-//    ascending k (lane order).  This is a 32-way merge -- the sort the
-//    reference does with std::sort on (row, col, k) keys happens in
-//    registers, and segments fall out directly.  Count pass + prefix sums +
-//    fill pass; the zero-product filter is applied per pair on the fly.
-//
-//  * general rows: fused enumerate+filter (count, scan, fill; raw pairs are
-//    never materialised), a stable segmented radix sort by
-//    output tile column per tile row (tsg_api.cu), then segment heads.
-//    One warp per 32 consecutive A tiles flattens their raw pairs and
-//    load-balances them across lanes with a shuffle binary search, so
-//    skewed B tile rows (R-MAT) keep all lanes busy.
+// This is the general path (some tile row of A has more than 32 tiles --
+// R-MAT, the rectangular product, the second AMG stage); light rows never
+// materialise a task list (tsg_panel.cu).  Fused enumerate+filter (count,
+// scan, fill; raw pairs are never materialised), a stable
+// segmented radix sort by output tile column per tile row (tsg_api.cu),
+// then segment heads.  One warp per 32 consecutive A tiles flattens their
+// raw pairs and load-balances them across lanes with a shuffle binary
+// search, so skewed B tile rows (R-MAT) keep all lanes busy.
 //
 #include "tsg_kernels.cuh"
 
@@ -36,86 +26,6 @@ namespace tsg {
 namespace {
 
 constexpr uint32_t kInf = 0xffffffffu;
-
-// ---------------------------------------------------------------- light rows
-template <bool kFill>
-__global__ void __launch_bounds__(256) merge_kernel(TileMat A, TileMat B,
-                                                   uint32_t* __restrict__ row_np,
-                                                   uint32_t* __restrict__ row_ns,
-                                                   uint32_t* __restrict__ row_nb,
-                                                   uint32_t* __restrict__ row_raw,
-                                                   const uint32_t* __restrict__ row_pair_off,
-                                                   const uint32_t* __restrict__ row_stage_off,
-                                                   TaskList tl) {
-  const int lane = threadIdx.x & 31;
-  const uint32_t I = blockIdx.x * 8 + (threadIdx.x >> 5);
-  if (I >= A.tile_rows) return;
-  const uint32_t a0 = A.trp[I];
-  const uint32_t na = A.trp[I + 1] - a0;  // <= 32 on this path
-  uint32_t colocc = 0, rowocc = 0, cur = 0, end = 0;
-  uint2 am = make_uint2(0, 0);
-  if (lane < na) {
-    const uint32_t a = a0 + lane;
-    const uint2 ac = __ldg(A.tco + a);
-    colocc = ac.y & 0xffffu;
-    rowocc = ac.y >> 16;
-    cur = __ldg(B.trp + ac.x);
-    end = __ldg(B.trp + ac.x + 1);
-    if (kFill) am = __ldg(A.meta[kRoleA] + a);
-  }
-  const uint32_t raw_len = end - cur;  // raw pairs of this A tile (pipeline.cpp:52-58)
-  uint2 bt = cur < end ? __ldg(B.tco + cur) : make_uint2(kInf, 0);
-  uint2 bn = cur + 1 < end ? __ldg(B.tco + cur + 1) : make_uint2(kInf, 0);
-  uint32_t np = 0, ns = 0, nb = 0;
-  uint32_t pair_base = 0, seg_base = 0, stage_base = 0;
-  if (kFill) {
-    pair_base = row_pair_off[I];
-    seg_base = tl.seg_row_ptr[I];
-    stage_base = row_stage_off[I];
-  }
-  while (true) {
-    const uint32_t J = __reduce_min_sync(kFull, bt.x);
-    if (J == kInf) break;
-    const bool take = bt.x == J;
-    const bool pass = take && (colocc & (bt.y >> 16)) != 0u;
-    const unsigned pb = __ballot_sync(kFull, pass);
-    if (pb) {
-      // staging bound: rows any A tile of the run occupies x columns any B tile occupies
-      const uint32_t ro = __reduce_or_sync(kFull, pass ? rowocc : 0u);
-      const uint32_t co = __reduce_or_sync(kFull, pass ? (bt.y & 0xffffu) : 0u);
-      if (kFill) {
-        if (pass) {
-          const uint32_t pos = pair_base + np + __popc(pb & lanemask_lt());
-          const uint2 bm = __ldg(B.meta[kRoleB] + cur);
-          tl.pmeta[pos] = make_uint4(am.x, am.y, bm.x, bm.y);
-        }
-        if (lane == 0) {
-          const uint32_t s = seg_base + ns;
-          tl.seg_off[s] = pair_base + np;
-          tl.seg_col[s] = J;
-          tl.stage_off[s] = stage_base + nb;
-        }
-      }
-      np += __popc(pb);
-      nb += __popc(ro) * __popc(co);
-      ++ns;
-    }
-    if (take) {
-      ++cur;
-      bt = bn;
-      bn = cur + 1 < end ? __ldg(B.tco + cur + 1) : make_uint2(kInf, 0);
-    }
-  }
-  if (!kFill) {
-    const uint32_t rw = __reduce_add_sync(kFull, raw_len);
-    if (lane == 0) {
-      row_np[I] = np;
-      row_ns[I] = ns;
-      row_nb[I] = nb;
-      row_raw[I] = rw;
-    }
-  }
-}
 
 // ------------------------------------------------------------- general rows
 template <bool kFill>
@@ -265,22 +175,6 @@ __global__ void seg_stage_kernel(TaskList tl, const uint32_t* __restrict__ pair_
 }
 
 }  // namespace
-
-void launch_merge_count(const TileMat& A, const TileMat& B, uint32_t* row_np, uint32_t* row_ns,
-                        uint32_t* row_nb, uint32_t* row_raw, cudaStream_t st) {
-  const unsigned blocks = (A.tile_rows + 7) / 8;
-  if (blocks == 0) return;
-  merge_kernel<false><<<blocks, 256, 0, st>>>(A, B, row_np, row_ns, row_nb, row_raw, nullptr, nullptr,
-                                              TaskList{});
-}
-
-void launch_merge_fill(const TileMat& A, const TileMat& B, const uint32_t* row_pair_off,
-                       const uint32_t* row_stage_off, TaskList& tl, cudaStream_t st) {
-  const unsigned blocks = (A.tile_rows + 7) / 8;
-  if (blocks == 0) return;
-  merge_kernel<true><<<blocks, 256, 0, st>>>(A, B, nullptr, nullptr, nullptr, nullptr, row_pair_off,
-                                             row_stage_off, tl);
-}
 
 void launch_enum_count(const TileMat& A, const TileMat& B, uint64_t tA, uint32_t* tile_cnt,
                        unsigned long long* raw_total, cudaStream_t st) {
