@@ -447,16 +447,15 @@ void spgemm_impl(tsg_ctx* ctx, const tsg_csr* Ain, const tsg_csr* Bin, tsg_csr_o
     record(ctx, timing, 2);
     record(ctx, timing, 3);  // the merge is the sort: no separate phase
     record(ctx, timing, 4);  // the counting pass is fused into the numeric pass
-    float* sval = static_cast<float*>(arena(stage_total * 8));
-    int32_t* scol = reinterpret_cast<int32_t*>(sval + stage_total);
+    uint2* stage = static_cast<uint2*>(arena(stage_total * sizeof(uint2)));
     if (timing) TSG_CUDA(cudaEventRecord(ctx->kev[0], s));
-    launch_panel_numeric(TA, TB, rows, row_stage, sval, scol, rowcnt, counted_d, opt.mode, s);
+    launch_panel_numeric(TA, TB, rows, row_stage, stage, rowcnt, counted_d, opt.mode, s);
     check_launch(ctx);
     if (timing) TSG_CUDA(cudaEventRecord(ctx->kev[1], s));
     record(ctx, timing, 5);
     finish_rows();
     if (timing) TSG_CUDA(cudaEventRecord(ctx->kev[2], s));
-    launch_panel_copy(rows, TA.tile_rows, row_stage, d_rp, sval, scol, d_col, d_val, err_flag, s);
+    launch_panel_copy(rows, TA.tile_rows, row_stage, d_rp, stage, d_col, d_val, err_flag, s);
     check_launch(ctx);
     if (timing) TSG_CUDA(cudaEventRecord(ctx->kev[3], s));
     record(ctx, timing, 6);

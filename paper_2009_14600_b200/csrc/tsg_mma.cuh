@@ -67,5 +67,21 @@ struct LaneLayout {
   }
 };
 
+// Realised row masks of an m16n16 accumulator tile, computed inside the
+// lane group that holds the rows: returns (row g mask) | (row g+8 mask) << 16
+// (bit c = column c nonzero), identical in the four lanes 4g .. 4g+3.
+__device__ __forceinline__ uint32_t group_row_masks(const float (&acc)[2][4], int t) {
+  uint32_t x = 0;
+#pragma unroll
+  for (int h = 0; h < 2; ++h)
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      if (acc[h][i] != 0.0f) x |= 1u << ((i & 1) + 8 * h + 16 * (i >> 1));
+  x <<= 2 * t;
+  x |= __shfl_xor_sync(kFull, x, 1);
+  x |= __shfl_xor_sync(kFull, x, 2);
+  return x;
+}
+
 }  // namespace
 }  // namespace tsg

@@ -110,11 +110,12 @@ constexpr int kSRow = 24;  // row stride of the ordered B scratch tile
 template <bool kOrdered>
 __global__ void __launch_bounds__(256, 4) panel_numeric_kernel(TileMat A, TileMat B, int64_t rows,
                                                               const uint32_t* __restrict__ row_stage,
-                                                              float* __restrict__ sval,
-                                                              int32_t* __restrict__ scol,
+                                                              uint2* __restrict__ stage,
                                                               int64_t* __restrict__ rowcnt,
                                                               unsigned long long* __restrict__ counted) {
   __shared__ __align__(16) uint4 s_meta[8][32];
+  // TENSOR: [A tile of the row][lane] -> chunk index (ORDERED keeps the metas)
+  __shared__ uint32_t s_aidx[kOrdered ? 1 : 8][32][32];
   __shared__ float sA[kOrdered ? 8 : 1][16 * kSA];
   __shared__ float sB[kOrdered ? 8 : 1][16 * kSRow];
   const int lane = threadIdx.x & 31;
@@ -128,11 +129,20 @@ __global__ void __launch_bounds__(256, 4) panel_numeric_kernel(TileMat A, TileMa
   Merge m;
   uint32_t a;
   m.start(A, B, I, lane, a);
-  const uint2 am = m.cur < m.end ? __ldg(A.meta[kRoleA] + a) : make_uint2(0, 0);
-  const int64_t row = int64_t(I) * 16 + (lane & 15);
-  const bool row_ok = lane < 16 && row < rows;
-  uint32_t wpos = row_ok ? __ldg(row_stage + row) : 0u;  // lane r: next staging slot of row r
-  const uint32_t wstart = wpos;
+  const uint32_t na = A.trp[I + 1] - A.trp[I];
+  const uint2 am = uint32_t(lane) < na ? __ldg(A.meta[kRoleA] + a) : make_uint2(0, 0);
+  if (!kOrdered) {
+    // this lane's chunk index in each of the row's A tiles (they are reused
+    // by every output tile of the row)
+    for (uint32_t l = 0; l < na; ++l) {
+      const uint32_t lm = __shfl_sync(kFull, am.x, l), base = __shfl_sync(kFull, am.y, l);
+      s_aidx[w][l][lane] = (lm & bit) ? base + __popc(lm & lt) : 0u;
+    }
+  }
+  // lanes of group g track the staging cursors of rows g and g+8
+  const int64_t rg = int64_t(I) * 16 + L.g, rg8 = rg + 8;
+  uint32_t wg = rg < rows ? __ldg(row_stage + rg) : 0u, wg8 = rg8 < rows ? __ldg(row_stage + rg8) : 0u;
+  const uint32_t wg0 = wg, wg80 = wg8;
   uint32_t nstruct = 0;
   while (true) {
     const uint32_t J = __reduce_min_sync(kFull, m.bt.x);
@@ -141,21 +151,24 @@ __global__ void __launch_bounds__(256, 4) panel_numeric_kernel(TileMat A, TileMa
     const bool pass = take && (m.colocc & (m.bt.y >> 16)) != 0u;
     const unsigned pb = __ballot_sync(kFull, pass);
     if (pb) {
-      // the run's operand metas, in ascending k (lane) order
+      // the run's pairs, in ascending k (lane) order: {A tile of the row, B meta}
       if (pass) {
         const uint2 bm = __ldg(B.meta[kRoleB] + m.cur);
-        s_meta[w][__popc(pb & lt)] = make_uint4(am.x, am.y, bm.x, bm.y);
+        s_meta[w][__popc(pb & lt)] = kOrdered ? make_uint4(am.x, am.y, bm.x, bm.y)
+                                              : make_uint4(uint32_t(lane), 0u, bm.x, bm.y);
       }
       const uint32_t n = __popc(pb);
-      if (n & 1u) s_meta[w][n] = make_uint4(0, 0, 0, 0);  // pad the last pair of two
       __syncwarp();
       float acc[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
       if (!kOrdered) {
         uint32_t sac[2][2] = {{0u, 0u}, {0u, 0u}};
-        for (uint32_t u = 0; u < n; u += 2) {  // the zero pad adds exact zeros
-          const uint4 m0 = s_meta[w][u], m1 = s_meta[w][u + 1];
-          const uint4 fa0 = load_chunk(cA, m0.x, m0.y, lt, bit), fb0 = load_chunk(cB, m0.z, m0.w, lt, bit);
-          const uint4 fa1 = load_chunk(cA, m1.x, m1.y, lt, bit), fb1 = load_chunk(cB, m1.z, m1.w, lt, bit);
+        for (uint32_t u = 0; u < n; u += 2) {
+          const uint4 m0 = s_meta[w][u];
+          const uint4 m1 = u + 1 < n ? s_meta[w][u + 1] : make_uint4(0, 0, 0, 0);
+          const uint4 fa0 = __ldg(cA + s_aidx[w][m0.x][lane]), fb0 = load_chunk(cB, m0.z, m0.w, lt, bit);
+          // an absent second pair reads the zero chunk: adds exact zeros
+          const uint4 fa1 = __ldg(cA + (u + 1 < n ? s_aidx[w][m1.x][lane] : 0u));
+          const uint4 fb1 = load_chunk(cB, m1.z, m1.w, lt, bit);
           mma16816(acc[0], fa0, fb0.x, fb0.y);
           mma16816(acc[1], fa0, fb0.z, fb0.w);
           const uint4 xa0 = nz_h2(fa0), xb0 = nz_h2(fb0);
@@ -218,39 +231,29 @@ __global__ void __launch_bounds__(256, 4) panel_numeric_kernel(TileMat A, TileMa
       }
       // finalize_segment: bitmap = accumulators != 0 (cancelled slots and -0
       // drop: compact()); row r's entries append to row r's staging region
-      unsigned Bal[2][4];
-#pragma unroll
-      for (int h = 0; h < 2; ++h)
-#pragma unroll
-        for (int i = 0; i < 4; ++i) Bal[h][i] = __ballot_sync(kFull, acc[h][i] != 0.0f);
-      const unsigned rm = row_mask_from_ballots(Bal, lane);  // row lane & 15
-      const uint32_t pg = __shfl_sync(kFull, wpos, L.g), pg8 = __shfl_sync(kFull, wpos, L.g + 8);
-      const uint32_t mg = __shfl_sync(kFull, rm, L.g), mg8 = __shfl_sync(kFull, rm, L.g + 8);
+      const uint32_t rmg = group_row_masks(acc, L.t);  // rows g | g+8 << 16
       const int32_t cj = int32_t(J * 16u) + 2 * L.t;
 #pragma unroll
       for (int q = 0; q < 2; ++q) {
-        const uint32_t p = q ? pg8 : pg, mr = q ? mg8 : mg;
+        const uint32_t p = q ? wg8 : wg, mr = q ? (rmg >> 16) : (rmg & 0xffffu);
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           const float v0 = acc[h][2 * q], v1 = acc[h][2 * q + 1];
           const uint32_t e0 = p + __popc(mr & L.cm[h]);
-          if (v0 != 0.0f) {
-            sval[e0] = v0;
-            scol[e0] = cj + 8 * h;
-          }
-          if (v1 != 0.0f) {
-            const uint32_t e1 = e0 + (v0 != 0.0f);
-            sval[e1] = v1;
-            scol[e1] = cj + 8 * h + 1;
-          }
+          if (v0 != 0.0f) stage[e0] = make_uint2(__float_as_uint(v0), uint32_t(cj + 8 * h));
+          if (v1 != 0.0f) stage[e0 + (v0 != 0.0f)] = make_uint2(__float_as_uint(v1), uint32_t(cj + 8 * h + 1));
         }
       }
-      if (lane < 16) wpos += __popc(rm);
+      wg += __popc(rmg & 0xffffu);
+      wg8 += __popc(rmg >> 16);
       __syncwarp();  // s_meta is rewritten by the next run
     }
     if (take) m.advance(B);
   }
-  if (row_ok) rowcnt[row] = int64_t(wpos - wstart);
+  if (L.t == 0) {
+    if (rg < rows) rowcnt[rg] = int64_t(wg - wg0);
+    if (rg8 < rows) rowcnt[rg8] = int64_t(wg8 - wg80);
+  }
   nstruct = __reduce_add_sync(kFull, nstruct);
   if (lane == 0 && nstruct) atomicAdd(counted, (unsigned long long)nstruct);
 }
@@ -262,8 +265,7 @@ __global__ void __launch_bounds__(256, 4) panel_numeric_kernel(TileMat A, TileMa
 __global__ void __launch_bounds__(256) panel_copy_kernel(int64_t rows, uint32_t tile_rows,
                                                         const uint32_t* __restrict__ row_stage,
                                                         const int64_t* __restrict__ row_ptr,
-                                                        const float* __restrict__ sval,
-                                                        const int32_t* __restrict__ scol,
+                                                        const uint2* __restrict__ stage,
                                                         int32_t* __restrict__ col,
                                                         float* __restrict__ val,
                                                         unsigned* __restrict__ err_flag) {
@@ -289,10 +291,10 @@ __global__ void __launch_bounds__(256) panel_copy_kernel(int64_t rows, uint32_t 
     }
     const uint32_t o = __shfl_sync(kFull, off, r), sr = __shfl_sync(kFull, src0, r);
     if (q < T) {
-      const uint32_t k = sr + (q - o);
-      const float x = __ldg(sval + k);
+      const uint2 e = __ldg(stage + sr + (q - o));
+      const float x = __uint_as_float(e.x);
       bad |= !isfinite(x);
-      col[base + q] = __ldg(scol + k);
+      col[base + q] = int32_t(e.y);
       val[base + q] = x;
     }
   }
@@ -309,23 +311,21 @@ void launch_panel_count(const TileMat& A, const TileMat& B, int64_t rows, uint32
 }
 
 void launch_panel_numeric(const TileMat& A, const TileMat& B, int64_t rows, const uint32_t* row_stage,
-                          float* sval, int32_t* scol, int64_t* rowcnt, unsigned long long* counted,
-                          int mode, cudaStream_t st) {
+                          uint2* stage, int64_t* rowcnt, unsigned long long* counted, int mode,
+                          cudaStream_t st) {
   const unsigned blocks = (A.tile_rows + 7) / 8;
   if (blocks == 0) return;
   if (mode == 1)
-    panel_numeric_kernel<true><<<blocks, 256, 0, st>>>(A, B, rows, row_stage, sval, scol, rowcnt, counted);
+    panel_numeric_kernel<true><<<blocks, 256, 0, st>>>(A, B, rows, row_stage, stage, rowcnt, counted);
   else
-    panel_numeric_kernel<false><<<blocks, 256, 0, st>>>(A, B, rows, row_stage, sval, scol, rowcnt, counted);
+    panel_numeric_kernel<false><<<blocks, 256, 0, st>>>(A, B, rows, row_stage, stage, rowcnt, counted);
 }
 
 void launch_panel_copy(int64_t rows, uint32_t tile_rows, const uint32_t* row_stage, const int64_t* row_ptr,
-                       const float* sval, const int32_t* scol, int32_t* col, float* val,
-                       unsigned* err_flag, cudaStream_t st) {
+                       const uint2* stage, int32_t* col, float* val, unsigned* err_flag, cudaStream_t st) {
   const unsigned blocks = (tile_rows + 7) / 8;
   if (blocks == 0) return;
-  panel_copy_kernel<<<blocks, 256, 0, st>>>(rows, tile_rows, row_stage, row_ptr, sval, scol, col, val,
-                                            err_flag);
+  panel_copy_kernel<<<blocks, 256, 0, st>>>(rows, tile_rows, row_stage, row_ptr, stage, col, val, err_flag);
 }
 
 }  // namespace tsg

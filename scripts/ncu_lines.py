@@ -6,6 +6,8 @@ import csv, re, subprocess, sys, tempfile, os, glob
 from collections import Counter
 
 rep, kname, obj = sys.argv[1], sys.argv[2], sys.argv[3]
+# "ncu-regex::mangled-substring" when the two names differ (template kernels)
+kname, dname = (kname.split("::", 1) + [None])[:2] if "::" in kname else (kname, kname)
 top = int(sys.argv[4]) if len(sys.argv) > 4 else 25
 src = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass",
                       "--kernel-name", f"regex:{kname}"], capture_output=True, text=True).stdout
@@ -26,12 +28,12 @@ dis = subprocess.run(["nvdisasm", "-g", "-c", cub], capture_output=True, text=Tr
 lines, cur, infn = {}, None, False
 for ln in dis.splitlines():
     if ln.startswith("//---------------------"):
-        infn = kname in ln
+        infn = dname in ln
     if not infn:
         continue
-    m = re.search(r'line (\d+)', ln)
+    m = re.search(r'File "([^"]+)", line (\d+)', ln)
     if "//## File" in ln and m:
-        cur = int(m.group(1))
+        cur = (m.group(1), int(m.group(2)))
     m2 = re.match(r'\s+/\*([0-9a-f]{4,})\*/', ln)
     if m2 and cur is not None:
         lines[int(m2.group(1), 16)] = cur
@@ -40,9 +42,14 @@ for a, (n, s) in execs.items():
     c[lines.get(a, -1)] += n
     w[lines.get(a, -1)] += s
 tot, tw = sum(c.values()), max(1, sum(w.values()))
-path = re.search(r'File "([^"]+)"', dis)
-srcl = open(path.group(1)).read().splitlines() if path else []
+srcs = {}
 for l, n in c.most_common(top):
-    txt = srcl[l - 1].strip()[:70] if 0 < l <= len(srcl) else "?"
-    print(f"{n:11d} {100*n/tot:5.1f}% stall {100*w[l]/tw:5.1f}%  L{l:4d} {txt}")
+    txt, tag = "?", "?"
+    if l != -1:
+        f, ln_ = l
+        if f not in srcs:
+            srcs[f] = open(f).read().splitlines() if os.path.exists(f) else []
+        txt = srcs[f][ln_ - 1].strip()[:64] if 0 < ln_ <= len(srcs[f]) else "?"
+        tag = f"{os.path.basename(f)[:14]}:{ln_}"
+    print(f"{n:11d} {100*n/tot:5.1f}% stall {100*w[l]/tw:5.1f}%  {tag:20s} {txt}")
 print("total", tot)
