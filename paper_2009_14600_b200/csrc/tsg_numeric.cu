@@ -280,17 +280,29 @@ __global__ void __launch_bounds__(256) numeric_thin_kernel(TaskList tl, const ui
               if (b == 0.0f) continue;
               const uint32_t want = uint32_t(r << 4 | c);
               const float pr2 = __fmul_rn(a, b);
+              // slot list kept sorted (row-major): position = slots below
+              int pos = 0;
               bool hit = false;
 #pragma unroll
-              for (int i = 0; i < kThin; ++i)
-                if (slot[i] == want) {
-                  acc[i] = __fadd_rn(acc[i], pr2);
-                  hit = true;
-                }
-              if (!hit) {  // new structural slot (n < kThin: the bound holds it)
+              for (int i = 0; i < kThin; ++i) {
+                if (i >= n) break;
+                pos += slot[i] < want;
+                hit |= slot[i] == want;
+              }
+              if (hit) {
 #pragma unroll
                 for (int i = 0; i < kThin; ++i)
-                  if (i == n) {
+                  if (i == pos) acc[i] = __fadd_rn(acc[i], pr2);
+              } else {  // new structural slot (n < kThin: the bound holds it)
+#pragma unroll
+                for (int i = kThin - 1; i > 0; --i)
+                  if (i > pos && i <= n) {
+                    slot[i] = slot[i - 1];
+                    acc[i] = acc[i - 1];
+                  }
+#pragma unroll
+                for (int i = 0; i < kThin; ++i)
+                  if (i == pos) {
                     slot[i] = want;
                     acc[i] = __fadd_rn(0.0f, pr2);
                   }
@@ -301,24 +313,12 @@ __global__ void __launch_bounds__(256) numeric_thin_kernel(TaskList tl, const ui
         }
       }
       nstruct = uint32_t(n);
-      // row-major order: sorting network on (slot, value), empty slots (0xffff) last
-#pragma unroll
-      for (int i = 0; i < kThin; ++i)
-#pragma unroll
-        for (int j = 0; j + 1 < kThin - i; ++j)
-          if (slot[j] > slot[j + 1]) {
-            const uint32_t t = slot[j];
-            slot[j] = slot[j + 1];
-            slot[j + 1] = t;
-            const float v = acc[j];
-            acc[j] = acc[j + 1];
-            acc[j + 1] = v;
-          }
       uint32_t w[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // row masks, rows 2q | 2q+1 << 16
       uint32_t e = 0;
 #pragma unroll
       for (int i = 0; i < kThin; ++i) {
-        if (i < n && acc[i] != 0.0f) {  // realised (cancelled slots drop: compact())
+        if (i >= n) break;
+        if (acc[i] != 0.0f) {  // realised (cancelled slots drop: compact())
           const uint32_t r = slot[i] >> 4, bitpos = (slot[i] & 15u) + 16u * (r & 1u);
 #pragma unroll
           for (int q = 0; q < 8; ++q)
