@@ -278,18 +278,22 @@ def run_ours(args):
     peaks = json.loads((Path(ROOT) / "MEASURED_PEAKS.json").read_text()) if (Path(ROOT) / "MEASURED_PEAKS.json").exists() else {}
     peak = float(peaks.get("hbm_gbs", 6650.0))
     peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
-    # dominant kernel: the SEaC numeric kernel (largest single launch); its
-    # algorithmic bytes over its own CUDA-event duration
+    # dominant kernel: the fused numeric pass (light rows: panel_numeric_kernel,
+    # task list + counting + SEaC multiply + compaction of each tile row;
+    # general rows: the thin + warp numeric kernels); its SURVEY 8(d) numeric
+    # bytes over its own CUDA-event duration
     dom = "multiply"
     kms = phase_ms.get("numeric_kernel") or phase_ms.get(dom)
     achieved = bytes_[dom] / (kms * 1e-3) / 1e9 if kms else 0.0
-    traffic = None
-    prof = Path(ROOT) / "profiles" / "r01_ncu_full_fem27.json"
-    if args.config == "fem27" and world == 1 and prof.exists():
+    light = sd["sort"] * 1e3 < 0.05 if not chain else False
+    kname = "panel_numeric_kernel" if light else "numeric_thin_kernel+numeric_tc_kernel"
+    traffic, prof_name = None, f"profiles/r01_ncu_full_{args.config}.json"
+    prof = Path(ROOT) / prof_name
+    if world == 1 and prof.exists():
         kk = json.loads(prof.read_text())["kernels"]
-        for name, k in kk.items():
-            if name.startswith("numeric_tc_kernel"):
-                traffic = int(k["dram_read_bytes"] + k["dram_write_bytes"])
+        tot = [k["dram_read_bytes"] + k["dram_write_bytes"] for name, k in kk.items()
+               if any(name.startswith(x) for x in kname.split("+"))]
+        traffic = int(sum(tot)) if tot else None
 
     # ---- e2e: host CSR in (pinned), host CSR out, through the public API
     pin = []
@@ -350,11 +354,10 @@ def run_ours(args):
         "gpu_launches": int(launches),
         "gpu_launches_per_step": launches / max(1, args.steps),
         "phase_ms": {k: round(v, 4) for k, v in phase_ms.items()},
-        "roofline": {"bound": "hbm", "kernel": "numeric_tc_kernel (SEaC multiply)", "achieved": round(achieved, 1),
+        "roofline": {"bound": "hbm", "kernel": kname, "achieved": round(achieved, 1),
                      "peak": peak, "peak_source": peak_src, "unit": "GB/s", "frac": round(achieved / peak, 4),
                      "kernel_ms": round(kms, 4) if kms else None, "algorithmic_bytes": int(bytes_[dom]),
-                     "traffic": traffic, "traffic_source": "profiles/r01_ncu_full_fem27.json (ncu --set full)"
-                     if traffic else None},
+                     "traffic": traffic, "traffic_source": f"{prof_name} (ncu --set full)" if traffic else None},
         "clocks": clk.summary(),
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -6,6 +6,7 @@ usage: python scripts/ncu_json.py <report.ncu-rep> <out.json> "<source text>"
 """
 import csv
 import json
+import re
 import subprocess
 import sys
 
@@ -30,7 +31,9 @@ scale_bytes = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
 res = {"source": source, "kernels": {}}
 for v in rows[2:]:
     name = v[h.index("Kernel Name")]
-    name = name.split("(")[0].replace("void ", "").replace("unnamed>::", "").strip()
+    name = name.split("(")[0].replace("void ", "").replace("tsg::<unnamed>::", "").replace("<unnamed>::", "").strip()
+    if name.startswith("cub::"):
+        name = name.split("<")[0]
     d = {}
     for k, (m, sc) in keys.items():
         if m not in h:

@@ -1,0 +1,21 @@
+"""One spGEMM call on device-resident inputs of a bench config (for ncu
+captures: every kernel launched here belongs to that single call)."""
+import sys
+
+sys.path.insert(0, ".")
+import torch  # noqa: E402
+
+from paper_2009_14600_b200 import workloads as W  # noqa: E402
+from paper_2009_14600_b200.tilemul import Context  # noqa: E402
+
+cfg = sys.argv[1] if len(sys.argv) > 1 else "fem27"
+mode = sys.argv[2] if len(sys.argv) > 2 else "tensor"
+ctx = Context(device=0)
+mats = [M.to_device("cuda") for M in W.make(cfg)]
+torch.cuda.synchronize()
+if len(mats) == 3:
+    r = ctx.spgemm_chain(mats, out="device", mode=mode)
+else:
+    r = ctx.spgemm(mats[0], mats[1] if len(mats) > 1 else mats[0], out="device", mode=mode)
+torch.cuda.synchronize()
+print(cfg, r.stats["nnz_c"])
