@@ -55,6 +55,19 @@ struct DimensionError : Error {
 struct PrecisionError : Error {
   using Error::Error;
 };
+// input-side taxonomy of the reference front end (errors.hpp:14-33)
+struct ParseError : Error {
+  using Error::Error;
+};
+struct UnsupportedError : ParseError {
+  using ParseError::ParseError;
+};
+struct IoError : Error {
+  using Error::Error;
+};
+struct FormatError : Error {
+  using Error::Error;
+};
 
 inline void throw_status(int st, const std::string& msg) {
   switch (st) {
@@ -93,6 +106,9 @@ struct TiledMatrix {
   std::vector<TileEntry> tiles;
   std::vector<float> elements;
   std::uint64_t nnz() const { return elements.size(); }
+  std::uint64_t tile_rows() const { return (rows + kTileDim - 1) / kTileDim; }
+  std::uint64_t tile_cols() const { return (cols + kTileDim - 1) / kTileDim; }
+  friend bool operator==(const TiledMatrix&, const TiledMatrix&) = default;  // tile_format.hpp:54
 };
 
 struct PhaseTiming {
