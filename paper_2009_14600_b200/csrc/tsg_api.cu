@@ -32,6 +32,7 @@
 #include "tsg_kernels.cuh"
 
 namespace tsg {
+constexpr int kPipeChunks = 8;  // tile-row chunks of the pipelined host-output path
 int tuning_variant(const char* name, int dflt) {
   const char* v = std::getenv(name);
   return v ? std::atoi(v) : dflt;
@@ -48,6 +49,11 @@ struct tsg_ctx {
   uint64_t launches = 0;
   double last_phase_ms[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   double last_numeric_kernel_ms = 0, last_assemble_kernel_ms = 0;
+  // pipelined host output: a second stream for device->host slices, its events,
+  // and pinned slots for the chunk ends
+  cudaStream_t d2h = nullptr;
+  cudaEvent_t pipe_ev[tsg::kPipeChunks + 1] = {};
+  void* pinned_pipe = nullptr;
   cudaEvent_t ev[8] = {};
   cudaEvent_t kev[4] = {};  // bracket the numeric and assembly kernels alone
   // pinned host blocks released by tsg_free_csr, reused by later host outputs
@@ -371,6 +377,7 @@ void spgemm_impl(tsg_ctx* ctx, const tsg_csr* Ain, const tsg_csr* Bin, tsg_csr_o
   uint64_t P = 0, S = 0, raw = 0, stage_total = 0, counted = 0;
   int64_t nnzC = 0;
   auto* owner = new OutOwner();
+  bool host_done = false;  // the pipelined light path ships the output itself
   owner->host = C->mem == TSG_MEM_HOST;
   C->_owner = owner;  // released by free_out on any later failure
   int64_t* d_rp = owner->host ? sc.alloc<int64_t>(rows + 1) : sc.alloc<int64_t>(rows + 1, true);
@@ -449,16 +456,82 @@ void spgemm_impl(tsg_ctx* ctx, const tsg_csr* Ain, const tsg_csr* Bin, tsg_csr_o
     record(ctx, timing, 4);  // the counting pass is fused into the numeric pass
     uint2* stage = static_cast<uint2*>(arena(stage_total * sizeof(uint2)));
     if (timing) TSG_CUDA(cudaEventRecord(ctx->kev[0], s));
-    launch_panel_numeric(TA, TB, rows, row_stage, stage, rowcnt, counted_d, opt.mode, s);
-    check_launch(ctx);
-    if (timing) TSG_CUDA(cudaEventRecord(ctx->kev[1], s));
-    record(ctx, timing, 5);
-    finish_rows();
-    if (timing) TSG_CUDA(cudaEventRecord(ctx->kev[2], s));
-    launch_panel_copy(rows, TA.tile_rows, row_stage, d_rp, stage, d_col, d_val, err_flag, s);
-    check_launch(ctx);
-    if (timing) TSG_CUDA(cudaEventRecord(ctx->kev[3], s));
-    record(ctx, timing, 6);
+    if (!owner->host || TA.tile_rows < 8 * kPipeChunks) {
+      launch_panel_numeric(TA, TB, rows, row_stage, stage, rowcnt, counted_d, opt.mode, 0, TA.tile_rows, s);
+      check_launch(ctx);
+      if (timing) TSG_CUDA(cudaEventRecord(ctx->kev[1], s));
+      record(ctx, timing, 5);
+      finish_rows();
+      if (timing) TSG_CUDA(cudaEventRecord(ctx->kev[2], s));
+      launch_panel_copy(rows, row_stage, d_rp, stage, d_col, d_val, err_flag, 0, TA.tile_rows, s);
+      check_launch(ctx);
+      if (timing) TSG_CUDA(cudaEventRecord(ctx->kev[3], s));
+      record(ctx, timing, 6);
+    } else {
+      // Host output: the result crosses PCIe (the slowest leg), so the panel
+      // pass runs in kPipeChunks tile-row chunks and chunk c's CSR slice
+      // goes to the host on a second stream while chunk c+1 computes.  Row
+      // pointers are a chained scan (each chunk starts from the previous
+      // chunk's end, read on the device); host buffers are sized by the
+      // staging bound, an upper bound on nnz(C).
+      TSG_CUDA(cudaMemsetAsync(d_rp, 0, sizeof(int64_t), s));
+      owner->p[0] = pinned_alloc(ctx, (rows + 1) * sizeof(int64_t), &owner->sz[0]);
+      owner->p[1] = pinned_alloc(ctx, std::max<uint64_t>(stage_total, 1) * sizeof(int32_t), &owner->sz[1]);
+      owner->p[2] = pinned_alloc(ctx, std::max<uint64_t>(stage_total, 1) * sizeof(float), &owner->sz[2]);
+      d_col = sc.alloc<int32_t>(stage_total);
+      d_val = sc.alloc<float>(stage_total);
+      auto* ends = reinterpret_cast<int64_t*>(ctx->pinned_pipe);  // d_rp at each chunk end
+      size_t tmp_bytes = 0;
+      TSG_CUDA(cub::DeviceScan::ExclusiveScan(nullptr, tmp_bytes, rowcnt, d_rp, cuda::std::plus<int64_t>(),
+                                              cub::FutureValue<int64_t>(d_rp), rows + 1, s));
+      void* tmp = sc.alloc<char>(tmp_bytes);
+      uint64_t sent = 0;  // entries already queued for the host
+      auto ship = [&](int c) {  // chunk c's column/value slice -> host (stream 2)
+        TSG_CUDA(cudaEventSynchronize(ctx->pipe_ev[c]));  // its end is readable now
+        const uint64_t hi = uint64_t(ends[c]);
+        TSG_CUDA(cudaStreamWaitEvent(ctx->d2h, ctx->pipe_ev[c], 0));
+        if (hi > sent) {
+          TSG_CUDA(cudaMemcpyAsync(static_cast<int32_t*>(owner->p[1]) + sent, d_col + sent, (hi - sent) * 4,
+                                   cudaMemcpyDeviceToHost, ctx->d2h));
+          TSG_CUDA(cudaMemcpyAsync(static_cast<float*>(owner->p[2]) + sent, d_val + sent, (hi - sent) * 4,
+                                   cudaMemcpyDeviceToHost, ctx->d2h));
+        }
+        sent = hi;
+      };
+      for (int c = 0; c < kPipeChunks; ++c) {
+        const uint32_t I0 = uint32_t(uint64_t(TA.tile_rows) * c / kPipeChunks);
+        const uint32_t I1 = uint32_t(uint64_t(TA.tile_rows) * (c + 1) / kPipeChunks);
+        const int64_t r0 = int64_t(I0) * 16, r1 = std::min<int64_t>(int64_t(I1) * 16, rows);
+        launch_panel_numeric(TA, TB, rows, row_stage, stage, rowcnt, counted_d, opt.mode, I0, I1, s);
+        check_launch(ctx);
+        // row_ptr[r0 .. r1] = row_ptr[r0] + exclusive prefix (row_ptr[r0] from the previous chunk)
+        TSG_CUDA(cub::DeviceScan::ExclusiveScan(tmp, tmp_bytes, rowcnt + r0, d_rp + r0,
+                                                cuda::std::plus<int64_t>(), cub::FutureValue<int64_t>(d_rp + r0),
+                                                r1 - r0 + 1, s));
+        launch_panel_copy(rows, row_stage, d_rp, stage, d_col, d_val, err_flag, I0, I1, s);
+        check_launch(ctx);
+        TSG_CUDA(cudaMemcpyAsync(ends + c, d_rp + r1, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+        TSG_CUDA(cudaEventRecord(ctx->pipe_ev[c], s));
+        if (c > 0) ship(c - 1);
+      }
+      ship(kPipeChunks - 1);
+      nnzC = int64_t(sent);
+      if (uint64_t(nnzC) >= (uint64_t(1) << 32))
+        throw Fail{TSG_ERR_OTHER, "output beyond 2^32 elements needs row-panel batching"};
+      counted = readback(ctx, counted_d);
+      TSG_CUDA(cudaMemcpyAsync(owner->p[0], d_rp, (rows + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->d2h));
+      TSG_CUDA(cudaEventRecord(ctx->pipe_ev[kPipeChunks], ctx->d2h));
+      TSG_CUDA(cudaStreamWaitEvent(s, ctx->pipe_ev[kPipeChunks], 0));  // the final sync covers stream 2
+      if (st) st->d2h_bytes += (rows + 1) * sizeof(int64_t) + uint64_t(nnzC) * 8;
+      host_done = true;
+      if (timing) {
+        TSG_CUDA(cudaEventRecord(ctx->kev[1], s));
+        TSG_CUDA(cudaEventRecord(ctx->kev[2], s));
+        TSG_CUDA(cudaEventRecord(ctx->kev[3], s));
+      }
+      record(ctx, timing, 5);
+      record(ctx, timing, 6);
+    }
   } else {
     // ---- general rows: task list, sort, numeric, assembly --------------------------
     TaskList tl;
@@ -566,7 +639,7 @@ void spgemm_impl(tsg_ctx* ctx, const tsg_csr* Ain, const tsg_csr* Bin, tsg_csr_o
   C->rows = Ain->rows;
   C->cols = Bin->cols;
   C->nnz = nnzC;
-  if (owner->host) {
+  if (owner->host && !host_done) {
     owner->p[0] = pinned_alloc(ctx, (rows + 1) * sizeof(int64_t), &owner->sz[0]);
     owner->p[1] = pinned_alloc(ctx, nnzC * sizeof(int32_t), &owner->sz[1]);
     owner->p[2] = pinned_alloc(ctx, nnzC * sizeof(float), &owner->sz[2]);
@@ -682,6 +755,10 @@ int tsg_create(tsg_ctx** out, int device, void* stream) {
     e = cudaMemPoolSetAttribute(ctx->pool, cudaMemPoolAttrReleaseThreshold, &thr);
   }
   if (e == cudaSuccess) e = cudaMallocHost(&ctx->pinned, 64);
+  if (e == cudaSuccess) e = cudaMallocHost(&ctx->pinned_pipe, 8 * (tsg::kPipeChunks + 1));
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->d2h, cudaStreamNonBlocking);
+  for (int i = 0; i <= tsg::kPipeChunks && e == cudaSuccess; ++i)
+    e = cudaEventCreateWithFlags(&ctx->pipe_ev[i], cudaEventDisableTiming);
   for (int i = 0; i < 8 && e == cudaSuccess; ++i) e = cudaEventCreate(&ctx->ev[i]);
   for (int i = 0; i < 4 && e == cudaSuccess; ++i) e = cudaEventCreate(&ctx->kev[i]);
   if (e != cudaSuccess) {
@@ -703,6 +780,13 @@ int tsg_destroy(tsg_ctx* ctx) {
   if (ctx->stage_buf) cudaFreeAsync(ctx->stage_buf, ctx->stream);
   cudaStreamSynchronize(ctx->stream);
   if (ctx->pinned) cudaFreeHost(ctx->pinned);
+  if (ctx->pinned_pipe) cudaFreeHost(ctx->pinned_pipe);
+  for (auto& e : ctx->pipe_ev)
+    if (e) cudaEventDestroy(e);
+  if (ctx->d2h) {
+    cudaStreamSynchronize(ctx->d2h);
+    cudaStreamDestroy(ctx->d2h);
+  }
   for (auto& b : ctx->pinned_free) cudaFreeHost(b.first);
   if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
   delete ctx;

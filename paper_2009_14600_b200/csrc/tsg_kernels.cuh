@@ -55,12 +55,14 @@ void launch_cbar(const int32_t* colA, int64_t nnzA, int64_t inner, const int64_t
 // light rows (<= 32 A tiles per tile row): the fused panel pass (tsg_panel.cu)
 void launch_panel_count(const TileMat& A, const TileMat& B, int64_t rows, uint32_t* row_np,
                         uint32_t* row_ns, uint32_t* row_raw, uint32_t* row_bound, cudaStream_t st);
-// staging slot = {value bits, column}, row r's region at row_stage[r]
+// staging slot = {value bits, column}, row r's region at row_stage[r]; both
+// passes work on the tile rows [I0, I1)
 void launch_panel_numeric(const TileMat& A, const TileMat& B, int64_t rows, const uint32_t* row_stage,
                           uint2* stage, int64_t* rowcnt, unsigned long long* counted, int mode,
-                          cudaStream_t st);
-void launch_panel_copy(int64_t rows, uint32_t tile_rows, const uint32_t* row_stage, const int64_t* row_ptr,
-                       const uint2* stage, int32_t* col, float* val, unsigned* err_flag, cudaStream_t st);
+                          uint32_t I0, uint32_t I1, cudaStream_t st);
+void launch_panel_copy(int64_t rows, const uint32_t* row_stage, const int64_t* row_ptr, const uint2* stage,
+                       int32_t* col, float* val, unsigned* err_flag, uint32_t I0, uint32_t I1,
+                       cudaStream_t st);
 // (2) symbolic -- general: enumerate + filter, stable sort, segment heads
 void launch_enum_count(const TileMat& A, const TileMat& B, uint64_t tA, uint32_t* tile_cnt,
                        unsigned long long* raw_total, cudaStream_t st);

@@ -112,7 +112,8 @@ __global__ void __launch_bounds__(256, 4) panel_numeric_kernel(TileMat A, TileMa
                                                               const uint32_t* __restrict__ row_stage,
                                                               uint2* __restrict__ stage,
                                                               int64_t* __restrict__ rowcnt,
-                                                              unsigned long long* __restrict__ counted) {
+                                                              unsigned long long* __restrict__ counted,
+                                                              uint32_t I0, uint32_t I1) {
   __shared__ __align__(16) uint4 s_meta[8][32];
   // TENSOR: [A tile of the row][lane] -> chunk index (ORDERED keeps the metas)
   __shared__ uint32_t s_aidx[kOrdered ? 1 : 8][32][32];
@@ -120,8 +121,8 @@ __global__ void __launch_bounds__(256, 4) panel_numeric_kernel(TileMat A, TileMa
   __shared__ float sB[kOrdered ? 8 : 1][16 * kSRow];
   const int lane = threadIdx.x & 31;
   const int w = threadIdx.x >> 5;
-  const uint32_t I = blockIdx.x * 8 + w;
-  if (I >= A.tile_rows) return;
+  const uint32_t I = I0 + blockIdx.x * 8 + w;
+  if (I >= I1) return;
   const uint4* cA = A.chunk[kRoleA];
   const uint4* cB = B.chunk[kRoleB];
   const unsigned lt = lanemask_lt(), bit = 1u << lane;
@@ -268,9 +269,9 @@ __global__ void __launch_bounds__(256) panel_copy_kernel(int64_t rows, uint32_t 
                                                         const uint2* __restrict__ stage,
                                                         int32_t* __restrict__ col,
                                                         float* __restrict__ val,
-                                                        unsigned* __restrict__ err_flag) {
+                                                        unsigned* __restrict__ err_flag, uint32_t I0) {
   const int lane = threadIdx.x & 31;
-  const uint32_t I = blockIdx.x * 8 + (threadIdx.x >> 5);
+  const uint32_t I = I0 + blockIdx.x * 8 + (threadIdx.x >> 5);
   if (I >= tile_rows) return;
   const int64_t r0 = int64_t(I) * 16;
   const int64_t r1 = r0 + 16 < rows ? r0 + 16 : rows;
@@ -312,20 +313,21 @@ void launch_panel_count(const TileMat& A, const TileMat& B, int64_t rows, uint32
 
 void launch_panel_numeric(const TileMat& A, const TileMat& B, int64_t rows, const uint32_t* row_stage,
                           uint2* stage, int64_t* rowcnt, unsigned long long* counted, int mode,
-                          cudaStream_t st) {
-  const unsigned blocks = (A.tile_rows + 7) / 8;
-  if (blocks == 0) return;
+                          uint32_t I0, uint32_t I1, cudaStream_t st) {
+  const unsigned blocks = (I1 - I0 + 7) / 8;
+  if (I1 <= I0) return;
   if (mode == 1)
-    panel_numeric_kernel<true><<<blocks, 256, 0, st>>>(A, B, rows, row_stage, stage, rowcnt, counted);
+    panel_numeric_kernel<true><<<blocks, 256, 0, st>>>(A, B, rows, row_stage, stage, rowcnt, counted, I0, I1);
   else
-    panel_numeric_kernel<false><<<blocks, 256, 0, st>>>(A, B, rows, row_stage, stage, rowcnt, counted);
+    panel_numeric_kernel<false><<<blocks, 256, 0, st>>>(A, B, rows, row_stage, stage, rowcnt, counted, I0, I1);
 }
 
-void launch_panel_copy(int64_t rows, uint32_t tile_rows, const uint32_t* row_stage, const int64_t* row_ptr,
-                       const uint2* stage, int32_t* col, float* val, unsigned* err_flag, cudaStream_t st) {
-  const unsigned blocks = (tile_rows + 7) / 8;
-  if (blocks == 0) return;
-  panel_copy_kernel<<<blocks, 256, 0, st>>>(rows, tile_rows, row_stage, row_ptr, stage, col, val, err_flag);
+void launch_panel_copy(int64_t rows, const uint32_t* row_stage, const int64_t* row_ptr, const uint2* stage,
+                       int32_t* col, float* val, unsigned* err_flag, uint32_t I0, uint32_t I1,
+                       cudaStream_t st) {
+  if (I1 <= I0) return;
+  const unsigned blocks = (I1 - I0 + 7) / 8;
+  panel_copy_kernel<<<blocks, 256, 0, st>>>(rows, I1, row_stage, row_ptr, stage, col, val, err_flag, I0);
 }
 
 }  // namespace tsg
