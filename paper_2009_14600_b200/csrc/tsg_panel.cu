@@ -107,8 +107,8 @@ __global__ void __launch_bounds__(256) panel_count_kernel(TileMat A, TileMat B, 
 constexpr int kSA = 17;    // padded row stride of the ordered A scratch tile
 constexpr int kSRow = 24;  // row stride of the ordered B scratch tile
 
-template <bool kOrdered>
-__global__ void __launch_bounds__(256, 4) panel_numeric_kernel(TileMat A, TileMat B, int64_t rows,
+template <bool kOrdered, int kMinBlocks>
+__global__ void __launch_bounds__(256, kMinBlocks) panel_numeric_kernel(TileMat A, TileMat B, int64_t rows,
                                                               const uint32_t* __restrict__ row_stage,
                                                               uint2* __restrict__ stage,
                                                               int64_t* __restrict__ rowcnt,
@@ -316,10 +316,12 @@ void launch_panel_numeric(const TileMat& A, const TileMat& B, int64_t rows, cons
                           uint32_t I0, uint32_t I1, cudaStream_t st) {
   const unsigned blocks = (I1 - I0 + 7) / 8;
   if (I1 <= I0) return;
-  if (mode == 1)
-    panel_numeric_kernel<true><<<blocks, 256, 0, st>>>(A, B, rows, row_stage, stage, rowcnt, counted, I0, I1);
-  else
-    panel_numeric_kernel<false><<<blocks, 256, 0, st>>>(A, B, rows, row_stage, stage, rowcnt, counted, I0, I1);
+  if (mode == 1) {
+    panel_numeric_kernel<true, 4><<<blocks, 256, 0, st>>>(A, B, rows, row_stage, stage, rowcnt, counted, I0, I1);
+  } else {
+    auto k = tuning_variant("TSG_PANEL_MINB", 4) == 5 ? panel_numeric_kernel<false, 5> : panel_numeric_kernel<false, 4>;
+    k<<<blocks, 256, 0, st>>>(A, B, rows, row_stage, stage, rowcnt, counted, I0, I1);
+  }
 }
 
 void launch_panel_copy(int64_t rows, const uint32_t* row_stage, const int64_t* row_ptr, const uint2* stage,
