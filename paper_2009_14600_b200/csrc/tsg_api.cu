@@ -584,6 +584,7 @@ void spgemm_impl(tsg_ctx* ctx, const tsg_csr* Ain, const tsg_csr* Bin, tsg_csr_o
     launch_seg_fill(TA, row_pair_off, keys, tl, s);
     check_launch(ctx);
     tl.pmeta = sc.alloc<uint4>(P + 1);
+    tl.pocc = sc.alloc<uint2>(P + 1);
     auto* pair_bound = sc.alloc<uint32_t>(P + 1);
     launch_pair_meta(TA, TB, pairs, tl, pair_bound, s);
     check_launch(ctx);
@@ -608,7 +609,7 @@ void spgemm_impl(tsg_ctx* ctx, const tsg_csr* Ain, const tsg_csr* Bin, tsg_csr_o
     auto* list = sc.alloc<uint32_t>(S);
     auto* list_len = sc.alloc<uint32_t>(1);
     TSG_CUDA(cudaMemsetAsync(list_len, 0, sizeof(uint32_t), s));
-    launch_numeric_thin(tl, pairs, TA, TB, sg, heavy, s);
+    launch_numeric_thin(tl, TA, TB, sg, heavy, s);
     check_launch(ctx);
     if (S > 0) {
       cub::CountingInputIterator<uint32_t> ids(0);

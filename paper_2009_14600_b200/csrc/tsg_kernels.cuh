@@ -25,6 +25,7 @@ struct CsrView {  // device CSR input
 struct TaskList {
   uint64_t npairs = 0, nseg = 0;
   uint4* pmeta = nullptr;           // [P+1] {A lane mask, A chunk base, B lane mask, B chunk base}; [P] = 0
+  uint2* pocc = nullptr;            // [P+1] {A occupancy, B occupancy} (tco.y of the two tiles)
   uint32_t* seg_row_ptr = nullptr;  // [tile_rows+1] first segment of each tile row
   uint32_t* seg_off = nullptr;      // [S+1] first pair of each segment
   uint32_t* seg_col = nullptr;      // [S] output tile column J
@@ -82,8 +83,8 @@ void launch_seg_stage(const TaskList& tl, const uint32_t* pair_stage, cudaStream
 // (3) numeric -- fused boolean count (counting_pass) + SEaC multiply, staged output.
 // Thin segments (tiny staging bound): thread per segment, sequential fp32;
 // flags the others in `heavy` (general path, where the tile pairs exist).
-void launch_numeric_thin(const TaskList& tl, const uint64_t* pairs, const TileMat& A, const TileMat& B,
-                         Staged& sg, uint8_t* heavy, cudaStream_t st);
+void launch_numeric_thin(const TaskList& tl, const TileMat& A, const TileMat& B, Staged& sg, uint8_t* heavy,
+                         cudaStream_t st);
 // warp per segment over all segments, or over list[0 .. *list_len) when list != null
 void launch_numeric(const TaskList& tl, const TileMat& A, const TileMat& B, Staged& sg, int mode,
                     const uint32_t* list, const uint32_t* list_len, cudaStream_t st);

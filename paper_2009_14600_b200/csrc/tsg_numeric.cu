@@ -244,8 +244,7 @@ __device__ __forceinline__ float tile_value(const uint4* __restrict__ chunks, ui
   return __half2float(__ushort_as_half(uint16_t(word >> (16 * (j & 1)))));
 }
 
-__global__ void __launch_bounds__(256) numeric_thin_kernel(TaskList tl, const uint64_t* __restrict__ pairs,
-                                                          TileMat A, TileMat B, Staged sg,
+__global__ void __launch_bounds__(256) numeric_thin_kernel(TaskList tl, TileMat A, TileMat B, Staged sg,
                                                           uint8_t* __restrict__ heavy) {
   const uint64_t s = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x;
   uint32_t nstruct = 0;
@@ -264,10 +263,12 @@ __global__ void __launch_bounds__(256) numeric_thin_kernel(TaskList tl, const ui
       int n = 0;
       const uint32_t p0 = tl.seg_off[s], p1 = tl.seg_off[s + 1];
       for (uint32_t p = p0; p < p1; ++p) {
-        const uint64_t pr = __ldg(reinterpret_cast<const unsigned long long*>(pairs) + p);
-        const uint32_t ta = uint32_t(pr), tb = uint32_t(pr >> 32);
-        const uint32_t oa = __ldg(&A.tco[ta].y), ob = __ldg(&B.tco[tb].y);
-        const uint2 ma = __ldg(A.meta[kRoleA] + ta), mb = __ldg(B.meta[kRoleB] + tb);
+        // operand metas and occupancies of the pair, stored per pair by
+        // pair_meta_kernel: consecutive segments read consecutive pairs
+        const uint4 mt = __ldg(tl.pmeta + p);
+        const uint2 oc = __ldg(tl.pocc + p);
+        const uint32_t oa = oc.x, ob = oc.y;
+        const uint2 ma = make_uint2(mt.x, mt.y), mb = make_uint2(mt.z, mt.w);
         for (uint32_t km = (oa & 0xffffu) & (ob >> 16); km; km &= km - 1) {
           const int k = __ffs(km) - 1;
           for (uint32_t rm = oa >> 16; rm; rm &= rm - 1) {
@@ -364,11 +365,11 @@ unsigned resident_blocks(const void* kernel, uint64_t nseg) {
 
 }  // namespace
 
-void launch_numeric_thin(const TaskList& tl, const uint64_t* pairs, const TileMat& A, const TileMat& B,
-                         Staged& sg, uint8_t* heavy, cudaStream_t st) {
+void launch_numeric_thin(const TaskList& tl, const TileMat& A, const TileMat& B, Staged& sg, uint8_t* heavy,
+                         cudaStream_t st) {
   if (tl.nseg == 0) return;
   const uint64_t blocks = (tl.nseg + 255) / 256;
-  numeric_thin_kernel<<<unsigned(blocks), 256, 0, st>>>(tl, pairs, A, B, sg, heavy);
+  numeric_thin_kernel<<<unsigned(blocks), 256, 0, st>>>(tl, A, B, sg, heavy);
 }
 
 void launch_numeric(const TaskList& tl, const TileMat& A, const TileMat& B, Staged& sg, int mode,

@@ -157,6 +157,7 @@ __global__ void pair_meta_kernel(TileMat A, TileMat B, const uint64_t* __restric
   if (i > tl.npairs) return;
   if (i == tl.npairs) {  // pad entry: zero metas (chunk 0), no staging
     tl.pmeta[i] = make_uint4(0, 0, 0, 0);
+    tl.pocc[i] = make_uint2(0, 0);
     pair_bound[i] = 0;
     return;
   }
@@ -164,8 +165,10 @@ __global__ void pair_meta_kernel(TileMat A, TileMat B, const uint64_t* __restric
   const uint32_t a = uint32_t(pr), b = uint32_t(pr >> 32);
   const uint2 am = __ldg(A.meta[kRoleA] + a);
   const uint2 bm = __ldg(B.meta[kRoleB] + b);
+  const uint32_t oa = __ldg(&A.tco[a].y), ob = __ldg(&B.tco[b].y);
   tl.pmeta[i] = make_uint4(am.x, am.y, bm.x, bm.y);
-  pair_bound[i] = __popc(__ldg(&A.tco[a].y) >> 16) * __popc(__ldg(&B.tco[b].y) & 0xffffu);
+  tl.pocc[i] = make_uint2(oa, ob);  // so the thin kernel reads each pair coalesced
+  pair_bound[i] = __popc(oa >> 16) * __popc(ob & 0xffffu);
 }
 
 // segment s's staging region starts at the bound prefix of its first pair
