@@ -624,11 +624,27 @@ void spgemm_impl(tsg_ctx* ctx, const tsg_csr* Ain, const tsg_csr* Bin, tsg_csr_o
     record(ctx, timing, 5);
 
     // tiled -> CSR: realised row counts, scan, assembly
-    launch_row_counts(rows, TA.tile_rows, tl, sg, rowcnt, s);
-    check_launch(ctx);
+    AsmChunks ch;
+    const uint64_t max_chunks = uint64_t(TA.tile_rows) + S / kChunkSegs + 1;
+    ch.n = sc.alloc<uint32_t>(1);
+    ch.tile_row = sc.alloc<uint32_t>(max_chunks);
+    ch.seg_begin = sc.alloc<uint32_t>(max_chunks);
+    ch.seg_end = sc.alloc<uint32_t>(max_chunks);
+    ch.off = sc.alloc<uint32_t>(max_chunks * 16);
+    auto* nchunks = sc.alloc<uint32_t>(nr);
+    auto* chunk_base = sc.alloc<uint32_t>(nr);
+    TSG_CUDA(cudaMemsetAsync(nchunks + nr - 1, 0, 4, s));
+    launch_asm_chunks(TA.tile_rows, tl.seg_row_ptr, nchunks, chunk_base, ch, s);
+    exclusive_sum(ctx, sc, nchunks, chunk_base, nr);
+    launch_asm_chunk_fill(TA.tile_rows, tl.seg_row_ptr, chunk_base, ch, s);
+    TSG_CUDA(cudaMemsetAsync(rowcnt, 0, (rows + 1) * sizeof(int64_t), s));
+    launch_row_counts(rows, ch, max_chunks, sg, rowcnt, s);
+    check_launch(ctx, 3);
     finish_rows();
+    launch_chunk_offsets(rows, TA.tile_rows, chunk_base, d_rp, ch, s);
+    check_launch(ctx);
     if (timing) TSG_CUDA(cudaEventRecord(ctx->kev[2], s));
-    launch_assemble(rows, TA.tile_rows, tl, sg, d_rp, d_col, d_val, err_flag, s);
+    launch_assemble(rows, ch, max_chunks, tl, sg, d_col, d_val, err_flag, s);
     check_launch(ctx);
     if (timing) TSG_CUDA(cudaEventRecord(ctx->kev[3], s));
     record(ctx, timing, 6);

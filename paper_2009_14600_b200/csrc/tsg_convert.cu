@@ -73,8 +73,6 @@ __device__ __forceinline__ unsigned short load_half(const void* val, int64_t p,
   return h;
 }
 
-constexpr int kConvW = 768;  // panel entries staged in shared memory per warp
-
 template <bool kFill, int kDtype>
 __global__ void __launch_bounds__(256) convert_kernel(CsrView in, TileMat out, int roles,
                                                      const uint32_t* __restrict__ tile_base,
@@ -85,8 +83,6 @@ __global__ void __launch_bounds__(256) convert_kernel(CsrView in, TileMat out, i
                                                      int drop_nonfinite) {
   // per warp: the tile staged densely (row-major) and transposed, as fp16 bits
   __shared__ __align__(16) uint16_t s_tile[8][2][256];
-  __shared__ int32_t s_col[8][kConvW];
-  __shared__ uint16_t s_h[8][kConvW];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
   const uint32_t I = blockIdx.x * 8 + wib;
@@ -102,24 +98,6 @@ __global__ void __launch_bounds__(256) convert_kernel(CsrView in, TileMat out, i
   int32_t prev_col = -1;
   if (!kFill && has_row && end < p) err |= kErrInvariant;
 
-  // The panel's entries are contiguous in the CSR: when they fit, load them
-  // once with coalesced loads (columns and binary16 values, dropped entries
-  // as 0) so the per-row merge below reads shared memory.
-  const int64_t r0 = int64_t(I) * kTile, r1 = r0 + kTile < in.rows ? r0 + kTile : in.rows;
-  const int64_t E0 = in.row_ptr[r0], E1 = in.row_ptr[r1];
-  const bool staged = E1 >= E0 && E1 - E0 <= kConvW;
-  int32_t* scol = s_col[wib];
-  uint16_t* sh = s_h[wib];
-  if (staged) {
-    for (int64_t q = E0 + lane; q < E1; q += 32) {
-      bool keep;
-      const unsigned short h = load_half<kDtype>(in.val, q, drop_nonfinite, err, keep);
-      scol[q - E0] = __ldg(in.col + q);
-      sh[q - E0] = keep ? h : 0;
-    }
-    __syncwarp();
-  }
-
   uint32_t ntiles = 0, nvals = 0;
   uint32_t tbase = 0;
   uint32_t cbase[2] = {0, 0};
@@ -129,7 +107,7 @@ __global__ void __launch_bounds__(256) convert_kernel(CsrView in, TileMat out, i
     cbase[0] = cbase[1] = 1u + val_base[I];
   }
   while (true) {
-    const uint32_t my_tc = (p < end) ? uint32_t(staged ? scol[p - E0] : __ldg(in.col + p)) >> 4 : 0xffffffffu;
+    const uint32_t my_tc = (p < end) ? uint32_t(__ldg(in.col + p)) >> 4 : 0xffffffffu;
     const uint32_t J = __reduce_min_sync(kFull, my_tc);
     if (J == 0xffffffffu) break;
     if (kFill) {
@@ -139,20 +117,14 @@ __global__ void __launch_bounds__(256) convert_kernel(CsrView in, TileMat out, i
     }
     uint32_t rm = 0;
     while (p < end) {
-      const int32_t c = staged ? scol[p - E0] : __ldg(in.col + p);
+      const int32_t c = __ldg(in.col + p);
       if ((uint32_t(c) >> 4) != J) break;
       if (!kFill) {
         if (c <= prev_col || c >= in.cols || c < 0) err |= kErrInvariant;
         prev_col = c;
       }
       bool keep;
-      unsigned short h;
-      if (staged) {
-        h = sh[p - E0];
-        keep = h != 0;
-      } else {
-        h = load_half<kDtype>(in.val, p, drop_nonfinite, err, keep);
-      }
+      const unsigned short h = load_half<kDtype>(in.val, p, drop_nonfinite, err, keep);
       if (keep) {
         rm |= 1u << (c & 15);
         if (kFill) {

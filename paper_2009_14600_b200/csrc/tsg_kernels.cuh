@@ -89,11 +89,28 @@ void launch_numeric_thin(const TaskList& tl, const TileMat& A, const TileMat& B,
 void launch_numeric(const TaskList& tl, const TileMat& A, const TileMat& B, Staged& sg, int mode,
                     const uint32_t* list, const uint32_t* list_len, cudaStream_t st);
 
-// (4) assembly: realised row counts -> (CUB scan -> row_ptr) -> CSR
-void launch_row_counts(int64_t rows, uint32_t tile_rows, const TaskList& tl, const Staged& sg,
+// (4) assembly.  A tile row's segments are cut into chunks of at most
+// kChunkSegs (one warp each, so hub tile rows spread over many warps):
+//   launch_asm_chunks (chunks per tile row) -> host scan -> launch_asm_chunk_fill
+//   launch_row_counts (realised (chunk, row) counts, row totals) -> host scan -> row_ptr
+//   launch_chunk_offsets (CSR offset of each chunk's rows) -> launch_assemble
+constexpr uint32_t kChunkSegs = 512;
+struct AsmChunks {
+  uint32_t* n = nullptr;          // number of chunks (device)
+  uint32_t* tile_row = nullptr;   // [chunks]
+  uint32_t* seg_begin = nullptr;  // [chunks]
+  uint32_t* seg_end = nullptr;    // [chunks]
+  uint32_t* off = nullptr;        // [chunks*16] row counts, then CSR offsets
+};
+void launch_asm_chunks(uint32_t tile_rows, const uint32_t* seg_row_ptr, uint32_t* nchunks, uint32_t* chunk_base,
+                       AsmChunks& ch, cudaStream_t st);
+void launch_asm_chunk_fill(uint32_t tile_rows, const uint32_t* seg_row_ptr, const uint32_t* chunk_base,
+                           AsmChunks& ch, cudaStream_t st);
+void launch_row_counts(int64_t rows, const AsmChunks& ch, uint64_t max_chunks, const Staged& sg,
                        int64_t* rowcnt, cudaStream_t st);
-void launch_assemble(int64_t rows, uint32_t tile_rows, const TaskList& tl, const Staged& sg,
-                     const int64_t* row_ptr, int32_t* col, float* val, unsigned* err_flag,
-                     cudaStream_t st);
+void launch_chunk_offsets(int64_t rows, uint32_t tile_rows, const uint32_t* chunk_base, const int64_t* row_ptr,
+                          AsmChunks& ch, cudaStream_t st);
+void launch_assemble(int64_t rows, const AsmChunks& ch, uint64_t max_chunks, const TaskList& tl,
+                     const Staged& sg, int32_t* col, float* val, unsigned* err_flag, cudaStream_t st);
 
 }  // namespace tsg

@@ -23,16 +23,40 @@ namespace tsg {
 
 namespace {
 
-// Realised entries per CSR row: warp per tile row, lanes over its segments
-// (32-byte row-mask record per segment), one sum per row r.
-__global__ void __launch_bounds__(256) row_count_kernel(int64_t rows, uint32_t tile_rows,
-                                                       const uint32_t* __restrict__ srp,
-                                                       const uint16_t* __restrict__ rmask,
-                                                       int64_t* __restrict__ rowcnt) {
-  const int lane = threadIdx.x & 31;
-  const uint32_t I = blockIdx.x * 8 + (threadIdx.x >> 5);
-  if (I >= tile_rows) return;
+// Segment chunks: a tile row's segments in runs of at most kChunkSegs, so
+// hub tile rows (R-MAT) are spread over many warps.  Thread per tile row.
+__global__ void chunk_fill_kernel(uint32_t tile_rows, const uint32_t* __restrict__ srp,
+                                  const uint32_t* __restrict__ chunk_base, AsmChunks ch) {
+  const uint32_t I = blockIdx.x * blockDim.x + threadIdx.x;
+  if (I > tile_rows) return;
+  if (I == tile_rows) {
+    *ch.n = chunk_base[tile_rows];
+    return;
+  }
   const uint32_t s0 = srp[I], s1 = srp[I + 1];
+  uint32_t c = chunk_base[I];
+  for (uint32_t s = s0; s < s1; s += kChunkSegs, ++c) {
+    ch.tile_row[c] = I;
+    ch.seg_begin[c] = s;
+    ch.seg_end[c] = min(s1, s + kChunkSegs);
+  }
+}
+
+__global__ void chunk_count_kernel(uint32_t tile_rows, const uint32_t* __restrict__ srp,
+                                   uint32_t* __restrict__ nchunks) {
+  const uint32_t I = blockIdx.x * blockDim.x + threadIdx.x;
+  if (I < tile_rows) nchunks[I] = (srp[I + 1] - srp[I] + kChunkSegs - 1) / kChunkSegs;
+}
+
+// Realised entries per (chunk, CSR row): warp per chunk, lanes over its
+// segments (32-byte row-mask record per segment); row totals by atomics.
+__global__ void __launch_bounds__(256) row_count_kernel(int64_t rows, AsmChunks ch,
+                                                       const uint16_t* __restrict__ rmask,
+                                                       unsigned long long* __restrict__ rowcnt) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t c = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (c >= *ch.n) return;
+  const uint32_t s0 = ch.seg_begin[c], s1 = ch.seg_end[c], I = ch.tile_row[c];
   uint32_t sum[16];
 #pragma unroll
   for (int r = 0; r < 16; ++r) sum[r] = 0;
@@ -50,7 +74,27 @@ __global__ void __launch_bounds__(256) row_count_kernel(int64_t rows, uint32_t t
     if (lane == r) mine = t;
   }
   const int64_t row = int64_t(I) * 16 + lane;
-  if (lane < 16 && row < rows) rowcnt[row] = mine;
+  if (lane < 16) {
+    ch.off[size_t(c) * 16 + lane] = mine;  // count for now; offsets after the scan
+    if (row < rows && mine) atomicAdd(rowcnt + row, (unsigned long long)mine);
+  }
+}
+
+// Counts -> CSR offsets of each chunk's rows: warp per tile row walks its
+// chunks in order (lane r carries row r).
+__global__ void __launch_bounds__(256) chunk_offset_kernel(int64_t rows, uint32_t tile_rows,
+                                                          const uint32_t* __restrict__ chunk_base,
+                                                          const int64_t* __restrict__ row_ptr, AsmChunks ch) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t I = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (I >= tile_rows || lane >= 16) return;
+  const int64_t row = int64_t(I) * 16 + lane;
+  uint32_t carry = row < rows ? uint32_t(row_ptr[row]) : 0u;
+  for (uint32_t c = chunk_base[I]; c < chunk_base[I + 1]; ++c) {
+    const uint32_t n = ch.off[size_t(c) * 16 + lane];
+    ch.off[size_t(c) * 16 + lane] = carry;
+    carry += n;
+  }
 }
 
 __device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v, int lane) {
@@ -98,8 +142,7 @@ constexpr uint32_t kAsmW = 512;  // staged values per warp batch (shared memory)
 //       instruction covers at most a few contiguous CSR ranges.
 // Non-finite values raise kErrPrecision here (finalize_segment's check,
 // kernels.cpp:115-127).
-__global__ void __launch_bounds__(256) assemble_kernel(int64_t rows, uint32_t tile_rows, TaskList tl,
-                                                      Staged sg, const int64_t* __restrict__ row_ptr,
+__global__ void __launch_bounds__(256) assemble_kernel(int64_t rows, AsmChunks ch, TaskList tl, Staged sg,
                                                       int32_t* __restrict__ col,
                                                       float* __restrict__ val,
                                                       unsigned* __restrict__ err_flag) {
@@ -110,13 +153,13 @@ __global__ void __launch_bounds__(256) assemble_kernel(int64_t rows, uint32_t ti
   __shared__ uint32_t s_ctr[8][16];
   const int lane = threadIdx.x & 31;
   const int w = threadIdx.x >> 5;
-  const uint32_t I = blockIdx.x * 8 + w;
-  if (I >= tile_rows) return;
+  const uint32_t c = blockIdx.x * 8 + w;
+  if (c >= *ch.n) return;
   float* sv = s_val[w];
   int32_t* sc = s_col[w];
-  const uint32_t s0 = tl.seg_row_ptr[I], s1 = tl.seg_row_ptr[I + 1];
-  const int64_t row = int64_t(I) * 16 + (lane & 15);
-  uint32_t carry = (lane < 16 && row < rows) ? uint32_t(row_ptr[row]) : 0u;  // lane r: row r
+  const uint32_t s0 = ch.seg_begin[c], s1 = ch.seg_end[c];
+  // lane r: CSR position of row r's first entry in this chunk
+  uint32_t carry = lane < 16 ? ch.off[size_t(c) * 16 + lane] : 0u;
   const uint4* rec = reinterpret_cast<const uint4*>(sg.rmask);
   const unsigned lt = lanemask_lt();
   bool bad = false;
@@ -239,19 +282,38 @@ __global__ void __launch_bounds__(256) assemble_kernel(int64_t rows, uint32_t ti
 
 }  // namespace
 
-void launch_row_counts(int64_t rows, uint32_t tile_rows, const TaskList& tl, const Staged& sg,
-                       int64_t* rowcnt, cudaStream_t st) {
-  const unsigned blocks = (tile_rows + 7) / 8;
-  if (blocks == 0) return;
-  row_count_kernel<<<blocks, 256, 0, st>>>(rows, tile_rows, tl.seg_row_ptr, sg.rmask, rowcnt);
+void launch_asm_chunks(uint32_t tile_rows, const uint32_t* seg_row_ptr, uint32_t* nchunks, uint32_t* chunk_base,
+                       AsmChunks& ch, cudaStream_t st) {
+  if (tile_rows == 0) return;
+  chunk_count_kernel<<<(tile_rows + 255) / 256, 256, 0, st>>>(tile_rows, seg_row_ptr, nchunks);
+  (void)chunk_base;  // scanned by the host between the two kernels
 }
 
-void launch_assemble(int64_t rows, uint32_t tile_rows, const TaskList& tl, const Staged& sg,
-                     const int64_t* row_ptr, int32_t* col, float* val, unsigned* err_flag,
-                     cudaStream_t st) {
+void launch_asm_chunk_fill(uint32_t tile_rows, const uint32_t* seg_row_ptr, const uint32_t* chunk_base,
+                           AsmChunks& ch, cudaStream_t st) {
+  chunk_fill_kernel<<<(tile_rows + 1 + 255) / 256, 256, 0, st>>>(tile_rows, seg_row_ptr, chunk_base, ch);
+}
+
+void launch_row_counts(int64_t rows, const AsmChunks& ch, uint64_t max_chunks, const Staged& sg,
+                       int64_t* rowcnt, cudaStream_t st) {
+  const uint64_t blocks = (max_chunks + 7) / 8;
+  if (blocks == 0) return;
+  row_count_kernel<<<unsigned(blocks), 256, 0, st>>>(rows, ch, sg.rmask,
+                                                      reinterpret_cast<unsigned long long*>(rowcnt));
+}
+
+void launch_chunk_offsets(int64_t rows, uint32_t tile_rows, const uint32_t* chunk_base, const int64_t* row_ptr,
+                          AsmChunks& ch, cudaStream_t st) {
   const unsigned blocks = (tile_rows + 7) / 8;
   if (blocks == 0) return;
-  assemble_kernel<<<blocks, 256, 0, st>>>(rows, tile_rows, tl, sg, row_ptr, col, val, err_flag);
+  chunk_offset_kernel<<<blocks, 256, 0, st>>>(rows, tile_rows, chunk_base, row_ptr, ch);
+}
+
+void launch_assemble(int64_t rows, const AsmChunks& ch, uint64_t max_chunks, const TaskList& tl,
+                     const Staged& sg, int32_t* col, float* val, unsigned* err_flag, cudaStream_t st) {
+  const uint64_t blocks = (max_chunks + 7) / 8;
+  if (blocks == 0) return;
+  assemble_kernel<<<unsigned(blocks), 256, 0, st>>>(rows, ch, tl, sg, col, val, err_flag);
 }
 
 }  // namespace tsg
