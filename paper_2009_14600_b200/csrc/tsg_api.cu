@@ -209,7 +209,7 @@ void readback_many(tsg_ctx* ctx, const T* const (&src)[N], T (&dst)[N]) {
 // array is sized by the input nnz (an upper bound on tiles and chunks).
 // Returns the device address of the tile count (trp[tile_rows]).
 const uint32_t* convert(tsg_ctx* ctx, Scratch& sc, const CsrView& in, TileMat& T, int roles,
-                        unsigned* err_flag, int drop_nonfinite) {
+                        unsigned* err_flag, int drop_nonfinite, const uint8_t* needed = nullptr) {
   T.rows = in.rows;
   T.cols = in.cols;
   T.tile_rows = uint32_t((in.rows + 15) / 16);
@@ -219,7 +219,7 @@ const uint32_t* convert(tsg_ctx* ctx, Scratch& sc, const CsrView& in, TileMat& T
   auto* row_nv = sc.alloc<uint32_t>(nr);
   TSG_CUDA(cudaMemsetAsync(row_nt + nr - 1, 0, sizeof(uint32_t), ctx->stream));
   TSG_CUDA(cudaMemsetAsync(row_nv + nr - 1, 0, sizeof(uint32_t), ctx->stream));
-  launch_convert_count(in, T, row_nt, row_nv, err_flag, drop_nonfinite, ctx->stream);
+  launch_convert_count(in, T, row_nt, row_nv, err_flag, drop_nonfinite, needed, ctx->stream);
   check_launch(ctx);
   T.trp = sc.alloc<uint32_t>(nr);
   auto* vbase = sc.alloc<uint32_t>(nr);
@@ -235,7 +235,7 @@ const uint32_t* convert(tsg_ctx* ctx, Scratch& sc, const CsrView& in, TileMat& T
     T.chunk[role] = sc.alloc<uint4>(cap + 1);
     TSG_CUDA(cudaMemsetAsync(T.chunk[role], 0, sizeof(uint4), ctx->stream));  // zero chunk 0
   }
-  launch_convert_fill(in, T, roles, T.trp, vbase, drop_nonfinite, ctx->stream);
+  launch_convert_fill(in, T, roles, T.trp, vbase, drop_nonfinite, needed, ctx->stream);
   check_launch(ctx);
   return T.trp + nr - 1;
 }
@@ -355,7 +355,15 @@ void spgemm_impl(tsg_ctx* ctx, const tsg_csr* Ain, const tsg_csr* Bin, tsg_csr_o
   TileMat TA, TB_own;
   const uint32_t* ntA_d = convert(ctx, sc, dA, TA, same ? 3 : 1, err_flag, opt.drop_nonfinite);
   const uint32_t* ntB_d = ntA_d;
-  if (!same) ntB_d = convert(ctx, sc, dB, TB_own, 2, err_flag, opt.drop_nonfinite);
+  if (!same) {
+    // only the B tile rows A's tiles refer to are tiled (a row panel of A --
+    // multi-GPU, or any A that touches part of B -- converts its slice of B)
+    auto* needed = sc.alloc<uint8_t>((dB.rows + 15) / 16 + 1);
+    TSG_CUDA(cudaMemsetAsync(needed, 0, (dB.rows + 15) / 16 + 1, s));
+    launch_mark_needed(TA, needed, s);
+    check_launch(ctx);
+    ntB_d = convert(ctx, sc, dB, TB_own, 2, err_flag, opt.drop_nonfinite, needed);
+  }
   const TileMat& TB = same ? TA : TB_own;
   launch_row_stats(TA, dscal + 1, s);
   check_launch(ctx);

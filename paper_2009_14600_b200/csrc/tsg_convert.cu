@@ -80,7 +80,8 @@ __global__ void __launch_bounds__(256) convert_kernel(CsrView in, TileMat out, i
                                                      uint32_t* __restrict__ row_ntiles,
                                                      uint32_t* __restrict__ row_nvals,
                                                      unsigned* __restrict__ err_flag,
-                                                     int drop_nonfinite) {
+                                                     int drop_nonfinite,
+                                                     const uint8_t* __restrict__ needed) {
   // per warp: the tile staged densely (row-major) and transposed, as fp16 bits
   __shared__ __align__(16) uint16_t s_tile[8][2][256];
   const int lane = threadIdx.x & 31;
@@ -98,6 +99,25 @@ __global__ void __launch_bounds__(256) convert_kernel(CsrView in, TileMat out, i
   int32_t prev_col = -1;
   if (!kFill && has_row && end < p) err |= kErrInvariant;
 
+  // A tile row no tile of the other operand refers to is only validated (the
+  // reference validates the whole input, tile_format.cpp:34-51): no tiles.
+  if (needed && !needed[I]) {
+    if (kFill) return;
+    for (; p < end; ++p) {
+      const int32_t c = __ldg(in.col + p);
+      if (c <= prev_col || c >= in.cols || c < 0) err |= kErrInvariant;
+      prev_col = c;
+      bool keep;
+      load_half<kDtype>(in.val, p, drop_nonfinite, err, keep);
+    }
+    const unsigned e = __reduce_or_sync(kFull, err);
+    if (lane == 0) {
+      row_ntiles[I] = 0;
+      row_nvals[I] = 0;
+      if (e) atomicOr(err_flag, e);
+    }
+    return;
+  }
   uint32_t ntiles = 0, nvals = 0;
   uint32_t tbase = 0;
   uint32_t cbase[2] = {0, 0};
@@ -185,6 +205,13 @@ __global__ void __launch_bounds__(256) convert_kernel(CsrView in, TileMat out, i
   }
 }
 
+// B tile rows that some A tile refers to (A's tile columns).
+__global__ void mark_needed_kernel(const TileMat A, uint8_t* __restrict__ needed) {
+  const uint32_t nt = A.trp[A.tile_rows];
+  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < nt; t += gridDim.x * blockDim.x)
+    needed[__ldg(&A.tco[t].x)] = 1;
+}
+
 __global__ void row_stats_kernel(const uint32_t* __restrict__ trp, uint32_t tile_rows,
                                  unsigned* __restrict__ max_row_tiles) {
   unsigned m = 0;
@@ -219,23 +246,31 @@ __global__ void cbar_dot_kernel(const unsigned* __restrict__ hist, const int64_t
 
 void launch_convert_count(const CsrView& in, TileMat& out, uint32_t* row_ntiles,
                           uint32_t* row_nvals, unsigned* err_flag, int drop_nonfinite,
-                          cudaStream_t st) {
+                          const uint8_t* needed, cudaStream_t st) {
   const unsigned blocks = (out.tile_rows + 7) / 8;
   if (blocks == 0) return;
   auto k = in.dtype == 0 ? convert_kernel<false, 0> : in.dtype == 2 ? convert_kernel<false, 2>
                                                                     : convert_kernel<false, 1>;
   k<<<blocks, 256, 0, st>>>(in, out, 0, nullptr, nullptr, row_ntiles, row_nvals, err_flag,
-                            drop_nonfinite);
+                            drop_nonfinite, needed);
 }
 
 void launch_convert_fill(const CsrView& in, TileMat& out, int roles, const uint32_t* tile_base,
-                         const uint32_t* val_base, int drop_nonfinite, cudaStream_t st) {
+                         const uint32_t* val_base, int drop_nonfinite, const uint8_t* needed,
+                         cudaStream_t st) {
   const unsigned blocks = (out.tile_rows + 7) / 8;
   if (blocks == 0) return;
   auto k = in.dtype == 0 ? convert_kernel<true, 0> : in.dtype == 2 ? convert_kernel<true, 2>
                                                                    : convert_kernel<true, 1>;
   k<<<blocks, 256, 0, st>>>(in, out, roles, tile_base, val_base, nullptr, nullptr, nullptr,
-                            drop_nonfinite);
+                            drop_nonfinite, needed);
+}
+
+void launch_mark_needed(const TileMat& A, uint8_t* needed, cudaStream_t st) {
+  if (A.cap == 0) return;
+  unsigned blocks = unsigned((A.cap + 255) / 256);
+  if (blocks > 2368) blocks = 2368;
+  mark_needed_kernel<<<blocks, 256, 0, st>>>(A, needed);
 }
 
 void launch_row_stats(const TileMat& A, unsigned* max_row_tiles, cudaStream_t st) {

@@ -44,11 +44,15 @@ struct Staged {
 };
 
 // (1) conversion
+// `needed` (nullable): per tile row, whether the other operand refers to it;
+// unneeded tile rows are validated but get no tiles
 void launch_convert_count(const CsrView& in, TileMat& out, uint32_t* row_ntiles,
                           uint32_t* row_nvals, unsigned* err_flag, int drop_nonfinite,
-                          cudaStream_t st);
+                          const uint8_t* needed, cudaStream_t st);
 void launch_convert_fill(const CsrView& in, TileMat& out, int roles, const uint32_t* tile_base,
-                         const uint32_t* val_base, int drop_nonfinite, cudaStream_t st);
+                         const uint32_t* val_base, int drop_nonfinite, const uint8_t* needed,
+                         cudaStream_t st);
+void launch_mark_needed(const TileMat& A, uint8_t* needed, cudaStream_t st);
 void launch_row_stats(const TileMat& A, unsigned* max_row_tiles, cudaStream_t st);
 void launch_cbar(const int32_t* colA, int64_t nnzA, int64_t inner, const int64_t* rpB,
                  unsigned* hist, unsigned long long* out, cudaStream_t st);

@@ -170,3 +170,43 @@ def test_general_path_thin_and_heavy(ctx, density):
         got = ctx.spgemm(Au, Bu, mode=mode)
         assert csr_bits_equal(got.C, want), (mode, first_diff(got.C, want))
         assert got.stats["counted_elements"] == port.tile_stats(Au, Bu, 16)["counted_elements"]
+
+
+@pytest.mark.parametrize("name,world", [("fem27", 8), ("poisson", 4), ("rmat", 4)])
+def test_row_panels_concatenate_to_full_product(ctx, name, world):
+    """The multi-GPU decomposition on one GPU: each rank's
+    work-balanced A row panel times the full B (only the B tile rows the panel
+    refers to are tiled) concatenates to the single-call product bit for bit."""
+    from paper_2009_14600_b200 import distributed as D
+    mats = W.make_small(name) if name == "rmat" else W.make(name)
+    A = mats[0]
+    full = ctx.spgemm(A, A).C
+    rp, cols, vals = [np.zeros(1, np.int64)], [], []
+    for r0, r1 in D.panel_bounds(A, A, world):
+        Cp = ctx.spgemm(D.take_rows(A, r0, r1), A).C
+        rp.append(np.asarray(Cp.row_ptr)[1:] + rp[-1][-1])
+        cols.append(np.asarray(Cp.col))
+        vals.append(np.asarray(Cp.val))
+    assert np.array_equal(np.concatenate(rp), np.asarray(full.row_ptr))
+    assert np.array_equal(np.concatenate(cols), np.asarray(full.col))
+    assert np.array_equal(np.concatenate(vals).view(np.uint32), np.asarray(full.val).view(np.uint32))
+
+
+def test_unreferenced_b_rows_are_still_validated(ctx):
+    """Tile rows of B that A never refers to are not tiled, but an invalid
+    entry there still raises like the reference's from_element_coo
+    (tile_format.cpp:34-51, 82-96)."""
+    A = T.Csr(4, 64, np.array([0, 1, 1, 1, 1]), np.array([0], np.int32), np.array([1.0], np.float32))
+    rp = np.arange(65, dtype=np.int64)
+    col = np.zeros(64, np.int32)
+    val = np.ones(64, np.float32)
+    val[40] = 1e6  # row 40: B tile row 2, never referenced by A's column 0
+    with pytest.raises(T.OverflowError):
+        ctx.spgemm(A, T.Csr(64, 64, rp, col, val))
+    col2 = col.copy()
+    rp2 = rp.copy()
+    rp2[41:] += 1  # row 40 holds two entries, unsorted
+    col2 = np.insert(col2, 41, 0)
+    val2 = np.insert(np.ones(64, np.float32), 41, 1.0)
+    with pytest.raises(T.InvariantError):
+        ctx.spgemm(A, T.Csr(64, 64, rp2, col2, val2))
