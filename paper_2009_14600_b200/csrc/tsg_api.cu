@@ -15,6 +15,7 @@
 // a stream-ordered memory pool (cudaMallocFromPoolAsync), so steady-state
 // calls do not touch the driver allocator.  The host synchronises only to
 // read data-dependent sizes (tile, pair, segment, element counts).
+#include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 #include <cub/device/device_segmented_sort.cuh>
 #include <cub/device/device_select.cuh>
@@ -229,6 +230,7 @@ const uint32_t* convert(tsg_ctx* ctx, Scratch& sc, const CsrView& in, TileMat& T
   T.cap = cap;
   T.tco = sc.alloc<uint2>(cap);
   T.rm2 = sc.alloc<uint32_t>(cap * 8);
+  T.trow = sc.alloc<uint32_t>(cap);
   for (int role = 0; role < 2; ++role) {
     if (!(roles & (1 << role))) continue;
     T.meta[role] = sc.alloc<uint2>(cap);
@@ -560,7 +562,16 @@ void spgemm_impl(tsg_ctx* ctx, const tsg_csr* Ain, const tsg_csr* Bin, tsg_csr_o
     tl.npairs = P;
     uint64_t* pairs_u = sc.alloc<uint64_t>(P);
     uint32_t* keys_u = sc.alloc<uint32_t>(P);
-    launch_enum_fill(TA, TB, tA, tile_off, pairs_u, keys_u, s);
+    auto bits_of = [](uint64_t n) {
+      uint32_t b = 0;
+      while ((uint64_t(1) << b) < n) ++b;
+      return b;
+    };
+    const uint32_t jbits = bits_of(TB.tile_cols), ibits = bits_of(TA.tile_rows);
+    // the tile row rides in the key's high bits when it fits (radix sort);
+    // otherwise keys are the column alone (segmented sort per tile row)
+    const uint32_t key_shift = jbits + ibits <= 32 ? jbits : 32;
+    launch_enum_fill(TA, TB, tA, tile_off, pairs_u, keys_u, key_shift, s);
     check_launch(ctx);
     launch_row_pair_off(TA, tile_off, row_pair_off, s);
     check_launch(ctx);
@@ -568,7 +579,17 @@ void spgemm_impl(tsg_ctx* ctx, const tsg_csr* Ain, const tsg_csr* Bin, tsg_csr_o
     // stable sort by output tile column within each tile row
     uint64_t* pairs = sc.alloc<uint64_t>(P + 1);
     uint32_t* keys = sc.alloc<uint32_t>(P);
-    if (P > 0) {
+    if (P > 0 && jbits + ibits <= 32) {
+      // keys are (tile row << jbits | tile col): one stable LSD radix sort of
+      // just the key bits in use (tiles are enumerated in row order, so this
+      // is the per-tile-row sort by output column, k order kept by stability)
+      size_t bytes = 0;
+      TSG_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, keys_u, keys, pairs_u, pairs, P, 0,
+                                               int(jbits + ibits), s));
+      void* tmp = sc.alloc<char>(bytes);
+      TSG_CUDA(cub::DeviceRadixSort::SortPairs(tmp, bytes, keys_u, keys, pairs_u, pairs, P, 0,
+                                               int(jbits + ibits), s));
+    } else if (P > 0) {
       size_t bytes = 0;
       TSG_CUDA(cub::DeviceSegmentedSort::StableSortPairs(nullptr, bytes, keys_u, keys, pairs_u,
                                                          pairs, int(P), int(TA.tile_rows),
@@ -580,6 +601,7 @@ void spgemm_impl(tsg_ctx* ctx, const tsg_csr* Ain, const tsg_csr* Bin, tsg_csr_o
     }
     auto* row_nseg = sc.alloc<uint32_t>(nr);
     TSG_CUDA(cudaMemsetAsync(row_nseg + nr - 1, 0, sizeof(uint32_t), s));
+    const uint32_t jmask = jbits >= 32 ? 0xffffffffu : (1u << jbits) - 1u;
     launch_seg_count(TA, row_pair_off, keys, row_nseg, s);
     check_launch(ctx);
     S = total_u32(ctx, sc, row_nseg, nr);
@@ -589,7 +611,7 @@ void spgemm_impl(tsg_ctx* ctx, const tsg_csr* Ain, const tsg_csr* Bin, tsg_csr_o
     tl.seg_col = sc.alloc<uint32_t>(S);
     tl.stage_off = sc.alloc<uint32_t>(S + 1);
     TSG_CUDA(cudaMemcpyAsync(tl.seg_off + S, row_pair_off + nr - 1, 4, cudaMemcpyDeviceToDevice, s));
-    launch_seg_fill(TA, row_pair_off, keys, tl, s);
+    launch_seg_fill(TA, row_pair_off, keys, jmask, tl, s);
     check_launch(ctx);
     tl.pmeta = sc.alloc<uint4>(P + 1);
     tl.pocc = sc.alloc<uint2>(P + 1);

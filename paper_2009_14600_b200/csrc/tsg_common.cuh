@@ -13,6 +13,7 @@
 //                           masks: word g = row g | row g+8 << 16 (bit c of
 //                           row r <=> slot (r,c) nonzero; reference bit 8r+c,
 //                           tile_format.hpp:20-23)
+//   trow  u32[T]            tile row of each tile (the general path's sort key)
 //   meta  uint2[T]  (per operand role)  {lane mask, first chunk}
 //   chunk uint4[]   (per operand role)  16-byte lane chunks, chunk 0 = zeros
 //
@@ -44,6 +45,7 @@ struct TileMat {
   uint32_t* trp = nullptr;
   uint2* tco = nullptr;
   uint32_t* rm2 = nullptr;
+  uint32_t* trow = nullptr;  // [T] tile row of each tile
   uint2* meta[2] = {nullptr, nullptr};
   uint4* chunk[2] = {nullptr, nullptr};
 };

@@ -164,7 +164,10 @@ __global__ void __launch_bounds__(256) convert_kernel(CsrView in, TileMat out, i
       __syncwarp();
       const uint32_t t = tbase + ntiles;
       const uint32_t colocc = __reduce_or_sync(kFull, rm) & 0xffffu;
-      if (lane == 0) out.tco[t] = make_uint2(J, colocc | ((any & 0xffffu) << 16));
+      if (lane == 0) {
+        out.tco[t] = make_uint2(J, colocc | ((any & 0xffffu) << 16));
+        out.trow[t] = I;
+      }
       // the 256-bit mask as interleaved row masks: word g = row g | row g+8 << 16
       const uint32_t rm_hi = __shfl_sync(kFull, rm, (lane & 7) + 8);
       if (lane < 8) out.rm2[size_t(t) * 8 + lane] = rm | (rm_hi << 16);

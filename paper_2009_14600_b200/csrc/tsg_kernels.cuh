@@ -72,12 +72,12 @@ void launch_panel_copy(int64_t rows, const uint32_t* row_stage, const int64_t* r
 void launch_enum_count(const TileMat& A, const TileMat& B, uint64_t tA, uint32_t* tile_cnt,
                        unsigned long long* raw_total, cudaStream_t st);
 void launch_enum_fill(const TileMat& A, const TileMat& B, uint64_t tA, const uint32_t* tile_off,
-                      uint64_t* pairs, uint32_t* keys, cudaStream_t st);
+                      uint64_t* pairs, uint32_t* keys, uint32_t key_shift, cudaStream_t st);
 void launch_row_pair_off(const TileMat& A, const uint32_t* tile_off, uint32_t* row_pair_off,
                          cudaStream_t st);
 void launch_seg_count(const TileMat& A, const uint32_t* row_pair_off, const uint32_t* keys,
                       uint32_t* row_nseg, cudaStream_t st);
-void launch_seg_fill(const TileMat& A, const uint32_t* row_pair_off, const uint32_t* keys,
+void launch_seg_fill(const TileMat& A, const uint32_t* row_pair_off, const uint32_t* keys, uint32_t jmask,
                      TaskList& tl, cudaStream_t st);
 // per sorted pair: operand metas and the staging bound popc(rows A) * popc(cols B)
 void launch_pair_meta(const TileMat& A, const TileMat& B, const uint64_t* pairs, TaskList& tl,

@@ -34,7 +34,8 @@ __global__ void __launch_bounds__(256) enum_kernel(TileMat A, TileMat B, uint64_
                                                   const uint32_t* __restrict__ tile_off,
                                                   uint64_t* __restrict__ pairs,
                                                   uint32_t* __restrict__ keys,
-                                                  unsigned long long* __restrict__ raw_total) {
+                                                  unsigned long long* __restrict__ raw_total,
+                                                  uint32_t key_shift) {
   __shared__ uint32_t s_cnt[8][33];
   __shared__ unsigned long long s_raw[8];
   const int lane = threadIdx.x & 31;
@@ -91,7 +92,8 @@ __global__ void __launch_bounds__(256) enum_kernel(TileMat A, TileMat B, uint64_
       if (kFill && pass) {
         const uint32_t pos = off_s + before + __popc(pbal & grp & lanemask_lt());
         pairs[pos] = (a0 + uint64_t(s)) | (uint64_t(b) << 32);
-        keys[pos] = bt.x;
+        // (tile row << shift) | tile col; shift 32 drops the row (segmented sort)
+        keys[pos] = (key_shift < 32 ? (__ldg(A.trow + a0 + s) << key_shift) : 0u) | bt.x;
       }
       __syncwarp();
       if (active && lane == __ffs(grp) - 1) s_cnt[wib][s] = before + __popc(pbal & grp);
@@ -120,7 +122,7 @@ __global__ void row_pair_off_kernel(const uint32_t* __restrict__ trp, uint32_t t
 // Segment heads after the per-row sort: a new segment starts at each row
 // start and wherever the output tile column changes (pipeline.cpp:94-107).
 template <bool kFill>
-__global__ void __launch_bounds__(256) seg_kernel(uint32_t tile_rows,
+__global__ void __launch_bounds__(256) seg_kernel(uint32_t jmask, uint32_t tile_rows,
                                                  const uint32_t* __restrict__ row_pair_off,
                                                  const uint32_t* __restrict__ keys,
                                                  uint32_t* __restrict__ row_nseg, TaskList tl) {
@@ -142,7 +144,7 @@ __global__ void __launch_bounds__(256) seg_kernel(uint32_t tile_rows,
     if (kFill && head) {
       const uint32_t s = base + nseg + __popc(hb & lanemask_lt());
       tl.seg_off[s] = i;
-      tl.seg_col[s] = key;
+      tl.seg_col[s] = key & jmask;
     }
     nseg += __popc(hb);
     carry = __shfl_sync(kFull, key, 31);
@@ -185,16 +187,16 @@ void launch_enum_count(const TileMat& A, const TileMat& B, uint64_t tA, uint32_t
   const uint64_t blocks = (warps + 7) / 8;
   if (blocks == 0) return;
   enum_kernel<false><<<unsigned(blocks), 256, 0, st>>>(A, B, tA, tile_cnt, nullptr, nullptr,
-                                                        nullptr, raw_total);
+                                                        nullptr, raw_total, 32);
 }
 
 void launch_enum_fill(const TileMat& A, const TileMat& B, uint64_t tA, const uint32_t* tile_off,
-                      uint64_t* pairs, uint32_t* keys, cudaStream_t st) {
+                      uint64_t* pairs, uint32_t* keys, uint32_t key_shift, cudaStream_t st) {
   const uint64_t warps = (tA + 31) / 32;
   const uint64_t blocks = (warps + 7) / 8;
   if (blocks == 0) return;
   enum_kernel<true><<<unsigned(blocks), 256, 0, st>>>(A, B, tA, nullptr, tile_off, pairs, keys,
-                                                       nullptr);
+                                                       nullptr, key_shift);
 }
 
 void launch_row_pair_off(const TileMat& A, const uint32_t* tile_off, uint32_t* row_pair_off,
@@ -208,14 +210,14 @@ void launch_seg_count(const TileMat& A, const uint32_t* row_pair_off, const uint
                       uint32_t* row_nseg, cudaStream_t st) {
   const unsigned blocks = (A.tile_rows + 7) / 8;
   if (blocks == 0) return;
-  seg_kernel<false><<<blocks, 256, 0, st>>>(A.tile_rows, row_pair_off, keys, row_nseg, TaskList{});
+  seg_kernel<false><<<blocks, 256, 0, st>>>(0xffffffffu, A.tile_rows, row_pair_off, keys, row_nseg, TaskList{});
 }
 
-void launch_seg_fill(const TileMat& A, const uint32_t* row_pair_off, const uint32_t* keys,
+void launch_seg_fill(const TileMat& A, const uint32_t* row_pair_off, const uint32_t* keys, uint32_t jmask,
                      TaskList& tl, cudaStream_t st) {
   const unsigned blocks = (A.tile_rows + 7) / 8;
   if (blocks == 0) return;
-  seg_kernel<true><<<blocks, 256, 0, st>>>(A.tile_rows, row_pair_off, keys, nullptr, tl);
+  seg_kernel<true><<<blocks, 256, 0, st>>>(jmask, A.tile_rows, row_pair_off, keys, nullptr, tl);
 }
 
 void launch_pair_meta(const TileMat& A, const TileMat& B, const uint64_t* pairs, TaskList& tl,
