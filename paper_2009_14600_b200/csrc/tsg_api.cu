@@ -231,6 +231,10 @@ const uint32_t* convert(tsg_ctx* ctx, Scratch& sc, const CsrView& in, TileMat& T
   T.tco = sc.alloc<uint2>(cap);
   T.rm2 = sc.alloc<uint32_t>(cap * 8);
   T.trow = sc.alloc<uint32_t>(cap);
+  if (roles & 2) {
+    T.etile = sc.alloc<uint32_t>(cap);
+    T.csr_rp = in.row_ptr;
+  }
   for (int role = 0; role < 2; ++role) {
     if (!(roles & (1 << role))) continue;
     T.meta[role] = sc.alloc<uint2>(cap);

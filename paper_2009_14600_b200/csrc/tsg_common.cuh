@@ -46,6 +46,11 @@ struct TileMat {
   uint2* tco = nullptr;
   uint32_t* rm2 = nullptr;
   uint32_t* trow = nullptr;  // [T] tile row of each tile
+  // (B-role conversions) per input CSR entry: its tile, | kDupEntry unless it
+  // is the first kept entry of that tile in its row, kNoTile if dropped; and
+  // the input row pointers -- single-column A tiles enumerate through them
+  uint32_t* etile = nullptr;
+  const int64_t* csr_rp = nullptr;
   uint2* meta[2] = {nullptr, nullptr};
   uint4* chunk[2] = {nullptr, nullptr};
 };
@@ -77,6 +82,9 @@ __host__ __device__ inline void rc_of(int role, int lane, int j, int& r, int& c)
 
 // Accumulator (C/D fragment, two n8 halves: acc[0] = cols 0..7, acc[1] = 8..15):
 //   acc[h][i]: row g + 8*(i>>1), col 2t + (i&1) + 8*h.
+
+constexpr uint32_t kNoTile = 0xffffffffu;
+constexpr uint32_t kDupEntry = 0x80000000u;
 
 // Device error flags (OR-ed), mapped to tsg_status by the host.
 enum ErrBits : unsigned {

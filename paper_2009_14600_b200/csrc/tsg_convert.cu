@@ -102,7 +102,11 @@ __global__ void __launch_bounds__(256) convert_kernel(CsrView in, TileMat out, i
   // A tile row no tile of the other operand refers to is only validated (the
   // reference validates the whole input, tile_format.cpp:34-51): no tiles.
   if (needed && !needed[I]) {
-    if (kFill) return;
+    if (kFill) {
+      if (out.etile)
+        for (; p < end; ++p) out.etile[p] = kNoTile;
+      return;
+    }
     for (; p < end; ++p) {
       const int32_t c = __ldg(in.col + p);
       if (c <= prev_col || c >= in.cols || c < 0) err |= kErrInvariant;
@@ -136,6 +140,7 @@ __global__ void __launch_bounds__(256) convert_kernel(CsrView in, TileMat out, i
       __syncwarp();
     }
     uint32_t rm = 0;
+    bool first = true;  // first kept entry of this tile in this row
     while (p < end) {
       const int32_t c = __ldg(in.col + p);
       if ((uint32_t(c) >> 4) != J) break;
@@ -151,6 +156,10 @@ __global__ void __launch_bounds__(256) convert_kernel(CsrView in, TileMat out, i
           st[lane * 16 + (c & 15)] = h;
           stT[(c & 15) * 16 + lane] = h;
         }
+      }
+      if (kFill && out.etile) {
+        out.etile[p] = keep ? ((tbase + ntiles) | (first ? 0u : kDupEntry)) : kNoTile;
+        first &= !keep;
       }
       ++p;
     }

@@ -45,12 +45,28 @@ __global__ void __launch_bounds__(256) enum_kernel(TileMat A, TileMat B, uint64_
   if (a0 < tA) {
     const uint64_t a = a0 + lane;
     const bool valid = a < tA;
-    uint32_t bs = 0, bl = 0, colocc = 0, base_off = 0;
+    // Each A tile's candidate list: a single-column tile (one inner slot kk,
+    // ~1 nnz per tile on R-MAT / rect) takes B's CSR row 16k+kk -- its first
+    // kept entry per tile names exactly the B tiles that pass the
+    // zero-product filter; others take B's tile row k with the occupancy
+    // filter (pipeline.cpp:23-35).  Raw pairs are B tile row lengths either way.
+    uint32_t bs = 0, bl = 0, colocc = 0, base_off = 0, raw_len = 0;
+    bool single = false;
     if (valid) {
       const uint2 ac = __ldg(A.tco + a);
-      bs = __ldg(B.trp + ac.x);
-      bl = __ldg(B.trp + ac.x + 1) - bs;
+      const uint32_t ts = __ldg(B.trp + ac.x), te = __ldg(B.trp + ac.x + 1);
+      raw_len = te - ts;
       colocc = ac.y & 0xffffu;
+      single = B.etile != nullptr && __popc(colocc) == 1;
+      if (single) {
+        const int64_t row = int64_t(ac.x) * 16 + (__ffs(colocc) - 1);
+        const int64_t e0 = row < B.rows ? __ldg(B.csr_rp + row) : 0, e1 = row < B.rows ? __ldg(B.csr_rp + row + 1) : 0;
+        bs = uint32_t(e0);
+        bl = uint32_t(e1 - e0);
+      } else {
+        bs = ts;
+        bl = raw_len;
+      }
       if (kFill) base_off = __ldg(tile_off + a);
     }
     uint32_t incl = bl;
@@ -61,7 +77,8 @@ __global__ void __launch_bounds__(256) enum_kernel(TileMat A, TileMat B, uint64_
     }
     const uint32_t excl = incl - bl;
     const uint32_t total = __shfl_sync(kFull, incl, 31);
-    raw = total;
+    raw = __reduce_add_sync(kFull, raw_len);
+    const unsigned single_mask = __ballot_sync(kFull, single);
     s_cnt[wib][lane] = 0;
     __syncwarp();
     for (uint32_t q0 = 0; q0 < total; q0 += 32) {
@@ -79,12 +96,21 @@ __global__ void __launch_bounds__(256) enum_kernel(TileMat A, TileMat B, uint64_
       const uint32_t ex_s = __shfl_sync(kFull, excl, s & 31);
       const uint32_t co_s = __shfl_sync(kFull, colocc, s & 31);
       const uint32_t off_s = __shfl_sync(kFull, base_off, s & 31);
-      const uint32_t b = bs_s + (q - ex_s);
+      const bool single_s = (single_mask >> (s & 31)) & 1u;
+      uint32_t b = bs_s + (q - ex_s);
       bool pass = false;
-      uint2 bt = make_uint2(0, 0);
+      uint32_t J = 0;
       if (active) {
-        bt = __ldg(B.tco + b);
-        pass = (co_s & (bt.y >> 16)) != 0;
+        if (single_s) {
+          const uint32_t t = __ldg(B.etile + b);  // b is an entry index here
+          pass = (t & kDupEntry) == 0u;            // kNoTile has the bit set too
+          b = t & ~kDupEntry;
+          if (kFill && pass) J = __ldg(&B.tco[b].x);
+        } else {
+          const uint2 bt = __ldg(B.tco + b);
+          pass = (co_s & (bt.y >> 16)) != 0;
+          J = bt.x;
+        }
       }
       const unsigned grp = __match_any_sync(kFull, s);
       const unsigned pbal = __ballot_sync(kFull, pass);
@@ -93,7 +119,7 @@ __global__ void __launch_bounds__(256) enum_kernel(TileMat A, TileMat B, uint64_
         const uint32_t pos = off_s + before + __popc(pbal & grp & lanemask_lt());
         pairs[pos] = (a0 + uint64_t(s)) | (uint64_t(b) << 32);
         // (tile row << shift) | tile col; shift 32 drops the row (segmented sort)
-        keys[pos] = (key_shift < 32 ? (__ldg(A.trow + a0 + s) << key_shift) : 0u) | bt.x;
+        keys[pos] = (key_shift < 32 ? (__ldg(A.trow + a0 + s) << key_shift) : 0u) | J;
       }
       __syncwarp();
       if (active && lane == __ffs(grp) - 1) s_cnt[wib][s] = before + __popc(pbal & grp);
