@@ -402,22 +402,39 @@ void spgemm_impl(tsg_ctx* ctx, const tsg_csr* Ain, const tsg_csr* Bin, tsg_csr_o
   TSG_CUDA(cudaMemsetAsync(counted_d, 0, sizeof(unsigned long long), s));
   auto* rowcnt = sc.alloc<int64_t>(rows + 1);  // realised entries per CSR row
   TSG_CUDA(cudaMemsetAsync(rowcnt + rows, 0, sizeof(int64_t), s));
-  // the realised row counts -> row_ptr, nnz(C) and counted elements to the host
-  auto finish_rows = [&]() {
+  // the realised row counts -> row_ptr, nnz(C) and counted elements to the
+  // host (plus, optionally, two more device totals in the same synchronisation)
+  auto scan_rows = [&](const unsigned long long* extra = nullptr, unsigned long long* out = nullptr) {
     exclusive_sum(ctx, sc, rowcnt, d_rp, uint64_t(rows) + 1);
-    const unsigned long long* src[2] = {counted_d, reinterpret_cast<const unsigned long long*>(d_rp + rows)};
-    unsigned long long v[2];
-    readback_many(ctx, src, v);
+    const unsigned long long* nz = reinterpret_cast<const unsigned long long*>(d_rp + rows);
+    unsigned long long v[6];
+    if (extra) {  // extra[0..3] (contiguous device totals) in the same synchronisation
+      const unsigned long long* src[6] = {counted_d, nz, extra, extra + 1, extra + 2, extra + 3};
+      readback_many(ctx, src, v);
+      for (int i = 0; i < 4; ++i) out[i] = v[2 + i];
+    } else {
+      const unsigned long long* src[2] = {counted_d, nz};
+      unsigned long long w[2];
+      readback_many(ctx, src, w);
+      v[0] = w[0];
+      v[1] = w[1];
+    }
     counted = v[0];
     nnzC = int64_t(v[1]);
     if (uint64_t(nnzC) >= (uint64_t(1) << 32))
       throw Fail{TSG_ERR_OTHER, "output beyond 2^32 elements needs row-panel batching"};
+  };
+  auto alloc_out = [&]() {
     d_col = sc.alloc<int32_t>(nnzC, !owner->host);
     d_val = sc.alloc<float>(nnzC, !owner->host);
     if (!owner->host) {
       owner->p[1] = d_col;
       owner->p[2] = d_val;
     }
+  };
+  auto finish_rows = [&]() {
+    scan_rows();
+    alloc_out();
   };
   // grow-only staging arena (bytes)
   auto arena = [&](size_t need) -> void* {
@@ -456,26 +473,59 @@ void spgemm_impl(tsg_ctx* ctx, const tsg_csr* Ain, const tsg_csr* Bin, tsg_csr_o
       sum_u32_kernel<<<blocks, 256, 0, s>>>(row_bound, uint64_t(rows), tot_d + 3);
       check_launch(ctx, 4);
     }
-    const unsigned long long* src[4] = {tot_d, tot_d + 1, tot_d + 2, tot_d + 3};
-    unsigned long long v[4];
-    readback_many(ctx, src, v);
-    P = v[0];
-    S = v[1];
-    raw = v[2];
-    stage_total = v[3];
-    if (stage_total >= (uint64_t(1) << 32))
-      throw Fail{TSG_ERR_OTHER, "staged slots beyond 2^32 need row-panel batching"};
+    auto read_totals = [&]() {
+      const unsigned long long* src[4] = {tot_d, tot_d + 1, tot_d + 2, tot_d + 3};
+      unsigned long long v[4];
+      readback_many(ctx, src, v);
+      P = v[0];
+      S = v[1];
+      raw = v[2];
+      stage_total = v[3];
+      if (stage_total >= (uint64_t(1) << 32))
+        throw Fail{TSG_ERR_OTHER, "staged slots beyond 2^32 need row-panel batching"};
+    };
+    // Device output with a staging arena already in place: launch the panel
+    // pass without reading the staging total back first; the kernel checks it
+    // against the arena on the device and the totals are read with nnz(C)
+    // (a too-small arena -- rare after the first call -- reruns the pass).
+    const bool speculative = !owner->host && ctx->stage_cap >= 16;
+    if (!speculative) read_totals();
     record(ctx, timing, 2);
     record(ctx, timing, 3);  // the merge is the sort: no separate phase
     record(ctx, timing, 4);  // the counting pass is fused into the numeric pass
-    uint2* stage = static_cast<uint2*>(arena(stage_total * sizeof(uint2)));
+    uint2* stage = static_cast<uint2*>(speculative ? ctx->stage_buf : arena(stage_total * sizeof(uint2)));
+    uint64_t stage_cap_slots = speculative ? ctx->stage_cap / sizeof(uint2) : stage_total;
     if (timing) TSG_CUDA(cudaEventRecord(ctx->kev[0], s));
     if (!owner->host || TA.tile_rows < 8 * kPipeChunks) {
-      launch_panel_numeric(TA, TB, rows, row_stage, stage, rowcnt, counted_d, opt.mode, 0, TA.tile_rows, s);
+      launch_panel_numeric(TA, TB, rows, row_stage, stage_cap_slots, stage, rowcnt, counted_d, opt.mode, 0,
+                           TA.tile_rows, s);
       check_launch(ctx);
       if (timing) TSG_CUDA(cudaEventRecord(ctx->kev[1], s));
       record(ctx, timing, 5);
-      finish_rows();
+      if (speculative) {
+        // one synchronisation: counted, nnz(C), P, S, raw pairs, staging total
+        unsigned long long t[4];
+        scan_rows(tot_d, t);
+        P = t[0];
+        S = t[1];
+        raw = t[2];
+        stage_total = t[3];
+        if (stage_total >= (uint64_t(1) << 32))
+          throw Fail{TSG_ERR_OTHER, "staged slots beyond 2^32 need row-panel batching"};
+        if (stage_total > stage_cap_slots) {  // the rare arena overflow: redo the pass
+          read_totals();
+          stage = static_cast<uint2*>(arena(stage_total * sizeof(uint2)));
+          stage_cap_slots = stage_total;
+          TSG_CUDA(cudaMemsetAsync(counted_d, 0, sizeof(unsigned long long), s));
+          launch_panel_numeric(TA, TB, rows, row_stage, stage_cap_slots, stage, rowcnt, counted_d, opt.mode, 0,
+                               TA.tile_rows, s);
+          check_launch(ctx);
+          scan_rows();
+        }
+        alloc_out();
+      } else {
+        finish_rows();
+      }
       if (timing) TSG_CUDA(cudaEventRecord(ctx->kev[2], s));
       launch_panel_copy(rows, row_stage, d_rp, stage, d_col, d_val, err_flag, 0, TA.tile_rows, s);
       check_launch(ctx);
@@ -516,7 +566,8 @@ void spgemm_impl(tsg_ctx* ctx, const tsg_csr* Ain, const tsg_csr* Bin, tsg_csr_o
         const uint32_t I0 = uint32_t(uint64_t(TA.tile_rows) * c / kPipeChunks);
         const uint32_t I1 = uint32_t(uint64_t(TA.tile_rows) * (c + 1) / kPipeChunks);
         const int64_t r0 = int64_t(I0) * 16, r1 = std::min<int64_t>(int64_t(I1) * 16, rows);
-        launch_panel_numeric(TA, TB, rows, row_stage, stage, rowcnt, counted_d, opt.mode, I0, I1, s);
+        launch_panel_numeric(TA, TB, rows, row_stage, stage_cap_slots, stage, rowcnt, counted_d, opt.mode, I0, I1,
+                             s);
         check_launch(ctx);
         // row_ptr[r0 .. r1] = row_ptr[r0] + exclusive prefix (row_ptr[r0] from the previous chunk)
         TSG_CUDA(cub::DeviceScan::ExclusiveScan(tmp, tmp_bytes, rowcnt + r0, d_rp + r0,

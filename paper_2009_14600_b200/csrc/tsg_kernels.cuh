@@ -62,8 +62,10 @@ void launch_panel_count(const TileMat& A, const TileMat& B, int64_t rows, uint32
                         uint32_t* row_ns, uint32_t* row_raw, uint32_t* row_bound, cudaStream_t st);
 // staging slot = {value bits, column}, row r's region at row_stage[r]; both
 // passes work on the tile rows [I0, I1)
+// The pass does nothing when the staging total row_stage[rows] exceeds
+// stage_cap slots (the host checks and reruns with a bigger arena).
 void launch_panel_numeric(const TileMat& A, const TileMat& B, int64_t rows, const uint32_t* row_stage,
-                          uint2* stage, int64_t* rowcnt, unsigned long long* counted, int mode,
+                          uint64_t stage_cap, uint2* stage, int64_t* rowcnt, unsigned long long* counted, int mode,
                           uint32_t I0, uint32_t I1, cudaStream_t st);
 void launch_panel_copy(int64_t rows, const uint32_t* row_stage, const int64_t* row_ptr, const uint2* stage,
                        int32_t* col, float* val, unsigned* err_flag, uint32_t I0, uint32_t I1,

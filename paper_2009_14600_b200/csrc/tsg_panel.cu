@@ -110,7 +110,7 @@ constexpr int kSRow = 24;  // row stride of the ordered B scratch tile
 template <bool kOrdered, int kMinBlocks>
 __global__ void __launch_bounds__(256, kMinBlocks) panel_numeric_kernel(TileMat A, TileMat B, int64_t rows,
                                                               const uint32_t* __restrict__ row_stage,
-                                                              uint2* __restrict__ stage,
+                                                              uint64_t stage_cap, uint2* __restrict__ stage,
                                                               int64_t* __restrict__ rowcnt,
                                                               unsigned long long* __restrict__ counted,
                                                               uint32_t I0, uint32_t I1) {
@@ -123,6 +123,7 @@ __global__ void __launch_bounds__(256, kMinBlocks) panel_numeric_kernel(TileMat 
   const int w = threadIdx.x >> 5;
   const uint32_t I = I0 + blockIdx.x * 8 + w;
   if (I >= I1) return;
+  if (__ldg(row_stage + rows) > stage_cap) return;  // arena too small: the host reruns the pass
   const uint4* cA = A.chunk[kRoleA];
   const uint4* cB = B.chunk[kRoleB];
   const unsigned lt = lanemask_lt(), bit = 1u << lane;
@@ -312,15 +313,16 @@ void launch_panel_count(const TileMat& A, const TileMat& B, int64_t rows, uint32
 }
 
 void launch_panel_numeric(const TileMat& A, const TileMat& B, int64_t rows, const uint32_t* row_stage,
-                          uint2* stage, int64_t* rowcnt, unsigned long long* counted, int mode,
+                          uint64_t stage_cap, uint2* stage, int64_t* rowcnt, unsigned long long* counted, int mode,
                           uint32_t I0, uint32_t I1, cudaStream_t st) {
   const unsigned blocks = (I1 - I0 + 7) / 8;
   if (I1 <= I0) return;
   if (mode == 1) {
-    panel_numeric_kernel<true, 4><<<blocks, 256, 0, st>>>(A, B, rows, row_stage, stage, rowcnt, counted, I0, I1);
+    panel_numeric_kernel<true, 4><<<blocks, 256, 0, st>>>(A, B, rows, row_stage, stage_cap, stage, rowcnt, counted,
+                                                           I0, I1);
   } else {
     auto k = tuning_variant("TSG_PANEL_MINB", 4) == 5 ? panel_numeric_kernel<false, 5> : panel_numeric_kernel<false, 4>;
-    k<<<blocks, 256, 0, st>>>(A, B, rows, row_stage, stage, rowcnt, counted, I0, I1);
+    k<<<blocks, 256, 0, st>>>(A, B, rows, row_stage, stage_cap, stage, rowcnt, counted, I0, I1);
   }
 }
 
