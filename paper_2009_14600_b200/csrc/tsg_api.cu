@@ -330,52 +330,79 @@ void tiles_from_csr(int64_t rows, const std::vector<int64_t>& rp, const std::vec
   out->val = static_cast<float*>(dup(vv.data(), vv.size() * 4));
 }
 
-void spgemm_impl(tsg_ctx* ctx, const tsg_csr* Ain, const tsg_csr* Bin, tsg_csr_out* C,
-                 const tsg_options& opt, tsg_run_stats* st, tsg_tiles_out* tiles) {
-  check_csr(Ain, "A");
-  check_csr(Bin, "B");
-  if (!C) throw Fail{TSG_ERR_OTHER, "C is NULL"};
-  if (Ain->cols != Bin->rows)
-    throw Fail{TSG_ERR_DIMENSION, "inner dimensions differ: A is " + std::to_string(Ain->rows) +
-                                      "x" + std::to_string(Ain->cols) + ", B is " +
-                                      std::to_string(Bin->rows) + "x" + std::to_string(Bin->cols)};
-  const bool timing = opt.phase_timing != 0;
-  cudaStream_t s = ctx->stream;
-  Scratch sc(ctx);
-  const uint64_t launches0 = ctx->launches;
-  record(ctx, timing, 0);
+// One tsg_spgemm call.  The phases share the call's stream, scratch and
+// output bookkeeping, so they are members of one object; spgemm_impl runs
+// them in order (the pass chain of spgemm_square, kernels.cpp:222-302).
+struct Call {
+  tsg_ctx* ctx;
+  const tsg_csr* Ain;
+  const tsg_csr* Bin;
+  tsg_csr_out* C;
+  const tsg_options& opt;
+  tsg_run_stats* st;
+  const bool timing;
+  cudaStream_t s;
+  Scratch sc;
+  uint64_t launches0;
 
-  // device scalars: [0] error flags, [1] max A tiles per tile row
-  auto* dscal = sc.alloc<unsigned>(2);
-  TSG_CUDA(cudaMemsetAsync(dscal, 0, 2 * sizeof(unsigned), s));
-  unsigned* err_flag = dscal;
-
-  const bool same = Ain == Bin ||
-                    (Ain->row_ptr == Bin->row_ptr && Ain->col == Bin->col && Ain->val == Bin->val &&
-                     Ain->rows == Bin->rows && Ain->cols == Bin->cols && Ain->mem == Bin->mem &&
-                     Ain->dtype == Bin->dtype && Ain->nnz == Bin->nnz);
-  const CsrView dA = stage(ctx, sc, Ain, st);
-  const CsrView dB = same ? dA : stage(ctx, sc, Bin, st);
-
-  // ---- (1) conversion ------------------------------------------------------
+  unsigned* dscal = nullptr;  // [0] error flags, [1] max A tiles per tile row
+  unsigned* err_flag = nullptr;
+  bool same = false;
+  CsrView dA, dB;
   TileMat TA, TB_own;
-  const uint32_t* ntA_d = convert(ctx, sc, dA, TA, same ? 3 : 1, err_flag, opt.drop_nonfinite);
-  const uint32_t* ntB_d = ntA_d;
-  if (!same) {
-    // only the B tile rows A's tiles refer to are tiled (a row panel of A --
-    // multi-GPU, or any A that touches part of B -- converts its slice of B)
-    auto* needed = sc.alloc<uint8_t>((dB.rows + 15) / 16 + 1);
-    TSG_CUDA(cudaMemsetAsync(needed, 0, (dB.rows + 15) / 16 + 1, s));
-    launch_mark_needed(TA, needed, s);
+  const TileMat* TB = nullptr;
+  uint64_t tA = 0, tB = 0;
+  bool light = false;
+
+  int64_t rows = 0;
+  uint64_t nr = 0;  // tile rows + 1
+  uint64_t P = 0, S = 0, raw = 0, stage_total = 0, counted = 0;
+  int64_t nnzC = 0;
+  OutOwner* owner = nullptr;
+  bool host_done = false;  // the pipelined light path ships the output itself
+  int64_t* d_rp = nullptr;
+  int32_t* d_col = nullptr;
+  float* d_val = nullptr;
+  unsigned long long* counted_d = nullptr;
+  int64_t* rowcnt = nullptr;  // realised entries per CSR row
+
+  Call(tsg_ctx* c, const tsg_csr* a, const tsg_csr* b, tsg_csr_out* out, const tsg_options& o,
+       tsg_run_stats* stats)
+      : ctx(c), Ain(a), Bin(b), C(out), opt(o), st(stats), timing(o.phase_timing != 0), s(c->stream),
+        sc(c), launches0(c->launches) {}
+
+  // ---- (1) validation, staging of host inputs, CSR -> 16x16 tiles ----------------
+  void convert_operands() {
+    check_csr(Ain, "A");
+    check_csr(Bin, "B");
+    if (!C) throw Fail{TSG_ERR_OTHER, "C is NULL"};
+    if (Ain->cols != Bin->rows)
+      throw Fail{TSG_ERR_DIMENSION, "inner dimensions differ: A is " + std::to_string(Ain->rows) + "x" +
+                                        std::to_string(Ain->cols) + ", B is " + std::to_string(Bin->rows) +
+                                        "x" + std::to_string(Bin->cols)};
+    record(ctx, timing, 0);
+    dscal = sc.alloc<unsigned>(2);
+    TSG_CUDA(cudaMemsetAsync(dscal, 0, 2 * sizeof(unsigned), s));
+    err_flag = dscal;
+    same = Ain == Bin || (Ain->row_ptr == Bin->row_ptr && Ain->col == Bin->col && Ain->val == Bin->val &&
+                          Ain->rows == Bin->rows && Ain->cols == Bin->cols && Ain->mem == Bin->mem &&
+                          Ain->dtype == Bin->dtype && Ain->nnz == Bin->nnz);
+    dA = stage(ctx, sc, Ain, st);
+    dB = same ? dA : stage(ctx, sc, Bin, st);
+    const uint32_t* ntA_d = convert(ctx, sc, dA, TA, same ? 3 : 1, err_flag, opt.drop_nonfinite);
+    const uint32_t* ntB_d = ntA_d;
+    if (!same) {
+      // only the B tile rows A's tiles refer to are tiled (a row panel of A --
+      // multi-GPU, or any A that touches part of B -- converts its slice of B)
+      auto* needed = sc.alloc<uint8_t>((dB.rows + 15) / 16 + 1);
+      TSG_CUDA(cudaMemsetAsync(needed, 0, (dB.rows + 15) / 16 + 1, s));
+      launch_mark_needed(TA, needed, s);
+      check_launch(ctx);
+      ntB_d = convert(ctx, sc, dB, TB_own, 2, err_flag, opt.drop_nonfinite, needed);
+    }
+    TB = same ? &TA : &TB_own;
+    launch_row_stats(TA, dscal + 1, s);
     check_launch(ctx);
-    ntB_d = convert(ctx, sc, dB, TB_own, 2, err_flag, opt.drop_nonfinite, needed);
-  }
-  const TileMat& TB = same ? TA : TB_own;
-  launch_row_stats(TA, dscal + 1, s);
-  check_launch(ctx);
-  uint64_t tA, tB;
-  bool light;
-  {
     const unsigned* src[4] = {dscal, dscal + 1, ntA_d, ntB_d};
     unsigned v[4];
     readback_many(ctx, src, v);
@@ -383,61 +410,52 @@ void spgemm_impl(tsg_ctx* ctx, const tsg_csr* Ain, const tsg_csr* Bin, tsg_csr_o
     light = v[1] <= 32;
     tA = v[2];
     tB = v[3];
-  }
-  record(ctx, timing, 1);
+    record(ctx, timing, 1);
 
-  const int64_t rows = Ain->rows;
-  const uint64_t nr = uint64_t(TA.tile_rows) + 1;
-  uint64_t P = 0, S = 0, raw = 0, stage_total = 0, counted = 0;
-  int64_t nnzC = 0;
-  auto* owner = new OutOwner();
-  bool host_done = false;  // the pipelined light path ships the output itself
-  owner->host = C->mem == TSG_MEM_HOST;
-  C->_owner = owner;  // released by free_out on any later failure
-  int64_t* d_rp = owner->host ? sc.alloc<int64_t>(rows + 1) : sc.alloc<int64_t>(rows + 1, true);
-  if (!owner->host) owner->p[0] = d_rp;
-  int32_t* d_col = nullptr;
-  float* d_val = nullptr;
-  auto* counted_d = sc.alloc<unsigned long long>(1);
-  TSG_CUDA(cudaMemsetAsync(counted_d, 0, sizeof(unsigned long long), s));
-  auto* rowcnt = sc.alloc<int64_t>(rows + 1);  // realised entries per CSR row
-  TSG_CUDA(cudaMemsetAsync(rowcnt + rows, 0, sizeof(int64_t), s));
-  // the realised row counts -> row_ptr, nnz(C) and counted elements to the
-  // host (plus, optionally, two more device totals in the same synchronisation)
-  auto scan_rows = [&](const unsigned long long* extra = nullptr, unsigned long long* out = nullptr) {
+    rows = Ain->rows;
+    nr = uint64_t(TA.tile_rows) + 1;
+    owner = new OutOwner();
+    owner->host = C->mem == TSG_MEM_HOST;
+    C->_owner = owner;  // released by free_out on any later failure
+    d_rp = owner->host ? sc.alloc<int64_t>(rows + 1) : sc.alloc<int64_t>(rows + 1, true);
+    if (!owner->host) owner->p[0] = d_rp;
+    counted_d = sc.alloc<unsigned long long>(1);
+    TSG_CUDA(cudaMemsetAsync(counted_d, 0, sizeof(unsigned long long), s));
+    rowcnt = sc.alloc<int64_t>(rows + 1);
+    TSG_CUDA(cudaMemsetAsync(rowcnt + rows, 0, sizeof(int64_t), s));
+  }
+
+  // realised row counts -> row_ptr; nnz(C) and counted elements to the host,
+  // plus (optionally) four more contiguous device totals in the same sync
+  void scan_rows(const unsigned long long* extra = nullptr, unsigned long long* out = nullptr) {
     exclusive_sum(ctx, sc, rowcnt, d_rp, uint64_t(rows) + 1);
     const unsigned long long* nz = reinterpret_cast<const unsigned long long*>(d_rp + rows);
     unsigned long long v[6];
-    if (extra) {  // extra[0..3] (contiguous device totals) in the same synchronisation
+    if (extra) {
       const unsigned long long* src[6] = {counted_d, nz, extra, extra + 1, extra + 2, extra + 3};
       readback_many(ctx, src, v);
       for (int i = 0; i < 4; ++i) out[i] = v[2 + i];
     } else {
       const unsigned long long* src[2] = {counted_d, nz};
-      unsigned long long w[2];
-      readback_many(ctx, src, w);
-      v[0] = w[0];
-      v[1] = w[1];
+      readback_many(ctx, src, *reinterpret_cast<unsigned long long(*)[2]>(v));
     }
     counted = v[0];
     nnzC = int64_t(v[1]);
     if (uint64_t(nnzC) >= (uint64_t(1) << 32))
       throw Fail{TSG_ERR_OTHER, "output beyond 2^32 elements needs row-panel batching"};
-  };
-  auto alloc_out = [&]() {
+  }
+
+  void alloc_out() {
     d_col = sc.alloc<int32_t>(nnzC, !owner->host);
     d_val = sc.alloc<float>(nnzC, !owner->host);
     if (!owner->host) {
       owner->p[1] = d_col;
       owner->p[2] = d_val;
     }
-  };
-  auto finish_rows = [&]() {
-    scan_rows();
-    alloc_out();
-  };
+  }
+
   // grow-only staging arena (bytes)
-  auto arena = [&](size_t need) -> void* {
+  void* arena(size_t need) {
     need = std::max<size_t>(need, 16);
     if (need > ctx->stage_cap) {
       if (ctx->stage_buf) TSG_CUDA(cudaFreeAsync(ctx->stage_buf, s));
@@ -448,20 +466,25 @@ void spgemm_impl(tsg_ctx* ctx, const tsg_csr* Ain, const tsg_csr* Bin, tsg_csr_o
       ctx->stage_cap = cap;
     }
     return ctx->stage_buf;
-  };
+  }
 
-  if (light) {
-    // ---- light rows: one fused pass per tile row (tsg_panel.cu) -----------------
+  void check_stage_total() const {
+    if (stage_total >= (uint64_t(1) << 32))
+      throw Fail{TSG_ERR_OTHER, "staged slots beyond 2^32 need row-panel batching"};
+  }
+
+  // ---- light rows: one fused pass per tile row (tsg_panel.cu) --------------------
+  void light_path() {
     auto* row_np = sc.alloc<uint32_t>(nr);
     auto* row_ns = sc.alloc<uint32_t>(nr);
     auto* row_raw = sc.alloc<uint32_t>(nr);
     auto* row_bound = sc.alloc<uint32_t>(rows + 1);
     auto* row_stage = sc.alloc<uint32_t>(rows + 1);
     TSG_CUDA(cudaMemsetAsync(row_bound + rows, 0, 4, s));
-    launch_panel_count(TA, TB, rows, row_np, row_ns, row_raw, row_bound, s);
+    launch_panel_count(TA, *TB, rows, row_np, row_ns, row_raw, row_bound, s);
     check_launch(ctx);
     exclusive_sum(ctx, sc, row_bound, row_stage, uint64_t(rows) + 1);
-    // exact u64 totals (guard the u32 staging offsets)
+    // exact u64 totals: P, S, raw pairs, staging slots (guards the u32 offsets)
     auto* tot_d = sc.alloc<unsigned long long>(4);
     TSG_CUDA(cudaMemsetAsync(tot_d, 0, 4 * sizeof(unsigned long long), s));
     {
@@ -473,16 +496,18 @@ void spgemm_impl(tsg_ctx* ctx, const tsg_csr* Ain, const tsg_csr* Bin, tsg_csr_o
       sum_u32_kernel<<<blocks, 256, 0, s>>>(row_bound, uint64_t(rows), tot_d + 3);
       check_launch(ctx, 4);
     }
-    auto read_totals = [&]() {
-      const unsigned long long* src[4] = {tot_d, tot_d + 1, tot_d + 2, tot_d + 3};
-      unsigned long long v[4];
-      readback_many(ctx, src, v);
+    auto take_totals = [&](const unsigned long long (&v)[4]) {
       P = v[0];
       S = v[1];
       raw = v[2];
       stage_total = v[3];
-      if (stage_total >= (uint64_t(1) << 32))
-        throw Fail{TSG_ERR_OTHER, "staged slots beyond 2^32 need row-panel batching"};
+      check_stage_total();
+    };
+    auto read_totals = [&]() {
+      const unsigned long long* src[4] = {tot_d, tot_d + 1, tot_d + 2, tot_d + 3};
+      unsigned long long v[4];
+      readback_many(ctx, src, v);
+      take_totals(v);
     };
     // Device output with a staging arena already in place: launch the panel
     // pass without reading the staging total back first; the kernel checks it
@@ -494,111 +519,109 @@ void spgemm_impl(tsg_ctx* ctx, const tsg_csr* Ain, const tsg_csr* Bin, tsg_csr_o
     record(ctx, timing, 3);  // the merge is the sort: no separate phase
     record(ctx, timing, 4);  // the counting pass is fused into the numeric pass
     uint2* stage = static_cast<uint2*>(speculative ? ctx->stage_buf : arena(stage_total * sizeof(uint2)));
-    uint64_t stage_cap_slots = speculative ? ctx->stage_cap / sizeof(uint2) : stage_total;
+    uint64_t cap_slots = speculative ? ctx->stage_cap / sizeof(uint2) : stage_total;
     if (timing) TSG_CUDA(cudaEventRecord(ctx->kev[0], s));
-    if (!owner->host || TA.tile_rows < 8 * kPipeChunks) {
-      launch_panel_numeric(TA, TB, rows, row_stage, stage_cap_slots, stage, rowcnt, counted_d, opt.mode, 0,
-                           TA.tile_rows, s);
-      check_launch(ctx);
-      if (timing) TSG_CUDA(cudaEventRecord(ctx->kev[1], s));
-      record(ctx, timing, 5);
-      if (speculative) {
-        // one synchronisation: counted, nnz(C), P, S, raw pairs, staging total
-        unsigned long long t[4];
-        scan_rows(tot_d, t);
-        P = t[0];
-        S = t[1];
-        raw = t[2];
-        stage_total = t[3];
-        if (stage_total >= (uint64_t(1) << 32))
-          throw Fail{TSG_ERR_OTHER, "staged slots beyond 2^32 need row-panel batching"};
-        if (stage_total > stage_cap_slots) {  // the rare arena overflow: redo the pass
-          read_totals();
-          stage = static_cast<uint2*>(arena(stage_total * sizeof(uint2)));
-          stage_cap_slots = stage_total;
-          TSG_CUDA(cudaMemsetAsync(counted_d, 0, sizeof(unsigned long long), s));
-          launch_panel_numeric(TA, TB, rows, row_stage, stage_cap_slots, stage, rowcnt, counted_d, opt.mode, 0,
-                               TA.tile_rows, s);
-          check_launch(ctx);
-          scan_rows();
-        }
-        alloc_out();
-      } else {
-        finish_rows();
-      }
-      if (timing) TSG_CUDA(cudaEventRecord(ctx->kev[2], s));
-      launch_panel_copy(rows, row_stage, d_rp, stage, d_col, d_val, err_flag, 0, TA.tile_rows, s);
-      check_launch(ctx);
-      if (timing) TSG_CUDA(cudaEventRecord(ctx->kev[3], s));
-      record(ctx, timing, 6);
-    } else {
-      // Host output: the result crosses PCIe (the slowest leg), so the panel
-      // pass runs in kPipeChunks tile-row chunks and chunk c's CSR slice
-      // goes to the host on a second stream while chunk c+1 computes.  Row
-      // pointers are a chained scan (each chunk starts from the previous
-      // chunk's end, read on the device); host buffers are sized by the
-      // staging bound, an upper bound on nnz(C).
-      TSG_CUDA(cudaMemsetAsync(d_rp, 0, sizeof(int64_t), s));
-      owner->p[0] = pinned_alloc(ctx, (rows + 1) * sizeof(int64_t), &owner->sz[0]);
-      owner->p[1] = pinned_alloc(ctx, std::max<uint64_t>(stage_total, 1) * sizeof(int32_t), &owner->sz[1]);
-      owner->p[2] = pinned_alloc(ctx, std::max<uint64_t>(stage_total, 1) * sizeof(float), &owner->sz[2]);
-      d_col = sc.alloc<int32_t>(stage_total);
-      d_val = sc.alloc<float>(stage_total);
-      auto* ends = reinterpret_cast<int64_t*>(ctx->pinned_pipe);  // d_rp at each chunk end
-      size_t tmp_bytes = 0;
-      TSG_CUDA(cub::DeviceScan::ExclusiveScan(nullptr, tmp_bytes, rowcnt, d_rp, cuda::std::plus<int64_t>(),
-                                              cub::FutureValue<int64_t>(d_rp), rows + 1, s));
-      void* tmp = sc.alloc<char>(tmp_bytes);
-      uint64_t sent = 0;  // entries already queued for the host
-      auto ship = [&](int c) {  // chunk c's column/value slice -> host (stream 2)
-        TSG_CUDA(cudaEventSynchronize(ctx->pipe_ev[c]));  // its end is readable now
-        const uint64_t hi = uint64_t(ends[c]);
-        TSG_CUDA(cudaStreamWaitEvent(ctx->d2h, ctx->pipe_ev[c], 0));
-        if (hi > sent) {
-          TSG_CUDA(cudaMemcpyAsync(static_cast<int32_t*>(owner->p[1]) + sent, d_col + sent, (hi - sent) * 4,
-                                   cudaMemcpyDeviceToHost, ctx->d2h));
-          TSG_CUDA(cudaMemcpyAsync(static_cast<float*>(owner->p[2]) + sent, d_val + sent, (hi - sent) * 4,
-                                   cudaMemcpyDeviceToHost, ctx->d2h));
-        }
-        sent = hi;
-      };
-      for (int c = 0; c < kPipeChunks; ++c) {
-        const uint32_t I0 = uint32_t(uint64_t(TA.tile_rows) * c / kPipeChunks);
-        const uint32_t I1 = uint32_t(uint64_t(TA.tile_rows) * (c + 1) / kPipeChunks);
-        const int64_t r0 = int64_t(I0) * 16, r1 = std::min<int64_t>(int64_t(I1) * 16, rows);
-        launch_panel_numeric(TA, TB, rows, row_stage, stage_cap_slots, stage, rowcnt, counted_d, opt.mode, I0, I1,
-                             s);
-        check_launch(ctx);
-        // row_ptr[r0 .. r1] = row_ptr[r0] + exclusive prefix (row_ptr[r0] from the previous chunk)
-        TSG_CUDA(cub::DeviceScan::ExclusiveScan(tmp, tmp_bytes, rowcnt + r0, d_rp + r0,
-                                                cuda::std::plus<int64_t>(), cub::FutureValue<int64_t>(d_rp + r0),
-                                                r1 - r0 + 1, s));
-        launch_panel_copy(rows, row_stage, d_rp, stage, d_col, d_val, err_flag, I0, I1, s);
-        check_launch(ctx);
-        TSG_CUDA(cudaMemcpyAsync(ends + c, d_rp + r1, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
-        TSG_CUDA(cudaEventRecord(ctx->pipe_ev[c], s));
-        if (c > 0) ship(c - 1);
-      }
-      ship(kPipeChunks - 1);
-      nnzC = int64_t(sent);
-      if (uint64_t(nnzC) >= (uint64_t(1) << 32))
-        throw Fail{TSG_ERR_OTHER, "output beyond 2^32 elements needs row-panel batching"};
-      counted = readback(ctx, counted_d);
-      TSG_CUDA(cudaMemcpyAsync(owner->p[0], d_rp, (rows + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->d2h));
-      TSG_CUDA(cudaEventRecord(ctx->pipe_ev[kPipeChunks], ctx->d2h));
-      TSG_CUDA(cudaStreamWaitEvent(s, ctx->pipe_ev[kPipeChunks], 0));  // the final sync covers stream 2
-      if (st) st->d2h_bytes += (rows + 1) * sizeof(int64_t) + uint64_t(nnzC) * 8;
-      host_done = true;
-      if (timing) {
-        TSG_CUDA(cudaEventRecord(ctx->kev[1], s));
-        TSG_CUDA(cudaEventRecord(ctx->kev[2], s));
-        TSG_CUDA(cudaEventRecord(ctx->kev[3], s));
-      }
-      record(ctx, timing, 5);
-      record(ctx, timing, 6);
+    if (owner->host && TA.tile_rows >= 8 * kPipeChunks) {
+      light_host_pipelined(row_stage, stage, cap_slots);
+      return;
     }
-  } else {
-    // ---- general rows: task list, sort, numeric, assembly --------------------------
+    launch_panel_numeric(TA, *TB, rows, row_stage, cap_slots, stage, rowcnt, counted_d, opt.mode, 0, TA.tile_rows,
+                         s);
+    check_launch(ctx);
+    if (timing) TSG_CUDA(cudaEventRecord(ctx->kev[1], s));
+    record(ctx, timing, 5);
+    if (speculative) {
+      unsigned long long t[4];
+      scan_rows(tot_d, t);  // one synchronisation: counted, nnz(C), P, S, raw, staging slots
+      take_totals(t);
+      if (stage_total > cap_slots) {  // the rare arena overflow: redo the pass
+        stage = static_cast<uint2*>(arena(stage_total * sizeof(uint2)));
+        cap_slots = stage_total;
+        TSG_CUDA(cudaMemsetAsync(counted_d, 0, sizeof(unsigned long long), s));
+        launch_panel_numeric(TA, *TB, rows, row_stage, cap_slots, stage, rowcnt, counted_d, opt.mode, 0,
+                             TA.tile_rows, s);
+        check_launch(ctx);
+        scan_rows();
+      }
+    } else {
+      scan_rows();
+    }
+    alloc_out();
+    if (timing) TSG_CUDA(cudaEventRecord(ctx->kev[2], s));
+    launch_panel_copy(rows, row_stage, d_rp, stage, d_col, d_val, err_flag, 0, TA.tile_rows, s);
+    check_launch(ctx);
+    if (timing) TSG_CUDA(cudaEventRecord(ctx->kev[3], s));
+    record(ctx, timing, 6);
+  }
+
+  // Host output: the result crosses PCIe (the slowest leg), so the panel pass
+  // runs in kPipeChunks tile-row chunks and chunk c's CSR slice goes to the
+  // host on a second stream while chunk c+1 computes.  Row pointers are a
+  // chained scan (each chunk starts from the previous chunk's end, read on
+  // the device); host buffers are sized by the staging bound, an upper bound
+  // on nnz(C).
+  void light_host_pipelined(const uint32_t* row_stage, uint2* stage, uint64_t cap_slots) {
+    TSG_CUDA(cudaMemsetAsync(d_rp, 0, sizeof(int64_t), s));
+    owner->p[0] = pinned_alloc(ctx, (rows + 1) * sizeof(int64_t), &owner->sz[0]);
+    owner->p[1] = pinned_alloc(ctx, std::max<uint64_t>(stage_total, 1) * sizeof(int32_t), &owner->sz[1]);
+    owner->p[2] = pinned_alloc(ctx, std::max<uint64_t>(stage_total, 1) * sizeof(float), &owner->sz[2]);
+    d_col = sc.alloc<int32_t>(stage_total);
+    d_val = sc.alloc<float>(stage_total);
+    auto* ends = reinterpret_cast<int64_t*>(ctx->pinned_pipe);  // row_ptr at each chunk end
+    size_t tmp_bytes = 0;
+    TSG_CUDA(cub::DeviceScan::ExclusiveScan(nullptr, tmp_bytes, rowcnt, d_rp, cuda::std::plus<int64_t>(),
+                                            cub::FutureValue<int64_t>(d_rp), rows + 1, s));
+    void* tmp = sc.alloc<char>(tmp_bytes);
+    uint64_t sent = 0;  // entries already queued for the host
+    auto ship = [&](int c) {  // chunk c's column/value slice -> host (stream 2)
+      TSG_CUDA(cudaEventSynchronize(ctx->pipe_ev[c]));  // its end is readable now
+      const uint64_t hi = uint64_t(ends[c]);
+      TSG_CUDA(cudaStreamWaitEvent(ctx->d2h, ctx->pipe_ev[c], 0));
+      if (hi > sent) {
+        TSG_CUDA(cudaMemcpyAsync(static_cast<int32_t*>(owner->p[1]) + sent, d_col + sent, (hi - sent) * 4,
+                                 cudaMemcpyDeviceToHost, ctx->d2h));
+        TSG_CUDA(cudaMemcpyAsync(static_cast<float*>(owner->p[2]) + sent, d_val + sent, (hi - sent) * 4,
+                                 cudaMemcpyDeviceToHost, ctx->d2h));
+      }
+      sent = hi;
+    };
+    for (int c = 0; c < kPipeChunks; ++c) {
+      const uint32_t I0 = uint32_t(uint64_t(TA.tile_rows) * c / kPipeChunks);
+      const uint32_t I1 = uint32_t(uint64_t(TA.tile_rows) * (c + 1) / kPipeChunks);
+      const int64_t r0 = int64_t(I0) * 16, r1 = std::min<int64_t>(int64_t(I1) * 16, rows);
+      launch_panel_numeric(TA, *TB, rows, row_stage, cap_slots, stage, rowcnt, counted_d, opt.mode, I0, I1, s);
+      check_launch(ctx);
+      // row_ptr[r0 .. r1] = row_ptr[r0] + exclusive prefix (row_ptr[r0] from the previous chunk)
+      TSG_CUDA(cub::DeviceScan::ExclusiveScan(tmp, tmp_bytes, rowcnt + r0, d_rp + r0, cuda::std::plus<int64_t>(),
+                                              cub::FutureValue<int64_t>(d_rp + r0), r1 - r0 + 1, s));
+      launch_panel_copy(rows, row_stage, d_rp, stage, d_col, d_val, err_flag, I0, I1, s);
+      check_launch(ctx);
+      TSG_CUDA(cudaMemcpyAsync(ends + c, d_rp + r1, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+      TSG_CUDA(cudaEventRecord(ctx->pipe_ev[c], s));
+      if (c > 0) ship(c - 1);
+    }
+    ship(kPipeChunks - 1);
+    nnzC = int64_t(sent);
+    if (uint64_t(nnzC) >= (uint64_t(1) << 32))
+      throw Fail{TSG_ERR_OTHER, "output beyond 2^32 elements needs row-panel batching"};
+    counted = readback(ctx, counted_d);
+    TSG_CUDA(cudaMemcpyAsync(owner->p[0], d_rp, (rows + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->d2h));
+    TSG_CUDA(cudaEventRecord(ctx->pipe_ev[kPipeChunks], ctx->d2h));
+    TSG_CUDA(cudaStreamWaitEvent(s, ctx->pipe_ev[kPipeChunks], 0));  // the final sync covers stream 2
+    if (st) st->d2h_bytes += (rows + 1) * sizeof(int64_t) + uint64_t(nnzC) * 8;
+    host_done = true;
+    if (timing) {
+      TSG_CUDA(cudaEventRecord(ctx->kev[1], s));
+      TSG_CUDA(cudaEventRecord(ctx->kev[2], s));
+      TSG_CUDA(cudaEventRecord(ctx->kev[3], s));
+    }
+    record(ctx, timing, 5);
+    record(ctx, timing, 6);
+  }
+
+  // ---- general rows: task list, sort, numeric, assembly ----------------------------
+  void general_path() {
+    const TileMat& B = *TB;
     TaskList tl;
     tl.seg_row_ptr = sc.alloc<uint32_t>(nr);
     uint32_t* row_pair_off = sc.alloc<uint32_t>(nr);
@@ -607,12 +630,11 @@ void spgemm_impl(tsg_ctx* ctx, const tsg_csr* Ain, const tsg_csr* Bin, tsg_csr_o
     auto* tile_off = sc.alloc<uint32_t>(tA + 1);
     auto* tile_cnt = sc.alloc<uint32_t>(tA + 1);
     TSG_CUDA(cudaMemsetAsync(tile_cnt + tA, 0, sizeof(uint32_t), s));
-    launch_enum_count(TA, TB, tA, tile_cnt, raw_d, s);
+    launch_enum_count(TA, B, tA, tile_cnt, raw_d, s);
     check_launch(ctx);
     P = total_u32(ctx, sc, tile_cnt, tA);
     raw = readback(ctx, raw_d);
-    if (P >= (uint64_t(1) << 31))
-      throw Fail{TSG_ERR_OTHER, "task list beyond 2^31 pairs needs row-panel batching"};
+    if (P >= (uint64_t(1) << 31)) throw Fail{TSG_ERR_OTHER, "task list beyond 2^31 pairs needs row-panel batching"};
     exclusive_sum(ctx, sc, tile_cnt, tile_off, tA + 1);
     tl.npairs = P;
     uint64_t* pairs_u = sc.alloc<uint64_t>(P);
@@ -622,11 +644,11 @@ void spgemm_impl(tsg_ctx* ctx, const tsg_csr* Ain, const tsg_csr* Bin, tsg_csr_o
       while ((uint64_t(1) << b) < n) ++b;
       return b;
     };
-    const uint32_t jbits = bits_of(TB.tile_cols), ibits = bits_of(TA.tile_rows);
+    const uint32_t jbits = bits_of(B.tile_cols), ibits = bits_of(TA.tile_rows);
     // the tile row rides in the key's high bits when it fits (radix sort);
     // otherwise keys are the column alone (segmented sort per tile row)
-    const uint32_t key_shift = jbits + ibits <= 32 ? jbits : 32;
-    launch_enum_fill(TA, TB, tA, tile_off, pairs_u, keys_u, key_shift, s);
+    const bool radix = jbits + ibits <= 32;
+    launch_enum_fill(TA, B, tA, tile_off, pairs_u, keys_u, radix ? jbits : 32, s);
     check_launch(ctx);
     launch_row_pair_off(TA, tile_off, row_pair_off, s);
     check_launch(ctx);
@@ -634,7 +656,7 @@ void spgemm_impl(tsg_ctx* ctx, const tsg_csr* Ain, const tsg_csr* Bin, tsg_csr_o
     // stable sort by output tile column within each tile row
     uint64_t* pairs = sc.alloc<uint64_t>(P + 1);
     uint32_t* keys = sc.alloc<uint32_t>(P);
-    if (P > 0 && jbits + ibits <= 32) {
+    if (P > 0 && radix) {
       // keys are (tile row << jbits | tile col): one stable LSD radix sort of
       // just the key bits in use (tiles are enumerated in row order, so this
       // is the per-tile-row sort by output column, k order kept by stability)
@@ -646,13 +668,11 @@ void spgemm_impl(tsg_ctx* ctx, const tsg_csr* Ain, const tsg_csr* Bin, tsg_csr_o
                                                int(jbits + ibits), s));
     } else if (P > 0) {
       size_t bytes = 0;
-      TSG_CUDA(cub::DeviceSegmentedSort::StableSortPairs(nullptr, bytes, keys_u, keys, pairs_u,
-                                                         pairs, int(P), int(TA.tile_rows),
-                                                         row_pair_off, row_pair_off + 1, s));
+      TSG_CUDA(cub::DeviceSegmentedSort::StableSortPairs(nullptr, bytes, keys_u, keys, pairs_u, pairs, int(P),
+                                                         int(TA.tile_rows), row_pair_off, row_pair_off + 1, s));
       void* tmp = sc.alloc<char>(bytes);
-      TSG_CUDA(cub::DeviceSegmentedSort::StableSortPairs(tmp, bytes, keys_u, keys, pairs_u,
-                                                         pairs, int(P), int(TA.tile_rows),
-                                                         row_pair_off, row_pair_off + 1, s));
+      TSG_CUDA(cub::DeviceSegmentedSort::StableSortPairs(tmp, bytes, keys_u, keys, pairs_u, pairs, int(P),
+                                                         int(TA.tile_rows), row_pair_off, row_pair_off + 1, s));
     }
     auto* row_nseg = sc.alloc<uint32_t>(nr);
     TSG_CUDA(cudaMemsetAsync(row_nseg + nr - 1, 0, sizeof(uint32_t), s));
@@ -671,11 +691,10 @@ void spgemm_impl(tsg_ctx* ctx, const tsg_csr* Ain, const tsg_csr* Bin, tsg_csr_o
     tl.pmeta = sc.alloc<uint4>(P + 1);
     tl.pocc = sc.alloc<uint2>(P + 1);
     auto* pair_bound = sc.alloc<uint32_t>(P + 1);
-    launch_pair_meta(TA, TB, pairs, tl, pair_bound, s);
+    launch_pair_meta(TA, B, pairs, tl, pair_bound, s);
     check_launch(ctx);
     stage_total = total_u32(ctx, sc, pair_bound, P);
-    if (stage_total >= (uint64_t(1) << 32))
-      throw Fail{TSG_ERR_OTHER, "staged slots beyond 2^32 need row-panel batching"};
+    check_stage_total();
     auto* pair_stage = sc.alloc<uint32_t>(P + 1);
     exclusive_sum(ctx, sc, pair_bound, pair_stage, P + 1);
     launch_seg_stage(tl, pair_stage, s);
@@ -694,7 +713,7 @@ void spgemm_impl(tsg_ctx* ctx, const tsg_csr* Ain, const tsg_csr* Bin, tsg_csr_o
     auto* list = sc.alloc<uint32_t>(S);
     auto* list_len = sc.alloc<uint32_t>(1);
     TSG_CUDA(cudaMemsetAsync(list_len, 0, sizeof(uint32_t), s));
-    launch_numeric_thin(tl, TA, TB, sg, heavy, s);
+    launch_numeric_thin(tl, TA, B, sg, heavy, s);
     check_launch(ctx);
     if (S > 0) {
       cub::CountingInputIterator<uint32_t> ids(0);
@@ -703,12 +722,12 @@ void spgemm_impl(tsg_ctx* ctx, const tsg_csr* Ain, const tsg_csr* Bin, tsg_csr_o
       void* tmp = sc.alloc<char>(bytes);
       TSG_CUDA(cub::DeviceSelect::Flagged(tmp, bytes, ids, heavy, list, list_len, int64_t(S), s));
     }
-    launch_numeric(tl, TA, TB, sg, opt.mode, list, list_len, s);
+    launch_numeric(tl, TA, B, sg, opt.mode, list, list_len, s);
     check_launch(ctx);
     if (timing) TSG_CUDA(cudaEventRecord(ctx->kev[1], s));
     record(ctx, timing, 5);
 
-    // tiled -> CSR: realised row counts, scan, assembly
+    // tiled -> CSR: segment chunks, realised (chunk, row) counts, scan, assembly
     AsmChunks ch;
     const uint64_t max_chunks = uint64_t(TA.tile_rows) + S / kChunkSegs + 1;
     ch.n = sc.alloc<uint32_t>(1);
@@ -719,13 +738,14 @@ void spgemm_impl(tsg_ctx* ctx, const tsg_csr* Ain, const tsg_csr* Bin, tsg_csr_o
     auto* nchunks = sc.alloc<uint32_t>(nr);
     auto* chunk_base = sc.alloc<uint32_t>(nr);
     TSG_CUDA(cudaMemsetAsync(nchunks + nr - 1, 0, 4, s));
-    launch_asm_chunks(TA.tile_rows, tl.seg_row_ptr, nchunks, chunk_base, ch, s);
+    launch_asm_chunks(TA.tile_rows, tl.seg_row_ptr, nchunks, s);
     exclusive_sum(ctx, sc, nchunks, chunk_base, nr);
     launch_asm_chunk_fill(TA.tile_rows, tl.seg_row_ptr, chunk_base, ch, s);
     TSG_CUDA(cudaMemsetAsync(rowcnt, 0, (rows + 1) * sizeof(int64_t), s));
     launch_row_counts(rows, ch, max_chunks, sg, rowcnt, s);
     check_launch(ctx, 3);
-    finish_rows();
+    scan_rows();
+    alloc_out();
     launch_chunk_offsets(rows, TA.tile_rows, chunk_base, d_rp, ch, s);
     check_launch(ctx);
     if (timing) TSG_CUDA(cudaEventRecord(ctx->kev[2], s));
@@ -734,75 +754,88 @@ void spgemm_impl(tsg_ctx* ctx, const tsg_csr* Ain, const tsg_csr* Bin, tsg_csr_o
     if (timing) TSG_CUDA(cudaEventRecord(ctx->kev[3], s));
     record(ctx, timing, 6);
   }
-  // non-finite accumulators are flagged by the assembly (read at the final sync)
-  unsigned* flags_host = reinterpret_cast<unsigned*>(reinterpret_cast<char*>(ctx->pinned) + 56);
-  TSG_CUDA(cudaMemcpyAsync(flags_host, err_flag, 4, cudaMemcpyDeviceToHost, s));
 
-  C->rows = Ain->rows;
-  C->cols = Bin->cols;
-  C->nnz = nnzC;
-  if (owner->host && !host_done) {
-    owner->p[0] = pinned_alloc(ctx, (rows + 1) * sizeof(int64_t), &owner->sz[0]);
-    owner->p[1] = pinned_alloc(ctx, nnzC * sizeof(int32_t), &owner->sz[1]);
-    owner->p[2] = pinned_alloc(ctx, nnzC * sizeof(float), &owner->sz[2]);
-    TSG_CUDA(cudaMemcpyAsync(owner->p[0], d_rp, (rows + 1) * sizeof(int64_t),
-                             cudaMemcpyDeviceToHost, s));
-    if (nnzC) {
-      TSG_CUDA(cudaMemcpyAsync(owner->p[1], d_col, nnzC * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
-      TSG_CUDA(cudaMemcpyAsync(owner->p[2], d_val, nnzC * sizeof(float), cudaMemcpyDeviceToHost, s));
+  // ---- output hand-off, error flags, phase times and counters ----------------------
+  void finish(tsg_tiles_out* tiles) {
+    // non-finite accumulators are flagged by the CSR pass (read at the final sync)
+    unsigned* flags_host = reinterpret_cast<unsigned*>(reinterpret_cast<char*>(ctx->pinned) + 56);
+    TSG_CUDA(cudaMemcpyAsync(flags_host, err_flag, 4, cudaMemcpyDeviceToHost, s));
+    C->rows = Ain->rows;
+    C->cols = Bin->cols;
+    C->nnz = nnzC;
+    if (owner->host && !host_done) {
+      owner->p[0] = pinned_alloc(ctx, (rows + 1) * sizeof(int64_t), &owner->sz[0]);
+      owner->p[1] = pinned_alloc(ctx, nnzC * sizeof(int32_t), &owner->sz[1]);
+      owner->p[2] = pinned_alloc(ctx, nnzC * sizeof(float), &owner->sz[2]);
+      TSG_CUDA(cudaMemcpyAsync(owner->p[0], d_rp, (rows + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+      if (nnzC) {
+        TSG_CUDA(cudaMemcpyAsync(owner->p[1], d_col, nnzC * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+        TSG_CUDA(cudaMemcpyAsync(owner->p[2], d_val, nnzC * sizeof(float), cudaMemcpyDeviceToHost, s));
+      }
+      if (st) st->d2h_bytes += (rows + 1) * sizeof(int64_t) + nnzC * (sizeof(int32_t) + sizeof(float));
     }
-    if (st) st->d2h_bytes += (rows + 1) * sizeof(int64_t) + nnzC * (sizeof(int32_t) + sizeof(float));
-  }
-  C->row_ptr = static_cast<int64_t*>(owner->p[0]);
-  C->col = static_cast<int32_t*>(owner->p[1]);
-  C->val = static_cast<float*>(owner->p[2]);
+    C->row_ptr = static_cast<int64_t*>(owner->p[0]);
+    C->col = static_cast<int32_t*>(owner->p[1]);
+    C->val = static_cast<float*>(owner->p[2]);
 
-  TSG_CUDA(cudaStreamSynchronize(s));
-  raise_flags(*flags_host);
-  if (tiles) {  // test path: 16x16 tiled view of the realised C
-    std::vector<int64_t> h_rp(rows + 1);
-    std::vector<int32_t> h_col(nnzC);
-    std::vector<float> h_val(nnzC);
-    TSG_CUDA(cudaMemcpy(h_rp.data(), d_rp, (rows + 1) * 8, cudaMemcpyDeviceToHost));
-    if (nnzC) {
-      TSG_CUDA(cudaMemcpy(h_col.data(), d_col, nnzC * 4, cudaMemcpyDeviceToHost));
-      TSG_CUDA(cudaMemcpy(h_val.data(), d_val, nnzC * 4, cudaMemcpyDeviceToHost));
+    TSG_CUDA(cudaStreamSynchronize(s));
+    raise_flags(*flags_host);
+    if (tiles) {  // test path: 16x16 tiled view of the realised C
+      std::vector<int64_t> h_rp(rows + 1);
+      std::vector<int32_t> h_col(nnzC);
+      std::vector<float> h_val(nnzC);
+      TSG_CUDA(cudaMemcpy(h_rp.data(), d_rp, (rows + 1) * 8, cudaMemcpyDeviceToHost));
+      if (nnzC) {
+        TSG_CUDA(cudaMemcpy(h_col.data(), d_col, nnzC * 4, cudaMemcpyDeviceToHost));
+        TSG_CUDA(cudaMemcpy(h_val.data(), d_val, nnzC * 4, cudaMemcpyDeviceToHost));
+      }
+      tiles_from_csr(rows, h_rp, h_col, h_val, tiles);
     }
-    tiles_from_csr(rows, h_rp, h_col, h_val, tiles);
-  }
-  if (timing) {
-    float ms[7] = {0};
-    for (int i = 1; i <= 6; ++i) TSG_CUDA(cudaEventElapsedTime(&ms[i], ctx->ev[i - 1], ctx->ev[i]));
-    float tot = 0;
-    TSG_CUDA(cudaEventElapsedTime(&tot, ctx->ev[0], ctx->ev[6]));
-    for (int i = 1; i <= 6; ++i) ctx->last_phase_ms[i] = ms[i];
-    ctx->last_phase_ms[7] = tot;
-    float kn = 0, kc = 0;
-    TSG_CUDA(cudaEventElapsedTime(&kn, ctx->kev[0], ctx->kev[1]));
-    TSG_CUDA(cudaEventElapsedTime(&kc, ctx->kev[2], ctx->kev[3]));
-    ctx->last_numeric_kernel_ms = kn;
-    ctx->last_assemble_kernel_ms = kc;
+    if (timing) {
+      float ms[7] = {0};
+      for (int i = 1; i <= 6; ++i) TSG_CUDA(cudaEventElapsedTime(&ms[i], ctx->ev[i - 1], ctx->ev[i]));
+      float tot = 0;
+      TSG_CUDA(cudaEventElapsedTime(&tot, ctx->ev[0], ctx->ev[6]));
+      for (int i = 1; i <= 6; ++i) ctx->last_phase_ms[i] = ms[i];
+      ctx->last_phase_ms[7] = tot;
+      float kn = 0, kc = 0;
+      TSG_CUDA(cudaEventElapsedTime(&kn, ctx->kev[0], ctx->kev[1]));
+      TSG_CUDA(cudaEventElapsedTime(&kc, ctx->kev[2], ctx->kev[3]));
+      ctx->last_numeric_kernel_ms = kn;
+      ctx->last_assemble_kernel_ms = kc;
+      if (st) {
+        st->convert += ms[1] * 1e-3;
+        st->task_list += ms[2] * 1e-3;
+        st->sort += ms[3] * 1e-3;
+        st->counting += ms[4] * 1e-3;
+        st->multiply += ms[5] * 1e-3;
+        st->compaction += ms[6] * 1e-3;
+        st->total += tot * 1e-3;
+      }
+    }
     if (st) {
-      st->convert += ms[1] * 1e-3;
-      st->task_list += ms[2] * 1e-3;
-      st->sort += ms[3] * 1e-3;
-      st->counting += ms[4] * 1e-3;
-      st->multiply += ms[5] * 1e-3;
-      st->compaction += ms[6] * 1e-3;
-      st->total += tot * 1e-3;
+      st->tiles_a += tA;
+      st->tiles_b += tB;
+      st->raw_pairs += raw;
+      st->filtered_pairs += P;
+      st->segments += S;
+      st->counted_elements += counted;
+      st->nnz_c = uint64_t(nnzC);
+      st->staged_slots += stage_total;
+      st->kernel_launches += ctx->launches - launches0;
     }
   }
-  if (st) {
-    st->tiles_a += tA;
-    st->tiles_b += tB;
-    st->raw_pairs += raw;
-    st->filtered_pairs += P;
-    st->segments += S;
-    st->counted_elements += counted;
-    st->nnz_c = uint64_t(nnzC);
-    st->staged_slots += stage_total;
-    st->kernel_launches += ctx->launches - launches0;
-  }
+};
+
+void spgemm_impl(tsg_ctx* ctx, const tsg_csr* Ain, const tsg_csr* Bin, tsg_csr_out* C,
+                 const tsg_options& opt, tsg_run_stats* st, tsg_tiles_out* tiles) {
+  Call call(ctx, Ain, Bin, C, opt, st);
+  call.convert_operands();
+  if (call.light)
+    call.light_path();
+  else
+    call.general_path();
+  call.finish(tiles);
 }
 
 void free_out(tsg_ctx* ctx, tsg_csr_out* C) {

@@ -108,8 +108,7 @@ struct AsmChunks {
   uint32_t* seg_end = nullptr;    // [chunks]
   uint32_t* off = nullptr;        // [chunks*16] row counts, then CSR offsets
 };
-void launch_asm_chunks(uint32_t tile_rows, const uint32_t* seg_row_ptr, uint32_t* nchunks, uint32_t* chunk_base,
-                       AsmChunks& ch, cudaStream_t st);
+void launch_asm_chunks(uint32_t tile_rows, const uint32_t* seg_row_ptr, uint32_t* nchunks, cudaStream_t st);
 void launch_asm_chunk_fill(uint32_t tile_rows, const uint32_t* seg_row_ptr, const uint32_t* chunk_base,
                            AsmChunks& ch, cudaStream_t st);
 void launch_row_counts(int64_t rows, const AsmChunks& ch, uint64_t max_chunks, const Staged& sg,

@@ -282,11 +282,9 @@ __global__ void __launch_bounds__(256) assemble_kernel(int64_t rows, AsmChunks c
 
 }  // namespace
 
-void launch_asm_chunks(uint32_t tile_rows, const uint32_t* seg_row_ptr, uint32_t* nchunks, uint32_t* chunk_base,
-                       AsmChunks& ch, cudaStream_t st) {
+void launch_asm_chunks(uint32_t tile_rows, const uint32_t* seg_row_ptr, uint32_t* nchunks, cudaStream_t st) {
   if (tile_rows == 0) return;
   chunk_count_kernel<<<(tile_rows + 255) / 256, 256, 0, st>>>(tile_rows, seg_row_ptr, nchunks);
-  (void)chunk_base;  // scanned by the host between the two kernels
 }
 
 void launch_asm_chunk_fill(uint32_t tile_rows, const uint32_t* seg_row_ptr, const uint32_t* chunk_base,
