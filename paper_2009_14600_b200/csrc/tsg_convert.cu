@@ -73,6 +73,8 @@ __device__ __forceinline__ unsigned short load_half(const void* val, int64_t p,
   return h;
 }
 
+constexpr int kBitW = 64;  // count-pass bitmap words per warp (2048 tile columns)
+
 template <bool kFill, int kDtype>
 __global__ void __launch_bounds__(256) convert_kernel(CsrView in, TileMat out, int roles,
                                                      const uint32_t* __restrict__ tile_base,
@@ -84,6 +86,7 @@ __global__ void __launch_bounds__(256) convert_kernel(CsrView in, TileMat out, i
                                                      const uint8_t* __restrict__ needed) {
   // per warp: the tile staged densely (row-major) and transposed, as fp16 bits
   __shared__ __align__(16) uint16_t s_tile[8][2][256];
+  __shared__ uint32_t s_bits[kFill ? 1 : 8][kBitW];  // count pass: tile-column bitmap
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
   const uint32_t I = blockIdx.x * 8 + wib;
@@ -121,6 +124,64 @@ __global__ void __launch_bounds__(256) convert_kernel(CsrView in, TileMat out, i
       if (e) atomicOr(err_flag, e);
     }
     return;
+  }
+  if (!kFill) {
+    // Count pass over a panel whose tile columns span at most kBitW*32 tiles
+    // (banded matrices: FEM27, Poisson): no merge -- lanes take the panel's
+    // entries (contiguous in the CSR) 32 at a time, validate them
+    // (tile_format.cpp:34-51, 82-96) and mark each kept entry's tile column
+    // in a bitmap; tiles = popcount.  Wider panels take the merge below.
+    const int64_t r0 = int64_t(I) * kTile, r1 = r0 + kTile < in.rows ? r0 + kTile : in.rows;
+    const int64_t E0 = in.row_ptr[r0], E1 = in.row_ptr[r1];
+    const bool rows_ok = __all_sync(kFull, !has_row || end >= p);
+    uint32_t jlo = 0xffffffffu, jhi = 0;
+    if (has_row && end > p) {
+      jlo = uint32_t(__ldg(in.col + p)) >> 4;
+      jhi = uint32_t(__ldg(in.col + end - 1)) >> 4;
+    }
+    jlo = __reduce_min_sync(kFull, jlo);
+    jhi = __reduce_max_sync(kFull, jhi);
+    if (rows_ok && E1 >= E0 && (jlo == 0xffffffffu || jhi - jlo < uint32_t(kBitW) * 32u)) {
+      uint32_t* bm = s_bits[wib];
+      for (int i = lane; i < kBitW; i += 32) bm[i] = 0;
+      __syncwarp();
+      // lane r < 16: first entry of row r (rows past the panel: E1)
+      const int64_t rstart = lane < kTile && row < in.rows ? p : E1;
+      uint32_t nv = 0;
+      for (int64_t q0 = E0; q0 < E1; q0 += 32) {
+        const int64_t q = q0 + lane;
+        int r = 0;  // last row whose start is <= q
+#pragma unroll
+        for (int b = 8; b > 0; b >>= 1) {
+          const int64_t v = __shfl_sync(kFull, rstart, r + b);
+          if (v <= q) r += b;
+        }
+        const int64_t first = __shfl_sync(kFull, rstart, r);
+        if (q < E1) {
+          const int32_t c = __ldg(in.col + q);
+          if (c >= in.cols || c < 0 || (q > first && c <= __ldg(in.col + q - 1))) err |= kErrInvariant;
+          bool keep;
+          load_half<kDtype>(in.val, q, drop_nonfinite, err, keep);
+          const uint32_t j = (uint32_t(c) >> 4) - jlo;
+          if (keep && c >= 0 && j < uint32_t(kBitW) * 32u) {
+            atomicOr(bm + (j >> 5), 1u << (j & 31));
+            ++nv;
+          }
+        }
+      }
+      __syncwarp();
+      uint32_t nt = 0;
+      for (int i = lane; i < kBitW; i += 32) nt += __popc(bm[i]);
+      nt = __reduce_add_sync(kFull, nt);
+      nv = __reduce_add_sync(kFull, nv);
+      const unsigned e = __reduce_or_sync(kFull, err);
+      if (lane == 0) {
+        row_ntiles[I] = nt;
+        row_nvals[I] = nv;
+        if (e) atomicOr(err_flag, e);
+      }
+      return;
+    }
   }
   uint32_t ntiles = 0, nvals = 0;
   uint32_t tbase = 0;
