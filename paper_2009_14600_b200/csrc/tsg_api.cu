@@ -16,6 +16,7 @@
 // calls do not touch the driver allocator.  The host synchronises only to
 // read data-dependent sizes (tile, pair, segment, element counts).
 #include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_segmented_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 #include <cub/device/device_segmented_sort.cuh>
 #include <cub/device/device_select.cuh>
@@ -647,7 +648,12 @@ struct Call {
     const uint32_t jbits = bits_of(B.tile_cols), ibits = bits_of(TA.tile_rows);
     // the tile row rides in the key's high bits when it fits (radix sort);
     // otherwise keys are the column alone (segmented sort per tile row)
-    const bool radix = jbits + ibits <= 32;
+    // Sort choice (measured): tile rows holding thousands of pairs each
+    // (R-MAT) sort fastest per tile row over just the column bits; shorter
+    // rows (rect, AMG) as one global radix sort over (row, column) keys.
+    const bool long_rows = P >= 4096ull * TA.tile_rows;
+    const int sort_variant = tuning_variant("TSG_SORT", long_rows ? 1 : 0);
+    const bool radix = jbits + ibits <= 32 && sort_variant == 0;
     launch_enum_fill(TA, B, tA, tile_off, pairs_u, keys_u, radix ? jbits : 32, s);
     check_launch(ctx);
     launch_row_pair_off(TA, tile_off, row_pair_off, s);
@@ -666,6 +672,15 @@ struct Call {
       void* tmp = sc.alloc<char>(bytes);
       TSG_CUDA(cub::DeviceRadixSort::SortPairs(tmp, bytes, keys_u, keys, pairs_u, pairs, P, 0,
                                                int(jbits + ibits), s));
+    } else if (P > 0 && sort_variant == 1) {
+      size_t bytes = 0;
+      TSG_CUDA(cub::DeviceSegmentedRadixSort::SortPairs(nullptr, bytes, keys_u, keys, pairs_u, pairs, int(P),
+                                                        int(TA.tile_rows), row_pair_off, row_pair_off + 1, 0,
+                                                        int(jbits), s));
+      void* tmp = sc.alloc<char>(bytes);
+      TSG_CUDA(cub::DeviceSegmentedRadixSort::SortPairs(tmp, bytes, keys_u, keys, pairs_u, pairs, int(P),
+                                                        int(TA.tile_rows), row_pair_off, row_pair_off + 1, 0,
+                                                        int(jbits), s));
     } else if (P > 0) {
       size_t bytes = 0;
       TSG_CUDA(cub::DeviceSegmentedSort::StableSortPairs(nullptr, bytes, keys_u, keys, pairs_u, pairs, int(P),
