@@ -239,6 +239,7 @@ const uint32_t* convert(tsg_ctx* ctx, Scratch& sc, const CsrView& in, TileMat& T
   for (int role = 0; role < 2; ++role) {
     if (!(roles & (1 << role))) continue;
     T.meta[role] = sc.alloc<uint2>(cap);
+    T.rec[role] = sc.alloc<uint4>(cap);
     T.chunk[role] = sc.alloc<uint4>(cap + 1);
     TSG_CUDA(cudaMemsetAsync(T.chunk[role], 0, sizeof(uint4), ctx->stream));  // zero chunk 0
   }

@@ -16,6 +16,8 @@
 //   trow  u32[T]            tile row of each tile (the general path's sort key)
 //   meta  uint2[T]  (per operand role)  {lane mask, first chunk}
 //   chunk uint4[]   (per operand role)  16-byte lane chunks, chunk 0 = zeros
+//   rec   uint4[T]  (per operand role)  {lane mask, first chunk, occupancy, tile col}
+//                   -- meta and tco in one 16-byte record for random gathers
 //
 // Lane-dense operand chunks (our layout, not the reference's ascending-bit
 // order): mma.m16n8k16 lane L holds 8 fp16 slots of a 16x16 operand in four
@@ -52,6 +54,7 @@ struct TileMat {
   uint32_t* etile = nullptr;
   const int64_t* csr_rp = nullptr;
   uint2* meta[2] = {nullptr, nullptr};
+  uint4* rec[2] = {nullptr, nullptr};  // {lane mask, first chunk, occupancy, tile column}: one gather per tile
   uint4* chunk[2] = {nullptr, nullptr};
 };
 

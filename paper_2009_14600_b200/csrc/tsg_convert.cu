@@ -260,7 +260,10 @@ __global__ void __launch_bounds__(256) convert_kernel(CsrView in, TileMat out, i
           out.chunk[role][cbase[role] + __popc(lm & lanemask_lt())] =
               role == kRoleA ? make_uint4(reg[0], reg[1], reg[2], reg[3])
                              : make_uint4(reg[0], reg[2], reg[1], reg[3]);
-        if (lane == 0) out.meta[role][t] = make_uint2(lm, cbase[role]);
+        if (lane == 0) {
+          out.meta[role][t] = make_uint2(lm, cbase[role]);
+          if (out.rec[role]) out.rec[role][t] = make_uint4(lm, cbase[role], colocc | ((any & 0xffffu) << 16), J);
+        }
         cbase[role] += __popc(lm);
       }
       __syncwarp();

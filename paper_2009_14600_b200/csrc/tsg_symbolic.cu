@@ -191,10 +191,9 @@ __global__ void pair_meta_kernel(TileMat A, TileMat B, const uint64_t* __restric
   }
   const uint64_t pr = pairs[i];
   const uint32_t a = uint32_t(pr), b = uint32_t(pr >> 32);
-  const uint2 am = __ldg(A.meta[kRoleA] + a);
-  const uint2 bm = __ldg(B.meta[kRoleB] + b);
-  const uint32_t oa = __ldg(&A.tco[a].y), ob = __ldg(&B.tco[b].y);
-  tl.pmeta[i] = make_uint4(am.x, am.y, bm.x, bm.y);
+  const uint4 ra = __ldg(A.rec[kRoleA] + a), rb = __ldg(B.rec[kRoleB] + b);  // one sector each
+  const uint32_t oa = ra.z, ob = rb.z;
+  tl.pmeta[i] = make_uint4(ra.x, ra.y, rb.x, rb.y);
   tl.pocc[i] = make_uint2(oa, ob);  // so the thin kernel reads each pair coalesced
   pair_bound[i] = __popc(oa >> 16) * __popc(ob & 0xffffu);
 }
