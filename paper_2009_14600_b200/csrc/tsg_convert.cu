@@ -73,7 +73,7 @@ __device__ __forceinline__ unsigned short load_half(const void* val, int64_t p,
   return h;
 }
 
-constexpr int kBitW = 64;  // count-pass bitmap words per warp (2048 tile columns)
+constexpr int kBitW = 256;  // count-pass bitmap words per warp (8192 tile columns)
 
 template <bool kFill, int kDtype>
 __global__ void __launch_bounds__(256) convert_kernel(CsrView in, TileMat out, int roles,
