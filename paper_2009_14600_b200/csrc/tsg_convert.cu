@@ -191,8 +191,11 @@ __global__ void __launch_bounds__(256) convert_kernel(CsrView in, TileMat out, i
     // chunk capacity of a tile row = its kept nnz (every present lane holds >= 1)
     cbase[0] = cbase[1] = 1u + val_base[I];
   }
+  // column of the lane's next entry, loaded one entry ahead so the row walk
+  // below is not a chain of dependent global loads
+  int32_t c_cur = p < end ? __ldg(in.col + p) : 0;
   while (true) {
-    const uint32_t my_tc = (p < end) ? uint32_t(__ldg(in.col + p)) >> 4 : 0xffffffffu;
+    const uint32_t my_tc = (p < end) ? uint32_t(c_cur) >> 4 : 0xffffffffu;
     const uint32_t J = __reduce_min_sync(kFull, my_tc);
     if (J == 0xffffffffu) break;
     if (kFill) {
@@ -203,8 +206,9 @@ __global__ void __launch_bounds__(256) convert_kernel(CsrView in, TileMat out, i
     uint32_t rm = 0;
     bool first = true;  // first kept entry of this tile in this row
     while (p < end) {
-      const int32_t c = __ldg(in.col + p);
+      const int32_t c = c_cur;
       if ((uint32_t(c) >> 4) != J) break;
+      const int32_t c_next = p + 1 < end ? __ldg(in.col + p + 1) : 0;
       if (!kFill) {
         if (c <= prev_col || c >= in.cols || c < 0) err |= kErrInvariant;
         prev_col = c;
@@ -223,6 +227,7 @@ __global__ void __launch_bounds__(256) convert_kernel(CsrView in, TileMat out, i
         first &= !keep;
       }
       ++p;
+      c_cur = c_next;
     }
     // Termination holds for any input: the lane holding the minimum tile
     // column always consumes at least one entry.  Invalid input only sets
