@@ -368,6 +368,15 @@ struct Call {
   unsigned long long* counted_d = nullptr;
   int64_t* rowcnt = nullptr;  // realised entries per CSR row
 
+  // chained products: A given as tiles by the previous stage (pre_a), and/or
+  // this stage's result emitted as the next stage's A tiles (emit_out); the
+  // emitted arrays outlive this call and are listed in `keep`
+  const TileMat* pre_a = nullptr;
+  uint64_t pre_a_tiles = 0;
+  TileMat* emit_out = nullptr;
+  uint64_t emit_tiles = 0;
+  std::vector<void*>* keep = nullptr;
+
   Call(tsg_ctx* c, const tsg_csr* a, const tsg_csr* b, tsg_csr_out* out, const tsg_options& o,
        tsg_run_stats* stats)
       : ctx(c), Ain(a), Bin(b), C(out), opt(o), st(stats), timing(o.phase_timing != 0), s(c->stream),
@@ -375,7 +384,7 @@ struct Call {
 
   // ---- (1) validation, staging of host inputs, CSR -> 16x16 tiles ----------------
   void convert_operands() {
-    check_csr(Ain, "A");
+    if (!pre_a) check_csr(Ain, "A");
     check_csr(Bin, "B");
     if (!C) throw Fail{TSG_ERR_OTHER, "C is NULL"};
     if (Ain->cols != Bin->rows)
@@ -386,12 +395,18 @@ struct Call {
     dscal = sc.alloc<unsigned>(2);
     TSG_CUDA(cudaMemsetAsync(dscal, 0, 2 * sizeof(unsigned), s));
     err_flag = dscal;
-    same = Ain == Bin || (Ain->row_ptr == Bin->row_ptr && Ain->col == Bin->col && Ain->val == Bin->val &&
-                          Ain->rows == Bin->rows && Ain->cols == Bin->cols && Ain->mem == Bin->mem &&
-                          Ain->dtype == Bin->dtype && Ain->nnz == Bin->nnz);
-    dA = stage(ctx, sc, Ain, st);
+    same = !pre_a && (Ain == Bin || (Ain->row_ptr == Bin->row_ptr && Ain->col == Bin->col &&
+                                     Ain->val == Bin->val && Ain->rows == Bin->rows && Ain->cols == Bin->cols &&
+                                     Ain->mem == Bin->mem && Ain->dtype == Bin->dtype && Ain->nnz == Bin->nnz));
+    const uint32_t* ntA_d;
+    if (pre_a) {  // the previous stage's emitted tiles
+      TA = *pre_a;
+      ntA_d = TA.trp + TA.tile_rows;
+    } else {
+      dA = stage(ctx, sc, Ain, st);
+      ntA_d = convert(ctx, sc, dA, TA, same ? 3 : 1, err_flag, opt.drop_nonfinite);
+    }
     dB = same ? dA : stage(ctx, sc, Bin, st);
-    const uint32_t* ntA_d = convert(ctx, sc, dA, TA, same ? 3 : 1, err_flag, opt.drop_nonfinite);
     const uint32_t* ntB_d = ntA_d;
     if (!same) {
       // only the B tile rows A's tiles refer to are tiled (a row panel of A --
@@ -511,6 +526,11 @@ struct Call {
       readback_many(ctx, src, v);
       take_totals(v);
     };
+    if (emit_out) {
+      read_totals();
+      light_emit(row_ns);
+      return;
+    }
     // Device output with a staging arena already in place: launch the panel
     // pass without reading the staging total back first; the kernel checks it
     // against the arena on the device and the totals are read with nnz(C)
@@ -553,6 +573,69 @@ struct Call {
     launch_panel_copy(rows, row_stage, d_rp, stage, d_col, d_val, err_flag, 0, TA.tile_rows, s);
     check_launch(ctx);
     if (timing) TSG_CUDA(cudaEventRecord(ctx->kev[3], s));
+    record(ctx, timing, 6);
+  }
+
+  // Chained product, light rows: the result goes to the next stage as A tiles
+  // (panel pass in emit mode, then compaction into a dense CSR-of-tiles).
+  void light_emit(const uint32_t* row_ns) {
+    auto kept = [&](auto* p) {
+      keep->push_back(p);
+      return p;
+    };
+    record(ctx, timing, 2);
+    record(ctx, timing, 3);
+    record(ctx, timing, 4);
+    TileEmit em;
+    auto* tile_base = sc.alloc<uint32_t>(nr);
+    exclusive_sum(ctx, sc, row_ns, tile_base, nr);
+    em.tile_base = tile_base;
+    em.tco = sc.alloc<uint2>(S);
+    em.rm2 = sc.alloc<uint32_t>(S * 8);
+    em.trow = sc.alloc<uint32_t>(S);
+    em.meta = sc.alloc<uint2>(S);
+    em.rec = sc.alloc<uint4>(S);
+    em.chunk = kept(sc.alloc<uint4>(32 * S + 1, true));
+    TSG_CUDA(cudaMemsetAsync(em.chunk, 0, sizeof(uint4), s));
+    em.rtiles = sc.alloc<uint32_t>(nr);
+    TSG_CUDA(cudaMemsetAsync(em.rtiles + nr - 1, 0, sizeof(uint32_t), s));
+    em.err_flag = err_flag;
+    if (timing) TSG_CUDA(cudaEventRecord(ctx->kev[0], s));
+    launch_panel_numeric(TA, *TB, rows, nullptr, 0, nullptr, nullptr, counted_d, opt.mode, 0, TA.tile_rows, s, &em);
+    check_launch(ctx);
+    if (timing) TSG_CUDA(cudaEventRecord(ctx->kev[1], s));
+    record(ctx, timing, 5);
+    TileMat& T = *emit_out;
+    T = TileMat{};
+    T.rows = rows;
+    T.cols = TB->cols;
+    T.tile_rows = TA.tile_rows;
+    T.tile_cols = uint32_t((T.cols + 15) / 16);
+    T.trp = kept(sc.alloc<uint32_t>(nr, true));
+    exclusive_sum(ctx, sc, em.rtiles, T.trp, nr);
+    {
+      const unsigned long long* src[1] = {counted_d};
+      unsigned long long v[1];
+      uint32_t* tiles_h = reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(ctx->pinned) + 48);
+      TSG_CUDA(cudaMemcpyAsync(tiles_h, T.trp + nr - 1, 4, cudaMemcpyDeviceToHost, s));
+      readback_many(ctx, src, v);
+      counted = v[0];
+      emit_tiles = *tiles_h;
+    }
+    const uint64_t nt = std::max<uint64_t>(emit_tiles, 1);
+    T.cap = emit_tiles;
+    T.tco = kept(sc.alloc<uint2>(nt, true));
+    T.rm2 = kept(sc.alloc<uint32_t>(nt * 8, true));
+    T.trow = kept(sc.alloc<uint32_t>(nt, true));
+    T.meta[kRoleA] = kept(sc.alloc<uint2>(nt, true));
+    T.rec[kRoleA] = kept(sc.alloc<uint4>(nt, true));
+    T.chunk[kRoleA] = em.chunk;
+    if (timing) TSG_CUDA(cudaEventRecord(ctx->kev[2], s));
+    launch_emit_compact(TA.tile_rows, em, T.trp, T, s);
+    check_launch(ctx);
+    if (timing) TSG_CUDA(cudaEventRecord(ctx->kev[3], s));
+    nnzC = 0;
+    stage_total = 0;  // no staging: the tiles are written in place
     record(ctx, timing, 6);
   }
 
@@ -776,10 +859,10 @@ struct Call {
     // non-finite accumulators are flagged by the CSR pass (read at the final sync)
     unsigned* flags_host = reinterpret_cast<unsigned*>(reinterpret_cast<char*>(ctx->pinned) + 56);
     TSG_CUDA(cudaMemcpyAsync(flags_host, err_flag, 4, cudaMemcpyDeviceToHost, s));
-    C->rows = Ain->rows;
+    C->rows = rows;
     C->cols = Bin->cols;
     C->nnz = nnzC;
-    if (owner->host && !host_done) {
+    if (owner->host && !host_done && !emit_out) {
       owner->p[0] = pinned_alloc(ctx, (rows + 1) * sizeof(int64_t), &owner->sz[0]);
       owner->p[1] = pinned_alloc(ctx, nnzC * sizeof(int32_t), &owner->sz[1]);
       owner->p[2] = pinned_alloc(ctx, nnzC * sizeof(float), &owner->sz[2]);
@@ -829,6 +912,7 @@ struct Call {
         st->total += tot * 1e-3;
       }
     }
+    if (emit_out && !light) throw Fail{TSG_ERR_OTHER, "internal: tile emission needs the light-row path"};
     if (st) {
       st->tiles_a += tA;
       st->tiles_b += tB;
@@ -852,6 +936,28 @@ void spgemm_impl(tsg_ctx* ctx, const tsg_csr* Ain, const tsg_csr* Bin, tsg_csr_o
   else
     call.general_path();
   call.finish(tiles);
+}
+
+// One stage of a chain (tsg_spgemm_chain).  `pre_a`: A as the previous
+// stage's tiles (else Ain as CSR).  `emit`: when this stage takes the
+// light-row path, its result becomes the next stage's A tiles (returns
+// true); otherwise C receives CSR as usual (returns false).
+bool chain_stage(tsg_ctx* ctx, const tsg_csr* Ain, const TileMat* pre_a, uint64_t pre_a_tiles,
+                 const tsg_csr* Bin, tsg_csr_out* C, TileMat* emit, std::vector<void*>* keep,
+                 const tsg_options& opt, tsg_run_stats* st) {
+  Call call(ctx, Ain, Bin, C, opt, st);
+  call.pre_a = pre_a;
+  call.pre_a_tiles = pre_a_tiles;
+  call.keep = keep;
+  call.convert_operands();
+  if (call.light) {
+    call.emit_out = emit;
+    call.light_path();
+  } else {
+    call.general_path();
+  }
+  call.finish(nullptr);
+  return emit && call.light;
 }
 
 void free_out(tsg_ctx* ctx, tsg_csr_out* C) {
@@ -980,33 +1086,86 @@ int tsg_spgemm_chain(tsg_ctx* ctx, int n, const tsg_csr* const* X, tsg_csr_out* 
   tsg_default_options(&o);
   if (opt) o = *opt;
   o.want_tiles = 0;
+  ctx->err.clear();
+  // Left to right.  Between stages the intermediate is rounded to binary16
+  // (kernels.cpp:239-258).  When a stage takes the light-row path its result
+  // goes to the next stage directly as A tiles (the downcast fused into the
+  // emission); otherwise as a device fp32 CSR rounded by the next conversion.
+  std::vector<void*> keep[2];  // emitted tile arrays of the previous / current stage
+  TileMat tiles[2];
+  const TileMat* pre = nullptr;
   tsg_csr_out cur{};
   bool have_cur = false;
-  for (int i = 1; i < n; ++i) {
-    tsg_csr left;
-    if (!have_cur) {
-      left = *X[0];
-    } else {
-      // intermediate: device fp32 CSR, rounded to binary16 by the next
-      // conversion (kernels.cpp:239-258 semantics)
-      left.rows = cur.rows;
-      left.cols = cur.cols;
-      left.nnz = cur.nnz;
-      left.row_ptr = cur.row_ptr;
-      left.col = cur.col;
-      left.val = cur.val;
-      left.dtype = TSG_F32;
-      left.mem = TSG_MEM_DEVICE;
+  int rc = TSG_OK;
+  try {
+    TSG_CUDA(cudaSetDevice(ctx->device));
+    for (int i = 1; i < n && rc == TSG_OK; ++i) {
+      const bool last = i == n - 1;
+      tsg_csr left{};
+      if (!pre) {
+        if (!have_cur) {
+          left = *X[0];
+        } else {
+          left.rows = cur.rows;
+          left.cols = cur.cols;
+          left.nnz = cur.nnz;
+          left.row_ptr = cur.row_ptr;
+          left.col = cur.col;
+          left.val = cur.val;
+          left.dtype = TSG_F32;
+          left.mem = TSG_MEM_DEVICE;
+        }
+      } else {
+        left.rows = pre->rows;
+        left.cols = pre->cols;
+      }
+      tsg_csr_out next{};
+      next.mem = last ? C->mem : TSG_MEM_DEVICE;
+      const int w = i & 1;
+      for (void* p : keep[w]) cudaFreeAsync(p, ctx->stream);
+      keep[w].clear();
+      bool emitted = false;
+      try {
+        emitted = chain_stage(ctx, &left, pre, pre ? pre->cap : 0, X[i], &next, last ? nullptr : &tiles[w],
+                              &keep[w], o, stats);
+      } catch (const Fail& f) {
+        ctx->err = f.msg;
+        cudaStreamSynchronize(ctx->stream);
+        if (next._owner) free_out(ctx, &next);
+        rc = f.code;
+      } catch (const std::exception& e) {
+        ctx->err = e.what();
+        cudaStreamSynchronize(ctx->stream);
+        if (next._owner) free_out(ctx, &next);
+        rc = TSG_ERR_OTHER;
+      }
+      if (have_cur) free_out(ctx, &cur);
+      have_cur = false;
+      for (void* p : keep[w ^ 1]) cudaFreeAsync(p, ctx->stream);  // the previous stage's tiles are consumed
+      keep[w ^ 1].clear();
+      if (rc != TSG_OK) break;
+      if (emitted) {
+        free_out(ctx, &next);  // no CSR for an emitting stage
+        pre = &tiles[w];
+      } else {
+        pre = nullptr;
+        cur = next;
+        have_cur = true;
+      }
     }
-    tsg_csr_out next{};
-    next.mem = (i == n - 1) ? C->mem : TSG_MEM_DEVICE;
-    const int rc = tsg_spgemm(ctx, &left, X[i], &next, &o, stats, nullptr);
+  } catch (const Fail& f) {
+    ctx->err = f.msg;
+    rc = f.code;
+  }
+  for (auto& k : keep)
+    for (void* p : k) cudaFreeAsync(p, ctx->stream);
+  if (rc != TSG_OK) {
     if (have_cur) free_out(ctx, &cur);
-    if (rc != TSG_OK) return rc;
-    cur = next;
-    have_cur = true;
+    cudaStreamSynchronize(ctx->stream);
+    return rc;
   }
   *C = cur;
+  cudaStreamSynchronize(ctx->stream);
   return TSG_OK;
 }
 

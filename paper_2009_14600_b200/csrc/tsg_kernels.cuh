@@ -62,11 +62,26 @@ void launch_panel_count(const TileMat& A, const TileMat& B, int64_t rows, uint32
                         uint32_t* row_ns, uint32_t* row_raw, uint32_t* row_bound, cudaStream_t st);
 // staging slot = {value bits, column}, row r's region at row_stage[r]; both
 // passes work on the tile rows [I0, I1)
+// Emit mode (chained products): output tiles become A-operand tiles of the
+// next stage instead of CSR (tsg_panel.cu emit_tile); slots per tile row
+// from tile_base, realised tiles per tile row in rtiles.
+struct TileEmit {
+  uint2* tco = nullptr;
+  uint32_t* rm2 = nullptr;
+  uint32_t* trow = nullptr;
+  uint2* meta = nullptr;
+  uint4* rec = nullptr;
+  uint4* chunk = nullptr;  // chunk 0 = zeros; tile row I's chunks from 1 + 32 * tile_base[I]
+  const uint32_t* tile_base = nullptr;
+  uint32_t* rtiles = nullptr;
+  unsigned* err_flag = nullptr;
+};
 // The pass does nothing when the staging total row_stage[rows] exceeds
 // stage_cap slots (the host checks and reruns with a bigger arena).
 void launch_panel_numeric(const TileMat& A, const TileMat& B, int64_t rows, const uint32_t* row_stage,
                           uint64_t stage_cap, uint2* stage, int64_t* rowcnt, unsigned long long* counted, int mode,
-                          uint32_t I0, uint32_t I1, cudaStream_t st);
+                          uint32_t I0, uint32_t I1, cudaStream_t st, const TileEmit* emit = nullptr);
+void launch_emit_compact(uint32_t tile_rows, const TileEmit& em, const uint32_t* trp, TileMat& T, cudaStream_t st);
 void launch_panel_copy(int64_t rows, const uint32_t* row_stage, const int64_t* row_ptr, const uint2* stage,
                        int32_t* col, float* val, unsigned* err_flag, uint32_t I0, uint32_t I1,
                        cudaStream_t st);

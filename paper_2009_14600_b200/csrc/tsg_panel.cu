@@ -107,13 +107,75 @@ __global__ void __launch_bounds__(256) panel_count_kernel(TileMat A, TileMat B, 
 constexpr int kSA = 17;    // padded row stride of the ordered A scratch tile
 constexpr int kSRow = 24;  // row stride of the ordered B scratch tile
 
-template <bool kOrdered, int kMinBlocks>
+// Chained products (R.A.P): instead of CSR, the run's output tile is
+// emitted as an A-operand tile of the next stage.  The accumulator fragment
+// of mma.m16n8k16 (two n8 halves) has exactly the A-operand register layout
+// (reg0 = row g cols 2t..2t+1, reg1 = row g+8, reg2/3 = cols +8), so the tile
+// is four cvt.rn.f16x2 per lane -- the binary16 downcast between stages
+// (kernels.cpp:239-258: RNE, |x| > 65504 overflows, values rounding to zero
+// drop) -- and the lane-dense chunk write.  Tiles of a tile row go to slots
+// from em.tile_base[I] in column order; the host compacts them afterwards.
+__device__ __forceinline__ void emit_tile(const float (&acc)[2][4], uint32_t J, uint32_t I, int lane,
+                                          const LaneLayout& L, unsigned lt, const TileEmit& em,
+                                          uint32_t& e_tiles, uint32_t& e_chunks) {
+  uint32_t hv[4];
+  bool over = false, bad = false;
+#pragma unroll
+  for (int h = 0; h < 2; ++h)
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const float v0 = acc[h][2 * q], v1 = acc[h][2 * q + 1];
+      bad |= !isfinite(v0) || !isfinite(v1);
+      over |= fabsf(v0) > 65504.0f || fabsf(v1) > 65504.0f;
+      const __half2 hh = __floats2half2_rn(v0, v1);
+      hv[q + 2 * h] = *reinterpret_cast<const uint32_t*>(&hh);
+    }
+  // a non-finite accumulator is the multiplication pass's error (raised
+  // before the next stage's conversion would see the overflow)
+  const bool any_bad = __any_sync(kFull, bad), any_over = __any_sync(kFull, over);
+  if ((any_bad || any_over) && lane == 0)
+    atomicOr(em.err_flag, any_bad ? unsigned(kErrPrecision) : unsigned(kErrOverflow));
+  // nonzero binary16 slots -> per-lane bits, then the group's two row masks
+  uint32_t x = 0;
+#pragma unroll
+  for (int h = 0; h < 2; ++h)
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const uint32_t w = hv[q + 2 * h];
+      if (w & 0x7fffu) x |= 1u << (8 * h + 16 * q);
+      if (w & 0x7fff0000u) x |= 1u << (8 * h + 16 * q + 1);
+    }
+  const bool present = x != 0u;
+  x <<= 2 * L.t;
+  x |= __shfl_xor_sync(kFull, x, 1);
+  x |= __shfl_xor_sync(kFull, x, 2);  // rows g | g+8 << 16
+  const unsigned lm = __ballot_sync(kFull, present);
+  if (lm == 0u) return;  // every slot cancelled or underflowed: no tile
+  const uint32_t t = em.tile_base[I] + e_tiles;
+  const uint32_t cb = 1u + 32u * em.tile_base[I] + e_chunks;
+  if (present) em.chunk[cb + __popc(lm & lt)] = make_uint4(hv[0], hv[1], hv[2], hv[3]);
+  if (L.t == 0) em.rm2[size_t(t) * 8 + L.g] = x;
+  const uint32_t colocc = __reduce_or_sync(kFull, (x | (x >> 16)) & 0xffffu);
+  const uint32_t rowocc =
+      __reduce_or_sync(kFull, (((x & 0xffffu) != 0u) << L.g) | (((x >> 16) != 0u) << (L.g + 8)));
+  if (lane == 0) {
+    const uint32_t occ = colocc | (rowocc << 16);
+    em.tco[t] = make_uint2(J, occ);
+    em.trow[t] = I;
+    em.meta[t] = make_uint2(lm, cb);
+    em.rec[t] = make_uint4(lm, cb, occ, J);
+  }
+  ++e_tiles;
+  e_chunks += __popc(lm);
+}
+
+template <bool kOrdered, int kMinBlocks, bool kEmit>
 __global__ void __launch_bounds__(256, kMinBlocks) panel_numeric_kernel(TileMat A, TileMat B, int64_t rows,
                                                               const uint32_t* __restrict__ row_stage,
                                                               uint64_t stage_cap, uint2* __restrict__ stage,
                                                               int64_t* __restrict__ rowcnt,
                                                               unsigned long long* __restrict__ counted,
-                                                              uint32_t I0, uint32_t I1) {
+                                                              uint32_t I0, uint32_t I1, TileEmit em) {
   __shared__ __align__(16) uint4 s_meta[8][32];
   // TENSOR: [A tile of the row][lane] -> chunk index (ORDERED keeps the metas)
   __shared__ uint32_t s_aidx[kOrdered ? 1 : 8][32][32];
@@ -123,7 +185,7 @@ __global__ void __launch_bounds__(256, kMinBlocks) panel_numeric_kernel(TileMat 
   const int w = threadIdx.x >> 5;
   const uint32_t I = I0 + blockIdx.x * 8 + w;
   if (I >= I1) return;
-  if (__ldg(row_stage + rows) > stage_cap) return;  // arena too small: the host reruns the pass
+  if (!kEmit && __ldg(row_stage + rows) > stage_cap) return;  // arena too small: the host reruns the pass
   const uint4* cA = A.chunk[kRoleA];
   const uint4* cB = B.chunk[kRoleB];
   const unsigned lt = lanemask_lt(), bit = 1u << lane;
@@ -143,9 +205,11 @@ __global__ void __launch_bounds__(256, kMinBlocks) panel_numeric_kernel(TileMat 
   }
   // lanes of group g track the staging cursors of rows g and g+8
   const int64_t rg = int64_t(I) * 16 + L.g, rg8 = rg + 8;
-  uint32_t wg = rg < rows ? __ldg(row_stage + rg) : 0u, wg8 = rg8 < rows ? __ldg(row_stage + rg8) : 0u;
+  uint32_t wg = !kEmit && rg < rows ? __ldg(row_stage + rg) : 0u;
+  uint32_t wg8 = !kEmit && rg8 < rows ? __ldg(row_stage + rg8) : 0u;
   const uint32_t wg0 = wg, wg80 = wg8;
   uint32_t nstruct = 0;
+  uint32_t e_tiles = 0, e_chunks = 0;  // emit mode: tiles / chunks written for this tile row
   while (true) {
     const uint32_t J = __reduce_min_sync(kFull, m.bt.x);
     if (J == kInf) break;
@@ -231,6 +295,12 @@ __global__ void __launch_bounds__(256, kMinBlocks) panel_numeric_kernel(TileMat 
 #pragma unroll
           for (int i = 0; i < 4; ++i) nstruct += snz[h][i];
       }
+      if (kEmit) {
+        emit_tile(acc, J, I, lane, L, lt, em, e_tiles, e_chunks);
+        __syncwarp();
+        if (take) m.advance(B);
+        continue;
+      }
       // finalize_segment: bitmap = accumulators != 0 (cancelled slots and -0
       // drop: compact()); row r's entries append to row r's staging region
       const uint32_t rmg = group_row_masks(acc, L.t);  // rows g | g+8 << 16
@@ -252,7 +322,9 @@ __global__ void __launch_bounds__(256, kMinBlocks) panel_numeric_kernel(TileMat 
     }
     if (take) m.advance(B);
   }
-  if (L.t == 0) {
+  if (kEmit) {
+    if (lane == 0) em.rtiles[I] = e_tiles;
+  } else if (L.t == 0) {
     if (rg < rows) rowcnt[rg] = int64_t(wg - wg0);
     if (rg8 < rows) rowcnt[rg8] = int64_t(wg8 - wg80);
   }
@@ -314,16 +386,42 @@ void launch_panel_count(const TileMat& A, const TileMat& B, int64_t rows, uint32
 
 void launch_panel_numeric(const TileMat& A, const TileMat& B, int64_t rows, const uint32_t* row_stage,
                           uint64_t stage_cap, uint2* stage, int64_t* rowcnt, unsigned long long* counted, int mode,
-                          uint32_t I0, uint32_t I1, cudaStream_t st) {
+                          uint32_t I0, uint32_t I1, cudaStream_t st, const TileEmit* emit) {
   const unsigned blocks = (I1 - I0 + 7) / 8;
   if (I1 <= I0) return;
-  if (mode == 1) {
-    panel_numeric_kernel<true, 4><<<blocks, 256, 0, st>>>(A, B, rows, row_stage, stage_cap, stage, rowcnt, counted,
-                                                           I0, I1);
-  } else {
-    auto k = tuning_variant("TSG_PANEL_MINB", 4) == 5 ? panel_numeric_kernel<false, 5> : panel_numeric_kernel<false, 4>;
-    k<<<blocks, 256, 0, st>>>(A, B, rows, row_stage, stage_cap, stage, rowcnt, counted, I0, I1);
+  const TileEmit em = emit ? *emit : TileEmit{};
+  using K = void (*)(TileMat, TileMat, int64_t, const uint32_t*, uint64_t, uint2*, int64_t*, unsigned long long*,
+                     uint32_t, uint32_t, TileEmit);
+  K k;
+  if (mode == 1)
+    k = emit ? panel_numeric_kernel<true, 4, true> : panel_numeric_kernel<true, 4, false>;
+  else if (emit)
+    k = panel_numeric_kernel<false, 4, true>;
+  else
+    k = tuning_variant("TSG_PANEL_MINB", 4) == 5 ? panel_numeric_kernel<false, 5, false>
+                                                  : panel_numeric_kernel<false, 4, false>;
+  k<<<blocks, 256, 0, st>>>(A, B, rows, row_stage, stage_cap, stage, rowcnt, counted, I0, I1, em);
+}
+
+// Emitted tiles (gapped per tile row) -> dense CSR-of-tiles: warp per tile row.
+__global__ void emit_compact_kernel(uint32_t tile_rows, TileEmit em, const uint32_t* __restrict__ trp, TileMat T) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t I = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (I >= tile_rows) return;
+  const uint32_t src = em.tile_base[I], dst = trp[I], n = em.rtiles[I];
+  for (uint32_t i = lane; i < n; i += 32) {
+    T.tco[dst + i] = em.tco[src + i];
+    T.trow[dst + i] = em.trow[src + i];
+    T.meta[kRoleA][dst + i] = em.meta[src + i];
+    T.rec[kRoleA][dst + i] = em.rec[src + i];
   }
+  for (uint32_t i = lane; i < 8 * n; i += 32) T.rm2[size_t(dst) * 8 + i] = em.rm2[size_t(src) * 8 + i];
+}
+
+void launch_emit_compact(uint32_t tile_rows, const TileEmit& em, const uint32_t* trp, TileMat& T, cudaStream_t st) {
+  const unsigned blocks = (tile_rows + 7) / 8;
+  if (blocks == 0) return;
+  emit_compact_kernel<<<blocks, 256, 0, st>>>(tile_rows, em, trp, T);
 }
 
 void launch_panel_copy(int64_t rows, const uint32_t* row_stage, const int64_t* row_ptr, const uint2* stage,
