@@ -210,3 +210,61 @@ def test_unreferenced_b_rows_are_still_validated(ctx):
     val2 = np.insert(np.ones(64, np.float32), 41, 1.0)
     with pytest.raises(T.InvariantError):
         ctx.spgemm(A, T.Csr(64, 64, rp2, col2, val2))
+
+
+def _dyadic(M, seed, exps):
+    """Values +-2^e, e drawn from `exps`: exact products and short sums, so
+    the TENSOR path is bit-exact too; tiny exponents underflow binary16."""
+    rng = np.random.default_rng(seed)
+    e = rng.choice(np.asarray(exps, np.float64), M.nnz)
+    s = np.where(rng.random(M.nnz) < 0.5, -1.0, 1.0)
+    M.val = (s * np.exp2(e)).astype(np.float32)
+    return M
+
+
+@pytest.mark.parametrize("kind", ["signed", "unit", "tiny"])
+def test_chain_fused_stages(ctx, kind):
+    """tsg_spgemm_chain hands a light-row stage's result to the next stage as
+    binary16 A tiles without a CSR round trip; the rounding, overflow check,
+    underflow drop and cancellation must equal the reference's CSR ->
+    binary16 conversion between stages (kernels.cpp:239-258).  Chain 1:
+    light (emits) -> light on emitted tiles (emits) -> general on emitted
+    tiles.  Chain 2: light (emits) -> general on emitted tiles (CSR) ->
+    general on the converted CSR."""
+    n = 700
+    S0, S1 = W.random_uniform(n, n, 1050, 31), W.random_uniform(n, n, 1050, 33)
+    wide = _signed_wide(n, n, 60 * n, 32, "unit")
+    last = W.random_uniform(n, 500, 4 * n, 34)
+    for i, M in enumerate((S0, S1, wide, last)):
+        if kind == "signed":
+            M.val = W._round_half(-4.0 + 8.0 * W.uniform(40 + i, M.nnz))
+        elif kind == "unit":
+            M.val = np.where(W.uniform(40 + i, M.nnz) < 0.5, -1.0, 1.0).astype(np.float32)
+        else:
+            _dyadic(M, 40 + i, [-9, -8, -7, -4, 0])
+    for mats in ([S0, S1, wide, last], [S0, wide, S1, last]):
+        want = ref.chain(mats)
+        for mode in ("ordered", "tensor"):
+            got = ctx.spgemm_chain(mats, mode=mode).C
+            if mode == "ordered" or kind == "unit":  # +-1: every sum exact on the MMA too
+                assert csr_bits_equal(got, want), (mode, first_diff(got, want))
+            else:  # MMA rounding may move an intermediate across a binary16 boundary
+                assert got.rows == want.rows and got.cols == want.cols and got.nnz > 0
+
+
+def test_chain_intermediate_overflow(ctx):
+    """An intermediate beyond binary16 range raises like the reference's
+    conversion of it (tile_format.cpp from_element_coo)."""
+    n = 32
+    rp = np.arange(n + 1, dtype=np.int64)
+    X = T.Csr(n, n, rp, np.arange(n, dtype=np.int32), np.full(n, 300.0, np.float32))
+    I = T.Csr(n, n, rp, np.arange(n, dtype=np.int32), np.ones(n, np.float32))
+    with pytest.raises(T.OverflowError):
+        ctx.spgemm_chain([X, X, I])
+    with pytest.raises(Exception):
+        ref.chain([X, X, I])
+    # just inside the range: 255^2 = 65025 rounds to binary16 65024
+    X.val[:] = 255.0
+    got = ctx.spgemm_chain([X, X, I]).C
+    assert csr_bits_equal(got, ref.chain([X, X, I]))
+    assert np.all(np.asarray(got.val) == 65024.0)
