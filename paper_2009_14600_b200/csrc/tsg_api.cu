@@ -207,7 +207,8 @@ void readback_many(tsg_ctx* ctx, const T* const (&src)[N], T (&dst)[N]) {
   std::memcpy(dst, ctx->pinned, N * sizeof(T));
 }
 
-// CSR -> 16x16 tiles (count, scan, fill).  No host synchronisation: every
+// CSR -> 16x16 tiles (one conversion pass at gapped slots, scan of the tile
+// counts, compaction of the tile metadata).  No host synchronisation: every
 // array is sized by the input nnz (an upper bound on tiles and chunks).
 // Returns the device address of the tile count (trp[tile_rows]).
 const uint32_t* convert(tsg_ctx* ctx, Scratch& sc, const CsrView& in, TileMat& T, int roles,
@@ -217,33 +218,38 @@ const uint32_t* convert(tsg_ctx* ctx, Scratch& sc, const CsrView& in, TileMat& T
   T.tile_rows = uint32_t((in.rows + 15) / 16);
   T.tile_cols = uint32_t((in.cols + 15) / 16);
   const uint64_t nr = uint64_t(T.tile_rows) + 1;
-  auto* row_nt = sc.alloc<uint32_t>(nr);
-  auto* row_nv = sc.alloc<uint32_t>(nr);
-  TSG_CUDA(cudaMemsetAsync(row_nt + nr - 1, 0, sizeof(uint32_t), ctx->stream));
-  TSG_CUDA(cudaMemsetAsync(row_nv + nr - 1, 0, sizeof(uint32_t), ctx->stream));
-  launch_convert_count(in, T, row_nt, row_nv, err_flag, drop_nonfinite, needed, ctx->stream);
-  check_launch(ctx);
-  T.trp = sc.alloc<uint32_t>(nr);
-  auto* vbase = sc.alloc<uint32_t>(nr);
-  exclusive_sum(ctx, sc, row_nt, T.trp, nr);
-  exclusive_sum(ctx, sc, row_nv, vbase, nr);
   const uint64_t cap = uint64_t(in.nnz);
   T.cap = cap;
-  T.tco = sc.alloc<uint2>(cap);
-  T.rm2 = sc.alloc<uint32_t>(cap * 8);
-  T.trow = sc.alloc<uint32_t>(cap);
+  ConvertScratch cs;
+  cs.rm2 = sc.alloc<uint32_t>(cap * 8);
+  cs.ntiles = sc.alloc<uint32_t>(nr);
+  cs.walk_list = sc.alloc<uint32_t>(nr);
+  cs.walk_count = sc.alloc<uint32_t>(1);
+  TSG_CUDA(cudaMemsetAsync(cs.walk_count, 0, sizeof(uint32_t), ctx->stream));
+  TSG_CUDA(cudaMemsetAsync(cs.ntiles + nr - 1, 0, sizeof(uint32_t), ctx->stream));
   if (roles & 2) {
     T.etile = sc.alloc<uint32_t>(cap);
     T.csr_rp = in.row_ptr;
   }
   for (int role = 0; role < 2; ++role) {
     if (!(roles & (1 << role))) continue;
-    T.meta[role] = sc.alloc<uint2>(cap);
-    T.rec[role] = sc.alloc<uint4>(cap);
+    cs.rec[role] = sc.alloc<uint4>(cap);
     T.chunk[role] = sc.alloc<uint4>(cap + 1);
     TSG_CUDA(cudaMemsetAsync(T.chunk[role], 0, sizeof(uint4), ctx->stream));  // zero chunk 0
   }
-  launch_convert_fill(in, T, roles, T.trp, vbase, drop_nonfinite, needed, ctx->stream);
+  launch_convert(in, T, roles, cs, err_flag, drop_nonfinite, needed, ctx->stream);
+  check_launch(ctx, 2);
+  T.trp = sc.alloc<uint32_t>(nr);
+  exclusive_sum(ctx, sc, cs.ntiles, T.trp, nr);
+  T.tco = sc.alloc<uint2>(cap);
+  T.rm2 = sc.alloc<uint32_t>(cap * 8);
+  T.trow = sc.alloc<uint32_t>(cap);
+  for (int role = 0; role < 2; ++role) {
+    if (!(roles & (1 << role))) continue;
+    T.meta[role] = sc.alloc<uint2>(cap);
+    T.rec[role] = sc.alloc<uint4>(cap);
+  }
+  launch_tiles_compact(in, cs, T, roles, ctx->stream);
   check_launch(ctx);
   return T.trp + nr - 1;
 }
@@ -444,7 +450,7 @@ struct Call {
 
   // realised row counts -> row_ptr; nnz(C) and counted elements to the host,
   // plus (optionally) four more contiguous device totals in the same sync
-  void scan_rows(const unsigned long long* extra = nullptr, unsigned long long* out = nullptr) {
+  void scan_rows(const unsigned long long* extra = nullptr, unsigned long long* out = nullptr, bool check = true) {
     exclusive_sum(ctx, sc, rowcnt, d_rp, uint64_t(rows) + 1);
     const unsigned long long* nz = reinterpret_cast<const unsigned long long*>(d_rp + rows);
     unsigned long long v[6];
@@ -458,7 +464,7 @@ struct Call {
     }
     counted = v[0];
     nnzC = int64_t(v[1]);
-    if (uint64_t(nnzC) >= (uint64_t(1) << 32))
+    if (check && uint64_t(nnzC) >= (uint64_t(1) << 32))
       throw Fail{TSG_ERR_OTHER, "output beyond 2^32 elements needs row-panel batching"};
   }
 
@@ -498,27 +504,36 @@ struct Call {
     auto* row_bound = sc.alloc<uint32_t>(rows + 1);
     auto* row_stage = sc.alloc<uint32_t>(rows + 1);
     TSG_CUDA(cudaMemsetAsync(row_bound + rows, 0, 4, s));
-    launch_panel_count(TA, *TB, rows, row_np, row_ns, row_raw, row_bound, s);
-    check_launch(ctx);
-    exclusive_sum(ctx, sc, row_bound, row_stage, uint64_t(rows) + 1);
     // exact u64 totals: P, S, raw pairs, staging slots (guards the u32 offsets)
     auto* tot_d = sc.alloc<unsigned long long>(4);
     TSG_CUDA(cudaMemsetAsync(tot_d, 0, 4 * sizeof(unsigned long long), s));
-    {
-      const uint64_t n = std::max<uint64_t>(nr, uint64_t(rows) + 1);
-      const unsigned blocks = unsigned(std::min<uint64_t>((n + 255) / 256, 1184));
-      sum_u32_kernel<<<blocks, 256, 0, s>>>(row_np, nr - 1, tot_d);
-      sum_u32_kernel<<<blocks, 256, 0, s>>>(row_ns, nr - 1, tot_d + 1);
-      sum_u32_kernel<<<blocks, 256, 0, s>>>(row_raw, nr - 1, tot_d + 2);
-      sum_u32_kernel<<<blocks, 256, 0, s>>>(row_bound, uint64_t(rows), tot_d + 3);
-      check_launch(ctx, 4);
+    const unsigned sblocks = unsigned(std::min<uint64_t>((std::max<uint64_t>(nr, rows + 1) + 255) / 256, 1184));
+    // Staging bound.  Device output from CSR operands: the element-level bound
+    // (one cheap pass over A's column indices; the numeric pass then counts
+    // the statistics).  Host output (the bound sizes the pinned buffers) and
+    // chained stages: the tight per-output-tile bound of panel_count_kernel.
+    bool elem = !owner->host && !pre_a && !emit_out && tuning_variant("TSG_LIGHT_BOUND", 1) == 1;
+    auto count_bound = [&]() {
+      launch_panel_count(TA, *TB, rows, row_np, row_ns, row_raw, row_bound, s);
+      check_launch(ctx);
+      sum_u32_kernel<<<sblocks, 256, 0, s>>>(row_np, nr - 1, tot_d);
+      sum_u32_kernel<<<sblocks, 256, 0, s>>>(row_ns, nr - 1, tot_d + 1);
+      sum_u32_kernel<<<sblocks, 256, 0, s>>>(row_raw, nr - 1, tot_d + 2);
+      check_launch(ctx, 3);
+    };
+    if (elem) {
+      launch_elem_bound(dA, dB.row_ptr, Bin->cols, row_bound, tot_d + 3, s);
+    } else {
+      count_bound();
+      sum_u32_kernel<<<sblocks, 256, 0, s>>>(row_bound, uint64_t(rows), tot_d + 3);
     }
+    check_launch(ctx);
+    exclusive_sum(ctx, sc, row_bound, row_stage, uint64_t(rows) + 1);
     auto take_totals = [&](const unsigned long long (&v)[4]) {
       P = v[0];
       S = v[1];
       raw = v[2];
       stage_total = v[3];
-      check_stage_total();
     };
     auto read_totals = [&]() {
       const unsigned long long* src[4] = {tot_d, tot_d + 1, tot_d + 2, tot_d + 3};
@@ -526,8 +541,20 @@ struct Call {
       readback_many(ctx, src, v);
       take_totals(v);
     };
+    // an element bound beyond the u32 staging offsets: the tight bound instead
+    auto fall_back = [&]() {
+      elem = false;
+      TSG_CUDA(cudaMemsetAsync(tot_d, 0, 4 * sizeof(unsigned long long), s));
+      count_bound();
+      sum_u32_kernel<<<sblocks, 256, 0, s>>>(row_bound, uint64_t(rows), tot_d + 3);
+      check_launch(ctx);
+      exclusive_sum(ctx, sc, row_bound, row_stage, uint64_t(rows) + 1);
+      read_totals();
+      check_stage_total();
+    };
     if (emit_out) {
       read_totals();
+      check_stage_total();
       light_emit(row_ns);
       return;
     }
@@ -536,7 +563,11 @@ struct Call {
     // against the arena on the device and the totals are read with nnz(C)
     // (a too-small arena -- rare after the first call -- reruns the pass).
     const bool speculative = !owner->host && ctx->stage_cap >= 16;
-    if (!speculative) read_totals();
+    if (!speculative) {
+      read_totals();
+      if (elem && stage_total >= (uint64_t(1) << 32)) fall_back();
+      check_stage_total();
+    }
     record(ctx, timing, 2);
     record(ctx, timing, 3);  // the merge is the sort: no separate phase
     record(ctx, timing, 4);  // the counting pass is fused into the numeric pass
@@ -544,29 +575,43 @@ struct Call {
     uint64_t cap_slots = speculative ? ctx->stage_cap / sizeof(uint2) : stage_total;
     if (timing) TSG_CUDA(cudaEventRecord(ctx->kev[0], s));
     if (owner->host && TA.tile_rows >= 8 * kPipeChunks) {
-      light_host_pipelined(row_stage, stage, cap_slots);
+      light_host_pipelined(row_stage, tot_d + 3, stage, cap_slots);
       return;
     }
-    launch_panel_numeric(TA, *TB, rows, row_stage, cap_slots, stage, rowcnt, counted_d, opt.mode, 0, TA.tile_rows,
-                         s);
+    launch_panel_numeric(TA, *TB, rows, row_stage, cap_slots, stage, rowcnt, counted_d, tot_d + 3,
+                         elem ? tot_d : nullptr, opt.mode, 0, TA.tile_rows, s);
     check_launch(ctx);
     if (timing) TSG_CUDA(cudaEventRecord(ctx->kev[1], s));
     record(ctx, timing, 5);
     if (speculative) {
       unsigned long long t[4];
-      scan_rows(tot_d, t);  // one synchronisation: counted, nnz(C), P, S, raw, staging slots
+      // one synchronisation: counted, nnz(C), P, S, raw, staging slots (the
+      // row counts are meaningless when the pass found the arena too small)
+      scan_rows(tot_d, t, false);
       take_totals(t);
-      if (stage_total > cap_slots) {  // the rare arena overflow: redo the pass
+      if (stage_total > cap_slots || (stage_total >> 32)) {  // the rare arena overflow: redo the pass
+        if (elem && stage_total >= (uint64_t(1) << 32)) fall_back();
+        check_stage_total();
         stage = static_cast<uint2*>(arena(stage_total * sizeof(uint2)));
         cap_slots = stage_total;
         TSG_CUDA(cudaMemsetAsync(counted_d, 0, sizeof(unsigned long long), s));
-        launch_panel_numeric(TA, *TB, rows, row_stage, cap_slots, stage, rowcnt, counted_d, opt.mode, 0,
-                             TA.tile_rows, s);
+        if (elem) TSG_CUDA(cudaMemsetAsync(tot_d, 0, 3 * sizeof(unsigned long long), s));
+        launch_panel_numeric(TA, *TB, rows, row_stage, cap_slots, stage, rowcnt, counted_d, tot_d + 3,
+                             elem ? tot_d : nullptr, opt.mode, 0, TA.tile_rows, s);
         check_launch(ctx);
-        scan_rows();
+        scan_rows(tot_d, t);
+        take_totals(t);
+      } else if (uint64_t(nnzC) >= (uint64_t(1) << 32)) {
+        throw Fail{TSG_ERR_OTHER, "output beyond 2^32 elements needs row-panel batching"};
       }
     } else {
-      scan_rows();
+      if (elem) {
+        unsigned long long t[4];
+        scan_rows(tot_d, t);
+        take_totals(t);
+      } else {
+        scan_rows();
+      }
     }
     alloc_out();
     if (timing) TSG_CUDA(cudaEventRecord(ctx->kev[2], s));
@@ -601,7 +646,8 @@ struct Call {
     TSG_CUDA(cudaMemsetAsync(em.rtiles + nr - 1, 0, sizeof(uint32_t), s));
     em.err_flag = err_flag;
     if (timing) TSG_CUDA(cudaEventRecord(ctx->kev[0], s));
-    launch_panel_numeric(TA, *TB, rows, nullptr, 0, nullptr, nullptr, counted_d, opt.mode, 0, TA.tile_rows, s, &em);
+    launch_panel_numeric(TA, *TB, rows, nullptr, 0, nullptr, nullptr, counted_d, nullptr, nullptr, opt.mode, 0,
+                         TA.tile_rows, s, &em);
     check_launch(ctx);
     if (timing) TSG_CUDA(cudaEventRecord(ctx->kev[1], s));
     record(ctx, timing, 5);
@@ -645,7 +691,8 @@ struct Call {
   // chained scan (each chunk starts from the previous chunk's end, read on
   // the device); host buffers are sized by the staging bound, an upper bound
   // on nnz(C).
-  void light_host_pipelined(const uint32_t* row_stage, uint2* stage, uint64_t cap_slots) {
+  void light_host_pipelined(const uint32_t* row_stage, const unsigned long long* need, uint2* stage,
+                            uint64_t cap_slots) {
     TSG_CUDA(cudaMemsetAsync(d_rp, 0, sizeof(int64_t), s));
     owner->p[0] = pinned_alloc(ctx, (rows + 1) * sizeof(int64_t), &owner->sz[0]);
     owner->p[1] = pinned_alloc(ctx, std::max<uint64_t>(stage_total, 1) * sizeof(int32_t), &owner->sz[1]);
@@ -674,7 +721,8 @@ struct Call {
       const uint32_t I0 = uint32_t(uint64_t(TA.tile_rows) * c / kPipeChunks);
       const uint32_t I1 = uint32_t(uint64_t(TA.tile_rows) * (c + 1) / kPipeChunks);
       const int64_t r0 = int64_t(I0) * 16, r1 = std::min<int64_t>(int64_t(I1) * 16, rows);
-      launch_panel_numeric(TA, *TB, rows, row_stage, cap_slots, stage, rowcnt, counted_d, opt.mode, I0, I1, s);
+      launch_panel_numeric(TA, *TB, rows, row_stage, cap_slots, stage, rowcnt, counted_d, need, nullptr, opt.mode,
+                           I0, I1, s);
       check_launch(ctx);
       // row_ptr[r0 .. r1] = row_ptr[r0] + exclusive prefix (row_ptr[r0] from the previous chunk)
       TSG_CUDA(cub::DeviceScan::ExclusiveScan(tmp, tmp_bytes, rowcnt + r0, d_rp + r0, cuda::std::plus<int64_t>(),

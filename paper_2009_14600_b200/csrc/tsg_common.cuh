@@ -48,7 +48,8 @@ struct TileMat {
   uint2* tco = nullptr;
   uint32_t* rm2 = nullptr;
   uint32_t* trow = nullptr;  // [T] tile row of each tile
-  // (B-role conversions) per input CSR entry: its tile, | kDupEntry unless it
+  // (B-role conversions) per input CSR entry: its tile's rank within its
+  // tile row (add trp[tile row]), | kDupEntry unless it
   // is the first kept entry of that tile in its row, kNoTile if dropped; and
   // the input row pointers -- single-column A tiles enumerate through them
   uint32_t* etile = nullptr;

@@ -11,13 +11,16 @@
 //     (the std::sort at tile_format.cpp:106-110 is replaced by a 16-way
 //      merge across the rows of a tile row: CSR rows are already sorted).
 //
-// One warp per tile row (16 CSR rows, lane r<16 owns row r).  Each step the
-// warp takes the minimum pending tile column (REDUX), every row lane
-// consumes its entries in that tile, and the tile is emitted.  Two passes
-// (count, fill) with a prefix sum between them; the fill pass stages each
-// tile densely in shared memory and cuts the lane-dense operand chunks of
-// one or both roles (A order and/or B order, see tsg_common.cuh), plus the
-// tile's 256-bit occupancy mask and row/column occupancy words.
+// One warp per tile row (16 CSR rows), one pass: the tile row's tiles are
+// counted first (bitmap of tile columns, or the row walk for panels wider
+// than 8192 tile columns), the tile base comes from a decoupled look-back
+// over the preceding tile rows, then each tile is staged densely in shared
+// memory and cut into the lane-dense operand chunks of one or both roles
+// (A order and/or B order, see tsg_common.cuh), plus the tile's 256-bit
+// occupancy mask and row/column occupancy words.
+#include <algorithm>
+#include <type_traits>
+
 #include "tsg_kernels.cuh"
 
 namespace tsg {
@@ -73,217 +76,464 @@ __device__ __forceinline__ unsigned short load_half(const void* val, int64_t p,
   return h;
 }
 
-constexpr int kBitW = 256;  // count-pass bitmap words per warp (8192 tile columns)
+// load_half on an already loaded value (same checks and rounding).
+template <int kDtype, class Raw>
+__device__ __forceinline__ unsigned short raw_to_half(Raw x, bool drop_nonfinite, unsigned& err, bool& keep) {
+  unsigned short h = 0;
+  keep = false;
+  if constexpr (kDtype == 0) {
+    h = x;
+    if ((h & 0x7c00u) == 0x7c00u) {  // inf / nan
+      if (!drop_nonfinite) err |= kErrOverflow;
+      return 0;
+    }
+  } else {
+    if (!isfinite(x)) {
+      if (!drop_nonfinite) err |= kErrOverflow;
+      return 0;
+    }
+    if (fabs(double(x)) > 65504.0) {
+      err |= kErrOverflow;
+      return 0;
+    }
+    if constexpr (kDtype == 1)
+      h = __half_as_ushort(__float2half_rn(x));
+    else
+      h = f64_to_half_bits(x);
+  }
+  keep = (h & 0x7fffu) != 0;  // exact zero or underflow-to-(+-)0 dropped
+  return h;
+}
 
-template <bool kFill, int kDtype>
-__global__ void __launch_bounds__(256) convert_kernel(CsrView in, TileMat out, int roles,
-                                                     const uint32_t* __restrict__ tile_base,
-                                                     const uint32_t* __restrict__ val_base,
-                                                     uint32_t* __restrict__ row_ntiles,
-                                                     uint32_t* __restrict__ row_nvals,
-                                                     unsigned* __restrict__ err_flag,
-                                                     int drop_nonfinite,
-                                                     const uint8_t* __restrict__ needed) {
-  // per warp: the tile staged densely (row-major) and transposed, as fp16 bits
-  __shared__ __align__(16) uint16_t s_tile[8][2][256];
-  __shared__ uint32_t s_bits[kFill ? 1 : 8][kBitW];  // count pass: tile-column bitmap
-  const int lane = threadIdx.x & 31;
-  const int wib = threadIdx.x >> 5;
+constexpr int kBitW = 256;  // fast path: bitmap words (panels spanning <= 8192 tile columns)
+constexpr int kFastT = 64;  // fast path: tiles per panel
+constexpr int kFastU = 16;  // fast path: entries per lane (panels of <= 512 entries)
+
+// Output of the conversion kernels before compaction: tile row I's tiles at
+// slots [E0, E0 + n) with E0 = its first CSR entry (a panel never holds more
+// tiles than entries), chunks from 1 + E0 per role; the dense CSR-of-tiles
+// arrays are derived from rm2 + rec by tiles_compact_kernel.
+struct Gapped {
+  uint32_t* rm2 = nullptr;
+  uint4* rec[2] = {nullptr, nullptr};  // {lane mask, first chunk, occupancy, tile col}
+  uint4* chunk[2] = {nullptr, nullptr};
+  uint32_t* etile = nullptr;  // per entry: tile rank within its tile row | kDupEntry, or kNoTile
+  uint32_t* ntiles = nullptr;  // per tile row
+};
+
+struct FastSmem {
+  uint32_t bits[kBitW];       // tile-column bitmap of the panel
+  uint16_t pre[kBitW];        // tiles before each bitmap word
+  uint32_t rm[kFastT][8];     // per tile: word g = row g | row g+8 << 16
+  uint32_t lm[kFastT][2];     // per tile and role: lane presence mask
+  uint32_t cb[kFastT][2];     // per tile and role: first chunk
+};
+
+// Tile-slot (r, c) of a 16x16 tile -> its lane and fp16 position in the
+// lane's 16-byte chunk.  A order: lane (g, t) holds rows g, g+8 x cols 2t,
+// 2t+1, 2t+8, 2t+9 in regs i = (r>>3) + 2(c>>3).  B order (the transposed
+// tile, regs stored {0, 2, 1, 3}): lane (c&7, (r&7)>>1), word
+// 2(c>>3) + (r>>3), half r&1.
+__device__ __forceinline__ void slot_lane(int role, int r, int c, int& L, int& h16) {
+  if (role == kRoleA) {
+    L = (r & 7) * 4 + ((c & 7) >> 1);
+    h16 = 2 * ((r >> 3) + 2 * (c >> 3)) + (c & 1);
+  } else {
+    L = (c & 7) * 4 + ((r & 7) >> 1);
+    h16 = 2 * (2 * (c >> 3) + (r >> 3)) + (r & 1);
+  }
+}
+
+// Fast path, warp per tile row (panel): the panel's entries are loaded once
+// (coalesced, up to kFastU per lane, kept in registers); their tile columns
+// are marked in a bitmap whose prefix popcounts rank the tiles; shared-memory
+// atomics build each tile's 256-bit mask and lane presence masks; a prefix
+// over the tiles gives the chunk bases; the chunk ranges are zeroed and
+// every entry stores its fp16 value at its chunk slot.  Panels outside the
+// limits go to the walk list.
+template <int kDtype>
+__global__ void __launch_bounds__(256, 4) convert_fast_kernel(CsrView in, uint32_t tile_rows, Gapped out, int roles,
+                                                          uint32_t* __restrict__ walk_list,
+                                                          uint32_t* __restrict__ walk_count,
+                                                          unsigned* __restrict__ err_flag, int drop_nonfinite,
+                                                          const uint8_t* __restrict__ needed) {
+  __shared__ __align__(16) FastSmem smem[8];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const uint32_t I = blockIdx.x * 8 + wib;
-  if (I >= out.tile_rows) return;
-  uint16_t* st = s_tile[wib][0];
-  uint16_t* stT = s_tile[wib][1];
-
-  const int64_t row = int64_t(I) * kTile + lane;
+  if (I >= tile_rows) return;
+  FastSmem& sm = smem[wib];
+  const int64_t r0 = int64_t(I) * kTile, r1 = r0 + kTile < in.rows ? r0 + kTile : in.rows;
+  const int64_t row = r0 + lane;
   const bool has_row = lane < kTile && row < in.rows;
-  int64_t p = has_row ? in.row_ptr[row] : 0;
+  const int64_t p = has_row ? in.row_ptr[row] : 0;
   const int64_t end = has_row ? in.row_ptr[row + 1] : 0;
+  const int64_t E0 = in.row_ptr[r0], E1 = in.row_ptr[r1];
+  const bool rows_ok = __all_sync(kFull, !has_row || (end >= p && p >= E0 && end <= E1));
+  if (!rows_ok || E1 - E0 > 32 * kFastU || E1 < E0) {  // the walk (it validates an unreferenced panel too)
+    if (lane == 0) walk_list[atomicAdd(walk_count, 1u)] = I;
+    return;
+  }
+  const uint32_t E = uint32_t(E1 - E0);
+  // every load of the panel in flight at once: columns and raw values
+  int32_t c[kFastU];
+  using Raw = typename std::conditional<kDtype == 2, double, typename std::conditional<kDtype == 1, float,
+                                                                                      unsigned short>::type>::type;
+  Raw v[kFastU];
+#pragma unroll
+  for (int u = 0; u < kFastU; ++u) {
+    const uint32_t q = 32 * u + lane;
+    c[u] = q < E ? __ldg(in.col + E0 + q) : -1;
+    v[u] = q < E ? __ldg(static_cast<const Raw*>(in.val) + E0 + q) : Raw(0);
+  }
+  const bool skip = needed && !needed[I];
+  uint32_t jlo = 0xffffffffu, jhi = 0;
+#pragma unroll
+  for (int u = 0; u < kFastU; ++u)
+    if (c[u] >= 0) {
+      jlo = min(jlo, uint32_t(c[u]) >> 4);
+      jhi = max(jhi, uint32_t(c[u]) >> 4);
+    }
+  jlo = __reduce_min_sync(kFull, jlo);
+  jhi = __reduce_max_sync(kFull, jhi);
+  if (jlo != 0xffffffffu && jhi - jlo >= uint32_t(kBitW) * 32u) {  // too wide for the bitmap
+    if (lane == 0) walk_list[atomicAdd(walk_count, 1u)] = I;
+    return;
+  }
+  // lane r < 16: offset of row r's first entry in the panel (rows past the end: E)
+  const uint32_t rs = lane < kTile && row < in.rows ? uint32_t(p - E0) : E;
+  for (int i = lane; i < kBitW; i += 32) sm.bits[i] = 0;
+  __syncwarp();
   unsigned err = 0;
-  int32_t prev_col = -1;
-  if (!kFill && has_row && end < p) err |= kErrInvariant;
-
-  // A tile row no tile of the other operand refers to is only validated (the
-  // reference validates the whole input, tile_format.cpp:34-51): no tiles.
-  if (needed && !needed[I]) {
-    if (kFill) {
-      if (out.etile)
-        for (; p < end; ++p) out.etile[p] = kNoTile;
-      return;
-    }
-    for (; p < end; ++p) {
-      const int32_t c = __ldg(in.col + p);
-      if (c <= prev_col || c >= in.cols || c < 0) err |= kErrInvariant;
-      prev_col = c;
+  // entries: column, and packed {fp16 bits, row, kept}
+  uint32_t pk[kFastU];
+#pragma unroll
+  for (int u = 0; u < kFastU; ++u) {
+    pk[u] = 0;
+    if (32u * u >= E) break;
+    const uint32_t q = 32 * u + lane;
+    const int32_t up = __shfl_up_sync(kFull, c[u], 1);
+    const int32_t last = __shfl_sync(kFull, c[u > 0 ? u - 1 : 0], 31);  // lane 31 of the previous step
+    const int32_t cprev = lane > 0 ? up : (u > 0 ? last : -1);
+    int r = 0;  // last row whose start is <= q
+#pragma unroll
+    for (int b = 8; b > 0; b >>= 1)
+      if (__shfl_sync(kFull, rs, r + b) <= q) r += b;
+    const uint32_t first = __shfl_sync(kFull, rs, r);
+    if (q < E) {
       bool keep;
-      load_half<kDtype>(in.val, p, drop_nonfinite, err, keep);
+      const uint16_t h = raw_to_half<kDtype>(v[u], drop_nonfinite, err, keep);
+      if (c[u] >= in.cols || c[u] < 0 || (q > first && c[u] <= cprev)) err |= kErrInvariant;
+      const uint32_t j = (uint32_t(c[u]) >> 4) - jlo;
+      keep = keep && !skip && c[u] >= 0 && j < uint32_t(kBitW) * 32u;
+      if (keep) atomicOr(&sm.bits[j >> 5], 1u << (j & 31));
+      else if (out.etile) out.etile[E0 + q] = kNoTile;
+      pk[u] = uint32_t(h) | (uint32_t(r) << 16) | (keep ? 1u << 20 : 0u);
     }
-    const unsigned e = __reduce_or_sync(kFull, err);
+  }
+  __syncwarp();
+  // ranks: tiles before each bitmap word (lane owns words 8 lane .. 8 lane + 7)
+  uint32_t wc[8], lsum = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    wc[i] = __popc(sm.bits[8 * lane + i]);
+    lsum += wc[i];
+  }
+  uint32_t incl = lsum;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t v = __shfl_up_sync(kFull, incl, o);
+    if (lane >= o) incl += v;
+  }
+  const uint32_t ntiles = __shfl_sync(kFull, incl, 31);
+  {
+    uint32_t run = incl - lsum;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      sm.pre[8 * lane + i] = uint16_t(run);
+      run += wc[i];
+    }
+  }
+  const unsigned e_all = __reduce_or_sync(kFull, err);
+  if (skip || ntiles > uint32_t(kFastT)) {
     if (lane == 0) {
-      row_ntiles[I] = 0;
-      row_nvals[I] = 0;
-      if (e) atomicOr(err_flag, e);
+      if (skip) out.ntiles[I] = 0;
+      else walk_list[atomicAdd(walk_count, 1u)] = I;  // too many tiles: the walk (re-validates)
+      if (skip && e_all) atomicOr(err_flag, e_all);
     }
     return;
   }
-  if (!kFill) {
-    // Count pass over a panel whose tile columns span at most kBitW*32 tiles
-    // (banded matrices: FEM27, Poisson): no merge -- lanes take the panel's
-    // entries (contiguous in the CSR) 32 at a time, validate them
-    // (tile_format.cpp:34-51, 82-96) and mark each kept entry's tile column
-    // in a bitmap; tiles = popcount.  Wider panels take the merge below.
-    const int64_t r0 = int64_t(I) * kTile, r1 = r0 + kTile < in.rows ? r0 + kTile : in.rows;
-    const int64_t E0 = in.row_ptr[r0], E1 = in.row_ptr[r1];
-    const bool rows_ok = __all_sync(kFull, !has_row || end >= p);
-    uint32_t jlo = 0xffffffffu, jhi = 0;
-    if (has_row && end > p) {
-      jlo = uint32_t(__ldg(in.col + p)) >> 4;
-      jhi = uint32_t(__ldg(in.col + end - 1)) >> 4;
-    }
-    jlo = __reduce_min_sync(kFull, jlo);
-    jhi = __reduce_max_sync(kFull, jhi);
-    if (rows_ok && E1 >= E0 && (jlo == 0xffffffffu || jhi - jlo < uint32_t(kBitW) * 32u)) {
-      uint32_t* bm = s_bits[wib];
-      for (int i = lane; i < kBitW; i += 32) bm[i] = 0;
-      __syncwarp();
-      // lane r < 16: first entry of row r (rows past the panel: E1)
-      const int64_t rstart = lane < kTile && row < in.rows ? p : E1;
-      uint32_t nv = 0;
-      for (int64_t q0 = E0; q0 < E1; q0 += 32) {
-        const int64_t q = q0 + lane;
-        int r = 0;  // last row whose start is <= q
+  for (uint32_t i = lane; i < ntiles * 8u; i += 32) sm.rm[i >> 3][i & 7] = 0;
+  for (uint32_t i = lane; i < ntiles * 2u; i += 32) sm.lm[i >> 1][i & 1] = 0;
+  __syncwarp();
+  // tile rank of each kept entry; masks
+  uint32_t carry = 0xffffffffu;  // (row, tile) key of the last kept entry so far
 #pragma unroll
-        for (int b = 8; b > 0; b >>= 1) {
-          const int64_t v = __shfl_sync(kFull, rstart, r + b);
-          if (v <= q) r += b;
-        }
-        const int64_t first = __shfl_sync(kFull, rstart, r);
-        if (q < E1) {
-          const int32_t c = __ldg(in.col + q);
-          if (c >= in.cols || c < 0 || (q > first && c <= __ldg(in.col + q - 1))) err |= kErrInvariant;
-          bool keep;
-          load_half<kDtype>(in.val, q, drop_nonfinite, err, keep);
-          const uint32_t j = (uint32_t(c) >> 4) - jlo;
-          if (keep && c >= 0 && j < uint32_t(kBitW) * 32u) {
-            atomicOr(bm + (j >> 5), 1u << (j & 31));
-            ++nv;
-          }
-        }
+  for (int u = 0; u < kFastU; ++u) {
+    if (32u * u >= E) break;
+    const bool keep = (pk[u] >> 20) & 1u;
+    const int r = (pk[u] >> 16) & 15;
+    uint32_t k = 0;
+    if (keep) {
+      const uint32_t j = (uint32_t(c[u]) >> 4) - jlo;
+      k = sm.pre[j >> 5] + __popc(sm.bits[j >> 5] & ((1u << (j & 31)) - 1u));
+      const int cc = c[u] & 15;
+      atomicOr(&sm.rm[k][r & 7], 1u << (cc + 16 * (r >> 3)));
+      int L, h16;
+      slot_lane(kRoleA, r, cc, L, h16);
+      atomicOr(&sm.lm[k][0], 1u << L);
+      slot_lane(kRoleB, r, cc, L, h16);
+      atomicOr(&sm.lm[k][1], 1u << L);
+      pk[u] |= k << 21;  // k < 64: bits 21..26
+    }
+    if (out.etile) {  // the first kept entry of each (row, tile) names the tile; later ones are duplicates
+      const uint32_t key = keep ? (uint32_t(r) << 16) | k : 0xfffffffeu;
+      const unsigned kb = __ballot_sync(kFull, keep);
+      const unsigned peers = __match_any_sync(kFull, key) & kb;
+      if (keep) {
+        const bool dup = (peers & lanemask_lt()) != 0u || key == carry;
+        out.etile[E0 + 32 * u + lane] = k | (dup ? kDupEntry : 0u);
       }
-      __syncwarp();
-      uint32_t nt = 0;
-      for (int i = lane; i < kBitW; i += 32) nt += __popc(bm[i]);
-      nt = __reduce_add_sync(kFull, nt);
-      nv = __reduce_add_sync(kFull, nv);
+      if (kb) carry = __shfl_sync(kFull, key, 31 - __clz(kb));
+    }
+  }
+  __syncwarp();
+  // per tile (lane k, k + 32): chunk bases, metadata
+  uint32_t cbA[2], cbB[2];
+  {
+    uint32_t nA[2], nB[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const uint32_t k = lane + 32 * h;
+      nA[h] = k < ntiles ? __popc(sm.lm[k][0]) : 0u;
+      nB[h] = k < ntiles ? __popc(sm.lm[k][1]) : 0u;
+    }
+    uint32_t ia = nA[0], ib = nB[0];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t va = __shfl_up_sync(kFull, ia, o), vb = __shfl_up_sync(kFull, ib, o);
+      if (lane >= o) {
+        ia += va;
+        ib += vb;
+      }
+    }
+    const uint32_t ta = __shfl_sync(kFull, ia, 31), tb = __shfl_sync(kFull, ib, 31);
+    uint32_t ja = nA[1], jb = nB[1];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t va = __shfl_up_sync(kFull, ja, o), vb = __shfl_up_sync(kFull, jb, o);
+      if (lane >= o) {
+        ja += va;
+        jb += vb;
+      }
+    }
+    const uint32_t base = 1u + uint32_t(E0);
+    cbA[0] = base + ia - nA[0];
+    cbB[0] = base + ib - nB[0];
+    cbA[1] = base + ta + ja - nA[1];
+    cbB[1] = base + tb + jb - nB[1];
+    const uint32_t totA = ta + __shfl_sync(kFull, ja, 31), totB = tb + __shfl_sync(kFull, jb, 31);
+    // zero the panel's chunk ranges (the values are stored into them below)
+    for (uint32_t i = lane; i < totA && (roles & 1); i += 32) out.chunk[kRoleA][base + i] = make_uint4(0, 0, 0, 0);
+    for (uint32_t i = lane; i < totB && (roles & 2); i += 32) out.chunk[kRoleB][base + i] = make_uint4(0, 0, 0, 0);
+  }
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const uint32_t k = lane + 32 * h;
+    if (k >= ntiles) continue;
+    // tile column: the k-th set bit of the bitmap
+    int w = 0;
+#pragma unroll
+    for (int b = kBitW / 2; b > 0; b >>= 1)
+      if (sm.pre[w + b] <= k) w += b;
+    uint32_t word = sm.bits[w];
+    for (uint32_t n = k - sm.pre[w]; n > 0; --n) word &= word - 1u;
+    const uint32_t J = jlo + uint32_t(w) * 32u + uint32_t(__ffs(word) - 1);
+    uint32_t colocc = 0, rowocc = 0;
+    const uint4* rmv = reinterpret_cast<const uint4*>(sm.rm[k]);
+    uint4 m0 = rmv[0], m1 = rmv[1];
+    const uint32_t mw[8] = {m0.x, m0.y, m0.z, m0.w, m1.x, m1.y, m1.z, m1.w};
+#pragma unroll
+    for (int gg = 0; gg < 8; ++gg) {
+      colocc |= mw[gg] | (mw[gg] >> 16);
+      rowocc |= ((mw[gg] & 0xffffu) != 0u ? 1u << gg : 0u) | ((mw[gg] >> 16) != 0u ? 1u << (gg + 8) : 0u);
+    }
+    const uint32_t occ = (colocc & 0xffffu) | (rowocc << 16);
+    uint4* dst = reinterpret_cast<uint4*>(out.rm2 + size_t(E0 + k) * 8);
+    dst[0] = m0;
+    dst[1] = m1;
+    if (roles & 1) out.rec[kRoleA][E0 + k] = make_uint4(sm.lm[k][0], cbA[h], occ, J);
+    if (roles & 2) out.rec[kRoleB][E0 + k] = make_uint4(sm.lm[k][1], cbB[h], occ, J);
+    sm.cb[k][0] = cbA[h];
+    sm.cb[k][1] = cbB[h];
+  }
+  __syncwarp();  // chunk zeros before the value stores (same warp: ordered by the barrier)
+  // every kept entry stores its fp16 value into its chunk slots
+#pragma unroll
+  for (int u = 0; u < kFastU; ++u) {
+    if (32u * u >= E) break;
+    if (!((pk[u] >> 20) & 1u)) continue;
+    const uint32_t k = (pk[u] >> 21) & 63u;
+    const int r = (pk[u] >> 16) & 15, cc = c[u] & 15;
+    const uint16_t hv = uint16_t(pk[u]);
+#pragma unroll
+    for (int role = 0; role < 2; ++role) {
+      if (!(roles & (1 << role))) continue;
+      int L, h16;
+      slot_lane(role, r, cc, L, h16);
+      const uint32_t idx = sm.cb[k][role] + __popc(sm.lm[k][role] & ((1u << L) - 1u));
+      reinterpret_cast<uint16_t*>(out.chunk[role] + idx)[h16] = hv;
+    }
+  }
+  if (lane == 0) {
+    out.ntiles[I] = ntiles;
+    if (e_all) atomicOr(err_flag, e_all);
+  }
+}
+
+// A-order regs of a densely staged tile (row-major fp16 bits): lane (g, t)
+// holds reg i = rows g + 8(i&1), cols 2t + 8(i>>1) .. +1.
+__device__ __forceinline__ void staged_regs(const uint16_t* tl, int lane, uint32_t (&r)[4]) {
+  const int g = lane >> 2, tq = lane & 3;
+  const uint32_t* tw = reinterpret_cast<const uint32_t*>(tl);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) r[i] = tw[((g + 8 * (i & 1)) * 16 + 2 * tq + 8 * (i >> 1)) >> 1];
+}
+
+// The general panel walk (any column span, any number of tiles): warp per
+// listed tile row, lanes r < 16 own CSR rows; each step takes the minimum
+// pending tile column (REDUX), every row lane consumes its entries in that
+// tile, and the tile is staged densely and cut.
+template <int kDtype>
+__global__ void __launch_bounds__(256) convert_walk_kernel(CsrView in, Gapped out, int roles,
+                                                          const uint32_t* __restrict__ walk_list,
+                                                          const uint32_t* __restrict__ walk_count,
+                                                          unsigned* __restrict__ err_flag, int drop_nonfinite,
+                                                          const uint8_t* __restrict__ needed) {
+  __shared__ __align__(16) uint16_t s_tile[8][2][256];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  uint16_t* st = s_tile[wib][0];
+  uint16_t* stT = s_tile[wib][1];
+  const uint32_t n_list = *walk_count;
+  for (uint32_t li = blockIdx.x * 8 + wib; li < n_list; li += gridDim.x * 8) {
+    const uint32_t I = walk_list[li];
+    const int64_t row = int64_t(I) * kTile + lane;
+    const bool has_row = lane < kTile && row < in.rows;
+    int64_t p = has_row ? in.row_ptr[row] : 0;
+    const int64_t end = has_row ? in.row_ptr[row + 1] : 0;
+    const int64_t E0 = in.row_ptr[int64_t(I) * kTile];
+    unsigned err = 0;
+    if (has_row && end < p) err |= kErrInvariant;
+    if (needed && !needed[I]) {  // validation only (tile_format.cpp:34-51): no tiles
+      int32_t prev_col = -1;
+      for (int64_t q = p; q < end; ++q) {
+        const int32_t c = __ldg(in.col + q);
+        if (c <= prev_col || c >= in.cols || c < 0) err |= kErrInvariant;
+        prev_col = c;
+        bool keep;
+        load_half<kDtype>(in.val, q, drop_nonfinite, err, keep);
+        if (out.etile) out.etile[q] = kNoTile;
+      }
       const unsigned e = __reduce_or_sync(kFull, err);
       if (lane == 0) {
-        row_ntiles[I] = nt;
-        row_nvals[I] = nv;
+        out.ntiles[I] = 0;
         if (e) atomicOr(err_flag, e);
       }
-      return;
+      continue;
     }
-  }
-  uint32_t ntiles = 0, nvals = 0;
-  uint32_t tbase = 0;
-  uint32_t cbase[2] = {0, 0};
-  if (kFill) {
-    tbase = tile_base[I];
-    // chunk capacity of a tile row = its kept nnz (every present lane holds >= 1)
-    cbase[0] = cbase[1] = 1u + val_base[I];
-  }
-  // column of the lane's next entry, loaded one entry ahead so the row walk
-  // below is not a chain of dependent global loads
-  int32_t c_cur = p < end ? __ldg(in.col + p) : 0;
-  while (true) {
-    const uint32_t my_tc = (p < end) ? uint32_t(c_cur) >> 4 : 0xffffffffu;
-    const uint32_t J = __reduce_min_sync(kFull, my_tc);
-    if (J == 0xffffffffu) break;
-    if (kFill) {
+    uint32_t ntiles = 0;
+    uint32_t cbase[2] = {1u + uint32_t(E0), 1u + uint32_t(E0)};
+    int32_t prev_col = -1;
+    int32_t c_cur = p < end ? __ldg(in.col + p) : 0;  // one entry ahead: the walk is not a chain of loads
+    while (true) {
+      const uint32_t my_tc = (p < end) ? uint32_t(c_cur) >> 4 : 0xffffffffu;
+      const uint32_t J = __reduce_min_sync(kFull, my_tc);
+      if (J == 0xffffffffu) break;
       reinterpret_cast<uint4*>(st)[lane] = make_uint4(0, 0, 0, 0);
       reinterpret_cast<uint4*>(stT)[lane] = make_uint4(0, 0, 0, 0);
       __syncwarp();
-    }
-    uint32_t rm = 0;
-    bool first = true;  // first kept entry of this tile in this row
-    while (p < end) {
-      const int32_t c = c_cur;
-      if ((uint32_t(c) >> 4) != J) break;
-      const int32_t c_next = p + 1 < end ? __ldg(in.col + p + 1) : 0;
-      if (!kFill) {
+      uint32_t rm = 0;
+      bool first = true;  // first kept entry of this tile in this row
+      while (p < end) {
+        const int32_t c = c_cur;
+        if ((uint32_t(c) >> 4) != J) break;
+        const int32_t c_next = p + 1 < end ? __ldg(in.col + p + 1) : 0;
         if (c <= prev_col || c >= in.cols || c < 0) err |= kErrInvariant;
         prev_col = c;
-      }
-      bool keep;
-      const unsigned short h = load_half<kDtype>(in.val, p, drop_nonfinite, err, keep);
-      if (keep) {
-        rm |= 1u << (c & 15);
-        if (kFill) {
+        bool keep;
+        const unsigned short h = load_half<kDtype>(in.val, p, drop_nonfinite, err, keep);
+        if (keep) {
+          rm |= 1u << (c & 15);
           st[lane * 16 + (c & 15)] = h;
           stT[(c & 15) * 16 + lane] = h;
         }
+        if (out.etile) {
+          out.etile[p] = keep ? (ntiles | (first ? 0u : kDupEntry)) : kNoTile;
+          first &= !keep;
+        }
+        ++p;
+        c_cur = c_next;
       }
-      if (kFill && out.etile) {
-        out.etile[p] = keep ? ((tbase + ntiles) | (first ? 0u : kDupEntry)) : kNoTile;
-        first &= !keep;
-      }
-      ++p;
-      c_cur = c_next;
-    }
-    // Termination holds for any input: the lane holding the minimum tile
-    // column always consumes at least one entry.  Invalid input only sets
-    // the flag; the host discards the results.
-    const unsigned any = __ballot_sync(kFull, rm != 0);
-    if (any == 0) continue;  // every value of this tile dropped
-    const uint32_t tile_nnz = __reduce_add_sync(kFull, __popc(rm));
-    if (kFill) {
+      // Termination holds for any input: the lane holding the minimum tile
+      // column always consumes at least one entry.  Invalid input only sets
+      // the flag; the host discards the results.
+      const unsigned any = __ballot_sync(kFull, rm != 0);
+      if (any == 0) continue;  // every value of this tile dropped
       __syncwarp();
-      const uint32_t t = tbase + ntiles;
-      const uint32_t colocc = __reduce_or_sync(kFull, rm) & 0xffffu;
-      if (lane == 0) {
-        out.tco[t] = make_uint2(J, colocc | ((any & 0xffffu) << 16));
-        out.trow[t] = I;
-      }
+      const uint32_t t = uint32_t(E0) + ntiles;
+      const uint32_t occ = (__reduce_or_sync(kFull, rm) & 0xffffu) | ((any & 0xffffu) << 16);
       // the 256-bit mask as interleaved row masks: word g = row g | row g+8 << 16
       const uint32_t rm_hi = __shfl_sync(kFull, rm, (lane & 7) + 8);
       if (lane < 8) out.rm2[size_t(t) * 8 + lane] = rm | (rm_hi << 16);
-      // cut the lane chunks: A order reads row pairs (r, 2t..2t+1) of the
-      // staged tile, B order the same pairs of the transposed tile
 #pragma unroll
       for (int role = 0; role < 2; ++role) {
         if (!(roles & (1 << role))) continue;
-        const uint16_t* src = role == kRoleA ? st : stT;
-        const int g = lane >> 2, tq = lane & 3;
-        uint32_t reg[4];
-#pragma unroll
-        for (int i = 0; i < 4; ++i)  // reg i = rows g + 8(i&1), cols 2t + 8(i>>1) .. +1
-          reg[i] = *reinterpret_cast<const uint32_t*>(src + (g + 8 * (i & 1)) * 16 + 2 * tq + 8 * (i >> 1));
-        const bool present = (reg[0] | reg[1] | reg[2] | reg[3]) != 0u;
-        const unsigned lm = __ballot_sync(kFull, present);
-        // B chunks are stored {reg0, reg2, reg1, reg3}: the {b0, b1} operand
-        // pair of each n8 MMA is then one aligned register pair
-        if (present)
-          out.chunk[role][cbase[role] + __popc(lm & lanemask_lt())] =
-              role == kRoleA ? make_uint4(reg[0], reg[1], reg[2], reg[3])
-                             : make_uint4(reg[0], reg[2], reg[1], reg[3]);
-        if (lane == 0) {
-          out.meta[role][t] = make_uint2(lm, cbase[role]);
-          if (out.rec[role]) out.rec[role][t] = make_uint4(lm, cbase[role], colocc | ((any & 0xffffu) << 16), J);
+        uint32_t rg[4];
+        staged_regs(role == kRoleA ? st : stT, lane, rg);
+        if (role == kRoleB) {  // the transposed tile in A order, stored {reg0, reg2, reg1, reg3}
+          const uint32_t t1 = rg[1];
+          rg[1] = rg[2];
+          rg[2] = t1;
         }
+        const bool present = (rg[0] | rg[1] | rg[2] | rg[3]) != 0u;
+        const unsigned lm = __ballot_sync(kFull, present);
+        if (present) out.chunk[role][cbase[role] + __popc(lm & lanemask_lt())] = make_uint4(rg[0], rg[1], rg[2], rg[3]);
+        if (lane == 0) out.rec[role][t] = make_uint4(lm, cbase[role], occ, J);
         cbase[role] += __popc(lm);
       }
       __syncwarp();
+      ++ntiles;
     }
-    ++ntiles;
-    nvals += tile_nnz;
-  }
-  if (!kFill) {
     const unsigned e = __reduce_or_sync(kFull, err);
     if (lane == 0) {
-      row_ntiles[I] = ntiles;
-      row_nvals[I] = nvals;
+      out.ntiles[I] = ntiles;
       if (e) atomicOr(err_flag, e);
     }
   }
+}
+
+// Gapped tiles -> the dense CSR-of-tiles arrays (warp per tile row).
+__global__ void __launch_bounds__(256) tiles_compact_kernel(CsrView in, uint32_t tile_rows, Gapped g, TileMat T,
+                                                           int roles) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t I = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (I >= tile_rows) return;
+  const uint32_t src = uint32_t(in.row_ptr[int64_t(I) * kTile]), dst = T.trp[I], n = g.ntiles[I];
+  const int r0 = (roles & 1) ? 0 : 1;
+  for (uint32_t i = lane; i < n; i += 32) {
+    const uint4 rec0 = g.rec[r0][src + i];
+    T.tco[dst + i] = make_uint2(rec0.w, rec0.z);
+    T.trow[dst + i] = I;
+#pragma unroll
+    for (int role = 0; role < 2; ++role) {
+      if (!(roles & (1 << role))) continue;
+      const uint4 rc = role == r0 ? rec0 : g.rec[role][src + i];
+      T.meta[role][dst + i] = make_uint2(rc.x, rc.y);
+      T.rec[role][dst + i] = rc;
+    }
+  }
+  const uint4* s4 = reinterpret_cast<const uint4*>(g.rm2 + size_t(src) * 8);
+  uint4* d4 = reinterpret_cast<uint4*>(T.rm2 + size_t(dst) * 8);
+  for (uint32_t i = lane; i < 2 * n; i += 32) d4[i] = s4[i];
 }
 
 // B tile rows that some A tile refers to (A's tile columns).
@@ -325,26 +575,33 @@ __global__ void cbar_dot_kernel(const unsigned* __restrict__ hist, const int64_t
 
 }  // namespace
 
-void launch_convert_count(const CsrView& in, TileMat& out, uint32_t* row_ntiles,
-                          uint32_t* row_nvals, unsigned* err_flag, int drop_nonfinite,
-                          const uint8_t* needed, cudaStream_t st) {
-  const unsigned blocks = (out.tile_rows + 7) / 8;
-  if (blocks == 0) return;
-  auto k = in.dtype == 0 ? convert_kernel<false, 0> : in.dtype == 2 ? convert_kernel<false, 2>
-                                                                    : convert_kernel<false, 1>;
-  k<<<blocks, 256, 0, st>>>(in, out, 0, nullptr, nullptr, row_ntiles, row_nvals, err_flag,
-                            drop_nonfinite, needed);
+void launch_convert(const CsrView& in, TileMat& out, int roles, const ConvertScratch& cs, unsigned* err_flag,
+                    int drop_nonfinite, const uint8_t* needed, cudaStream_t st) {
+  if (out.tile_rows == 0) return;
+  Gapped g;
+  g.rm2 = cs.rm2;
+  g.rec[0] = cs.rec[0];
+  g.rec[1] = cs.rec[1];
+  g.chunk[0] = out.chunk[0];
+  g.chunk[1] = out.chunk[1];
+  g.etile = out.etile;
+  g.ntiles = cs.ntiles;
+  auto kf = in.dtype == 0 ? convert_fast_kernel<0> : in.dtype == 2 ? convert_fast_kernel<2> : convert_fast_kernel<1>;
+  kf<<<(out.tile_rows + 7) / 8, 256, 0, st>>>(in, out.tile_rows, g, roles, cs.walk_list, cs.walk_count, err_flag,
+                                    drop_nonfinite, needed);
+  auto kw = in.dtype == 0 ? convert_walk_kernel<0> : in.dtype == 2 ? convert_walk_kernel<2> : convert_walk_kernel<1>;
+  const unsigned wblocks = std::min<unsigned>((out.tile_rows + 7) / 8, 148u * 8u);
+  kw<<<wblocks, 256, 0, st>>>(in, g, roles, cs.walk_list, cs.walk_count, err_flag, drop_nonfinite, needed);
 }
 
-void launch_convert_fill(const CsrView& in, TileMat& out, int roles, const uint32_t* tile_base,
-                         const uint32_t* val_base, int drop_nonfinite, const uint8_t* needed,
-                         cudaStream_t st) {
-  const unsigned blocks = (out.tile_rows + 7) / 8;
-  if (blocks == 0) return;
-  auto k = in.dtype == 0 ? convert_kernel<true, 0> : in.dtype == 2 ? convert_kernel<true, 2>
-                                                                   : convert_kernel<true, 1>;
-  k<<<blocks, 256, 0, st>>>(in, out, roles, tile_base, val_base, nullptr, nullptr, nullptr,
-                            drop_nonfinite, needed);
+void launch_tiles_compact(const CsrView& in, const ConvertScratch& cs, TileMat& out, int roles, cudaStream_t st) {
+  if (out.tile_rows == 0) return;
+  Gapped g;
+  g.rm2 = cs.rm2;
+  g.rec[0] = cs.rec[0];
+  g.rec[1] = cs.rec[1];
+  g.ntiles = cs.ntiles;
+  tiles_compact_kernel<<<(out.tile_rows + 7) / 8, 256, 0, st>>>(in, out.tile_rows, g, out, roles);
 }
 
 void launch_mark_needed(const TileMat& A, uint8_t* needed, cudaStream_t st) {

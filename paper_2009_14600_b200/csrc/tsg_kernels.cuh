@@ -46,12 +46,22 @@ struct Staged {
 // (1) conversion
 // `needed` (nullable): per tile row, whether the other operand refers to it;
 // unneeded tile rows are validated but get no tiles
-void launch_convert_count(const CsrView& in, TileMat& out, uint32_t* row_ntiles,
-                          uint32_t* row_nvals, unsigned* err_flag, int drop_nonfinite,
-                          const uint8_t* needed, cudaStream_t st);
-void launch_convert_fill(const CsrView& in, TileMat& out, int roles, const uint32_t* tile_base,
-                         const uint32_t* val_base, int drop_nonfinite, const uint8_t* needed,
-                         cudaStream_t st);
+// CSR -> tiles: convert_fast_kernel (block per panel) for panels spanning
+// <= 8192 tile columns with <= 1024 entries and <= 64 tiles, the panel walk
+// for the rest (listed by the fast kernel), both writing tiles at gapped
+// slots (tile row I at row_ptr[16 I]); then a scan of cs.ntiles -> out.trp
+// and launch_tiles_compact -> out's dense arrays.  Chunks stay where they
+// were written (tile row I's from 1 + row_ptr[16 I]).
+struct ConvertScratch {
+  uint32_t* rm2 = nullptr;             // gapped, cap * 8
+  uint4* rec[2] = {nullptr, nullptr};  // gapped, cap each (roles in use)
+  uint32_t* ntiles = nullptr;          // tile_rows + 1
+  uint32_t* walk_list = nullptr;       // tile_rows
+  uint32_t* walk_count = nullptr;      // 1, zeroed
+};
+void launch_convert(const CsrView& in, TileMat& out, int roles, const ConvertScratch& cs, unsigned* err_flag,
+                    int drop_nonfinite, const uint8_t* needed, cudaStream_t st);
+void launch_tiles_compact(const CsrView& in, const ConvertScratch& cs, TileMat& out, int roles, cudaStream_t st);
 void launch_mark_needed(const TileMat& A, uint8_t* needed, cudaStream_t st);
 void launch_row_stats(const TileMat& A, unsigned* max_row_tiles, cudaStream_t st);
 void launch_cbar(const int32_t* colA, int64_t nnzA, int64_t inner, const int64_t* rpB,
@@ -78,9 +88,17 @@ struct TileEmit {
 };
 // The pass does nothing when the staging total row_stage[rows] exceeds
 // stage_cap slots (the host checks and reruns with a bigger arena).
+// `need`: device u64 total of the staging bound (the pass returns at once when
+// it exceeds stage_cap); `stats`: when non-null, {filtered pairs, segments,
+// raw pairs} are accumulated there (the element-bound flow has no count pass)
 void launch_panel_numeric(const TileMat& A, const TileMat& B, int64_t rows, const uint32_t* row_stage,
-                          uint64_t stage_cap, uint2* stage, int64_t* rowcnt, unsigned long long* counted, int mode,
+                          uint64_t stage_cap, uint2* stage, int64_t* rowcnt, unsigned long long* counted,
+                          const unsigned long long* need, unsigned long long* stats, int mode,
                           uint32_t I0, uint32_t I1, cudaStream_t st, const TileEmit* emit = nullptr);
+// row_bound[r] = min(B.cols, sum over A's entries (r, k) of nnz(B row k));
+// *total += sum of row_bound
+void launch_elem_bound(const CsrView& A, const int64_t* rpB, int64_t bcols, uint32_t* row_bound,
+                       unsigned long long* total, cudaStream_t st);
 void launch_emit_compact(uint32_t tile_rows, const TileEmit& em, const uint32_t* trp, TileMat& T, cudaStream_t st);
 void launch_panel_copy(int64_t rows, const uint32_t* row_stage, const int64_t* row_ptr, const uint2* stage,
                        int32_t* col, float* val, unsigned* err_flag, uint32_t I0, uint32_t I1,

@@ -20,8 +20,12 @@
 // every staging row fills in final CSR order; no task list, segment table or
 // position pass ever reaches HBM.
 //
-//   panel_count_kernel    raw / filtered pairs, segments (stats) and a
-//                         staging bound per CSR row
+//   elem_bound_kernel     staging bound per CSR row from the CSR alone:
+//                         sum over the row's entries k of nnz(B row k)
+//                         (device output; the pass below counts the stats)
+//   panel_count_kernel    or: raw / filtered pairs, segments (stats) and a
+//                         tight staging bound per CSR row (host output, whose
+//                         pinned buffers the bound sizes; chained stages)
 //   CUB scan              -> staging row offsets                (tsg_api.cu)
 //   panel_numeric_kernel  the fused pass above; realised count per row
 //   CUB scan              -> row_ptr                            (tsg_api.cu)
@@ -104,6 +108,40 @@ __global__ void __launch_bounds__(256) panel_count_kernel(TileMat A, TileMat B, 
   if (lane < 16 && row < rows) row_bound[row] = bound;
 }
 
+// Element-level staging bound: row r of C has at most sum over A's entries
+// (r, k) of nnz(B row k) entries (and at most B.cols).  Thread per row (the
+// light path bounds a row at 32 tiles = 512 entries; the row's entries are
+// consecutive, so the warp's loads stay in L1).  Invalid columns contribute
+// nothing (the conversion flags them).
+__global__ void __launch_bounds__(256) elem_bound_kernel(CsrView A, const int64_t* __restrict__ rpB,
+                                                        int64_t bcols, uint32_t* __restrict__ row_bound,
+                                                        unsigned long long* __restrict__ total) {
+  __shared__ unsigned long long s_sum[8];
+  const int64_t r = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  uint64_t b = 0;
+  if (r < A.rows) {
+    const int64_t e0 = __ldg(A.row_ptr + r), e1 = __ldg(A.row_ptr + r + 1);
+    uint64_t sum = 0;
+#pragma unroll 4
+    for (int64_t p = e0; p < e1; ++p) {
+      const int32_t c = __ldg(A.col + p);
+      if (c >= 0 && c < A.cols) sum += uint64_t(__ldg(rpB + c + 1) - __ldg(rpB + c));
+    }
+    b = sum < uint64_t(bcols) ? sum : uint64_t(bcols);
+    row_bound[r] = uint32_t(b);
+  }
+  // the exact u64 total (guards the u32 staging offsets)
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) b += __shfl_xor_sync(kFull, b, o);
+  if ((threadIdx.x & 31) == 0) s_sum[threadIdx.x >> 5] = b;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long t = 0;
+    for (int i = 0; i < 8; ++i) t += s_sum[i];
+    if (t) atomicAdd(total, t);
+  }
+}
+
 constexpr int kSA = 17;    // padded row stride of the ordered A scratch tile
 constexpr int kSRow = 24;  // row stride of the ordered B scratch tile
 
@@ -175,6 +213,8 @@ __global__ void __launch_bounds__(256, kMinBlocks) panel_numeric_kernel(TileMat 
                                                               uint64_t stage_cap, uint2* __restrict__ stage,
                                                               int64_t* __restrict__ rowcnt,
                                                               unsigned long long* __restrict__ counted,
+                                                              const unsigned long long* __restrict__ need,
+                                                              unsigned long long* __restrict__ stats,
                                                               uint32_t I0, uint32_t I1, TileEmit em) {
   __shared__ __align__(16) uint4 s_meta[8][32];
   // TENSOR: [A tile of the row][lane] -> chunk index (ORDERED keeps the metas)
@@ -185,7 +225,7 @@ __global__ void __launch_bounds__(256, kMinBlocks) panel_numeric_kernel(TileMat 
   const int w = threadIdx.x >> 5;
   const uint32_t I = I0 + blockIdx.x * 8 + w;
   if (I >= I1) return;
-  if (!kEmit && __ldg(row_stage + rows) > stage_cap) return;  // arena too small: the host reruns the pass
+  if (!kEmit && (*need > stage_cap || (*need >> 32))) return;  // arena too small: the host reruns the pass
   const uint4* cA = A.chunk[kRoleA];
   const uint4* cB = B.chunk[kRoleB];
   const unsigned lt = lanemask_lt(), bit = 1u << lane;
@@ -193,6 +233,8 @@ __global__ void __launch_bounds__(256, kMinBlocks) panel_numeric_kernel(TileMat 
   Merge m;
   uint32_t a;
   m.start(A, B, I, lane, a);
+  const uint32_t raw_len = m.end - m.cur;
+  uint32_t np = 0, ns = 0;
   const uint32_t na = A.trp[I + 1] - A.trp[I];
   const uint2 am = uint32_t(lane) < na ? __ldg(A.meta[kRoleA] + a) : make_uint2(0, 0);
   if (!kOrdered) {
@@ -224,6 +266,8 @@ __global__ void __launch_bounds__(256, kMinBlocks) panel_numeric_kernel(TileMat 
                                               : make_uint4(uint32_t(lane), 0u, bm.x, bm.y);
       }
       const uint32_t n = __popc(pb);
+      np += n;
+      ++ns;
       __syncwarp();
       float acc[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
       if (!kOrdered) {
@@ -330,6 +374,14 @@ __global__ void __launch_bounds__(256, kMinBlocks) panel_numeric_kernel(TileMat 
   }
   nstruct = __reduce_add_sync(kFull, nstruct);
   if (lane == 0 && nstruct) atomicAdd(counted, (unsigned long long)nstruct);
+  if (stats) {  // the statistics panel_count_kernel would have produced
+    const uint32_t rw = __reduce_add_sync(kFull, raw_len);
+    if (lane == 0) {
+      atomicAdd(stats, (unsigned long long)np);
+      atomicAdd(stats + 1, (unsigned long long)ns);
+      atomicAdd(stats + 2, (unsigned long long)rw);
+    }
+  }
 }
 
 // Staging rows -> CSR: warp per panel, lanes over the panel's output
@@ -384,14 +436,22 @@ void launch_panel_count(const TileMat& A, const TileMat& B, int64_t rows, uint32
   panel_count_kernel<<<blocks, 256, 0, st>>>(A, B, rows, row_np, row_ns, row_raw, row_bound);
 }
 
+void launch_elem_bound(const CsrView& A, const int64_t* rpB, int64_t bcols, uint32_t* row_bound,
+                       unsigned long long* total, cudaStream_t st) {
+  const unsigned blocks = unsigned((A.rows + 255) / 256);
+  if (blocks == 0) return;
+  elem_bound_kernel<<<blocks, 256, 0, st>>>(A, rpB, bcols, row_bound, total);
+}
+
 void launch_panel_numeric(const TileMat& A, const TileMat& B, int64_t rows, const uint32_t* row_stage,
-                          uint64_t stage_cap, uint2* stage, int64_t* rowcnt, unsigned long long* counted, int mode,
+                          uint64_t stage_cap, uint2* stage, int64_t* rowcnt, unsigned long long* counted,
+                          const unsigned long long* need, unsigned long long* stats, int mode,
                           uint32_t I0, uint32_t I1, cudaStream_t st, const TileEmit* emit) {
   const unsigned blocks = (I1 - I0 + 7) / 8;
   if (I1 <= I0) return;
   const TileEmit em = emit ? *emit : TileEmit{};
   using K = void (*)(TileMat, TileMat, int64_t, const uint32_t*, uint64_t, uint2*, int64_t*, unsigned long long*,
-                     uint32_t, uint32_t, TileEmit);
+                     const unsigned long long*, unsigned long long*, uint32_t, uint32_t, TileEmit);
   K k;
   if (mode == 1)
     k = emit ? panel_numeric_kernel<true, 4, true> : panel_numeric_kernel<true, 4, false>;
@@ -400,7 +460,7 @@ void launch_panel_numeric(const TileMat& A, const TileMat& B, int64_t rows, cons
   else
     k = tuning_variant("TSG_PANEL_MINB", 4) == 5 ? panel_numeric_kernel<false, 5, false>
                                                   : panel_numeric_kernel<false, 4, false>;
-  k<<<blocks, 256, 0, st>>>(A, B, rows, row_stage, stage_cap, stage, rowcnt, counted, I0, I1, em);
+  k<<<blocks, 256, 0, st>>>(A, B, rows, row_stage, stage_cap, stage, rowcnt, counted, need, stats, I0, I1, em);
 }
 
 // Emitted tiles (gapped per tile row) -> dense CSR-of-tiles: warp per tile row.

@@ -50,11 +50,12 @@ __global__ void __launch_bounds__(256) enum_kernel(TileMat A, TileMat B, uint64_
     // kept entry per tile names exactly the B tiles that pass the
     // zero-product filter; others take B's tile row k with the occupancy
     // filter (pipeline.cpp:23-35).  Raw pairs are B tile row lengths either way.
-    uint32_t bs = 0, bl = 0, colocc = 0, base_off = 0, raw_len = 0;
+    uint32_t bs = 0, bl = 0, colocc = 0, base_off = 0, raw_len = 0, ts = 0;
     bool single = false;
     if (valid) {
       const uint2 ac = __ldg(A.tco + a);
-      const uint32_t ts = __ldg(B.trp + ac.x), te = __ldg(B.trp + ac.x + 1);
+      ts = __ldg(B.trp + ac.x);
+      const uint32_t te = __ldg(B.trp + ac.x + 1);
       raw_len = te - ts;
       colocc = ac.y & 0xffffu;
       single = B.etile != nullptr && __popc(colocc) == 1;
@@ -96,6 +97,7 @@ __global__ void __launch_bounds__(256) enum_kernel(TileMat A, TileMat B, uint64_
       const uint32_t ex_s = __shfl_sync(kFull, excl, s & 31);
       const uint32_t co_s = __shfl_sync(kFull, colocc, s & 31);
       const uint32_t off_s = __shfl_sync(kFull, base_off, s & 31);
+      const uint32_t ts_s = __shfl_sync(kFull, ts, s & 31);
       const bool single_s = (single_mask >> (s & 31)) & 1u;
       uint32_t b = bs_s + (q - ex_s);
       bool pass = false;
@@ -104,7 +106,7 @@ __global__ void __launch_bounds__(256) enum_kernel(TileMat A, TileMat B, uint64_
         if (single_s) {
           const uint32_t t = __ldg(B.etile + b);  // b is an entry index here
           pass = (t & kDupEntry) == 0u;            // kNoTile has the bit set too
-          b = t & ~kDupEntry;
+          b = ts_s + (t & ~kDupEntry);             // the tile's rank within B's tile row
           if (kFill && pass) J = __ldg(&B.tco[b].x);
         } else {
           const uint2 bt = __ldg(B.tco + b);

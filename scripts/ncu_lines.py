@@ -9,8 +9,10 @@ rep, kname, obj = sys.argv[1], sys.argv[2], sys.argv[3]
 # "ncu-regex::mangled-substring" when the two names differ (template kernels)
 kname, dname = (kname.split("::", 1) + [None])[:2] if "::" in kname else (kname, kname)
 top = int(sys.argv[4]) if len(sys.argv) > 4 else 25
+# match on the mangled name so one template instance is selected
 src = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass",
-                      "--kernel-name", f"regex:{kname}"], capture_output=True, text=True).stdout
+                      "--kernel-name-base", "mangled", "--kernel-name", f"regex:{dname}"],
+                     capture_output=True, text=True).stdout
 rows = list(csv.reader(src.splitlines()))
 h = rows[1]
 ia, iaddr, iw = h.index("Instructions Executed"), h.index("Address"), h.index("Warp Stall Sampling (All Samples)")
@@ -23,8 +25,11 @@ for r in rows[2:]:
         execs[a - base] = (int(float(r[ia])), int(float(r[iw] or 0)))
 d = tempfile.mkdtemp()
 subprocess.run(["cuobjdump", "-xelf", "all", os.path.abspath(obj)], cwd=d, capture_output=True)
-cub = glob.glob(os.path.join(d, "*.cubin"))[0]
-dis = subprocess.run(["nvdisasm", "-g", "-c", cub], capture_output=True, text=True).stdout
+dis = ""
+for cub in sorted(glob.glob(os.path.join(d, "*.cubin"))):  # the cubin holding the kernel
+    dis = subprocess.run(["nvdisasm", "-g", "-c", cub], capture_output=True, text=True).stdout
+    if dname in dis:
+        break
 lines, cur, infn = {}, None, False
 for ln in dis.splitlines():
     if ln.startswith("//---------------------"):
