@@ -34,10 +34,14 @@
 #include "tsg_kernels.cuh"
 
 namespace tsg {
-constexpr int kPipeChunks = 8;  // tile-row chunks of the pipelined host-output path
+constexpr int kPipeChunks = 16;  // max tile-row chunks of the pipelined host-output path (TSG_PIPE, default 8)
 int tuning_variant(const char* name, int dflt) {
   const char* v = std::getenv(name);
   return v ? std::atoi(v) : dflt;
+}
+int pipe_chunks() {
+  static const int n = std::max(1, std::min(kPipeChunks, tuning_variant("TSG_PIPE", 8)));
+  return n;
 }
 }  // namespace tsg
 
@@ -574,7 +578,7 @@ struct Call {
     uint2* stage = static_cast<uint2*>(speculative ? ctx->stage_buf : arena(stage_total * sizeof(uint2)));
     uint64_t cap_slots = speculative ? ctx->stage_cap / sizeof(uint2) : stage_total;
     if (timing) TSG_CUDA(cudaEventRecord(ctx->kev[0], s));
-    if (owner->host && TA.tile_rows >= 8 * kPipeChunks) {
+    if (owner->host && TA.tile_rows >= 8u * uint32_t(pipe_chunks())) {
       light_host_pipelined(row_stage, tot_d + 3, stage, cap_slots);
       return;
     }
@@ -717,9 +721,10 @@ struct Call {
       }
       sent = hi;
     };
-    for (int c = 0; c < kPipeChunks; ++c) {
-      const uint32_t I0 = uint32_t(uint64_t(TA.tile_rows) * c / kPipeChunks);
-      const uint32_t I1 = uint32_t(uint64_t(TA.tile_rows) * (c + 1) / kPipeChunks);
+    const int nch = pipe_chunks();
+    for (int c = 0; c < nch; ++c) {
+      const uint32_t I0 = uint32_t(uint64_t(TA.tile_rows) * c / nch);
+      const uint32_t I1 = uint32_t(uint64_t(TA.tile_rows) * (c + 1) / nch);
       const int64_t r0 = int64_t(I0) * 16, r1 = std::min<int64_t>(int64_t(I1) * 16, rows);
       launch_panel_numeric(TA, *TB, rows, row_stage, cap_slots, stage, rowcnt, counted_d, need, nullptr, opt.mode,
                            I0, I1, s);
@@ -733,7 +738,7 @@ struct Call {
       TSG_CUDA(cudaEventRecord(ctx->pipe_ev[c], s));
       if (c > 0) ship(c - 1);
     }
-    ship(kPipeChunks - 1);
+    ship(nch - 1);
     nnzC = int64_t(sent);
     if (uint64_t(nnzC) >= (uint64_t(1) << 32))
       throw Fail{TSG_ERR_OTHER, "output beyond 2^32 elements needs row-panel batching"};

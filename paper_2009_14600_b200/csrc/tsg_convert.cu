@@ -124,9 +124,10 @@ struct Gapped {
 struct FastSmem {
   uint32_t bits[kBitW];       // tile-column bitmap of the panel
   uint16_t pre[kBitW];        // tiles before each bitmap word
+  uint8_t row[32 * kFastU];   // row of each entry of the panel
   uint32_t rm[kFastT][8];     // per tile: word g = row g | row g+8 << 16
   uint32_t lm[kFastT][2];     // per tile and role: lane presence mask
-  uint32_t cb[kFastT][2];     // per tile and role: first chunk
+  uint2 cl[kFastT][2];        // per tile and role: {first chunk, lane mask}
 };
 
 // Tile-slot (r, c) of a 16x16 tile -> its lane and fp16 position in the
@@ -202,6 +203,8 @@ __global__ void __launch_bounds__(256, 4) convert_fast_kernel(CsrView in, uint32
   // lane r < 16: offset of row r's first entry in the panel (rows past the end: E)
   const uint32_t rs = lane < kTile && row < in.rows ? uint32_t(p - E0) : E;
   for (int i = lane; i < kBitW; i += 32) sm.bits[i] = 0;
+  if (has_row)
+    for (uint32_t q = rs; q < uint32_t(end - E0); ++q) sm.row[q] = uint8_t(lane);
   __syncwarp();
   unsigned err = 0;
   // entries: column, and packed {fp16 bits, row, kept}
@@ -214,15 +217,12 @@ __global__ void __launch_bounds__(256, 4) convert_fast_kernel(CsrView in, uint32
     const int32_t up = __shfl_up_sync(kFull, c[u], 1);
     const int32_t last = __shfl_sync(kFull, c[u > 0 ? u - 1 : 0], 31);  // lane 31 of the previous step
     const int32_t cprev = lane > 0 ? up : (u > 0 ? last : -1);
-    int r = 0;  // last row whose start is <= q
-#pragma unroll
-    for (int b = 8; b > 0; b >>= 1)
-      if (__shfl_sync(kFull, rs, r + b) <= q) r += b;
-    const uint32_t first = __shfl_sync(kFull, rs, r);
     if (q < E) {
+      const int r = sm.row[q];
+      const bool later = q > 0 && sm.row[q - 1] == r;  // not the first entry of its row
       bool keep;
       const uint16_t h = raw_to_half<kDtype>(v[u], drop_nonfinite, err, keep);
-      if (c[u] >= in.cols || c[u] < 0 || (q > first && c[u] <= cprev)) err |= kErrInvariant;
+      if (c[u] >= in.cols || c[u] < 0 || (later && c[u] <= cprev)) err |= kErrInvariant;
       const uint32_t j = (uint32_t(c[u]) >> 4) - jlo;
       keep = keep && !skip && c[u] >= 0 && j < uint32_t(kBitW) * 32u;
       if (keep) atomicOr(&sm.bits[j >> 5], 1u << (j & 31));
@@ -363,8 +363,8 @@ __global__ void __launch_bounds__(256, 4) convert_fast_kernel(CsrView in, uint32
     dst[1] = m1;
     if (roles & 1) out.rec[kRoleA][E0 + k] = make_uint4(sm.lm[k][0], cbA[h], occ, J);
     if (roles & 2) out.rec[kRoleB][E0 + k] = make_uint4(sm.lm[k][1], cbB[h], occ, J);
-    sm.cb[k][0] = cbA[h];
-    sm.cb[k][1] = cbB[h];
+    sm.cl[k][0] = make_uint2(cbA[h], sm.lm[k][0]);
+    sm.cl[k][1] = make_uint2(cbB[h], sm.lm[k][1]);
   }
   __syncwarp();  // chunk zeros before the value stores (same warp: ordered by the barrier)
   // every kept entry stores its fp16 value into its chunk slots
@@ -380,7 +380,8 @@ __global__ void __launch_bounds__(256, 4) convert_fast_kernel(CsrView in, uint32
       if (!(roles & (1 << role))) continue;
       int L, h16;
       slot_lane(role, r, cc, L, h16);
-      const uint32_t idx = sm.cb[k][role] + __popc(sm.lm[k][role] & ((1u << L) - 1u));
+      const uint2 cl = sm.cl[k][role];
+      const uint32_t idx = cl.x + __popc(cl.y & ((1u << L) - 1u));
       reinterpret_cast<uint16_t*>(out.chunk[role] + idx)[h16] = hv;
     }
   }
