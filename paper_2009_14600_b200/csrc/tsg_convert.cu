@@ -202,7 +202,10 @@ __global__ void __launch_bounds__(256, 4) convert_fast_kernel(CsrView in, uint32
   }
   // lane r < 16: offset of row r's first entry in the panel (rows past the end: E)
   const uint32_t rs = lane < kTile && row < in.rows ? uint32_t(p - E0) : E;
-  for (int i = lane; i < kBitW; i += 32) sm.bits[i] = 0;
+  // panels spanning <= 1024 tile columns (most banded ones) use one bitmap
+  // word per lane
+  const bool narrow = jlo == 0xffffffffu || jhi - jlo < 1024u;
+  for (int i = lane; i < (narrow ? 32 : kBitW); i += 32) sm.bits[i] = 0;
   if (has_row)
     for (uint32_t q = rs; q < uint32_t(end - E0); ++q) sm.row[q] = uint8_t(lane);
   __syncwarp();
@@ -231,21 +234,33 @@ __global__ void __launch_bounds__(256, 4) convert_fast_kernel(CsrView in, uint32
     }
   }
   __syncwarp();
-  // ranks: tiles before each bitmap word (lane owns words 8 lane .. 8 lane + 7)
-  uint32_t wc[8], lsum = 0;
+  // ranks: tiles before each bitmap word (lane owns word lane, or words
+  // 8 lane .. 8 lane + 7)
+  uint32_t ntiles;
+  if (narrow) {
+    const uint32_t wc = __popc(sm.bits[lane]);
+    uint32_t incl = wc;
 #pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    wc[i] = __popc(sm.bits[8 * lane + i]);
-    lsum += wc[i];
-  }
-  uint32_t incl = lsum;
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t v = __shfl_up_sync(kFull, incl, o);
+      if (lane >= o) incl += v;
+    }
+    ntiles = __shfl_sync(kFull, incl, 31);
+    sm.pre[lane] = uint16_t(incl - wc);
+  } else {
+    uint32_t wc[8], lsum = 0;
 #pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const uint32_t v = __shfl_up_sync(kFull, incl, o);
-    if (lane >= o) incl += v;
-  }
-  const uint32_t ntiles = __shfl_sync(kFull, incl, 31);
-  {
+    for (int i = 0; i < 8; ++i) {
+      wc[i] = __popc(sm.bits[8 * lane + i]);
+      lsum += wc[i];
+    }
+    uint32_t incl = lsum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t v = __shfl_up_sync(kFull, incl, o);
+      if (lane >= o) incl += v;
+    }
+    ntiles = __shfl_sync(kFull, incl, 31);
     uint32_t run = incl - lsum;
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
@@ -342,8 +357,7 @@ __global__ void __launch_bounds__(256, 4) convert_fast_kernel(CsrView in, uint32
     if (k >= ntiles) continue;
     // tile column: the k-th set bit of the bitmap
     int w = 0;
-#pragma unroll
-    for (int b = kBitW / 2; b > 0; b >>= 1)
+    for (int b = narrow ? 16 : kBitW / 2; b > 0; b >>= 1)
       if (sm.pre[w + b] <= k) w += b;
     uint32_t word = sm.bits[w];
     for (uint32_t n = k - sm.pre[w]; n > 0; --n) word &= word - 1u;

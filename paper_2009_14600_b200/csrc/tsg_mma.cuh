@@ -40,6 +40,15 @@ __device__ __forceinline__ uint32_t count_nz_h2(uint32_t x) {
   return ((x & 0x7fffu) != 0u) + ((x & 0x7fff0000u) != 0u);
 }
 
+// nonzero halves of four .f16x2 registers holding non-negative counts (the
+// 0/1-indicator accumulators: bit 15 of each half is clear): adding 0x7fff
+// to a half sets its bit 15 exactly when it is nonzero, without a carry
+// into the next half
+__device__ __forceinline__ uint32_t count_nz_counts(uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+  constexpr uint32_t M = 0x7fff7fffu, H = 0x80008000u;
+  return __popc((a + M) & H) + __popc((b + M) & H) + __popc((c + M) & H) + __popc((d + M) & H);
+}
+
 // chunk index of this lane for a tile with meta {lane mask, base}; 0 = zeros
 __device__ __forceinline__ uint32_t chunk_index(uint32_t lm, uint32_t base, int lane) {
   return ((lm >> lane) & 1u) ? base + __popc(lm & lanemask_lt()) : 0u;

@@ -138,8 +138,7 @@ __global__ void __launch_bounds__(256, kMinBlocks) numeric_tc_kernel(TaskList tl
       }
       __syncwarp();
     }
-    nstruct += count_nz_h2(sac[0][0]) + count_nz_h2(sac[0][1]) + count_nz_h2(sac[1][0]) +
-               count_nz_h2(sac[1][1]);
+    nstruct += count_nz_counts(sac[0][0], sac[0][1], sac[1][0], sac[1][1]);
     emit_tile(acc, so, s, lane, L, sg, s_v[w]);
   }
   finish(nstruct, sg, lane);

@@ -290,8 +290,7 @@ __global__ void __launch_bounds__(256, kMinBlocks) panel_numeric_kernel(TileMat 
           mma16816_h(sac[0], xa1, xb1.x, xb1.y);
           mma16816_h(sac[1], xa1, xb1.z, xb1.w);
         }
-        nstruct += count_nz_h2(sac[0][0]) + count_nz_h2(sac[0][1]) + count_nz_h2(sac[1][0]) +
-                   count_nz_h2(sac[1][1]);
+        nstruct += count_nz_counts(sac[0][0], sac[0][1], sac[1][0], sac[1][1]);
       } else {
         bool snz[2][4] = {{false, false, false, false}, {false, false, false, false}};
         for (uint32_t u = 0; u < n; ++u) {
