@@ -34,6 +34,7 @@
 #include "tsg_kernels.cuh"
 
 namespace tsg {
+constexpr int kGatherMax = 16;  // scalars per gathered readback
 constexpr int kPipeChunks = 16;  // max tile-row chunks of the pipelined host-output path (TSG_PIPE, default 8)
 int tuning_variant(const char* name, int dflt) {
   const char* v = std::getenv(name);
@@ -209,6 +210,29 @@ void readback_many(tsg_ctx* ctx, const T* const (&src)[N], T (&dst)[N]) {
                              cudaMemcpyDeviceToHost, ctx->stream));
   TSG_CUDA(cudaStreamSynchronize(ctx->stream));
   std::memcpy(dst, ctx->pinned, N * sizeof(T));
+}
+
+// Device scalars (u32 or u64) -> host in one copy and one synchronisation:
+// a one-block kernel gathers them into a device array first.
+struct ScalarGather {
+  const void* p[kGatherMax];
+  uint32_t wide = 0;  // bit i: p[i] is a u64
+  int n = 0;
+};
+__global__ void gather_scalars_kernel(ScalarGather g, unsigned long long* out) {
+  const int i = threadIdx.x;
+  if (i < g.n)
+    out[i] = ((g.wide >> i) & 1u) ? *static_cast<const unsigned long long*>(g.p[i])
+                                  : *static_cast<const uint32_t*>(g.p[i]);
+}
+void readback_gather(tsg_ctx* ctx, Scratch& sc, const ScalarGather& g, unsigned long long* dst) {
+  auto* d = sc.alloc<unsigned long long>(kGatherMax);
+  gather_scalars_kernel<<<1, 32, 0, ctx->stream>>>(g, d);
+  check_launch(ctx);
+  unsigned long long* h = reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(ctx->pinned) + 64);
+  TSG_CUDA(cudaMemcpyAsync(h, d, g.n * sizeof(unsigned long long), cudaMemcpyDeviceToHost, ctx->stream));
+  TSG_CUDA(cudaStreamSynchronize(ctx->stream));
+  std::memcpy(dst, h, g.n * sizeof(unsigned long long));
 }
 
 // CSR -> 16x16 tiles (one conversion pass at gapped slots, scan of the tile
@@ -393,7 +417,11 @@ struct Call {
         sc(c), launches0(c->launches) {}
 
   // ---- (1) validation, staging of host inputs, CSR -> 16x16 tiles ----------------
-  void convert_operands() {
+  // readback of the conversion results deferred to the speculative light pass
+  const unsigned* ntA_dev = nullptr;
+  const unsigned* ntB_dev = nullptr;
+
+  void convert_operands(bool defer = false) {
     if (!pre_a) check_csr(Ain, "A");
     check_csr(Bin, "B");
     if (!C) throw Fail{TSG_ERR_OTHER, "C is NULL"};
@@ -430,13 +458,17 @@ struct Call {
     TB = same ? &TA : &TB_own;
     launch_row_stats(TA, dscal + 1, s);
     check_launch(ctx);
-    const unsigned* src[4] = {dscal, dscal + 1, ntA_d, ntB_d};
-    unsigned v[4];
-    readback_many(ctx, src, v);
-    raise_flags(v[0]);
-    light = v[1] <= 32;
-    tA = v[2];
-    tB = v[3];
+    ntA_dev = ntA_d;
+    ntB_dev = ntB_d;
+    if (!defer) {
+      const unsigned* src[4] = {dscal, dscal + 1, ntA_d, ntB_d};
+      unsigned v[4];
+      readback_many(ctx, src, v);
+      raise_flags(v[0]);
+      light = v[1] <= 32;
+      tA = v[2];
+      tB = v[3];
+    }
     record(ctx, timing, 1);
 
     rows = Ain->rows;
@@ -501,6 +533,77 @@ struct Call {
   }
 
   // ---- light rows: one fused pass per tile row (tsg_panel.cu) --------------------
+  // Device output, CSR operands, staging arena in place: the whole light
+  // pass is enqueued before the conversion results are read -- the numeric
+  // kernel itself returns when the rows are not light, the input is invalid
+  // or the arena is too small -- and ONE synchronisation then reads the
+  // conversion results, the statistics and nnz(C).  Returns false when the
+  // rows are not light (the caller takes the general path).
+  bool light_speculative() {
+    auto* row_bound = sc.alloc<uint32_t>(rows + 1);
+    auto* row_stage = sc.alloc<uint32_t>(rows + 1);
+    TSG_CUDA(cudaMemsetAsync(row_bound + rows, 0, 4, s));
+    auto* tot_d = sc.alloc<unsigned long long>(4);
+    TSG_CUDA(cudaMemsetAsync(tot_d, 0, 4 * sizeof(unsigned long long), s));
+    launch_elem_bound(dA, dB.row_ptr, Bin->cols, row_bound, tot_d + 3, s);
+    check_launch(ctx);
+    exclusive_sum(ctx, sc, row_bound, row_stage, uint64_t(rows) + 1);
+    record(ctx, timing, 2);
+    record(ctx, timing, 3);
+    record(ctx, timing, 4);
+    uint2* stage = static_cast<uint2*>(ctx->stage_buf);
+    const uint64_t cap_slots = ctx->stage_cap / sizeof(uint2);
+    if (timing) TSG_CUDA(cudaEventRecord(ctx->kev[0], s));
+    launch_panel_numeric(TA, *TB, rows, row_stage, cap_slots, stage, rowcnt, counted_d, tot_d + 3, tot_d, opt.mode,
+                         0, TA.tile_rows, s, nullptr, dscal);
+    check_launch(ctx);
+    if (timing) TSG_CUDA(cudaEventRecord(ctx->kev[1], s));
+    record(ctx, timing, 5);
+    exclusive_sum(ctx, sc, rowcnt, d_rp, uint64_t(rows) + 1);
+    ScalarGather g;
+    const void* ps[10] = {dscal, dscal + 1, ntA_dev, ntB_dev, counted_d, d_rp + rows, tot_d, tot_d + 1, tot_d + 2,
+                          tot_d + 3};
+    for (int i = 0; i < 10; ++i) g.p[i] = ps[i];
+    g.wide = 0x3f0u;  // counted, nnz and the four totals are u64
+    g.n = 10;
+    unsigned long long v[10];
+    readback_gather(ctx, sc, g, v);
+    raise_flags(unsigned(v[0]));
+    light = v[1] <= 32;
+    tA = v[2];
+    tB = v[3];
+    if (!light) return false;
+    counted = v[4];
+    nnzC = int64_t(v[5]);
+    P = v[6];
+    S = v[7];
+    raw = v[8];
+    stage_total = v[9];
+    if (stage_total > cap_slots || (stage_total >> 32)) {  // the rare arena overflow: redo the pass
+      check_stage_total();
+      stage = static_cast<uint2*>(arena(stage_total * sizeof(uint2)));
+      TSG_CUDA(cudaMemsetAsync(counted_d, 0, sizeof(unsigned long long), s));
+      TSG_CUDA(cudaMemsetAsync(tot_d, 0, 3 * sizeof(unsigned long long), s));
+      launch_panel_numeric(TA, *TB, rows, row_stage, stage_total, stage, rowcnt, counted_d, tot_d + 3, tot_d,
+                           opt.mode, 0, TA.tile_rows, s);
+      check_launch(ctx);
+      unsigned long long t[4];
+      scan_rows(tot_d, t);
+      P = t[0];
+      S = t[1];
+      raw = t[2];
+    } else if (uint64_t(nnzC) >= (uint64_t(1) << 32)) {
+      throw Fail{TSG_ERR_OTHER, "output beyond 2^32 elements needs row-panel batching"};
+    }
+    alloc_out();
+    if (timing) TSG_CUDA(cudaEventRecord(ctx->kev[2], s));
+    launch_panel_copy(rows, row_stage, d_rp, stage, d_col, d_val, err_flag, 0, TA.tile_rows, s);
+    check_launch(ctx);
+    if (timing) TSG_CUDA(cudaEventRecord(ctx->kev[3], s));
+    record(ctx, timing, 6);
+    return true;
+  }
+
   void light_path() {
     auto* row_np = sc.alloc<uint32_t>(nr);
     auto* row_ns = sc.alloc<uint32_t>(nr);
@@ -983,11 +1086,17 @@ struct Call {
 void spgemm_impl(tsg_ctx* ctx, const tsg_csr* Ain, const tsg_csr* Bin, tsg_csr_out* C,
                  const tsg_options& opt, tsg_run_stats* st, tsg_tiles_out* tiles) {
   Call call(ctx, Ain, Bin, C, opt, st);
-  call.convert_operands();
-  if (call.light)
+  // one synchronisation for conversion + light pass when it can be speculated
+  const bool spec = C && C->mem != TSG_MEM_HOST && ctx->stage_cap >= 16 &&
+                    tuning_variant("TSG_LIGHT_BOUND", 1) == 1 && tuning_variant("TSG_SPECULATE", 1) == 1;
+  call.convert_operands(spec);
+  if (spec) {
+    if (!call.light_speculative()) call.general_path();
+  } else if (call.light) {
     call.light_path();
-  else
+  } else {
     call.general_path();
+  }
   call.finish(tiles);
 }
 
@@ -1064,7 +1173,7 @@ int tsg_create(tsg_ctx** out, int device, void* stream) {
     uint64_t thr = ~uint64_t(0);
     e = cudaMemPoolSetAttribute(ctx->pool, cudaMemPoolAttrReleaseThreshold, &thr);
   }
-  if (e == cudaSuccess) e = cudaMallocHost(&ctx->pinned, 64);
+  if (e == cudaSuccess) e = cudaMallocHost(&ctx->pinned, 64 + 8 * kGatherMax);
   if (e == cudaSuccess) e = cudaMallocHost(&ctx->pinned_pipe, 8 * (tsg::kPipeChunks + 1));
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->d2h, cudaStreamNonBlocking);
   for (int i = 0; i <= tsg::kPipeChunks && e == cudaSuccess; ++i)

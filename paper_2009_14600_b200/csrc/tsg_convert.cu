@@ -227,7 +227,9 @@ __global__ void __launch_bounds__(256, 4) convert_fast_kernel(CsrView in, uint32
       const uint16_t h = raw_to_half<kDtype>(v[u], drop_nonfinite, err, keep);
       if (c[u] >= in.cols || c[u] < 0 || (later && c[u] <= cprev)) err |= kErrInvariant;
       const uint32_t j = (uint32_t(c[u]) >> 4) - jlo;
-      keep = keep && !skip && c[u] >= 0 && j < uint32_t(kBitW) * 32u;
+      // out-of-range columns (flagged) never form tiles: the tile structure
+      // stays in range even for invalid input
+      keep = keep && !skip && c[u] >= 0 && c[u] < in.cols && j < uint32_t(kBitW) * 32u;
       if (keep) atomicOr(&sm.bits[j >> 5], 1u << (j & 31));
       else if (out.etile) out.etile[E0 + q] = kNoTile;
       pk[u] = uint32_t(h) | (uint32_t(r) << 16) | (keep ? 1u << 20 : 0u);
@@ -476,6 +478,7 @@ __global__ void __launch_bounds__(256) convert_walk_kernel(CsrView in, Gapped ou
         prev_col = c;
         bool keep;
         const unsigned short h = load_half<kDtype>(in.val, p, drop_nonfinite, err, keep);
+        keep = keep && c >= 0 && c < in.cols;  // out-of-range columns (flagged) never form tiles
         if (keep) {
           rm |= 1u << (c & 15);
           st[lane * 16 + (c & 15)] = h;

@@ -215,7 +215,8 @@ __global__ void __launch_bounds__(256, kMinBlocks) panel_numeric_kernel(TileMat 
                                                               unsigned long long* __restrict__ counted,
                                                               const unsigned long long* __restrict__ need,
                                                               unsigned long long* __restrict__ stats,
-                                                              uint32_t I0, uint32_t I1, TileEmit em) {
+                                                              uint32_t I0, uint32_t I1, TileEmit em,
+                                                              const unsigned* __restrict__ gate) {
   __shared__ __align__(16) uint4 s_meta[8][32];
   // TENSOR: [A tile of the row][lane] -> chunk index (ORDERED keeps the metas)
   __shared__ uint32_t s_aidx[kOrdered ? 1 : 8][32][32];
@@ -225,7 +226,10 @@ __global__ void __launch_bounds__(256, kMinBlocks) panel_numeric_kernel(TileMat 
   const int w = threadIdx.x >> 5;
   const uint32_t I = I0 + blockIdx.x * 8 + w;
   if (I >= I1) return;
-  if (!kEmit && (*need > stage_cap || (*need >> 32))) return;  // arena too small: the host reruns the pass
+  if (!kEmit && (*need > stage_cap || (*need >> 32))) return;
+  // speculative launch: {error flags, max A tiles per tile row} of the
+  // conversion; invalid input or rows that are not light -> nothing to do
+  if (gate && ((gate[0] & kErrInvariant) || gate[1] > 32u)) return;  // arena too small: the host reruns the pass
   const uint4* cA = A.chunk[kRoleA];
   const uint4* cB = B.chunk[kRoleB];
   const unsigned lt = lanemask_lt(), bit = 1u << lane;
@@ -445,12 +449,12 @@ void launch_elem_bound(const CsrView& A, const int64_t* rpB, int64_t bcols, uint
 void launch_panel_numeric(const TileMat& A, const TileMat& B, int64_t rows, const uint32_t* row_stage,
                           uint64_t stage_cap, uint2* stage, int64_t* rowcnt, unsigned long long* counted,
                           const unsigned long long* need, unsigned long long* stats, int mode,
-                          uint32_t I0, uint32_t I1, cudaStream_t st, const TileEmit* emit) {
+                          uint32_t I0, uint32_t I1, cudaStream_t st, const TileEmit* emit, const unsigned* gate) {
   const unsigned blocks = (I1 - I0 + 7) / 8;
   if (I1 <= I0) return;
   const TileEmit em = emit ? *emit : TileEmit{};
   using K = void (*)(TileMat, TileMat, int64_t, const uint32_t*, uint64_t, uint2*, int64_t*, unsigned long long*,
-                     const unsigned long long*, unsigned long long*, uint32_t, uint32_t, TileEmit);
+                     const unsigned long long*, unsigned long long*, uint32_t, uint32_t, TileEmit, const unsigned*);
   K k;
   if (mode == 1)
     k = emit ? panel_numeric_kernel<true, 4, true> : panel_numeric_kernel<true, 4, false>;
@@ -459,7 +463,7 @@ void launch_panel_numeric(const TileMat& A, const TileMat& B, int64_t rows, cons
   else
     k = tuning_variant("TSG_PANEL_MINB", 4) == 5 ? panel_numeric_kernel<false, 5, false>
                                                   : panel_numeric_kernel<false, 4, false>;
-  k<<<blocks, 256, 0, st>>>(A, B, rows, row_stage, stage_cap, stage, rowcnt, counted, need, stats, I0, I1, em);
+  k<<<blocks, 256, 0, st>>>(A, B, rows, row_stage, stage_cap, stage, rowcnt, counted, need, stats, I0, I1, em, gate);
 }
 
 // Emitted tiles (gapped per tile row) -> dense CSR-of-tiles: warp per tile row.

@@ -268,3 +268,24 @@ def test_chain_intermediate_overflow(ctx):
     got = ctx.spgemm_chain([X, X, I]).C
     assert csr_bits_equal(got, ref.chain([X, X, I]))
     assert np.all(np.asarray(got.val) == 65024.0)
+
+
+def test_device_output_speculation(ctx):
+    """Device output with a warm staging arena enqueues the light pass before
+    reading the conversion results back (one synchronisation): invalid input
+    must still raise, general-path inputs must fall through to the general
+    path, and results must equal the host-output path's."""
+    A = W.fem27(16)
+    ctx.spgemm(A, A, out="device")  # warms the arena
+    for M in (A, _signed_wide(300, 6000, 9000, 21, "signed")):
+        B = M if M.rows == M.cols else _signed_wide(6000, 400, 9600, 22, "signed")
+        dev = ctx.spgemm(M, B, out="device").C.to_numpy()
+        host = ctx.spgemm(M, B).C
+        assert csr_bits_equal(dev, host), first_diff(dev, host)
+    bad = T.Csr(8, 8, np.array([0, 2, 2, 2, 2, 2, 2, 2, 2]), np.array([3, 1], np.int32), np.array([1.0, 2.0]))
+    with pytest.raises(T.InvariantError):
+        ctx.spgemm(bad, bad, out="device")
+    oob = T.Csr(8, 8, np.array([0, 1, 1, 1, 1, 1, 1, 1, 1]), np.array([9], np.int32), np.array([1.0]))
+    with pytest.raises(T.InvariantError):
+        ctx.spgemm(oob, oob, out="device")
+    assert csr_bits_equal(ctx.spgemm(A, A, out="device").C.to_numpy(), ctx.spgemm(A, A).C)
