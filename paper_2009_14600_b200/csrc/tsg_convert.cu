@@ -182,18 +182,28 @@ __global__ void __launch_bounds__(256, 4) convert_fast_kernel(CsrView in, uint32
   Raw v[kFastU];
 #pragma unroll
   for (int u = 0; u < kFastU; ++u) {
+    c[u] = -1;
+    v[u] = Raw(0);
+  }
+#pragma unroll
+  for (int u = 0; u < kFastU; ++u) {
+    if (32u * u >= E) break;
     const uint32_t q = 32 * u + lane;
-    c[u] = q < E ? __ldg(in.col + E0 + q) : -1;
-    v[u] = q < E ? __ldg(static_cast<const Raw*>(in.val) + E0 + q) : Raw(0);
+    if (q < E) {
+      c[u] = __ldg(in.col + E0 + q);
+      v[u] = __ldg(static_cast<const Raw*>(in.val) + E0 + q);
+    }
   }
   const bool skip = needed && !needed[I];
   uint32_t jlo = 0xffffffffu, jhi = 0;
 #pragma unroll
-  for (int u = 0; u < kFastU; ++u)
+  for (int u = 0; u < kFastU; ++u) {
+    if (32u * u >= E) break;
     if (c[u] >= 0) {
       jlo = min(jlo, uint32_t(c[u]) >> 4);
       jhi = max(jhi, uint32_t(c[u]) >> 4);
     }
+  }
   jlo = __reduce_min_sync(kFull, jlo);
   jhi = __reduce_max_sync(kFull, jhi);
   if (jlo != 0xffffffffu && jhi - jlo >= uint32_t(kBitW) * 32u) {  // too wide for the bitmap
