@@ -121,15 +121,6 @@ struct Gapped {
   uint32_t* ntiles = nullptr;  // per tile row
 };
 
-struct FastSmem {
-  uint32_t bits[kBitW];       // tile-column bitmap of the panel
-  uint16_t pre[kBitW];        // tiles before each bitmap word
-  uint8_t row[32 * kFastU];   // row of each entry of the panel
-  uint32_t rm[kFastT][8];     // per tile: word g = row g | row g+8 << 16
-  uint32_t lm[kFastT][2];     // per tile and role: lane presence mask
-  uint2 cl[kFastT][2];        // per tile and role: {first chunk, lane mask}
-};
-
 // Tile-slot (r, c) of a 16x16 tile -> its lane and fp16 position in the
 // lane's 16-byte chunk.  A order: lane (g, t) holds rows g, g+8 x cols 2t,
 // 2t+1, 2t+8, 2t+9 in regs i = (r>>3) + 2(c>>3).  B order (the transposed
@@ -144,6 +135,142 @@ __device__ __forceinline__ void slot_lane(int role, int r, int c, int& L, int& h
     h16 = 2 * (2 * (c >> 3) + (r >> 3)) + (r & 1);
   }
 }
+
+struct __align__(16) FastSmem {  // 16-byte multiple: the tiles use 16-byte accesses
+  uint8_t row[32 * kFastU];  // row of each entry of the panel
+  union {
+    struct {                    // bitmap path
+      uint32_t bits[kBitW];     // tile-column bitmap of the panel
+      uint16_t pre[kBitW];      // tiles before each bitmap word
+      uint32_t rm[kFastT][8];   // per tile: word g = row g | row g+8 << 16
+      uint32_t lm[kFastT][2];   // per tile and role: lane presence mask
+      uint2 cl[kFastT][2];      // per tile and role: {first chunk, lane mask}
+    };
+    struct {                              // sort path
+      unsigned long long items[32 * kFastU];  // (tile col, row, col, entry, fp16) sorted
+      uint16_t ts[32 * kFastU + 1];       // first item of each tile
+    };
+  };
+};
+
+// Sort path for panels the bitmap cannot rank (wider than 8192 tile columns,
+// or more than kFastT tiles: R-MAT, the rectangular products): the panel's
+// kept entries, as 64-bit items (tile col << 40 | row << 36 | col & 15 << 32
+// | entry << 16 | fp16), are bitonic-sorted in shared memory; runs of equal
+// tile column are the tiles, in (row, col) order inside; lanes then emit one
+// tile each.
+__device__ __forceinline__ uint32_t sparse_panel(FastSmem& sm, const Gapped& out, int roles, int64_t E0, uint32_t E,
+                                                 uint32_t nk, int lane) {
+  unsigned long long* it = sm.items;
+  uint32_t P2 = 32;
+  while (P2 < E) P2 <<= 1;
+  // bitonic sort, ascending (padding items are ~0)
+  for (uint32_t k = 2; k <= P2; k <<= 1)
+    for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+      for (uint32_t pidx = lane; pidx < P2 / 2; pidx += 32) {
+        const uint32_t i = ((pidx & ~(j - 1u)) << 1) | (pidx & (j - 1u)), l = i | j;
+        const unsigned long long x = it[i], y = it[l];
+        const bool up = (i & k) == 0u;
+        if ((x > y) == up) {
+          it[i] = y;
+          it[l] = x;
+        }
+      }
+      __syncwarp();
+    }
+  // tile starts -> tile ranks; etile (first kept entry of each (row, tile))
+  uint32_t ntiles = 0;
+  const unsigned lt = lanemask_lt();
+  for (uint32_t i0 = 0; i0 < nk; i0 += 32) {
+    const uint32_t i = i0 + lane;
+    const unsigned long long x = i < nk ? it[i] : ~0ull;
+    const unsigned long long xp = i > 0 && i < nk ? it[i - 1] : ~0ull;
+    const bool start = i < nk && (i == 0 || (x >> 40) != (xp >> 40));
+    const unsigned sb = __ballot_sync(kFull, start);
+    const uint32_t t = ntiles + __popc(sb & lt) + (start ? 1u : 0u) - 1u;  // tile of item i
+    if (start) sm.ts[t] = uint16_t(i);
+    if (i < nk && out.etile) {
+      const bool first_row = start || ((x >> 36) & 15u) != ((xp >> 36) & 15u);
+      out.etile[E0 + ((x >> 16) & 0xffffu)] = t | (first_row ? 0u : kDupEntry);
+    }
+    ntiles += __popc(sb);
+  }
+  if (lane == 0) sm.ts[ntiles] = uint16_t(nk);
+  __syncwarp();
+  // lanes emit tiles t = lane, lane + 32, ...; chunk bases by a warp scan
+  uint32_t runA = 1u + uint32_t(E0), runB = 1u + uint32_t(E0);
+  for (uint32_t t0 = 0; t0 < ntiles; t0 += 32) {
+    const uint32_t t = t0 + lane;
+    uint32_t rm[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    uint32_t lmA = 0, lmB = 0, a = 0, b = 0, J = 0;
+    if (t < ntiles) {
+      a = sm.ts[t];
+      b = sm.ts[t + 1];
+      J = uint32_t(it[a] >> 40);
+      for (uint32_t i = a; i < b; ++i) {
+        const unsigned long long x = it[i];
+        const int r = int(x >> 36) & 15, cc = int(x >> 32) & 15;
+#pragma unroll
+        for (int g = 0; g < 8; ++g)
+          if (g == (r & 7)) rm[g] |= 1u << (cc + 16 * (r >> 3));
+        int L, h16;
+        slot_lane(kRoleA, r, cc, L, h16);
+        lmA |= 1u << L;
+        slot_lane(kRoleB, r, cc, L, h16);
+        lmB |= 1u << L;
+      }
+    }
+    const uint32_t nA = (roles & 1) ? __popc(lmA) : 0u, nB = (roles & 2) ? __popc(lmB) : 0u;
+    uint32_t iA = nA, iB = nB;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t va = __shfl_up_sync(kFull, iA, o), vb = __shfl_up_sync(kFull, iB, o);
+      if (lane >= o) {
+        iA += va;
+        iB += vb;
+      }
+    }
+    const uint32_t cbA = runA + iA - nA, cbB = runB + iB - nB;
+    runA += __shfl_sync(kFull, iA, 31);
+    runB += __shfl_sync(kFull, iB, 31);
+    if (t < ntiles) {
+      uint32_t colocc = 0, rowocc = 0;
+#pragma unroll
+      for (int g = 0; g < 8; ++g) {
+        colocc |= rm[g] | (rm[g] >> 16);
+        rowocc |= ((rm[g] & 0xffffu) != 0u ? 1u << g : 0u) | ((rm[g] >> 16) != 0u ? 1u << (g + 8) : 0u);
+      }
+      const uint32_t occ = (colocc & 0xffffu) | (rowocc << 16);
+      uint4* dst = reinterpret_cast<uint4*>(out.rm2 + size_t(E0 + t) * 8);
+      dst[0] = make_uint4(rm[0], rm[1], rm[2], rm[3]);
+      dst[1] = make_uint4(rm[4], rm[5], rm[6], rm[7]);
+#pragma unroll
+      for (int role = 0; role < 2; ++role) {
+        if (!(roles & (1 << role))) continue;
+        const uint32_t lm = role == kRoleA ? lmA : lmB, cb = role == kRoleA ? cbA : cbB;
+        out.rec[role][E0 + t] = make_uint4(lm, cb, occ, J);
+        uint32_t n = 0;
+        for (uint32_t m = lm; m; m &= m - 1u, ++n) {  // present lanes, ascending
+          const int Lw = __ffs(m) - 1;
+          uint32_t w[4] = {0, 0, 0, 0};
+          for (uint32_t i = a; i < b; ++i) {
+            const unsigned long long x = it[i];
+            int L, h16;
+            slot_lane(role, int(x >> 36) & 15, int(x >> 32) & 15, L, h16);
+            if (L != Lw) continue;
+            const uint32_t hv = uint32_t(x & 0xffffu) << (16 * (h16 & 1));
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              if (q == (h16 >> 1)) w[q] |= hv;
+          }
+          out.chunk[role][cb + n] = make_uint4(w[0], w[1], w[2], w[3]);
+        }
+      }
+    }
+  }
+  return ntiles;
+}
+
 
 // Fast path, warp per tile row (panel): the panel's entries are loaded once
 // (coalesced, up to kFastU per lane, kept in registers); their tile columns
@@ -206,7 +333,9 @@ __global__ void __launch_bounds__(256, 4) convert_fast_kernel(CsrView in, uint32
   }
   jlo = __reduce_min_sync(kFull, jlo);
   jhi = __reduce_max_sync(kFull, jhi);
-  if (jlo != 0xffffffffu && jhi - jlo >= uint32_t(kBitW) * 32u) {  // too wide for the bitmap
+  // too wide for the bitmap: the sort path (tile columns must fit 24 bits)
+  const bool wide = jlo != 0xffffffffu && jhi - jlo >= uint32_t(kBitW) * 32u;
+  if (wide && jhi >= (1u << 24)) {
     if (lane == 0) walk_list[atomicAdd(walk_count, 1u)] = I;
     return;
   }
@@ -215,7 +344,8 @@ __global__ void __launch_bounds__(256, 4) convert_fast_kernel(CsrView in, uint32
   // panels spanning <= 1024 tile columns (most banded ones) use one bitmap
   // word per lane
   const bool narrow = jlo == 0xffffffffu || jhi - jlo < 1024u;
-  for (int i = lane; i < (narrow ? 32 : kBitW); i += 32) sm.bits[i] = 0;
+  if (!wide)
+    for (int i = lane; i < (narrow ? 32 : kBitW); i += 32) sm.bits[i] = 0;
   if (has_row)
     for (uint32_t q = rs; q < uint32_t(end - E0); ++q) sm.row[q] = uint8_t(lane);
   __syncwarp();
@@ -239,17 +369,47 @@ __global__ void __launch_bounds__(256, 4) convert_fast_kernel(CsrView in, uint32
       const uint32_t j = (uint32_t(c[u]) >> 4) - jlo;
       // out-of-range columns (flagged) never form tiles: the tile structure
       // stays in range even for invalid input
-      keep = keep && !skip && c[u] >= 0 && c[u] < in.cols && j < uint32_t(kBitW) * 32u;
-      if (keep) atomicOr(&sm.bits[j >> 5], 1u << (j & 31));
-      else if (out.etile) out.etile[E0 + q] = kNoTile;
+      keep = keep && !skip && c[u] >= 0 && c[u] < in.cols && (wide || j < uint32_t(kBitW) * 32u);
+      if (keep && !wide) atomicOr(&sm.bits[j >> 5], 1u << (j & 31));
+      if (!keep && out.etile) out.etile[E0 + q] = kNoTile;
       pk[u] = uint32_t(h) | (uint32_t(r) << 16) | (keep ? 1u << 20 : 0u);
     }
   }
   __syncwarp();
+  // the sort path: the panel's kept entries as items
+  auto sort_path = [&]() {
+    uint32_t P2 = 32;
+    while (P2 < E) P2 <<= 1;
+    uint32_t nk = 0;
+#pragma unroll
+    for (int u = 0; u < kFastU; ++u) {
+      if (32u * u >= P2) break;
+      const uint32_t q = 32 * u + lane;
+      const bool kp = q < E && ((pk[u] >> 20) & 1u);
+      nk += __popc(__ballot_sync(kFull, kp));
+      sm.items[q] = kp ? (static_cast<unsigned long long>(uint32_t(c[u]) >> 4) << 40) |
+                             (static_cast<unsigned long long>((pk[u] >> 16) & 15u) << 36) |
+                             (static_cast<unsigned long long>(uint32_t(c[u]) & 15u) << 32) |
+                             (static_cast<unsigned long long>(q) << 16) | (pk[u] & 0xffffu)
+                       : ~0ull;
+    }
+    __syncwarp();
+    const uint32_t nt = sparse_panel(sm, out, roles, E0, E, nk, lane);
+    const unsigned e = __reduce_or_sync(kFull, err);
+    if (lane == 0) {
+      out.ntiles[I] = nt;
+      if (e) atomicOr(err_flag, e);
+    }
+  };
+  if (wide && !skip) {
+    sort_path();
+    return;
+  }
   // ranks: tiles before each bitmap word (lane owns word lane, or words
   // 8 lane .. 8 lane + 7)
-  uint32_t ntiles;
-  if (narrow) {
+  uint32_t ntiles = 0;
+  if (wide) {
+  } else if (narrow) {
     const uint32_t wc = __popc(sm.bits[lane]);
     uint32_t incl = wc;
 #pragma unroll
@@ -281,12 +441,16 @@ __global__ void __launch_bounds__(256, 4) convert_fast_kernel(CsrView in, uint32
     }
   }
   const unsigned e_all = __reduce_or_sync(kFull, err);
-  if (skip || ntiles > uint32_t(kFastT)) {
+  if (skip) {
     if (lane == 0) {
-      if (skip) out.ntiles[I] = 0;
-      else walk_list[atomicAdd(walk_count, 1u)] = I;  // too many tiles: the walk (re-validates)
-      if (skip && e_all) atomicOr(err_flag, e_all);
+      out.ntiles[I] = 0;
+      if (e_all) atomicOr(err_flag, e_all);
     }
+    return;
+  }
+  if (ntiles > uint32_t(kFastT)) {  // too many tiles to stage: the sort path
+    __syncwarp();
+    sort_path();
     return;
   }
   for (uint32_t i = lane; i < ntiles * 8u; i += 32) sm.rm[i >> 3][i & 7] = 0;
