@@ -240,7 +240,8 @@ void readback_gather(tsg_ctx* ctx, Scratch& sc, const ScalarGather& g, unsigned 
 // array is sized by the input nnz (an upper bound on tiles and chunks).
 // Returns the device address of the tile count (trp[tile_rows]).
 const uint32_t* convert(tsg_ctx* ctx, Scratch& sc, const CsrView& in, TileMat& T, int roles,
-                        unsigned* err_flag, int drop_nonfinite, const uint8_t* needed = nullptr) {
+                        unsigned* err_flag, int drop_nonfinite, const uint8_t* needed = nullptr,
+                        uint8_t* mark = nullptr) {
   T.rows = in.rows;
   T.cols = in.cols;
   T.tile_rows = uint32_t((in.rows + 15) / 16);
@@ -253,6 +254,7 @@ const uint32_t* convert(tsg_ctx* ctx, Scratch& sc, const CsrView& in, TileMat& T
   cs.ntiles = sc.alloc<uint32_t>(nr);
   cs.walk_list = sc.alloc<uint32_t>(nr);
   cs.walk_count = sc.alloc<uint32_t>(1);
+  cs.mark = mark;
   TSG_CUDA(cudaMemsetAsync(cs.walk_count, 0, sizeof(uint32_t), ctx->stream));
   TSG_CUDA(cudaMemsetAsync(cs.ntiles + nr - 1, 0, sizeof(uint32_t), ctx->stream));
   if (roles & 2) {
@@ -437,24 +439,28 @@ struct Call {
                                      Ain->val == Bin->val && Ain->rows == Bin->rows && Ain->cols == Bin->cols &&
                                      Ain->mem == Bin->mem && Ain->dtype == Bin->dtype && Ain->nnz == Bin->nnz));
     const uint32_t* ntA_d;
+    // the B tile rows A's tiles refer to (A's tile columns), marked by A's
+    // conversion: only those are tiled (a row panel of A -- multi-GPU, or any
+    // A that touches part of B -- converts its slice of B)
+    uint8_t* needed = nullptr;
+    if (!same) {
+      needed = sc.alloc<uint8_t>((Bin->rows + 15) / 16 + 1);
+      TSG_CUDA(cudaMemsetAsync(needed, 0, (Bin->rows + 15) / 16 + 1, s));
+    }
     if (pre_a) {  // the previous stage's emitted tiles
       TA = *pre_a;
       ntA_d = TA.trp + TA.tile_rows;
+      if (needed) {
+        launch_mark_needed(TA, needed, s);
+        check_launch(ctx);
+      }
     } else {
       dA = stage(ctx, sc, Ain, st);
-      ntA_d = convert(ctx, sc, dA, TA, same ? 3 : 1, err_flag, opt.drop_nonfinite);
+      ntA_d = convert(ctx, sc, dA, TA, same ? 3 : 1, err_flag, opt.drop_nonfinite, nullptr, needed);
     }
     dB = same ? dA : stage(ctx, sc, Bin, st);
     const uint32_t* ntB_d = ntA_d;
-    if (!same) {
-      // only the B tile rows A's tiles refer to are tiled (a row panel of A --
-      // multi-GPU, or any A that touches part of B -- converts its slice of B)
-      auto* needed = sc.alloc<uint8_t>((dB.rows + 15) / 16 + 1);
-      TSG_CUDA(cudaMemsetAsync(needed, 0, (dB.rows + 15) / 16 + 1, s));
-      launch_mark_needed(TA, needed, s);
-      check_launch(ctx);
-      ntB_d = convert(ctx, sc, dB, TB_own, 2, err_flag, opt.drop_nonfinite, needed);
-    }
+    if (!same) ntB_d = convert(ctx, sc, dB, TB_own, 2, err_flag, opt.drop_nonfinite, needed);
     TB = same ? &TA : &TB_own;
     launch_row_stats(TA, dscal + 1, s);
     check_launch(ctx);
@@ -873,10 +879,26 @@ struct Call {
     TSG_CUDA(cudaMemsetAsync(tile_cnt + tA, 0, sizeof(uint32_t), s));
     launch_enum_count(TA, B, tA, tile_cnt, raw_d, s);
     check_launch(ctx);
-    P = total_u32(ctx, sc, tile_cnt, tA);
-    raw = readback(ctx, raw_d);
-    if (P >= (uint64_t(1) << 31)) throw Fail{TSG_ERR_OTHER, "task list beyond 2^31 pairs needs row-panel batching"};
+    // pair offsets per A tile and per tile row; the u64 pair total read back
+    // with the raw-pair total in one sync
     exclusive_sum(ctx, sc, tile_cnt, tile_off, tA + 1);
+    launch_row_pair_off(TA, tile_off, row_pair_off, s);
+    check_launch(ctx);
+    auto* p_d = sc.alloc<unsigned long long>(1);
+    TSG_CUDA(cudaMemsetAsync(p_d, 0, sizeof(unsigned long long), s));
+    if (tA) {
+      const unsigned blocks = unsigned(std::min<uint64_t>((tA + 255) / 256, 1184));
+      sum_u32_kernel<<<blocks, 256, 0, s>>>(tile_cnt, tA, p_d);
+      check_launch(ctx);
+    }
+    {
+      const unsigned long long* src[2] = {p_d, raw_d};
+      unsigned long long v[2];
+      readback_many(ctx, src, v);
+      P = v[0];
+      raw = v[1];
+    }
+    if (P >= (uint64_t(1) << 31)) throw Fail{TSG_ERR_OTHER, "task list beyond 2^31 pairs needs row-panel batching"};
     tl.npairs = P;
     uint64_t* pairs_u = sc.alloc<uint64_t>(P);
     uint32_t* keys_u = sc.alloc<uint32_t>(P);
@@ -891,12 +913,15 @@ struct Call {
     // Sort choice (measured): tile rows holding thousands of pairs each
     // (R-MAT) sort fastest per tile row over just the column bits; shorter
     // rows (rect, AMG) as one global radix sort over (row, column) keys.
+    // Sort choice (measured): tile rows holding thousands of pairs each
+    // (R-MAT) sort fastest per tile row over just the column bits; shorter
+    // rows (rect, AMG) as one global radix sort over (row, column) keys.  (A
+    // block-per-tile-row shared-memory sort measured 1.64 ms on rect, no
+    // better than the global radix.)
     const bool long_rows = P >= 4096ull * TA.tile_rows;
     const int sort_variant = tuning_variant("TSG_SORT", long_rows ? 1 : 0);
     const bool radix = jbits + ibits <= 32 && sort_variant == 0;
     launch_enum_fill(TA, B, tA, tile_off, pairs_u, keys_u, radix ? jbits : 32, s);
-    check_launch(ctx);
-    launch_row_pair_off(TA, tile_off, row_pair_off, s);
     check_launch(ctx);
     record(ctx, timing, 2);
     // stable sort by output tile column within each tile row

@@ -119,7 +119,12 @@ struct Gapped {
   uint4* chunk[2] = {nullptr, nullptr};
   uint32_t* etile = nullptr;  // per entry: tile rank within its tile row | kDupEntry, or kNoTile
   uint32_t* ntiles = nullptr;  // per tile row
+  uint8_t* mark = nullptr;     // optional: mark[J] = 1 for every tile column J (the B tile rows A needs)
 };
+
+__device__ __forceinline__ void mark_column(const Gapped& out, uint32_t J) {
+  if (out.mark && !out.mark[J]) out.mark[J] = 1;  // most tiles share their column's flag: skip the store
+}
 
 // Tile-slot (r, c) of a 16x16 tile -> its lane and fp16 position in the
 // lane's 16-byte chunk.  A order: lane (g, t) holds rows g, g+8 x cols 2t,
@@ -244,6 +249,7 @@ __device__ __forceinline__ uint32_t sparse_panel(FastSmem& sm, const Gapped& out
       uint4* dst = reinterpret_cast<uint4*>(out.rm2 + size_t(E0 + t) * 8);
       dst[0] = make_uint4(rm[0], rm[1], rm[2], rm[3]);
       dst[1] = make_uint4(rm[4], rm[5], rm[6], rm[7]);
+      mark_column(out, J);
 #pragma unroll
       for (int role = 0; role < 2; ++role) {
         if (!(roles & (1 << role))) continue;
@@ -551,6 +557,7 @@ __global__ void __launch_bounds__(256, 4) convert_fast_kernel(CsrView in, uint32
     uint4* dst = reinterpret_cast<uint4*>(out.rm2 + size_t(E0 + k) * 8);
     dst[0] = m0;
     dst[1] = m1;
+    mark_column(out, J);
     if (roles & 1) out.rec[kRoleA][E0 + k] = make_uint4(sm.lm[k][0], cbA[h], occ, J);
     if (roles & 2) out.rec[kRoleB][E0 + k] = make_uint4(sm.lm[k][1], cbB[h], occ, J);
     sm.cl[k][0] = make_uint2(cbA[h], sm.lm[k][0]);
@@ -676,6 +683,7 @@ __global__ void __launch_bounds__(256) convert_walk_kernel(CsrView in, Gapped ou
       // the 256-bit mask as interleaved row masks: word g = row g | row g+8 << 16
       const uint32_t rm_hi = __shfl_sync(kFull, rm, (lane & 7) + 8);
       if (lane < 8) out.rm2[size_t(t) * 8 + lane] = rm | (rm_hi << 16);
+      if (lane == 0) mark_column(out, J);
 #pragma unroll
       for (int role = 0; role < 2; ++role) {
         if (!(roles & (1 << role))) continue;
@@ -731,8 +739,10 @@ __global__ void __launch_bounds__(256) tiles_compact_kernel(CsrView in, uint32_t
 // B tile rows that some A tile refers to (A's tile columns).
 __global__ void mark_needed_kernel(const TileMat A, uint8_t* __restrict__ needed) {
   const uint32_t nt = A.trp[A.tile_rows];
-  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < nt; t += gridDim.x * blockDim.x)
-    needed[__ldg(&A.tco[t].x)] = 1;
+  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < nt; t += gridDim.x * blockDim.x) {
+    const uint32_t J = __ldg(&A.tco[t].x);
+    if (!needed[J]) needed[J] = 1;  // most A tiles share their column's flag: skip the contended store
+  }
 }
 
 __global__ void row_stats_kernel(const uint32_t* __restrict__ trp, uint32_t tile_rows,
@@ -778,6 +788,7 @@ void launch_convert(const CsrView& in, TileMat& out, int roles, const ConvertScr
   g.chunk[1] = out.chunk[1];
   g.etile = out.etile;
   g.ntiles = cs.ntiles;
+  g.mark = cs.mark;
   auto kf = in.dtype == 0 ? convert_fast_kernel<0> : in.dtype == 2 ? convert_fast_kernel<2> : convert_fast_kernel<1>;
   kf<<<(out.tile_rows + 7) / 8, 256, 0, st>>>(in, out.tile_rows, g, roles, cs.walk_list, cs.walk_count, err_flag,
                                     drop_nonfinite, needed);

@@ -58,6 +58,7 @@ struct ConvertScratch {
   uint32_t* ntiles = nullptr;          // tile_rows + 1
   uint32_t* walk_list = nullptr;       // tile_rows
   uint32_t* walk_count = nullptr;      // 1, zeroed
+  uint8_t* mark = nullptr;             // optional, zeroed: set for every tile column
 };
 void launch_convert(const CsrView& in, TileMat& out, int roles, const ConvertScratch& cs, unsigned* err_flag,
                     int drop_nonfinite, const uint8_t* needed, cudaStream_t st);
