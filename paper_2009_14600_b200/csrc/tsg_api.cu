@@ -384,6 +384,7 @@ struct Call {
   uint64_t launches0;
 
   unsigned* dscal = nullptr;  // [0] error flags, [1] max A tiles per tile row
+  unsigned* work = nullptr;
   unsigned* err_flag = nullptr;
   bool same = false;
   CsrView dA, dB;
@@ -433,6 +434,7 @@ struct Call {
                                         "x" + std::to_string(Bin->cols)};
     record(ctx, timing, 0);
     dscal = sc.alloc<unsigned>(2);
+    work = sc.alloc<unsigned>(1);  // tile-row counter of the persistent numeric pass
     TSG_CUDA(cudaMemsetAsync(dscal, 0, 2 * sizeof(unsigned), s));
     err_flag = dscal;
     same = !pre_a && (Ain == Bin || (Ain->row_ptr == Bin->row_ptr && Ain->col == Bin->col &&
@@ -561,7 +563,7 @@ struct Call {
     const uint64_t cap_slots = ctx->stage_cap / sizeof(uint2);
     if (timing) TSG_CUDA(cudaEventRecord(ctx->kev[0], s));
     launch_panel_numeric(TA, *TB, rows, row_stage, cap_slots, stage, rowcnt, counted_d, tot_d + 3, tot_d, opt.mode,
-                         0, TA.tile_rows, s, nullptr, dscal);
+                         0, TA.tile_rows, s, nullptr, dscal, work);
     check_launch(ctx);
     if (timing) TSG_CUDA(cudaEventRecord(ctx->kev[1], s));
     record(ctx, timing, 5);
@@ -591,7 +593,7 @@ struct Call {
       TSG_CUDA(cudaMemsetAsync(counted_d, 0, sizeof(unsigned long long), s));
       TSG_CUDA(cudaMemsetAsync(tot_d, 0, 3 * sizeof(unsigned long long), s));
       launch_panel_numeric(TA, *TB, rows, row_stage, stage_total, stage, rowcnt, counted_d, tot_d + 3, tot_d,
-                           opt.mode, 0, TA.tile_rows, s);
+                           opt.mode, 0, TA.tile_rows, s, nullptr, nullptr, work);
       check_launch(ctx);
       unsigned long long t[4];
       scan_rows(tot_d, t);
@@ -692,7 +694,7 @@ struct Call {
       return;
     }
     launch_panel_numeric(TA, *TB, rows, row_stage, cap_slots, stage, rowcnt, counted_d, tot_d + 3,
-                         elem ? tot_d : nullptr, opt.mode, 0, TA.tile_rows, s);
+                         elem ? tot_d : nullptr, opt.mode, 0, TA.tile_rows, s, nullptr, nullptr, work);
     check_launch(ctx);
     if (timing) TSG_CUDA(cudaEventRecord(ctx->kev[1], s));
     record(ctx, timing, 5);
@@ -710,7 +712,7 @@ struct Call {
         TSG_CUDA(cudaMemsetAsync(counted_d, 0, sizeof(unsigned long long), s));
         if (elem) TSG_CUDA(cudaMemsetAsync(tot_d, 0, 3 * sizeof(unsigned long long), s));
         launch_panel_numeric(TA, *TB, rows, row_stage, cap_slots, stage, rowcnt, counted_d, tot_d + 3,
-                             elem ? tot_d : nullptr, opt.mode, 0, TA.tile_rows, s);
+                             elem ? tot_d : nullptr, opt.mode, 0, TA.tile_rows, s, nullptr, nullptr, work);
         check_launch(ctx);
         scan_rows(tot_d, t);
         take_totals(t);
@@ -760,7 +762,7 @@ struct Call {
     em.err_flag = err_flag;
     if (timing) TSG_CUDA(cudaEventRecord(ctx->kev[0], s));
     launch_panel_numeric(TA, *TB, rows, nullptr, 0, nullptr, nullptr, counted_d, nullptr, nullptr, opt.mode, 0,
-                         TA.tile_rows, s, &em);
+                         TA.tile_rows, s, &em, nullptr, work);
     check_launch(ctx);
     if (timing) TSG_CUDA(cudaEventRecord(ctx->kev[1], s));
     record(ctx, timing, 5);
@@ -836,7 +838,7 @@ struct Call {
       const uint32_t I1 = uint32_t(uint64_t(TA.tile_rows) * (c + 1) / nch);
       const int64_t r0 = int64_t(I0) * 16, r1 = std::min<int64_t>(int64_t(I1) * 16, rows);
       launch_panel_numeric(TA, *TB, rows, row_stage, cap_slots, stage, rowcnt, counted_d, need, nullptr, opt.mode,
-                           I0, I1, s);
+                           I0, I1, s, nullptr, nullptr, work);
       check_launch(ctx);
       // row_ptr[r0 .. r1] = row_ptr[r0] + exclusive prefix (row_ptr[r0] from the previous chunk)
       TSG_CUDA(cub::DeviceScan::ExclusiveScan(tmp, tmp_bytes, rowcnt + r0, d_rp + r0, cuda::std::plus<int64_t>(),

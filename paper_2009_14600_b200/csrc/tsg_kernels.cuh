@@ -96,7 +96,7 @@ void launch_panel_numeric(const TileMat& A, const TileMat& B, int64_t rows, cons
                           uint64_t stage_cap, uint2* stage, int64_t* rowcnt, unsigned long long* counted,
                           const unsigned long long* need, unsigned long long* stats, int mode,
                           uint32_t I0, uint32_t I1, cudaStream_t st, const TileEmit* emit = nullptr,
-                          const unsigned* gate = nullptr);
+                          const unsigned* gate = nullptr, unsigned* work = nullptr);
 // row_bound[r] = min(B.cols, sum over A's entries (r, k) of nnz(B row k));
 // *total += sum of row_bound
 void launch_elem_bound(const CsrView& A, const int64_t* rpB, int64_t bcols, uint32_t* row_bound,

@@ -31,6 +31,8 @@
 //   CUB scan              -> row_ptr                            (tsg_api.cu)
 //   panel_copy_kernel     staging rows -> CSR (contiguous copies), the
 //                         non-finite check of finalize_segment
+#include <algorithm>
+
 #include "tsg_kernels.cuh"
 #include "tsg_mma.cuh"
 
@@ -216,7 +218,8 @@ __global__ void __launch_bounds__(256, kMinBlocks) panel_numeric_kernel(TileMat 
                                                               const unsigned long long* __restrict__ need,
                                                               unsigned long long* __restrict__ stats,
                                                               uint32_t I0, uint32_t I1, TileEmit em,
-                                                              const unsigned* __restrict__ gate) {
+                                                              const unsigned* __restrict__ gate,
+                                                              unsigned* __restrict__ work) {
   __shared__ __align__(16) uint4 s_meta[8][32];
   // TENSOR: [A tile of the row][lane] -> chunk index (ORDERED keeps the metas)
   __shared__ uint32_t s_aidx[kOrdered ? 1 : 8][32][32];
@@ -224,21 +227,32 @@ __global__ void __launch_bounds__(256, kMinBlocks) panel_numeric_kernel(TileMat 
   __shared__ float sB[kOrdered ? 8 : 1][16 * kSRow];
   const int lane = threadIdx.x & 31;
   const int w = threadIdx.x >> 5;
-  const uint32_t I = I0 + blockIdx.x * 8 + w;
-  if (I >= I1) return;
-  if (!kEmit && (*need > stage_cap || (*need >> 32))) return;
+  if (!kEmit && (*need > stage_cap || (*need >> 32))) return;  // arena too small: the host reruns the pass
   // speculative launch: {error flags, max A tiles per tile row} of the
   // conversion; invalid input or rows that are not light -> nothing to do
-  if (gate && ((gate[0] & kErrInvariant) || gate[1] > 32u)) return;  // arena too small: the host reruns the pass
+  if (gate && ((gate[0] & kErrInvariant) || gate[1] > 32u)) return;
   const uint4* cA = A.chunk[kRoleA];
   const uint4* cB = B.chunk[kRoleB];
   const unsigned lt = lanemask_lt(), bit = 1u << lane;
   const LaneLayout L(lane);
+  uint32_t nstruct = 0, np = 0, ns = 0, rw = 0;
+  // persistent warps (`work` != null) take tile rows from a counter, so the
+  // last wave does not leave SMs idle; otherwise warp w of block b owns one
+  for (uint32_t it = 0;; ++it) {
+  uint32_t I;
+  if (work) {
+    I = 0;
+    if (lane == 0) I = I0 + atomicAdd(work, 1u);
+    I = __shfl_sync(kFull, I, 0);
+  } else {
+    I = it == 0 ? I0 + blockIdx.x * 8 + w : I1;
+  }
+  if (I >= I1) break;
+  __syncwarp();  // the previous row's shared scratch is no longer read
   Merge m;
   uint32_t a;
   m.start(A, B, I, lane, a);
-  const uint32_t raw_len = m.end - m.cur;
-  uint32_t np = 0, ns = 0;
+  rw += __reduce_add_sync(kFull, m.end - m.cur);  // raw pairs of this tile row
   const uint32_t na = A.trp[I + 1] - A.trp[I];
   const uint2 am = uint32_t(lane) < na ? __ldg(A.meta[kRoleA] + a) : make_uint2(0, 0);
   if (!kOrdered) {
@@ -254,7 +268,6 @@ __global__ void __launch_bounds__(256, kMinBlocks) panel_numeric_kernel(TileMat 
   uint32_t wg = !kEmit && rg < rows ? __ldg(row_stage + rg) : 0u;
   uint32_t wg8 = !kEmit && rg8 < rows ? __ldg(row_stage + rg8) : 0u;
   const uint32_t wg0 = wg, wg80 = wg8;
-  uint32_t nstruct = 0;
   uint32_t e_tiles = 0, e_chunks = 0;  // emit mode: tiles / chunks written for this tile row
   while (true) {
     const uint32_t J = __reduce_min_sync(kFull, m.bt.x);
@@ -375,15 +388,13 @@ __global__ void __launch_bounds__(256, kMinBlocks) panel_numeric_kernel(TileMat 
     if (rg < rows) rowcnt[rg] = int64_t(wg - wg0);
     if (rg8 < rows) rowcnt[rg8] = int64_t(wg8 - wg80);
   }
+  }  // tile rows
   nstruct = __reduce_add_sync(kFull, nstruct);
   if (lane == 0 && nstruct) atomicAdd(counted, (unsigned long long)nstruct);
-  if (stats) {  // the statistics panel_count_kernel would have produced
-    const uint32_t rw = __reduce_add_sync(kFull, raw_len);
-    if (lane == 0) {
-      atomicAdd(stats, (unsigned long long)np);
-      atomicAdd(stats + 1, (unsigned long long)ns);
-      atomicAdd(stats + 2, (unsigned long long)rw);
-    }
+  if (stats && lane == 0 && (np | rw)) {  // the statistics panel_count_kernel would have produced
+    atomicAdd(stats, (unsigned long long)np);
+    atomicAdd(stats + 1, (unsigned long long)ns);
+    atomicAdd(stats + 2, (unsigned long long)rw);
   }
 }
 
@@ -449,12 +460,14 @@ void launch_elem_bound(const CsrView& A, const int64_t* rpB, int64_t bcols, uint
 void launch_panel_numeric(const TileMat& A, const TileMat& B, int64_t rows, const uint32_t* row_stage,
                           uint64_t stage_cap, uint2* stage, int64_t* rowcnt, unsigned long long* counted,
                           const unsigned long long* need, unsigned long long* stats, int mode,
-                          uint32_t I0, uint32_t I1, cudaStream_t st, const TileEmit* emit, const unsigned* gate) {
-  const unsigned blocks = (I1 - I0 + 7) / 8;
+                          uint32_t I0, uint32_t I1, cudaStream_t st, const TileEmit* emit, const unsigned* gate,
+                          unsigned* work) {
+  unsigned blocks = (I1 - I0 + 7) / 8;
   if (I1 <= I0) return;
   const TileEmit em = emit ? *emit : TileEmit{};
   using K = void (*)(TileMat, TileMat, int64_t, const uint32_t*, uint64_t, uint2*, int64_t*, unsigned long long*,
-                     const unsigned long long*, unsigned long long*, uint32_t, uint32_t, TileEmit, const unsigned*);
+                     const unsigned long long*, unsigned long long*, uint32_t, uint32_t, TileEmit, const unsigned*,
+                     unsigned*);
   K k;
   if (mode == 1)
     k = emit ? panel_numeric_kernel<true, 4, true> : panel_numeric_kernel<true, 4, false>;
@@ -463,7 +476,25 @@ void launch_panel_numeric(const TileMat& A, const TileMat& B, int64_t rows, cons
   else
     k = tuning_variant("TSG_PANEL_MINB", 4) == 5 ? panel_numeric_kernel<false, 5, false>
                                                   : panel_numeric_kernel<false, 4, false>;
-  k<<<blocks, 256, 0, st>>>(A, B, rows, row_stage, stage_cap, stage, rowcnt, counted, need, stats, I0, I1, em, gate);
+  if (work) {  // persistent: one resident wave takes the tile rows from the counter
+    static int cached[8] = {0};
+    const int slot = (mode == 1 ? 4 : 0) + (emit ? 2 : 0);
+    if (!cached[slot]) {
+      int per_sm = 0, dev = 0, sms = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, reinterpret_cast<const void*>(k), 256, 0);
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      cached[slot] = std::max(1, per_sm) * std::max(1, sms);
+    }
+    if (blocks <= unsigned(cached[slot])) {
+      work = nullptr;  // one wave covers every tile row: static assignment
+    } else {
+      blocks = unsigned(cached[slot]);
+      cudaMemsetAsync(work, 0, sizeof(unsigned), st);
+    }
+  }
+  k<<<blocks, 256, 0, st>>>(A, B, rows, row_stage, stage_cap, stage, rowcnt, counted, need, stats, I0, I1, em, gate,
+                            work);
 }
 
 // Emitted tiles (gapped per tile row) -> dense CSR-of-tiles: warp per tile row.
