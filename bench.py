@@ -428,8 +428,10 @@ def run_reference(args):
         from paper_2009_14600_b200.tilemul import Csr
         cb += W.cbar(Csr(RA.rows, RA.cols, RA.row_ptr, RA.col, RA.val), mats[2])
     cores = os.cpu_count() or 1
-    steps = max(1, min(args.steps, 5))
-    warm = max(0, min(args.warmup, 1))
+    # bounded: a FEM27 run is ~1.8 s on 16 host threads, so K <= 10, W <= 3
+    # keeps the reference arm under a minute
+    steps = max(1, min(args.steps, 10))
+    warm = max(0, min(args.warmup, 3))
     for _ in range(warm):
         cpu_run(mats, cores)
     secs = [cpu_run(mats, cores).times["total"] for _ in range(steps)]
