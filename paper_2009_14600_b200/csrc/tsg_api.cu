@@ -774,17 +774,10 @@ struct Call {
     T.tile_cols = uint32_t((T.cols + 15) / 16);
     T.trp = kept(sc.alloc<uint32_t>(nr, true));
     exclusive_sum(ctx, sc, em.rtiles, T.trp, nr);
-    {
-      const unsigned long long* src[1] = {counted_d};
-      unsigned long long v[1];
-      uint32_t* tiles_h = reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(ctx->pinned) + 48);
-      TSG_CUDA(cudaMemcpyAsync(tiles_h, T.trp + nr - 1, 4, cudaMemcpyDeviceToHost, s));
-      readback_many(ctx, src, v);
-      counted = v[0];
-      emit_tiles = *tiles_h;
-    }
-    const uint64_t nt = std::max<uint64_t>(emit_tiles, 1);
-    T.cap = emit_tiles;
+    // the dense arrays are sized by the segment count S (an emitted tile per
+    // segment at most): no readback here; counted is read by finish()
+    const uint64_t nt = std::max<uint64_t>(S, 1);
+    T.cap = S;
     T.tco = kept(sc.alloc<uint2>(nt, true));
     T.rm2 = kept(sc.alloc<uint32_t>(nt * 8, true));
     T.trow = kept(sc.alloc<uint32_t>(nt, true));
@@ -1042,6 +1035,8 @@ struct Call {
     // non-finite accumulators are flagged by the CSR pass (read at the final sync)
     unsigned* flags_host = reinterpret_cast<unsigned*>(reinterpret_cast<char*>(ctx->pinned) + 56);
     TSG_CUDA(cudaMemcpyAsync(flags_host, err_flag, 4, cudaMemcpyDeviceToHost, s));
+    unsigned long long* counted_host = reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(ctx->pinned) + 40);
+    if (emit_out) TSG_CUDA(cudaMemcpyAsync(counted_host, counted_d, 8, cudaMemcpyDeviceToHost, s));
     C->rows = rows;
     C->cols = Bin->cols;
     C->nnz = nnzC;
@@ -1061,6 +1056,7 @@ struct Call {
     C->val = static_cast<float*>(owner->p[2]);
 
     TSG_CUDA(cudaStreamSynchronize(s));
+    if (emit_out) counted = *counted_host;
     raise_flags(*flags_host);
     if (tiles) {  // test path: 16x16 tiled view of the realised C
       std::vector<int64_t> h_rp(rows + 1);
