@@ -289,3 +289,62 @@ def test_device_output_speculation(ctx):
     with pytest.raises(T.InvariantError):
         ctx.spgemm(oob, oob, out="device")
     assert csr_bits_equal(ctx.spgemm(A, A, out="device").C.to_numpy(), ctx.spgemm(A, A).C)
+
+
+def _coo(rows, cols, r, c, v):
+    """CSR from unsorted (row, col, value) triples; duplicates keep the first."""
+    r, c, v = np.asarray(r, np.int64), np.asarray(c, np.int64), np.asarray(v, np.float32)
+    key = r * cols + c
+    key, first = np.unique(key, return_index=True)
+    return W._from_rows_cols(rows, cols, key // cols, key % cols, v[first])
+
+
+@pytest.mark.parametrize("shape", ["wide_sparse", "many_tiles", "dense_panel", "zeros_and_underflow"])
+def test_conversion_paths(ctx, shape):
+    """Every conversion path, checked through the product (ORDERED bit-exact
+    against the reference's oracle, both operand roles, A.A and A.B):
+    wide_sparse   panels spanning > 8192 tile columns, <= 512 entries (sort path)
+    many_tiles    narrow panels with > 64 tiles (bitmap -> sort path)
+    dense_panel   panels of > 512 entries (the walk)
+    zeros_and_underflow  explicit zeros, values that round to zero and
+                  duplicate-tile entries in B rows (the etile first-entry rule)"""
+    from oracle import port
+    rng = np.random.default_rng({"wide_sparse": 1, "many_tiles": 2, "dense_panel": 3, "zeros_and_underflow": 4}[shape])
+    if shape == "wide_sparse":
+        n, m = 4096, 300000
+        nnz = 6 * n
+        A = _coo(n, m, rng.integers(0, n, nnz), rng.integers(0, m, nnz), rng.choice([-2.0, -1.0, 0.5, 1.0], nnz))
+        B = _coo(m, 512, rng.integers(0, m, 3 * m // 10), rng.integers(0, 512, 3 * m // 10),
+                 rng.choice([-1.0, 1.0, 2.0], 3 * m // 10))
+    elif shape == "many_tiles":
+        n = 2048
+        r = np.repeat(np.arange(n), 20)
+        c = (r // 16) * 16 + rng.integers(0, 4000, r.size)  # ~20 entries/row over ~250 tile columns
+        c = np.minimum(c, 8000)
+        A = _coo(n, 8192, r, c, rng.choice([-1.0, 1.0, 0.25], r.size))
+        B = _coo(8192, 2048, rng.integers(0, 8192, 60000), rng.integers(0, 2048, 60000),
+                 rng.choice([-1.0, 2.0], 60000))
+    elif shape == "dense_panel":
+        n = 256
+        r = np.repeat(np.arange(n), 60)
+        c = rng.integers(0, 30000, r.size)
+        A = _coo(n, 30000, r, c, rng.choice([-1.0, 1.0, 3.0], r.size))
+        B = _coo(30000, 700, rng.integers(0, 30000, 90000), rng.integers(0, 700, 90000),
+                 rng.choice([-0.5, 1.0], 90000))
+    else:
+        n = 1024
+        r = rng.integers(0, n, 12000)
+        c = rng.integers(0, n, 12000)
+        v = rng.choice([0.0, 1e-9, -1e-9, 1.0, -2.0, 0.5], 12000)  # zeros and binary16 underflows dropped
+        A = _coo(n, n, r, c, v)
+        B = _coo(n, n, rng.integers(0, n, 9000), rng.integers(0, n, 9000),
+                 rng.choice([0.0, 1e-9, 1.0, -1.0, 4.0], 9000))
+    for X, Y in ((A, B), (A, A) if A.rows == A.cols else (B, A)):
+        if X.cols != Y.rows:
+            continue
+        want = port.spgemm_mixed(X, Y)
+        got = ctx.spgemm(X, Y, mode="ordered")
+        assert csr_bits_equal(got.C, want), (shape, first_diff(got.C, want))
+        assert got.stats["counted_elements"] == port.tile_stats(X, Y, 16)["counted_elements"]
+        dev = ctx.spgemm(X, Y, mode="ordered", out="device").C.to_numpy()
+        assert csr_bits_equal(dev, want), (shape, "device", first_diff(dev, want))
