@@ -102,9 +102,13 @@ void launch_panel_numeric(const TileMat& A, const TileMat& B, int64_t rows, cons
 void launch_elem_bound(const CsrView& A, const int64_t* rpB, int64_t bcols, uint32_t* row_bound,
                        unsigned long long* total, cudaStream_t st);
 void launch_emit_compact(uint32_t tile_rows, const TileEmit& em, const uint32_t* trp, TileMat& T, cudaStream_t st);
+// dcol (nullable): also writes the host transport -- first[row] = the row's
+// first column, dcol[p] = column delta to the previous entry of the row (0 at
+// a row start); *ovf |= 1 when some delta exceeds 16 bits
 void launch_panel_copy(int64_t rows, const uint32_t* row_stage, const int64_t* row_ptr, const uint2* stage,
                        int32_t* col, float* val, unsigned* err_flag, uint32_t I0, uint32_t I1,
-                       cudaStream_t st);
+                       cudaStream_t st, uint16_t* dcol = nullptr, int32_t* first = nullptr,
+                       unsigned* ovf = nullptr);
 // (2) symbolic -- general: enumerate + filter, stable sort, segment heads
 void launch_enum_count(const TileMat& A, const TileMat& B, uint64_t tA, uint32_t* tile_cnt,
                        unsigned long long* raw_total, cudaStream_t st);

@@ -348,3 +348,26 @@ def test_conversion_paths(ctx, shape):
         assert got.stats["counted_elements"] == port.tile_stats(X, Y, 16)["counted_elements"]
         dev = ctx.spgemm(X, Y, mode="ordered", out="device").C.to_numpy()
         assert csr_bits_equal(dev, want), (shape, "device", first_diff(dev, want))
+
+
+@pytest.mark.parametrize("delta", ["0", "1"])
+def test_host_output_column_transport(ctx, monkeypatch, delta):
+    """Host output of the light path ships each slice's columns as a first
+    column per row plus 16-bit deltas, decoded on the host; slices with a
+    gap beyond 16 bits ship int32 columns.  Rows < 2048 here have small gaps,
+    rows >= 2048 a 150000-column gap: both transports in one call."""
+    from oracle import port
+    monkeypatch.setenv("TSG_DELTA_COLS", delta)  # read by the library on every call
+    n, m = 4096, 200000
+    A = _coo(n, n, np.arange(n), np.arange(n), np.ones(n))
+    r = np.repeat(np.arange(n), 3)
+    far = np.where(np.arange(n) >= 2048, 150000, 40)
+    c = np.stack([np.arange(n), np.arange(n) + 17, np.arange(n) + far], 1).ravel()
+    B = _coo(n, m, r, c, np.tile([1.0, -2.0, 0.5], n))
+    want = port.spgemm_mixed(A, B)
+    host = ctx.spgemm(A, B)
+    assert csr_bits_equal(host.C, want), first_diff(host.C, want)
+    dev = ctx.spgemm(A, B, out="device").C.to_numpy()
+    assert csr_bits_equal(dev, want), first_diff(dev, want)
+    F = W.fem27(24)  # every slice delta-coded
+    assert csr_bits_equal(ctx.spgemm(F, F).C, ctx.spgemm(F, F, out="device").C.to_numpy())
