@@ -402,6 +402,7 @@ __global__ void __launch_bounds__(256, kMinBlocks) panel_numeric_kernel(TileMat 
 // positions (the 16 rows are consecutive in the CSR), each taken from its
 // row's staging region.  Non-finite values raise kErrPrecision
 // (finalize_segment, kernels.cpp:115-127).
+template <bool kDelta>
 __global__ void __launch_bounds__(256) panel_copy_kernel(int64_t rows, uint32_t tile_rows,
                                                         const uint32_t* __restrict__ row_stage,
                                                         const int64_t* __restrict__ row_ptr,
@@ -441,7 +442,7 @@ __global__ void __launch_bounds__(256) panel_copy_kernel(int64_t rows, uint32_t 
       col[base + q] = int32_t(e.y);
       val[base + q] = x;
     }
-    if (dcol) {  // host transport: first column per row + 16-bit deltas
+    if (kDelta) {  // host transport: first column per row + 16-bit deltas
       uint32_t prev = __shfl_up_sync(kFull, e.y, 1);
       if (lane == 0) prev = carry;
       carry = __shfl_sync(kFull, e.y, 31);
@@ -458,7 +459,7 @@ __global__ void __launch_bounds__(256) panel_copy_kernel(int64_t rows, uint32_t 
     }
   }
   if (__any_sync(kFull, bad) && lane == 0) atomicOr(err_flag, unsigned(kErrPrecision));
-  if (dcol && __any_sync(kFull, wide) && lane == 0) atomicOr(ovf, 1u);
+  if (kDelta && __any_sync(kFull, wide) && lane == 0) atomicOr(ovf, 1u);
 }
 
 }  // namespace
@@ -543,8 +544,12 @@ void launch_panel_copy(int64_t rows, const uint32_t* row_stage, const int64_t* r
                        cudaStream_t st, uint16_t* dcol, int32_t* first, unsigned* ovf) {
   if (I1 <= I0) return;
   const unsigned blocks = (I1 - I0 + 7) / 8;
-  panel_copy_kernel<<<blocks, 256, 0, st>>>(rows, I1, row_stage, row_ptr, stage, col, val, err_flag, I0, dcol,
-                                            first, ovf);
+  if (dcol)
+    panel_copy_kernel<true><<<blocks, 256, 0, st>>>(rows, I1, row_stage, row_ptr, stage, col, val, err_flag, I0,
+                                                    dcol, first, ovf);
+  else
+    panel_copy_kernel<false><<<blocks, 256, 0, st>>>(rows, I1, row_stage, row_ptr, stage, col, val, err_flag, I0,
+                                                     nullptr, nullptr, nullptr);
 }
 
 }  // namespace tsg
