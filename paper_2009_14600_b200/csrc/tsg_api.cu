@@ -662,8 +662,12 @@ struct Call {
     S = v[7];
     raw = v[8];
     stage_total = v[9];
-    if (stage_total > cap_slots || (stage_total >> 32)) {  // the rare arena overflow: redo the pass
-      check_stage_total();
+    if (stage_total >> 32) {  // element bound beyond the u32 staging offsets: the tight bound
+      TSG_CUDA(cudaMemsetAsync(counted_d, 0, sizeof(unsigned long long), s));
+      light_path();
+      return true;
+    }
+    if (stage_total > cap_slots) {  // the rare arena overflow: redo the pass
       stage = static_cast<uint2*>(arena(stage_total * sizeof(uint2)));
       TSG_CUDA(cudaMemsetAsync(counted_d, 0, sizeof(unsigned long long), s));
       TSG_CUDA(cudaMemsetAsync(tot_d, 0, 3 * sizeof(unsigned long long), s));
@@ -970,7 +974,8 @@ struct Call {
     // (3) decode each delta-coded slice as it lands (rows split over the pool)
     if (delta) {
       if (!ctx->workers) {
-        const unsigned hc = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+        const unsigned hc = std::max(1u, std::min(unsigned(tuning_variant("TSG_POOL", 16)),
+                                                  std::thread::hardware_concurrency()));
         ctx->workers = new HostPool(hc);
       }
       const unsigned parts = ctx->workers->size();
