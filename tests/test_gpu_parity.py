@@ -371,3 +371,21 @@ def test_host_output_column_transport(ctx, monkeypatch, delta):
     assert csr_bits_equal(dev, want), first_diff(dev, want)
     F = W.fem27(24)  # every slice delta-coded
     assert csr_bits_equal(ctx.spgemm(F, F).C, ctx.spgemm(F, F, out="device").C.to_numpy())
+
+
+def test_chain_device_output_and_empty_stages(ctx):
+    """A chain returned on the device equals the host result; an empty
+    intermediate (no overlap between stages) yields an empty product."""
+    R, A, P = W.amg(32)
+    host = ctx.spgemm_chain([R, A, P]).C
+    dev = ctx.spgemm_chain([R, A, P], out="device").C.to_numpy()
+    assert csr_bits_equal(dev, host), first_diff(dev, host)
+    n = 64
+    X = T.Csr(n, n, np.concatenate([np.zeros(n // 2 + 1, np.int64), np.arange(1, n // 2 + 1, dtype=np.int64)]),
+              np.arange(n // 2, dtype=np.int32), np.ones(n // 2, np.float32))  # rows n/2.. hold cols 0..n/2-1
+    Y = T.Csr(n, n, np.concatenate([np.zeros(n // 2 + 1, np.int64), np.arange(1, n // 2 + 1, dtype=np.int64)]),
+              np.arange(n // 2, dtype=np.int32), np.ones(n // 2, np.float32))
+    # X.Y = 0: X's columns (< n/2) hit Y's empty rows
+    C = ctx.spgemm_chain([X, Y, X]).C
+    assert C.nnz == 0 and np.all(np.asarray(C.row_ptr) == 0)
+    assert csr_bits_equal(C, ref.chain([X, Y, X]))
