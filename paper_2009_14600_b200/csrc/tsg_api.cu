@@ -484,9 +484,7 @@ struct Call {
   // this stage's result emitted as the next stage's A tiles (emit_out); the
   // emitted arrays outlive this call and are listed in `keep`
   const TileMat* pre_a = nullptr;
-  uint64_t pre_a_tiles = 0;
   TileMat* emit_out = nullptr;
-  uint64_t emit_tiles = 0;
   std::vector<void*>* keep = nullptr;
 
   Call(tsg_ctx* c, const tsg_csr* a, const tsg_csr* b, tsg_csr_out* out, const tsg_options& o,
@@ -1288,12 +1286,11 @@ void spgemm_impl(tsg_ctx* ctx, const tsg_csr* Ain, const tsg_csr* Bin, tsg_csr_o
 // stage's tiles (else Ain as CSR).  `emit`: when this stage takes the
 // light-row path, its result becomes the next stage's A tiles (returns
 // true); otherwise C receives CSR as usual (returns false).
-bool chain_stage(tsg_ctx* ctx, const tsg_csr* Ain, const TileMat* pre_a, uint64_t pre_a_tiles,
+bool chain_stage(tsg_ctx* ctx, const tsg_csr* Ain, const TileMat* pre_a,
                  const tsg_csr* Bin, tsg_csr_out* C, TileMat* emit, std::vector<void*>* keep,
                  const tsg_options& opt, tsg_run_stats* st) {
   Call call(ctx, Ain, Bin, C, opt, st);
   call.pre_a = pre_a;
-  call.pre_a_tiles = pre_a_tiles;
   call.keep = keep;
   call.convert_operands();
   if (call.light) {
@@ -1477,7 +1474,7 @@ int tsg_spgemm_chain(tsg_ctx* ctx, int n, const tsg_csr* const* X, tsg_csr_out* 
       keep[w].clear();
       bool emitted = false;
       try {
-        emitted = chain_stage(ctx, &left, pre, pre ? pre->cap : 0, X[i], &next, last ? nullptr : &tiles[w],
+        emitted = chain_stage(ctx, &left, pre, X[i], &next, last ? nullptr : &tiles[w],
                               &keep[w], o, stats);
       } catch (const Fail& f) {
         ctx->err = f.msg;
