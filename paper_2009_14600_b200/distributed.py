@@ -65,16 +65,19 @@ def broadcast_csr(M: Csr | None, src: int, device, dist) -> Csr:
     dist.broadcast(meta, src=src)
     rows, cols, nnz, dt = (int(x) for x in meta.tolist())
     vdt = {0: torch.float16, 1: torch.float32, 2: torch.float64}[dt]
+    # one collective: row_ptr | col | val in a flat byte buffer
+    esz = torch.empty(0, dtype=vdt).element_size()
+    sizes = [8 * (rows + 1), 4 * nnz, esz * nnz]
+    flat = torch.empty(sum(sizes), dtype=torch.uint8, device=device)
+    o = [0, sizes[0], sizes[0] + sizes[1], sum(sizes)]
+    rp = flat[o[0]:o[1]].view(torch.int64)
+    col = flat[o[1]:o[2]].view(torch.int32)
+    val = flat[o[2]:o[3]].view(vdt)
     if rank == src:
-        rp = torch.from_numpy(np.ascontiguousarray(M.row_ptr, np.int64)).to(device)
-        col = torch.from_numpy(np.ascontiguousarray(M.col, np.int32)).to(device)
-        val = torch.from_numpy(np.ascontiguousarray(M.val)).to(device)
-    else:
-        rp = torch.empty(rows + 1, dtype=torch.int64, device=device)
-        col = torch.empty(nnz, dtype=torch.int32, device=device)
-        val = torch.empty(nnz, dtype=vdt, device=device)
-    for t in (rp, col, val):
-        dist.broadcast(t, src=src)
+        rp.copy_(torch.from_numpy(np.ascontiguousarray(M.row_ptr, np.int64)))
+        col.copy_(torch.from_numpy(np.ascontiguousarray(M.col, np.int32)))
+        val.copy_(torch.from_numpy(np.ascontiguousarray(M.val)))
+    dist.broadcast(flat, src=src)
     return Csr(rows, cols, rp, col, val)
 
 
