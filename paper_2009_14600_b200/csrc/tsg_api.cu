@@ -316,7 +316,7 @@ void readback_gather(tsg_ctx* ctx, Scratch& sc, const ScalarGather& g, unsigned 
 // Returns the device address of the tile count (trp[tile_rows]).
 const uint32_t* convert(tsg_ctx* ctx, Scratch& sc, const CsrView& in, TileMat& T, int roles,
                         unsigned* err_flag, int drop_nonfinite, const uint8_t* needed = nullptr,
-                        uint8_t* mark = nullptr) {
+                        uint8_t* mark = nullptr, uint32_t* walk_count_zeroed = nullptr) {
   T.rows = in.rows;
   T.cols = in.cols;
   T.tile_rows = uint32_t((in.rows + 15) / 16);
@@ -328,10 +328,16 @@ const uint32_t* convert(tsg_ctx* ctx, Scratch& sc, const CsrView& in, TileMat& T
   cs.rm2 = sc.alloc<uint32_t>(cap * 8);
   cs.ntiles = sc.alloc<uint32_t>(nr);
   cs.walk_list = sc.alloc<uint32_t>(nr);
-  cs.walk_count = sc.alloc<uint32_t>(1);
   cs.mark = mark;
-  TSG_CUDA(cudaMemsetAsync(cs.walk_count, 0, sizeof(uint32_t), ctx->stream));
-  TSG_CUDA(cudaMemsetAsync(cs.ntiles + nr - 1, 0, sizeof(uint32_t), ctx->stream));
+  if (walk_count_zeroed) {
+    cs.walk_count = walk_count_zeroed;
+  } else {
+    cs.walk_count = sc.alloc<uint32_t>(1);
+    TSG_CUDA(cudaMemsetAsync(cs.walk_count, 0, sizeof(uint32_t), ctx->stream));
+  }
+  // ntiles[tile_rows] and chunk 0 of each role are zeroed by the fast kernel
+  // (which is not launched for an empty matrix)
+  if (T.tile_rows == 0) TSG_CUDA(cudaMemsetAsync(cs.ntiles, 0, sizeof(uint32_t), ctx->stream));
   if (roles & 2) {
     T.etile = sc.alloc<uint32_t>(cap);
     T.csr_rp = in.row_ptr;
@@ -340,7 +346,6 @@ const uint32_t* convert(tsg_ctx* ctx, Scratch& sc, const CsrView& in, TileMat& T
     if (!(roles & (1 << role))) continue;
     cs.rec[role] = sc.alloc<uint4>(cap);
     T.chunk[role] = sc.alloc<uint4>(cap + 1);
-    TSG_CUDA(cudaMemsetAsync(T.chunk[role], 0, sizeof(uint4), ctx->stream));  // zero chunk 0
   }
   launch_convert(in, T, roles, cs, err_flag, drop_nonfinite, needed, ctx->stream);
   check_launch(ctx, 2);
@@ -458,6 +463,7 @@ struct Call {
   Scratch sc;
   uint64_t launches0;
 
+  unsigned long long* zblk = nullptr;  // zero-initialised scalars (convert_operands)
   unsigned* dscal = nullptr;  // [0] error flags, [1] max A tiles per tile row
   unsigned* work = nullptr;
   unsigned* err_flag = nullptr;
@@ -506,9 +512,14 @@ struct Call {
                                         std::to_string(Ain->cols) + ", B is " + std::to_string(Bin->rows) +
                                         "x" + std::to_string(Bin->cols)};
     record(ctx, timing, 0);
-    dscal = sc.alloc<unsigned>(2);
+    // the call's small zero-initialised device scalars, one memset:
+    // [0] error flags + max A tiles per tile row, [1] counted, [2..5] totals
+    // of the speculative light pass, [6] [7] the conversions' walk counters
+    zblk = sc.alloc<unsigned long long>(8);
+    TSG_CUDA(cudaMemsetAsync(zblk, 0, 8 * sizeof(unsigned long long), s));
+    dscal = reinterpret_cast<unsigned*>(zblk);
+    counted_d = zblk + 1;
     work = sc.alloc<unsigned>(1);  // tile-row counter of the persistent numeric pass
-    TSG_CUDA(cudaMemsetAsync(dscal, 0, 2 * sizeof(unsigned), s));
     err_flag = dscal;
     same = !pre_a && (Ain == Bin || (Ain->row_ptr == Bin->row_ptr && Ain->col == Bin->col &&
                                      Ain->val == Bin->val && Ain->rows == Bin->rows && Ain->cols == Bin->cols &&
@@ -531,11 +542,14 @@ struct Call {
       }
     } else {
       dA = stage(ctx, sc, Ain, st);
-      ntA_d = convert(ctx, sc, dA, TA, same ? 3 : 1, err_flag, opt.drop_nonfinite, nullptr, needed);
+      ntA_d = convert(ctx, sc, dA, TA, same ? 3 : 1, err_flag, opt.drop_nonfinite, nullptr, needed,
+                      reinterpret_cast<uint32_t*>(zblk + 6));
     }
     dB = same ? dA : stage(ctx, sc, Bin, st);
     const uint32_t* ntB_d = ntA_d;
-    if (!same) ntB_d = convert(ctx, sc, dB, TB_own, 2, err_flag, opt.drop_nonfinite, needed);
+    if (!same)
+      ntB_d = convert(ctx, sc, dB, TB_own, 2, err_flag, opt.drop_nonfinite, needed, nullptr,
+                      reinterpret_cast<uint32_t*>(zblk + 7));
     TB = same ? &TA : &TB_own;
     launch_row_stats(TA, dscal + 1, s);
     check_launch(ctx);
@@ -559,9 +573,7 @@ struct Call {
     C->_owner = owner;  // released by free_out on any later failure
     d_rp = owner->host ? sc.alloc<int64_t>(rows + 1) : sc.alloc<int64_t>(rows + 1, true);
     if (!owner->host) owner->p[0] = d_rp;
-    counted_d = sc.alloc<unsigned long long>(1);
-    TSG_CUDA(cudaMemsetAsync(counted_d, 0, sizeof(unsigned long long), s));
-    rowcnt = sc.alloc<int64_t>(rows + 1);
+    rowcnt = sc.alloc<int64_t>(rows + 1);  // rowcnt[rows] = 0: written by the numeric kernels
     TSG_CUDA(cudaMemsetAsync(rowcnt + rows, 0, sizeof(int64_t), s));
   }
 
@@ -624,8 +636,7 @@ struct Call {
     auto* row_bound = sc.alloc<uint32_t>(rows + 1);
     auto* row_stage = sc.alloc<uint32_t>(rows + 1);
     TSG_CUDA(cudaMemsetAsync(row_bound + rows, 0, 4, s));
-    auto* tot_d = sc.alloc<unsigned long long>(4);
-    TSG_CUDA(cudaMemsetAsync(tot_d, 0, 4 * sizeof(unsigned long long), s));
+    auto* tot_d = zblk + 2;  // zeroed with the call's scalars
     launch_elem_bound(dA, dB.row_ptr, Bin->cols, row_bound, tot_d + 3, s);
     check_launch(ctx);
     exclusive_sum(ctx, sc, row_bound, row_stage, uint64_t(rows) + 1);

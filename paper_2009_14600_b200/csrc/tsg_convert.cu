@@ -293,6 +293,11 @@ __global__ void __launch_bounds__(256, 4) convert_fast_kernel(CsrView in, uint32
                                                           const uint8_t* __restrict__ needed) {
   __shared__ __align__(16) FastSmem smem[8];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {  // the scan's tail and the zero chunk of each role
+    out.ntiles[tile_rows] = 0;
+    if (roles & 1) out.chunk[kRoleA][0] = make_uint4(0, 0, 0, 0);
+    if (roles & 2) out.chunk[kRoleB][0] = make_uint4(0, 0, 0, 0);
+  }
   const uint32_t I = blockIdx.x * 8 + wib;
   if (I >= tile_rows) return;
   FastSmem& sm = smem[wib];
