@@ -316,7 +316,8 @@ void readback_gather(tsg_ctx* ctx, Scratch& sc, const ScalarGather& g, unsigned 
 // Returns the device address of the tile count (trp[tile_rows]).
 const uint32_t* convert(tsg_ctx* ctx, Scratch& sc, const CsrView& in, TileMat& T, int roles,
                         unsigned* err_flag, int drop_nonfinite, const uint8_t* needed = nullptr,
-                        uint8_t* mark = nullptr, uint32_t* walk_count_zeroed = nullptr) {
+                        uint8_t* mark = nullptr, uint32_t* walk_count_zeroed = nullptr,
+                        unsigned* max_row_tiles = nullptr) {
   T.rows = in.rows;
   T.cols = in.cols;
   T.tile_rows = uint32_t((in.rows + 15) / 16);
@@ -359,7 +360,7 @@ const uint32_t* convert(tsg_ctx* ctx, Scratch& sc, const CsrView& in, TileMat& T
     T.meta[role] = sc.alloc<uint2>(cap);
     T.rec[role] = sc.alloc<uint4>(cap);
   }
-  launch_tiles_compact(in, cs, T, roles, ctx->stream);
+  launch_tiles_compact(in, cs, T, roles, ctx->stream, max_row_tiles);
   check_launch(ctx);
   return T.trp + nr - 1;
 }
@@ -543,7 +544,7 @@ struct Call {
     } else {
       dA = stage(ctx, sc, Ain, st);
       ntA_d = convert(ctx, sc, dA, TA, same ? 3 : 1, err_flag, opt.drop_nonfinite, nullptr, needed,
-                      reinterpret_cast<uint32_t*>(zblk + 6));
+                      reinterpret_cast<uint32_t*>(zblk + 6), dscal + 1);
     }
     dB = same ? dA : stage(ctx, sc, Bin, st);
     const uint32_t* ntB_d = ntA_d;
@@ -551,8 +552,10 @@ struct Call {
       ntB_d = convert(ctx, sc, dB, TB_own, 2, err_flag, opt.drop_nonfinite, needed, nullptr,
                       reinterpret_cast<uint32_t*>(zblk + 7));
     TB = same ? &TA : &TB_own;
-    launch_row_stats(TA, dscal + 1, s);
-    check_launch(ctx);
+    if (pre_a) {  // converted A tiles report their largest tile row in the compaction
+      launch_row_stats(TA, dscal + 1, s);
+      check_launch(ctx);
+    }
     ntA_dev = ntA_d;
     ntB_dev = ntB_d;
     if (!defer) {

@@ -718,9 +718,17 @@ __global__ void __launch_bounds__(256) convert_walk_kernel(CsrView in, Gapped ou
 
 // Gapped tiles -> the dense CSR-of-tiles arrays (warp per tile row).
 __global__ void __launch_bounds__(256) tiles_compact_kernel(CsrView in, uint32_t tile_rows, Gapped g, TileMat T,
-                                                           int roles) {
+                                                           int roles, unsigned* __restrict__ max_row_tiles) {
   const int lane = threadIdx.x & 31;
   const uint32_t I = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (max_row_tiles) {  // the largest tile row (the light-path test), one atomic per block
+    __shared__ unsigned s_max;
+    if (threadIdx.x == 0) s_max = 0;
+    __syncthreads();
+    if (lane == 0 && I < tile_rows) atomicMax(&s_max, g.ntiles[I]);
+    __syncthreads();
+    if (threadIdx.x == 0 && s_max) atomicMax(max_row_tiles, s_max);
+  }
   if (I >= tile_rows) return;
   const uint32_t src = uint32_t(in.row_ptr[int64_t(I) * kTile]), dst = T.trp[I], n = g.ntiles[I];
   const int r0 = (roles & 1) ? 0 : 1;
@@ -802,14 +810,15 @@ void launch_convert(const CsrView& in, TileMat& out, int roles, const ConvertScr
   kw<<<wblocks, 256, 0, st>>>(in, g, roles, cs.walk_list, cs.walk_count, err_flag, drop_nonfinite, needed);
 }
 
-void launch_tiles_compact(const CsrView& in, const ConvertScratch& cs, TileMat& out, int roles, cudaStream_t st) {
+void launch_tiles_compact(const CsrView& in, const ConvertScratch& cs, TileMat& out, int roles, cudaStream_t st,
+                          unsigned* max_row_tiles) {
   if (out.tile_rows == 0) return;
   Gapped g;
   g.rm2 = cs.rm2;
   g.rec[0] = cs.rec[0];
   g.rec[1] = cs.rec[1];
   g.ntiles = cs.ntiles;
-  tiles_compact_kernel<<<(out.tile_rows + 7) / 8, 256, 0, st>>>(in, out.tile_rows, g, out, roles);
+  tiles_compact_kernel<<<(out.tile_rows + 7) / 8, 256, 0, st>>>(in, out.tile_rows, g, out, roles, max_row_tiles);
 }
 
 void launch_mark_needed(const TileMat& A, uint8_t* needed, cudaStream_t st) {

@@ -62,7 +62,9 @@ struct ConvertScratch {
 };
 void launch_convert(const CsrView& in, TileMat& out, int roles, const ConvertScratch& cs, unsigned* err_flag,
                     int drop_nonfinite, const uint8_t* needed, cudaStream_t st);
-void launch_tiles_compact(const CsrView& in, const ConvertScratch& cs, TileMat& out, int roles, cudaStream_t st);
+// max_row_tiles (nullable): atomicMax of the tiles per tile row
+void launch_tiles_compact(const CsrView& in, const ConvertScratch& cs, TileMat& out, int roles, cudaStream_t st,
+                          unsigned* max_row_tiles = nullptr);
 void launch_mark_needed(const TileMat& A, uint8_t* needed, cudaStream_t st);
 void launch_row_stats(const TileMat& A, unsigned* max_row_tiles, cudaStream_t st);
 void launch_cbar(const int32_t* colA, int64_t nnzA, int64_t inner, const int64_t* rpB,
