@@ -11,7 +11,14 @@ from paper_2009_14600_b200.tilemul import Context  # noqa: E402
 cfg = sys.argv[1] if len(sys.argv) > 1 else "fem27"
 mode = sys.argv[2] if len(sys.argv) > 2 else "tensor"
 ctx = Context(device=0)
-mats = [M.to_device("cuda") for M in W.make(cfg)]
+def dev(M):
+    """Device CSR as bench.py builds it: binary16 values as fp16 when exact."""
+    D = M.to_device("cuda")
+    h = D.val.to(torch.float16)
+    return type(D)(D.rows, D.cols, D.row_ptr, D.col, h) if torch.equal(h.to(D.val.dtype), D.val) else D
+
+
+mats = [dev(M) for M in W.make(cfg)]
 torch.cuda.synchronize()
 if len(mats) == 3:
     r = ctx.spgemm_chain(mats, out="device", mode=mode)
