@@ -492,6 +492,7 @@ struct Call {
   // emitted arrays outlive this call and are listed in `keep`
   const TileMat* pre_a = nullptr;
   TileMat* emit_out = nullptr;
+  unsigned long long* emit_tot = nullptr;  // emit mode: P, S, raw accumulated by the numeric pass
   std::vector<void*>* keep = nullptr;
 
   Call(tsg_ctx* c, const tsg_csr* a, const tsg_csr* b, tsg_csr_out* out, const tsg_options& o,
@@ -704,6 +705,21 @@ struct Call {
   }
 
   void light_path() {
+    if (emit_out) {  // chained stage: no staging, only the output tiles per tile row are bounded
+      auto* row_tb = sc.alloc<uint32_t>(nr);
+      TSG_CUDA(cudaMemsetAsync(row_tb + nr - 1, 0, sizeof(uint32_t), s));
+      launch_row_tile_bound(TA, *TB, row_tb, s);
+      check_launch(ctx);
+      emit_tot = sc.alloc<unsigned long long>(4);  // P, S, raw (numeric pass), tile bound
+      TSG_CUDA(cudaMemsetAsync(emit_tot, 0, 4 * sizeof(unsigned long long), s));
+      const unsigned blocks = unsigned(std::min<uint64_t>((nr + 255) / 256, 1184));
+      sum_u32_kernel<<<blocks, 256, 0, s>>>(row_tb, nr - 1, emit_tot + 3);
+      check_launch(ctx);
+      const uint64_t cap = readback(ctx, emit_tot + 3);
+      if (cap >= (uint64_t(1) << 31)) throw Fail{TSG_ERR_OTHER, "emitted tiles beyond 2^31 need row-panel batching"};
+      light_emit(row_tb, cap);
+      return;
+    }
     auto* row_np = sc.alloc<uint32_t>(nr);
     auto* row_ns = sc.alloc<uint32_t>(nr);
     auto* row_raw = sc.alloc<uint32_t>(nr);
@@ -758,12 +774,6 @@ struct Call {
       read_totals();
       check_stage_total();
     };
-    if (emit_out) {
-      read_totals();
-      check_stage_total();
-      light_emit(row_ns);
-      return;
-    }
     // Device output with a staging arena already in place: launch the panel
     // pass without reading the staging total back first; the kernel checks it
     // against the arena on the device and the totals are read with nnz(C)
@@ -829,7 +839,8 @@ struct Call {
 
   // Chained product, light rows: the result goes to the next stage as A tiles
   // (panel pass in emit mode, then compaction into a dense CSR-of-tiles).
-  void light_emit(const uint32_t* row_ns) {
+  // Chained product, light rows, `cap` = the bound on the emitted tiles
+  void light_emit(const uint32_t* row_tb, uint64_t cap) {
     auto kept = [&](auto* p) {
       keep->push_back(p);
       return p;
@@ -839,8 +850,9 @@ struct Call {
     record(ctx, timing, 4);
     TileEmit em;
     auto* tile_base = sc.alloc<uint32_t>(nr);
-    exclusive_sum(ctx, sc, row_ns, tile_base, nr);
+    exclusive_sum(ctx, sc, row_tb, tile_base, nr);
     em.tile_base = tile_base;
+    const uint64_t S = std::max<uint64_t>(cap, 1);
     em.tco = sc.alloc<uint2>(S);
     em.rm2 = sc.alloc<uint32_t>(S * 8);
     em.trow = sc.alloc<uint32_t>(S);
@@ -852,7 +864,7 @@ struct Call {
     TSG_CUDA(cudaMemsetAsync(em.rtiles + nr - 1, 0, sizeof(uint32_t), s));
     em.err_flag = err_flag;
     if (timing) TSG_CUDA(cudaEventRecord(ctx->kev[0], s));
-    launch_panel_numeric(TA, *TB, rows, nullptr, 0, nullptr, nullptr, counted_d, nullptr, nullptr, opt.mode, 0,
+    launch_panel_numeric(TA, *TB, rows, nullptr, 0, nullptr, nullptr, counted_d, nullptr, emit_tot, opt.mode, 0,
                          TA.tile_rows, s, &em, nullptr, work);
     check_launch(ctx);
     if (timing) TSG_CUDA(cudaEventRecord(ctx->kev[1], s));
@@ -865,10 +877,10 @@ struct Call {
     T.tile_cols = uint32_t((T.cols + 15) / 16);
     T.trp = kept(sc.alloc<uint32_t>(nr, true));
     exclusive_sum(ctx, sc, em.rtiles, T.trp, nr);
-    // the dense arrays are sized by the segment count S (an emitted tile per
-    // segment at most): no readback here; counted is read by finish()
-    const uint64_t nt = std::max<uint64_t>(S, 1);
-    T.cap = S;
+    // the dense arrays are sized by the bound (no readback here); counted
+    // and the statistics are read by finish()
+    const uint64_t nt = S;
+    T.cap = cap;
     T.tco = kept(sc.alloc<uint2>(nt, true));
     T.rm2 = kept(sc.alloc<uint32_t>(nt * 8, true));
     T.trow = kept(sc.alloc<uint32_t>(nt, true));
@@ -1209,7 +1221,11 @@ struct Call {
     unsigned* flags_host = reinterpret_cast<unsigned*>(reinterpret_cast<char*>(ctx->pinned) + 56);
     TSG_CUDA(cudaMemcpyAsync(flags_host, err_flag, 4, cudaMemcpyDeviceToHost, s));
     unsigned long long* counted_host = reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(ctx->pinned) + 40);
-    if (emit_out) TSG_CUDA(cudaMemcpyAsync(counted_host, counted_d, 8, cudaMemcpyDeviceToHost, s));
+    unsigned long long* tot_host = reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(ctx->pinned) + 64);
+    if (emit_out) {
+      TSG_CUDA(cudaMemcpyAsync(counted_host, counted_d, 8, cudaMemcpyDeviceToHost, s));
+      if (emit_tot) TSG_CUDA(cudaMemcpyAsync(tot_host, emit_tot, 24, cudaMemcpyDeviceToHost, s));
+    }
     C->rows = rows;
     C->cols = Bin->cols;
     C->nnz = nnzC;
@@ -1229,7 +1245,14 @@ struct Call {
     C->val = static_cast<float*>(owner->p[2]);
 
     TSG_CUDA(cudaStreamSynchronize(s));
-    if (emit_out) counted = *counted_host;
+    if (emit_out) {
+      counted = *counted_host;
+      if (emit_tot) {
+        P = tot_host[0];
+        S = tot_host[1];
+        raw = tot_host[2];
+      }
+    }
     raise_flags(*flags_host);
     if (tiles) {  // test path: 16x16 tiled view of the realised C
       std::vector<int64_t> h_rp(rows + 1);

@@ -104,6 +104,8 @@ void launch_panel_numeric(const TileMat& A, const TileMat& B, int64_t rows, cons
 void launch_elem_bound(const CsrView& A, const int64_t* rpB, int64_t bcols, uint32_t* row_bound,
                        unsigned long long* total, cudaStream_t st);
 void launch_emit_compact(uint32_t tile_rows, const TileEmit& em, const uint32_t* trp, TileMat& T, cudaStream_t st);
+// bound[I] = min(B.tile_cols, raw pairs of A's tile row I): output tiles of the row at most
+void launch_row_tile_bound(const TileMat& A, const TileMat& B, uint32_t* bound, cudaStream_t st);
 // dcol (nullable): also writes the host transport -- first[row] = the row's
 // first column, dcol[p] = column delta to the previous entry of the row (0 at
 // a row start); *ovf |= 1 when some delta exceeds 16 bits

@@ -144,6 +144,22 @@ __global__ void __launch_bounds__(256) elem_bound_kernel(CsrView A, const int64_
   }
 }
 
+// Upper bound of the output tiles of each tile row (chained stages, emit
+// mode): min(B tile columns, raw pairs of the row).  Warp per tile row.
+__global__ void __launch_bounds__(256) row_tile_bound_kernel(TileMat A, TileMat B, uint32_t* __restrict__ bound) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t I = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (I >= A.tile_rows) return;
+  const uint32_t a0 = A.trp[I], na = A.trp[I + 1] - a0;
+  uint32_t raw = 0;
+  for (uint32_t l = lane; l < na; l += 32) {
+    const uint32_t k = __ldg(&A.tco[a0 + l].x);
+    raw += __ldg(B.trp + k + 1) - __ldg(B.trp + k);
+  }
+  raw = __reduce_add_sync(kFull, raw);
+  if (lane == 0) bound[I] = raw < B.tile_cols ? raw : B.tile_cols;
+}
+
 constexpr int kSA = 17;    // padded row stride of the ordered A scratch tile
 constexpr int kSRow = 24;  // row stride of the ordered B scratch tile
 
@@ -531,6 +547,12 @@ __global__ void emit_compact_kernel(uint32_t tile_rows, TileEmit em, const uint3
     T.rec[kRoleA][dst + i] = em.rec[src + i];
   }
   for (uint32_t i = lane; i < 8 * n; i += 32) T.rm2[size_t(dst) * 8 + i] = em.rm2[size_t(src) * 8 + i];
+}
+
+void launch_row_tile_bound(const TileMat& A, const TileMat& B, uint32_t* bound, cudaStream_t st) {
+  const unsigned blocks = (A.tile_rows + 7) / 8;
+  if (blocks == 0) return;
+  row_tile_bound_kernel<<<blocks, 256, 0, st>>>(A, B, bound);
 }
 
 void launch_emit_compact(uint32_t tile_rows, const TileEmit& em, const uint32_t* trp, TileMat& T, cudaStream_t st) {
