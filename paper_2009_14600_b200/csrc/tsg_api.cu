@@ -1139,7 +1139,29 @@ struct Call {
     const uint32_t jmask = jbits >= 32 ? 0xffffffffu : (1u << jbits) - 1u;
     launch_seg_count(TA, row_pair_off, keys, row_nseg, s);
     check_launch(ctx);
-    S = total_u32(ctx, sc, row_nseg, nr);
+    // per-pair operand metas and staging bounds need only the sorted pairs:
+    // launched before the segment count is read, so one synchronisation
+    // returns both the segment count and the staging total
+    tl.pmeta = sc.alloc<uint4>(P + 1);
+    tl.pocc = sc.alloc<uint2>(P + 1);
+    auto* pair_bound = sc.alloc<uint32_t>(P + 1);
+    launch_pair_meta(TA, B, pairs, tl, pair_bound, s);
+    check_launch(ctx);
+    {
+      auto* t_d = sc.alloc<unsigned long long>(2);
+      TSG_CUDA(cudaMemsetAsync(t_d, 0, 2 * sizeof(unsigned long long), s));
+      const unsigned b1 = unsigned(std::min<uint64_t>((nr + 255) / 256, 1184));
+      const unsigned b2 = unsigned(std::min<uint64_t>((P + 255) / 256, 1184));
+      if (nr) sum_u32_kernel<<<b1, 256, 0, s>>>(row_nseg, nr, t_d);
+      if (P) sum_u32_kernel<<<b2, 256, 0, s>>>(pair_bound, P, t_d + 1);
+      check_launch(ctx, 2);
+      const unsigned long long* src[2] = {t_d, t_d + 1};
+      unsigned long long v[2];
+      readback_many(ctx, src, v);
+      S = v[0];
+      stage_total = v[1];
+    }
+    check_stage_total();
     exclusive_sum(ctx, sc, row_nseg, tl.seg_row_ptr, nr);
     tl.nseg = S;
     tl.seg_off = sc.alloc<uint32_t>(S + 1);
@@ -1148,13 +1170,6 @@ struct Call {
     TSG_CUDA(cudaMemcpyAsync(tl.seg_off + S, row_pair_off + nr - 1, 4, cudaMemcpyDeviceToDevice, s));
     launch_seg_fill(TA, row_pair_off, keys, jmask, tl, s);
     check_launch(ctx);
-    tl.pmeta = sc.alloc<uint4>(P + 1);
-    tl.pocc = sc.alloc<uint2>(P + 1);
-    auto* pair_bound = sc.alloc<uint32_t>(P + 1);
-    launch_pair_meta(TA, B, pairs, tl, pair_bound, s);
-    check_launch(ctx);
-    stage_total = total_u32(ctx, sc, pair_bound, P);
-    check_stage_total();
     auto* pair_stage = sc.alloc<uint32_t>(P + 1);
     exclusive_sum(ctx, sc, pair_bound, pair_stage, P + 1);
     launch_seg_stage(tl, pair_stage, s);
