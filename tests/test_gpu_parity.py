@@ -389,3 +389,19 @@ def test_chain_device_output_and_empty_stages(ctx):
     C = ctx.spgemm_chain([X, Y, X]).C
     assert C.nnz == 0 and np.all(np.asarray(C.row_ptr) == 0)
     assert csr_bits_equal(C, ref.chain([X, Y, X]))
+
+
+@pytest.mark.parametrize("name", ["fem27", "rmat"])
+def test_fp16_device_operands(ctx, name):
+    """bench.py hands the device step binary16 values as fp16 (TSG_F16):
+    the conversion's fp16 path (bitmap, sort and walk panels) must give the
+    same product as fp32 operands."""
+    import torch
+    A = W.make_small(name)[0] if name == "rmat" else W.fem27(24)
+    D32 = A.to_device("cuda")
+    D16 = T.Csr(D32.rows, D32.cols, D32.row_ptr, D32.col, D32.val.to(torch.float16))
+    assert torch.equal(D16.val.to(torch.float32), D32.val)  # the workloads are binary16-valued
+    for mode in ("tensor", "ordered"):
+        a = ctx.spgemm(D32, D32, mode=mode, out="device").C.to_numpy()
+        b = ctx.spgemm(D16, D16, mode=mode, out="device").C.to_numpy()
+        assert csr_bits_equal(b, a), (mode, first_diff(b, a))
