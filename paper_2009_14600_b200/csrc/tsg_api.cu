@@ -15,12 +15,7 @@
 // a stream-ordered memory pool (cudaMallocFromPoolAsync), so steady-state
 // calls do not touch the driver allocator.  The host synchronises only to
 // read data-dependent sizes (tile, pair, segment, element counts).
-#include <cub/device/device_radix_sort.cuh>
-#include <cub/device/device_segmented_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
-#include <cub/device/device_segmented_sort.cuh>
-#include <cub/device/device_select.cuh>
-#include <cub/iterator/counting_input_iterator.cuh>
 
 #include <cstdint>
 #include <cstdio>
@@ -343,6 +338,7 @@ const uint32_t* convert(tsg_ctx* ctx, Scratch& sc, const CsrView& in, TileMat& T
     T.etile = sc.alloc<uint32_t>(cap);
     T.csr_rp = in.row_ptr;
   }
+  T.h16 = sc.alloc<uint16_t>(cap);
   for (int role = 0; role < 2; ++role) {
     if (!(roles & (1 << role))) continue;
     cs.rec[role] = sc.alloc<uint4>(cap);
@@ -1046,185 +1042,138 @@ struct Call {
     record(ctx, timing, 6);
   }
 
-  // ---- general rows: task list, sort, numeric, assembly ----------------------------
+  // ---- general rows: per-chunk element SEaC in shared memory (tsg_esc.cu) ----------
   void general_path() {
     const TileMat& B = *TB;
-    TaskList tl;
-    tl.seg_row_ptr = sc.alloc<uint32_t>(nr);
-    uint32_t* row_pair_off = sc.alloc<uint32_t>(nr);
-    auto* raw_d = sc.alloc<unsigned long long>(1);
-    TSG_CUDA(cudaMemsetAsync(raw_d, 0, sizeof(unsigned long long), s));
-    auto* tile_off = sc.alloc<uint32_t>(tA + 1);
-    auto* tile_cnt = sc.alloc<uint32_t>(tA + 1);
-    TSG_CUDA(cudaMemsetAsync(tile_cnt + tA, 0, sizeof(uint32_t), s));
-    launch_enum_count(TA, B, tA, tile_cnt, raw_d, s);
-    check_launch(ctx);
-    // pair offsets per A tile and per tile row; the u64 pair total read back
-    // with the raw-pair total in one sync
-    exclusive_sum(ctx, sc, tile_cnt, tile_off, tA + 1);
-    launch_row_pair_off(TA, tile_off, row_pair_off, s);
-    check_launch(ctx);
-    auto* p_d = sc.alloc<unsigned long long>(1);
-    TSG_CUDA(cudaMemsetAsync(p_d, 0, sizeof(unsigned long long), s));
-    if (tA) {
-      const unsigned blocks = unsigned(std::min<uint64_t>((tA + 255) / 256, 1184));
-      sum_u32_kernel<<<blocks, 256, 0, s>>>(tile_cnt, tA, p_d);
-      check_launch(ctx);
-    }
-    {
-      const unsigned long long* src[2] = {p_d, raw_d};
-      unsigned long long v[2];
-      readback_many(ctx, src, v);
-      P = v[0];
-      raw = v[1];
-    }
-    if (P >= (uint64_t(1) << 31)) throw Fail{TSG_ERR_OTHER, "task list beyond 2^31 pairs needs row-panel batching"};
-    tl.npairs = P;
-    uint64_t* pairs_u = sc.alloc<uint64_t>(P);
-    uint32_t* keys_u = sc.alloc<uint32_t>(P);
-    auto bits_of = [](uint64_t n) {
-      uint32_t b = 0;
-      while ((uint64_t(1) << b) < n) ++b;
-      return b;
-    };
-    const uint32_t jbits = bits_of(B.tile_cols), ibits = bits_of(TA.tile_rows);
-    // the tile row rides in the key's high bits when it fits (radix sort);
-    // otherwise keys are the column alone (segmented sort per tile row)
-    // Sort choice (measured): tile rows holding thousands of pairs each
-    // (R-MAT) sort fastest per tile row over just the column bits; shorter
-    // rows (rect, AMG) as one global radix sort over (row, column) keys.
-    // Sort choice (measured): tile rows holding thousands of pairs each
-    // (R-MAT) sort fastest per tile row over just the column bits; shorter
-    // rows (rect, AMG) as one global radix sort over (row, column) keys.  (A
-    // block-per-tile-row shared-memory sort measured 1.64 ms on rect, no
-    // better than the global radix.)
-    const bool long_rows = P >= 4096ull * TA.tile_rows;
-    const int sort_variant = tuning_variant("TSG_SORT", long_rows ? 1 : 0);
-    const bool radix = jbits + ibits <= 32 && sort_variant == 0;
-    launch_enum_fill(TA, B, tA, tile_off, pairs_u, keys_u, radix ? jbits : 32, s);
-    check_launch(ctx);
-    record(ctx, timing, 2);
-    // stable sort by output tile column within each tile row
-    uint64_t* pairs = sc.alloc<uint64_t>(P + 1);
-    uint32_t* keys = sc.alloc<uint32_t>(P);
-    if (P > 0 && radix) {
-      // keys are (tile row << jbits | tile col): one stable LSD radix sort of
-      // just the key bits in use (tiles are enumerated in row order, so this
-      // is the per-tile-row sort by output column, k order kept by stability)
-      size_t bytes = 0;
-      TSG_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, keys_u, keys, pairs_u, pairs, P, 0,
-                                               int(jbits + ibits), s));
-      void* tmp = sc.alloc<char>(bytes);
-      TSG_CUDA(cub::DeviceRadixSort::SortPairs(tmp, bytes, keys_u, keys, pairs_u, pairs, P, 0,
-                                               int(jbits + ibits), s));
-    } else if (P > 0 && sort_variant == 1) {
-      size_t bytes = 0;
-      TSG_CUDA(cub::DeviceSegmentedRadixSort::SortPairs(nullptr, bytes, keys_u, keys, pairs_u, pairs, int(P),
-                                                        int(TA.tile_rows), row_pair_off, row_pair_off + 1, 0,
-                                                        int(jbits), s));
-      void* tmp = sc.alloc<char>(bytes);
-      TSG_CUDA(cub::DeviceSegmentedRadixSort::SortPairs(tmp, bytes, keys_u, keys, pairs_u, pairs, int(P),
-                                                        int(TA.tile_rows), row_pair_off, row_pair_off + 1, 0,
-                                                        int(jbits), s));
-    } else if (P > 0) {
-      size_t bytes = 0;
-      TSG_CUDA(cub::DeviceSegmentedSort::StableSortPairs(nullptr, bytes, keys_u, keys, pairs_u, pairs, int(P),
-                                                         int(TA.tile_rows), row_pair_off, row_pair_off + 1, s));
-      void* tmp = sc.alloc<char>(bytes);
-      TSG_CUDA(cub::DeviceSegmentedSort::StableSortPairs(tmp, bytes, keys_u, keys, pairs_u, pairs, int(P),
-                                                         int(TA.tile_rows), row_pair_off, row_pair_off + 1, s));
-    }
-    auto* row_nseg = sc.alloc<uint32_t>(nr);
-    TSG_CUDA(cudaMemsetAsync(row_nseg + nr - 1, 0, sizeof(uint32_t), s));
-    const uint32_t jmask = jbits >= 32 ? 0xffffffffu : (1u << jbits) - 1u;
-    launch_seg_count(TA, row_pair_off, keys, row_nseg, s);
-    check_launch(ctx);
-    // per-pair operand metas and staging bounds need only the sorted pairs:
-    // launched before the segment count is read, so one synchronisation
-    // returns both the segment count and the staging total
-    tl.pmeta = sc.alloc<uint4>(P + 1);
-    tl.pocc = sc.alloc<uint2>(P + 1);
-    auto* pair_bound = sc.alloc<uint32_t>(P + 1);
-    launch_pair_meta(TA, B, pairs, tl, pair_bound, s);
-    check_launch(ctx);
-    {
-      auto* t_d = sc.alloc<unsigned long long>(2);
-      TSG_CUDA(cudaMemsetAsync(t_d, 0, 2 * sizeof(unsigned long long), s));
-      const unsigned b1 = unsigned(std::min<uint64_t>((nr + 255) / 256, 1184));
-      const unsigned b2 = unsigned(std::min<uint64_t>((P + 255) / 256, 1184));
-      if (nr) sum_u32_kernel<<<b1, 256, 0, s>>>(row_nseg, nr, t_d);
-      if (P) sum_u32_kernel<<<b2, 256, 0, s>>>(pair_bound, P, t_d + 1);
+    EscArgs g;
+    g.rowsA = rows;
+    g.tile_rows = TA.tile_rows;
+    g.target = uint32_t(std::max(256, tuning_variant("TSG_ESC_TARGET", int(kEscTarget))));
+    int64_t nnzA = 0;
+    if (pre_a) {  // the previous stage's A tiles -> CSR with binary16 values
+      auto* rp = sc.alloc<int64_t>(rows + 1);
+      TSG_CUDA(cudaMemsetAsync(rowcnt + rows, 0, sizeof(int64_t), s));
+      launch_tiles_rowcount(TA, rowcnt, s);
+      exclusive_sum(ctx, sc, rowcnt, rp, uint64_t(rows) + 1);
+      nnzA = int64_t(readback(ctx, rp + rows));
+      auto* col = sc.alloc<int32_t>(nnzA);
+      auto* h = sc.alloc<uint16_t>(nnzA);
+      launch_tiles_to_csr(TA, rp, col, h, s);
       check_launch(ctx, 2);
-      const unsigned long long* src[2] = {t_d, t_d + 1};
-      unsigned long long v[2];
-      readback_many(ctx, src, v);
-      S = v[0];
-      stage_total = v[1];
+      g.rpA = rp;
+      g.colA = col;
+      g.hA = h;
+    } else {
+      nnzA = dA.nnz;
+      g.rpA = dA.row_ptr;
+      g.colA = dA.col;
+      g.hA = TA.h16;
     }
-    check_stage_total();
-    exclusive_sum(ctx, sc, row_nseg, tl.seg_row_ptr, nr);
-    tl.nseg = S;
-    tl.seg_off = sc.alloc<uint32_t>(S + 1);
-    tl.seg_col = sc.alloc<uint32_t>(S);
-    tl.stage_off = sc.alloc<uint32_t>(S + 1);
-    TSG_CUDA(cudaMemcpyAsync(tl.seg_off + S, row_pair_off + nr - 1, 4, cudaMemcpyDeviceToDevice, s));
-    launch_seg_fill(TA, row_pair_off, keys, jmask, tl, s);
+    g.colsB = Bin->cols;
+    g.rpB = dB.row_ptr;
+    g.colB = dB.col;
+    g.hB = B.h16;
+    // B row records {first entry, end, first col, last col}: one gather per A entry
+    auto* brec = sc.alloc<uint4>(uint64_t(std::max<int64_t>(Bin->rows, 1)));
+    launch_esc_brec(g, Bin->rows, brec, s);
+    g.brec = brec;
+    // (1) product histogram over output columns -> its prefix G (heavy-row cuts)
+    const uint64_t inner = uint64_t(std::max<int64_t>(Bin->rows, 1));
+    auto* colcnt = sc.alloc<uint32_t>(inner);
+    TSG_CUDA(cudaMemsetAsync(colcnt, 0, inner * sizeof(uint32_t), s));
+    const uint64_t nc1 = uint64_t(Bin->cols) + 1;
+    auto* hist = sc.alloc<unsigned long long>(nc1);
+    TSG_CUDA(cudaMemsetAsync(hist, 0, nc1 * sizeof(unsigned long long), s));
+    launch_esc_hist(g, nnzA, Bin->rows, colcnt, hist, s);
+    check_launch(ctx, 3);
+    auto* G = sc.alloc<unsigned long long>(nc1);
+    exclusive_sum(ctx, sc, hist, G, nc1);
+    // (2) products per tile row -> units (groups of light rows, column ranges
+    // of heavy rows) and output records; tile-pair statistics
+    // tot: [0] products, [1] segments, [2] raw pairs, [3] filtered pairs, [4] pool pieces (u32)
+    auto* tot = sc.alloc<unsigned long long>(8);
+    TSG_CUDA(cudaMemsetAsync(tot, 0, 8 * sizeof(unsigned long long), s));
+    auto* prod = sc.alloc<unsigned long long>(nr);
+    TSG_CUDA(cudaMemsetAsync(prod + nr - 1, 0, sizeof(unsigned long long), s));
+    launch_esc_plan_prod(g, prod, tot, s);
     check_launch(ctx);
-    auto* pair_stage = sc.alloc<uint32_t>(P + 1);
-    exclusive_sum(ctx, sc, pair_bound, pair_stage, P + 1);
-    launch_seg_stage(tl, pair_stage, s);
+    auto* ppre = sc.alloc<unsigned long long>(nr);
+    exclusive_sum(ctx, sc, prod, ppre, nr);
+    auto* nrec = sc.alloc<uint32_t>(nr);
+    auto* nwk = sc.alloc<uint32_t>(nr);
+    TSG_CUDA(cudaMemsetAsync(nrec + nr - 1, 0, sizeof(uint32_t), s));
+    TSG_CUDA(cudaMemsetAsync(nwk + nr - 1, 0, sizeof(uint32_t), s));
+    launch_esc_plan_group(g, ppre, nrec, nwk, s);
+    check_launch(ctx);
+    auto* rbase = sc.alloc<uint32_t>(nr);
+    auto* wbase = sc.alloc<uint32_t>(nr);
+    exclusive_sum(ctx, sc, nrec, rbase, nr);
+    exclusive_sum(ctx, sc, nwk, wbase, nr);
+    auto* njt = sc.alloc<uint32_t>(uint64_t(B.rows) + 1);
+    launch_esc_pairstats(TA, B, tA, njt, tot + 2, s);
+    check_launch(ctx, 2);
+    record(ctx, timing, 2);
+    uint64_t nrecs = 0, nunits = 0, products = 0;
+    {
+      ScalarGather sg;
+      sg.p[0] = rbase + nr - 1;
+      sg.p[1] = wbase + nr - 1;
+      sg.p[2] = tot;
+      sg.wide = 0x4u;
+      sg.n = 3;
+      unsigned long long v[3];
+      readback_gather(ctx, sc, sg, v);
+      nrecs = v[0];
+      nunits = v[1];
+      products = v[2];
+    }
+    auto* units = sc.alloc<uint4>(nunits);
+    launch_esc_plan_fill(g, ppre, nwk, wbase, G, units, s);
     check_launch(ctx);
     record(ctx, timing, 3);
-    record(ctx, timing, 4);  // the counting pass is fused into the numeric kernels
-
-    // numeric: counting + SEaC multiply -> staged tiles
-    Staged sg;
-    sg.val = static_cast<float*>(arena(stage_total * sizeof(float)));
-    sg.rmask = sc.alloc<uint16_t>(S * 16);
-    sg.counted = counted_d;
-    if (timing) TSG_CUDA(cudaEventRecord(ctx->kev[0], s));
-    // thin segments: thread each; the rest: warp each, from a compacted list
-    auto* heavy = sc.alloc<uint8_t>(S);
-    auto* list = sc.alloc<uint32_t>(S);
-    auto* list_len = sc.alloc<uint32_t>(1);
-    TSG_CUDA(cudaMemsetAsync(list_len, 0, sizeof(uint32_t), s));
-    launch_numeric_thin(tl, TA, B, sg, heavy, s);
-    check_launch(ctx);
-    if (S > 0) {
-      cub::CountingInputIterator<uint32_t> ids(0);
-      size_t bytes = 0;
-      TSG_CUDA(cub::DeviceSelect::Flagged(nullptr, bytes, ids, heavy, list, list_len, int64_t(S), s));
-      void* tmp = sc.alloc<char>(bytes);
-      TSG_CUDA(cub::DeviceSelect::Flagged(tmp, bytes, ids, heavy, list, list_len, int64_t(S), s));
+    record(ctx, timing, 4);
+    // (3) multiply: staging for every product (realised entries <= products)
+    auto* ctr = sc.alloc<unsigned long long>(2);  // [0] work counter (u32), [1] staging top
+    g.units = units;
+    g.nunits = wbase + nr - 1;
+    g.rec_base = rbase;
+    g.nrec = rbase + nr - 1;
+    g.stage = static_cast<uint2*>(arena(std::max<uint64_t>(products, 1) * sizeof(uint2)));
+    g.err_flag = err_flag;
+    g.counted = counted_d;
+    g.segs = tot + 1;
+    g.piece_top = reinterpret_cast<uint32_t*>(tot + 4);
+    g.work = reinterpret_cast<unsigned*>(ctr);
+    g.stage_top = ctr + 1;
+    uint64_t pool = std::max<uint64_t>(4096, nunits / 8);
+    unsigned long long t[4];
+    for (int attempt = 0;; ++attempt) {
+      g.pool_cap = uint32_t(std::min<uint64_t>(pool, 0xfffffff0ull - nrecs));
+      g.pieces = sc.alloc<EscPiece>(nrecs + g.pool_cap);
+      TSG_CUDA(cudaMemsetAsync(ctr, 0, 2 * sizeof(unsigned long long), s));
+      if (timing) TSG_CUDA(cudaEventRecord(ctx->kev[0], s));
+      launch_esc(g, ctx->device, s);
+      check_launch(ctx);
+      if (timing) TSG_CUDA(cudaEventRecord(ctx->kev[1], s));
+      record(ctx, timing, 5);
+      launch_esc_rowcount(g, rbase, rowcnt, s);
+      check_launch(ctx);
+      scan_rows(tot + 1, t);
+      if (t[3] <= g.pool_cap || attempt > 8) break;
+      // the overflow-piece pool was too small (pathological column skew): rerun
+      pool = t[3] * 2;
+      TSG_CUDA(cudaMemsetAsync(counted_d, 0, sizeof(unsigned long long), s));
+      TSG_CUDA(cudaMemsetAsync(tot + 1, 0, sizeof(unsigned long long), s));
+      TSG_CUDA(cudaMemsetAsync(tot + 4, 0, sizeof(unsigned long long), s));
+      TSG_CUDA(cudaMemsetAsync(err_flag, 0, sizeof(unsigned), s));
     }
-    launch_numeric(tl, TA, B, sg, opt.mode, list, list_len, s);
-    check_launch(ctx);
-    if (timing) TSG_CUDA(cudaEventRecord(ctx->kev[1], s));
-    record(ctx, timing, 5);
-
-    // tiled -> CSR: segment chunks, realised (chunk, row) counts, scan, assembly
-    AsmChunks ch;
-    const uint64_t max_chunks = uint64_t(TA.tile_rows) + S / kChunkSegs + 1;
-    ch.n = sc.alloc<uint32_t>(1);
-    ch.tile_row = sc.alloc<uint32_t>(max_chunks);
-    ch.seg_begin = sc.alloc<uint32_t>(max_chunks);
-    ch.seg_end = sc.alloc<uint32_t>(max_chunks);
-    ch.off = sc.alloc<uint32_t>(max_chunks * 16);
-    auto* nchunks = sc.alloc<uint32_t>(nr);
-    auto* chunk_base = sc.alloc<uint32_t>(nr);
-    TSG_CUDA(cudaMemsetAsync(nchunks + nr - 1, 0, 4, s));
-    launch_asm_chunks(TA.tile_rows, tl.seg_row_ptr, nchunks, s);
-    exclusive_sum(ctx, sc, nchunks, chunk_base, nr);
-    launch_asm_chunk_fill(TA.tile_rows, tl.seg_row_ptr, chunk_base, ch, s);
-    TSG_CUDA(cudaMemsetAsync(rowcnt, 0, (rows + 1) * sizeof(int64_t), s));
-    launch_row_counts(rows, ch, max_chunks, sg, rowcnt, s);
-    check_launch(ctx, 3);
-    scan_rows();
+    S = t[0];
+    raw = t[1];
+    P = t[2];
+    stage_total = products;
     alloc_out();
-    launch_chunk_offsets(rows, TA.tile_rows, chunk_base, d_rp, ch, s);
-    check_launch(ctx);
     if (timing) TSG_CUDA(cudaEventRecord(ctx->kev[2], s));
-    launch_assemble(rows, ch, max_chunks, tl, sg, d_col, d_val, err_flag, s);
+    launch_esc_copy(g, d_rp, d_col, d_val, s);
     check_launch(ctx);
     if (timing) TSG_CUDA(cudaEventRecord(ctx->kev[3], s));
     record(ctx, timing, 6);

@@ -54,6 +54,9 @@ struct TileMat {
   // the input row pointers -- single-column A tiles enumerate through them
   uint32_t* etile = nullptr;
   const int64_t* csr_rp = nullptr;
+  // per input CSR entry: its rounded binary16 value (0 when dropped) -- the
+  // general path multiplies straight from the CSR
+  uint16_t* h16 = nullptr;
   uint2* meta[2] = {nullptr, nullptr};
   uint4* rec[2] = {nullptr, nullptr};  // {lane mask, first chunk, occupancy, tile column}: one gather per tile
   uint4* chunk[2] = {nullptr, nullptr};
@@ -96,6 +99,7 @@ enum ErrBits : unsigned {
   kErrOverflow = 2u,   // |x| > 65504 or non-finite input
   kErrPrecision = 4u,  // non-finite accumulator
   kCancelled = 8u,     // an output slot cancelled to exactly 0 (compaction needed)
+  kErrPool = 16u,      // general path: the overflow-piece pool was too small (the host reruns)
 };
 
 __device__ __forceinline__ unsigned lanemask_lt() {

@@ -118,6 +118,7 @@ struct Gapped {
   uint4* rec[2] = {nullptr, nullptr};  // {lane mask, first chunk, occupancy, tile col}
   uint4* chunk[2] = {nullptr, nullptr};
   uint32_t* etile = nullptr;  // per entry: tile rank within its tile row | kDupEntry, or kNoTile
+  uint16_t* h16 = nullptr;    // per entry: rounded binary16 value, 0 when dropped
   uint32_t* ntiles = nullptr;  // per tile row
   uint8_t* mark = nullptr;     // optional: mark[J] = 1 for every tile column J (the B tile rows A needs)
 };
@@ -383,6 +384,7 @@ __global__ void __launch_bounds__(256, 4) convert_fast_kernel(CsrView in, uint32
       keep = keep && !skip && c[u] >= 0 && c[u] < in.cols && (wide || j < uint32_t(kBitW) * 32u);
       if (keep && !wide) atomicOr(&sm.bits[j >> 5], 1u << (j & 31));
       if (!keep && out.etile) out.etile[E0 + q] = kNoTile;
+      if (out.h16) out.h16[E0 + q] = keep ? h : uint16_t(0);
       pk[u] = uint32_t(h) | (uint32_t(r) << 16) | (keep ? 1u << 20 : 0u);
     }
   }
@@ -635,6 +637,7 @@ __global__ void __launch_bounds__(256) convert_walk_kernel(CsrView in, Gapped ou
         bool keep;
         load_half<kDtype>(in.val, q, drop_nonfinite, err, keep);
         if (out.etile) out.etile[q] = kNoTile;
+        if (out.h16) out.h16[q] = 0;
       }
       const unsigned e = __reduce_or_sync(kFull, err);
       if (lane == 0) {
@@ -665,6 +668,7 @@ __global__ void __launch_bounds__(256) convert_walk_kernel(CsrView in, Gapped ou
         bool keep;
         const unsigned short h = load_half<kDtype>(in.val, p, drop_nonfinite, err, keep);
         keep = keep && c >= 0 && c < in.cols;  // out-of-range columns (flagged) never form tiles
+        if (out.h16) out.h16[p] = keep ? h : (unsigned short)0;
         if (keep) {
           rm |= 1u << (c & 15);
           st[lane * 16 + (c & 15)] = h;
@@ -800,6 +804,7 @@ void launch_convert(const CsrView& in, TileMat& out, int roles, const ConvertScr
   g.chunk[0] = out.chunk[0];
   g.chunk[1] = out.chunk[1];
   g.etile = out.etile;
+  g.h16 = out.h16;
   g.ntiles = cs.ntiles;
   g.mark = cs.mark;
   auto kf = in.dtype == 0 ? convert_fast_kernel<0> : in.dtype == 2 ? convert_fast_kernel<2> : convert_fast_kernel<1>;

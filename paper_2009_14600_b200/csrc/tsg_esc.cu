@@ -1,0 +1,1068 @@
+// tsg_esc.cu -- general rows: the tSparse symbolic + SEaC numeric phases for
+// tile rows of A with more than 32 tiles (R-MAT, the rectangular product,
+// the second AMG stage), fused per work unit in shared memory.
+//
+// GPU restatement at T = 16 of
+//   enumerate_pairs / filter_zero_products  proj/src/pipeline.cpp:37-70
+//   sort_and_segment                        proj/src/pipeline.cpp:72-109
+//   counting_pass                           proj/src/kernels.cpp:79-103
+//   expand_tile / tile_mm_reference         proj/src/kernels.cpp:17-38
+//   multiply_pass / finalize_segment        proj/src/kernels.cpp:105-203
+//   compact + to_element_coo                proj/src/kernels.cpp:205-220,
+//                                           proj/src/tile_format.cpp:131-154
+// On these matrices a tile holds ~1 nonzero, so a tile pair is ~1 product:
+// the tile pairs of a unit are expanded straight into their element products
+// (r, c, a*b) -- the "expand" of SEaC, done at enumeration -- and radix-sorted
+// in shared memory by the output tile key (tile row, J, in-tile column,
+// in-tile row), stable, so products of one slot keep ascending k.  Runs of
+// equal (tile row, J) are the segments (output tiles, sort_and_segment);
+// runs of equal slot are summed in that order with one fp32 rounding per
+// product (tile_mm_reference: bit-identical to the reference in both numeric
+// modes); sums != 0 are the realised bitmap (finalize_segment / compact()),
+// written row-major, one piece per tile row.  No task list reaches HBM.
+//
+// Work units: up to 16 aligned light tile rows whose products fit one sort
+// (kCap), or one column range of a heavy tile row (cut at quantiles of the
+// global product-column distribution, 16-aligned so segment counts add up).
+// A heavy unit whose products exceed kCap anyway is halved by column until it
+// fits, or becomes a dense ordered leaf (<= 256 columns).
+//
+//   esc_brec        B row records {first entry, end, first col, last col}
+//   esc_colcount/colhist/scan   product histogram over output columns -> G
+//   esc_plan_prod/scan/group/fill   units and output records
+//   esc_kernel      persistent CTAs over the units
+//   esc_rowcount / scan / esc_copy   pieces -> CSR
+//   esc_njt / esc_pairstats         raw and filtered tile-pair counts
+#include <algorithm>
+
+#include "tsg_kernels.cuh"
+
+namespace tsg {
+
+namespace {
+
+constexpr int kNT = kEscThreads;  // threads per CTA
+constexpr int kWarps = kNT / 32;
+constexpr int kMaxIPT = 16;             // products per thread, at most
+constexpr int kCap = kNT * kMaxIPT;     // products per sorted leaf
+constexpr int kGroup = 16;              // light tile rows per unit, at most
+constexpr uint32_t kDenseW = 256;       // columns of a dense leaf (16 x 256 accumulators)
+constexpr uint32_t kMaxWidth = 1u << 28;  // sorted-leaf width: J < 2^24 keeps the key in 32 bits
+constexpr uint32_t kGroupFlag = 0x80000000u;
+
+struct EscSmem {
+  union {
+    // the leaf's A entries with products in range (compacted): {first B
+    // entry in range, products << 8 | row within the unit (16 b + r), product
+    // prefix, A value (fp32 bits)}; entry ne is the sentinel {-, -, P, -}
+    uint4 t[kCap + 1];
+    struct {
+      uint32_t key[kCap];  // products: blocked, vectors rotated (phys())
+      float val[kCap];
+      union {
+        uint32_t ctr[8 * kNT + 8 * kNT / 32];  // radix digit counters, [digit pair][thread], padded
+        struct {                               // realised entries, staging order, padded
+          uint32_t col[kCap + kCap / 32];
+          float val[kCap + kCap / 32];
+        } o;
+      } x;
+    } s;
+    struct {
+      float acc[16 * kDenseW];
+      uint8_t flag[16 * kDenseW];
+    } d;
+  };
+  int64_t rowp[kGroup * 16 + 1];
+  int32_t adj[256];   // staging index - realised rank, per (r, b)
+  uint32_t cnt[256];  // realised entries per (b, r)
+  uint32_t wsum[2 * kWarps];
+  uint32_t stk[80];
+  uint32_t bc[16];
+};
+
+__device__ __forceinline__ uint32_t half_nz(uint16_t h) { return h & 0x7fffu; }
+__device__ __forceinline__ uint32_t cpad(uint32_t L) { return L + (L >> 5); }
+__device__ __forceinline__ uint32_t opad(uint32_t o) { return o + (o >> 5); }
+
+// Blocked layout: thread t owns items IPT t .. IPT t + IPT-1; its 16-byte
+// vectors are rotated so an LDS.128 phase of 8 lanes hits 8 bank groups.
+template <int IPT>
+__device__ __forceinline__ uint32_t phys(uint32_t g) {
+  constexpr uint32_t NV = IPT / 4;
+  if (NV == 1) return g;
+  const uint32_t t = g / IPT, i = g % IPT, q = i >> 2;
+  const uint32_t rot = NV == 4 ? ((t >> 1) & 3u) : ((t >> 2) & 1u);
+  return t * IPT + (((q + rot) & (NV - 1)) << 2) + (i & 3u);
+}
+
+// exclusive block scan of two u32 (totals in ta, tb)
+__device__ __forceinline__ void block_scan2(EscSmem& sm, uint32_t& a, uint32_t& b, uint32_t& ta, uint32_t& tb) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  uint32_t ia = a, ib = b;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t va = __shfl_up_sync(kFull, ia, o), vb = __shfl_up_sync(kFull, ib, o);
+    if (lane >= o) {
+      ia += va;
+      ib += vb;
+    }
+  }
+  if (lane == 31) {
+    sm.wsum[w] = ia;
+    sm.wsum[kWarps + w] = ib;
+  }
+  __syncthreads();
+  uint32_t pa = 0, pb = 0;
+  ta = 0;
+  tb = 0;
+#pragma unroll
+  for (int i = 0; i < kWarps; ++i) {
+    const uint32_t x = sm.wsum[i], y = sm.wsum[kWarps + i];
+    if (i < w) {
+      pa += x;
+      pb += y;
+    }
+    ta += x;
+    tb += y;
+  }
+  a = pa + ia - a;
+  b = pb + ib - b;
+  __syncthreads();
+}
+
+// One stable LSD pass on the 4-bit digit at `shift` over the valid items
+// (mask vm) in registers: per-thread digit counts as 4-bit fields of a u64,
+// a raking scan of the [digit][thread] counters, scatter, blocked reload.
+// Returns the item count (dense from now on).
+template <int IPT>
+__device__ __forceinline__ uint32_t radix_pass(EscSmem& sm, uint32_t (&key)[IPT], float (&val)[IPT], uint32_t vm,
+                                               int shift) {
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  unsigned long long C = 0, rk = 0;
+  uint32_t nv = 0, d0 = 0;
+#pragma unroll
+  for (int i = 0; i < IPT; ++i) {
+    if ((vm >> i) & 1u) {
+      const uint32_t s = ((key[i] >> shift) & 15u) << 2;
+      if (nv == 0) d0 = s;
+      rk |= ((C >> s) & 15ull) << (4 * i);
+      C += 1ull << s;
+      ++nv;
+    }
+  }
+  uint32_t w8[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) w8[j] = uint32_t((C >> (4 * j)) & 15u) | (uint32_t((C >> (4 * j + 32)) & 15u) << 16);
+  if (IPT == 16 && nv == 16 && C == (d0 == 60 ? 0ull : (1ull << (d0 + 4)))) {
+    // all 16 items share digit d: its count (16) carried out of the 4-bit field
+    const uint32_t d = d0 >> 2;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) w8[j] = uint32_t(j) == (d & 7u) ? (16u << (16 * (d >> 3))) : 0u;
+  }
+#pragma unroll
+  for (int j = 0; j < 8; ++j) sm.s.x.ctr[cpad(j * kNT + tid)] = w8[j];
+  __syncthreads();
+  // raking: thread t sums the linear counters 8t .. 8t+7 (digit-major order)
+  uint32_t v[8], sum = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    v[i] = sm.s.x.ctr[cpad(8 * tid + i)];
+    sum += v[i];
+  }
+  uint32_t inc = sum;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(kFull, inc, o);
+    if (lane >= o) inc += y;
+  }
+  if (lane == 31) sm.wsum[w] = inc;
+  __syncthreads();
+  uint32_t run = inc - sum, T = 0;
+#pragma unroll
+  for (int i = 0; i < kWarps; ++i) {
+    const uint32_t y = sm.wsum[i];
+    if (i < w) run += y;
+    T += y;
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    sm.s.x.ctr[cpad(8 * tid + i)] = run;
+    run += v[i];
+  }
+  __syncthreads();
+  const uint32_t tlo = T & 0xffffu;  // items with digits 0..7: the base of digit 8
+#pragma unroll
+  for (int i = 0; i < IPT; ++i) {
+    if ((vm >> i) & 1u) {
+      const uint32_t d = (key[i] >> shift) & 15u;
+      const uint32_t p = sm.s.x.ctr[cpad((d & 7u) * kNT + tid)];
+      const uint32_t dst = (d < 8 ? (p & 0xffffu) : (p >> 16) + tlo) + uint32_t((rk >> (4 * i)) & 15u);
+      const uint32_t q = phys<IPT>(dst);
+      sm.s.key[q] = key[i];
+      sm.s.val[q] = val[i];
+    }
+  }
+  __syncthreads();
+  const uint4* k4 = reinterpret_cast<const uint4*>(sm.s.key) + tid * (IPT / 4);
+  const float4* v4 = reinterpret_cast<const float4*>(sm.s.val) + tid * (IPT / 4);
+#pragma unroll
+  for (int q = 0; q < IPT / 4; ++q) {
+    const uint32_t rot = IPT == 16 ? ((uint32_t(tid) >> 1) & 3u) : IPT == 8 ? ((uint32_t(tid) >> 2) & 1u) : 0u;
+    const uint32_t pq = (q + rot) & (IPT / 4 - 1);
+    const uint4 kk = k4[pq];
+    const float4 vv = v4[pq];
+    key[4 * q] = kk.x;
+    key[4 * q + 1] = kk.y;
+    key[4 * q + 2] = kk.z;
+    key[4 * q + 3] = kk.w;
+    val[4 * q] = vv.x;
+    val[4 * q + 1] = vv.y;
+    val[4 * q + 2] = vv.z;
+    val[4 * q + 3] = vv.w;
+  }
+  return tlo + (T >> 16);
+}
+
+template <int IPT>
+__device__ __forceinline__ uint32_t valid_mask(uint32_t n) {
+  const uint32_t g0 = threadIdx.x * IPT;
+  if (n <= g0) return 0u;
+  const uint32_t k = n - g0;
+  return k >= uint32_t(IPT) ? (1u << IPT) - 1u : (1u << k) - 1u;
+}
+
+// first B entry of [b0, b1) with column >= c
+__device__ __forceinline__ uint32_t lower_col(const int32_t* __restrict__ colB, uint32_t b0, uint32_t b1, uint32_t c) {
+  while (b0 < b1) {
+    const uint32_t m = (b0 + b1) >> 1;
+    if (uint32_t(__ldg(colB + m)) < c)
+      b0 = m + 1;
+    else
+      b1 = m;
+  }
+  return b0;
+}
+
+struct Unit {
+  uint32_t I, lo, hi, nb, rec0;  // first tile row, column range, tile rows, first output record
+};
+
+// Output records of a unit (thread 0's chain state for a heavy unit).
+struct PieceChain {
+  uint32_t prev = kNoPiece;  // last record written by this unit
+};
+
+// The leaf's realised entries are in sm.s.x.o (staging order, n of them),
+// counts per (b, r) in sm.cnt: staging + records.  All threads.
+__device__ void write_pieces(EscSmem& sm, const EscArgs& g, const Unit& u, uint32_t n, PieceChain& pc) {
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    const unsigned long long base = n ? atomicAdd(g.stage_top, (unsigned long long)n) : 0ull;
+    uint32_t rec = kNoPiece;
+    if (u.nb > 1 || pc.prev == kNoPiece) {
+      rec = u.rec0;
+    } else if (n > 0) {  // a later leaf of a halved heavy unit: a pool piece chained after the last
+      const uint32_t slot = atomicAdd(g.piece_top, 1u);
+      if (slot < g.pool_cap)
+        rec = *g.nrec + slot;
+      else
+        atomicOr(g.err_flag, unsigned(kErrPool));
+    }
+    if (u.nb == 1 && rec != kNoPiece) {
+      if (pc.prev != kNoPiece) g.pieces[pc.prev].next = rec;
+      pc.prev = rec;
+    }
+    sm.bc[0] = rec;
+    sm.bc[2] = uint32_t(base);
+    sm.bc[3] = uint32_t(base >> 32);
+  }
+  __syncthreads();
+  const uint32_t rec = sm.bc[0];
+  const unsigned long long base = (unsigned long long)sm.bc[2] | ((unsigned long long)sm.bc[3] << 32);
+  if (rec != kNoPiece && tid < int(u.nb)) {  // thread b: the record of tile row I + b
+    EscPiece& p = g.pieces[rec + tid];
+    uint32_t off = 0;
+    for (int b = 0; b < tid; ++b)
+      for (int r = 0; r < 16; ++r) off += sm.cnt[b * 16 + r];
+    p.I = u.I + tid;
+    p.next = kNoPiece;
+    p.off = base + off;
+#pragma unroll
+    for (int r = 0; r < 16; ++r) p.cnt[r] = sm.cnt[tid * 16 + r];
+  }
+  if (rec != kNoPiece)
+    for (uint32_t o = tid; o < n; o += kNT) {
+      const uint32_t q = opad(o);
+      g.stage[base + o] = make_uint2(sm.s.x.o.col[q], __float_as_uint(sm.s.x.o.val[q]));
+    }
+  __syncthreads();
+}
+
+// The leaf's entry table; false (nothing built) when its products exceed kCap.
+__device__ bool build_table(EscSmem& sm, const EscArgs& g, const Unit& u, uint32_t lo, uint32_t hi,
+                            uint32_t& P, uint32_t& ne) {
+  const int tid = threadIdx.x;
+  const int nrow = 16 * int(u.nb);
+  const int64_t E0 = sm.rowp[0], E1 = sm.rowp[nrow];
+  const bool full = lo == 0 && int64_t(hi) >= g.colsB;
+  P = 0;
+  ne = 0;
+  for (int64_t e0 = E0; e0 < E1; e0 += kNT) {
+    const int64_t e = e0 + tid;
+    uint32_t len = 0, blo = 0, br = 0;
+    uint16_t a = 0;
+    if (e < E1) {
+      a = __ldg(g.hA + e);
+      if (half_nz(a)) {
+        const uint4 rb = __ldg(g.brec + __ldg(g.colA + e));  // {first entry, end, first col, last col}
+        blo = rb.x;
+        uint32_t bhi = rb.y;
+        if (!full && bhi > blo) {
+          if (rb.z >= hi || rb.w < lo) {
+            bhi = blo;
+          } else {
+            if (rb.z < lo) blo = lower_col(g.colB, blo, bhi, lo);
+            if (rb.w >= hi) bhi = lower_col(g.colB, blo, bhi, hi);
+          }
+        }
+        len = bhi - blo;
+        for (int b = 128; b > 0; b >>= 1)  // row within the unit: last rowp <= e
+          if (int(br) + b < nrow && sm.rowp[br + b] <= e) br += b;
+      }
+    }
+    const uint32_t f0 = len > 0 ? 1u : 0u, l0 = len < uint32_t(kCap) ? len : uint32_t(kCap) + 1u;
+    uint32_t f = f0, lc = l0, ft, lt;
+    block_scan2(sm, f, lc, ft, lt);
+    if (P + lt > uint32_t(kCap)) return false;
+    if (f0) sm.t[ne + f] = make_uint4(blo, (l0 << 8) | br, P + lc, __float_as_uint(__half2float(__ushort_as_half(a))));
+    ne += ft;
+    P += lt;
+  }
+  if (tid == 0) sm.t[ne] = make_uint4(0u, 0u, P, 0u);
+  __syncthreads();
+  return true;
+}
+
+// Sorted leaf: expand, sort by (tile row, J, cc, r), segments, combine, write.
+template <int IPT>
+__device__ void sort_leaf(EscSmem& sm, const EscArgs& g, const Unit& u, uint32_t lo, uint32_t hi, uint32_t P,
+                          uint32_t ne, PieceChain& pc, unsigned long long& segs, unsigned long long& structural) {
+  const int tid = threadIdx.x, lane = tid & 31;
+  const uint32_t jr = (hi - lo + 15u) >> 4;  // tile columns of the leaf
+  int jb = 0;
+  while ((1u << jb) < jr) ++jb;
+  const int bshift = 8 + jb;  // tile row within the unit above J
+  // ---- expand: thread t generates products IPT t .. IPT t + IPT-1
+  uint32_t key[IPT];
+  float val[IPT];
+  uint32_t vm = 0;
+  const uint32_t g0 = uint32_t(tid) * IPT;
+#pragma unroll
+  for (int i = 0; i < IPT; ++i) {
+    key[i] = 0;
+    val[i] = 0.f;
+  }
+  if (g0 < P) {
+    uint32_t e = 0, top = ne;  // largest e with pre[e] <= g0
+    while (top - e > 1) {
+      const uint32_t m = (e + top) >> 1;
+      if (sm.t[m].z <= g0)
+        e = m;
+      else
+        top = m;
+    }
+    uint4 te = sm.t[e];
+    uint32_t nxt = sm.t[e + 1].z;
+#pragma unroll
+    for (int i = 0; i < IPT; ++i) {
+      const uint32_t gi = g0 + i;
+      if (gi < P) {
+        while (gi >= nxt) {
+          te = sm.t[++e];
+          nxt = sm.t[e + 1].z;
+        }
+        const uint32_t base = te.z, blo = te.x, br = te.y & 0xffu;
+        const float a = __uint_as_float(te.w);
+        const uint32_t idx = blo + (gi - base);
+        const uint32_t c = uint32_t(__ldg(g.colB + idx));
+        const uint16_t hb = __ldg(g.hB + idx);
+        if (half_nz(hb)) {
+          vm |= 1u << i;
+          key[i] = ((br >> 4) << bshift) | (((c - lo) >> 4) << 8) | ((c & 15u) << 4) | (br & 15u);
+          val[i] = __fmul_rn(a, __half2float(__ushort_as_half(hb)));
+        }
+      }
+    }
+  }
+  __syncthreads();  // the table (aliased by the sort buffer) is consumed
+  // ---- sort: cc, J digits, tile row (stable: ascending k survives)
+  uint32_t n = radix_pass<IPT>(sm, key, val, vm, 4);
+  for (int s = 8; s < bshift; s += 4) n = radix_pass<IPT>(sm, key, val, valid_mask<IPT>(n), s);
+  if (u.nb > 1) n = radix_pass<IPT>(sm, key, val, valid_mask<IPT>(n), bshift);
+  // segments: runs of (tile row, J) -- the output tiles of sort_and_segment
+  {
+    const uint32_t vmn = valid_mask<IPT>(n);
+    const uint32_t prev = (g0 > 0 && g0 < n) ? (sm.s.key[phys<IPT>(g0 - 1)] >> 8) : 0xffffffffu;
+    uint32_t heads = 0;
+#pragma unroll
+    for (int i = 0; i < IPT; ++i)
+      if ((vmn >> i) & 1u) heads += (key[i] >> 8) != (i == 0 ? prev : (key[i - 1] >> 8)) ? 1u : 0u;
+    heads = __reduce_add_sync(kFull, heads);
+    if (lane == 0 && heads) atomicAdd(&sm.bc[7], heads);
+  }
+  // ---- row: order (r, tile row, J, cc); a (tile row, r) group is one CSR row slice
+  n = radix_pass<IPT>(sm, key, val, valid_mask<IPT>(n), 0);
+  const uint32_t vmn = valid_mask<IPT>(n);
+  const bool cont = g0 > 0 && g0 < n && sm.s.key[phys<IPT>(g0 - 1)] == key[0];
+  // group index (r, b) of a key: 16 r + b
+  auto rb_of = [&](uint32_t k) { return ((k & 15u) << 4) | (k >> bshift); };
+  auto run_tail = [&](uint32_t kcur, float s) {  // a run continuing into later threads
+    for (uint32_t gg = g0 + IPT; gg < n; ++gg) {
+      const uint32_t q = phys<IPT>(gg);
+      if (sm.s.key[q] != kcur) break;
+      s = __fadd_rn(s, sm.s.val[q]);
+    }
+    return s;
+  };
+  // pass 1: realised entries per (b, r) (runs owned by this thread)
+  if (tid < 256) sm.cnt[tid] = 0;
+  __syncthreads();
+  uint32_t nreal = 0, nstruct = 0;
+  bool bad = false;
+  {
+    bool owned = false;
+    uint32_t kcur = 0, gcur = 0xffffffffu, crun = 0;
+    float s = 0.f;
+    auto close_run = [&](float x) {
+      if (x != 0.0f) {
+        ++nreal;
+        const uint32_t gr = rb_of(kcur);
+        if (gr != gcur) {
+          if (crun) atomicAdd(&sm.cnt[((gcur & 15u) << 4) | (gcur >> 4)], crun);  // sm.cnt is [b][r]
+          gcur = gr;
+          crun = 0;
+        }
+        ++crun;
+      }
+      bad |= !isfinite(x);
+    };
+#pragma unroll
+    for (int i = 0; i < IPT; ++i) {
+      if ((vmn >> i) & 1u) {
+        const bool head = i == 0 ? !cont : key[i] != key[i - 1];
+        if (head) {
+          if (owned) close_run(s);
+          owned = true;
+          kcur = key[i];
+          s = val[i];
+          ++nstruct;
+        } else if (owned) {
+          s = __fadd_rn(s, val[i]);
+        }
+      }
+    }
+    if (owned) close_run(run_tail(kcur, s));
+    if (crun) atomicAdd(&sm.cnt[((gcur & 15u) << 4) | (gcur >> 4)], crun);
+  }
+  if (__any_sync(kFull, bad) && lane == 0) atomicOr(g.err_flag, unsigned(kErrPrecision));
+  nstruct = __reduce_add_sync(kFull, nstruct);
+  if (lane == 0 && nstruct) atomicAdd(&sm.bc[1], nstruct);
+  uint32_t off = nreal, zero = 0, tot, dt;
+  block_scan2(sm, off, zero, tot, dt);  // (its barriers also publish sm.cnt)
+  // staging index = realised rank + adj[r][b]: the unit's tile rows one after
+  // another, each row-major.  Thread t: group (r, b) = (t >> 4, t & 15) for the
+  // rank of its first entry (entries of the groups before it in (r, b) order),
+  // and (b, r) = (t >> 4, t & 15) for its staging index (row-major order)
+  {
+    uint32_t x = sm.cnt[((tid & 15) << 4) | (tid >> 4)], y = sm.cnt[tid], tx, ty;
+    block_scan2(sm, x, y, tx, ty);
+    sm.adj[((tid & 15) << 4) | (tid >> 4)] = int32_t(y);  // (r, b) slot <- staging start of (b, r)
+    __syncthreads();
+    sm.adj[tid] -= int32_t(x);
+  }
+  __syncthreads();
+  // pass 2: write the realised entries at their staging index
+  {
+    bool owned = false;
+    uint32_t kcur = 0, o = off;
+    float s = 0.f;
+    const uint32_t jmask = (1u << jb) - 1u;
+    auto emit = [&](float x) {
+      if (x != 0.0f) {
+        const uint32_t q = opad(uint32_t(int32_t(o) + sm.adj[rb_of(kcur)]));
+        sm.s.x.o.col[q] = lo + (((kcur >> 8) & jmask) << 4) + ((kcur >> 4) & 15u);
+        sm.s.x.o.val[q] = x;
+        ++o;
+      }
+    };
+#pragma unroll
+    for (int i = 0; i < IPT; ++i) {
+      if ((vmn >> i) & 1u) {
+        const bool head = i == 0 ? !cont : key[i] != key[i - 1];
+        if (head) {
+          if (owned) emit(s);
+          owned = true;
+          kcur = key[i];
+          s = val[i];
+        } else if (owned) {
+          s = __fadd_rn(s, val[i]);
+        }
+      }
+    }
+    if (owned) emit(run_tail(kcur, s));
+  }
+  __syncthreads();
+  if (tid == 0) {
+    segs += sm.bc[7];
+    structural += sm.bc[1];
+    sm.bc[7] = 0;
+    sm.bc[1] = 0;
+  }
+  write_pieces(sm, g, u, tot, pc);
+}
+
+// Dense leaf (a heavy unit's <= 256 columns whose products exceed kCap):
+// 16 x 256 fp32 accumulators; warp w owns rows w and w + 8 and walks their A
+// entries in ascending k, lanes over the B row's entries in range -- per slot
+// the products are added in k order (the reference's sequence).
+__device__ void dense_leaf(EscSmem& sm, const EscArgs& g, const Unit& u, uint32_t lo, uint32_t hi, PieceChain& pc,
+                           unsigned long long& segs, unsigned long long& structural) {
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const uint32_t width = hi - lo;
+  for (uint32_t i = tid; i < 16 * kDenseW; i += kNT) {
+    sm.d.acc[i] = 0.f;
+    sm.d.flag[i] = 0;
+  }
+  if (tid == 0) sm.bc[7] = 0;
+  __syncthreads();
+  for (int rr = w; rr < 16; rr += kWarps) {
+    const int64_t e0 = sm.rowp[rr], e1 = sm.rowp[rr + 1];
+    for (int64_t e = e0; e < e1; ++e) {
+      const uint16_t a = __ldg(g.hA + e);
+      if (!half_nz(a)) continue;
+      const uint4 rb = __ldg(g.brec + __ldg(g.colA + e));
+      const uint32_t blo = lower_col(g.colB, rb.x, rb.y, lo), bhi = lower_col(g.colB, blo, rb.y, hi);
+      const float af = __half2float(__ushort_as_half(a));
+      for (uint32_t j = blo + lane; j < bhi; j += 32) {
+        const uint16_t hb = __ldg(g.hB + j);
+        if (!half_nz(hb)) continue;
+        const uint32_t slot = uint32_t(rr) * kDenseW + (uint32_t(__ldg(g.colB + j)) - lo);
+        const float p = __fmul_rn(af, __half2float(__ushort_as_half(hb)));
+        sm.d.acc[slot] = sm.d.flag[slot] ? __fadd_rn(sm.d.acc[slot], p) : p;
+        sm.d.flag[slot] = 1;
+      }
+      __syncwarp();
+    }
+  }
+  __syncthreads();
+  // thread t: row t >> 4, columns 16 (t & 15) .. +15 (one tile column)
+  const uint32_t row = tid >> 4, tc = tid & 15;
+  uint32_t nreal = 0, nst = 0;
+  bool bad = false;
+  float v[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    const uint32_t c = tc * 16 + i, s = row * kDenseW + c;
+    v[i] = 0.f;
+    if (c < width && sm.d.flag[s]) {
+      ++nst;
+      v[i] = sm.d.acc[s];
+      nreal += v[i] != 0.0f;
+      bad |= !isfinite(v[i]);
+    }
+  }
+  if (nst) atomicOr(&sm.bc[7], 1u << tc);  // tile column tc holds a structural entry
+  if (__any_sync(kFull, bad) && lane == 0) atomicOr(g.err_flag, unsigned(kErrPrecision));
+  if (tid < 256) sm.cnt[tid] = 0;
+  __syncthreads();  // the accumulators are in registers before the output aliases them
+  uint32_t off = nreal, zero = 0, tot, dt;
+  if (nreal) atomicAdd(&sm.cnt[row], nreal);
+  block_scan2(sm, off, zero, tot, dt);
+  {
+    uint32_t o = off;
+#pragma unroll
+    for (int i = 0; i < 16; ++i)
+      if (v[i] != 0.0f) {
+        const uint32_t q = opad(o++);
+        sm.s.x.o.col[q] = lo + tc * 16 + i;
+        sm.s.x.o.val[q] = v[i];
+      }
+  }
+  nst = __reduce_add_sync(kFull, nst);
+  if (lane == 0 && nst) atomicAdd(&sm.bc[1], nst);
+  __syncthreads();
+  if (tid == 0) {
+    segs += __popc(sm.bc[7]);
+    structural += sm.bc[1];
+    sm.bc[7] = 0;
+    sm.bc[1] = 0;
+  }
+  write_pieces(sm, g, u, tot, pc);
+}
+
+__global__ void __launch_bounds__(kNT, 3) esc_kernel(EscArgs g) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  EscSmem& sm = *reinterpret_cast<EscSmem*>(smem_raw);
+  const int tid = threadIdx.x;
+  unsigned long long segs = 0, structural = 0;  // thread 0's tallies
+  if (tid == 0) {
+    sm.bc[1] = 0;
+    sm.bc[7] = 0;
+  }
+  const uint32_t nunits = *g.nunits;
+  for (;;) {
+    if (tid == 0) sm.bc[0] = atomicAdd(g.work, 1u);
+    __syncthreads();
+    const uint32_t ui = sm.bc[0];
+    __syncthreads();
+    if (ui >= nunits) break;
+    const uint4 wu = g.units[ui];
+    Unit u;
+    u.I = wu.x;
+    u.lo = wu.y;
+    u.hi = wu.z;
+    u.nb = (wu.w & kGroupFlag) ? (wu.w & 0xffu) : 1u;
+    u.rec0 = g.rec_base[u.I] + ((wu.w & kGroupFlag) ? 0u : wu.w);
+    for (int i = tid; i <= 16 * int(u.nb); i += kNT) {
+      int64_t r = int64_t(u.I) * 16 + i;
+      if (r > g.rowsA) r = g.rowsA;
+      sm.rowp[i] = __ldg(g.rpA + r);
+    }
+    PieceChain pc;
+    if (u.nb == 1) {  // a heavy unit's record starts empty (a unit without products keeps it)
+      if (tid < 16) g.pieces[u.rec0].cnt[tid] = 0;
+      if (tid == 0) {
+        g.pieces[u.rec0].I = u.I;
+        g.pieces[u.rec0].next = kNoPiece;
+        g.pieces[u.rec0].off = 0;
+      }
+    }
+    if (tid == 0) {
+      sm.stk[0] = u.lo;
+      sm.stk[1] = u.hi;
+      sm.bc[4] = 1;  // stack depth
+    }
+    __syncthreads();
+    while (true) {
+      const uint32_t depth = sm.bc[4];
+      if (depth == 0) break;
+      const uint32_t lo = sm.stk[2 * (depth - 1)], hi = sm.stk[2 * (depth - 1) + 1];
+      __syncthreads();
+      if (tid == 0) sm.bc[4] = depth - 1;
+      uint32_t P = 0, ne = 0;
+      const bool fits = hi > lo && hi - lo <= kMaxWidth && build_table(sm, g, u, lo, hi, P, ne);
+      if (hi <= lo) {
+      } else if (fits) {
+        if (P <= uint32_t(kNT) * 4)
+          sort_leaf<4>(sm, g, u, lo, hi, P, ne, pc, segs, structural);
+        else if (P <= uint32_t(kNT) * 8)
+          sort_leaf<8>(sm, g, u, lo, hi, P, ne, pc, segs, structural);
+        else
+          sort_leaf<16>(sm, g, u, lo, hi, P, ne, pc, segs, structural);
+      } else if (u.nb > 1) {  // cannot happen: a group's products fit (planned exactly)
+        if (tid == 0) atomicOr(g.err_flag, unsigned(kErrPool));
+      } else if (hi - lo <= kDenseW) {
+        dense_leaf(sm, g, u, lo, hi, pc, segs, structural);
+      } else {  // halve (16-aligned), left half first
+        if (tid == 0) {
+          uint32_t mid = (lo + ((hi - lo) >> 1)) & ~15u;
+          if (mid <= lo) mid = lo + 16;
+          const uint32_t d = sm.bc[4];
+          sm.stk[2 * d] = mid;
+          sm.stk[2 * d + 1] = hi;
+          sm.stk[2 * d + 2] = lo;
+          sm.stk[2 * d + 3] = mid;
+          sm.bc[4] = d + 2;
+        }
+      }
+      __syncthreads();
+    }
+  }
+  if (tid == 0) {
+    if (segs) atomicAdd(g.segs, segs);
+    if (structural) atomicAdd(g.counted, structural);
+  }
+}
+
+// ---------------------------------------------------------------- planning
+
+__global__ void esc_brec_kernel(int64_t rows, const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
+                                uint4* __restrict__ brec) {
+  for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k < rows; k += int64_t(gridDim.x) * blockDim.x) {
+    const uint32_t b0 = uint32_t(rp[k]), b1 = uint32_t(rp[k + 1]);
+    brec[k] = make_uint4(b0, b1, b1 > b0 ? uint32_t(__ldg(col + b0)) : 0u, b1 > b0 ? uint32_t(__ldg(col + b1 - 1)) : 0u);
+  }
+}
+
+// colcnt[k] = kept A entries in column k
+__global__ void esc_colcount_kernel(int64_t nnz, const int32_t* __restrict__ col, const uint16_t* __restrict__ h,
+                                    uint32_t* __restrict__ colcnt) {
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < nnz; e += int64_t(gridDim.x) * blockDim.x)
+    if (half_nz(__ldg(h + e))) atomicAdd(colcnt + __ldg(col + e), 1u);
+}
+
+// hist[c] += colcnt[k] for every kept B entry (k, c): warp per B row
+__global__ void esc_colhist_kernel(int64_t rowsB, const int64_t* __restrict__ rpB, const int32_t* __restrict__ colB,
+                                   const uint16_t* __restrict__ hB, const uint32_t* __restrict__ colcnt,
+                                   unsigned long long* __restrict__ hist) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t k = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5; k < rowsB;
+       k += (int64_t(gridDim.x) * blockDim.x) >> 5) {
+    const uint32_t w = __ldg(colcnt + k);
+    if (!w) continue;
+    const int64_t b1 = __ldg(rpB + k + 1);
+    for (int64_t e = __ldg(rpB + k) + lane; e < b1; e += 32)
+      if (half_nz(__ldg(hB + e))) atomicAdd(hist + __ldg(colB + e), (unsigned long long)w);
+  }
+}
+
+// products of each tile row: kept A entries x their B row lengths
+__global__ void __launch_bounds__(256) esc_plan_prod_kernel(int64_t rowsA, uint32_t tile_rows,
+                                                           const int64_t* __restrict__ rpA,
+                                                           const int32_t* __restrict__ colA,
+                                                           const uint16_t* __restrict__ hA,
+                                                           const uint4* __restrict__ brec,
+                                                           unsigned long long* __restrict__ prod,
+                                                           unsigned long long* __restrict__ total) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t I = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (I >= tile_rows) return;
+  const int64_t r0 = int64_t(I) * 16, r1 = r0 + 16 < rowsA ? r0 + 16 : rowsA;
+  const int64_t e0 = rpA[r0], e1 = rpA[r1];
+  unsigned long long p = 0;
+  for (int64_t e = e0 + lane; e < e1; e += 32)
+    if (half_nz(__ldg(hA + e))) {
+      const uint4 rb = __ldg(brec + __ldg(colA + e));
+      p += rb.y - rb.x;
+    }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) p += __shfl_xor_sync(kFull, p, o);
+  if (lane == 0) {
+    prod[I] = p;
+    if (p) atomicAdd(total, p);
+  }
+}
+
+// the aligned group of 2^gbits tile rows that tile row I joins (gbits = 0:
+// alone); a heavy row (> kCap products) returns -1
+__device__ __forceinline__ int group_bits(uint32_t I, uint32_t tile_rows, const unsigned long long* __restrict__ pre,
+                                          bool allow) {
+  if (pre[I + 1] - pre[I] > uint64_t(kCap)) return -1;
+  int gb = 0;
+  if (allow)
+    for (int b = 4; b >= 1; --b) {
+      const uint32_t I0 = I & ~((1u << b) - 1u), I1 = min(I0 + (1u << b), tile_rows);
+      if (pre[I1] - pre[I0] <= uint64_t(kCap)) {
+        gb = b;
+        break;
+      }
+    }
+  return gb;
+}
+
+// output records (nrec) and work units (nwk) per tile row
+__global__ void esc_plan_group_kernel(uint32_t tile_rows, const unsigned long long* __restrict__ pre, bool allow,
+                                      uint32_t max_chunks, uint32_t target, uint32_t* __restrict__ nrec,
+                                      uint32_t* __restrict__ nwk) {
+  const uint32_t I = blockIdx.x * blockDim.x + threadIdx.x;
+  if (I >= tile_rows) return;
+  const int gb = group_bits(I, tile_rows, pre, allow);
+  if (gb < 0) {
+    const uint64_t p = pre[I + 1] - pre[I];
+    const uint64_t n = std::min<uint64_t>(max_chunks, (p + target - 1) / target);
+    nrec[I] = uint32_t(n);
+    nwk[I] = uint32_t(n);
+  } else {
+    nrec[I] = 1;
+    nwk[I] = (I & ((1u << gb) - 1u)) == 0u ? 1u : 0u;
+  }
+}
+
+// unit descriptors {I, c0, c1, j | kGroupFlag + nb}: a heavy tile row's
+// column ranges at quantiles of the global product-column distribution G
+__global__ void __launch_bounds__(256) esc_plan_fill_kernel(uint32_t tile_rows, int64_t colsB,
+                                                           const unsigned long long* __restrict__ pre, bool allow,
+                                                           const uint32_t* __restrict__ nwk,
+                                                           const uint32_t* __restrict__ wbase,
+                                                           const unsigned long long* __restrict__ G,
+                                                           uint4* __restrict__ units) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t I = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (I >= tile_rows) return;
+  const uint32_t n = nwk[I], b = wbase[I];
+  if (n == 0) return;
+  const int gb = group_bits(I, tile_rows, pre, allow);
+  if (gb >= 0) {
+    if (lane == 0) {
+      const uint32_t nb = min(1u << gb, tile_rows - I);
+      units[b] = make_uint4(I, 0u, uint32_t(colsB), kGroupFlag | nb);
+    }
+    return;
+  }
+  const double Gt = double(G[colsB]);
+  auto quant = [&](uint32_t j) -> uint32_t {  // 16-aligned column of the j/n quantile
+    if (j == 0) return 0u;
+    if (j >= n) return uint32_t(colsB);
+    const double want = Gt * double(j) / double(n);
+    int64_t lo = 0, hi = colsB;  // smallest c with G[c] >= want
+    while (lo < hi) {
+      const int64_t m = (lo + hi) >> 1;
+      if (double(__ldg(G + m)) < want)
+        lo = m + 1;
+      else
+        hi = m;
+    }
+    return uint32_t(lo) & ~15u;
+  };
+  for (uint32_t j = lane; j < n; j += 32) units[b + j] = make_uint4(I, quant(j), quant(j + 1), j);
+}
+
+// ---------------------------------------------------------------- assembly
+
+// rowcnt[16 I + r] = realised entries of row r; each piece gets its offset
+// within the row.  Warp per tile row, lane r < 16 = row r.
+__global__ void __launch_bounds__(256) esc_rowcount_kernel(int64_t rows, uint32_t tile_rows,
+                                                          const uint32_t* __restrict__ base, EscPiece* pieces,
+                                                          int64_t* __restrict__ rowcnt) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t I = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (I >= tile_rows || lane >= 16) return;
+  uint32_t acc = 0;
+  for (uint32_t c = base[I]; c < base[I + 1]; ++c)
+    for (uint32_t p = c; p != kNoPiece; p = pieces[p].next) {
+      const uint32_t n = pieces[p].cnt[lane];
+      pieces[p].roff[lane] = acc;
+      acc += n;
+    }
+  const int64_t row = int64_t(I) * 16 + lane;
+  if (row < rows) rowcnt[row] = acc;
+}
+
+// staged pieces -> CSR: warp per piece
+__global__ void __launch_bounds__(256) esc_copy_kernel(const uint32_t* __restrict__ nrec,
+                                                      const uint32_t* __restrict__ piece_top, uint32_t pool_cap,
+                                                      const EscPiece* __restrict__ pieces,
+                                                      const uint2* __restrict__ stage,
+                                                      const int64_t* __restrict__ row_ptr,
+                                                      int32_t* __restrict__ col, float* __restrict__ val) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t np = *nrec + min(*piece_top, pool_cap);
+  for (uint32_t p = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; p < np; p += (gridDim.x * blockDim.x) >> 5) {
+    const EscPiece& pc = pieces[p];
+    const uint32_t cnt = lane < 16 ? pc.cnt[lane] : 0u;
+    const uint32_t ro = lane < 16 ? pc.roff[lane] : 0u;
+    uint32_t inc = cnt;  // each row's start within the piece
+#pragma unroll
+    for (int o = 1; o < 16; o <<= 1) {
+      const uint32_t v = __shfl_up_sync(kFull, inc, o);
+      if (lane >= o) inc += v;
+    }
+    const uint32_t total = __shfl_sync(kFull, inc, 15);
+    const uint32_t start = inc - cnt;
+    const int64_t dst0 = lane < 16 && cnt ? row_ptr[int64_t(pc.I) * 16 + lane] + ro : 0;
+    const unsigned long long off = pc.off;
+    // lanes over the piece's entries; entry q belongs to the last row whose start <= q
+    for (uint32_t q0 = 0; q0 < total; q0 += 32) {
+      const uint32_t q = q0 + lane;
+      int r = 0;
+#pragma unroll
+      for (int b = 8; b > 0; b >>= 1) {
+        const uint32_t s = __shfl_sync(kFull, start, r + b);
+        if (s <= q) r += b;
+      }
+      const uint32_t sr = __shfl_sync(kFull, start, r);
+      const int64_t d = __shfl_sync(kFull, dst0, r);
+      if (q < total) {
+        const uint2 e = __ldg(stage + off + q);
+        col[d + (q - sr)] = int32_t(e.x);
+        val[d + (q - sr)] = __uint_as_float(e.y);
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------- statistics
+
+// njt[row] = tiles touched by B's CSR row (first kept entry of each tile)
+__global__ void esc_njt_kernel(int64_t rows, const int64_t* __restrict__ rp, const uint32_t* __restrict__ etile,
+                               uint32_t* __restrict__ njt) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t k = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5; k < rows;
+       k += (int64_t(gridDim.x) * blockDim.x) >> 5) {
+    uint32_t n = 0;
+    const int64_t e1 = rp[k + 1];
+    for (int64_t e = rp[k] + lane; e < e1; e += 32) n += (__ldg(etile + e) & kDupEntry) == 0u;
+    n = __reduce_add_sync(kFull, n);
+    if (lane == 0) njt[k] = n;
+  }
+}
+
+// raw pairs = sum over A tiles of B tile-row lengths (pipeline.cpp:52-58);
+// filtered = pairs passing tile_product_nonzero (pipeline.cpp:23-35): a
+// single-column A tile passes exactly the tiles its B row touches (njt);
+// others test B's row occupancies.  Warp per 32 A tiles.
+__global__ void __launch_bounds__(256) esc_pairstats_kernel(TileMat A, TileMat B, uint32_t tA,
+                                                           const uint32_t* __restrict__ njt,
+                                                           unsigned long long* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t a0 = (blockIdx.x * 8 + (threadIdx.x >> 5)) * 32;
+  if (a0 >= tA) return;
+  const uint32_t a = a0 + lane;
+  unsigned long long raw = 0, filt = 0;
+  uint32_t K = 0, co = 0;
+  bool multi = false;
+  if (a < tA) {
+    const uint2 t = __ldg(A.tco + a);
+    K = t.x;
+    co = t.y & 0xffffu;
+    raw = __ldg(B.trp + K + 1) - __ldg(B.trp + K);
+    if (__popc(co) == 1) {
+      const int64_t row = int64_t(K) * 16 + (__ffs(co) - 1);
+      filt = row < B.rows ? __ldg(njt + row) : 0u;
+    } else {
+      multi = co != 0;
+    }
+  }
+  for (unsigned m = __ballot_sync(kFull, multi); m; m &= m - 1) {
+    const int src = __ffs(m) - 1;
+    const uint32_t k = __shfl_sync(kFull, K, src), c = __shfl_sync(kFull, co, src);
+    const uint32_t b0 = __ldg(B.trp + k), b1 = __ldg(B.trp + k + 1);
+    uint32_t n = 0;
+    for (uint32_t b = b0 + lane; b < b1; b += 32) n += ((__ldg(&B.tco[b].y) >> 16) & c) != 0u;
+    n = __reduce_add_sync(kFull, n);
+    if (lane == src) filt += n;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    raw += __shfl_xor_sync(kFull, raw, o);
+    filt += __shfl_xor_sync(kFull, filt, o);
+  }
+  if (lane == 0) {
+    if (raw) atomicAdd(out, raw);
+    if (filt) atomicAdd(out + 1, filt);
+  }
+}
+
+// ---------------------------------------------------------------- chained A
+// A chained stage's A arrives as A-role tiles (the previous stage's emitted
+// output, tsg_panel.cu emit_tile); the general path reads CSR.  Warp per tile
+// row, lane r < 16 = row r walks the row's tiles in column order.
+__device__ __forceinline__ uint32_t tile_row_mask(const TileMat& A, uint32_t t, int r) {
+  return (__ldg(A.rm2 + size_t(t) * 8 + (r & 7)) >> (16 * (r >> 3))) & 0xffffu;
+}
+
+__global__ void __launch_bounds__(256) tiles_rowcount_kernel(TileMat A, int64_t* __restrict__ rowcnt) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t I = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (I >= A.tile_rows || lane >= 16) return;
+  uint32_t n = 0;
+  for (uint32_t t = A.trp[I]; t < A.trp[I + 1]; ++t) n += __popc(tile_row_mask(A, t, lane));
+  const int64_t row = int64_t(I) * 16 + lane;
+  if (row < A.rows) rowcnt[row] = n;
+}
+
+__global__ void __launch_bounds__(256) tiles_to_csr_kernel(TileMat A, const int64_t* __restrict__ rp,
+                                                          int32_t* __restrict__ col, uint16_t* __restrict__ h16) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t I = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (I >= A.tile_rows || lane >= 16) return;
+  const int64_t row = int64_t(I) * 16 + lane;
+  if (row >= A.rows) return;
+  int64_t p = rp[row];
+  for (uint32_t t = A.trp[I]; t < A.trp[I + 1]; ++t) {
+    uint32_t m = tile_row_mask(A, t, lane);
+    if (!m) continue;
+    const uint32_t J = __ldg(&A.tco[t].x);
+    const uint2 mt = __ldg(A.meta[kRoleA] + t);
+    for (; m; m &= m - 1u) {
+      const int cc = __ffs(m) - 1;
+      int L, j;
+      slot_of(kRoleA, lane, cc, L, j);
+      const uint4 ch = __ldg(A.chunk[kRoleA] + ((mt.x >> L) & 1u ? mt.y + __popc(mt.x & ((1u << L) - 1u)) : 0u));
+      const uint32_t wd = (j >> 1) == 0 ? ch.x : (j >> 1) == 1 ? ch.y : (j >> 1) == 2 ? ch.z : ch.w;
+      col[p] = int32_t(J * 16u + uint32_t(cc));
+      h16[p] = uint16_t(wd >> (16 * (j & 1)));
+      ++p;
+    }
+  }
+}
+
+bool allow_groups(const EscArgs& g) { return (g.colsB + 15) / 16 <= (int64_t(1) << 20); }
+
+}  // namespace
+
+size_t esc_smem_bytes() { return sizeof(EscSmem); }
+
+void launch_esc_brec(const EscArgs& g, int64_t rowsB, uint4* brec, cudaStream_t st) {
+  if (rowsB > 0)
+    esc_brec_kernel<<<unsigned(std::min<int64_t>((rowsB + 255) / 256, 4096)), 256, 0, st>>>(rowsB, g.rpB, g.colB,
+                                                                                            brec);
+}
+
+void launch_esc_hist(const EscArgs& g, int64_t nnzA, int64_t rowsB, uint32_t* colcnt, unsigned long long* hist,
+                     cudaStream_t st) {
+  if (nnzA > 0) esc_colcount_kernel<<<1184, 256, 0, st>>>(nnzA, g.colA, g.hA, colcnt);
+  if (rowsB > 0) esc_colhist_kernel<<<2368, 256, 0, st>>>(rowsB, g.rpB, g.colB, g.hB, colcnt, hist);
+}
+
+void launch_esc_plan_prod(const EscArgs& g, unsigned long long* prod, unsigned long long* total, cudaStream_t st) {
+  if (g.tile_rows == 0) return;
+  esc_plan_prod_kernel<<<(g.tile_rows + 7) / 8, 256, 0, st>>>(g.rowsA, g.tile_rows, g.rpA, g.colA, g.hA, g.brec,
+                                                              prod, total);
+}
+
+void launch_esc_plan_group(const EscArgs& g, const unsigned long long* pre, uint32_t* nrec, uint32_t* nwk,
+                           cudaStream_t st) {
+  if (g.tile_rows == 0) return;
+  const uint32_t max_chunks = uint32_t(std::max<int64_t>(1, std::min<int64_t>((g.colsB + 15) / 16, 1 << 30)));
+  esc_plan_group_kernel<<<(g.tile_rows + 255) / 256, 256, 0, st>>>(g.tile_rows, pre, allow_groups(g), max_chunks,
+                                                                   g.target, nrec, nwk);
+}
+
+void launch_esc_plan_fill(const EscArgs& g, const unsigned long long* pre, const uint32_t* nwk, const uint32_t* wbase,
+                          const unsigned long long* G, uint4* units, cudaStream_t st) {
+  if (g.tile_rows == 0) return;
+  esc_plan_fill_kernel<<<(g.tile_rows + 7) / 8, 256, 0, st>>>(g.tile_rows, g.colsB, pre, allow_groups(g), nwk, wbase,
+                                                              G, units);
+}
+
+void launch_esc(const EscArgs& g, int device, cudaStream_t st) {
+  static int per_sm[16] = {0}, sms[16] = {0};
+  const int d = device & 15;
+  const size_t smem = sizeof(EscSmem);
+  if (!per_sm[d]) {
+    cudaFuncSetAttribute(esc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    int n = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, esc_kernel, kNT, smem);
+    cudaDeviceGetAttribute(&sms[d], cudaDevAttrMultiProcessorCount, device);
+    per_sm[d] = std::max(1, n);
+  }
+  esc_kernel<<<unsigned(per_sm[d] * sms[d]), kNT, smem, st>>>(g);
+}
+
+void launch_esc_rowcount(const EscArgs& g, const uint32_t* base, int64_t* rowcnt, cudaStream_t st) {
+  if (g.tile_rows == 0) return;
+  esc_rowcount_kernel<<<(g.tile_rows + 7) / 8, 256, 0, st>>>(g.rowsA, g.tile_rows, base, g.pieces, rowcnt);
+}
+
+void launch_esc_copy(const EscArgs& g, const int64_t* row_ptr, int32_t* col, float* val, cudaStream_t st) {
+  esc_copy_kernel<<<148 * 16, 256, 0, st>>>(g.nrec, g.piece_top, g.pool_cap, g.pieces, g.stage, row_ptr, col, val);
+}
+
+void launch_esc_pairstats(const TileMat& A, const TileMat& B, uint64_t tA, uint32_t* njt,
+                          unsigned long long* out, cudaStream_t st) {
+  if (B.rows > 0) esc_njt_kernel<<<2368, 256, 0, st>>>(B.rows, B.csr_rp, B.etile, njt);
+  if (tA > 0) esc_pairstats_kernel<<<unsigned((tA + 255) / 256), 256, 0, st>>>(A, B, uint32_t(tA), njt, out);
+}
+
+void launch_tiles_rowcount(const TileMat& A, int64_t* rowcnt, cudaStream_t st) {
+  if (A.tile_rows == 0) return;
+  tiles_rowcount_kernel<<<(A.tile_rows + 7) / 8, 256, 0, st>>>(A, rowcnt);
+}
+
+void launch_tiles_to_csr(const TileMat& A, const int64_t* rp, int32_t* col, uint16_t* h16, cudaStream_t st) {
+  if (A.tile_rows == 0) return;
+  tiles_to_csr_kernel<<<(A.tile_rows + 7) / 8, 256, 0, st>>>(A, rp, col, h16);
+}
+
+}  // namespace tsg

@@ -18,31 +18,6 @@ struct CsrView {  // device CSR input
   int dtype = 1;  // 0 f16 bits, 1 f32, 2 f64
 };
 
-// Sorted tile-pair task list (pipeline.hpp:22-34 at T=16): pairs sorted by
-// (output tile row, output tile col, inner k), one segment per output tile.
-// Each pair is stored as its two operands' metas (pmeta), so the numeric
-// kernels reach the lane chunks with one indirection.
-struct TaskList {
-  uint64_t npairs = 0, nseg = 0;
-  uint4* pmeta = nullptr;           // [P+1] {A lane mask, A chunk base, B lane mask, B chunk base}; [P] = 0
-  uint2* pocc = nullptr;            // [P+1] {A occupancy, B occupancy} (tco.y of the two tiles)
-  uint32_t* seg_row_ptr = nullptr;  // [tile_rows+1] first segment of each tile row
-  uint32_t* seg_off = nullptr;      // [S+1] first pair of each segment
-  uint32_t* seg_col = nullptr;      // [S] output tile column J
-  uint32_t* stage_off = nullptr;    // [S+1] staged-entry region of each segment (upper bound)
-};
-
-// Numeric output in tile order (MulResult, kernels.hpp:24-30): each
-// segment's realised (nonzero) bitmap as 16 row masks, and its values packed
-// row-major (bit order, like TiledMatrix.elements) at stage_off[s].  The
-// assembly pass turns it into CSR (compact + to_element_coo,
-// kernels.cpp:205-220, tile_format.cpp:131-154).
-struct Staged {
-  float* val = nullptr;                   // [stage cap]
-  uint16_t* rmask = nullptr;              // [S*16] realised row masks (bit c of row r)
-  unsigned long long* counted = nullptr;  // structural (counted) nonzeros, CountResult.total_elements
-};
-
 // (1) conversion
 // `needed` (nullable): per tile row, whether the other operand refers to it;
 // unneeded tile rows are validated but get no tiles
@@ -113,52 +88,60 @@ void launch_panel_copy(int64_t rows, const uint32_t* row_stage, const int64_t* r
                        int32_t* col, float* val, unsigned* err_flag, uint32_t I0, uint32_t I1,
                        cudaStream_t st, uint16_t* dcol = nullptr, int32_t* first = nullptr,
                        unsigned* ovf = nullptr);
-// (2) symbolic -- general: enumerate + filter, stable sort, segment heads
-void launch_enum_count(const TileMat& A, const TileMat& B, uint64_t tA, uint32_t* tile_cnt,
-                       unsigned long long* raw_total, cudaStream_t st);
-void launch_enum_fill(const TileMat& A, const TileMat& B, uint64_t tA, const uint32_t* tile_off,
-                      uint64_t* pairs, uint32_t* keys, uint32_t key_shift, cudaStream_t st);
-void launch_row_pair_off(const TileMat& A, const uint32_t* tile_off, uint32_t* row_pair_off,
-                         cudaStream_t st);
-void launch_seg_count(const TileMat& A, const uint32_t* row_pair_off, const uint32_t* keys,
-                      uint32_t* row_nseg, cudaStream_t st);
-void launch_seg_fill(const TileMat& A, const uint32_t* row_pair_off, const uint32_t* keys, uint32_t jmask,
-                     TaskList& tl, cudaStream_t st);
-// per sorted pair: operand metas and the staging bound popc(rows A) * popc(cols B)
-void launch_pair_meta(const TileMat& A, const TileMat& B, const uint64_t* pairs, TaskList& tl,
-                      uint32_t* pair_bound, cudaStream_t st);
-void launch_seg_stage(const TaskList& tl, const uint32_t* pair_stage, cudaStream_t st);
-
-// (3) numeric -- fused boolean count (counting_pass) + SEaC multiply, staged output.
-// Thin segments (tiny staging bound): thread per segment, sequential fp32;
-// flags the others in `heavy` (general path, where the tile pairs exist).
-void launch_numeric_thin(const TaskList& tl, const TileMat& A, const TileMat& B, Staged& sg, uint8_t* heavy,
-                         cudaStream_t st);
-// warp per segment over all segments, or over list[0 .. *list_len) when list != null
-void launch_numeric(const TaskList& tl, const TileMat& A, const TileMat& B, Staged& sg, int mode,
-                    const uint32_t* list, const uint32_t* list_len, cudaStream_t st);
-
-// (4) assembly.  A tile row's segments are cut into chunks of at most
-// kChunkSegs (one warp each, so hub tile rows spread over many warps):
-//   launch_asm_chunks (chunks per tile row) -> host scan -> launch_asm_chunk_fill
-//   launch_row_counts (realised (chunk, row) counts, row totals) -> host scan -> row_ptr
-//   launch_chunk_offsets (CSR offset of each chunk's rows) -> launch_assemble
-constexpr uint32_t kChunkSegs = 512;
-struct AsmChunks {
-  uint32_t* n = nullptr;          // number of chunks (device)
-  uint32_t* tile_row = nullptr;   // [chunks]
-  uint32_t* seg_begin = nullptr;  // [chunks]
-  uint32_t* seg_end = nullptr;    // [chunks]
-  uint32_t* off = nullptr;        // [chunks*16] row counts, then CSR offsets
+// (2)+(3) general rows: per (tile row, column range) chunk, the tile pairs
+// expanded into element products, sorted by output tile key in shared
+// memory, summed in k order, written as row-major pieces (tsg_esc.cu)
+constexpr int kEscThreads = 256;
+constexpr uint32_t kEscTarget = 3072;  // products per unit of a heavy tile row (sorted leaves hold 4096)
+constexpr uint32_t kNoPiece = 0xffffffffu;
+struct EscPiece {             // one sorted output piece: rows of tile row I, row-major
+  uint32_t I, next;           // tile row; next piece of the same record (kNoPiece: last)
+  unsigned long long off;     // its first staged {col, value} slot
+  uint32_t cnt[16];           // realised entries per row
+  uint32_t roff[16];          // (assembly) entries of the row in earlier pieces
 };
-void launch_asm_chunks(uint32_t tile_rows, const uint32_t* seg_row_ptr, uint32_t* nchunks, cudaStream_t st);
-void launch_asm_chunk_fill(uint32_t tile_rows, const uint32_t* seg_row_ptr, const uint32_t* chunk_base,
-                           AsmChunks& ch, cudaStream_t st);
-void launch_row_counts(int64_t rows, const AsmChunks& ch, uint64_t max_chunks, const Staged& sg,
-                       int64_t* rowcnt, cudaStream_t st);
-void launch_chunk_offsets(int64_t rows, uint32_t tile_rows, const uint32_t* chunk_base, const int64_t* row_ptr,
-                          AsmChunks& ch, cudaStream_t st);
-void launch_assemble(int64_t rows, const AsmChunks& ch, uint64_t max_chunks, const TaskList& tl,
-                     const Staged& sg, int32_t* col, float* val, unsigned* err_flag, cudaStream_t st);
+struct EscArgs {
+  int64_t rowsA = 0;
+  uint32_t tile_rows = 0;
+  uint32_t target = kEscTarget;       // products per unit of a heavy tile row
+  const int64_t* rpA = nullptr;
+  const int32_t* colA = nullptr;
+  const uint16_t* hA = nullptr;  // rounded A values (binary16 bits, 0 = dropped)
+  int64_t colsB = 0;
+  const int64_t* rpB = nullptr;
+  const int32_t* colB = nullptr;
+  const uint16_t* hB = nullptr;
+  const uint4* brec = nullptr;        // per B row {first entry, end, first col, last col}
+  const uint4* units = nullptr;       // {tile row, c0, c1, heavy piece index | group flag + tile rows}
+  const uint32_t* nunits = nullptr;   // device: number of units
+  const uint32_t* rec_base = nullptr; // first output record of each tile row
+  const uint32_t* nrec = nullptr;     // device: number of records (the pool follows them)
+  EscPiece* pieces = nullptr;
+  uint32_t* piece_top = nullptr;      // pool pieces used
+  uint32_t pool_cap = 0;
+  uint2* stage = nullptr;             // {col, value bits}
+  unsigned long long* stage_top = nullptr;
+  unsigned* work = nullptr;
+  unsigned* err_flag = nullptr;
+  unsigned long long* counted = nullptr;
+  unsigned long long* segs = nullptr;
+};
+size_t esc_smem_bytes();
+void launch_esc_brec(const EscArgs& g, int64_t rowsB, uint4* brec, cudaStream_t st);
+void launch_esc_hist(const EscArgs& g, int64_t nnzA, int64_t rowsB, uint32_t* colcnt, unsigned long long* hist,
+                     cudaStream_t st);
+void launch_esc_plan_prod(const EscArgs& g, unsigned long long* prod, unsigned long long* total, cudaStream_t st);
+void launch_esc_plan_group(const EscArgs& g, const unsigned long long* pre, uint32_t* nrec, uint32_t* nwk,
+                           cudaStream_t st);
+void launch_esc_plan_fill(const EscArgs& g, const unsigned long long* pre, const uint32_t* nwk, const uint32_t* wbase,
+                          const unsigned long long* G, uint4* units, cudaStream_t st);
+void launch_esc(const EscArgs& g, int device, cudaStream_t st);
+void launch_esc_rowcount(const EscArgs& g, const uint32_t* base, int64_t* rowcnt, cudaStream_t st);
+void launch_esc_copy(const EscArgs& g, const int64_t* row_ptr, int32_t* col, float* val, cudaStream_t st);
+void launch_esc_pairstats(const TileMat& A, const TileMat& B, uint64_t tA, uint32_t* njt, unsigned long long* out,
+                          cudaStream_t st);
+// A given as A-role tiles (a chained stage) -> CSR with binary16 values
+void launch_tiles_rowcount(const TileMat& A, int64_t* rowcnt, cudaStream_t st);
+void launch_tiles_to_csr(const TileMat& A, const int64_t* rp, int32_t* col, uint16_t* h16, cudaStream_t st);
 
 }  // namespace tsg
