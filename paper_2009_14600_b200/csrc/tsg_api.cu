@@ -470,6 +470,18 @@ struct Call {
   const TileMat* TB = nullptr;
   uint64_t tA = 0, tB = 0;
   bool light = false;
+  int nl = 1;  // merge lists per lane of the light-row pass (tile rows of up to 32 nl A tiles)
+
+  // Light-row (tensor-core panel) pass or general rows (element SEaC): tile
+  // rows of at most 32 A tiles always take the panel pass; up to 128 when the
+  // tiles are dense enough for the MMA to pay (>= 4 entries per A tile on
+  // average; a chained stage's A is a product, dense); thinner or longer tile
+  // rows take the general path.
+  void decide(uint32_t max_row_tiles) {
+    nl = max_row_tiles <= 32 ? 1 : max_row_tiles <= 64 ? 2 : 4;
+    const bool dense = pre_a || (tA > 0 && uint64_t(dA.nnz) >= 4 * tA);
+    light = max_row_tiles <= 32 || (max_row_tiles <= 128 && dense);
+  }
 
   int64_t rows = 0;
   uint64_t nr = 0;  // tile rows + 1
@@ -560,9 +572,9 @@ struct Call {
       unsigned v[4];
       readback_many(ctx, src, v);
       raise_flags(v[0]);
-      light = v[1] <= 32;
       tA = v[2];
       tB = v[3];
+      decide(v[1]);
     }
     record(ctx, timing, 1);
 
@@ -646,8 +658,8 @@ struct Call {
     uint2* stage = static_cast<uint2*>(ctx->stage_buf);
     const uint64_t cap_slots = ctx->stage_cap / sizeof(uint2);
     if (timing) TSG_CUDA(cudaEventRecord(ctx->kev[0], s));
-    launch_panel_numeric(TA, *TB, rows, row_stage, cap_slots, stage, rowcnt, counted_d, tot_d + 3, tot_d, opt.mode,
-                         0, TA.tile_rows, s, nullptr, dscal, work);
+    TSG_CUDA(launch_panel_numeric(TA, *TB, rows, row_stage, cap_slots, stage, rowcnt, counted_d, tot_d + 3, tot_d, opt.mode,
+                         0, TA.tile_rows, s, nullptr, dscal, work, 1));
     check_launch(ctx);
     if (timing) TSG_CUDA(cudaEventRecord(ctx->kev[1], s));
     record(ctx, timing, 5);
@@ -661,10 +673,14 @@ struct Call {
     unsigned long long v[10];
     readback_gather(ctx, sc, g, v);
     raise_flags(unsigned(v[0]));
-    light = v[1] <= 32;
     tA = v[2];
     tB = v[3];
+    decide(unsigned(v[1]));
     if (!light) return false;
+    if (nl > 1) {  // the speculative pass (one merge list) stood down: the multi-list pass
+      light_path();
+      return true;
+    }
     counted = v[4];
     nnzC = int64_t(v[5]);
     P = v[6];
@@ -680,8 +696,8 @@ struct Call {
       stage = static_cast<uint2*>(arena(stage_total * sizeof(uint2)));
       TSG_CUDA(cudaMemsetAsync(counted_d, 0, sizeof(unsigned long long), s));
       TSG_CUDA(cudaMemsetAsync(tot_d, 0, 3 * sizeof(unsigned long long), s));
-      launch_panel_numeric(TA, *TB, rows, row_stage, stage_total, stage, rowcnt, counted_d, tot_d + 3, tot_d,
-                           opt.mode, 0, TA.tile_rows, s, nullptr, nullptr, work);
+      TSG_CUDA(launch_panel_numeric(TA, *TB, rows, row_stage, stage_total, stage, rowcnt, counted_d, tot_d + 3, tot_d,
+                           opt.mode, 0, TA.tile_rows, s, nullptr, nullptr, work, nl));
       check_launch(ctx);
       unsigned long long t[4];
       scan_rows(tot_d, t);
@@ -732,7 +748,7 @@ struct Call {
     // chained stages: the tight per-output-tile bound of panel_count_kernel.
     bool elem = !owner->host && !pre_a && !emit_out && tuning_variant("TSG_LIGHT_BOUND", 1) == 1;
     auto count_bound = [&]() {
-      launch_panel_count(TA, *TB, rows, row_np, row_ns, row_raw, row_bound, s);
+      launch_panel_count(TA, *TB, rows, row_np, row_ns, row_raw, row_bound, nl, s);
       check_launch(ctx);
       sum_u32_kernel<<<sblocks, 256, 0, s>>>(row_np, nr - 1, tot_d);
       sum_u32_kernel<<<sblocks, 256, 0, s>>>(row_ns, nr - 1, tot_d + 1);
@@ -790,8 +806,8 @@ struct Call {
       light_host_pipelined(row_stage, tot_d + 3, stage, cap_slots);
       return;
     }
-    launch_panel_numeric(TA, *TB, rows, row_stage, cap_slots, stage, rowcnt, counted_d, tot_d + 3,
-                         elem ? tot_d : nullptr, opt.mode, 0, TA.tile_rows, s, nullptr, nullptr, work);
+    TSG_CUDA(launch_panel_numeric(TA, *TB, rows, row_stage, cap_slots, stage, rowcnt, counted_d, tot_d + 3,
+                         elem ? tot_d : nullptr, opt.mode, 0, TA.tile_rows, s, nullptr, nullptr, work, nl));
     check_launch(ctx);
     if (timing) TSG_CUDA(cudaEventRecord(ctx->kev[1], s));
     record(ctx, timing, 5);
@@ -808,8 +824,8 @@ struct Call {
         cap_slots = stage_total;
         TSG_CUDA(cudaMemsetAsync(counted_d, 0, sizeof(unsigned long long), s));
         if (elem) TSG_CUDA(cudaMemsetAsync(tot_d, 0, 3 * sizeof(unsigned long long), s));
-        launch_panel_numeric(TA, *TB, rows, row_stage, cap_slots, stage, rowcnt, counted_d, tot_d + 3,
-                             elem ? tot_d : nullptr, opt.mode, 0, TA.tile_rows, s, nullptr, nullptr, work);
+        TSG_CUDA(launch_panel_numeric(TA, *TB, rows, row_stage, cap_slots, stage, rowcnt, counted_d, tot_d + 3,
+                             elem ? tot_d : nullptr, opt.mode, 0, TA.tile_rows, s, nullptr, nullptr, work, nl));
         check_launch(ctx);
         scan_rows(tot_d, t);
         take_totals(t);
@@ -860,8 +876,8 @@ struct Call {
     TSG_CUDA(cudaMemsetAsync(em.rtiles + nr - 1, 0, sizeof(uint32_t), s));
     em.err_flag = err_flag;
     if (timing) TSG_CUDA(cudaEventRecord(ctx->kev[0], s));
-    launch_panel_numeric(TA, *TB, rows, nullptr, 0, nullptr, nullptr, counted_d, nullptr, emit_tot, opt.mode, 0,
-                         TA.tile_rows, s, &em, nullptr, work);
+    TSG_CUDA(launch_panel_numeric(TA, *TB, rows, nullptr, 0, nullptr, nullptr, counted_d, nullptr, emit_tot, opt.mode, 0,
+                         TA.tile_rows, s, &em, nullptr, work, nl));
     check_launch(ctx);
     if (timing) TSG_CUDA(cudaEventRecord(ctx->kev[1], s));
     record(ctx, timing, 5);
@@ -940,8 +956,8 @@ struct Call {
       const int64_t r0 = int64_t(I0) * 16, r1 = std::min<int64_t>(int64_t(I1) * 16, rows);
       cr0[c] = r0;
       cr1[c] = r1;
-      launch_panel_numeric(TA, *TB, rows, row_stage, cap_slots, stage, rowcnt, counted_d, need, nullptr, opt.mode,
-                           I0, I1, s, nullptr, nullptr, work);
+      TSG_CUDA(launch_panel_numeric(TA, *TB, rows, row_stage, cap_slots, stage, rowcnt, counted_d, need, nullptr, opt.mode,
+                           I0, I1, s, nullptr, nullptr, work, nl));
       check_launch(ctx);
       // row_ptr[r0 .. r1] = row_ptr[r0] + exclusive prefix (row_ptr[r0] from the previous chunk)
       TSG_CUDA(cub::DeviceScan::ExclusiveScan(tmp, tmp_bytes, rowcnt + r0, d_rp + r0, cuda::std::plus<int64_t>(),

@@ -320,6 +320,18 @@ __device__ bool build_table(EscSmem& sm, const EscArgs& g, const Unit& u, uint32
         if (!full && bhi > blo) {
           if (rb.z >= hi || rb.w < lo) {
             bhi = blo;
+          } else if (bhi - blo <= 8) {  // short row: its columns in one round trip
+            uint32_t c8[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) c8[j] = blo + j < bhi ? uint32_t(__ldg(g.colB + blo + j)) : 0xffffffffu;
+            uint32_t nlo = 0, nhi = 0;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              nlo += c8[j] < lo;
+              nhi += c8[j] < hi;
+            }
+            bhi = blo + nhi;
+            blo += nlo;
           } else {
             if (rb.z < lo) blo = lower_col(g.colB, blo, bhi, lo);
             if (rb.w >= hi) bhi = lower_col(g.colB, blo, bhi, hi);
@@ -373,24 +385,38 @@ __device__ void sort_leaf(EscSmem& sm, const EscArgs& g, const Unit& u, uint32_t
     }
     uint4 te = sm.t[e];
     uint32_t nxt = sm.t[e + 1].z;
+    // (1) B entry index of every item (shared memory only), the row in key[i]
+    // and the A value in val[i]; (2) all the thread's global loads in flight at
+    // once; (3) keys and exact products
+    uint32_t idx[IPT];
 #pragma unroll
     for (int i = 0; i < IPT; ++i) {
       const uint32_t gi = g0 + i;
+      idx[i] = 0;
       if (gi < P) {
         while (gi >= nxt) {
           te = sm.t[++e];
           nxt = sm.t[e + 1].z;
         }
-        const uint32_t base = te.z, blo = te.x, br = te.y & 0xffu;
-        const float a = __uint_as_float(te.w);
-        const uint32_t idx = blo + (gi - base);
-        const uint32_t c = uint32_t(__ldg(g.colB + idx));
-        const uint16_t hb = __ldg(g.hB + idx);
-        if (half_nz(hb)) {
-          vm |= 1u << i;
-          key[i] = ((br >> 4) << bshift) | (((c - lo) >> 4) << 8) | ((c & 15u) << 4) | (br & 15u);
-          val[i] = __fmul_rn(a, __half2float(__ushort_as_half(hb)));
-        }
+        idx[i] = te.x + (gi - te.z);
+        key[i] = te.y & 0xffu;
+        val[i] = __uint_as_float(te.w);
+      }
+    }
+    uint32_t cc[IPT];
+    uint16_t hb[IPT];
+#pragma unroll
+    for (int i = 0; i < IPT; ++i) {
+      cc[i] = g0 + i < P ? uint32_t(__ldg(g.colB + idx[i])) : 0u;
+      hb[i] = g0 + i < P ? __ldg(g.hB + idx[i]) : uint16_t(0);
+    }
+#pragma unroll
+    for (int i = 0; i < IPT; ++i) {
+      if (half_nz(hb[i])) {
+        const uint32_t c = cc[i], br = key[i];
+        vm |= 1u << i;
+        key[i] = ((br >> 4) << bshift) | (((c - lo) >> 4) << 8) | ((c & 15u) << 4) | (br & 15u);
+        val[i] = __fmul_rn(val[i], __half2float(__ushort_as_half(hb[i])));
       }
     }
   }

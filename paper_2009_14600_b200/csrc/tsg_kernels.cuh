@@ -46,8 +46,9 @@ void launch_cbar(const int32_t* colA, int64_t nnzA, int64_t inner, const int64_t
                  unsigned* hist, unsigned long long* out, cudaStream_t st);
 
 // light rows (<= 32 A tiles per tile row): the fused panel pass (tsg_panel.cu)
+// nl: merge lists per lane (1, 2, 4): tile rows of up to 32 nl A tiles
 void launch_panel_count(const TileMat& A, const TileMat& B, int64_t rows, uint32_t* row_np,
-                        uint32_t* row_ns, uint32_t* row_raw, uint32_t* row_bound, cudaStream_t st);
+                        uint32_t* row_ns, uint32_t* row_raw, uint32_t* row_bound, int nl, cudaStream_t st);
 // staging slot = {value bits, column}, row r's region at row_stage[r]; both
 // passes work on the tile rows [I0, I1)
 // Emit mode (chained products): output tiles become A-operand tiles of the
@@ -69,11 +70,11 @@ struct TileEmit {
 // `need`: device u64 total of the staging bound (the pass returns at once when
 // it exceeds stage_cap); `stats`: when non-null, {filtered pairs, segments,
 // raw pairs} are accumulated there (the element-bound flow has no count pass)
-void launch_panel_numeric(const TileMat& A, const TileMat& B, int64_t rows, const uint32_t* row_stage,
-                          uint64_t stage_cap, uint2* stage, int64_t* rowcnt, unsigned long long* counted,
-                          const unsigned long long* need, unsigned long long* stats, int mode,
-                          uint32_t I0, uint32_t I1, cudaStream_t st, const TileEmit* emit = nullptr,
-                          const unsigned* gate = nullptr, unsigned* work = nullptr);
+cudaError_t launch_panel_numeric(const TileMat& A, const TileMat& B, int64_t rows, const uint32_t* row_stage,
+                                 uint64_t stage_cap, uint2* stage, int64_t* rowcnt, unsigned long long* counted,
+                                 const unsigned long long* need, unsigned long long* stats, int mode, uint32_t I0,
+                                 uint32_t I1, cudaStream_t st, const TileEmit* emit = nullptr,
+                                 const unsigned* gate = nullptr, unsigned* work = nullptr, int nl = 1);
 // row_bound[r] = min(B.cols, sum over A's entries (r, k) of nnz(B row k));
 // *total += sum of row_bound
 void launch_elem_bound(const CsrView& A, const int64_t* rpB, int64_t bcols, uint32_t* row_bound,

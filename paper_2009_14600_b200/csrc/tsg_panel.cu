@@ -32,6 +32,7 @@
 //   panel_copy_kernel     staging rows -> CSR (contiguous copies), the
 //                         non-finite check of finalize_segment
 #include <algorithm>
+#include <mutex>
 
 #include "tsg_kernels.cuh"
 #include "tsg_mma.cuh"
@@ -42,29 +43,45 @@ namespace {
 
 constexpr uint32_t kInf = 0xffffffffu;
 
-// Warp state of the 32-way merge over tile row I.
-struct Merge {
-  uint32_t colocc = 0, rowocc = 0, cur = 0, end = 0;
-  uint2 bt, bn;
-  __device__ __forceinline__ void start(const TileMat& A, const TileMat& B, uint32_t I, int lane,
-                                        uint32_t& a) {
-    const uint32_t a0 = A.trp[I];
-    const uint32_t na = A.trp[I + 1] - a0;  // <= 32 on this path
-    a = a0 + lane;
-    if (uint32_t(lane) < na) {
-      const uint2 ac = __ldg(A.tco + a);
-      colocc = ac.y & 0xffffu;
-      rowocc = ac.y >> 16;
-      cur = __ldg(B.trp + ac.x);
-      end = __ldg(B.trp + ac.x + 1);
+// Warp state of the 32-way merge over tile row I (NL lists per lane when a tile row holds
+// more than 32 A tiles).
+// The same merge with NL lists per lane: lane l owns A tiles l, l + 32, ...
+// (tile rows of up to 32 NL tiles).  A run's pairs in ascending k are list 0
+// lanes 0..31, then list 1, ... (tiles of a tile row are sorted by k).
+template <int NL>
+struct MergeN {
+  uint32_t occ[NL], cur[NL], end[NL];
+  uint2 bt[NL], bn[NL];
+  __device__ __forceinline__ void start(const TileMat& A, const TileMat& B, uint32_t I, int lane, uint32_t& a0,
+                                        uint32_t& na) {
+    a0 = A.trp[I];
+    na = A.trp[I + 1] - a0;  // <= 32 NL on this path
+#pragma unroll
+    for (int q = 0; q < NL; ++q) {
+      occ[q] = 0;
+      cur[q] = 0;
+      end[q] = 0;
+      const uint32_t t = uint32_t(lane) + 32u * q;
+      if (t < na) {
+        const uint2 ac = __ldg(A.tco + a0 + t);
+        occ[q] = ac.y;
+        cur[q] = __ldg(B.trp + ac.x);
+        end[q] = __ldg(B.trp + ac.x + 1);
+      }
+      bt[q] = cur[q] < end[q] ? __ldg(B.tco + cur[q]) : make_uint2(kInf, 0);
+      bn[q] = cur[q] + 1 < end[q] ? __ldg(B.tco + cur[q] + 1) : make_uint2(kInf, 0);
     }
-    bt = cur < end ? __ldg(B.tco + cur) : make_uint2(kInf, 0);
-    bn = cur + 1 < end ? __ldg(B.tco + cur + 1) : make_uint2(kInf, 0);
   }
-  __device__ __forceinline__ void advance(const TileMat& B) {
-    ++cur;
-    bt = bn;
-    bn = cur + 1 < end ? __ldg(B.tco + cur + 1) : make_uint2(kInf, 0);
+  __device__ __forceinline__ uint32_t min_head() const {
+    uint32_t j = bt[0].x;
+#pragma unroll
+    for (int q = 1; q < NL; ++q) j = min(j, bt[q].x);
+    return j;
+  }
+  __device__ __forceinline__ void advance(const TileMat& B, int q) {
+    ++cur[q];
+    bt[q] = bn[q];
+    bn[q] = cur[q] + 1 < end[q] ? __ldg(B.tco + cur[q] + 1) : make_uint2(kInf, 0);
   }
 };
 
@@ -72,6 +89,7 @@ struct Merge {
 // row r of the panel, a staging bound: the sum over the row's output tiles
 // that cover row r (OR of the run's A row occupancy) of the run's column
 // span (OR of its B column occupancy).
+template <int NL>
 __global__ void __launch_bounds__(256) panel_count_kernel(TileMat A, TileMat B, int64_t rows,
                                                          uint32_t* __restrict__ row_np,
                                                          uint32_t* __restrict__ row_ns,
@@ -80,25 +98,33 @@ __global__ void __launch_bounds__(256) panel_count_kernel(TileMat A, TileMat B, 
   const int lane = threadIdx.x & 31;
   const uint32_t I = blockIdx.x * 8 + (threadIdx.x >> 5);
   if (I >= A.tile_rows) return;
-  Merge m;
-  uint32_t a;
-  m.start(A, B, I, lane, a);
-  const uint32_t raw_len = m.end - m.cur;  // raw pairs of this A tile (pipeline.cpp:52-58)
+  MergeN<NL> m;
+  uint32_t a0, na;
+  m.start(A, B, I, lane, a0, na);
+  uint32_t raw_len = 0;  // raw pairs of this lane's A tiles (pipeline.cpp:52-58)
+#pragma unroll
+  for (int q = 0; q < NL; ++q) raw_len += m.end[q] - m.cur[q];
   uint32_t np = 0, ns = 0, bound = 0;
   while (true) {
-    const uint32_t J = __reduce_min_sync(kFull, m.bt.x);
+    const uint32_t J = __reduce_min_sync(kFull, m.min_head());
     if (J == kInf) break;
-    const bool take = m.bt.x == J;
-    const bool pass = take && (m.colocc & (m.bt.y >> 16)) != 0u;
-    const unsigned pb = __ballot_sync(kFull, pass);
-    if (pb) {
-      const uint32_t ro = __reduce_or_sync(kFull, pass ? m.rowocc : 0u);
-      const uint32_t co = __reduce_or_sync(kFull, pass ? (m.bt.y & 0xffffu) : 0u);
+    uint32_t ro = 0, co = 0, npass = 0;
+#pragma unroll
+    for (int q = 0; q < NL; ++q) {
+      const bool take = m.bt[q].x == J;
+      const bool pass = take && (m.occ[q] & (m.bt[q].y >> 16) & 0xffffu) != 0u;
+      npass += __popc(__ballot_sync(kFull, pass));
+      ro |= pass ? (m.occ[q] >> 16) : 0u;
+      co |= pass ? (m.bt[q].y & 0xffffu) : 0u;
+      if (take) m.advance(B, q);
+    }
+    if (npass) {
+      ro = __reduce_or_sync(kFull, ro);
+      co = __reduce_or_sync(kFull, co);
       bound += ((ro >> (lane & 15)) & 1u) * __popc(co);  // lane r: row r
-      np += __popc(pb);
+      np += npass;
       ++ns;
     }
-    if (take) m.advance(B);
   }
   const uint32_t rw = __reduce_add_sync(kFull, raw_len);
   if (lane == 0) {
@@ -225,7 +251,7 @@ __device__ __forceinline__ void emit_tile(const float (&acc)[2][4], uint32_t J, 
   e_chunks += __popc(lm);
 }
 
-template <bool kOrdered, int kMinBlocks, bool kEmit>
+template <bool kOrdered, int kMinBlocks, bool kEmit, int NL>
 __global__ void __launch_bounds__(256, kMinBlocks) panel_numeric_kernel(TileMat A, TileMat B, int64_t rows,
                                                               const uint32_t* __restrict__ row_stage,
                                                               uint64_t stage_cap, uint2* __restrict__ stage,
@@ -236,9 +262,12 @@ __global__ void __launch_bounds__(256, kMinBlocks) panel_numeric_kernel(TileMat 
                                                               uint32_t I0, uint32_t I1, TileEmit em,
                                                               const unsigned* __restrict__ gate,
                                                               unsigned* __restrict__ work) {
-  __shared__ __align__(16) uint4 s_meta[8][32];
-  // TENSOR: [A tile of the row][lane] -> chunk index (ORDERED keeps the metas)
-  __shared__ uint32_t s_aidx[kOrdered ? 1 : 8][32][32];
+  // the run's pairs: {A lane mask, A chunk base, B lane mask, B chunk base}
+  // (one list, TENSOR: {A tile of the row, -, B meta} with the A chunk index
+  // of every lane precomputed per tile row in s_aidx)
+  constexpr bool kTable = !kOrdered && NL == 1;
+  __shared__ __align__(16) uint4 s_meta[8][32 * NL];
+  __shared__ uint32_t s_aidx[kTable ? 8 : 1][32][32];
   __shared__ float sA[kOrdered ? 8 : 1][16 * kSA];
   __shared__ float sB[kOrdered ? 8 : 1][16 * kSRow];
   const int lane = threadIdx.x & 31;
@@ -246,7 +275,7 @@ __global__ void __launch_bounds__(256, kMinBlocks) panel_numeric_kernel(TileMat 
   if (!kEmit && (*need > stage_cap || (*need >> 32))) return;  // arena too small: the host reruns the pass
   // speculative launch: {error flags, max A tiles per tile row} of the
   // conversion; invalid input or rows that are not light -> nothing to do
-  if (gate && ((gate[0] & kErrInvariant) || gate[1] > 32u)) return;
+  if (gate && ((gate[0] & kErrInvariant) || gate[1] > 32u * NL)) return;
   const uint4* cA = A.chunk[kRoleA];
   const uint4* cB = B.chunk[kRoleB];
   const unsigned lt = lanemask_lt(), bit = 1u << lane;
@@ -265,17 +294,24 @@ __global__ void __launch_bounds__(256, kMinBlocks) panel_numeric_kernel(TileMat 
   }
   if (I >= I1) break;
   __syncwarp();  // the previous row's shared scratch is no longer read
-  Merge m;
-  uint32_t a;
-  m.start(A, B, I, lane, a);
-  rw += __reduce_add_sync(kFull, m.end - m.cur);  // raw pairs of this tile row
-  const uint32_t na = A.trp[I + 1] - A.trp[I];
-  const uint2 am = uint32_t(lane) < na ? __ldg(A.meta[kRoleA] + a) : make_uint2(0, 0);
-  if (!kOrdered) {
+  MergeN<NL> m;
+  uint32_t a0, na;
+  m.start(A, B, I, lane, a0, na);
+  {
+    uint32_t raw_len = 0;  // raw pairs of this tile row
+#pragma unroll
+    for (int q = 0; q < NL; ++q) raw_len += m.end[q] - m.cur[q];
+    rw += __reduce_add_sync(kFull, raw_len);
+  }
+  uint2 am[NL];
+#pragma unroll
+  for (int q = 0; q < NL; ++q)
+    am[q] = uint32_t(lane) + 32u * q < na ? __ldg(A.meta[kRoleA] + a0 + lane + 32 * q) : make_uint2(0, 0);
+  if (kTable) {
     // this lane's chunk index in each of the row's A tiles (they are reused
     // by every output tile of the row)
     for (uint32_t l = 0; l < na; ++l) {
-      const uint32_t lm = __shfl_sync(kFull, am.x, l), base = __shfl_sync(kFull, am.y, l);
+      const uint32_t lm = __shfl_sync(kFull, am[0].x, l), base = __shfl_sync(kFull, am[0].y, l);
       s_aidx[w][l][lane] = (lm & bit) ? base + __popc(lm & lt) : 0u;
     }
   }
@@ -286,19 +322,24 @@ __global__ void __launch_bounds__(256, kMinBlocks) panel_numeric_kernel(TileMat 
   const uint32_t wg0 = wg, wg80 = wg8;
   uint32_t e_tiles = 0, e_chunks = 0;  // emit mode: tiles / chunks written for this tile row
   while (true) {
-    const uint32_t J = __reduce_min_sync(kFull, m.bt.x);
+    const uint32_t J = __reduce_min_sync(kFull, m.min_head());
     if (J == kInf) break;
-    const bool take = m.bt.x == J;
-    const bool pass = take && (m.colocc & (m.bt.y >> 16)) != 0u;
-    const unsigned pb = __ballot_sync(kFull, pass);
-    if (pb) {
-      // the run's pairs, in ascending k (lane) order: {A tile of the row, B meta}
+    // the run's pairs, in ascending k (list, then lane) order
+    uint32_t n = 0;
+    bool take[NL];
+#pragma unroll
+    for (int q = 0; q < NL; ++q) {
+      take[q] = m.bt[q].x == J;
+      const bool pass = take[q] && (m.occ[q] & (m.bt[q].y >> 16) & 0xffffu) != 0u;
+      const unsigned pb = __ballot_sync(kFull, pass);
       if (pass) {
-        const uint2 bm = __ldg(B.meta[kRoleB] + m.cur);
-        s_meta[w][__popc(pb & lt)] = kOrdered ? make_uint4(am.x, am.y, bm.x, bm.y)
-                                              : make_uint4(uint32_t(lane), 0u, bm.x, bm.y);
+        const uint2 bm = __ldg(B.meta[kRoleB] + m.cur[q]);
+        s_meta[w][n + __popc(pb & lt)] = kTable ? make_uint4(uint32_t(lane), 0u, bm.x, bm.y)
+                                                : make_uint4(am[q].x, am[q].y, bm.x, bm.y);
       }
-      const uint32_t n = __popc(pb);
+      n += __popc(pb);
+    }
+    if (n) {
       np += n;
       ++ns;
       __syncwarp();
@@ -308,9 +349,11 @@ __global__ void __launch_bounds__(256, kMinBlocks) panel_numeric_kernel(TileMat 
         for (uint32_t u = 0; u < n; u += 2) {
           const uint4 m0 = s_meta[w][u];
           const uint4 m1 = u + 1 < n ? s_meta[w][u + 1] : make_uint4(0, 0, 0, 0);
-          const uint4 fa0 = __ldg(cA + s_aidx[w][m0.x][lane]), fb0 = load_chunk(cB, m0.z, m0.w, lt, bit);
+          const uint4 fa0 = kTable ? __ldg(cA + s_aidx[w][m0.x][lane]) : load_chunk(cA, m0.x, m0.y, lt, bit);
+          const uint4 fb0 = load_chunk(cB, m0.z, m0.w, lt, bit);
           // an absent second pair reads the zero chunk: adds exact zeros
-          const uint4 fa1 = __ldg(cA + (u + 1 < n ? s_aidx[w][m1.x][lane] : 0u));
+          const uint4 fa1 = kTable ? __ldg(cA + (u + 1 < n ? s_aidx[w][m1.x][lane] : 0u))
+                                   : load_chunk(cA, m1.x, m1.y, lt, bit);
           const uint4 fb1 = load_chunk(cB, m1.z, m1.w, lt, bit);
           mma16816(acc[0], fa0, fb0.x, fb0.y);
           mma16816(acc[1], fa0, fb0.z, fb0.w);
@@ -374,9 +417,7 @@ __global__ void __launch_bounds__(256, kMinBlocks) panel_numeric_kernel(TileMat 
       if (kEmit) {
         emit_tile(acc, J, I, lane, L, lt, em, e_tiles, e_chunks);
         __syncwarp();
-        if (take) m.advance(B);
-        continue;
-      }
+      } else {
       // finalize_segment: bitmap = accumulators != 0 (cancelled slots and -0
       // drop: compact()); row r's entries append to row r's staging region
       const uint32_t rmg = group_row_masks(acc, L.t);  // rows g | g+8 << 16
@@ -395,8 +436,11 @@ __global__ void __launch_bounds__(256, kMinBlocks) panel_numeric_kernel(TileMat 
       wg += __popc(rmg & 0xffffu);
       wg8 += __popc(rmg >> 16);
       __syncwarp();  // s_meta is rewritten by the next run
+      }
     }
-    if (take) m.advance(B);
+#pragma unroll
+    for (int q = 0; q < NL; ++q)
+      if (take[q]) m.advance(B, q);
   }
   if (kEmit) {
     if (lane == 0) em.rtiles[I] = e_tiles;
@@ -481,10 +525,11 @@ __global__ void __launch_bounds__(256) panel_copy_kernel(int64_t rows, uint32_t 
 }  // namespace
 
 void launch_panel_count(const TileMat& A, const TileMat& B, int64_t rows, uint32_t* row_np,
-                        uint32_t* row_ns, uint32_t* row_raw, uint32_t* row_bound, cudaStream_t st) {
+                        uint32_t* row_ns, uint32_t* row_raw, uint32_t* row_bound, int nl, cudaStream_t st) {
   const unsigned blocks = (A.tile_rows + 7) / 8;
   if (blocks == 0) return;
-  panel_count_kernel<<<blocks, 256, 0, st>>>(A, B, rows, row_np, row_ns, row_raw, row_bound);
+  auto k = nl <= 1 ? panel_count_kernel<1> : nl == 2 ? panel_count_kernel<2> : panel_count_kernel<4>;
+  k<<<blocks, 256, 0, st>>>(A, B, rows, row_np, row_ns, row_raw, row_bound);
 }
 
 void launch_elem_bound(const CsrView& A, const int64_t* rpB, int64_t bcols, uint32_t* row_bound,
@@ -494,44 +539,59 @@ void launch_elem_bound(const CsrView& A, const int64_t* rpB, int64_t bcols, uint
   elem_bound_kernel<<<blocks, 256, 0, st>>>(A, rpB, bcols, row_bound, total);
 }
 
-void launch_panel_numeric(const TileMat& A, const TileMat& B, int64_t rows, const uint32_t* row_stage,
-                          uint64_t stage_cap, uint2* stage, int64_t* rowcnt, unsigned long long* counted,
-                          const unsigned long long* need, unsigned long long* stats, int mode,
-                          uint32_t I0, uint32_t I1, cudaStream_t st, const TileEmit* emit, const unsigned* gate,
-                          unsigned* work) {
+namespace {
+using PanelK = void (*)(TileMat, TileMat, int64_t, const uint32_t*, uint64_t, uint2*, int64_t*, unsigned long long*,
+                        const unsigned long long*, unsigned long long*, uint32_t, uint32_t, TileEmit, const unsigned*,
+                        unsigned*);
+template <int NL>
+PanelK pick_panel(int mode, bool emit) {
+  constexpr int kB = NL == 1 ? 4 : 3;  // resident blocks per SM (registers of the NL merge lists)
+  if (mode == 1) return emit ? panel_numeric_kernel<true, kB, true, NL> : panel_numeric_kernel<true, kB, false, NL>;
+  return emit ? panel_numeric_kernel<false, kB, true, NL> : panel_numeric_kernel<false, kB, false, NL>;
+}
+}  // namespace
+
+cudaError_t launch_panel_numeric(const TileMat& A, const TileMat& B, int64_t rows, const uint32_t* row_stage,
+                                 uint64_t stage_cap, uint2* stage, int64_t* rowcnt, unsigned long long* counted,
+                                 const unsigned long long* need, unsigned long long* stats, int mode, uint32_t I0,
+                                 uint32_t I1, cudaStream_t st, const TileEmit* emit, const unsigned* gate,
+                                 unsigned* work, int nl) {
   unsigned blocks = (I1 - I0 + 7) / 8;
-  if (I1 <= I0) return;
+  if (I1 <= I0) return cudaSuccess;
   const TileEmit em = emit ? *emit : TileEmit{};
-  using K = void (*)(TileMat, TileMat, int64_t, const uint32_t*, uint64_t, uint2*, int64_t*, unsigned long long*,
-                     const unsigned long long*, unsigned long long*, uint32_t, uint32_t, TileEmit, const unsigned*,
-                     unsigned*);
-  K k;
-  if (mode == 1)
-    k = emit ? panel_numeric_kernel<true, 4, true> : panel_numeric_kernel<true, 4, false>;
-  else if (emit)
-    k = panel_numeric_kernel<false, 4, true>;
-  else
-    k = tuning_variant("TSG_PANEL_MINB", 4) == 5 ? panel_numeric_kernel<false, 5, false>
-                                                  : panel_numeric_kernel<false, 4, false>;
+  const int li = nl <= 1 ? 0 : nl == 2 ? 1 : 2;
+  const PanelK k = li == 0 ? pick_panel<1>(mode, emit) : li == 1 ? pick_panel<2>(mode, emit) : pick_panel<4>(mode, emit);
   if (work) {  // persistent: one resident wave takes the tile rows from the counter
-    static int cached[8] = {0};
-    const int slot = (mode == 1 ? 4 : 0) + (emit ? 2 : 0);
-    if (!cached[slot]) {
-      int per_sm = 0, dev = 0, sms = 0;
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, reinterpret_cast<const void*>(k), 256, 0);
-      cudaGetDevice(&dev);
-      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-      cached[slot] = std::max(1, per_sm) * std::max(1, sms);
+    // resident blocks of each kernel variant, per device (a process may drive several GPUs)
+    static std::mutex mu;
+    static int cached[16][12] = {};
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    const int slot = li * 4 + (mode == 1 ? 2 : 0) + (emit ? 1 : 0);
+    int waves;
+    {
+      std::lock_guard<std::mutex> g(mu);
+      int& c = cached[dev & 15][slot];
+      if (!c) {
+        int per_sm = 0, sms = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, reinterpret_cast<const void*>(k), 256, 0);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        c = std::max(1, per_sm) * std::max(1, sms);
+      }
+      waves = c;
     }
-    if (blocks <= unsigned(cached[slot])) {
+    if (blocks <= unsigned(waves)) {
       work = nullptr;  // one wave covers every tile row: static assignment
     } else {
-      blocks = unsigned(cached[slot]);
-      cudaMemsetAsync(work, 0, sizeof(unsigned), st);
+      blocks = unsigned(waves);
+      e = cudaMemsetAsync(work, 0, sizeof(unsigned), st);
+      if (e != cudaSuccess) return e;
     }
   }
   k<<<blocks, 256, 0, st>>>(A, B, rows, row_stage, stage_cap, stage, rowcnt, counted, need, stats, I0, I1, em, gate,
                             work);
+  return cudaSuccess;
 }
 
 // Emitted tiles (gapped per tile row) -> dense CSR-of-tiles: warp per tile row.
