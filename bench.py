@@ -1,22 +1,35 @@
 #!/usr/bin/env python
 """bench.py -- spGEMM GFLOPS (2 x intermediate products / device time).
 
-Workload (BASELINE.json configs[1], the config the metric is quoted on):
-C = A.A, A = 3D 27-point FEM-like stencil on a 64^3 grid (262,144 rows,
-6,859,000 nnz), fp16 in / fp32 accumulate, synthetic (generated
-deterministically, no dataset).  A "step" is one full spGEMM: CSR A (and B)
-resident in HBM -> CSR C in HBM, through the C ABI (tsg_spgemm), with every
-phase, allocation and size readback inside the timed region (PAPER.md:585
-counts allocations).  L2 (126 MB) is flushed with a 256 MB write before
-every timed step, outside the timed span.
+Workload (default): C = A.A, A = R-MAT power-law graph, 2^20 rows, edge
+factor 16, (a,b,c,d) = (0.45,0.15,0.15,0.25) -- BASELINE.json configs[2],
+the largest single-GPU configuration (575M filtered tile pairs, 583M output
+nonzeros; BASELINE's metric names no config, so the largest one that fits a
+GPU is the headline).  fp16 in / fp32 accumulate, synthetic (generated
+deterministically, no dataset).  The other configs (--config
+poisson|fem27|rect|amg) are parity cases and extra lines.
 
-  python bench.py [--gpus N --steps K --warmup W] [--config fem27]
+A "step" is one full spGEMM: CSR A (and B) resident in HBM -> CSR C in HBM,
+through the C ABI (tsg_spgemm), with every phase, allocation and size
+readback inside the timed region (PAPER.md:585 counts allocations).  L2
+(126 MB) is flushed with a 256 MB write before every timed step, outside the
+timed span.  `e2e` is the same call with pinned HOST CSR in and host CSR out
+(H2D + D2H inside the timed region).
+
+  python bench.py [--gpus N --steps K --warmup W] [--config rmat]
   python bench.py --impl reference ...   (the reference CPU implementation)
 
 N > 1 (torchrun, one rank per GPU, NCCL): A is split into tile-row panels
-balanced by rows; B is broadcast from rank 0 over NVLink each step (the
-exchange step of SURVEY.md 8(e)); value = total flops of all ranks / max
-over ranks of the step time.  Total work is fixed: "scaling": "strong".
+balanced by work (intermediate products per tile row); B is broadcast from
+rank 0 over NVLink each step (the exchange step of SURVEY.md 8(e)); value =
+total flops of all ranks / max over ranks of the step time.  Total work is
+fixed: "scaling": "strong".
+
+The CPU legs (cpu_baseline, --impl reference) time the reference compiled in
+place (oracle/_ref) on the host cores.  R-MAT takes minutes per full CPU run,
+so they time a bounded sample: every 64th tile row of A times the full B
+(~6.5% of the products, ~15-25 s per run); GFLOPS are the sample's own flops
+over its time.
 """
 from __future__ import annotations
 
@@ -52,7 +65,7 @@ def parse():
     p.add_argument("--steps", type=int, default=10)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    p.add_argument("--config", default="fem27", choices=list(CONFIG_TEXT))
+    p.add_argument("--config", default="rmat", choices=list(CONFIG_TEXT))
     p.add_argument("--mode", default="tensor", choices=["tensor", "ordered"])
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-sample-runs", type=int, default=3)
@@ -313,22 +326,31 @@ def run_ours(args):
     peaks = json.loads((Path(ROOT) / "MEASURED_PEAKS.json").read_text()) if (Path(ROOT) / "MEASURED_PEAKS.json").exists() else {}
     peak = float(peaks.get("hbm_gbs", 6650.0))
     peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
-    # dominant kernel: the fused numeric pass (light rows: panel_numeric_kernel,
-    # task list + counting + SEaC multiply + compaction of each tile row;
-    # general rows: the thin + warp numeric kernels); its SURVEY 8(d) numeric
-    # bytes over its own CUDA-event duration
+    # dominant kernel: the fused numeric pass -- light rows: panel_numeric_kernel
+    # (task list + counting + SEaC multiply of each tile row, tsg_panel.cu);
+    # general rows: esc_kernel (enumerate + sort + count + multiply of each
+    # work unit in shared memory, tsg_esc.cu).  Its time is the CUDA-event
+    # bracket of that one kernel launch on the library's stream (kev[0..1]).
+    # achieved = SURVEY 8(d) "numeric" bytes / that time (conservative: the
+    # fused kernel also performs the task-list and sort phases, whose SURVEY
+    # bytes are reported separately as achieved_fused_phases).
     dom = "multiply"
     kms = phase_ms.get("numeric_kernel") or phase_ms.get(dom)
     achieved = bytes_[dom] / (kms * 1e-3) / 1e9 if kms else 0.0
-    light = sd["sort"] * 1e3 < 0.05 if not chain else False
-    kname = "panel_numeric_kernel" if light else "numeric_thin_kernel+numeric_tc_kernel"
-    traffic, prof_name = None, f"profiles/r01_ncu_full_{args.config}.json"
-    prof = Path(ROOT) / prof_name
-    if world == 1 and prof.exists():
-        kk = json.loads(prof.read_text())["kernels"]
+    fused_bytes = bytes_["task_list"] + bytes_["sort"] + bytes_["multiply"]
+    achieved_fused = fused_bytes / (kms * 1e-3) / 1e9 if kms else 0.0
+    kname = L.PATH_KERNEL[sd["path"]]
+    traffic, prof_name = None, None
+    for rnd in ("r02", "r01"):
+        cand = Path(ROOT) / f"profiles/{rnd}_ncu_full_{args.config}.json"
+        if cand.exists():
+            prof_name = str(cand.relative_to(ROOT))
+            break
+    if world == 1 and prof_name:
+        kk = json.loads((Path(ROOT) / prof_name).read_text())["kernels"]
         tot = [k["dram_read_bytes"] + k["dram_write_bytes"] for name, k in kk.items()
-               if any(name.startswith(x) for x in kname.split("+"))]
-        traffic = int(sum(tot)) if tot else None
+               if name.split("<")[0].split("#")[0] == kname]
+        traffic = int(sum(tot) / len(tot)) if tot else None
 
     # ---- e2e: host CSR in (pinned), host CSR out, through the public API
     pin = []
@@ -384,19 +406,22 @@ def run_ours(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_max, 4),
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f16-in/f32-acc",
         "data": "synthetic (deterministic generator, paper_2009_14600_b200/workloads.py)",
-        "config": {"workload": CONFIG_TEXT[args.config], "config": args.config, "mode": args.mode,
-                   "flops_per_step": 2 * cb_total, "cbar": cb_total,
-                   "parallelism": f"A tile-row panels x{world}, B broadcast" if world > 1 else "single GPU",
-                   "l2": "flushed (256 MB write) before every timed step",
-                   "values_at_boundary": "binary16 bits (TSG_F16) when exact, on the device and over PCIe",
-                   "nnz_a": Afull.nnz, "nnz_c": sd["nnz_c"], "tiles_a": sd["tiles_a"],
-                   "filtered_pairs": sd["filtered_pairs"], "segments": sd["segments"]},
+        "config": config_key(args.config, cb_total, Afull.nnz),
+        "details": {"mode": args.mode,
+                    "parallelism": f"A tile-row panels x{world}, B broadcast" if world > 1 else "single GPU",
+                    "l2": "flushed (256 MB write) before every timed step",
+                    "values_at_boundary": "binary16 bits (TSG_F16) when exact, on the device and over PCIe",
+                    "nnz_c": sd["nnz_c"], "tiles_a": sd["tiles_a"], "raw_pairs": sd["raw_pairs"],
+                    "filtered_pairs": sd["filtered_pairs"], "segments": sd["segments"],
+                    "counted_elements": sd["counted_elements"], "path": kname,
+                    "device_mem_peak_bytes": sd["mem_peak"]},
         "e2e": {"value": round(e2e_value, 3), "unit": "GFLOPS", "ms_per_step": round(e2e_ms, 4),
                 "h2d_bytes_per_step": e2e_stats.get("h2d"), "d2h_bytes_per_step": e2e_stats.get("d2h")},
         "gpu_launches": int(launches),
         "gpu_launches_per_step": launches / max(1, args.steps),
         "phase_ms": {k: round(v, 4) for k, v in phase_ms.items()},
         "roofline": {"bound": "hbm", "kernel": kname, "achieved": round(achieved, 1),
+                     "achieved_fused_phases": round(achieved_fused, 1), "fused_phase_bytes": int(fused_bytes),
                      "peak": peak, "peak_source": peak_src, "unit": "GB/s", "frac": round(achieved / peak, 4),
                      "kernel_ms": round(kms, 4) if kms else None, "algorithmic_bytes": int(bytes_[dom]),
                      "traffic": traffic, "traffic_source": f"{prof_name} (ncu --set full)" if traffic else None},
@@ -411,7 +436,27 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+# Bounded CPU samples: every `stride`-th tile row of the first operand
+# (workloads.sample_tile_rows) times the full other operands.  R-MAT takes
+# minutes per full reference run (133.6 s on 8 threads), the
+# others finish in seconds and run whole.
+CPU_SAMPLE_STRIDE = {"rmat": 64}
+
+
+def cpu_sample(config, mats):
+    from paper_2009_14600_b200 import workloads as W
+    stride = CPU_SAMPLE_STRIDE.get(config, 1)
+    if stride == 1:
+        return mats, "the whole workload"
+    S = W.sample_tile_rows(mats[0], stride)
+    return ([S] + list(mats[1:]) if len(mats) > 1 else [S, mats[0]]), \
+        f"every {stride}th 16-row tile row of A ({S.rows} rows, {S.nnz} nnz) times the full B"
+
+
 def cpu_run(mats, threads):
+    """The reference: spgemm_square(A) for one operand, the pass composition
+    (kernels.cpp:222-302 phases) for A.B, the chain with the binary16
+    downcast for three."""
     from oracle import ref
     if len(mats) == 1:
         return ref.spgemm(mats[0], threads=threads)
@@ -420,20 +465,40 @@ def cpu_run(mats, threads):
     return ref.chain(mats, threads=threads)
 
 
+def sample_flops(smats):
+    from paper_2009_14600_b200 import workloads as W
+    from paper_2009_14600_b200.tilemul import Csr
+    if len(smats) == 1:
+        return 2 * W.cbar(smats[0], smats[0])
+    cb = W.cbar(smats[0], smats[1])
+    if len(smats) == 3:
+        RA = cpu_run(smats[:2], 1)  # only to size the second stage's C-bar (untimed)
+        cb += W.cbar(Csr(RA.rows, RA.cols, RA.row_ptr, RA.col, RA.val), smats[2])
+    return 2 * cb
+
+
 def cpu_baseline(args, mats, flops):
-    """The reference tilemul (oracle/_ref, compiled unmodified) on host cores."""
+    """The reference tilemul (oracle/_ref, compiled unmodified) on host cores,
+    on a bounded sample of the workload."""
     from oracle import ref
     if not ref.available():
         return {"value": None, "unavailable": "oracle/_ref/libref_tilemul.so not built"}
     cores = os.cpu_count() or 1
-    secs = []
-    for _ in range(max(1, args.cpu_sample_runs)):
-        r = cpu_run(mats, threads=cores)
-        secs.append(r.times["total"])
+    smats, what = cpu_sample(args.config, mats)
+    sflops = flops if smats is mats else sample_flops(smats)
+    runs = 1 if smats is not mats else max(1, args.cpu_sample_runs)
+    secs = [cpu_run(smats, threads=cores).times["total"] for _ in range(runs)]
     s = statistics.median(secs)
-    return {"value": round(flops / s / 1e9, 4), "unit": "GFLOPS", "cores": cores, "kind": "reference",
-            "sample": f"{len(secs)} full runs of the same workload (spgemm_square / pass composition, "
-                      f"pairing on, threads={cores}); median {s:.3f} s; input tiling untimed (SPEC.md:522)"}
+    return {"value": round(sflops / s / 1e9, 4), "unit": "GFLOPS", "cores": cores, "kind": "reference",
+            "sample": f"{what}: {sflops} flops; {len(secs)} run(s) of the reference "
+                      f"(spgemm_square / pass composition, pairing on, threads={cores}), median {s:.3f} s; "
+                      f"input tiling untimed (SPEC.md:522)"}
+
+
+def config_key(config, cb_total, nnz_a):
+    """The workload identity both arms print (same keys and values)."""
+    return {"workload": CONFIG_TEXT[config], "config": config, "flops_per_step": 2 * cb_total,
+            "cbar": cb_total, "nnz_a": nnz_a}
 
 
 def run_reference(args):
@@ -446,30 +511,33 @@ def run_reference(args):
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libref_tilemul.so not built"}))
         return
     from paper_2009_14600_b200 import workloads as W
+    from paper_2009_14600_b200.tilemul import Csr
     mats = operands(args.config)
     cb = W.cbar(mats[0], mats[1] if len(mats) > 1 else mats[0])
     if len(mats) == 3:
         RA = cpu_run(mats[:2], 1)  # only to size the second stage's C-bar
-        from paper_2009_14600_b200.tilemul import Csr
         cb += W.cbar(Csr(RA.rows, RA.cols, RA.row_ptr, RA.col, RA.val), mats[2])
+    smats, what = cpu_sample(args.config, mats)
+    sflops = 2 * cb if smats is mats else sample_flops(smats)
     cores = os.cpu_count() or 1
-    # bounded: a FEM27 run is ~1.8 s on 16 host threads, so K <= 10, W <= 3
-    # keeps the reference arm under a minute
-    steps = max(1, min(args.steps, 10))
-    warm = max(0, min(args.warmup, 3))
+    # bounded: a FEM27 run is ~1.8 s on 16 host threads, an R-MAT sample ~15-25 s;
+    # K <= 10 (<= 3 for a sampled workload), W <= 3 (<= 1) keep the arm to minutes
+    cap_k, cap_w = (10, 3) if smats is mats else (3, 1)
+    steps = max(1, min(args.steps, cap_k))
+    warm = max(0, min(args.warmup, cap_w))
     for _ in range(warm):
-        cpu_run(mats, cores)
-    secs = [cpu_run(mats, cores).times["total"] for _ in range(steps)]
+        cpu_run(smats, cores)
+    secs = [cpu_run(smats, cores).times["total"] for _ in range(steps)]
     s = float(np.mean(secs))
-    v = 2 * cb / s / 1e9
+    v = sflops / s / 1e9
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": round(v, 4), "unit": "GFLOPS", "n_gpus": world,
         "steps": steps, "warmup": warm, "ms_per_step": round(s * 1e3, 3), "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f16-in/f32-acc (CPU, sequential fp32)",
-        "data": "synthetic", "config": {"workload": CONFIG_TEXT[args.config], "config": args.config,
-                                        "flops_per_step": 2 * cb},
+        "data": "synthetic", "config": config_key(args.config, cb, mats[0].nnz),
         "cpu_baseline": {"value": round(v, 4), "unit": "GFLOPS", "cores": cores, "kind": "reference",
-                         "sample": f"{steps} full runs, pairing on, threads={cores}"},
+                         "sample": f"{what}: {sflops} flops per step; {steps} step(s) after {warm} warm-up "
+                                   f"(steps capped at {cap_k}, warm-up at {cap_w}); pairing on, threads={cores}"},
         "e2e": {"value": round(v, 4), "unit": "GFLOPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
 

@@ -35,7 +35,7 @@
 extern "C" {
 #endif
 
-#define TSG_ABI_VERSION 2
+#define TSG_ABI_VERSION 3
 
 /* Only the functions below are exported (the library builds with
  * -fvisibility=hidden). */
@@ -131,7 +131,30 @@ typedef struct {
   uint64_t kernel_launches;  /* own kernels launched by this call         */
   uint64_t h2d_bytes, d2h_bytes;
   uint64_t staged_slots;     /* numeric staging capacity (bound on nnz)   */
+  /* Device memory of the call in bytes: the B200 counterpart of the
+   * reference's MemoryReport (proj/include/tilemul/report.hpp:19-27, filled
+   * by memory_report, proj/src/analytics.cpp:120-152).  Allocated sizes by
+   * role; mem_peak is the high-water mark of the context's device pool
+   * during the call (everything the call held at once, staging arena
+   * included).  Summed over the devices of a multi-device context. */
+  uint64_t mem_input_tiles;    /* tile records of A and B (trp, tco, masks, metas) */
+  uint64_t mem_input_elements; /* operand chunks and rounded binary16 values      */
+  uint64_t mem_task_list;      /* work units / output pieces (general rows; the
+                                  light-row task list never leaves registers)    */
+  uint64_t mem_counting;       /* per-row bounds, offsets and counts              */
+  uint64_t mem_pre_compaction; /* staged {column, value} slots                    */
+  uint64_t mem_output;         /* output CSR                                      */
+  uint64_t mem_peak;
+  int32_t path;    /* numeric path of the (last) stage: tsg_path               */
+  int32_t devices; /* panel workers (GPUs) the call ran on                     */
 } tsg_run_stats;
+
+/* Which numeric kernel a call ran (tsg_run_stats.path). */
+typedef enum {
+  TSG_PATH_PANEL = 0,      /* light tile rows: panel_numeric_kernel (tensor-core SEaC) */
+  TSG_PATH_GENERAL = 1,    /* general tile rows: esc_kernel (element SEaC in smem)      */
+  TSG_PATH_PANEL_EMIT = 2  /* chained stage emitting the next stage's A tiles           */
+} tsg_path;
 
 typedef struct tsg_ctx tsg_ctx;
 
@@ -139,6 +162,26 @@ TSG_API void tsg_default_options(tsg_options* opt);
 
 /* device < 0: current device.  stream: cudaStream_t or NULL (own stream). */
 TSG_API int tsg_create(tsg_ctx** ctx, int device, void* stream);
+
+/* A context over n_devices GPUs (devices[i] = CUDA ordinals; NULL = 0 .. n-1).
+ * Every call splits A into n contiguous tile-row panels balanced by work
+ * (intermediate products per tile row); panel i runs on
+ * devices[i] with its own stream and host thread; B is replicated to every
+ * device (peer copies over NVLink from the device holding it, or H2D from
+ * host memory); the panels' CSR slices are concatenated in row order into
+ * one output on devices[0] (or the host), byte-identical to one GPU.  A
+ * chain (tsg_spgemm_chain) splits its first operand the same way: rank p
+ * computes X0_p . X1 . ... (AMG's R_p.A.P).  An ordinal may repeat: several
+ * panel workers then share one GPU (used to exercise the multi-device path
+ * on a single-GPU box).  Device inputs must live on devices[0].  The
+ * counterpart of one reference process using every host core
+ * (proj/include/tilemul/threading.hpp:14-45). */
+TSG_API int tsg_create_multi(tsg_ctx** ctx, int n_devices, const int* devices);
+
+/* Per-panel device times (ms, CUDA events on each panel's stream) of the
+ * last call of a multi-device context: out[i] for panel i, n entries at most;
+ * returns the panel count.  The max over panels is the call's critical path. */
+TSG_API int tsg_last_panel_ms(const tsg_ctx* ctx, double* out, int n);
 TSG_API int tsg_destroy(tsg_ctx* ctx);
 TSG_API const char* tsg_last_error(const tsg_ctx* ctx);
 TSG_API int tsg_abi_version(void);

@@ -264,16 +264,20 @@ int tsgo_tile_stats(int T, int64_t m, int64_t k, const int64_t* rpA, const int32
   unsigned char* seen = (unsigned char*)calloc((size_t)(tcols ? tcols : 1), 1);
   int64_t* touched = (int64_t*)malloc((size_t)(tcols ? tcols : 1) * sizeof(int64_t));
   uint64_t raw = 0, filt = 0, segs = 0, counted = 0;
+  /* tile_product_nonzero's row occupancy of every B tile, once (the test
+     itself is unchanged, pipeline.cpp:23-35) */
+  uint32_t* bro = (uint32_t*)malloc((size_t)(tB.ntiles ? tB.ntiles : 1) * sizeof(uint32_t));
+  for (int64_t b = 0; b < tB.ntiles; ++b) bro[b] = row_occ(tB.rows + b * T, T);
   for (int64_t I = 0; I < tA.tile_rows; ++I) {
     int64_t nt = 0;
     for (int64_t a = tA.trp[I]; a < tA.trp[I + 1]; ++a) {
       const int32_t kk = tA.tcol[a];
       const uint16_t* ar = tA.rows + a * T;
       const uint32_t aco = col_occ(ar, T);
+      raw += (uint64_t)(tB.trp[kk + 1] - tB.trp[kk]);
       for (int64_t b = tB.trp[kk]; b < tB.trp[kk + 1]; ++b) {
-        ++raw;
         const uint16_t* br = tB.rows + b * T;
-        if (!(aco & row_occ(br, T))) continue;
+        if (!(aco & bro[b])) continue;
         ++filt;
         const int32_t J = tB.tcol[b];
         if (!seen[J]) {
@@ -281,9 +285,10 @@ int tsgo_tile_stats(int T, int64_t m, int64_t k, const int64_t* rpA, const int32
           touched[nt++] = J;
         }
         uint16_t* acc = spa + (int64_t)J * T;
+        /* boolean_tile_mm (pipeline.cpp:11-21): row r of the product = OR of
+           B's rows q over the set bits q of A's row r */
         for (int r = 0; r < T; ++r)
-          for (int q = 0; q < T; ++q)
-            if ((ar[r] >> q) & 1u) acc[r] |= br[q];
+          for (uint32_t bits = ar[r]; bits; bits &= bits - 1) acc[r] |= br[__builtin_ctz(bits)];
       }
     }
     segs += (uint64_t)nt;
@@ -302,6 +307,7 @@ int tsgo_tile_stats(int T, int64_t m, int64_t k, const int64_t* rpA, const int32
   out[3] = filt;
   out[4] = segs;
   out[5] = counted;
+  free(bro);
   free(spa);
   free(seen);
   free(touched);

@@ -42,20 +42,27 @@ class tsg_options(C.Structure):
 STAT_TIMES = ("convert", "task_list", "sort", "counting", "multiply", "compaction", "total")
 STAT_COUNTS = ("tiles_a", "tiles_b", "raw_pairs", "filtered_pairs", "segments", "counted_elements",
                "nnz_c", "cbar", "kernel_launches", "h2d_bytes", "d2h_bytes",
-               "staged_slots")
+               "staged_slots", "mem_input_tiles", "mem_input_elements", "mem_task_list", "mem_counting",
+               "mem_pre_compaction", "mem_output", "mem_peak")
+STAT_INTS = ("path", "devices")
+TSG_PATH_PANEL, TSG_PATH_GENERAL, TSG_PATH_PANEL_EMIT = 0, 1, 2
+# the numeric kernel of each path (tsg_run_stats.path)
+PATH_KERNEL = {TSG_PATH_PANEL: "panel_numeric_kernel", TSG_PATH_GENERAL: "esc_kernel",
+               TSG_PATH_PANEL_EMIT: "panel_numeric_kernel"}
 
 
 class tsg_run_stats(C.Structure):
-    _fields_ = [(n, C.c_double) for n in STAT_TIMES] + [(n, C.c_uint64) for n in STAT_COUNTS]
+    _fields_ = ([(n, C.c_double) for n in STAT_TIMES] + [(n, C.c_uint64) for n in STAT_COUNTS] +
+                [(n, C.c_int32) for n in STAT_INTS])
 
     def as_dict(self) -> dict:
-        return {n: getattr(self, n) for n in STAT_TIMES + STAT_COUNTS}
+        return {n: getattr(self, n) for n in STAT_TIMES + STAT_COUNTS + STAT_INTS}
 
 
 # Every symbol include/tsparse_b200.h declares (checked by tests/test_abi.py).
 EXPORTS = ("tsg_default_options", "tsg_create", "tsg_destroy", "tsg_last_error", "tsg_abi_version",
            "tsg_spgemm", "tsg_spgemm_chain", "tsg_free_csr", "tsg_free_tiles", "tsg_cbar",
-           "tsg_launch_count", "tsg_last_kernel_ms")
+           "tsg_launch_count", "tsg_last_kernel_ms", "tsg_create_multi", "tsg_last_panel_ms")
 
 _lib = None
 
@@ -76,6 +83,10 @@ def load() -> C.CDLL:
     lib.tsg_default_options.restype = None
     lib.tsg_create.argtypes = [C.POINTER(P), C.c_int, P]
     lib.tsg_create.restype = C.c_int
+    lib.tsg_create_multi.argtypes = [C.POINTER(P), C.c_int, C.POINTER(C.c_int)]
+    lib.tsg_create_multi.restype = C.c_int
+    lib.tsg_last_panel_ms.argtypes = [P, C.POINTER(C.c_double), C.c_int]
+    lib.tsg_last_panel_ms.restype = C.c_int
     lib.tsg_destroy.argtypes = [P]
     lib.tsg_destroy.restype = C.c_int
     lib.tsg_last_error.argtypes = [P]

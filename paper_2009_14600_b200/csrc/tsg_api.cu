@@ -129,6 +129,10 @@ struct tsg_ctx {
   // never ask the pool for gigabytes at a new size
   void* stage_buf = nullptr;
   size_t stage_cap = 0;
+  // multi-device context (tsg_create_multi): one single-device context per
+  // panel worker; panel i runs on sub[i]; the last call's per-panel times
+  std::vector<tsg_ctx*> sub;
+  std::vector<double> panel_ms;
 };
 
 namespace {
@@ -148,9 +152,13 @@ struct Fail {
   } while (0)
 
 // Stream-ordered scratch, released (to the pool) when the scope ends.
+// Allocations are tallied by role (the MemoryReport fields of tsg_run_stats).
+enum MemCat : int { kMemTiles = 0, kMemElements, kMemTaskList, kMemCounting, kMemStaging, kMemOutput, kMemCats };
 struct Scratch {
   tsg_ctx* ctx;
   std::vector<void*> ptrs;
+  int cat = kMemCounting;          // role of the next allocations
+  uint64_t bytes[kMemCats] = {};   // bytes allocated per role
   explicit Scratch(tsg_ctx* c) : ctx(c) {}
   ~Scratch() {
     for (void* p : ptrs) cudaFreeAsync(p, ctx->stream);
@@ -161,8 +169,16 @@ struct Scratch {
     void* p = nullptr;
     TSG_CUDA(cudaMallocFromPoolAsync(&p, n * sizeof(T), ctx->pool, ctx->stream));
     if (!keep) ptrs.push_back(p);
+    bytes[cat] += n * sizeof(T);
     return static_cast<T*>(p);
   }
+};
+// RAII role switch for a block of allocations
+struct MemRole {
+  Scratch& sc;
+  int prev;
+  MemRole(Scratch& s, int c) : sc(s), prev(s.cat) { s.cat = c; }
+  ~MemRole() { sc.cat = prev; }
 };
 
 void check_launch(tsg_ctx* ctx, int n = 1) {
@@ -228,6 +244,10 @@ void check_csr(const tsg_csr* M, const char* name) {
     throw Fail{TSG_ERR_OTHER, std::string(name) + ": nnz beyond 2^29 needs row-panel batching"};
   if ((M->rows > 0 || M->nnz > 0) && (!M->row_ptr || (M->nnz > 0 && (!M->col || !M->val))))
     throw Fail{TSG_ERR_OTHER, std::string(name) + ": missing arrays"};
+  // host row pointers: the endpoints here (the full check, also for device
+  // input, is validate_rowptr_kernel before any entry is read)
+  if (M->mem == TSG_MEM_HOST && M->row_ptr && (M->row_ptr[0] != 0 || M->row_ptr[M->rows] != M->nnz))
+    throw Fail{TSG_ERR_INVARIANT, std::string(name) + ": row_ptr[0] must be 0 and row_ptr[rows] must equal nnz"};
 }
 
 // Device view of a CSR (copies host input; the H2D bytes are counted).
@@ -320,6 +340,7 @@ const uint32_t* convert(tsg_ctx* ctx, Scratch& sc, const CsrView& in, TileMat& T
   const uint64_t nr = uint64_t(T.tile_rows) + 1;
   const uint64_t cap = uint64_t(in.nnz);
   T.cap = cap;
+  MemRole role_tiles(sc, kMemTiles);
   ConvertScratch cs;
   cs.rm2 = sc.alloc<uint32_t>(cap * 8);
   cs.ntiles = sc.alloc<uint32_t>(nr);
@@ -338,14 +359,17 @@ const uint32_t* convert(tsg_ctx* ctx, Scratch& sc, const CsrView& in, TileMat& T
     T.etile = sc.alloc<uint32_t>(cap);
     T.csr_rp = in.row_ptr;
   }
-  T.h16 = sc.alloc<uint16_t>(cap);
-  for (int role = 0; role < 2; ++role) {
-    if (!(roles & (1 << role))) continue;
-    cs.rec[role] = sc.alloc<uint4>(cap);
-    T.chunk[role] = sc.alloc<uint4>(cap + 1);
+  {
+    MemRole role_el(sc, kMemElements);
+    T.h16 = sc.alloc<uint16_t>(cap);
+    for (int role = 0; role < 2; ++role)
+      if (roles & (1 << role)) T.chunk[role] = sc.alloc<uint4>(cap + 1);
   }
+  for (int role = 0; role < 2; ++role)
+    if (roles & (1 << role)) cs.rec[role] = sc.alloc<uint4>(cap);
+  launch_validate_rowptr(in, err_flag, ctx->stream);
   launch_convert(in, T, roles, cs, err_flag, drop_nonfinite, needed, ctx->stream);
-  check_launch(ctx, 2);
+  check_launch(ctx, 3);
   T.trp = sc.alloc<uint32_t>(nr);
   exclusive_sum(ctx, sc, cs.ntiles, T.trp, nr);
   T.tco = sc.alloc<uint2>(cap);
@@ -362,6 +386,8 @@ const uint32_t* convert(tsg_ctx* ctx, Scratch& sc, const CsrView& in, TileMat& T
 }
 
 void raise_flags(unsigned flags) {
+  if (flags & kErrRowPtr)
+    throw Fail{TSG_ERR_INVARIANT, "CSR row pointers malformed (row_ptr[0] != 0, row_ptr[rows] != nnz, or decreasing)"};
   if (flags & kErrInvariant)
     throw Fail{TSG_ERR_INVARIANT, "CSR entries unsorted, duplicated, or out of range"};
   if (flags & kErrOverflow)
@@ -470,6 +496,7 @@ struct Call {
   const TileMat* TB = nullptr;
   uint64_t tA = 0, tB = 0;
   bool light = false;
+  int path = TSG_PATH_PANEL;  // numeric kernel that ran (tsg_run_stats.path)
   int nl = 1;  // merge lists per lane of the light-row pass (tile rows of up to 32 nl A tiles)
 
   // Light-row (tensor-core panel) pass or general rows (element SEaC): tile
@@ -506,7 +533,11 @@ struct Call {
   Call(tsg_ctx* c, const tsg_csr* a, const tsg_csr* b, tsg_csr_out* out, const tsg_options& o,
        tsg_run_stats* stats)
       : ctx(c), Ain(a), Bin(b), C(out), opt(o), st(stats), timing(o.phase_timing != 0), s(c->stream),
-        sc(c), launches0(c->launches) {}
+        sc(c), launches0(c->launches) {
+    // the pool's high-water mark restarts at what is held now (mem_peak)
+    uint64_t zero = 0;
+    cudaMemPoolSetAttribute(ctx->pool, cudaMemPoolAttrUsedMemHigh, &zero);
+  }
 
   // ---- (1) validation, staging of host inputs, CSR -> 16x16 tiles ----------------
   // readback of the conversion results deferred to the speculative light pass
@@ -583,7 +614,10 @@ struct Call {
     owner = new OutOwner();
     owner->host = C->mem == TSG_MEM_HOST;
     C->_owner = owner;  // released by free_out on any later failure
-    d_rp = owner->host ? sc.alloc<int64_t>(rows + 1) : sc.alloc<int64_t>(rows + 1, true);
+    {
+      MemRole role_out(sc, kMemOutput);
+      d_rp = owner->host ? sc.alloc<int64_t>(rows + 1) : sc.alloc<int64_t>(rows + 1, true);
+    }
     if (!owner->host) owner->p[0] = d_rp;
     rowcnt = sc.alloc<int64_t>(rows + 1);  // rowcnt[rows] = 0: written by the numeric kernels
     TSG_CUDA(cudaMemsetAsync(rowcnt + rows, 0, sizeof(int64_t), s));
@@ -610,6 +644,7 @@ struct Call {
   }
 
   void alloc_out() {
+    MemRole role_out(sc, kMemOutput);
     d_col = sc.alloc<int32_t>(nnzC, !owner->host);
     d_val = sc.alloc<float>(nnzC, !owner->host);
     if (!owner->host) {
@@ -649,7 +684,7 @@ struct Call {
     auto* row_stage = sc.alloc<uint32_t>(rows + 1);
     TSG_CUDA(cudaMemsetAsync(row_bound + rows, 0, 4, s));
     auto* tot_d = zblk + 2;  // zeroed with the call's scalars
-    launch_elem_bound(dA, dB.row_ptr, Bin->cols, row_bound, tot_d + 3, s);
+    launch_elem_bound(dA, dB.row_ptr, Bin->cols, row_bound, tot_d + 3, err_flag, s);
     check_launch(ctx);
     exclusive_sum(ctx, sc, row_bound, row_stage, uint64_t(rows) + 1);
     record(ctx, timing, 2);
@@ -756,7 +791,7 @@ struct Call {
       check_launch(ctx, 3);
     };
     if (elem) {
-      launch_elem_bound(dA, dB.row_ptr, Bin->cols, row_bound, tot_d + 3, s);
+      launch_elem_bound(dA, dB.row_ptr, Bin->cols, row_bound, tot_d + 3, err_flag, s);
     } else {
       count_bound();
       sum_u32_kernel<<<sblocks, 256, 0, s>>>(row_bound, uint64_t(rows), tot_d + 3);
@@ -853,6 +888,7 @@ struct Call {
   // (panel pass in emit mode, then compaction into a dense CSR-of-tiles).
   // Chained product, light rows, `cap` = the bound on the emitted tiles
   void light_emit(const uint32_t* row_tb, uint64_t cap) {
+    path = TSG_PATH_PANEL_EMIT;
     auto kept = [&](auto* p) {
       keep->push_back(p);
       return p;
@@ -1060,6 +1096,7 @@ struct Call {
 
   // ---- general rows: per-chunk element SEaC in shared memory (tsg_esc.cu) ----------
   void general_path() {
+    path = TSG_PATH_GENERAL;
     const TileMat& B = *TB;
     EscArgs g;
     g.rowsA = rows;
@@ -1143,7 +1180,11 @@ struct Call {
       nunits = v[1];
       products = v[2];
     }
-    auto* units = sc.alloc<uint4>(nunits);
+    uint4* units;
+    {
+      MemRole role_tl(sc, kMemTaskList);
+      units = sc.alloc<uint4>(nunits);
+    }
     launch_esc_plan_fill(g, ppre, nwk, wbase, G, units, s);
     check_launch(ctx);
     record(ctx, timing, 3);
@@ -1165,7 +1206,10 @@ struct Call {
     unsigned long long t[4];
     for (int attempt = 0;; ++attempt) {
       g.pool_cap = uint32_t(std::min<uint64_t>(pool, 0xfffffff0ull - nrecs));
-      g.pieces = sc.alloc<EscPiece>(nrecs + g.pool_cap);
+      {
+        MemRole role_tl(sc, kMemTaskList);
+        g.pieces = sc.alloc<EscPiece>(nrecs + g.pool_cap);
+      }
       TSG_CUDA(cudaMemsetAsync(ctr, 0, 2 * sizeof(unsigned long long), s));
       if (timing) TSG_CUDA(cudaEventRecord(ctx->kev[0], s));
       launch_esc(g, ctx->device, s);
@@ -1278,6 +1322,17 @@ struct Call {
       st->nnz_c = uint64_t(nnzC);
       st->staged_slots += stage_total;
       st->kernel_launches += ctx->launches - launches0;
+      st->mem_input_tiles += sc.bytes[kMemTiles];
+      st->mem_input_elements += sc.bytes[kMemElements];
+      st->mem_task_list += sc.bytes[kMemTaskList];
+      st->mem_counting += sc.bytes[kMemCounting];
+      st->mem_pre_compaction += stage_total * sizeof(uint2) + sc.bytes[kMemStaging];
+      st->mem_output += sc.bytes[kMemOutput];
+      uint64_t high = 0;
+      if (cudaMemPoolGetAttribute(ctx->pool, cudaMemPoolAttrUsedMemHigh, &high) == cudaSuccess)
+        st->mem_peak = std::max<uint64_t>(st->mem_peak, uint64_t(high));
+      st->path = path;
+      st->devices = 1;
     }
   }
 };
@@ -1338,6 +1393,362 @@ void free_out(tsg_ctx* ctx, tsg_csr_out* C) {
   C->val = nullptr;
 }
 
+
+// ---------------------------------------------------------------- multi-device
+// tsg_create_multi: C = X0 . X1 ... with X0 split into contiguous tile-row
+// panels of ~equal work; panel i runs the single-device
+// path on sub[i] (own stream, own host thread per distinct GPU), the other
+// operands replicated per device; the panels' CSR slices are concatenated
+// in row order (byte-identical to one device: a C tile row depends only on
+// X0's tile row and the other operands).
+
+// work[I] = sum over X0's entries (r, k) in tile row I of nnz(X1 row k)
+__global__ void tile_row_work_kernel(CsrView A, const int64_t* __restrict__ rpB, unsigned long long* __restrict__ work) {
+  const int lane = threadIdx.x & 31;
+  const int64_t I = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5;
+  const int64_t r0 = I * 16;
+  if (r0 >= A.rows) return;
+  const int64_t r1 = r0 + 16 < A.rows ? r0 + 16 : A.rows;
+  const int64_t e0 = A.row_ptr[r0], e1 = A.row_ptr[r1];
+  unsigned long long w = 0;
+  for (int64_t e = e0 + lane; e < e1; e += 32) {
+    const int32_t c = A.col[e];
+    if (c >= 0 && c < A.cols) w += (unsigned long long)(rpB[c + 1] - rpB[c]);
+  }
+  for (int o = 16; o > 0; o >>= 1) w += __shfl_xor_sync(0xffffffffu, w, o);
+  if (lane == 0) work[I] = w;
+}
+
+// dst[i] = src[i] - src[0] + add, i < n (a row-pointer slice rebased)
+__global__ void rebase_kernel(const int64_t* __restrict__ src, int64_t n, int64_t add, int64_t* __restrict__ dst) {
+  const int64_t b = src[0];
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
+    dst[i] = src[i] - b + add;
+}
+
+// x[i] += add, i < n (in place)
+__global__ void add_kernel(int64_t* __restrict__ x, int64_t n, int64_t add) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
+    x[i] += add;
+}
+
+void add_offset(int64_t* x, int64_t n, int64_t add, cudaStream_t st) {
+  if (n <= 0 || add == 0) return;
+  const unsigned blocks = unsigned(std::min<int64_t>((n + 255) / 256, 1184));
+  add_kernel<<<blocks, 256, 0, st>>>(x, n, add);
+  TSG_CUDA(cudaGetLastError());
+}
+
+void rebase(const int64_t* src, int64_t n, int64_t add, int64_t* dst, cudaStream_t st) {
+  if (n <= 0) return;
+  const unsigned blocks = unsigned(std::min<int64_t>((n + 255) / 256, 1184));
+  rebase_kernel<<<blocks, 256, 0, st>>>(src, n, add, dst);
+  TSG_CUDA(cudaGetLastError());
+}
+
+// Panel boundaries (rows, 16-aligned): cut p = the first tile row whose
+// exclusive work prefix reaches p/n of the total (paper_2009_14600_b200/
+// distributed.py panel_bounds restates the same rule).
+std::vector<int64_t> panel_cuts(tsg_ctx* ctx, const tsg_csr* A, const tsg_csr* B, int n) {
+  const int64_t T = (A->rows + 15) / 16;
+  std::vector<unsigned long long> cum(T + 1, 0);
+  if (A->mem == TSG_MEM_HOST && B->mem == TSG_MEM_HOST) {
+    const unsigned nt = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+    std::vector<std::thread> th;
+    for (unsigned t = 0; t < nt; ++t)
+      th.emplace_back([&, t] {
+        for (int64_t I = T * t / nt; I < T * (t + 1) / nt; ++I) {
+          unsigned long long w = 0;
+          const int64_t r1 = std::min<int64_t>(A->rows, I * 16 + 16);
+          for (int64_t e = A->row_ptr[I * 16]; e < A->row_ptr[r1]; ++e) {
+            const int32_t c = A->col[e];
+            if (c >= 0 && c < A->cols) w += (unsigned long long)(B->row_ptr[c + 1] - B->row_ptr[c]);
+          }
+          cum[I + 1] = w;
+        }
+      });
+    for (auto& x : th) x.join();
+  } else {  // device operands (on devices[0]): the work per tile row on the device
+    tsg_ctx* c0 = ctx->sub[0];
+    TSG_CUDA(cudaSetDevice(c0->device));
+    Scratch sc(c0);
+    CsrView va = stage(c0, sc, A, nullptr);
+    CsrView vb = stage(c0, sc, B, nullptr);
+    auto* w = sc.alloc<unsigned long long>(uint64_t(std::max<int64_t>(T, 1)));
+    if (T > 0) {
+      tile_row_work_kernel<<<unsigned((T * 32 + 255) / 256), 256, 0, c0->stream>>>(va, vb.row_ptr, w);
+      check_launch(c0);
+      TSG_CUDA(cudaMemcpyAsync(cum.data() + 1, w, T * sizeof(unsigned long long), cudaMemcpyDeviceToHost, c0->stream));
+    }
+    TSG_CUDA(cudaStreamSynchronize(c0->stream));
+  }
+  for (int64_t I = 0; I < T; ++I) cum[I + 1] += cum[I];
+  std::vector<int64_t> cut(n + 1, 0);
+  const double total = double(cum[T]);
+  for (int p = 1; p < n; ++p) {
+    const double want = total * p / n;
+    const int64_t I = std::lower_bound(cum.begin(), cum.end(), want,
+                                       [](unsigned long long a, double b) { return double(a) < b; }) - cum.begin();
+    cut[p] = std::max(cut[p - 1], std::min<int64_t>(I, T));
+  }
+  cut[n] = T;
+  for (int p = 0; p <= n; ++p) cut[p] = std::min<int64_t>(cut[p] * 16, A->rows);
+  return cut;
+}
+
+// Device copy of operand M (on devices[0]) for another device (peer copy
+// over NVLink); owner pointers in `keep`.
+tsg_csr replicate(const tsg_csr* M, tsg_ctx* to, int from_dev, std::vector<std::pair<tsg_ctx*, void*>>& keep) {
+  tsg_csr r = *M;
+  const size_t b0 = (M->rows + 1) * sizeof(int64_t), b1 = M->nnz * sizeof(int32_t), b2 = M->nnz * dtype_size(M->dtype);
+  void* p[3] = {nullptr, nullptr, nullptr};
+  const size_t b[3] = {b0, b1, b2};
+  const void* src[3] = {M->row_ptr, M->col, M->val};
+  for (int i = 0; i < 3; ++i) {
+    TSG_CUDA(cudaMallocFromPoolAsync(&p[i], std::max<size_t>(b[i], 1), to->pool, to->stream));
+    keep.emplace_back(to, p[i]);
+    if (b[i]) TSG_CUDA(cudaMemcpyPeerAsync(p[i], to->device, src[i], from_dev, b[i], to->stream));
+  }
+  r.row_ptr = static_cast<int64_t*>(p[0]);
+  r.col = static_cast<int32_t*>(p[1]);
+  r.val = p[2];
+  return r;
+}
+
+void merge_stats(tsg_run_stats* into, const tsg_run_stats& s, bool first) {
+  double* t = &into->convert;
+  const double* u = &s.convert;
+  for (int i = 0; i < 7; ++i) t[i] = std::max(t[i], u[i]);  // phase times: the critical path
+  uint64_t* a = &into->tiles_a;
+  const uint64_t* b = &s.tiles_a;
+  for (int i = 0; i < 19; ++i) a[i] += b[i];  // counters and memory: sums over panels
+  if (first) into->path = s.path;
+}
+
+int spgemm_multi(tsg_ctx* ctx, int nops, const tsg_csr* const* X, tsg_csr_out* C, const tsg_options& o,
+                 tsg_run_stats* stats) {
+  const int n = int(ctx->sub.size());
+  const int dev0 = ctx->sub[0]->device;
+  if (!C) throw Fail{TSG_ERR_OTHER, "C is NULL"};
+  if (o.want_tiles) throw Fail{TSG_ERR_OTHER, "the tiled parity view needs a single-device context"};
+  for (int i = 0; i < nops; ++i) check_csr(X[i], i == 0 ? "A" : "B");
+  for (int i = 0; i + 1 < nops; ++i)
+    if (X[i]->cols != X[i + 1]->rows)
+      throw Fail{TSG_ERR_DIMENSION, "inner dimensions differ: " + std::to_string(X[i]->rows) + "x" +
+                                        std::to_string(X[i]->cols) + " . " + std::to_string(X[i + 1]->rows) + "x" +
+                                        std::to_string(X[i + 1]->cols)};
+  const tsg_csr* A = X[0];
+  const std::vector<int64_t> cut = panel_cuts(ctx, A, X[1], n);
+  // panels, grouped by device (one host thread per distinct GPU; panels
+  // sharing a GPU run one after another)
+  std::vector<int> devs;
+  for (auto* c : ctx->sub)
+    if (std::find(devs.begin(), devs.end(), c->device) == devs.end()) devs.push_back(c->device);
+  std::vector<tsg_csr_out> outs(n);
+  std::vector<tsg_run_stats> pst(n);
+  std::vector<Fail> fails(n, Fail{TSG_OK, ""});
+  ctx->panel_ms.assign(n, 0.0);
+  std::vector<std::vector<std::pair<tsg_ctx*, void*>>> keeps(devs.size());
+  auto run_device = [&](size_t di) {
+    const int d = devs[di];
+    std::vector<tsg_csr> rep(nops);  // X1.. on this device
+    bool have_rep = false;
+    for (int p = 0; p < n; ++p) {
+      tsg_ctx* c = ctx->sub[p];
+      if (c->device != d) continue;
+      try {
+        TSG_CUDA(cudaSetDevice(d));
+        if (!have_rep) {
+          for (int i = 1; i < nops; ++i)
+            rep[i] = (X[i]->mem == TSG_MEM_DEVICE && d != dev0) ? replicate(X[i], c, dev0, keeps[di]) : *X[i];
+          have_rep = true;
+        }
+        cudaEvent_t ev[2];
+        TSG_CUDA(cudaEventCreate(&ev[0]));
+        TSG_CUDA(cudaEventCreate(&ev[1]));
+        TSG_CUDA(cudaEventRecord(ev[0], c->stream));
+        // X0's panel [r0, r1) with rebased row pointers (on this device)
+        const int64_t r0 = cut[p], r1 = cut[p + 1];
+        tsg_csr a = *A;
+        a.rows = r1 - r0;
+        std::vector<int64_t> hrp;
+        if (A->mem == TSG_MEM_HOST) {
+          const int64_t e0 = A->row_ptr[r0];
+          hrp.resize(r1 - r0 + 1);
+          for (int64_t r = r0; r <= r1; ++r) hrp[r - r0] = A->row_ptr[r] - e0;
+          a.row_ptr = hrp.data();
+          a.nnz = hrp.back();
+          a.col = A->col + e0;
+          a.val = static_cast<const char*>(A->val) + e0 * dtype_size(A->dtype);
+        } else {
+          int64_t e[2];
+          TSG_CUDA(cudaMemcpyAsync(e, A->row_ptr + r0, sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream));
+          TSG_CUDA(cudaMemcpyAsync(e + 1, A->row_ptr + r1, sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream));
+          TSG_CUDA(cudaStreamSynchronize(c->stream));
+          a.nnz = e[1] - e[0];
+          void* rp = nullptr;
+          TSG_CUDA(cudaMallocFromPoolAsync(&rp, (a.rows + 1) * sizeof(int64_t), c->pool, c->stream));
+          keeps[di].emplace_back(c, rp);
+          if (d == dev0) {
+            rebase(A->row_ptr + r0, a.rows + 1, 0, static_cast<int64_t*>(rp), c->stream);
+            a.col = A->col + e[0];
+            a.val = static_cast<const char*>(A->val) + e[0] * dtype_size(A->dtype);
+          } else {
+            void* tmp = nullptr;
+            TSG_CUDA(cudaMallocFromPoolAsync(&tmp, (a.rows + 1) * sizeof(int64_t), c->pool, c->stream));
+            keeps[di].emplace_back(c, tmp);
+            TSG_CUDA(cudaMemcpyPeerAsync(tmp, d, A->row_ptr + r0, dev0, (a.rows + 1) * sizeof(int64_t), c->stream));
+            rebase(static_cast<int64_t*>(tmp), a.rows + 1, 0, static_cast<int64_t*>(rp), c->stream);
+            void* cv[2] = {nullptr, nullptr};
+            const size_t bb[2] = {a.nnz * sizeof(int32_t), a.nnz * dtype_size(A->dtype)};
+            const void* src[2] = {A->col + e[0], static_cast<const char*>(A->val) + e[0] * dtype_size(A->dtype)};
+            for (int i = 0; i < 2; ++i) {
+              TSG_CUDA(cudaMallocFromPoolAsync(&cv[i], std::max<size_t>(bb[i], 1), c->pool, c->stream));
+              keeps[di].emplace_back(c, cv[i]);
+              if (bb[i]) TSG_CUDA(cudaMemcpyPeerAsync(cv[i], d, src[i], dev0, bb[i], c->stream));
+            }
+            a.col = static_cast<int32_t*>(cv[0]);
+            a.val = cv[1];
+          }
+          a.row_ptr = static_cast<int64_t*>(rp);
+        }
+        outs[p] = tsg_csr_out{};
+        outs[p].mem = TSG_MEM_DEVICE;
+        std::memset(&pst[p], 0, sizeof(tsg_run_stats));
+        if (nops == 2) {
+          spgemm_impl(c, &a, &rep[1], &outs[p], o, &pst[p], nullptr);
+        } else {
+          std::vector<const tsg_csr*> xs(nops);
+          xs[0] = &a;
+          for (int i = 1; i < nops; ++i) xs[i] = &rep[i];
+          const int rc = tsg_spgemm_chain(c, nops, xs.data(), &outs[p], &o, &pst[p]);
+          if (rc != TSG_OK) throw Fail{rc, c->err};
+        }
+        TSG_CUDA(cudaEventRecord(ev[1], c->stream));
+        TSG_CUDA(cudaEventSynchronize(ev[1]));
+        float ms = 0;
+        TSG_CUDA(cudaEventElapsedTime(&ms, ev[0], ev[1]));
+        ctx->panel_ms[p] = ms;
+        cudaEventDestroy(ev[0]);
+        cudaEventDestroy(ev[1]);
+      } catch (const Fail& f) {
+        fails[p] = f;
+      }
+    }
+  };
+  {
+    std::vector<std::thread> th;
+    for (size_t di = 0; di < devs.size(); ++di) th.emplace_back(run_device, di);
+    for (auto& t : th) t.join();
+  }
+  auto release = [&]() {
+    for (int p = 0; p < n; ++p)
+      if (outs[p]._owner) {
+        cudaSetDevice(ctx->sub[p]->device);
+        free_out(ctx->sub[p], &outs[p]);
+      }
+    for (auto& k : keeps)
+      for (auto& [c, ptr] : k) {
+        cudaSetDevice(c->device);
+        cudaFreeAsync(ptr, c->stream);
+      }
+    for (auto* c : ctx->sub) cudaStreamSynchronize(c->stream);
+    cudaSetDevice(dev0);
+  };
+  for (int p = 0; p < n; ++p)
+    if (fails[p].code != TSG_OK) {
+      release();
+      throw fails[p];
+    }
+  // concatenate: panel p's entries start at the sum of the earlier panels' nnz
+  int64_t nnz = 0;
+  std::vector<int64_t> base(n + 1, 0);
+  for (int p = 0; p < n; ++p) base[p + 1] = base[p] + outs[p].nnz;
+  nnz = base[n];
+  const int64_t rows = A->rows;
+  tsg_ctx* c0 = ctx->sub[0];
+  auto* owner = new OutOwner();
+  owner->host = C->mem == TSG_MEM_HOST;
+  C->_owner = owner;
+  uint64_t d2h = 0;
+  try {
+    if (owner->host) {
+      owner->p[0] = pinned_alloc(c0, (rows + 1) * sizeof(int64_t), &owner->sz[0]);
+      owner->p[1] = pinned_alloc(c0, std::max<int64_t>(nnz, 1) * sizeof(int32_t), &owner->sz[1]);
+      owner->p[2] = pinned_alloc(c0, std::max<int64_t>(nnz, 1) * sizeof(float), &owner->sz[2]);
+      for (int p = 0; p < n; ++p) {  // every device ships its slice straight into place
+        tsg_ctx* c = ctx->sub[p];
+        TSG_CUDA(cudaSetDevice(c->device));
+        const int64_t nr = cut[p + 1] - cut[p];
+        add_offset(outs[p].row_ptr, nr, base[p], c->stream);
+        TSG_CUDA(cudaMemcpyAsync(static_cast<int64_t*>(owner->p[0]) + cut[p], outs[p].row_ptr, nr * sizeof(int64_t),
+                                 cudaMemcpyDeviceToHost, c->stream));
+        if (outs[p].nnz) {
+          TSG_CUDA(cudaMemcpyAsync(static_cast<int32_t*>(owner->p[1]) + base[p], outs[p].col,
+                                   outs[p].nnz * sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream));
+          TSG_CUDA(cudaMemcpyAsync(static_cast<float*>(owner->p[2]) + base[p], outs[p].val,
+                                   outs[p].nnz * sizeof(float), cudaMemcpyDeviceToHost, c->stream));
+        }
+        d2h += nr * sizeof(int64_t) + outs[p].nnz * (sizeof(int32_t) + sizeof(float));
+      }
+      for (auto* c : ctx->sub) TSG_CUDA(cudaStreamSynchronize(c->stream));
+      static_cast<int64_t*>(owner->p[0])[rows] = nnz;
+    } else {
+      TSG_CUDA(cudaSetDevice(dev0));
+      for (int i = 0; i < 3; ++i) {
+        const size_t b = i == 0 ? (rows + 1) * sizeof(int64_t) : std::max<int64_t>(nnz, 1) * 4;
+        TSG_CUDA(cudaMallocFromPoolAsync(&owner->p[i], b, c0->pool, c0->stream));
+      }
+      for (auto* c : ctx->sub) TSG_CUDA(cudaStreamSynchronize(c->stream));  // every slice is final
+      auto* rp = static_cast<int64_t*>(owner->p[0]);
+      for (int p = 0; p < n; ++p) {
+        const int dp = ctx->sub[p]->device;
+        const int64_t nr = cut[p + 1] - cut[p];
+        if (nr > 0) {
+          TSG_CUDA(cudaMemcpyPeerAsync(rp + cut[p], dev0, outs[p].row_ptr, dp, nr * sizeof(int64_t), c0->stream));
+          add_offset(rp + cut[p], nr, base[p], c0->stream);
+        }
+        if (outs[p].nnz) {
+          TSG_CUDA(cudaMemcpyPeerAsync(static_cast<int32_t*>(owner->p[1]) + base[p], dev0, outs[p].col, dp,
+                                       outs[p].nnz * sizeof(int32_t), c0->stream));
+          TSG_CUDA(cudaMemcpyPeerAsync(static_cast<float*>(owner->p[2]) + base[p], dev0, outs[p].val, dp,
+                                       outs[p].nnz * sizeof(float), c0->stream));
+        }
+      }
+      TSG_CUDA(cudaMemcpyAsync(rp + rows, &base[n], sizeof(int64_t), cudaMemcpyHostToDevice, c0->stream));
+      TSG_CUDA(cudaStreamSynchronize(c0->stream));
+    }
+  } catch (...) {
+    release();
+    throw;
+  }
+  release();
+  C->rows = rows;
+  C->cols = X[nops - 1]->cols;
+  C->nnz = nnz;
+  C->row_ptr = static_cast<int64_t*>(owner->p[0]);
+  C->col = static_cast<int32_t*>(owner->p[1]);
+  C->val = static_cast<float*>(owner->p[2]);
+  if (stats) {
+    tsg_run_stats agg;
+    std::memset(&agg, 0, sizeof(agg));
+    for (int p = 0; p < n; ++p) merge_stats(&agg, pst[p], p == 0);
+    agg.nnz_c = uint64_t(nnz);
+    agg.d2h_bytes += d2h;
+    agg.devices = n;
+    double* t = &stats->convert;
+    const double* u = &agg.convert;
+    for (int i = 0; i < 7; ++i) t[i] += u[i];
+    uint64_t* a = &stats->tiles_a;
+    const uint64_t* b = &agg.tiles_a;
+    for (int i = 0; i < 19; ++i) a[i] += b[i];
+    stats->nnz_c = agg.nnz_c;
+    stats->path = agg.path;
+    stats->devices = n;
+  }
+  return TSG_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -1389,8 +1800,44 @@ int tsg_create(tsg_ctx** out, int device, void* stream) {
   return TSG_OK;
 }
 
+int tsg_create_multi(tsg_ctx** out, int n, const int* devices) {
+  if (!out || n < 1 || n > 1024) return TSG_ERR_OTHER;
+  *out = nullptr;
+  auto* m = new tsg_ctx();
+  for (int i = 0; i < n; ++i) {
+    tsg_ctx* c = nullptr;
+    const int rc = tsg_create(&c, devices ? devices[i] : i, nullptr);
+    if (rc != TSG_OK) {
+      for (auto* x : m->sub) tsg_destroy(x);
+      m->sub.clear();
+      delete m;
+      return rc;
+    }
+    m->sub.push_back(c);
+  }
+  // the front context: device, stream, pool and pinned cache of panel 0
+  m->device = m->sub[0]->device;
+  m->stream = m->sub[0]->stream;
+  m->pool = m->sub[0]->pool;
+  cudaSetDevice(m->device);
+  *out = m;
+  return TSG_OK;
+}
+
+int tsg_last_panel_ms(const tsg_ctx* ctx, double* out, int n) {
+  if (!ctx) return 0;
+  const int k = int(ctx->panel_ms.size());
+  for (int i = 0; i < k && i < n && out; ++i) out[i] = ctx->panel_ms[i];
+  return k;
+}
+
 int tsg_destroy(tsg_ctx* ctx) {
   if (!ctx) return TSG_OK;
+  if (!ctx->sub.empty()) {  // a multi-device front: everything belongs to the panel contexts
+    for (auto* c : ctx->sub) tsg_destroy(c);
+    delete ctx;
+    return TSG_OK;
+  }
   cudaStreamSynchronize(ctx->stream);
   for (auto& e : ctx->ev)
     if (e) cudaEventDestroy(e);
@@ -1427,6 +1874,10 @@ int tsg_spgemm(tsg_ctx* ctx, const tsg_csr* A, const tsg_csr* B, tsg_csr_out* C,
   if (C) C->_owner = nullptr;
   try {
     TSG_CUDA(cudaSetDevice(ctx->device));
+    if (!ctx->sub.empty()) {
+      const tsg_csr* X[2] = {A, B};
+      return spgemm_multi(ctx, 2, X, C, o, stats);
+    }
     spgemm_impl(ctx, A, B, C, o, stats, o.want_tiles ? tiles : nullptr);
     return TSG_OK;
   } catch (const Fail& f) {
@@ -1452,6 +1903,15 @@ int tsg_spgemm_chain(tsg_ctx* ctx, int n, const tsg_csr* const* X, tsg_csr_out* 
   if (opt) o = *opt;
   o.want_tiles = 0;
   ctx->err.clear();
+  if (!ctx->sub.empty()) {
+    try {
+      TSG_CUDA(cudaSetDevice(ctx->device));
+      return spgemm_multi(ctx, n, X, C, o, stats);
+    } catch (const Fail& f) {
+      ctx->err = f.msg;
+      return f.code;
+    }
+  }
   // Left to right.  Between stages the intermediate is rounded to binary16
   // (kernels.cpp:239-258).  When a stage takes the light-row path its result
   // goes to the next stage directly as A tiles (the downcast fused into the
@@ -1536,8 +1996,10 @@ int tsg_spgemm_chain(tsg_ctx* ctx, int n, const tsg_csr* const* X, tsg_csr_out* 
 
 void tsg_free_csr(tsg_ctx* ctx, tsg_csr_out* C) {
   if (!ctx) return;
-  free_out(ctx, C);
-  cudaStreamSynchronize(ctx->stream);
+  tsg_ctx* c = ctx->sub.empty() ? ctx : ctx->sub[0];  // a multi-device output lives on panel 0's device
+  cudaSetDevice(c->device);
+  free_out(c, C);
+  cudaStreamSynchronize(c->stream);
 }
 
 void tsg_free_tiles(tsg_tiles_out* t) {
@@ -1552,6 +2014,11 @@ void tsg_free_tiles(tsg_tiles_out* t) {
 
 int tsg_cbar(tsg_ctx* ctx, const tsg_csr* A, const tsg_csr* B, uint64_t* cbar) {
   if (!ctx || !cbar) return TSG_ERR_OTHER;
+  if (!ctx->sub.empty()) {
+    const int rc = tsg_cbar(ctx->sub[0], A, B, cbar);
+    ctx->err = ctx->sub[0]->err;
+    return rc;
+  }
   ctx->err.clear();
   try {
     check_csr(A, "A");
@@ -1574,10 +2041,16 @@ int tsg_cbar(tsg_ctx* ctx, const tsg_csr* A, const tsg_csr* B, uint64_t* cbar) {
   }
 }
 
-uint64_t tsg_launch_count(const tsg_ctx* ctx) { return ctx ? ctx->launches : 0; }
+uint64_t tsg_launch_count(const tsg_ctx* ctx) {
+  if (!ctx) return 0;
+  uint64_t n = ctx->launches;
+  for (auto* c : ctx->sub) n += c->launches;
+  return n;
+}
 
 double tsg_last_kernel_ms(const tsg_ctx* ctx, const char* phase) {
   if (!ctx || !phase) return 0.0;
+  if (!ctx->sub.empty()) return tsg_last_kernel_ms(ctx->sub[0], phase);
   if (std::strcmp(phase, "numeric_kernel") == 0) return ctx->last_numeric_kernel_ms;
   if (std::strcmp(phase, "assemble_kernel") == 0) return ctx->last_assemble_kernel_ms;
   static const char* names[] = {"", "convert", "task_list", "sort", "counting", "multiply",

@@ -100,6 +100,8 @@ enum ErrBits : unsigned {
   kErrPrecision = 4u,  // non-finite accumulator
   kCancelled = 8u,     // an output slot cancelled to exactly 0 (compaction needed)
   kErrPool = 16u,      // general path: the overflow-piece pool was too small (the host reruns)
+  kErrRowPtr = 32u,    // row_ptr[0] != 0, row_ptr[rows] != nnz or decreasing: no kernel reads the
+                       // entries (an InvariantError, like validate_coo, tile_format.cpp:34-51)
 };
 
 __device__ __forceinline__ unsigned lanemask_lt() {

@@ -301,6 +301,10 @@ __global__ void __launch_bounds__(256, 4) convert_fast_kernel(CsrView in, uint32
   }
   const uint32_t I = blockIdx.x * 8 + wib;
   if (I >= tile_rows) return;
+  if (*err_flag & kErrRowPtr) {  // malformed row pointers (validate_rowptr_kernel): no tiles, no reads
+    if (lane == 0) out.ntiles[I] = 0;
+    return;
+  }
   FastSmem& sm = smem[wib];
   const int64_t r0 = int64_t(I) * kTile, r1 = r0 + kTile < in.rows ? r0 + kTile : in.rows;
   const int64_t row = r0 + lane;
@@ -792,7 +796,28 @@ __global__ void cbar_dot_kernel(const unsigned* __restrict__ hist, const int64_t
   if ((threadIdx.x & 31) == 0 && acc) atomicAdd(out, acc);
 }
 
+// row_ptr[0] == 0, row_ptr[rows] == nnz, non-decreasing: checked before any
+// kernel indexes the entries through it (every later reader is gated on
+// kErrRowPtr).  Thread per row pointer.
+__global__ void validate_rowptr_kernel(const int64_t* __restrict__ rp, int64_t rows, int64_t nnz,
+                                       unsigned* __restrict__ err_flag) {
+  bool bad = false;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i <= rows; i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t v = rp[i];
+    if (i == 0) bad |= v != 0;
+    if (i == rows) bad |= v != nnz;
+    else bad |= rp[i + 1] < v;
+  }
+  if (__any_sync(kFull, bad) && (threadIdx.x & 31) == 0) atomicOr(err_flag, unsigned(kErrRowPtr));
+}
+
 }  // namespace
+
+void launch_validate_rowptr(const CsrView& in, unsigned* err_flag, cudaStream_t st) {
+  const int64_t n = in.rows + 1;
+  const unsigned blocks = unsigned(std::min<int64_t>((n + 255) / 256, 2368));
+  validate_rowptr_kernel<<<blocks, 256, 0, st>>>(in.row_ptr, in.rows, in.nnz, err_flag);
+}
 
 void launch_convert(const CsrView& in, TileMat& out, int roles, const ConvertScratch& cs, unsigned* err_flag,
                     int drop_nonfinite, const uint8_t* needed, cudaStream_t st) {

@@ -35,6 +35,8 @@ struct ConvertScratch {
   uint32_t* walk_count = nullptr;      // 1, zeroed
   uint8_t* mark = nullptr;             // optional, zeroed: set for every tile column
 };
+// sets kErrRowPtr in err_flag unless row_ptr[0] == 0, row_ptr[rows] == nnz and non-decreasing
+void launch_validate_rowptr(const CsrView& in, unsigned* err_flag, cudaStream_t st);
 void launch_convert(const CsrView& in, TileMat& out, int roles, const ConvertScratch& cs, unsigned* err_flag,
                     int drop_nonfinite, const uint8_t* needed, cudaStream_t st);
 // max_row_tiles (nullable): atomicMax of the tiles per tile row
@@ -77,8 +79,9 @@ cudaError_t launch_panel_numeric(const TileMat& A, const TileMat& B, int64_t row
                                  const unsigned* gate = nullptr, unsigned* work = nullptr, int nl = 1);
 // row_bound[r] = min(B.cols, sum over A's entries (r, k) of nnz(B row k));
 // *total += sum of row_bound
+// (gate: the call's error flags; malformed row pointers -> all bounds 0)
 void launch_elem_bound(const CsrView& A, const int64_t* rpB, int64_t bcols, uint32_t* row_bound,
-                       unsigned long long* total, cudaStream_t st);
+                       unsigned long long* total, const unsigned* gate, cudaStream_t st);
 void launch_emit_compact(uint32_t tile_rows, const TileEmit& em, const uint32_t* trp, TileMat& T, cudaStream_t st);
 // bound[I] = min(B.tile_cols, raw pairs of A's tile row I): output tiles of the row at most
 void launch_row_tile_bound(const TileMat& A, const TileMat& B, uint32_t* bound, cudaStream_t st);

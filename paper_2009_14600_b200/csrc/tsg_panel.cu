@@ -143,11 +143,14 @@ __global__ void __launch_bounds__(256) panel_count_kernel(TileMat A, TileMat B, 
 // nothing (the conversion flags them).
 __global__ void __launch_bounds__(256) elem_bound_kernel(CsrView A, const int64_t* __restrict__ rpB,
                                                         int64_t bcols, uint32_t* __restrict__ row_bound,
-                                                        unsigned long long* __restrict__ total) {
+                                                        unsigned long long* __restrict__ total,
+                                                        const unsigned* __restrict__ gate) {
   __shared__ unsigned long long s_sum[8];
   const int64_t r = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
   uint64_t b = 0;
-  if (r < A.rows) {
+  if (r < A.rows && (*gate & kErrRowPtr)) {
+    row_bound[r] = 0;
+  } else if (r < A.rows) {
     const int64_t e0 = __ldg(A.row_ptr + r), e1 = __ldg(A.row_ptr + r + 1);
     uint64_t sum = 0;
 #pragma unroll 4
@@ -275,7 +278,7 @@ __global__ void __launch_bounds__(256, kMinBlocks) panel_numeric_kernel(TileMat 
   if (!kEmit && (*need > stage_cap || (*need >> 32))) return;  // arena too small: the host reruns the pass
   // speculative launch: {error flags, max A tiles per tile row} of the
   // conversion; invalid input or rows that are not light -> nothing to do
-  if (gate && ((gate[0] & kErrInvariant) || gate[1] > 32u * NL)) return;
+  if (gate && ((gate[0] & (kErrInvariant | kErrRowPtr)) || gate[1] > 32u * NL)) return;
   const uint4* cA = A.chunk[kRoleA];
   const uint4* cB = B.chunk[kRoleB];
   const unsigned lt = lanemask_lt(), bit = 1u << lane;
@@ -533,10 +536,10 @@ void launch_panel_count(const TileMat& A, const TileMat& B, int64_t rows, uint32
 }
 
 void launch_elem_bound(const CsrView& A, const int64_t* rpB, int64_t bcols, uint32_t* row_bound,
-                       unsigned long long* total, cudaStream_t st) {
+                       unsigned long long* total, const unsigned* gate, cudaStream_t st) {
   const unsigned blocks = unsigned((A.rows + 255) / 256);
   if (blocks == 0) return;
-  elem_bound_kernel<<<blocks, 256, 0, st>>>(A, rpB, bcols, row_bound, total);
+  elem_bound_kernel<<<blocks, 256, 0, st>>>(A, rpB, bcols, row_bound, total, gate);
 }
 
 namespace {

@@ -116,6 +116,10 @@ def _view(M: Csr, keep: list) -> L.tsg_csr:
         col = M.col.contiguous().to(torch.int32)
         val = M.val.contiguous()
         keep += [rp, col, val]
+        # the conversions above (and whatever produced M) are queued on torch's
+        # current stream; the library runs on its own stream, so they must be
+        # complete before it reads the arrays
+        torch.cuda.current_stream(val.device).synchronize()
         v.row_ptr, v.col, v.val = rp.data_ptr(), col.data_ptr(), val.data_ptr()
         v.dtype = tdt[val.dtype]
         v.mem = L.TSG_MEM_DEVICE
@@ -140,12 +144,21 @@ def _np_from(ptr: int, n: int, dtype) -> np.ndarray:
 
 
 class Context:
-    """One tsg_ctx (device + stream + memory pool).  One per host thread."""
+    """One tsg_ctx (device + stream + memory pool).  One per host thread.
 
-    def __init__(self, device: int = -1, stream: int | None = None):
+    ``devices=[d0, d1, ...]`` makes a multi-device context (tsg_create_multi):
+    every call splits A into len(devices) work-balanced tile-row panels, one
+    per listed GPU (an ordinal may repeat), and concatenates the result."""
+
+    def __init__(self, device: int = -1, stream: int | None = None, devices: list | None = None):
         self._lib = L.load()
         h = C.c_void_p()
-        rc = self._lib.tsg_create(C.byref(h), device, C.c_void_p(stream) if stream else None)
+        if devices is not None:
+            arr = (C.c_int * len(devices))(*devices)
+            rc = self._lib.tsg_create_multi(C.byref(h), len(devices), arr)
+        else:
+            rc = self._lib.tsg_create(C.byref(h), device, C.c_void_p(stream) if stream else None)
+        self.n_panels = len(devices) if devices is not None else 1
         if rc != L.TSG_OK:
             raise Error(f"tsg_create failed ({rc})")
         self._h = h
@@ -248,6 +261,12 @@ class Context:
 
     def last_phase_ms(self, phase: str) -> float:
         return float(self._lib.tsg_last_kernel_ms(self._h, phase.encode()))
+
+    def panel_ms(self) -> list:
+        """Per-panel device times (ms) of the last call of a multi-device context."""
+        buf = (C.c_double * max(1, self.n_panels))()
+        k = self._lib.tsg_last_panel_ms(self._h, buf, self.n_panels)
+        return [float(buf[i]) for i in range(k)]
 
 
 class _CAI:

@@ -183,6 +183,22 @@ def amg(n: int = 128):
     return transpose(P), A, P
 
 
+def sample_tile_rows(A: Csr, stride: int) -> Csr:
+    """Every `stride`-th 16-row tile row of A (a strided row sample that keeps
+    the skew of the full matrix; bench.py's bounded CPU-reference sample)."""
+    if stride <= 1:
+        return A
+    rp = np.asarray(A.row_ptr, dtype=np.int64)
+    tr = np.arange(0, (A.rows + 15) // 16, stride, dtype=np.int64)
+    rows = (tr[:, None] * 16 + np.arange(16, dtype=np.int64)[None, :]).ravel()
+    rows = rows[rows < A.rows]
+    lens = rp[rows + 1] - rp[rows]
+    new_rp = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    # entry p of sampled row i comes from rp[rows[i]] + (p - new_rp[i])
+    idx = np.repeat(rp[rows] - new_rp[:-1], lens) + np.arange(int(new_rp[-1]), dtype=np.int64)
+    return Csr(len(rows), A.cols, new_rp, np.asarray(A.col)[idx], np.asarray(A.val)[idx])
+
+
 def cbar(A: Csr, B: Csr) -> int:
     """sum_k nnzA(:,k) * nnzB(k,:) (analytics.cpp:51-65 generalised)."""
     colc = np.bincount(np.asarray(A.col), minlength=A.cols).astype(np.int64)

@@ -5,6 +5,7 @@
 // Built by __graft_entry__.build(); run on the GPU by tests/test_gpu_shim.py.
 #include <bit>
 #include <cstdio>
+#include <cmath>
 #include <cstdlib>
 #include <map>
 #include <string>
@@ -155,6 +156,57 @@ int main() {
     ElementCoo RA = oracle(R, A);
     const ElementCoo want = oracle(RA, P);  // oracle rounds RA to binary16 on entry
     report(bit_equal(spgemm_chain({R, A, P}, true), want), "R.A.P chain", "48^3 ordered");
+  }
+  // gate: validate_coo (tile_format.hpp:66-69) -- unsorted, duplicated and
+  // out-of-range entries raise InvariantError before anything runs
+  {
+    int raised = 0;
+    ElementCoo bad;
+    bad.rows = bad.cols = 8;
+    bad.entries = {{1, 0, 1.0}, {0, 5, 1.0}};  // unsorted rows
+    try { spgemm(bad, bad); } catch (const InvariantError&) { ++raised; }
+    bad.entries = {{0, 3, 1.0}, {0, 3, 2.0}};  // duplicate
+    try { (void)from_element_coo(bad, ElementKind::Fp16Stored); } catch (const InvariantError&) { ++raised; }
+    bad.entries = {{0, 8, 1.0}};  // out of range
+    try { validate_coo(bad); } catch (const InvariantError&) { ++raised; }
+    report(raised == 3, "validate_coo -> InvariantError", std::to_string(raised) + "/3 raised");
+  }
+  // gate: from_element_coo(..., drop_nonfinite) (tile_format.cpp:82-86 contract)
+  {
+    ElementCoo m;
+    m.rows = m.cols = 16;
+    m.entries = {{0, 0, 2.0}, {0, 9, INFINITY}, {3, 3, 1e-9}, {9, 1, -0.5}};
+    bool raised = false;
+    try { (void)from_element_coo(m, ElementKind::Fp16Stored); } catch (const OverflowError&) { raised = true; }
+    const TiledMatrix t = from_element_coo(m, ElementKind::Fp16Stored, true);
+    const ElementCoo back = to_element_coo(t);
+    // inf dropped, 1e-9 underflows binary16 and drops, the rest round-trips
+    const bool ok = raised && back.entries.size() == 2 && back.entries[0].col == 0 && back.entries[1].row == 9 &&
+                    back.entries[1].value == -0.5 && t.tiles.size() == 2;
+    report(ok, "drop_nonfinite + underflow drop + round trip", std::to_string(back.entries.size()) + " entries");
+  }
+  // gate: to_element_coo(from_element_coo(x)) == x for a binary16 matrix, and
+  // SquareResult carries the device memory report and the GPU count
+  {
+    const ElementCoo coo = random_coo(200, 0.03);
+    const TiledMatrix A = from_element_coo(coo, ElementKind::Fp16Stored);
+    const bool rt = bit_equal(to_element_coo(A), coo);
+    const SquareResult r = spgemm_square(A);
+    const bool mem = r.memory.peak_bytes > 0 && r.memory.output_bytes > 0 && r.memory.input_tiles_bytes > 0 &&
+                     r.threads_used == 1;
+    report(rt && mem, "tiling round trip + MemoryReport",
+           "peak " + std::to_string(r.memory.peak_bytes) + " B, threads_used " + std::to_string(r.threads_used));
+  }
+  // gate: a multi-device context (several panel workers on GPU 0) returns the
+  // single-device product bit for bit
+  {
+    const ElementCoo A = random_coo(300, 0.02), B = random_coo(300, 0.02);
+    Context multi(std::vector<int>{0, 0, 0});
+    tsg_run_stats st{};
+    const ElementCoo one = spgemm(A, B, true);
+    const ElementCoo three = spgemm(A, B, true, &st, multi);
+    report(bit_equal(one, three) && st.devices == 3, "multi-device panels == one device",
+           std::to_string(one.entries.size()) + " entries, devices " + std::to_string(st.devices));
   }
   return failures;
 }

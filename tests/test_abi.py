@@ -28,7 +28,7 @@ def test_library_exports_every_symbol():
     lib = L.load()
     for name in declared():
         assert hasattr(lib, name), name
-    assert lib.tsg_abi_version() == 2
+    assert lib.tsg_abi_version() == 3
 
 
 def test_library_has_no_cpu_fallback_symbols():

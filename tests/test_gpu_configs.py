@@ -45,7 +45,7 @@ def test_config_full_size(ctx, name):
         assert np.allclose(res.C.val, want.val, rtol=2 ** -21, atol=0)
     else:
         assert csr_bits_equal(res.C, want), first_diff(res.C, want)
-    if name != "rmat":  # 6.8e9 raw tile pairs: too slow for the CPU restatement here
+    if name != "rmat":  # R-MAT (6.8e9 raw tile pairs): test_gpu_r02.py::test_rmat_full_size_t16_counters
         st16 = port.tile_stats(A, B, 16)
         for k in ("tiles_a", "raw_pairs", "filtered_pairs", "segments", "counted_elements"):
             assert res.stats[k] == st16[k], k

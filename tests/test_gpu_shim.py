@@ -17,4 +17,4 @@ def test_cpp_shim_acceptance():
     r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
     print(r.stdout)
     assert r.returncode == 0, r.stdout + r.stderr
-    assert r.stdout.count("PASS") >= 5
+    assert r.stdout.count("PASS") >= 9
