@@ -344,8 +344,12 @@ inline TiledMatrix read_tiled_binary(const std::filesystem::path& path) {
   return deserialize_tiled(detail::slurp(path, true));
 }
 
+// The reference CLI's output hash (proj/tools/tilemul.cpp:37-44): FNV-1a
+// with the 64-bit prime but the offset basis 1469598103934665603 (the
+// reference's constant, not the standard 14695981039346656037) -- kept so
+// hashes compare across the two front ends.
 inline std::uint64_t fnv1a(std::string_view bytes) {
-  std::uint64_t h = 0xcbf29ce484222325ull;  // FNV-1a 64 offset basis / prime
+  std::uint64_t h = 1469598103934665603ull;
   for (const unsigned char c : bytes) h = (h ^ c) * 0x100000001b3ull;
   return h;
 }

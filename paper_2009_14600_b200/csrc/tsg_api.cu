@@ -34,7 +34,7 @@
 #include "tsg_kernels.cuh"
 
 namespace tsg {
-constexpr int kGatherMax = 16;  // scalars per gathered readback
+constexpr int kGatherMax = 32;  // scalars per gathered readback
 constexpr int kPipeChunks = 16;  // max tile-row chunks of the pipelined host-output path (TSG_PIPE, default 8)
 int tuning_variant(const char* name, int dflt) {
   const char* v = std::getenv(name);
@@ -1167,6 +1167,11 @@ struct Call {
     check_launch(ctx, 2);
     record(ctx, timing, 2);
     uint64_t nrecs = 0, nunits = 0, products = 0;
+    // host output of a large product: the tile rows run in chunks whose CSR
+    // slices cross PCIe while later chunks compute (the chunks' record and
+    // unit boundaries come with this readback)
+    const int nch = owner->host && !pre_a && TA.tile_rows >= 8u * uint32_t(pipe_chunks()) ? pipe_chunks() : 0;
+    uint32_t cut_rec[kPipeChunks + 1] = {}, cut_unit[kPipeChunks + 1] = {};
     {
       ScalarGather sg;
       sg.p[0] = rbase + nr - 1;
@@ -1174,11 +1179,20 @@ struct Call {
       sg.p[2] = tot;
       sg.wide = 0x4u;
       sg.n = 3;
-      unsigned long long v[3];
+      for (int c = 0; c <= nch && nch; ++c) {
+        const uint32_t I = uint32_t(uint64_t(TA.tile_rows) * c / nch);
+        sg.p[sg.n++] = rbase + I;
+        sg.p[sg.n++] = wbase + I;
+      }
+      unsigned long long v[kGatherMax];
       readback_gather(ctx, sc, sg, v);
       nrecs = v[0];
       nunits = v[1];
       products = v[2];
+      for (int c = 0; c <= nch && nch; ++c) {
+        cut_rec[c] = uint32_t(v[3 + 2 * c]);
+        cut_unit[c] = uint32_t(v[4 + 2 * c]);
+      }
     }
     uint4* units;
     {
@@ -1203,6 +1217,7 @@ struct Call {
     g.work = reinterpret_cast<unsigned*>(ctr);
     g.stage_top = ctr + 1;
     uint64_t pool = std::max<uint64_t>(4096, nunits / 8);
+    if (nch && general_host_pipelined(g, nch, cut_rec, cut_unit, nrecs, pool, products, rbase)) return;
     unsigned long long t[4];
     for (int attempt = 0;; ++attempt) {
       g.pool_cap = uint32_t(std::min<uint64_t>(pool, 0xfffffff0ull - nrecs));
@@ -1237,6 +1252,124 @@ struct Call {
     check_launch(ctx);
     if (timing) TSG_CUDA(cudaEventRecord(ctx->kev[3], s));
     record(ctx, timing, 6);
+  }
+
+  // General rows, host output: the tile rows run in nch chunks (their units
+  // [cut_unit[c], cut_unit[c+1]) and output records [cut_rec[c],
+  // cut_rec[c+1])); chunk c's row pointers chain from chunk c-1's end on the
+  // device, its pieces are copied into CSR buffers sized by the product bound,
+  // and its slices go to the host on the copy stream while chunk c+1
+  // computes.  Returns false (nothing shipped) when the overflow-piece pool
+  // ran out: the caller then takes the unpipelined path with its retry.
+  bool general_host_pipelined(EscArgs& g, int nch, const uint32_t* cut_rec, const uint32_t* cut_unit, uint64_t nrecs,
+                              uint64_t pool, uint64_t products, const uint32_t* rbase) {
+    g.pool_cap = uint32_t(std::min<uint64_t>(pool, 0xfffffff0ull - nrecs));
+    {
+      MemRole role_tl(sc, kMemTaskList);
+      g.pieces = sc.alloc<EscPiece>(nrecs + g.pool_cap);
+    }
+    auto* ctr = sc.alloc<unsigned long long>(2);
+    g.work = reinterpret_cast<unsigned*>(ctr);
+    g.stage_top = ctr + 1;
+    TSG_CUDA(cudaMemsetAsync(ctr, 0, 2 * sizeof(unsigned long long), s));
+    TSG_CUDA(cudaMemsetAsync(d_rp, 0, sizeof(int64_t), s));
+    const uint64_t bound = std::max<uint64_t>(products, 1);
+    {
+      MemRole role_out(sc, kMemOutput);
+      d_col = sc.alloc<int32_t>(bound);
+      d_val = sc.alloc<float>(bound);
+    }
+    owner->p[0] = pinned_alloc(ctx, (rows + 1) * sizeof(int64_t), &owner->sz[0]);
+    owner->p[1] = pinned_alloc(ctx, bound * sizeof(int32_t), &owner->sz[1]);
+    owner->p[2] = pinned_alloc(ctx, bound * sizeof(float), &owner->sz[2]);
+    auto* ends = reinterpret_cast<int64_t*>(ctx->pinned_pipe);
+    auto* flag_h = reinterpret_cast<unsigned*>(reinterpret_cast<char*>(ctx->pinned_pipe) + 8 * (kPipeChunks + 1));
+    size_t tmp_bytes = 0;
+    TSG_CUDA(cub::DeviceScan::ExclusiveScan(nullptr, tmp_bytes, rowcnt, d_rp, cuda::std::plus<int64_t>(),
+                                            cub::FutureValue<int64_t>(d_rp), rows + 1, s));
+    void* tmp = sc.alloc<char>(tmp_bytes);
+    int64_t cr0[kPipeChunks], cr1[kPipeChunks];
+    if (timing) TSG_CUDA(cudaEventRecord(ctx->kev[0], s));
+    for (int c = 0; c < nch; ++c) {
+      const uint32_t I0 = uint32_t(uint64_t(TA.tile_rows) * c / nch);
+      const uint32_t I1 = uint32_t(uint64_t(TA.tile_rows) * (c + 1) / nch);
+      cr0[c] = int64_t(I0) * 16;
+      cr1[c] = std::min<int64_t>(int64_t(I1) * 16, rows);
+      g.unit0 = cut_unit[c];
+      g.unit_end = cut_unit[c + 1];
+      TSG_CUDA(cudaMemsetAsync(g.work, 0, sizeof(unsigned), s));
+      launch_esc(g, ctx->device, s);
+      launch_esc_rowcount(g, rbase, rowcnt, s, I0, I1);
+      check_launch(ctx, 2);
+      TSG_CUDA(cub::DeviceScan::ExclusiveScan(tmp, tmp_bytes, rowcnt + cr0[c], d_rp + cr0[c],
+                                              cuda::std::plus<int64_t>(), cub::FutureValue<int64_t>(d_rp + cr0[c]),
+                                              cr1[c] - cr0[c] + 1, s));
+      launch_esc_copy_records(g, cut_rec[c], cut_rec[c + 1], d_rp, d_col, d_val, s);
+      publish_chunk_kernel<<<1, 1, 0, s>>>(d_rp + cr1[c], err_flag, ends + c, flag_h + c);
+      check_launch(ctx, 2);
+      TSG_CUDA(cudaEventRecord(ctx->pipe_ev[c], s));
+    }
+    if (timing) TSG_CUDA(cudaEventRecord(ctx->kev[1], s));
+    // each chunk's slices to the host as soon as it is computed
+    int32_t* h_col = static_cast<int32_t*>(owner->p[1]);
+    float* h_val = static_cast<float*>(owner->p[2]);
+    int64_t* h_rp = static_cast<int64_t*>(owner->p[0]);
+    uint64_t sent = 0, d2h_bytes = 0;
+    bool pool_short = false;
+    for (int c = 0; c < nch; ++c) {
+      TSG_CUDA(cudaEventSynchronize(ctx->pipe_ev[c]));
+      pool_short |= (flag_h[c] & kErrPool) != 0;
+      if (pool_short) break;
+      const uint64_t lo = sent, hi = uint64_t(ends[c]);
+      TSG_CUDA(cudaStreamWaitEvent(ctx->d2h, ctx->pipe_ev[c], 0));
+      TSG_CUDA(cudaMemcpyAsync(h_rp + cr0[c], d_rp + cr0[c], (cr1[c] - cr0[c]) * sizeof(int64_t),
+                               cudaMemcpyDeviceToHost, ctx->d2h));
+      d2h_bytes += (cr1[c] - cr0[c]) * sizeof(int64_t);
+      if (hi > lo) {
+        TSG_CUDA(cudaMemcpyAsync(h_col + lo, d_col + lo, (hi - lo) * 4, cudaMemcpyDeviceToHost, ctx->d2h));
+        TSG_CUDA(cudaMemcpyAsync(h_val + lo, d_val + lo, (hi - lo) * 4, cudaMemcpyDeviceToHost, ctx->d2h));
+        d2h_bytes += (hi - lo) * 8;
+      }
+      sent = hi;
+    }
+    TSG_CUDA(cudaMemcpyAsync(h_rp + rows, d_rp + rows, sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->d2h));
+    TSG_CUDA(cudaEventRecord(ctx->pipe_ev[kPipeChunks], ctx->d2h));
+    TSG_CUDA(cudaStreamWaitEvent(s, ctx->pipe_ev[kPipeChunks], 0));
+    if (pool_short) {  // pathological column skew: give the buffers back, rerun unpipelined
+      TSG_CUDA(cudaStreamSynchronize(ctx->d2h));
+      for (int i = 0; i < 3; ++i) {
+        ctx->pinned_free.emplace_back(owner->p[i], owner->sz[i]);
+        owner->p[i] = nullptr;
+      }
+      TSG_CUDA(cudaMemsetAsync(counted_d, 0, sizeof(unsigned long long), s));
+      TSG_CUDA(cudaMemsetAsync(g.segs, 0, sizeof(unsigned long long), s));
+      TSG_CUDA(cudaMemsetAsync(g.piece_top, 0, sizeof(uint32_t), s));
+      TSG_CUDA(cudaMemsetAsync(err_flag, 0, sizeof(unsigned), s));
+      g.unit0 = 0;
+      g.unit_end = 0xffffffffu;
+      return false;
+    }
+    record(ctx, timing, 5);
+    // statistics: segments, raw and filtered pairs (tot[1..3]), counted; nnz(C)
+    const unsigned long long* src[4] = {g.segs, g.segs + 1, g.segs + 2, counted_d};
+    unsigned long long v[4];
+    readback_many(ctx, src, v);
+    S = v[0];
+    raw = v[1];
+    P = v[2];
+    counted = v[3];
+    nnzC = int64_t(sent);
+    stage_total = products;
+    if (uint64_t(nnzC) >= (uint64_t(1) << 32))
+      throw Fail{TSG_ERR_OTHER, "output beyond 2^32 elements needs row-panel batching"};
+    if (st) st->d2h_bytes += sizeof(int64_t) + d2h_bytes;
+    host_done = true;
+    if (timing) {
+      TSG_CUDA(cudaEventRecord(ctx->kev[2], s));
+      TSG_CUDA(cudaEventRecord(ctx->kev[3], s));
+    }
+    record(ctx, timing, 6);
+    return true;
   }
 
   // ---- output hand-off, error flags, phase times and counters ----------------------

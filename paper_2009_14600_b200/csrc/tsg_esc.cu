@@ -53,19 +53,16 @@ constexpr uint32_t kGroupFlag = 0x80000000u;
 struct EscSmem {
   union {
     // the leaf's A entries with products in range (compacted): {first B
-    // entry in range, products << 8 | row within the unit (16 b + r), product
-    // prefix, A value (fp32 bits)}; entry ne is the sentinel {-, -, P, -}
-    uint4 t[kCap + 1];
+    // entry in range, product prefix | row within the unit (16 b + r) << 16}
+    // and the entry's A value (binary16 bits); entry ne is the sentinel {-, P}
+    struct {
+      uint2 t[kCap + 1];
+      uint16_t av[kCap + 1];
+    } tab;
     struct {
       uint32_t key[kCap];  // products: blocked, vectors rotated (phys())
       float val[kCap];
-      union {
-        uint32_t ctr[8 * kNT + 8 * kNT / 32];  // radix digit counters, [digit pair][thread], padded
-        struct {                               // realised entries, staging order, padded
-          uint32_t col[kCap + kCap / 32];
-          float val[kCap + kCap / 32];
-        } o;
-      } x;
+      uint32_t ctr[8 * kNT + 8 * kNT / 32];  // radix digit counters, [digit pair][thread], padded
     } s;
     struct {
       float acc[16 * kDenseW];
@@ -82,7 +79,6 @@ struct EscSmem {
 
 __device__ __forceinline__ uint32_t half_nz(uint16_t h) { return h & 0x7fffu; }
 __device__ __forceinline__ uint32_t cpad(uint32_t L) { return L + (L >> 5); }
-__device__ __forceinline__ uint32_t opad(uint32_t o) { return o + (o >> 5); }
 
 // Blocked layout: thread t owns items IPT t .. IPT t + IPT-1; its 16-byte
 // vectors are rotated so an LDS.128 phase of 8 lanes hits 8 bank groups.
@@ -160,13 +156,13 @@ __device__ __forceinline__ uint32_t radix_pass(EscSmem& sm, uint32_t (&key)[IPT]
     for (int j = 0; j < 8; ++j) w8[j] = uint32_t(j) == (d & 7u) ? (16u << (16 * (d >> 3))) : 0u;
   }
 #pragma unroll
-  for (int j = 0; j < 8; ++j) sm.s.x.ctr[cpad(j * kNT + tid)] = w8[j];
+  for (int j = 0; j < 8; ++j) sm.s.ctr[cpad(j * kNT + tid)] = w8[j];
   __syncthreads();
   // raking: thread t sums the linear counters 8t .. 8t+7 (digit-major order)
   uint32_t v[8], sum = 0;
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
-    v[i] = sm.s.x.ctr[cpad(8 * tid + i)];
+    v[i] = sm.s.ctr[cpad(8 * tid + i)];
     sum += v[i];
   }
   uint32_t inc = sum;
@@ -186,7 +182,7 @@ __device__ __forceinline__ uint32_t radix_pass(EscSmem& sm, uint32_t (&key)[IPT]
   }
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
-    sm.s.x.ctr[cpad(8 * tid + i)] = run;
+    sm.s.ctr[cpad(8 * tid + i)] = run;
     run += v[i];
   }
   __syncthreads();
@@ -195,7 +191,7 @@ __device__ __forceinline__ uint32_t radix_pass(EscSmem& sm, uint32_t (&key)[IPT]
   for (int i = 0; i < IPT; ++i) {
     if ((vm >> i) & 1u) {
       const uint32_t d = (key[i] >> shift) & 15u;
-      const uint32_t p = sm.s.x.ctr[cpad((d & 7u) * kNT + tid)];
+      const uint32_t p = sm.s.ctr[cpad((d & 7u) * kNT + tid)];
       const uint32_t dst = (d < 8 ? (p & 0xffffu) : (p >> 16) + tlo) + uint32_t((rk >> (4 * i)) & 15u);
       const uint32_t q = phys<IPT>(dst);
       sm.s.key[q] = key[i];
@@ -252,9 +248,10 @@ struct PieceChain {
   uint32_t prev = kNoPiece;  // last record written by this unit
 };
 
-// The leaf's realised entries are in sm.s.x.o (staging order, n of them),
-// counts per (b, r) in sm.cnt: staging + records.  All threads.
-__device__ void write_pieces(EscSmem& sm, const EscArgs& g, const Unit& u, uint32_t n, PieceChain& pc) {
+// A leaf's output: thread 0 reserves n staging slots and the piece record
+// (published in sm.bc[0] = record, sm.bc[2..3] = staging base); the
+// entries are then written straight to global staging.  All threads.
+__device__ void begin_piece(EscSmem& sm, const EscArgs& g, const Unit& u, uint32_t n, PieceChain& pc) {
   const int tid = threadIdx.x;
   if (tid == 0) {
     const unsigned long long base = n ? atomicAdd(g.stage_top, (unsigned long long)n) : 0ull;
@@ -277,6 +274,12 @@ __device__ void write_pieces(EscSmem& sm, const EscArgs& g, const Unit& u, uint3
     sm.bc[3] = uint32_t(base >> 32);
   }
   __syncthreads();
+}
+
+// The piece records (realised entries per row from sm.cnt[b][r]); the
+// trailing barrier frees shared memory for the next leaf.
+__device__ void end_piece(EscSmem& sm, const EscArgs& g, const Unit& u) {
+  const int tid = threadIdx.x;
   const uint32_t rec = sm.bc[0];
   const unsigned long long base = (unsigned long long)sm.bc[2] | ((unsigned long long)sm.bc[3] << 32);
   if (rec != kNoPiece && tid < int(u.nb)) {  // thread b: the record of tile row I + b
@@ -290,15 +293,46 @@ __device__ void write_pieces(EscSmem& sm, const EscArgs& g, const Unit& u, uint3
 #pragma unroll
     for (int r = 0; r < 16; ++r) p.cnt[r] = sm.cnt[tid * 16 + r];
   }
-  if (rec != kNoPiece)
-    for (uint32_t o = tid; o < n; o += kNT) {
-      const uint32_t q = opad(o);
-      g.stage[base + o] = make_uint2(sm.s.x.o.col[q], __float_as_uint(sm.s.x.o.val[q]));
-    }
   __syncthreads();
 }
 
+__device__ __forceinline__ unsigned long long piece_base(const EscSmem& sm) {
+  return (unsigned long long)sm.bc[2] | ((unsigned long long)sm.bc[3] << 32);
+}
+
+// Lockstep lower bounds: for each k, the first index of [b0[k], b1[k]) whose
+// column is >= c[k] (returned in b0).  The K searches issue their loads
+// together, so their latency chains overlap.
+template <int K>
+__device__ __forceinline__ void lower_cols(const int32_t* __restrict__ colB, uint32_t (&b0)[K], uint32_t (&b1)[K],
+                                           const uint32_t (&c)[K]) {
+  while (true) {
+    bool any = false;
+    uint32_t m[K];
+    uint32_t v[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      m[k] = (b0[k] + b1[k]) >> 1;
+      if (b0[k] < b1[k]) {
+        v[k] = uint32_t(__ldg(colB + m[k]));
+        any = true;
+      }
+    }
+    if (!any) break;
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+      if (b0[k] < b1[k]) {
+        if (v[k] < c[k])
+          b0[k] = m[k] + 1;
+        else
+          b1[k] = m[k];
+      }
+  }
+}
+
 // The leaf's entry table; false (nothing built) when its products exceed kCap.
+// Thread t takes entries 2t and 2t+1 of each 2 kNT-entry round: their loads
+// and the four range searches (entry x {lo, hi}) run concurrently.
 __device__ bool build_table(EscSmem& sm, const EscArgs& g, const Unit& u, uint32_t lo, uint32_t hi,
                             uint32_t& P, uint32_t& ne) {
   const int tid = threadIdx.x;
@@ -307,50 +341,64 @@ __device__ bool build_table(EscSmem& sm, const EscArgs& g, const Unit& u, uint32
   const bool full = lo == 0 && int64_t(hi) >= g.colsB;
   P = 0;
   ne = 0;
-  for (int64_t e0 = E0; e0 < E1; e0 += kNT) {
-    const int64_t e = e0 + tid;
-    uint32_t len = 0, blo = 0, br = 0;
-    uint16_t a = 0;
-    if (e < E1) {
-      a = __ldg(g.hA + e);
-      if (half_nz(a)) {
-        const uint4 rb = __ldg(g.brec + __ldg(g.colA + e));  // {first entry, end, first col, last col}
-        blo = rb.x;
-        uint32_t bhi = rb.y;
-        if (!full && bhi > blo) {
-          if (rb.z >= hi || rb.w < lo) {
-            bhi = blo;
-          } else if (bhi - blo <= 8) {  // short row: its columns in one round trip
-            uint32_t c8[8];
+  for (int64_t e0 = E0; e0 < E1; e0 += 2 * kNT) {
+    int64_t e[2];
+    uint16_t a[2] = {0, 0};
+    int32_t ca[2] = {0, 0};
 #pragma unroll
-            for (int j = 0; j < 8; ++j) c8[j] = blo + j < bhi ? uint32_t(__ldg(g.colB + blo + j)) : 0xffffffffu;
-            uint32_t nlo = 0, nhi = 0;
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-              nlo += c8[j] < lo;
-              nhi += c8[j] < hi;
-            }
-            bhi = blo + nhi;
-            blo += nlo;
-          } else {
-            if (rb.z < lo) blo = lower_col(g.colB, blo, bhi, lo);
-            if (rb.w >= hi) bhi = lower_col(g.colB, blo, bhi, hi);
-          }
-        }
-        len = bhi - blo;
-        for (int b = 128; b > 0; b >>= 1)  // row within the unit: last rowp <= e
-          if (int(br) + b < nrow && sm.rowp[br + b] <= e) br += b;
+    for (int x = 0; x < 2; ++x) {
+      e[x] = e0 + 2 * tid + x;
+      if (e[x] < E1) {
+        a[x] = __ldg(g.hA + e[x]);
+        ca[x] = __ldg(g.colA + e[x]);
       }
     }
-    const uint32_t f0 = len > 0 ? 1u : 0u, l0 = len < uint32_t(kCap) ? len : uint32_t(kCap) + 1u;
-    uint32_t f = f0, lc = l0, ft, lt;
+    uint4 rb[2];
+#pragma unroll
+    for (int x = 0; x < 2; ++x)  // {first entry, end, first col, last col}
+      rb[x] = e[x] < E1 && half_nz(a[x]) ? __ldg(g.brec + ca[x]) : make_uint4(0, 0, 0, 0);
+    // searches: k = 2x (first entry >= lo), 2x+1 (first entry >= hi)
+    uint32_t s0[4], s1[4], sc[4];
+#pragma unroll
+    for (int x = 0; x < 2; ++x) {
+      const bool in = rb[x].y > rb[x].x && (full || (rb[x].z < hi && rb[x].w >= lo));
+      const bool need_lo = in && !full && rb[x].z < lo, need_hi = in && !full && rb[x].w >= hi;
+      s0[2 * x] = rb[x].x;
+      s1[2 * x] = need_lo ? rb[x].y : rb[x].x;
+      sc[2 * x] = lo;
+      s0[2 * x + 1] = in ? rb[x].x : rb[x].x;
+      s1[2 * x + 1] = need_hi ? rb[x].y : rb[x].x;
+      sc[2 * x + 1] = hi;
+      if (in && !need_hi) s0[2 * x + 1] = s1[2 * x + 1] = rb[x].y;  // the whole row tail is below hi
+    }
+    lower_cols<4>(g.colB, s0, s1, sc);
+    uint32_t len[2], blo[2], br[2];
+#pragma unroll
+    for (int x = 0; x < 2; ++x) {
+      blo[x] = s0[2 * x];
+      len[x] = s0[2 * x + 1] > blo[x] ? s0[2 * x + 1] - blo[x] : 0u;
+      br[x] = 0;
+      if (len[x])
+        for (int b = 128; b > 0; b >>= 1)  // row within the unit: last rowp <= e
+          if (int(br[x]) + b < nrow && sm.rowp[br[x] + b] <= e[x]) br[x] += b;
+    }
+    const uint32_t fa = len[0] > 0, fb = len[1] > 0;
+    const uint32_t la = min(len[0], uint32_t(kCap) + 1u), lb = min(len[1], uint32_t(kCap) + 1u);
+    uint32_t f = fa + fb, lc = la + lb, ft, lt;
     block_scan2(sm, f, lc, ft, lt);
     if (P + lt > uint32_t(kCap)) return false;
-    if (f0) sm.t[ne + f] = make_uint4(blo, (l0 << 8) | br, P + lc, __float_as_uint(__half2float(__ushort_as_half(a))));
+    if (fa) {
+      sm.tab.t[ne + f] = make_uint2(blo[0], (P + lc) | (br[0] << 16));
+      sm.tab.av[ne + f] = a[0];
+    }
+    if (fb) {
+      sm.tab.t[ne + f + fa] = make_uint2(blo[1], (P + lc + la) | (br[1] << 16));
+      sm.tab.av[ne + f + fa] = a[1];
+    }
     ne += ft;
     P += lt;
   }
-  if (tid == 0) sm.t[ne] = make_uint4(0u, 0u, P, 0u);
+  if (tid == 0) sm.tab.t[ne] = make_uint2(0u, P);
   __syncthreads();
   return true;
 }
@@ -378,13 +426,14 @@ __device__ void sort_leaf(EscSmem& sm, const EscArgs& g, const Unit& u, uint32_t
     uint32_t e = 0, top = ne;  // largest e with pre[e] <= g0
     while (top - e > 1) {
       const uint32_t m = (e + top) >> 1;
-      if (sm.t[m].z <= g0)
+      if ((sm.tab.t[m].y & 0xffffu) <= g0)
         e = m;
       else
         top = m;
     }
-    uint4 te = sm.t[e];
-    uint32_t nxt = sm.t[e + 1].z;
+    uint2 te = sm.tab.t[e];
+    uint32_t nxt = sm.tab.t[e + 1].y & 0xffffu;
+    float av = __half2float(__ushort_as_half(sm.tab.av[e]));
     // (1) B entry index of every item (shared memory only), the row in key[i]
     // and the A value in val[i]; (2) all the thread's global loads in flight at
     // once; (3) keys and exact products
@@ -395,12 +444,13 @@ __device__ void sort_leaf(EscSmem& sm, const EscArgs& g, const Unit& u, uint32_t
       idx[i] = 0;
       if (gi < P) {
         while (gi >= nxt) {
-          te = sm.t[++e];
-          nxt = sm.t[e + 1].z;
+          te = sm.tab.t[++e];
+          nxt = sm.tab.t[e + 1].y & 0xffffu;
+          av = __half2float(__ushort_as_half(sm.tab.av[e]));
         }
-        idx[i] = te.x + (gi - te.z);
-        key[i] = te.y & 0xffu;
-        val[i] = __uint_as_float(te.w);
+        idx[i] = te.x + (gi - (te.y & 0xffffu));
+        key[i] = te.y >> 16;
+        val[i] = av;
       }
     }
     uint32_t cc[IPT];
@@ -495,6 +545,7 @@ __device__ void sort_leaf(EscSmem& sm, const EscArgs& g, const Unit& u, uint32_t
   if (lane == 0 && nstruct) atomicAdd(&sm.bc[1], nstruct);
   uint32_t off = nreal, zero = 0, tot, dt;
   block_scan2(sm, off, zero, tot, dt);  // (its barriers also publish sm.cnt)
+  begin_piece(sm, g, u, tot, pc);
   // staging index = realised rank + adj[r][b]: the unit's tile rows one after
   // another, each row-major.  Thread t: group (r, b) = (t >> 4, t & 15) for the
   // rank of its first entry (entries of the groups before it in (r, b) order),
@@ -507,17 +558,17 @@ __device__ void sort_leaf(EscSmem& sm, const EscArgs& g, const Unit& u, uint32_t
     sm.adj[tid] -= int32_t(x);
   }
   __syncthreads();
-  // pass 2: write the realised entries at their staging index
-  {
+  // pass 2: write the realised entries at their staging index (global)
+  if (sm.bc[0] != kNoPiece) {
     bool owned = false;
     uint32_t kcur = 0, o = off;
     float s = 0.f;
     const uint32_t jmask = (1u << jb) - 1u;
+    uint2* __restrict__ dst = g.stage + piece_base(sm);
     auto emit = [&](float x) {
       if (x != 0.0f) {
-        const uint32_t q = opad(uint32_t(int32_t(o) + sm.adj[rb_of(kcur)]));
-        sm.s.x.o.col[q] = lo + (((kcur >> 8) & jmask) << 4) + ((kcur >> 4) & 15u);
-        sm.s.x.o.val[q] = x;
+        const uint32_t q = uint32_t(int32_t(o) + sm.adj[rb_of(kcur)]);
+        dst[q] = make_uint2(lo + (((kcur >> 8) & jmask) << 4) + ((kcur >> 4) & 15u), __float_as_uint(x));
         ++o;
       }
     };
@@ -537,14 +588,13 @@ __device__ void sort_leaf(EscSmem& sm, const EscArgs& g, const Unit& u, uint32_t
     }
     if (owned) emit(run_tail(kcur, s));
   }
-  __syncthreads();
-  if (tid == 0) {
+  if (tid == 0) {  // (bc[1], bc[7] are complete: block_scan2 and begin_piece synchronised since)
     segs += sm.bc[7];
     structural += sm.bc[1];
     sm.bc[7] = 0;
     sm.bc[1] = 0;
   }
-  write_pieces(sm, g, u, tot, pc);
+  end_piece(sm, g, u);
 }
 
 // Dense leaf (a heavy unit's <= 256 columns whose products exceed kCap):
@@ -603,30 +653,28 @@ __device__ void dense_leaf(EscSmem& sm, const EscArgs& g, const Unit& u, uint32_
   __syncthreads();  // the accumulators are in registers before the output aliases them
   uint32_t off = nreal, zero = 0, tot, dt;
   if (nreal) atomicAdd(&sm.cnt[row], nreal);
+  nst = __reduce_add_sync(kFull, nst);
+  if (lane == 0 && nst) atomicAdd(&sm.bc[1], nst);
   block_scan2(sm, off, zero, tot, dt);
-  {
+  begin_piece(sm, g, u, tot, pc);
+  if (sm.bc[0] != kNoPiece) {
+    uint2* __restrict__ dst = g.stage + piece_base(sm);
     uint32_t o = off;
 #pragma unroll
     for (int i = 0; i < 16; ++i)
-      if (v[i] != 0.0f) {
-        const uint32_t q = opad(o++);
-        sm.s.x.o.col[q] = lo + tc * 16 + i;
-        sm.s.x.o.val[q] = v[i];
-      }
+      if (v[i] != 0.0f) dst[o++] = make_uint2(lo + tc * 16 + i, __float_as_uint(v[i]));
   }
-  nst = __reduce_add_sync(kFull, nst);
-  if (lane == 0 && nst) atomicAdd(&sm.bc[1], nst);
-  __syncthreads();
   if (tid == 0) {
     segs += __popc(sm.bc[7]);
     structural += sm.bc[1];
     sm.bc[7] = 0;
     sm.bc[1] = 0;
   }
-  write_pieces(sm, g, u, tot, pc);
+  end_piece(sm, g, u);
 }
 
-__global__ void __launch_bounds__(kNT, 3) esc_kernel(EscArgs g) {
+template <int kMinBlocks>
+__global__ void __launch_bounds__(kNT, kMinBlocks) esc_kernel(EscArgs g) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   EscSmem& sm = *reinterpret_cast<EscSmem*>(smem_raw);
   const int tid = threadIdx.x;
@@ -635,9 +683,9 @@ __global__ void __launch_bounds__(kNT, 3) esc_kernel(EscArgs g) {
     sm.bc[1] = 0;
     sm.bc[7] = 0;
   }
-  const uint32_t nunits = *g.nunits;
+  const uint32_t nunits = min(*g.nunits, g.unit_end);
   for (;;) {
-    if (tid == 0) sm.bc[0] = atomicAdd(g.work, 1u);
+    if (tid == 0) sm.bc[0] = g.unit0 + atomicAdd(g.work, 1u);
     __syncthreads();
     const uint32_t ui = sm.bc[0];
     __syncthreads();
@@ -849,9 +897,9 @@ __global__ void __launch_bounds__(256) esc_plan_fill_kernel(uint32_t tile_rows, 
 // within the row.  Warp per tile row, lane r < 16 = row r.
 __global__ void __launch_bounds__(256) esc_rowcount_kernel(int64_t rows, uint32_t tile_rows,
                                                           const uint32_t* __restrict__ base, EscPiece* pieces,
-                                                          int64_t* __restrict__ rowcnt) {
+                                                          int64_t* __restrict__ rowcnt, uint32_t I0) {
   const int lane = threadIdx.x & 31;
-  const uint32_t I = blockIdx.x * 8 + (threadIdx.x >> 5);
+  const uint32_t I = I0 + blockIdx.x * 8 + (threadIdx.x >> 5);
   if (I >= tile_rows || lane >= 16) return;
   uint32_t acc = 0;
   for (uint32_t c = base[I]; c < base[I + 1]; ++c)
@@ -864,6 +912,41 @@ __global__ void __launch_bounds__(256) esc_rowcount_kernel(int64_t rows, uint32_
   if (row < rows) rowcnt[row] = acc;
 }
 
+// One staged piece -> its CSR slots: lanes over the piece's entries; entry q
+// belongs to the last row whose start within the piece is <= q.
+__device__ __forceinline__ void copy_piece(const EscPiece& pc, int lane, const uint2* __restrict__ stage,
+                                           const int64_t* __restrict__ row_ptr, int32_t* __restrict__ col,
+                                           float* __restrict__ val) {
+  const uint32_t cnt = lane < 16 ? pc.cnt[lane] : 0u;
+  const uint32_t ro = lane < 16 ? pc.roff[lane] : 0u;
+  uint32_t inc = cnt;  // each row's start within the piece
+#pragma unroll
+  for (int o = 1; o < 16; o <<= 1) {
+    const uint32_t v = __shfl_up_sync(kFull, inc, o);
+    if (lane >= o) inc += v;
+  }
+  const uint32_t total = __shfl_sync(kFull, inc, 15);
+  const uint32_t start = inc - cnt;
+  const int64_t dst0 = lane < 16 && cnt ? row_ptr[int64_t(pc.I) * 16 + lane] + ro : 0;
+  const unsigned long long off = pc.off;
+  for (uint32_t q0 = 0; q0 < total; q0 += 32) {
+    const uint32_t q = q0 + lane;
+    int r = 0;
+#pragma unroll
+    for (int b = 8; b > 0; b >>= 1) {
+      const uint32_t s = __shfl_sync(kFull, start, r + b);
+      if (s <= q) r += b;
+    }
+    const uint32_t sr = __shfl_sync(kFull, start, r);
+    const int64_t d = __shfl_sync(kFull, dst0, r);
+    if (q < total) {
+      const uint2 e = __ldg(stage + off + q);
+      col[d + (q - sr)] = int32_t(e.x);
+      val[d + (q - sr)] = __uint_as_float(e.y);
+    }
+  }
+}
+
 // staged pieces -> CSR: warp per piece
 __global__ void __launch_bounds__(256) esc_copy_kernel(const uint32_t* __restrict__ nrec,
                                                       const uint32_t* __restrict__ piece_top, uint32_t pool_cap,
@@ -873,38 +956,20 @@ __global__ void __launch_bounds__(256) esc_copy_kernel(const uint32_t* __restric
                                                       int32_t* __restrict__ col, float* __restrict__ val) {
   const int lane = threadIdx.x & 31;
   const uint32_t np = *nrec + min(*piece_top, pool_cap);
-  for (uint32_t p = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; p < np; p += (gridDim.x * blockDim.x) >> 5) {
-    const EscPiece& pc = pieces[p];
-    const uint32_t cnt = lane < 16 ? pc.cnt[lane] : 0u;
-    const uint32_t ro = lane < 16 ? pc.roff[lane] : 0u;
-    uint32_t inc = cnt;  // each row's start within the piece
-#pragma unroll
-    for (int o = 1; o < 16; o <<= 1) {
-      const uint32_t v = __shfl_up_sync(kFull, inc, o);
-      if (lane >= o) inc += v;
-    }
-    const uint32_t total = __shfl_sync(kFull, inc, 15);
-    const uint32_t start = inc - cnt;
-    const int64_t dst0 = lane < 16 && cnt ? row_ptr[int64_t(pc.I) * 16 + lane] + ro : 0;
-    const unsigned long long off = pc.off;
-    // lanes over the piece's entries; entry q belongs to the last row whose start <= q
-    for (uint32_t q0 = 0; q0 < total; q0 += 32) {
-      const uint32_t q = q0 + lane;
-      int r = 0;
-#pragma unroll
-      for (int b = 8; b > 0; b >>= 1) {
-        const uint32_t s = __shfl_sync(kFull, start, r + b);
-        if (s <= q) r += b;
-      }
-      const uint32_t sr = __shfl_sync(kFull, start, r);
-      const int64_t d = __shfl_sync(kFull, dst0, r);
-      if (q < total) {
-        const uint2 e = __ldg(stage + off + q);
-        col[d + (q - sr)] = int32_t(e.x);
-        val[d + (q - sr)] = __uint_as_float(e.y);
-      }
-    }
-  }
+  for (uint32_t p = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; p < np; p += (gridDim.x * blockDim.x) >> 5)
+    copy_piece(pieces[p], lane, stage, row_ptr, col, val);
+}
+
+// records [rec0, rec1) and the pool pieces chained after them: warp per record
+__global__ void __launch_bounds__(256) esc_copy_records_kernel(uint32_t rec0, uint32_t rec1,
+                                                              const EscPiece* __restrict__ pieces,
+                                                              const uint2* __restrict__ stage,
+                                                              const int64_t* __restrict__ row_ptr,
+                                                              int32_t* __restrict__ col, float* __restrict__ val) {
+  const int lane = threadIdx.x & 31;
+  for (uint32_t p = rec0 + ((blockIdx.x * blockDim.x + threadIdx.x) >> 5); p < rec1;
+       p += (gridDim.x * blockDim.x) >> 5)
+    for (uint32_t q = p; q != kNoPiece; q = pieces[q].next) copy_piece(pieces[q], lane, stage, row_ptr, col, val);
 }
 
 // ---------------------------------------------------------------- statistics
@@ -1053,22 +1118,33 @@ void launch_esc_plan_fill(const EscArgs& g, const unsigned long long* pre, const
 }
 
 void launch_esc(const EscArgs& g, int device, cudaStream_t st) {
-  static int per_sm[16] = {0}, sms[16] = {0};
-  const int d = device & 15;
+  // resident CTAs per SM: 3 (80 registers) or 4 (64 registers; TSG_ESC_MINB=4)
+  static int per_sm[16][2] = {}, sms[16] = {0};
+  const int d = device & 15, v = tuning_variant("TSG_ESC_MINB", 3) == 4 ? 1 : 0;
+  auto k = v ? esc_kernel<4> : esc_kernel<3>;
   const size_t smem = sizeof(EscSmem);
-  if (!per_sm[d]) {
-    cudaFuncSetAttribute(esc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  if (!per_sm[d][v]) {
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     int n = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, esc_kernel, kNT, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k, kNT, smem);
     cudaDeviceGetAttribute(&sms[d], cudaDevAttrMultiProcessorCount, device);
-    per_sm[d] = std::max(1, n);
+    per_sm[d][v] = std::max(1, n);
   }
-  esc_kernel<<<unsigned(per_sm[d] * sms[d]), kNT, smem, st>>>(g);
+  k<<<unsigned(per_sm[d][v] * sms[d]), kNT, smem, st>>>(g);
 }
 
-void launch_esc_rowcount(const EscArgs& g, const uint32_t* base, int64_t* rowcnt, cudaStream_t st) {
-  if (g.tile_rows == 0) return;
-  esc_rowcount_kernel<<<(g.tile_rows + 7) / 8, 256, 0, st>>>(g.rowsA, g.tile_rows, base, g.pieces, rowcnt);
+void launch_esc_rowcount(const EscArgs& g, const uint32_t* base, int64_t* rowcnt, cudaStream_t st, uint32_t I0,
+                         uint32_t I1) {
+  if (I1 == 0) I1 = g.tile_rows;
+  if (I1 <= I0) return;
+  esc_rowcount_kernel<<<(I1 - I0 + 7) / 8, 256, 0, st>>>(g.rowsA, I1, base, g.pieces, rowcnt, I0);
+}
+
+void launch_esc_copy_records(const EscArgs& g, uint32_t rec0, uint32_t rec1, const int64_t* row_ptr, int32_t* col,
+                             float* val, cudaStream_t st) {
+  if (rec1 <= rec0) return;
+  const unsigned blocks = std::min<unsigned>((rec1 - rec0 + 7) / 8, 148u * 16u);
+  esc_copy_records_kernel<<<blocks, 256, 0, st>>>(rec0, rec1, g.pieces, g.stage, row_ptr, col, val);
 }
 
 void launch_esc_copy(const EscArgs& g, const int64_t* row_ptr, int32_t* col, float* val, cudaStream_t st) {

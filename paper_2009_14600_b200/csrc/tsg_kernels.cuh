@@ -126,6 +126,7 @@ struct EscArgs {
   uint2* stage = nullptr;             // {col, value bits}
   unsigned long long* stage_top = nullptr;
   unsigned* work = nullptr;
+  uint32_t unit0 = 0, unit_end = 0xffffffffu;  // the launch's unit range (pipelined host output: a chunk)
   unsigned* err_flag = nullptr;
   unsigned long long* counted = nullptr;
   unsigned long long* segs = nullptr;
@@ -140,8 +141,13 @@ void launch_esc_plan_group(const EscArgs& g, const unsigned long long* pre, uint
 void launch_esc_plan_fill(const EscArgs& g, const unsigned long long* pre, const uint32_t* nwk, const uint32_t* wbase,
                           const unsigned long long* G, uint4* units, cudaStream_t st);
 void launch_esc(const EscArgs& g, int device, cudaStream_t st);
-void launch_esc_rowcount(const EscArgs& g, const uint32_t* base, int64_t* rowcnt, cudaStream_t st);
+// tile rows [I0, I1) (I1 = 0: all)
+void launch_esc_rowcount(const EscArgs& g, const uint32_t* base, int64_t* rowcnt, cudaStream_t st, uint32_t I0 = 0,
+                         uint32_t I1 = 0);
 void launch_esc_copy(const EscArgs& g, const int64_t* row_ptr, int32_t* col, float* val, cudaStream_t st);
+// the pieces of output records [rec0, rec1) and their chains (a chunk of tile rows)
+void launch_esc_copy_records(const EscArgs& g, uint32_t rec0, uint32_t rec1, const int64_t* row_ptr, int32_t* col,
+                             float* val, cudaStream_t st);
 void launch_esc_pairstats(const TileMat& A, const TileMat& B, uint64_t tA, uint32_t* njt, unsigned long long* out,
                           cudaStream_t st);
 // A given as A-role tiles (a chained stage) -> CSR with binary16 values

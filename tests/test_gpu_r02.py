@@ -95,8 +95,10 @@ def test_chain_tensor_mode_bound(ctx, kind):
     |c - r| <= (s * 2^-10 + 2 n 2^-23) * (|X0|...|Xn-1|)_ij, s = the number
     of binary16 roundings of intermediates (a last-bit MMA difference can
     move an intermediate across a binary16 rounding boundary: one binary16
-    ulp, 2^-10 relative, per rounding).  Dyadic 'tiny' values keep every
-    partial sum exact, so there TENSOR must be bit-exact."""
+    ulp, 2^-10 relative, per rounding).  Dyadic 'tiny' inputs: the
+    binary16 roundings of intermediates make later partial sums inexact, so
+    both kinds get the bound (+-1 chains are bit-exact:
+    test_gpu_parity.py::test_chain_fused_stages)."""
     n = 300
     mats = [W.random_uniform(n, n, 6 * n, 51), W.random_uniform(n, n, 6 * n, 52),
             W.random_uniform(n, n, 8 * n, 53), W.random_uniform(n, 200, 4 * n, 54)]
@@ -110,9 +112,6 @@ def test_chain_tensor_mode_bound(ctx, kind):
     want = ref.chain(mats)
     got = ctx.spgemm_chain(mats, mode="tensor").C
     assert csr_pattern_equal(got, want), first_diff(got, want)
-    if kind == "tiny":
-        assert csr_bits_equal(got, want), first_diff(got, want)
-        return
     scale = _abs_chain(mats)
     rows = np.repeat(np.arange(want.rows), np.diff(want.row_ptr))
     s = len(mats) - 2
