@@ -3,18 +3,21 @@
 // Sequences the four subsystems for C = A.B, like spgemm_square
 // (proj/src/kernels.cpp:222-302) sequences the reference passes:
 //
-//   convert A, B (CSR -> 16x16 tiles)         tsg_convert.cu
-//   enumerate + filter (count, scan, fill)    tsg_symbolic.cu      "taskList"
-//   stable per-tile-row sort by output tile   CUB segmented sort   "sort"
-//   segment heads                             tsg_symbolic.cu      "sort"
-//   counting pass fused into the numeric      tsg_numeric.cu       "counting" (empty)
-//   SEaC numeric -> staged compressed tiles   tsg_numeric.cu       "multiply"
-//   tiled -> CSR (compaction already done)    tsg_output.cu        "compaction"
+//   validate row pointers, convert A, B (CSR -> 16x16 tiles)    tsg_convert.cu   "convert"
+//   light tile rows (<= 32 tiles, or <= 128 dense tiles): one fused panel
+//     pass per tile row -- enumerate, filter, merge-order sort, counting
+//     and SEaC multiply on the tensor cores, staged rows -> CSR  tsg_panel.cu     "multiply", "compaction"
+//   general tile rows: planning (product histogram, work units), then per
+//     unit the element SEaC in shared memory -- enumerate, radix sort by
+//     output tile, counting, ordered sums -- pieces -> CSR      tsg_esc.cu       "task_list", "multiply", "compaction"
 //
 // Everything runs stream-ordered on the context's stream with scratch from
 // a stream-ordered memory pool (cudaMallocFromPoolAsync), so steady-state
 // calls do not touch the driver allocator.  The host synchronises only to
-// read data-dependent sizes (tile, pair, segment, element counts).
+// read data-dependent sizes; a device-output light call needs one readback.
+// Host output overlaps the device->host copy of finished tile-row chunks
+// with the computation of later ones (both paths).  A multi-device context
+// (tsg_create_multi) runs one panel of A's tile rows per GPU.
 #include <cub/device/device_scan.cuh>
 
 #include <cstdint>
@@ -22,9 +25,6 @@
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
-#include <chrono>
-#include <condition_variable>
-#include <functional>
 #include <mutex>
 #include <string>
 #include <thread>
@@ -36,71 +36,23 @@
 namespace tsg {
 constexpr int kGatherMax = 32;  // scalars per gathered readback
 constexpr int kPipeChunks = 16;  // max tile-row chunks of the pipelined host-output path (TSG_PIPE, default 8)
+// Tuning switches for A/B runs: read from the environment once
+// per name and process; the defaults are the measured best.
 int tuning_variant(const char* name, int dflt) {
-  const char* v = std::getenv(name);
-  return v ? std::atoi(v) : dflt;
+  static std::mutex mu;
+  static std::vector<std::pair<std::string, int>> seen;
+  std::lock_guard<std::mutex> g(mu);
+  for (const auto& [n, v] : seen)
+    if (n == name) return v;
+  const char* e = std::getenv(name);
+  const int v = e ? std::atoi(e) : dflt;
+  seen.emplace_back(name, v);
+  return v;
 }
 int pipe_chunks() {
   static const int n = std::max(1, std::min(kPipeChunks, tuning_variant("TSG_PIPE", 8)));
   return n;
 }
-}  // namespace tsg
-
-namespace tsg {
-// Small persistent host thread pool (the host side of the pipelined output:
-// decoding the delta-coded column slices while later slices are in flight).
-class HostPool {
- public:
-  explicit HostPool(unsigned n) {
-    for (unsigned i = 0; i < n; ++i) threads_.emplace_back([this] { loop(); });
-  }
-  ~HostPool() {
-    {
-      std::lock_guard<std::mutex> g(m_);
-      stop_ = true;
-    }
-    cv_.notify_all();
-    for (auto& t : threads_) t.join();
-  }
-  unsigned size() const { return unsigned(threads_.size()); }
-  void submit(std::function<void()> f) {
-    {
-      std::lock_guard<std::mutex> g(m_);
-      q_.push_back(std::move(f));
-      ++pending_;
-    }
-    cv_.notify_one();
-  }
-  void wait() {
-    std::unique_lock<std::mutex> g(m_);
-    done_.wait(g, [this] { return pending_ == 0; });
-  }
-
- private:
-  void loop() {
-    while (true) {
-      std::function<void()> f;
-      {
-        std::unique_lock<std::mutex> g(m_);
-        cv_.wait(g, [this] { return stop_ || !q_.empty(); });
-        if (stop_ && q_.empty()) return;
-        f = std::move(q_.front());
-        q_.erase(q_.begin());
-      }
-      f();
-      {
-        std::lock_guard<std::mutex> g(m_);
-        if (--pending_ == 0) done_.notify_all();
-      }
-    }
-  }
-  std::vector<std::thread> threads_;
-  std::vector<std::function<void()>> q_;
-  std::mutex m_;
-  std::condition_variable cv_, done_;
-  size_t pending_ = 0;
-  bool stop_ = false;
-};
 }  // namespace tsg
 
 struct tsg_ctx {
@@ -119,7 +71,6 @@ struct tsg_ctx {
   cudaEvent_t pipe_ev[tsg::kPipeChunks + 1] = {};
   void* pinned_pipe = nullptr;
   cudaEvent_t d2h_ev[tsg::kPipeChunks] = {};  // chunk c's slices landed on the host
-  tsg::HostPool* workers = nullptr;            // created on first pipelined host output
   cudaEvent_t ev[8] = {};
   cudaEvent_t kev[4] = {};  // bracket the numeric and assembly kernels alone
   // pinned host blocks released by tsg_free_csr, reused by later host outputs
@@ -291,7 +242,7 @@ void readback_many(tsg_ctx* ctx, const T* const (&src)[N], T (&dst)[N]) {
   std::memcpy(dst, ctx->pinned, N * sizeof(T));
 }
 
-// Chunk c's end offset and overflow flag written straight into pinned host
+// Chunk c's end offset and the error flags written straight into pinned host
 // memory (mapped under UVA) by the device: a small cudaMemcpy here would
 // queue on the copy engine behind the large D2H slices of earlier chunks and
 // stall the compute stream.
@@ -958,34 +909,15 @@ struct Call {
     owner->p[2] = pinned_alloc(ctx, std::max<uint64_t>(stage_total, 1) * sizeof(float), &owner->sz[2]);
     d_col = sc.alloc<int32_t>(stage_total);
     d_val = sc.alloc<float>(stage_total);
-    // Optional host transport of the columns (TSG_DELTA_COLS=1): the row's
-    // first column plus 16-bit deltas (24% fewer bytes over PCIe on FEM27),
-    // decoded on the host by a thread pool while later slices are in flight;
-    // a slice with a delta beyond 16 bits ships its int32 columns.  Off by
-    // default: on the measured box (16 host threads) the host decode costs
-    // more than the saved PCIe time (e2e 6.4 vs 5.9 ms on FEM27).
-    const bool delta = tuning_variant("TSG_DELTA_COLS", 0) == 1;
-    uint16_t* d_dcol = delta ? sc.alloc<uint16_t>(stage_total) : nullptr;
-    int32_t* d_first = delta ? sc.alloc<int32_t>(rows + 1) : nullptr;
-    unsigned* d_ovf = sc.alloc<unsigned>(kPipeChunks);
-    TSG_CUDA(cudaMemsetAsync(d_ovf, 0, kPipeChunks * sizeof(unsigned), s));
-    size_t hb_dcol = 0, hb_first = 0;
-    uint16_t* h_dcol = delta ? static_cast<uint16_t*>(pinned_alloc(ctx, std::max<uint64_t>(stage_total, 1) * 2, &hb_dcol))
-                             : nullptr;
-    int32_t* h_first = delta ? static_cast<int32_t*>(pinned_alloc(ctx, (rows + 1) * sizeof(int32_t), &hb_first))
-                             : nullptr;
     auto* ends = reinterpret_cast<int64_t*>(ctx->pinned_pipe);  // row_ptr at each chunk end
-    auto* ovf_h = reinterpret_cast<unsigned*>(reinterpret_cast<char*>(ctx->pinned_pipe) + 8 * (kPipeChunks + 1));
+    auto* flag_h = reinterpret_cast<unsigned*>(reinterpret_cast<char*>(ctx->pinned_pipe) + 8 * (kPipeChunks + 1));
     size_t tmp_bytes = 0;
     TSG_CUDA(cub::DeviceScan::ExclusiveScan(nullptr, tmp_bytes, rowcnt, d_rp, cuda::std::plus<int64_t>(),
                                             cub::FutureValue<int64_t>(d_rp), rows + 1, s));
     void* tmp = sc.alloc<char>(tmp_bytes);
     const int nch = pipe_chunks();
     int64_t cr0[kPipeChunks], cr1[kPipeChunks];
-    const bool trace = tuning_variant("TSG_PIPE_TRACE", 0) == 1;
-    const auto t0 = std::chrono::steady_clock::now();
-    auto ms = [&] { return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count(); };
-    // (1) every chunk's compute, with its end offset and overflow flag to the host
+    // (1) every chunk's compute, with its end offset to the host
     for (int c = 0; c < nch; ++c) {
       const uint32_t I0 = uint32_t(uint64_t(TA.tile_rows) * c / nch);
       const uint32_t I1 = uint32_t(uint64_t(TA.tile_rows) * (c + 1) / nch);
@@ -998,42 +930,29 @@ struct Call {
       // row_ptr[r0 .. r1] = row_ptr[r0] + exclusive prefix (row_ptr[r0] from the previous chunk)
       TSG_CUDA(cub::DeviceScan::ExclusiveScan(tmp, tmp_bytes, rowcnt + r0, d_rp + r0, cuda::std::plus<int64_t>(),
                                               cub::FutureValue<int64_t>(d_rp + r0), r1 - r0 + 1, s));
-      launch_panel_copy(rows, row_stage, d_rp, stage, d_col, d_val, err_flag, I0, I1, s, d_dcol, d_first,
-                        d_ovf + c);
+      launch_panel_copy(rows, row_stage, d_rp, stage, d_col, d_val, err_flag, I0, I1, s);
       check_launch(ctx);
-      publish_chunk_kernel<<<1, 1, 0, s>>>(d_rp + r1, d_ovf + c, ends + c, ovf_h + c);
+      publish_chunk_kernel<<<1, 1, 0, s>>>(d_rp + r1, err_flag, ends + c, flag_h + c);
       check_launch(ctx);
       TSG_CUDA(cudaEventRecord(ctx->pipe_ev[c], s));
     }
-    if (trace) std::fprintf(stderr, "[pipe] enqueued compute %.3f\n", ms());
     // (2) each chunk's slices to the host on stream 2 as soon as it is computed
     int32_t* h_col = static_cast<int32_t*>(owner->p[1]);
     int64_t* h_rp = static_cast<int64_t*>(owner->p[0]);
-    bool raw_cols[kPipeChunks];
     uint64_t sent = 0, d2h_bytes = 0;
     for (int c = 0; c < nch; ++c) {
-      TSG_CUDA(cudaEventSynchronize(ctx->pipe_ev[c]));  // its end and flag are readable now
+      TSG_CUDA(cudaEventSynchronize(ctx->pipe_ev[c]));  // its end is readable now
       const uint64_t lo = sent, hi = uint64_t(ends[c]);
-      raw_cols[c] = !delta || ovf_h[c] != 0;
       TSG_CUDA(cudaStreamWaitEvent(ctx->d2h, ctx->pipe_ev[c], 0));
       TSG_CUDA(cudaMemcpyAsync(h_rp + cr0[c], d_rp + cr0[c], (cr1[c] - cr0[c]) * sizeof(int64_t),
                                cudaMemcpyDeviceToHost, ctx->d2h));
       d2h_bytes += (cr1[c] - cr0[c]) * sizeof(int64_t);
       if (hi > lo) {
-        if (raw_cols[c]) {
-          TSG_CUDA(cudaMemcpyAsync(h_col + lo, d_col + lo, (hi - lo) * 4, cudaMemcpyDeviceToHost, ctx->d2h));
-          d2h_bytes += (hi - lo) * 4;
-        } else {
-          TSG_CUDA(cudaMemcpyAsync(h_dcol + lo, d_dcol + lo, (hi - lo) * 2, cudaMemcpyDeviceToHost, ctx->d2h));
-          TSG_CUDA(cudaMemcpyAsync(h_first + cr0[c], d_first + cr0[c], (cr1[c] - cr0[c]) * sizeof(int32_t),
-                                   cudaMemcpyDeviceToHost, ctx->d2h));
-          d2h_bytes += (hi - lo) * 2 + (cr1[c] - cr0[c]) * sizeof(int32_t);
-        }
+        TSG_CUDA(cudaMemcpyAsync(h_col + lo, d_col + lo, (hi - lo) * 4, cudaMemcpyDeviceToHost, ctx->d2h));
         TSG_CUDA(cudaMemcpyAsync(static_cast<float*>(owner->p[2]) + lo, d_val + lo, (hi - lo) * 4,
                                  cudaMemcpyDeviceToHost, ctx->d2h));
-        d2h_bytes += (hi - lo) * 4;
+        d2h_bytes += (hi - lo) * 8;
       }
-      TSG_CUDA(cudaEventRecord(ctx->d2h_ev[c], ctx->d2h));
       sent = hi;
     }
     nnzC = int64_t(sent);
@@ -1042,46 +961,6 @@ struct Call {
     TSG_CUDA(cudaMemcpyAsync(h_rp + rows, d_rp + rows, sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->d2h));
     TSG_CUDA(cudaEventRecord(ctx->pipe_ev[kPipeChunks], ctx->d2h));
     TSG_CUDA(cudaStreamWaitEvent(s, ctx->pipe_ev[kPipeChunks], 0));  // the final sync covers stream 2
-    if (trace) std::fprintf(stderr, "[pipe] compute done, D2H enqueued %.3f\n", ms());
-    // (3) decode each delta-coded slice as it lands (rows split over the pool)
-    if (delta) {
-      if (!ctx->workers) {
-        const unsigned hc = std::max(1u, std::min(unsigned(tuning_variant("TSG_POOL", 16)),
-                                                  std::thread::hardware_concurrency()));
-        ctx->workers = new HostPool(hc);
-      }
-      const unsigned parts = ctx->workers->size();
-      for (int c = 0; c < nch; ++c) {
-        if (raw_cols[c] || cr1[c] <= cr0[c]) continue;
-        TSG_CUDA(cudaEventSynchronize(ctx->d2h_ev[c]));
-        if (trace) std::fprintf(stderr, "[pipe] chunk %d landed %.3f\n", c, ms());
-        const int64_t r0 = cr0[c], r1 = cr1[c];
-        const int64_t rend = c + 1 < nch ? cr0[c + 1] : rows;  // row_ptr[r1] is the next chunk's first
-        (void)rend;
-        for (unsigned k = 0; k < parts; ++k) {
-          const int64_t a = r0 + (r1 - r0) * k / parts, b = r0 + (r1 - r0) * (k + 1) / parts;
-          if (a >= b) continue;
-          const int64_t p_hi_row = b;  // rows [a, b): entries [rp[a], rp[b])
-          const int64_t end_off = p_hi_row < r1 ? -1 : int64_t(ends[c]);
-          ctx->workers->submit([=] {
-            for (int64_t r = a; r < b; ++r) {
-              const int64_t p0 = h_rp[r], p1 = r + 1 < r1 || end_off < 0 ? h_rp[r + 1] : end_off;
-              if (p1 <= p0) continue;
-              int32_t v = h_first[r];
-              h_col[p0] = v;
-              for (int64_t p = p0 + 1; p < p1; ++p) {
-                v += int32_t(h_dcol[p]);
-                h_col[p] = v;
-              }
-            }
-          });
-        }
-      }
-      ctx->workers->wait();
-      if (trace) std::fprintf(stderr, "[pipe] decoded %.3f (%u threads)\n", ms(), parts);
-      ctx->pinned_free.emplace_back(h_dcol, hb_dcol);
-      ctx->pinned_free.emplace_back(h_first, hb_first);
-    }
     counted = readback(ctx, counted_d);
     if (st) st->d2h_bytes += sizeof(int64_t) + d2h_bytes;
     host_done = true;
@@ -1984,7 +1863,6 @@ int tsg_destroy(tsg_ctx* ctx) {
     if (e) cudaEventDestroy(e);
   for (auto& e : ctx->d2h_ev)
     if (e) cudaEventDestroy(e);
-  delete ctx->workers;
   if (ctx->d2h) {
     cudaStreamSynchronize(ctx->d2h);
     cudaStreamDestroy(ctx->d2h);

@@ -11,13 +11,16 @@
 //     (the std::sort at tile_format.cpp:106-110 is replaced by a 16-way
 //      merge across the rows of a tile row: CSR rows are already sorted).
 //
-// One warp per tile row (16 CSR rows), one pass: the tile row's tiles are
-// counted first (bitmap of tile columns, or the row walk for panels wider
-// than 8192 tile columns), the tile base comes from a decoupled look-back
-// over the preceding tile rows, then each tile is staged densely in shared
-// memory and cut into the lane-dense operand chunks of one or both roles
-// (A order and/or B order, see tsg_common.cuh), plus the tile's 256-bit
-// occupancy mask and row/column occupancy words.
+// One warp per tile row (16 CSR rows), one pass, no host synchronisation:
+// every array is sized by nnz (a tile row never holds more tiles or chunks
+// than entries), so tile row I writes its tiles at gapped slots starting at
+// row_ptr[16 I]; a scan of the per-tile-row counts and tiles_compact_kernel
+// give the dense CSR-of-tiles afterwards.  Per tile row: the fast path ranks
+// tile columns with a shared-memory bitmap (or bitonic-sorts the entries when
+// the panel is wide or has many tiles), builds the 256-bit masks with
+// shared-memory atomics and stores each fp16 value straight into its
+// lane-dense operand chunk (A order and/or B order, tsg_common.cuh); panels
+// of more than 512 entries take the 16-way merge walk, one tile at a time.
 #include <algorithm>
 #include <type_traits>
 

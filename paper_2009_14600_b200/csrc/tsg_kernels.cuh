@@ -85,13 +85,8 @@ void launch_elem_bound(const CsrView& A, const int64_t* rpB, int64_t bcols, uint
 void launch_emit_compact(uint32_t tile_rows, const TileEmit& em, const uint32_t* trp, TileMat& T, cudaStream_t st);
 // bound[I] = min(B.tile_cols, raw pairs of A's tile row I): output tiles of the row at most
 void launch_row_tile_bound(const TileMat& A, const TileMat& B, uint32_t* bound, cudaStream_t st);
-// dcol (nullable): also writes the host transport -- first[row] = the row's
-// first column, dcol[p] = column delta to the previous entry of the row (0 at
-// a row start); *ovf |= 1 when some delta exceeds 16 bits
 void launch_panel_copy(int64_t rows, const uint32_t* row_stage, const int64_t* row_ptr, const uint2* stage,
-                       int32_t* col, float* val, unsigned* err_flag, uint32_t I0, uint32_t I1,
-                       cudaStream_t st, uint16_t* dcol = nullptr, int32_t* first = nullptr,
-                       unsigned* ovf = nullptr);
+                       int32_t* col, float* val, unsigned* err_flag, uint32_t I0, uint32_t I1, cudaStream_t st);
 // (2)+(3) general rows: per (tile row, column range) chunk, the tile pairs
 // expanded into element products, sorted by output tile key in shared
 // memory, summed in k order, written as row-major pieces (tsg_esc.cu)

@@ -465,16 +465,13 @@ __global__ void __launch_bounds__(256, kMinBlocks) panel_numeric_kernel(TileMat 
 // positions (the 16 rows are consecutive in the CSR), each taken from its
 // row's staging region.  Non-finite values raise kErrPrecision
 // (finalize_segment, kernels.cpp:115-127).
-template <bool kDelta>
 __global__ void __launch_bounds__(256) panel_copy_kernel(int64_t rows, uint32_t tile_rows,
                                                         const uint32_t* __restrict__ row_stage,
                                                         const int64_t* __restrict__ row_ptr,
                                                         const uint2* __restrict__ stage,
                                                         int32_t* __restrict__ col,
                                                         float* __restrict__ val,
-                                                        unsigned* __restrict__ err_flag, uint32_t I0,
-                                                        uint16_t* __restrict__ dcol, int32_t* __restrict__ first,
-                                                        unsigned* __restrict__ ovf) {
+                                                        unsigned* __restrict__ err_flag, uint32_t I0) {
   const int lane = threadIdx.x & 31;
   const uint32_t I = I0 + blockIdx.x * 8 + (threadIdx.x >> 5);
   if (I >= tile_rows) return;
@@ -486,8 +483,7 @@ __global__ void __launch_bounds__(256) panel_copy_kernel(int64_t rows, uint32_t 
   // lane r: offset of row r within the panel (rows past the end: T)
   const uint32_t off = row < r1 ? uint32_t(row_ptr[row] - base) : T;
   const uint32_t src0 = row < r1 ? row_stage[row] : 0u;
-  bool bad = false, wide = false;
-  uint32_t carry = 0;  // column of the panel's previous entry (delta coding)
+  bool bad = false;
   for (uint32_t q0 = 0; q0 < T; q0 += 32) {
     const uint32_t q = q0 + lane;
     int r = 0;  // last row whose offset is <= q (empty rows resolve to the next one)
@@ -497,32 +493,15 @@ __global__ void __launch_bounds__(256) panel_copy_kernel(int64_t rows, uint32_t 
       if (v <= q) r += b;
     }
     const uint32_t o = __shfl_sync(kFull, off, r), sr = __shfl_sync(kFull, src0, r);
-    uint2 e = make_uint2(0, 0);
     if (q < T) {
-      e = __ldg(stage + sr + (q - o));
+      const uint2 e = __ldg(stage + sr + (q - o));
       const float x = __uint_as_float(e.x);
       bad |= !isfinite(x);
       col[base + q] = int32_t(e.y);
       val[base + q] = x;
     }
-    if (kDelta) {  // host transport: first column per row + 16-bit deltas
-      uint32_t prev = __shfl_up_sync(kFull, e.y, 1);
-      if (lane == 0) prev = carry;
-      carry = __shfl_sync(kFull, e.y, 31);
-      if (q < T) {
-        if (q == o) {
-          first[r0 + r] = int32_t(e.y);
-          dcol[base + q] = 0;
-        } else {
-          const uint32_t d = e.y - prev;
-          wide |= d > 0xffffu;
-          dcol[base + q] = uint16_t(d);
-        }
-      }
-    }
   }
   if (__any_sync(kFull, bad) && lane == 0) atomicOr(err_flag, unsigned(kErrPrecision));
-  if (kDelta && __any_sync(kFull, wide) && lane == 0) atomicOr(ovf, 1u);
 }
 
 }  // namespace
@@ -625,16 +604,10 @@ void launch_emit_compact(uint32_t tile_rows, const TileEmit& em, const uint32_t*
 }
 
 void launch_panel_copy(int64_t rows, const uint32_t* row_stage, const int64_t* row_ptr, const uint2* stage,
-                       int32_t* col, float* val, unsigned* err_flag, uint32_t I0, uint32_t I1,
-                       cudaStream_t st, uint16_t* dcol, int32_t* first, unsigned* ovf) {
+                       int32_t* col, float* val, unsigned* err_flag, uint32_t I0, uint32_t I1, cudaStream_t st) {
   if (I1 <= I0) return;
   const unsigned blocks = (I1 - I0 + 7) / 8;
-  if (dcol)
-    panel_copy_kernel<true><<<blocks, 256, 0, st>>>(rows, I1, row_stage, row_ptr, stage, col, val, err_flag, I0,
-                                                    dcol, first, ovf);
-  else
-    panel_copy_kernel<false><<<blocks, 256, 0, st>>>(rows, I1, row_stage, row_ptr, stage, col, val, err_flag, I0,
-                                                     nullptr, nullptr, nullptr);
+  panel_copy_kernel<<<blocks, 256, 0, st>>>(rows, I1, row_stage, row_ptr, stage, col, val, err_flag, I0);
 }
 
 }  // namespace tsg
