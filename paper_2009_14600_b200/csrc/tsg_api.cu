@@ -643,20 +643,29 @@ struct Call {
     record(ctx, timing, 4);
     uint2* stage = static_cast<uint2*>(ctx->stage_buf);
     const uint64_t cap_slots = ctx->stage_cap / sizeof(uint2);
+    // TSG_TC05=1: the tcgen05 variant of the light pass (TENSOR mode; the
+    // measured comparison of DESIGN.md §6)
+    const bool tc05 = opt.mode == TSG_MODE_TENSOR && tuning_variant("TSG_TC05", 0) == 1;
+    unsigned* fallback = sc.alloc<unsigned>(1);
+    TSG_CUDA(cudaMemsetAsync(fallback, 0, sizeof(unsigned), s));
     if (timing) TSG_CUDA(cudaEventRecord(ctx->kev[0], s));
-    TSG_CUDA(launch_panel_numeric(TA, *TB, rows, row_stage, cap_slots, stage, rowcnt, counted_d, tot_d + 3, tot_d, opt.mode,
-                         0, TA.tile_rows, s, nullptr, dscal, work, 1));
+    if (tc05)
+      TSG_CUDA(launch_tc05_panel(TA, *TB, rows, row_stage, cap_slots, stage, rowcnt, counted_d, tot_d + 3, tot_d, dscal,
+                                 work, fallback, ctx->device, s));
+    else
+      TSG_CUDA(launch_panel_numeric(TA, *TB, rows, row_stage, cap_slots, stage, rowcnt, counted_d, tot_d + 3, tot_d,
+                                    opt.mode, 0, TA.tile_rows, s, nullptr, dscal, work, 1));
     check_launch(ctx);
     if (timing) TSG_CUDA(cudaEventRecord(ctx->kev[1], s));
     record(ctx, timing, 5);
     exclusive_sum(ctx, sc, rowcnt, d_rp, uint64_t(rows) + 1);
     ScalarGather g;
-    const void* ps[10] = {dscal, dscal + 1, ntA_dev, ntB_dev, counted_d, d_rp + rows, tot_d, tot_d + 1, tot_d + 2,
-                          tot_d + 3};
-    for (int i = 0; i < 10; ++i) g.p[i] = ps[i];
+    const void* ps[11] = {dscal, dscal + 1, ntA_dev, ntB_dev, counted_d, d_rp + rows, tot_d, tot_d + 1, tot_d + 2,
+                          tot_d + 3, fallback};
+    for (int i = 0; i < 11; ++i) g.p[i] = ps[i];
     g.wide = 0x3f0u;  // counted, nnz and the four totals are u64
-    g.n = 10;
-    unsigned long long v[10];
+    g.n = 11;
+    unsigned long long v[11];
     readback_gather(ctx, sc, g, v);
     raise_flags(unsigned(v[0]));
     tA = v[2];
@@ -678,7 +687,7 @@ struct Call {
       light_path();
       return true;
     }
-    if (stage_total > cap_slots) {  // the rare arena overflow: redo the pass
+    if (stage_total > cap_slots || v[10]) {  // the rare arena overflow (or a tcgen05 panel fallback): redo the pass
       stage = static_cast<uint2*>(arena(stage_total * sizeof(uint2)));
       TSG_CUDA(cudaMemsetAsync(counted_d, 0, sizeof(unsigned long long), s));
       TSG_CUDA(cudaMemsetAsync(tot_d, 0, 3 * sizeof(unsigned long long), s));

@@ -77,6 +77,14 @@ cudaError_t launch_panel_numeric(const TileMat& A, const TileMat& B, int64_t row
                                  const unsigned long long* need, unsigned long long* stats, int mode, uint32_t I0,
                                  uint32_t I1, cudaStream_t st, const TileEmit* emit = nullptr,
                                  const unsigned* gate = nullptr, unsigned* work = nullptr, int nl = 1);
+// The same light-row pass on tcgen05 (tsg_tc05.cu; TENSOR mode, tile rows of
+// <= 32 A tiles): persistent CTAs over panels of 8 tile rows, M = 128 MMAs
+// with TMEM accumulators.  Sets *fallback when a panel gathers more B tiles
+// than its shared memory holds (the host then runs launch_panel_numeric).
+cudaError_t launch_tc05_panel(const TileMat& A, const TileMat& B, int64_t rows, const uint32_t* row_stage,
+                              uint64_t stage_cap, uint2* stage, int64_t* rowcnt, unsigned long long* counted,
+                              const unsigned long long* need, unsigned long long* stats, const unsigned* gate,
+                              unsigned* work, unsigned* fallback, int device, cudaStream_t st);
 // row_bound[r] = min(B.cols, sum over A's entries (r, k) of nnz(B row k));
 // *total += sum of row_bound
 // (gate: the call's error flags; malformed row pointers -> all bounds 0)
