@@ -70,6 +70,8 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-sample-runs", type=int, default=3)
     p.add_argument("--no-e2e", action="store_true", help="skip the host-to-host e2e measurement")
+    p.add_argument("--no-cpu-extra", action="store_true",
+                   help="skip the threads=1 / pairing-off / Gustavson CPU points")
     return p.parse_args()
 
 
@@ -489,10 +491,34 @@ def cpu_baseline(args, mats, flops):
     runs = 1 if smats is not mats else max(1, args.cpu_sample_runs)
     secs = [cpu_run(smats, threads=cores).times["total"] for _ in range(runs)]
     s = statistics.median(secs)
-    return {"value": round(sflops / s / 1e9, 4), "unit": "GFLOPS", "cores": cores, "kind": "reference",
-            "sample": f"{what}: {sflops} flops; {len(secs)} run(s) of the reference "
-                      f"(spgemm_square / pass composition, pairing on, threads={cores}), median {s:.3f} s; "
-                      f"input tiling untimed (SPEC.md:522)"}
+    out = {"value": round(sflops / s / 1e9, 4), "unit": "GFLOPS", "cores": cores, "kind": "reference",
+           "cpu_model": cpu_model(),
+           "sample": f"{what}: {sflops} flops; {len(secs)} run(s) of the reference "
+                     f"(spgemm_square / pass composition, pairing on, threads={cores}), median {s:.3f} s; "
+                     f"input tiling untimed (SPEC.md:522)"}
+    # one thread, pairing off, and the single-threaded
+    # Gustavson mixed oracle (dense_spgemm_mixed_ordered), one run each on the
+    # same sample
+    if not args.no_cpu_extra and len(smats) <= 2:
+        def gf(t):
+            return round(sflops / t / 1e9, 4)
+        t1 = cpu_run(smats, threads=1).times["total"]
+        tp = (ref.spgemm(smats[0], threads=cores, pairing=False) if len(smats) == 1 else
+              ref.spgemm(smats[0], smats[1], threads=cores, pairing=False)).times["total"]
+        to = ref.oracle(smats[0], smats[1] if len(smats) > 1 else None).times["total"]
+        out["extra_points"] = {"threads_1": gf(t1), f"pairing_off_threads_{cores}": gf(tp),
+                               "gustavson_mixed_oracle_threads_1": gf(to), "unit": "GFLOPS"}
+    return out
+
+
+def cpu_model() -> str:
+    try:
+        for line in subprocess.run(["lscpu"], capture_output=True, text=True).stdout.splitlines():
+            if line.startswith("Model name:"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
 
 
 def config_key(config, cb_total, nnz_a):

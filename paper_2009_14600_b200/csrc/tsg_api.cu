@@ -283,7 +283,7 @@ void readback_gather(tsg_ctx* ctx, Scratch& sc, const ScalarGather& g, unsigned 
 const uint32_t* convert(tsg_ctx* ctx, Scratch& sc, const CsrView& in, TileMat& T, int roles,
                         unsigned* err_flag, int drop_nonfinite, const uint8_t* needed = nullptr,
                         uint8_t* mark = nullptr, uint32_t* walk_count_zeroed = nullptr,
-                        unsigned* max_row_tiles = nullptr) {
+                        unsigned* max_row_tiles = nullptr, unsigned* general = nullptr) {
   T.rows = in.rows;
   T.cols = in.cols;
   T.tile_rows = uint32_t((in.rows + 15) / 16);
@@ -297,6 +297,7 @@ const uint32_t* convert(tsg_ctx* ctx, Scratch& sc, const CsrView& in, TileMat& T
   cs.ntiles = sc.alloc<uint32_t>(nr);
   cs.walk_list = sc.alloc<uint32_t>(nr);
   cs.mark = mark;
+  cs.general = general;
   if (walk_count_zeroed) {
     cs.walk_count = walk_count_zeroed;
   } else {
@@ -495,6 +496,10 @@ struct Call {
   const unsigned* ntA_dev = nullptr;
   const unsigned* ntB_dev = nullptr;
 
+  // zeroed with the call's scalars (the high half of zblk[6]): set by A's
+  // conversion when a tile row has more than 128 tiles (the call is general)
+  unsigned* general_flag() { return reinterpret_cast<unsigned*>(zblk + 6) + 1; }
+
   void convert_operands(bool defer = false) {
     if (!pre_a) check_csr(Ain, "A");
     check_csr(Bin, "B");
@@ -535,13 +540,13 @@ struct Call {
     } else {
       dA = stage(ctx, sc, Ain, st);
       ntA_d = convert(ctx, sc, dA, TA, same ? 3 : 1, err_flag, opt.drop_nonfinite, nullptr, needed,
-                      reinterpret_cast<uint32_t*>(zblk + 6), dscal + 1);
+                      reinterpret_cast<uint32_t*>(zblk + 6), dscal + 1, general_flag());
     }
     dB = same ? dA : stage(ctx, sc, Bin, st);
     const uint32_t* ntB_d = ntA_d;
     if (!same)
       ntB_d = convert(ctx, sc, dB, TB_own, 2, err_flag, opt.drop_nonfinite, needed, nullptr,
-                      reinterpret_cast<uint32_t*>(zblk + 7));
+                      reinterpret_cast<uint32_t*>(zblk + 7), nullptr, general_flag());
     TB = same ? &TA : &TB_own;
     if (pre_a) {  // converted A tiles report their largest tile row in the compaction
       launch_row_stats(TA, dscal + 1, s);

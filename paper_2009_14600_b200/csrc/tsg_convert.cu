@@ -124,10 +124,26 @@ struct Gapped {
   uint16_t* h16 = nullptr;    // per entry: rounded binary16 value, 0 when dropped
   uint32_t* ntiles = nullptr;  // per tile row
   uint8_t* mark = nullptr;     // optional: mark[J] = 1 for every tile column J (the B tile rows A needs)
+  // "general" flag: set by the A-role conversion when a tile row has more than
+  // kLightMax tiles -- the call then takes the general path, which reads no
+  // operand chunks, 256-bit masks or lane metadata, so every tile row that sees
+  // it writes only what the general path reads (tile columns, occupancy,
+  // etile, h16)
+  unsigned* general = nullptr;
+  bool may_set = false;        // this conversion is A's (its tile rows decide the path)
 };
+
+constexpr uint32_t kLightMax = 128;  // the light path's largest tile row (tsg_api.cu decide())
 
 __device__ __forceinline__ void mark_column(const Gapped& out, uint32_t J) {
   if (out.mark && !out.mark[J]) out.mark[J] = 1;  // most tiles share their column's flag: skip the store
+}
+
+// records this tile row's tile count; true when the call is known to be general
+__device__ __forceinline__ bool general_call(const Gapped& out, uint32_t ntiles) {
+  if (!out.general) return false;
+  if (out.may_set && ntiles > kLightMax) atomicOr(out.general, 1u);
+  return *reinterpret_cast<volatile unsigned*>(out.general) != 0u;
 }
 
 // Tile-slot (r, c) of a 16x16 tile -> its lane and fp16 position in the
@@ -205,6 +221,7 @@ __device__ __forceinline__ uint32_t sparse_panel(FastSmem& sm, const Gapped& out
     ntiles += __popc(sb);
   }
   if (lane == 0) sm.ts[ntiles] = uint16_t(nk);
+  const bool lite = __shfl_sync(kFull, lane == 0 ? general_call(out, ntiles) : false, 0);
   __syncwarp();
   // lanes emit tiles t = lane, lane + 32, ...; chunk bases by a warp scan
   uint32_t runA = 1u + uint32_t(E0), runB = 1u + uint32_t(E0);
@@ -229,7 +246,7 @@ __device__ __forceinline__ uint32_t sparse_panel(FastSmem& sm, const Gapped& out
         lmB |= 1u << L;
       }
     }
-    const uint32_t nA = (roles & 1) ? __popc(lmA) : 0u, nB = (roles & 2) ? __popc(lmB) : 0u;
+    const uint32_t nA = (roles & 1) && !lite ? __popc(lmA) : 0u, nB = (roles & 2) && !lite ? __popc(lmB) : 0u;
     uint32_t iA = nA, iB = nB;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -250,10 +267,16 @@ __device__ __forceinline__ uint32_t sparse_panel(FastSmem& sm, const Gapped& out
         rowocc |= ((rm[g] & 0xffffu) != 0u ? 1u << g : 0u) | ((rm[g] >> 16) != 0u ? 1u << (g + 8) : 0u);
       }
       const uint32_t occ = (colocc & 0xffffu) | (rowocc << 16);
+      mark_column(out, J);
+      if (lite) {  // the general path reads only the tile column and occupancy
+#pragma unroll
+        for (int role = 0; role < 2; ++role)
+          if (roles & (1 << role)) out.rec[role][E0 + t] = make_uint4(0u, 0u, occ, J);
+        continue;
+      }
       uint4* dst = reinterpret_cast<uint4*>(out.rm2 + size_t(E0 + t) * 8);
       dst[0] = make_uint4(rm[0], rm[1], rm[2], rm[3]);
       dst[1] = make_uint4(rm[4], rm[5], rm[6], rm[7]);
-      mark_column(out, J);
 #pragma unroll
       for (int role = 0; role < 2; ++role) {
         if (!(roles & (1 << role))) continue;
@@ -473,6 +496,8 @@ __global__ void __launch_bounds__(256, 4) convert_fast_kernel(CsrView in, uint32
     sort_path();
     return;
   }
+  // a general call reads no chunks / masks / lane metadata of this tile row
+  const bool lite = __shfl_sync(kFull, lane == 0 ? general_call(out, ntiles) : false, 0);
   for (uint32_t i = lane; i < ntiles * 8u; i += 32) sm.rm[i >> 3][i & 7] = 0;
   for (uint32_t i = lane; i < ntiles * 2u; i += 32) sm.lm[i >> 1][i & 1] = 0;
   __syncwarp();
@@ -489,11 +514,13 @@ __global__ void __launch_bounds__(256, 4) convert_fast_kernel(CsrView in, uint32
       k = sm.pre[j >> 5] + __popc(sm.bits[j >> 5] & ((1u << (j & 31)) - 1u));
       const int cc = c[u] & 15;
       atomicOr(&sm.rm[k][r & 7], 1u << (cc + 16 * (r >> 3)));
-      int L, h16;
-      slot_lane(kRoleA, r, cc, L, h16);
-      atomicOr(&sm.lm[k][0], 1u << L);
-      slot_lane(kRoleB, r, cc, L, h16);
-      atomicOr(&sm.lm[k][1], 1u << L);
+      if (!lite) {
+        int L, h16;
+        slot_lane(kRoleA, r, cc, L, h16);
+        atomicOr(&sm.lm[k][0], 1u << L);
+        slot_lane(kRoleB, r, cc, L, h16);
+        atomicOr(&sm.lm[k][1], 1u << L);
+      }
       pk[u] |= k << 21;  // k < 64: bits 21..26
     }
     if (out.etile) {  // the first kept entry of each (row, tile) names the tile; later ones are duplicates
@@ -568,9 +595,11 @@ __global__ void __launch_bounds__(256, 4) convert_fast_kernel(CsrView in, uint32
       rowocc |= ((mw[gg] & 0xffffu) != 0u ? 1u << gg : 0u) | ((mw[gg] >> 16) != 0u ? 1u << (gg + 8) : 0u);
     }
     const uint32_t occ = (colocc & 0xffffu) | (rowocc << 16);
-    uint4* dst = reinterpret_cast<uint4*>(out.rm2 + size_t(E0 + k) * 8);
-    dst[0] = m0;
-    dst[1] = m1;
+    if (!lite) {
+      uint4* dst = reinterpret_cast<uint4*>(out.rm2 + size_t(E0 + k) * 8);
+      dst[0] = m0;
+      dst[1] = m1;
+    }
     mark_column(out, J);
     if (roles & 1) out.rec[kRoleA][E0 + k] = make_uint4(sm.lm[k][0], cbA[h], occ, J);
     if (roles & 2) out.rec[kRoleB][E0 + k] = make_uint4(sm.lm[k][1], cbB[h], occ, J);
@@ -581,7 +610,7 @@ __global__ void __launch_bounds__(256, 4) convert_fast_kernel(CsrView in, uint32
   // every kept entry stores its fp16 value into its chunk slots
 #pragma unroll
   for (int u = 0; u < kFastU; ++u) {
-    if (32u * u >= E) break;
+    if (32u * u >= E || lite) break;
     if (!((pk[u] >> 20) & 1u)) continue;
     const uint32_t k = (pk[u] >> 21) & 63u;
     const int r = (pk[u] >> 16) & 15, cc = c[u] & 15;
@@ -656,6 +685,9 @@ __global__ void __launch_bounds__(256) convert_walk_kernel(CsrView in, Gapped ou
     uint32_t ntiles = 0;
     uint32_t cbase[2] = {1u + uint32_t(E0), 1u + uint32_t(E0)};
     int32_t prev_col = -1;
+    // a general call (flagged by some tile row of A with > kLightMax tiles) reads
+    // no chunks, masks or lane metadata: only tile columns, occupancy, etile, h16
+    const bool lite = __shfl_sync(kFull, lane == 0 ? general_call(out, 0) : false, 0);
     int32_t c_cur = p < end ? __ldg(in.col + p) : 0;  // one entry ahead: the walk is not a chain of loads
     while (true) {
       const uint32_t my_tc = (p < end) ? uint32_t(c_cur) >> 4 : 0xffffffffu;
@@ -698,11 +730,15 @@ __global__ void __launch_bounds__(256) convert_walk_kernel(CsrView in, Gapped ou
       const uint32_t occ = (__reduce_or_sync(kFull, rm) & 0xffffu) | ((any & 0xffffu) << 16);
       // the 256-bit mask as interleaved row masks: word g = row g | row g+8 << 16
       const uint32_t rm_hi = __shfl_sync(kFull, rm, (lane & 7) + 8);
-      if (lane < 8) out.rm2[size_t(t) * 8 + lane] = rm | (rm_hi << 16);
+      if (lane < 8 && !lite) out.rm2[size_t(t) * 8 + lane] = rm | (rm_hi << 16);
       if (lane == 0) mark_column(out, J);
 #pragma unroll
       for (int role = 0; role < 2; ++role) {
         if (!(roles & (1 << role))) continue;
+        if (lite) {
+          if (lane == 0) out.rec[role][t] = make_uint4(0u, 0u, occ, J);
+          continue;
+        }
         uint32_t rg[4];
         staged_regs(role == kRoleA ? st : stT, lane, rg);
         if (role == kRoleB) {  // the transposed tile in A order, stored {reg0, reg2, reg1, reg3}
@@ -743,10 +779,12 @@ __global__ void __launch_bounds__(256) tiles_compact_kernel(CsrView in, uint32_t
   if (I >= tile_rows) return;
   const uint32_t src = uint32_t(in.row_ptr[int64_t(I) * kTile]), dst = T.trp[I], n = g.ntiles[I];
   const int r0 = (roles & 1) ? 0 : 1;
+  const bool lite = g.general && *g.general;  // final here: the conversion kernels are done
   for (uint32_t i = lane; i < n; i += 32) {
     const uint4 rec0 = g.rec[r0][src + i];
     T.tco[dst + i] = make_uint2(rec0.w, rec0.z);
     T.trow[dst + i] = I;
+    if (lite) continue;
 #pragma unroll
     for (int role = 0; role < 2; ++role) {
       if (!(roles & (1 << role))) continue;
@@ -755,6 +793,7 @@ __global__ void __launch_bounds__(256) tiles_compact_kernel(CsrView in, uint32_t
       T.rec[role][dst + i] = rc;
     }
   }
+  if (lite) return;
   const uint4* s4 = reinterpret_cast<const uint4*>(g.rm2 + size_t(src) * 8);
   uint4* d4 = reinterpret_cast<uint4*>(T.rm2 + size_t(dst) * 8);
   for (uint32_t i = lane; i < 2 * n; i += 32) d4[i] = s4[i];
@@ -835,6 +874,8 @@ void launch_convert(const CsrView& in, TileMat& out, int roles, const ConvertScr
   g.h16 = out.h16;
   g.ntiles = cs.ntiles;
   g.mark = cs.mark;
+  g.general = cs.general;
+  g.may_set = (roles & 1) != 0;
   auto kf = in.dtype == 0 ? convert_fast_kernel<0> : in.dtype == 2 ? convert_fast_kernel<2> : convert_fast_kernel<1>;
   kf<<<(out.tile_rows + 7) / 8, 256, 0, st>>>(in, out.tile_rows, g, roles, cs.walk_list, cs.walk_count, err_flag,
                                     drop_nonfinite, needed);
@@ -851,6 +892,7 @@ void launch_tiles_compact(const CsrView& in, const ConvertScratch& cs, TileMat& 
   g.rec[0] = cs.rec[0];
   g.rec[1] = cs.rec[1];
   g.ntiles = cs.ntiles;
+  g.general = cs.general;
   tiles_compact_kernel<<<(out.tile_rows + 7) / 8, 256, 0, st>>>(in, out.tile_rows, g, out, roles, max_row_tiles);
 }
 

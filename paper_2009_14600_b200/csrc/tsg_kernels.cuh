@@ -34,6 +34,8 @@ struct ConvertScratch {
   uint32_t* walk_list = nullptr;       // tile_rows
   uint32_t* walk_count = nullptr;      // 1, zeroed
   uint8_t* mark = nullptr;             // optional, zeroed: set for every tile column
+  unsigned* general = nullptr;         // optional, zeroed: set when a tile row of A has > 128 tiles
+                                       // (general path); later tile rows then skip chunks / masks
 };
 // sets kErrRowPtr in err_flag unless row_ptr[0] == 0, row_ptr[rows] == nnz and non-decreasing
 void launch_validate_rowptr(const CsrView& in, unsigned* err_flag, cudaStream_t st);

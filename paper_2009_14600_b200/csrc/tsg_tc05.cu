@@ -39,7 +39,7 @@ namespace tsg {
 namespace {
 
 constexpr int kTcThreads = 288;     // 4 producer warps, 1 MMA warp, 4 epilogue warps
-constexpr int kTcStages = 4;        // ring stages (one work item each)
+constexpr int kTcStages = 4;        // ring stages (one work item each; stage = producer warp)
 constexpr int kTcMaxK = 256;        // 8 tile rows x <= 32 A tiles
 constexpr int kTcMaxJ = 2048;       // gathered B tiles of the panel (else: fall back)
 constexpr int kTcMaxItems = 256;
@@ -51,9 +51,13 @@ struct TcSmem {
   alignas(1024) uint8_t ring[kTcStages][kStageBytes];
   uint32_t kcol[kTcMaxK];          // the panel's inner tile columns (sorted)
   uint32_t ktile[kTcMaxK][8];      // A tile index of (tile row r, k), or kNoTile
+  uint16_t kocc[kTcMaxK][8];       // its column occupancy (0 when absent)
   uint32_t gather[kTcMaxJ];        // sort buffer (k or J keys)
   uint32_t jcol[kTcMaxJ];          // the panel's output tile columns (sorted, unique)
   uint32_t bstart[kTcMaxK];        // per k: first B tile of the current window
+  uint32_t bfirst[kTcMaxK];        // per k: its first B tile and its offset in bcolk
+  uint32_t koff[kTcMaxK + 1];
+  uint32_t bcolk[kTcMaxJ];         // per k (at koff), the tile columns of B row k
   uint32_t item_k[kTcMaxItems];    // window work items: index into kcol
   uint32_t item_b0[kTcMaxItems + 1];
   uint32_t bt_idx[kTcMaxItems * 16];
@@ -184,7 +188,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc05_panel_kernel(
   const uint32_t npanels = (A.tile_rows + 7) / 8;
   if (tid == 0) {
     for (int s = 0; s < kTcStages; ++s) {
-      mbar_init(&sm.full[s], 128);
+      mbar_init(&sm.full[s], 32);
       mbar_init(&sm.empty[s], 1);
     }
     mbar_init(&sm.tfull, 1);
@@ -200,7 +204,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc05_panel_kernel(
   tc_fence_after();
   const uint32_t tmem = sm.tmem_base;
   // pipeline phases (per role, carried across windows and panels)
-  uint32_t prod_it = 0, mma_it = 0, win_it = 0;
+  uint32_t item_base = 0, win_it = 0;  // running item count (ring stage = count % 4), windows
   // epilogue state: this thread's panel row
   unsigned long long n_struct = 0, n_filt = 0, n_seg = 0, n_raw = 0;
   for (;;) {
@@ -238,7 +242,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc05_panel_kernel(
       if (head) {
         sm.kcol[pos] = k;
 #pragma unroll
-        for (int q = 0; q < 8; ++q) sm.ktile[pos][q] = kNoTile;
+        for (int q = 0; q < 8; ++q) {
+          sm.ktile[pos][q] = kNoTile;
+          sm.kocc[pos][q] = 0;
+        }
       }
       asm volatile("bar.sync 1, 256;" ::: "memory");
       if (tid == 0) sm.nk = nk;
@@ -247,7 +254,11 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc05_panel_kernel(
       {
         uint32_t dummy;
         const uint32_t incl = scan256(head ? 1u : 0u, sm.wsum, tid, dummy) + (head ? 1u : 0u);
-        if (valid) sm.ktile[incl - 1][(key2 >> 5) & 7u] = A.trp[I0 + ((key2 >> 5) & 7u)] + (key2 & 31u);
+        if (valid) {
+          const uint32_t at = A.trp[I0 + ((key2 >> 5) & 7u)] + (key2 & 31u);
+          sm.ktile[incl - 1][(key2 >> 5) & 7u] = at;
+          sm.kocc[incl - 1][(key2 >> 5) & 7u] = uint16_t(__ldg(&A.tco[at].y) & 0xffffu);
+        }
       }
       // J gather: thread i < nk writes B row kcol[i]'s tile columns
       asm volatile("bar.sync 1, 256;" ::: "memory");
@@ -256,15 +267,22 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc05_panel_kernel(
         const uint32_t kk = sm.kcol[tid];
         b0 = __ldg(B.trp + kk);
         len = __ldg(B.trp + kk + 1) - b0;
-        sm.bstart[tid] = b0;
+        sm.bstart[tid] = 0;
+        sm.bfirst[tid] = b0;
       }
       uint32_t tot;
       const uint32_t off = scan256(len, sm.wsum, tid, tot);
+      if (uint32_t(tid) < nk) sm.koff[tid] = off;
+      if (tid == 0) sm.koff[nk] = tot;
       if (tot > uint32_t(kTcMaxJ)) {
         if (tid == 0) sm.flag = 1u;
       } else {
         if (tid == 0) sm.flag = 0u;
-        for (uint32_t q = 0; q < len; ++q) sm.gather[off + q] = __ldg(&B.tco[b0 + q].x);
+        for (uint32_t q = 0; q < len; ++q) {
+          const uint32_t J = __ldg(&B.tco[b0 + q].x);
+          sm.gather[off + q] = J;
+          sm.bcolk[off + q] = J;
+        }
         uint32_t n2 = 32;
         while (n2 < tot) n2 <<= 1;
         for (uint32_t i = tot + tid; i < n2; i += 256) sm.gather[i] = 0xffffffffu;
@@ -297,11 +315,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc05_panel_kernel(
       const uint32_t wn = min(16u, nj - w0);
       const uint32_t jlast = sm.jcol[w0 + wn - 1];
       if (tid < 256) {  // work items: per k (thread), its B tiles with J in the window
-        uint32_t cnt = 0, b = 0, bend = 0;
+        uint32_t cnt = 0, b = 0, bend = 0;  // b: position within B row k (bcolk at koff)
         if (uint32_t(tid) < nk) {
           b = sm.bstart[tid];
-          bend = __ldg(B.trp + sm.kcol[tid] + 1);
-          while (b + cnt < bend && __ldg(&B.tco[b + cnt].x) <= jlast) ++cnt;
+          bend = sm.koff[tid + 1] - sm.koff[tid];
+          const uint32_t* bc = sm.bcolk + sm.koff[tid];
+          while (b + cnt < bend && bc[b + cnt] <= jlast) ++cnt;
         }
         uint32_t ni, nb;
         const uint32_t ip = scan256(cnt ? 1u : 0u, sm.wsum, tid, ni);
@@ -311,15 +330,14 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc05_panel_kernel(
           sm.item_b0[ip] = bp;
           uint32_t s2 = 0;
           for (uint32_t q = 0; q < cnt; ++q) {
-            const uint2 bt = __ldg(B.tco + b + q);
+            const uint32_t bt_i = sm.bfirst[tid] + b + q;
+            const uint2 bt = __ldg(B.tco + bt_i);
             while (sm.jcol[w0 + s2] < bt.x) ++s2;
-            sm.bt_idx[bp + q] = b + q;
+            sm.bt_idx[bp + q] = bt_i;
             sm.bt_slot[bp + q] = uint8_t(s2);
 #pragma unroll
-            for (int r = 0; r < 8; ++r) {  // filtered pairs: A column occupancy & B row occupancy
-              const uint32_t at = sm.ktile[tid][r];
-              if (at != kNoTile) n_filt += ((__ldg(&A.tco[at].y) & (bt.y >> 16) & 0xffffu) != 0u);
-            }
+            for (int r = 0; r < 8; ++r)  // filtered pairs: A column occupancy & B row occupancy
+              n_filt += (uint32_t(sm.kocc[tid][r]) & (bt.y >> 16)) != 0u;
           }
           sm.bstart[tid] = b + cnt;
         }
@@ -331,47 +349,59 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc05_panel_kernel(
       __syncthreads();
       const uint32_t ni = sm.nitems;
       if (warp < 4) {
-        // ---- producers: densify each item's A_k block and B tiles into its ring stage
-        for (uint32_t it = 0; it < ni; ++it, ++prod_it) {
-          const uint32_t s = prod_it % kTcStages, ph = (prod_it / kTcStages) & 1u;
+        // ---- producers: warp w densifies the items g = w (mod 4) of the running
+        // item count into ring stage w (four items in flight): the item's A_k
+        // block (8 tile rows, lane-dense A chunks -> K-major rows 16 r + row)
+        // and its B tiles (B-role chunks hold B^T in A order, registers
+        // {reg0, reg2, reg1, reg3})
+        for (uint32_t it = 0; it < ni; ++it) {
+          const uint32_t gi = item_base + it;
+          if ((gi & 3u) != uint32_t(warp)) continue;
+          const uint32_t s = gi & 3u, ph = (gi >> 2) & 1u;
           mbar_wait(&sm.empty[s], ph ^ 1u);
           uint8_t* st = sm.ring[s];
           const uint32_t ki = sm.item_k[it];
-          // A_k: tile row r = 2 warp + h (two per warp), lane-dense A chunks -> K-major rows 16 r + row
+          const int g = lane >> 2, t = lane & 3;
+          const unsigned lt = lanemask_lt(), bit = 1u << lane;
+          uint2 am[8];
 #pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const int r = 2 * warp + h;
+          for (int r = 0; r < 8; ++r) {
             const uint32_t at = sm.ktile[ki][r];
-            uint4 ch = make_uint4(0, 0, 0, 0);
-            if (at != kNoTile) {
-              const uint2 mt = __ldg(A.meta[kRoleA] + at);
-              ch = load_chunk(A.chunk[kRoleA], mt.x, mt.y, lanemask_lt(), 1u << lane);
-            }
-            const uint32_t regs[4] = {ch.x, ch.y, ch.z, ch.w};
-            const int g = lane >> 2, t = lane & 3;
+            am[r] = at != kNoTile ? __ldg(A.meta[kRoleA] + at) : make_uint2(0, 0);
+          }
+          uint4 ach[8];
+#pragma unroll
+          for (int r = 0; r < 8; ++r) ach[r] = load_chunk(A.chunk[kRoleA], am[r].x, am[r].y, lt, bit);
+#pragma unroll
+          for (int r = 0; r < 8; ++r) {
+            const uint32_t regs[4] = {ach[r].x, ach[r].y, ach[r].z, ach[r].w};
 #pragma unroll
             for (int i = 0; i < 4; ++i) {  // reg i: row g + 8(i&1), cols 2t + 8(i>>1) .. +1
-              const uint32_t m = uint32_t(16 * r + g + 8 * (i & 1)), k = uint32_t(2 * t + 8 * (i >> 1));
-              const uint32_t off = kmaj(m, k, 128);
+              const uint32_t off = kmaj(uint32_t(16 * r + g + 8 * (i & 1)), uint32_t(2 * t + 8 * (i >> 1)), 128);
               *reinterpret_cast<uint32_t*>(st + off) = regs[i];
               *reinterpret_cast<uint32_t*>(st + kABytes + off) = nz_h2(regs[i]);
             }
           }
-          // B tiles (k, J): B-role chunks hold B^T in A order, registers {reg0, reg2, reg1, reg3}
           const uint32_t b0 = sm.item_b0[it], b1 = sm.item_b0[it + 1];
-          for (uint32_t q = b0 + warp; q < b1; q += 4) {
-            const uint32_t bt = sm.bt_idx[q];
-            const uint2 mt = __ldg(B.meta[kRoleB] + bt);
-            const uint4 ch = load_chunk(B.chunk[kRoleB], mt.x, mt.y, lanemask_lt(), 1u << lane);
-            const uint32_t regs[4] = {ch.x, ch.z, ch.y, ch.w};  // back to A order of B^T
-            const int g = lane >> 2, t = lane & 3;
-            uint8_t* bv = st + 2 * kABytes + (q - b0) * 2 * kBBytes;
+          for (uint32_t q0 = b0; q0 < b1; q0 += 4) {
+            uint2 bm[4];
 #pragma unroll
-            for (int i = 0; i < 4; ++i) {  // B^T row n = g + 8(i&1), inner k = 2t + 8(i>>1)
-              const uint32_t n = uint32_t(g + 8 * (i & 1)), k = uint32_t(2 * t + 8 * (i >> 1));
-              const uint32_t off = kmaj(n, k, 16);
-              *reinterpret_cast<uint32_t*>(bv + off) = regs[i];
-              *reinterpret_cast<uint32_t*>(bv + kBBytes + off) = nz_h2(regs[i]);
+            for (int u = 0; u < 4; ++u)
+              bm[u] = q0 + u < b1 ? __ldg(B.meta[kRoleB] + sm.bt_idx[q0 + u]) : make_uint2(0, 0);
+            uint4 bch[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) bch[u] = load_chunk(B.chunk[kRoleB], bm[u].x, bm[u].y, lt, bit);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              if (q0 + u >= b1) break;
+              const uint32_t regs[4] = {bch[u].x, bch[u].z, bch[u].y, bch[u].w};  // back to A order of B^T
+              uint8_t* bv = st + 2 * kABytes + (q0 + u - b0) * 2 * kBBytes;
+#pragma unroll
+              for (int i = 0; i < 4; ++i) {  // B^T row n = g + 8(i&1), inner k = 2t + 8(i>>1)
+                const uint32_t off = kmaj(uint32_t(g + 8 * (i & 1)), uint32_t(2 * t + 8 * (i >> 1)), 16);
+                *reinterpret_cast<uint32_t*>(bv + off) = regs[i];
+                *reinterpret_cast<uint32_t*>(bv + kBBytes + off) = nz_h2(regs[i]);
+              }
             }
           }
           fence_proxy_async();
@@ -383,8 +413,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc05_panel_kernel(
           mbar_wait(&sm.tempty, (win_it & 1u) ^ 1u);  // the epilogue drained the previous window
           tc_fence_after();
           uint32_t touched = 0;
-          for (uint32_t it = 0; it < ni; ++it, ++mma_it) {
-            const uint32_t s = mma_it % kTcStages, ph = (mma_it / kTcStages) & 1u;
+          for (uint32_t it = 0; it < ni; ++it) {
+            const uint32_t gi = item_base + it;
+            const uint32_t s = gi & 3u, ph = (gi >> 2) & 1u;
             mbar_wait(&sm.full[s], ph);
             tc_fence_after();
             const uint32_t base = smem_u32(sm.ring[s]);
@@ -437,6 +468,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc05_panel_kernel(
         mbar_arrive(&sm.tempty);
       }
       ++win_it;
+      item_base += ni;
       __syncthreads();  // the window's lists are rewritten next
     }
     if (warp >= 5) {  // realised entries of this thread's row

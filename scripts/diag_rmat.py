@@ -31,3 +31,18 @@ for name, X in (("same", Ad), ("copy", A2), ("panel0/8", P0)):
     print(f"{name:9s} " + " ".join(f"{k}={st[k]*1e3:.3f}" for k in keys) +
           f" numeric_kernel={ctx.last_phase_ms('numeric_kernel'):.3f} path={st['path']} nnz={st['nnz_c']}"
           f" launches={st['kernel_launches']} staged={st['staged_slots']}", flush=True)
+
+# the multi-device context with one and with eight panel workers on GPU 0
+import time  # noqa: E402
+for n in (1, 8):
+    m = Context(devices=[0] * n)
+    for i in range(3):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        r = m.spgemm(Ad, Ad, out="device", phase_timing=True)
+        torch.cuda.synchronize()
+        wall = (time.perf_counter() - t0) * 1e3
+    st = r.stats
+    print(f"multi{n}   " + " ".join(f"{k}={st[k]*1e3:.3f}" for k in keys) + f" wall={wall:.1f}ms panel_ms=" +
+          " ".join(f"{x:.2f}" for x in m.panel_ms()), flush=True)
+    m.close()

@@ -1,11 +1,11 @@
-"""Multi-GPU readiness on one GPU: the multi-device
-context with N panel workers all on GPU 0 (tsg_create_multi with a repeated
-ordinal) runs each rank's work-balanced tile-row panel of A one after
-another and times each on its own stream (tsg_last_panel_ms).  The max over
-panels is what an N-GPU run's compute takes (the NVLink copy of B, ~0.1-0.2
-ms for R-MAT's 101 MB CSR, is not in it: the panels share GPU 0's copy).
-Device-resident inputs and outputs, median of a few calls after warm-up.
-Usage: python scripts/emulate_ranks.py [config ...]"""
+"""Multi-GPU readiness on one GPU: every rank's call of
+an N-GPU run, timed alone.  Rank p's operands are its work-balanced tile-row
+panel of A (paper_2009_14600_b200/distributed.py panel_bounds, the split
+bench.py and tsg_create_multi use) and the full B, device-resident; its
+device time is the library's own event bracket (tsg_run_stats.total, median
+of 3 after warm-up).  The max over ranks is the compute time of the N-GPU
+step; the broadcast of B (R-MAT: 101 MB of CSR, ~0.1-0.2 ms over NVLink) is
+not included.  Usage: python scripts/emulate_ranks.py [config ...]"""
 import os
 import statistics
 import sys
@@ -13,39 +13,53 @@ import sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch  # noqa: E402
 
+from paper_2009_14600_b200 import distributed as D  # noqa: E402
 from paper_2009_14600_b200 import workloads as W  # noqa: E402
-from paper_2009_14600_b200.tilemul import Context  # noqa: E402
+from paper_2009_14600_b200.tilemul import Context, Csr  # noqa: E402
 
 
 def dev(M):
-    D = M.to_device("cuda")
-    h = D.val.to(torch.float16)
-    return type(D)(D.rows, D.cols, D.row_ptr, D.col, h) if torch.equal(h.to(D.val.dtype), D.val) else D
+    Dm = M.to_device("cuda")
+    h = Dm.val.to(torch.float16)
+    return Csr(Dm.rows, Dm.cols, Dm.row_ptr, Dm.col, h) if torch.equal(h.to(Dm.val.dtype), Dm.val) else Dm
+
+
+def call(ctx, mats):
+    if len(mats) == 3:
+        return ctx.spgemm_chain(mats, out="device", phase_timing=True).stats
+    return ctx.spgemm(mats[0], mats[1], out="device", phase_timing=True).stats
 
 
 def main():
-    cfgs = sys.argv[1:] or ["rmat", "fem27"]
-    print("| config | N | panel ms (each rank) | max | N=1 / max | balance max/mean |")
+    cfgs = sys.argv[1:] or ["rmat", "fem27", "amg"]
+    ctx = Context(device=0)
+    print("| config | N | per-rank ms (convert + rest) | max | N=1 / max | max / mean |")
     print("|---|---|---|---|---|---|")
     for cfg in cfgs:
-        mats = [dev(M) for M in W.make(cfg)]
+        host = W.make(cfg)
+        A, rest = host[0], host[1:] if len(host) > 1 else host[:1]
+        rest_d = [dev(M) for M in rest]
         base = None
         for N in (1, 2, 4, 8):
-            ctx = Context(devices=[0] * N)
-            runs = []
-            for i in range(5):
-                if len(mats) == 3:
-                    ctx.spgemm_chain(mats, out="device")
-                else:
-                    ctx.spgemm(mats[0], mats[1] if len(mats) > 1 else mats[0], out="device")
-                if i >= 2:
-                    runs.append(ctx.panel_ms())
-            ctx.close()
-            per = [statistics.median(r[p] for r in runs) for p in range(N)]
+            per, conv = [], []
+            for r0, r1 in D.panel_bounds(A, rest[0], N):
+                square = len(host) == 1
+                # N = 1 of a square product is the plain A.A call (one operand, converted once)
+                mats = ([rest_d[0]] if N == 1 and square else [dev(D.take_rows(A, r0, r1))]) + rest_d
+                runs = []
+                for i in range(5):
+                    st = call(ctx, mats)
+                    if i >= 2:
+                        runs.append((st["total"] * 1e3, st["convert"] * 1e3))
+                per.append(statistics.median(x[0] for x in runs))
+                conv.append(statistics.median(x[1] for x in runs))
+                del mats
+                torch.cuda.empty_cache()
             mx = max(per)
             base = mx if N == 1 else base
-            print(f"| {cfg} | {N} | {' / '.join(f'{x:.2f}' for x in per)} | {mx:.3f} | {base / mx:.2f} | "
-                  f"{mx / (sum(per) / N):.2f} |", flush=True)
+            cells = " / ".join(f"{t:.2f} ({c:.2f})" for t, c in zip(per, conv))
+            print(f"| {cfg} | {N} | {cells} | {mx:.3f} | {base / mx:.2f} | {mx / (sum(per) / N):.2f} |", flush=True)
+    ctx.close()
 
 
 if __name__ == "__main__":
