@@ -321,7 +321,7 @@ const uint32_t* convert(tsg_ctx* ctx, Scratch& sc, const CsrView& in, TileMat& T
     if (roles & (1 << role)) cs.rec[role] = sc.alloc<uint4>(cap);
   launch_validate_rowptr(in, err_flag, ctx->stream);
   launch_convert(in, T, roles, cs, err_flag, drop_nonfinite, needed, ctx->stream);
-  check_launch(ctx, 3);
+  check_launch(ctx, 4);
   T.trp = sc.alloc<uint32_t>(nr);
   exclusive_sum(ctx, sc, cs.ntiles, T.trp, nr);
   T.tco = sc.alloc<uint2>(cap);
@@ -753,7 +753,7 @@ struct Call {
       sum_u32_kernel<<<sblocks, 256, 0, s>>>(row_np, nr - 1, tot_d);
       sum_u32_kernel<<<sblocks, 256, 0, s>>>(row_ns, nr - 1, tot_d + 1);
       sum_u32_kernel<<<sblocks, 256, 0, s>>>(row_raw, nr - 1, tot_d + 2);
-      check_launch(ctx, 3);
+      check_launch(ctx, 4);
     };
     if (elem) {
       launch_elem_bound(dA, dB.row_ptr, Bin->cols, row_bound, tot_d + 3, err_flag, s);
@@ -1031,7 +1031,7 @@ struct Call {
     auto* hist = sc.alloc<unsigned long long>(nc1);
     TSG_CUDA(cudaMemsetAsync(hist, 0, nc1 * sizeof(unsigned long long), s));
     launch_esc_hist(g, nnzA, Bin->rows, colcnt, hist, s);
-    check_launch(ctx, 3);
+    check_launch(ctx, 4);
     auto* G = sc.alloc<unsigned long long>(nc1);
     exclusive_sum(ctx, sc, hist, G, nc1);
     // (2) products per tile row -> units (groups of light rows, column ranges

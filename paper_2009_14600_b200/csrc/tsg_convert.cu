@@ -139,11 +139,20 @@ __device__ __forceinline__ void mark_column(const Gapped& out, uint32_t J) {
   if (out.mark && !out.mark[J]) out.mark[J] = 1;  // most tiles share their column's flag: skip the store
 }
 
-// records this tile row's tile count; true when the call is known to be general
-__device__ __forceinline__ bool general_call(const Gapped& out, uint32_t ntiles) {
+// The general flag as a tile row starts (read early: its latency overlaps the
+// row's loads) ...
+__device__ __forceinline__ bool general_seen(const Gapped& out) {
+  return out.general && *reinterpret_cast<volatile unsigned*>(out.general) != 0u;
+}
+// ... and once its tile count is known: true when the call is general (this row
+// of A has more than kLightMax tiles, or the flag was already set)
+__device__ __forceinline__ bool general_call(const Gapped& out, uint32_t ntiles, bool seen) {
   if (!out.general) return false;
-  if (out.may_set && ntiles > kLightMax) atomicOr(out.general, 1u);
-  return *reinterpret_cast<volatile unsigned*>(out.general) != 0u;
+  if (out.may_set && ntiles > kLightMax) {
+    atomicOr(out.general, 1u);
+    return true;
+  }
+  return seen;
 }
 
 // Tile-slot (r, c) of a 16x16 tile -> its lane and fp16 position in the
@@ -185,7 +194,7 @@ struct __align__(16) FastSmem {  // 16-byte multiple: the tiles use 16-byte acce
 // tile column are the tiles, in (row, col) order inside; lanes then emit one
 // tile each.
 __device__ __forceinline__ uint32_t sparse_panel(FastSmem& sm, const Gapped& out, int roles, int64_t E0, uint32_t E,
-                                                 uint32_t nk, int lane) {
+                                                 uint32_t nk, int lane, bool seen) {
   unsigned long long* it = sm.items;
   uint32_t P2 = 32;
   while (P2 < E) P2 <<= 1;
@@ -221,7 +230,7 @@ __device__ __forceinline__ uint32_t sparse_panel(FastSmem& sm, const Gapped& out
     ntiles += __popc(sb);
   }
   if (lane == 0) sm.ts[ntiles] = uint16_t(nk);
-  const bool lite = __shfl_sync(kFull, lane == 0 ? general_call(out, ntiles) : false, 0);
+  const bool lite = __shfl_sync(kFull, lane == 0 ? general_call(out, ntiles, seen) : false, 0);
   __syncwarp();
   // lanes emit tiles t = lane, lane + 32, ...; chunk bases by a warp scan
   uint32_t runA = 1u + uint32_t(E0), runB = 1u + uint32_t(E0);
@@ -332,6 +341,7 @@ __global__ void __launch_bounds__(256, 4) convert_fast_kernel(CsrView in, uint32
     return;
   }
   FastSmem& sm = smem[wib];
+  const bool seen = lane == 0 && general_seen(out);
   const int64_t r0 = int64_t(I) * kTile, r1 = r0 + kTile < in.rows ? r0 + kTile : in.rows;
   const int64_t row = r0 + lane;
   const bool has_row = lane < kTile && row < in.rows;
@@ -437,7 +447,7 @@ __global__ void __launch_bounds__(256, 4) convert_fast_kernel(CsrView in, uint32
                        : ~0ull;
     }
     __syncwarp();
-    const uint32_t nt = sparse_panel(sm, out, roles, E0, E, nk, lane);
+    const uint32_t nt = sparse_panel(sm, out, roles, E0, E, nk, lane, seen);
     const unsigned e = __reduce_or_sync(kFull, err);
     if (lane == 0) {
       out.ntiles[I] = nt;
@@ -497,7 +507,7 @@ __global__ void __launch_bounds__(256, 4) convert_fast_kernel(CsrView in, uint32
     return;
   }
   // a general call reads no chunks / masks / lane metadata of this tile row
-  const bool lite = __shfl_sync(kFull, lane == 0 ? general_call(out, ntiles) : false, 0);
+  const bool lite = __shfl_sync(kFull, lane == 0 ? general_call(out, ntiles, seen) : false, 0);
   for (uint32_t i = lane; i < ntiles * 8u; i += 32) sm.rm[i >> 3][i & 7] = 0;
   for (uint32_t i = lane; i < ntiles * 2u; i += 32) sm.lm[i >> 1][i & 1] = 0;
   __syncwarp();
@@ -640,6 +650,24 @@ __device__ __forceinline__ void staged_regs(const uint16_t* tl, int lane, uint32
   for (int i = 0; i < 4; ++i) r[i] = tw[((g + 8 * (i & 1)) * 16 + 2 * tq + 8 * (i >> 1)) >> 1];
 }
 
+constexpr int kHubThreads = 256;
+constexpr uint32_t kHubMax = 4096;
+
+// Which listed tile rows convert_hub_kernel converts (the walk kernel takes
+// the rest): needed, well-formed row pointers, 512 < entries <= 4096, tile
+// columns that fit the 24-bit item field.  Warp-collective; every warp of
+// both kernels computes the same answer.
+__device__ __forceinline__ bool hub_takes(const CsrView& in, uint32_t I, const uint8_t* needed, int lane) {
+  if ((needed && !needed[I]) || in.cols > (int64_t(1) << 28)) return false;
+  const int64_t r0 = int64_t(I) * kTile, r1 = r0 + kTile < in.rows ? r0 + kTile : in.rows;
+  const int nr = int(r1 - r0);
+  const int64_t v = lane <= nr ? in.row_ptr[r0 + lane] : 0;
+  const int64_t nxt = __shfl_down_sync(kFull, v, 1);
+  const bool mono = lane >= nr || nxt >= v;
+  const int64_t E = __shfl_sync(kFull, v, nr) - __shfl_sync(kFull, v, 0);
+  return __all_sync(kFull, mono) && E > 32 * kFastU && E <= int64_t(kHubMax);
+}
+
 // The general panel walk (any column span, any number of tiles): warp per
 // listed tile row, lanes r < 16 own CSR rows; each step takes the minimum
 // pending tile column (REDUX), every row lane consumes its entries in that
@@ -657,6 +685,7 @@ __global__ void __launch_bounds__(256) convert_walk_kernel(CsrView in, Gapped ou
   const uint32_t n_list = *walk_count;
   for (uint32_t li = blockIdx.x * 8 + wib; li < n_list; li += gridDim.x * 8) {
     const uint32_t I = walk_list[li];
+    if (hub_takes(in, I, needed, lane)) continue;  // convert_hub_kernel's
     const int64_t row = int64_t(I) * kTile + lane;
     const bool has_row = lane < kTile && row < in.rows;
     int64_t p = has_row ? in.row_ptr[row] : 0;
@@ -687,7 +716,7 @@ __global__ void __launch_bounds__(256) convert_walk_kernel(CsrView in, Gapped ou
     int32_t prev_col = -1;
     // a general call (flagged by some tile row of A with > kLightMax tiles) reads
     // no chunks, masks or lane metadata: only tile columns, occupancy, etile, h16
-    const bool lite = __shfl_sync(kFull, lane == 0 ? general_call(out, 0) : false, 0);
+    const bool lite = __shfl_sync(kFull, lane == 0 ? general_seen(out) : false, 0);
     int32_t c_cur = p < end ? __ldg(in.col + p) : 0;  // one entry ahead: the walk is not a chain of loads
     while (true) {
       const uint32_t my_tc = (p < end) ? uint32_t(c_cur) >> 4 : 0xffffffffu;
@@ -760,6 +789,214 @@ __global__ void __launch_bounds__(256) convert_walk_kernel(CsrView in, Gapped ou
       out.ntiles[I] = ntiles;
       if (e) atomicOr(err_flag, e);
     }
+  }
+}
+
+// Hub panels (512 < entries <= 4096: R-MAT's dense tile rows), CTA per
+// listed tile row -- the CTA-wide form of sparse_panel: every entry becomes a
+// 64-bit item (tile column << 40 | row << 36 | col & 15 << 32 | entry << 16 |
+// fp16), the items are bitonic-sorted in shared memory, runs of equal tile
+// column are the tiles, and threads emit one tile each.  Tile rows it does not
+// take (more entries, or malformed rows) stay with convert_walk_kernel.
+
+
+struct HubSmem {
+  unsigned long long it[kHubMax];
+  uint16_t ts[kHubMax + 1];  // first item of each tile (<= 4096)
+  int64_t rp[kTile + 1];
+  uint32_t wsum[kHubThreads / 32];
+  uint32_t bad;
+};
+
+// exclusive block scan (kHubThreads threads)
+__device__ __forceinline__ uint32_t hub_scan(HubSmem& sm, uint32_t x, uint32_t& tot) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  uint32_t inc = x;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(kFull, inc, o);
+    if (lane >= o) inc += y;
+  }
+  if (lane == 31) sm.wsum[w] = inc;
+  __syncthreads();
+  uint32_t pre = 0;
+  tot = 0;
+#pragma unroll
+  for (int i = 0; i < kHubThreads / 32; ++i) {
+    const uint32_t v = sm.wsum[i];
+    if (i < w) pre += v;
+    tot += v;
+  }
+  __syncthreads();
+  return pre + inc - x;
+}
+
+template <int kDtype>
+__global__ void __launch_bounds__(kHubThreads) convert_hub_kernel(CsrView in, Gapped out, int roles,
+                                                                 const uint32_t* __restrict__ walk_list,
+                                                                 const uint32_t* __restrict__ walk_count,
+                                                                 unsigned* __restrict__ err_flag, int drop_nonfinite,
+                                                                 const uint8_t* __restrict__ needed) {
+  __shared__ HubSmem sm;
+  const int tid = threadIdx.x;
+  const uint32_t n_list = *walk_count;
+  for (uint32_t li = blockIdx.x; li < n_list; li += gridDim.x) {
+    const uint32_t I = walk_list[li];
+    if (!hub_takes(in, I, needed, tid & 31)) continue;  // the walk kernel's
+    const int64_t r0 = int64_t(I) * kTile, r1 = r0 + kTile < in.rows ? r0 + kTile : in.rows;
+    if (tid <= kTile) sm.rp[tid] = in.row_ptr[r0 + tid < r1 ? r0 + tid : r1];
+    __syncthreads();
+    const int64_t E0 = sm.rp[0];
+    const uint32_t E = uint32_t(sm.rp[r1 - r0] - E0);
+    uint32_t P2 = 1024;
+    while (P2 < E) P2 <<= 1;
+    unsigned err = 0;
+    // items (kept entries), sentinel ~0 for dropped entries and padding
+    for (uint32_t q = tid; q < P2; q += kHubThreads) {
+      unsigned long long item = ~0ull;
+      if (q < E) {
+        const int64_t e = E0 + q;
+        int r = 0;  // row: last rp <= e
+#pragma unroll
+        for (int b = 8; b > 0; b >>= 1)
+          if (r + b <= int(r1 - r0) - 1 && sm.rp[r + b] <= e) r += b;
+        while (r < int(r1 - r0) - 1 && sm.rp[r + 1] <= e) ++r;  // empty rows
+        const int32_t c = __ldg(in.col + e);
+        const bool later = e > sm.rp[r];
+        const int32_t cp = later ? __ldg(in.col + e - 1) : -1;
+        if (c >= in.cols || c < 0 || (later && c <= cp)) err |= kErrInvariant;
+        bool keep;
+        const unsigned short h = load_half<kDtype>(in.val, e, drop_nonfinite, err, keep);
+        keep = keep && c >= 0 && c < in.cols;
+        if (out.h16) out.h16[e] = keep ? h : (unsigned short)0;
+        if (out.etile && !keep) out.etile[e] = kNoTile;
+        if (keep)
+          item = (static_cast<unsigned long long>(uint32_t(c) >> 4) << 40) |
+                 (static_cast<unsigned long long>(r) << 36) |
+                 (static_cast<unsigned long long>(uint32_t(c) & 15u) << 32) |
+                 (static_cast<unsigned long long>(q) << 16) | h;
+      }
+      sm.it[q] = item;
+    }
+    __syncthreads();
+    // bitonic sort, ascending
+    for (uint32_t k = 2; k <= P2; k <<= 1)
+      for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+        for (uint32_t pidx = tid; pidx < P2 / 2; pidx += kHubThreads) {
+          const uint32_t i = ((pidx & ~(j - 1u)) << 1) | (pidx & (j - 1u)), l = i | j;
+          const unsigned long long x = sm.it[i], y = sm.it[l];
+          if ((x > y) == ((i & k) == 0u)) {
+            sm.it[i] = y;
+            sm.it[l] = x;
+          }
+        }
+        __syncthreads();
+      }
+    // kept items: the prefix below the first sentinel; tile heads -> tile ranks
+    uint32_t nk = 0;
+    {
+      uint32_t c = 0;
+      for (uint32_t q = tid; q < E; q += kHubThreads) c += sm.it[q] != ~0ull;
+      uint32_t tot;
+      hub_scan(sm, c, tot);
+      nk = tot;
+    }
+    uint32_t ntiles = 0;
+    for (uint32_t base = 0; base < nk; base += kHubThreads) {
+      const uint32_t i = base + tid;
+      const unsigned long long x = i < nk ? sm.it[i] : ~0ull;
+      const unsigned long long xp = i > 0 && i < nk ? sm.it[i - 1] : ~0ull;
+      const bool start = i < nk && (i == 0 || (x >> 40) != (xp >> 40));
+      uint32_t tot;
+      const uint32_t pos = hub_scan(sm, start ? 1u : 0u, tot);
+      const uint32_t t = ntiles + pos + (start ? 1u : 0u) - 1u;  // tile of item i
+      if (start) sm.ts[ntiles + pos] = uint16_t(i);
+      if (i < nk && out.etile) {
+        const bool first_row = start || ((x >> 36) & 15u) != ((xp >> 36) & 15u);
+        out.etile[E0 + ((x >> 16) & 0xffffu)] = t | (first_row ? 0u : kDupEntry);
+      }
+      ntiles += tot;
+    }
+    if (tid == 0) sm.ts[ntiles] = uint16_t(nk);
+    if (tid == 0) sm.bad = general_call(out, ntiles, general_seen(out)) ? 1u : 0u;
+    __syncthreads();
+    const bool lite = sm.bad != 0;
+    // threads emit tiles t = tid, tid + 256, ...; chunk bases by a block scan
+    uint32_t runA = 1u + uint32_t(E0), runB = 1u + uint32_t(E0);
+    for (uint32_t t0 = 0; t0 < ntiles; t0 += kHubThreads) {
+      const uint32_t t = t0 + tid;
+      uint32_t rm[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+      uint32_t lmA = 0, lmB = 0, a = 0, b = 0, J = 0;
+      if (t < ntiles) {
+        a = sm.ts[t];
+        b = sm.ts[t + 1];
+        J = uint32_t(sm.it[a] >> 40);
+        for (uint32_t i = a; i < b; ++i) {
+          const unsigned long long x = sm.it[i];
+          const int r = int(x >> 36) & 15, cc = int(x >> 32) & 15;
+#pragma unroll
+          for (int g = 0; g < 8; ++g)
+            if (g == (r & 7)) rm[g] |= 1u << (cc + 16 * (r >> 3));
+          int L, h16;
+          slot_lane(kRoleA, r, cc, L, h16);
+          lmA |= 1u << L;
+          slot_lane(kRoleB, r, cc, L, h16);
+          lmB |= 1u << L;
+        }
+      }
+      const uint32_t nA = (roles & 1) && !lite ? __popc(lmA) : 0u, nB = (roles & 2) && !lite ? __popc(lmB) : 0u;
+      uint32_t totA, totB;
+      const uint32_t pA = hub_scan(sm, nA, totA);
+      const uint32_t pB = hub_scan(sm, nB, totB);
+      const uint32_t cbA = runA + pA, cbB = runB + pB;
+      runA += totA;
+      runB += totB;
+      if (t < ntiles) {
+        uint32_t colocc = 0, rowocc = 0;
+#pragma unroll
+        for (int g = 0; g < 8; ++g) {
+          colocc |= rm[g] | (rm[g] >> 16);
+          rowocc |= ((rm[g] & 0xffffu) != 0u ? 1u << g : 0u) | ((rm[g] >> 16) != 0u ? 1u << (g + 8) : 0u);
+        }
+        const uint32_t occ = (colocc & 0xffffu) | (rowocc << 16);
+        mark_column(out, J);
+        if (lite) {
+#pragma unroll
+          for (int role = 0; role < 2; ++role)
+            if (roles & (1 << role)) out.rec[role][E0 + t] = make_uint4(0u, 0u, occ, J);
+        } else {
+          uint4* dst = reinterpret_cast<uint4*>(out.rm2 + size_t(E0 + t) * 8);
+          dst[0] = make_uint4(rm[0], rm[1], rm[2], rm[3]);
+          dst[1] = make_uint4(rm[4], rm[5], rm[6], rm[7]);
+#pragma unroll
+          for (int role = 0; role < 2; ++role) {
+            if (!(roles & (1 << role))) continue;
+            const uint32_t lm = role == kRoleA ? lmA : lmB, cb = role == kRoleA ? cbA : cbB;
+            out.rec[role][E0 + t] = make_uint4(lm, cb, occ, J);
+            uint32_t n = 0;
+            for (uint32_t m = lm; m; m &= m - 1u, ++n) {  // present lanes, ascending
+              const int Lw = __ffs(m) - 1;
+              uint32_t w[4] = {0, 0, 0, 0};
+              for (uint32_t i = a; i < b; ++i) {
+                const unsigned long long x = sm.it[i];
+                int L, h16;
+                slot_lane(role, int(x >> 36) & 15, int(x >> 32) & 15, L, h16);
+                if (L != Lw) continue;
+                const uint32_t hv = uint32_t(x & 0xffffu) << (16 * (h16 & 1));
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                  if (q == (h16 >> 1)) w[q] |= hv;
+              }
+              out.chunk[role][cb + n] = make_uint4(w[0], w[1], w[2], w[3]);
+            }
+          }
+        }
+      }
+    }
+    const unsigned e_or = __reduce_or_sync(kFull, err);
+    if (e_or && (tid & 31) == 0) atomicOr(err_flag, e_or);
+    if (tid == 0) out.ntiles[I] = ntiles;
+    __syncthreads();  // shared memory is rewritten by the next tile row
   }
 }
 
@@ -879,6 +1116,10 @@ void launch_convert(const CsrView& in, TileMat& out, int roles, const ConvertScr
   auto kf = in.dtype == 0 ? convert_fast_kernel<0> : in.dtype == 2 ? convert_fast_kernel<2> : convert_fast_kernel<1>;
   kf<<<(out.tile_rows + 7) / 8, 256, 0, st>>>(in, out.tile_rows, g, roles, cs.walk_list, cs.walk_count, err_flag,
                                     drop_nonfinite, needed);
+  auto kh = in.dtype == 0 ? convert_hub_kernel<0> : in.dtype == 2 ? convert_hub_kernel<2> : convert_hub_kernel<1>;
+  kh<<<std::min<unsigned>((out.tile_rows + 7) / 8, 148u * 4u), kHubThreads, 0, st>>>(in, g, roles, cs.walk_list,
+                                                                                   cs.walk_count, err_flag,
+                                                                                   drop_nonfinite, needed);
   auto kw = in.dtype == 0 ? convert_walk_kernel<0> : in.dtype == 2 ? convert_walk_kernel<2> : convert_walk_kernel<1>;
   const unsigned wblocks = std::min<unsigned>((out.tile_rows + 7) / 8, 148u * 8u);
   kw<<<wblocks, 256, 0, st>>>(in, g, roles, cs.walk_list, cs.walk_count, err_flag, drop_nonfinite, needed);
