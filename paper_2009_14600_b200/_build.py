@@ -19,7 +19,9 @@ LIB = PKG / "libtsparse_b200.so"
 SOURCES = ["tsg_convert.cu", "tsg_panel.cu", "tsg_esc.cu", "tsg_tc05.cu", "tsg_api.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-O2",
+# TSG_NVCC_FLAGS: extra nvcc flags for A/B builds (e.g. -DTSG_ESC_NT=512)
+EXTRA = os.environ.get("TSG_NVCC_FLAGS", "").split()
+FLAGS = EXTRA + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-O2",
          "-Xcompiler", "-fvisibility=hidden",
          "--expt-relaxed-constexpr", "-I", str(ROOT / "include"), "-I", str(CSRC)]
 

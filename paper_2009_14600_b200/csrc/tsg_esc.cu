@@ -43,7 +43,8 @@ namespace {
 
 constexpr int kNT = kEscThreads;  // threads per CTA
 constexpr int kWarps = kNT / 32;
-constexpr int kMaxIPT = 16;             // products per thread, at most
+constexpr int kMaxIPT = 4096 / kNT;     // products per thread, at most (16 at 256 threads, 8 at 512)
+static_assert(kNT == 256 || kNT == 512, "esc_kernel is written for 256 or 512 threads");
 constexpr int kCap = kNT * kMaxIPT;     // products per sorted leaf
 constexpr int kGroup = 16;              // light tile rows per unit, at most
 constexpr uint32_t kDenseW = 256;       // columns of a dense leaf (16 x 256 accumulators)
@@ -126,35 +127,13 @@ __device__ __forceinline__ void block_scan2(EscSmem& sm, uint32_t& a, uint32_t& 
   __syncthreads();
 }
 
-// One stable LSD pass on the 4-bit digit at `shift` over the valid items
-// (mask vm) in registers: per-thread digit counts as 4-bit fields of a u64,
-// a raking scan of the [digit][thread] counters, scatter, blocked reload.
-// Returns the item count (dense from now on).
-template <int IPT>
-__device__ __forceinline__ uint32_t radix_pass(EscSmem& sm, uint32_t (&key)[IPT], float (&val)[IPT], uint32_t vm,
-                                               int shift) {
+// Exclusive scan of the per-thread 4-bit-digit counts w8[j] = count(j) |
+// count(j + 8) << 16 over (digit, thread) order: afterwards
+// ctr[cpad(j kNT + t)] holds the starts of digits j and j + 8 (the latter
+// relative to tlo = items with digits 0..7) for thread t.  Returns the packed
+// totals (lo16: digits 0..7, hi16: digits 8..15).
+__device__ __forceinline__ uint32_t digit_scan(EscSmem& sm, const uint32_t (&w8)[8]) {
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  unsigned long long C = 0, rk = 0;
-  uint32_t nv = 0, d0 = 0;
-#pragma unroll
-  for (int i = 0; i < IPT; ++i) {
-    if ((vm >> i) & 1u) {
-      const uint32_t s = ((key[i] >> shift) & 15u) << 2;
-      if (nv == 0) d0 = s;
-      rk |= ((C >> s) & 15ull) << (4 * i);
-      C += 1ull << s;
-      ++nv;
-    }
-  }
-  uint32_t w8[8];
-#pragma unroll
-  for (int j = 0; j < 8; ++j) w8[j] = uint32_t((C >> (4 * j)) & 15u) | (uint32_t((C >> (4 * j + 32)) & 15u) << 16);
-  if (IPT == 16 && nv == 16 && C == (d0 == 60 ? 0ull : (1ull << (d0 + 4)))) {
-    // all 16 items share digit d: its count (16) carried out of the 4-bit field
-    const uint32_t d = d0 >> 2;
-#pragma unroll
-    for (int j = 0; j < 8; ++j) w8[j] = uint32_t(j) == (d & 7u) ? (16u << (16 * (d >> 3))) : 0u;
-  }
 #pragma unroll
   for (int j = 0; j < 8; ++j) sm.s.ctr[cpad(j * kNT + tid)] = w8[j];
   __syncthreads();
@@ -186,6 +165,39 @@ __device__ __forceinline__ uint32_t radix_pass(EscSmem& sm, uint32_t (&key)[IPT]
     run += v[i];
   }
   __syncthreads();
+  return T;
+}
+
+// One stable LSD pass on the 4-bit digit at `shift` over the valid items
+// (mask vm) in registers: per-thread digit counts as 4-bit fields of a u64,
+// a raking scan of the [digit][thread] counters, scatter, blocked reload.
+// Returns the item count (dense from now on).
+template <int IPT>
+__device__ __forceinline__ uint32_t radix_pass(EscSmem& sm, uint32_t (&key)[IPT], float (&val)[IPT], uint32_t vm,
+                                               int shift) {
+  const int tid = threadIdx.x;
+  unsigned long long C = 0, rk = 0;
+  uint32_t nv = 0, d0 = 0;
+#pragma unroll
+  for (int i = 0; i < IPT; ++i) {
+    if ((vm >> i) & 1u) {
+      const uint32_t s = ((key[i] >> shift) & 15u) << 2;
+      if (nv == 0) d0 = s;
+      rk |= ((C >> s) & 15ull) << (4 * i);
+      C += 1ull << s;
+      ++nv;
+    }
+  }
+  uint32_t w8[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) w8[j] = uint32_t((C >> (4 * j)) & 15u) | (uint32_t((C >> (4 * j + 32)) & 15u) << 16);
+  if (IPT == 16 && nv == 16 && C == (d0 == 60 ? 0ull : (1ull << (d0 + 4)))) {
+    // all 16 items share digit d: its count (16) carried out of the 4-bit field
+    const uint32_t d = d0 >> 2;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) w8[j] = uint32_t(j) == (d & 7u) ? (16u << (16 * (d >> 3))) : 0u;
+  }
+  const uint32_t T = digit_scan(sm, w8);
   const uint32_t tlo = T & 0xffffu;  // items with digits 0..7: the base of digit 8
 #pragma unroll
   for (int i = 0; i < IPT; ++i) {
@@ -403,6 +415,110 @@ __device__ bool build_table(EscSmem& sm, const EscArgs& g, const Unit& u, uint32
   return true;
 }
 
+// A single-tile-row leaf after its cc and J passes.  The products arrived in
+// row order and every pass was stable, so the items are sorted by (J, cc, r)
+// -- equal output slots adjacent, in ascending k -- and each row's entries
+// come in column order.  A digit scan over the rows of the realised entries
+// (digit_scan, as in a radix pass but without the scatter) gives every entry
+// its row-major staging index directly: no row pass, no shared-memory emit.
+template <int IPT>
+__device__ void rowmajor_emit(EscSmem& sm, const EscArgs& g, const Unit& u, uint32_t lo, int jb, uint32_t n,
+                              const uint32_t (&key)[IPT], const float (&val)[IPT], PieceChain& pc,
+                              unsigned long long& segs, unsigned long long& structural) {
+  const int tid = threadIdx.x, lane = tid & 31;
+  const uint32_t g0 = uint32_t(tid) * IPT;
+  const uint32_t vmn = valid_mask<IPT>(n);
+  const bool cont = g0 > 0 && g0 < n && sm.s.key[phys<IPT>(g0 - 1)] == key[0];
+  auto run_tail = [&](uint32_t kcur, float s) {  // a run continuing into later threads
+    for (uint32_t gg = g0 + IPT; gg < n; ++gg) {
+      const uint32_t q = phys<IPT>(gg);
+      if (sm.s.key[q] != kcur) break;
+      s = __fadd_rn(s, sm.s.val[q]);
+    }
+    return s;
+  };
+  // the runs this thread owns (heads in its items), summed in k order; f(key, sum) per run
+  auto for_runs = [&](auto&& f) {
+    bool owned = false;
+    uint32_t kcur = 0;
+    float s = 0.f;
+#pragma unroll
+    for (int i = 0; i < IPT; ++i) {
+      if ((vmn >> i) & 1u) {
+        const bool head = i == 0 ? !cont : key[i] != key[i - 1];
+        if (head) {
+          if (owned) f(kcur, s);
+          owned = true;
+          kcur = key[i];
+          s = val[i];
+        } else if (owned) {
+          s = __fadd_rn(s, val[i]);
+        }
+      }
+    }
+    if (owned) f(kcur, run_tail(kcur, s));
+  };
+  // pass 1: structural slots, realised entries per row (8-bit fields: a thread
+  // may own 16 entries of one row)
+  unsigned long long c0 = 0, c1 = 0;
+  uint32_t nstruct = 0;
+  bool bad = false;
+  for_runs([&](uint32_t k, float x) {
+    ++nstruct;
+    bad |= !isfinite(x);
+    if (x != 0.0f) {
+      const uint32_t r = k & 15u;
+      if (r < 8)
+        c0 += 1ull << (8 * r);
+      else
+        c1 += 1ull << (8 * (r - 8));
+    }
+  });
+  if (__any_sync(kFull, bad) && lane == 0) atomicOr(g.err_flag, unsigned(kErrPrecision));
+  nstruct = __reduce_add_sync(kFull, nstruct);
+  if (lane == 0 && nstruct) atomicAdd(&sm.bc[1], nstruct);
+  uint32_t w8[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) w8[j] = uint32_t((c0 >> (8 * j)) & 0xffu) | (uint32_t((c1 >> (8 * j)) & 0xffu) << 16);
+  const uint32_t T = digit_scan(sm, w8);
+  const uint32_t tlo = T & 0xffffu, tot = tlo + (T >> 16);
+  auto start_of = [&](uint32_t r, int t) {  // staging index of row r's first entry of thread t
+    const uint32_t p = sm.s.ctr[cpad((r & 7u) * kNT + t)];
+    return r < 8 ? (p & 0xffffu) : (p >> 16) + tlo;
+  };
+  if (tid < 16) {  // the piece's per-row counts (sm.cnt[b = 0][r])
+    const uint32_t st = start_of(uint32_t(tid), 0), en = tid == 15 ? tot : start_of(uint32_t(tid) + 1, 0);
+    sm.cnt[tid] = en - st;
+  }
+  begin_piece(sm, g, u, tot, pc);  // (its barrier publishes sm.cnt)
+  // pass 2: each realised entry at its row-major staging index
+  if (sm.bc[0] != kNoPiece) {
+    uint2* __restrict__ dst = g.stage + piece_base(sm);
+    const uint32_t jmask = (1u << jb) - 1u;
+    unsigned long long l0 = 0, l1 = 0;
+    for_runs([&](uint32_t k, float x) {
+      if (x == 0.0f) return;
+      const uint32_t r = k & 15u;
+      uint32_t rank;
+      if (r < 8) {
+        rank = uint32_t((l0 >> (8 * r)) & 0xffu);
+        l0 += 1ull << (8 * r);
+      } else {
+        rank = uint32_t((l1 >> (8 * (r - 8))) & 0xffu);
+        l1 += 1ull << (8 * (r - 8));
+      }
+      dst[start_of(r, tid) + rank] = make_uint2(lo + (((k >> 8) & jmask) << 4) + ((k >> 4) & 15u), __float_as_uint(x));
+    });
+  }
+  if (tid == 0) {
+    segs += sm.bc[7];
+    structural += sm.bc[1];
+    sm.bc[7] = 0;
+    sm.bc[1] = 0;
+  }
+  end_piece(sm, g, u);
+}
+
 // Sorted leaf: expand, sort by (tile row, J, cc, r), segments, combine, write.
 template <int IPT>
 __device__ void sort_leaf(EscSmem& sm, const EscArgs& g, const Unit& u, uint32_t lo, uint32_t hi, uint32_t P,
@@ -486,6 +602,10 @@ __device__ void sort_leaf(EscSmem& sm, const EscArgs& g, const Unit& u, uint32_t
     heads = __reduce_add_sync(kFull, heads);
     if (lane == 0 && heads) atomicAdd(&sm.bc[7], heads);
   }
+  if (u.nb == 1) {
+    rowmajor_emit<IPT>(sm, g, u, lo, jb, n, key, val, pc, segs, structural);
+    return;
+  }
   // ---- row: order (r, tile row, J, cc); a (tile row, r) group is one CSR row slice
   n = radix_pass<IPT>(sm, key, val, valid_mask<IPT>(n), 0);
   const uint32_t vmn = valid_mask<IPT>(n);
@@ -551,11 +671,12 @@ __device__ void sort_leaf(EscSmem& sm, const EscArgs& g, const Unit& u, uint32_t
   // rank of its first entry (entries of the groups before it in (r, b) order),
   // and (b, r) = (t >> 4, t & 15) for its staging index (row-major order)
   {
-    uint32_t x = sm.cnt[((tid & 15) << 4) | (tid >> 4)], y = sm.cnt[tid], tx, ty;
+    const bool grp = tid < 256;  // one thread per (b, r) group
+    uint32_t x = grp ? sm.cnt[((tid & 15) << 4) | (tid >> 4)] : 0u, y = grp ? sm.cnt[tid] : 0u, tx, ty;
     block_scan2(sm, x, y, tx, ty);
-    sm.adj[((tid & 15) << 4) | (tid >> 4)] = int32_t(y);  // (r, b) slot <- staging start of (b, r)
+    if (grp) sm.adj[((tid & 15) << 4) | (tid >> 4)] = int32_t(y);  // (r, b) slot <- staging start of (b, r)
     __syncthreads();
-    sm.adj[tid] -= int32_t(x);
+    if (grp) sm.adj[tid] -= int32_t(x);
   }
   __syncthreads();
   // pass 2: write the realised entries at their staging index (global)
@@ -631,8 +752,9 @@ __device__ void dense_leaf(EscSmem& sm, const EscArgs& g, const Unit& u, uint32_
     }
   }
   __syncthreads();
-  // thread t: row t >> 4, columns 16 (t & 15) .. +15 (one tile column)
+  // thread t < 256: row t >> 4, columns 16 (t & 15) .. +15 (one tile column)
   const uint32_t row = tid >> 4, tc = tid & 15;
+  const bool dl = tid < 256;
   uint32_t nreal = 0, nst = 0;
   bool bad = false;
   float v[16];
@@ -640,7 +762,7 @@ __device__ void dense_leaf(EscSmem& sm, const EscArgs& g, const Unit& u, uint32_
   for (int i = 0; i < 16; ++i) {
     const uint32_t c = tc * 16 + i, s = row * kDenseW + c;
     v[i] = 0.f;
-    if (c < width && sm.d.flag[s]) {
+    if (dl && c < width && sm.d.flag[s]) {
       ++nst;
       v[i] = sm.d.acc[s];
       nreal += v[i] != 0.0f;
@@ -729,9 +851,9 @@ __global__ void __launch_bounds__(kNT, kMinBlocks) esc_kernel(EscArgs g) {
       } else if (fits) {
         if (P <= uint32_t(kNT) * 4)
           sort_leaf<4>(sm, g, u, lo, hi, P, ne, pc, segs, structural);
-        else if (P <= uint32_t(kNT) * 8)
+        else if (kMaxIPT == 8 || P <= uint32_t(kNT) * 8)
           sort_leaf<8>(sm, g, u, lo, hi, P, ne, pc, segs, structural);
-        else
+        else if constexpr (kMaxIPT >= 16)
           sort_leaf<16>(sm, g, u, lo, hi, P, ne, pc, segs, structural);
       } else if (u.nb > 1) {  // cannot happen: a group's products fit (planned exactly)
         if (tid == 0) atomicOr(g.err_flag, unsigned(kErrPool));
@@ -1120,8 +1242,11 @@ void launch_esc_plan_fill(const EscArgs& g, const unsigned long long* pre, const
 void launch_esc(const EscArgs& g, int device, cudaStream_t st) {
   // resident CTAs per SM: 3 (80 registers) or 4 (64 registers; TSG_ESC_MINB=4)
   static int per_sm[16][2] = {}, sms[16] = {0};
-  const int d = device & 15, v = tuning_variant("TSG_ESC_MINB", 3) == 4 ? 1 : 0;
-  auto k = v ? esc_kernel<4> : esc_kernel<3>;
+  // 256 threads: 3 CTAs/SM (80 registers) or 4 (TSG_ESC_MINB=4, 64 registers);
+  // 512 threads: 2 CTAs/SM (64 registers) or 3 (TSG_ESC_MINB=3)
+  constexpr int kB0 = kNT == 512 ? 2 : 3;
+  const int d = device & 15, v = tuning_variant("TSG_ESC_MINB", kB0) == kB0 + 1 ? 1 : 0;
+  auto k = v ? esc_kernel<kB0 + 1> : esc_kernel<kB0>;
   const size_t smem = sizeof(EscSmem);
   if (!per_sm[d][v]) {
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));

@@ -100,7 +100,10 @@ void launch_panel_copy(int64_t rows, const uint32_t* row_stage, const int64_t* r
 // (2)+(3) general rows: per (tile row, column range) chunk, the tile pairs
 // expanded into element products, sorted by output tile key in shared
 // memory, summed in k order, written as row-major pieces (tsg_esc.cu)
-constexpr int kEscThreads = 256;
+#ifndef TSG_ESC_NT
+#define TSG_ESC_NT 512  // threads per esc_kernel CTA (512: 22.8 ms vs 256: 23.4 ms on R-MAT; build-time switch)
+#endif
+constexpr int kEscThreads = TSG_ESC_NT;
 constexpr uint32_t kEscTarget = 3072;  // products per unit of a heavy tile row (sorted leaves hold 4096)
 constexpr uint32_t kNoPiece = 0xffffffffu;
 struct EscPiece {             // one sorted output piece: rows of tile row I, row-major
