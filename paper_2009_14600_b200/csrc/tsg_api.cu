@@ -1056,7 +1056,7 @@ struct Call {
     exclusive_sum(ctx, sc, nrec, rbase, nr);
     exclusive_sum(ctx, sc, nwk, wbase, nr);
     auto* njt = sc.alloc<uint32_t>(uint64_t(B.rows) + 1);
-    launch_esc_pairstats(TA, B, tA, njt, tot + 2, s);
+    launch_esc_pairstats(TA, B, dB.col, tA, njt, tot + 2, s);
     check_launch(ctx, 2);
     record(ctx, timing, 2);
     uint64_t nrecs = 0, nunits = 0, products = 0;

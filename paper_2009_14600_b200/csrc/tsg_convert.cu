@@ -651,14 +651,16 @@ __device__ __forceinline__ void staged_regs(const uint16_t* tl, int lane, uint32
 }
 
 constexpr int kHubThreads = 256;
-constexpr uint32_t kHubMax = 4096;
+constexpr uint32_t kHubMax = 8192;      // entries of a hub panel
+constexpr uint32_t kHubWords = 2048;    // tile-column bitmap: spans of <= 65536 tile columns
+constexpr uint32_t kHubDefer = 0xfffffffeu;  // ntiles[I]: the hub kernel handed the row to the walk
 
-// Which listed tile rows convert_hub_kernel converts (the walk kernel takes
-// the rest): needed, well-formed row pointers, 512 < entries <= 4096, tile
-// columns that fit the 24-bit item field.  Warp-collective; every warp of
-// both kernels computes the same answer.
+// Which listed tile rows convert_hub_kernel may take (the walk kernel takes
+// the rest, and the ones the hub kernel hands back): needed, well-formed row
+// pointers, 512 < entries <= kHubMax.  Warp-collective; every warp of both
+// kernels computes the same answer.
 __device__ __forceinline__ bool hub_takes(const CsrView& in, uint32_t I, const uint8_t* needed, int lane) {
-  if ((needed && !needed[I]) || in.cols > (int64_t(1) << 28)) return false;
+  if (needed && !needed[I]) return false;
   const int64_t r0 = int64_t(I) * kTile, r1 = r0 + kTile < in.rows ? r0 + kTile : in.rows;
   const int nr = int(r1 - r0);
   const int64_t v = lane <= nr ? in.row_ptr[r0 + lane] : 0;
@@ -685,7 +687,7 @@ __global__ void __launch_bounds__(256) convert_walk_kernel(CsrView in, Gapped ou
   const uint32_t n_list = *walk_count;
   for (uint32_t li = blockIdx.x * 8 + wib; li < n_list; li += gridDim.x * 8) {
     const uint32_t I = walk_list[li];
-    if (hub_takes(in, I, needed, lane)) continue;  // convert_hub_kernel's
+    if (hub_takes(in, I, needed, lane) && out.ntiles[I] != kHubDefer) continue;  // convert_hub_kernel's
     const int64_t row = int64_t(I) * kTile + lane;
     const bool has_row = lane < kTile && row < in.rows;
     int64_t p = has_row ? in.row_ptr[row] : 0;
@@ -792,20 +794,21 @@ __global__ void __launch_bounds__(256) convert_walk_kernel(CsrView in, Gapped ou
   }
 }
 
-// Hub panels (512 < entries <= 4096: R-MAT's dense tile rows), CTA per
-// listed tile row -- the CTA-wide form of sparse_panel: every entry becomes a
-// 64-bit item (tile column << 40 | row << 36 | col & 15 << 32 | entry << 16 |
-// fp16), the items are bitonic-sorted in shared memory, runs of equal tile
-// column are the tiles, and threads emit one tile each.  Tile rows it does not
-// take (more entries, or malformed rows) stay with convert_walk_kernel.
-
-
+// Hub panels of a general call (512 < entries <= kHubMax: R-MAT's dense
+// tile rows), CTA per listed tile row.  A general call reads no operand
+// chunks, masks or lane metadata, so no sort is needed: the kept entries mark
+// their tile columns in a shared-memory bitmap, the bitmap's prefix popcounts
+// rank the tiles (tile columns ascending, like from_element_coo's sort), and
+// shared-memory atomics gather each tile's occupancy words.  Tile rows of a
+// call that is not (yet) known to be general, or spanning more than 65536 tile
+// columns, are handed back to convert_walk_kernel (ntiles = kHubDefer).
 struct HubSmem {
-  unsigned long long it[kHubMax];
-  uint16_t ts[kHubMax + 1];  // first item of each tile (<= 4096)
+  uint32_t bits[kHubWords];
+  uint16_t wpre[kHubWords];  // tiles before each bitmap word (<= kHubMax)
+  uint32_t occ[kHubMax];     // per tile: column occupancy | row occupancy << 16
   int64_t rp[kTile + 1];
   uint32_t wsum[kHubThreads / 32];
-  uint32_t bad;
+  uint32_t jlo, jhi, flag;
 };
 
 // exclusive block scan (kHubThreads threads)
@@ -844,153 +847,106 @@ __global__ void __launch_bounds__(kHubThreads) convert_hub_kernel(CsrView in, Ga
     const uint32_t I = walk_list[li];
     if (!hub_takes(in, I, needed, tid & 31)) continue;  // the walk kernel's
     const int64_t r0 = int64_t(I) * kTile, r1 = r0 + kTile < in.rows ? r0 + kTile : in.rows;
+    const int nr = int(r1 - r0);
     if (tid <= kTile) sm.rp[tid] = in.row_ptr[r0 + tid < r1 ? r0 + tid : r1];
+    if (tid == 0) {
+      sm.jlo = 0xffffffffu;
+      sm.jhi = 0;
+      sm.flag = general_seen(out) ? 1u : 0u;
+    }
     __syncthreads();
+    // the panel's tile-column span from each row's first and last column
+    if (tid < nr && sm.rp[tid + 1] > sm.rp[tid]) {
+      const int32_t c0 = __ldg(in.col + sm.rp[tid]), c1 = __ldg(in.col + sm.rp[tid + 1] - 1);
+      if (c0 >= 0 && c0 < in.cols) atomicMin(&sm.jlo, uint32_t(c0) >> 4);
+      if (c1 >= 0 && c1 < in.cols) atomicMax(&sm.jhi, uint32_t(c1) >> 4);
+    }
+    for (uint32_t i = tid; i < kHubWords; i += kHubThreads) sm.bits[i] = 0;
+    __syncthreads();
+    const uint32_t jlo = sm.jlo;
+    if (!sm.flag || (jlo != 0xffffffffu && sm.jhi - jlo >= kHubWords * 32u)) {
+      if (tid == 0) out.ntiles[I] = kHubDefer;  // not known general yet, or too wide: the walk
+      __syncthreads();
+      continue;
+    }
     const int64_t E0 = sm.rp[0];
-    const uint32_t E = uint32_t(sm.rp[r1 - r0] - E0);
-    uint32_t P2 = 1024;
-    while (P2 < E) P2 <<= 1;
+    const uint32_t E = uint32_t(sm.rp[nr] - E0);
     unsigned err = 0;
-    // items (kept entries), sentinel ~0 for dropped entries and padding
-    for (uint32_t q = tid; q < P2; q += kHubThreads) {
-      unsigned long long item = ~0ull;
-      if (q < E) {
-        const int64_t e = E0 + q;
-        int r = 0;  // row: last rp <= e
+    // (1) validation, rounding, kept entries mark their tile columns
+    for (uint32_t q = tid; q < E; q += kHubThreads) {
+      const int64_t e = E0 + q;
+      int r = 0;
 #pragma unroll
-        for (int b = 8; b > 0; b >>= 1)
-          if (r + b <= int(r1 - r0) - 1 && sm.rp[r + b] <= e) r += b;
-        while (r < int(r1 - r0) - 1 && sm.rp[r + 1] <= e) ++r;  // empty rows
-        const int32_t c = __ldg(in.col + e);
-        const bool later = e > sm.rp[r];
-        const int32_t cp = later ? __ldg(in.col + e - 1) : -1;
-        if (c >= in.cols || c < 0 || (later && c <= cp)) err |= kErrInvariant;
-        bool keep;
-        const unsigned short h = load_half<kDtype>(in.val, e, drop_nonfinite, err, keep);
-        keep = keep && c >= 0 && c < in.cols;
-        if (out.h16) out.h16[e] = keep ? h : (unsigned short)0;
-        if (out.etile && !keep) out.etile[e] = kNoTile;
-        if (keep)
-          item = (static_cast<unsigned long long>(uint32_t(c) >> 4) << 40) |
-                 (static_cast<unsigned long long>(r) << 36) |
-                 (static_cast<unsigned long long>(uint32_t(c) & 15u) << 32) |
-                 (static_cast<unsigned long long>(q) << 16) | h;
+      for (int b = 8; b > 0; b >>= 1)
+        if (r + b <= nr - 1 && sm.rp[r + b] <= e) r += b;
+      const int32_t c = __ldg(in.col + e);
+      const bool later = e > sm.rp[r];
+      const int32_t cp = later ? __ldg(in.col + e - 1) : -1;
+      if (c >= in.cols || c < 0 || (later && c <= cp)) err |= kErrInvariant;
+      bool keep;
+      const unsigned short h = load_half<kDtype>(in.val, e, drop_nonfinite, err, keep);
+      keep = keep && c >= 0 && c < in.cols && (uint32_t(c) >> 4) >= jlo && (uint32_t(c) >> 4) - jlo < kHubWords * 32u;
+      if (out.h16) out.h16[e] = keep ? h : (unsigned short)0;
+      if (keep) {
+        const uint32_t j = (uint32_t(c) >> 4) - jlo;
+        atomicOr(&sm.bits[j >> 5], 1u << (j & 31));
+      } else if (out.etile) {
+        out.etile[e] = kNoTile;
       }
-      sm.it[q] = item;
     }
     __syncthreads();
-    // bitonic sort, ascending
-    for (uint32_t k = 2; k <= P2; k <<= 1)
-      for (uint32_t j = k >> 1; j > 0; j >>= 1) {
-        for (uint32_t pidx = tid; pidx < P2 / 2; pidx += kHubThreads) {
-          const uint32_t i = ((pidx & ~(j - 1u)) << 1) | (pidx & (j - 1u)), l = i | j;
-          const unsigned long long x = sm.it[i], y = sm.it[l];
-          if ((x > y) == ((i & k) == 0u)) {
-            sm.it[i] = y;
-            sm.it[l] = x;
+    // (2) tile ranks: tiles before each bitmap word
+    uint32_t wc[kHubWords / kHubThreads], lsum = 0;
+#pragma unroll
+    for (int i = 0; i < int(kHubWords / kHubThreads); ++i) {
+      wc[i] = __popc(sm.bits[tid * (kHubWords / kHubThreads) + i]);
+      lsum += wc[i];
+    }
+    uint32_t ntiles;
+    uint32_t run = hub_scan(sm, lsum, ntiles);
+#pragma unroll
+    for (int i = 0; i < int(kHubWords / kHubThreads); ++i) {
+      sm.wpre[tid * (kHubWords / kHubThreads) + i] = uint16_t(run);
+      run += wc[i];
+    }
+    for (uint32_t t = tid; t < ntiles; t += kHubThreads) sm.occ[t] = 0;
+    if (tid == 0 && out.may_set && ntiles > kLightMax) atomicOr(out.general, 1u);
+    __syncthreads();
+    // (3) occupancy words; etile = tile rank | duplicate flag (an earlier kept
+    // entry of the same row in the same tile)
+    for (uint32_t q = tid; q < E; q += kHubThreads) {
+      const int64_t e = E0 + q;
+      if (out.h16 && out.h16[e] == 0) continue;  // dropped
+      int r = 0;
+#pragma unroll
+      for (int b = 8; b > 0; b >>= 1)
+        if (r + b <= nr - 1 && sm.rp[r + b] <= e) r += b;
+      const uint32_t c = uint32_t(__ldg(in.col + e)), j = (c >> 4) - jlo;
+      const uint32_t t = sm.wpre[j >> 5] + __popc(sm.bits[j >> 5] & ((1u << (j & 31)) - 1u));
+      atomicOr(&sm.occ[t], (1u << (c & 15u)) | (1u << (16 + r)));
+      if (out.etile) {
+        bool dup = false;  // walk back over the row's entries in the same tile
+        for (int64_t p = e - 1; p >= sm.rp[r]; --p) {
+          if ((uint32_t(__ldg(in.col + p)) >> 4) != (c >> 4)) break;
+          if (out.h16[p] != 0) {
+            dup = true;
+            break;
           }
         }
-        __syncthreads();
+        out.etile[e] = t | (dup ? kDupEntry : 0u);
       }
-    // kept items: the prefix below the first sentinel; tile heads -> tile ranks
-    uint32_t nk = 0;
-    {
-      uint32_t c = 0;
-      for (uint32_t q = tid; q < E; q += kHubThreads) c += sm.it[q] != ~0ull;
-      uint32_t tot;
-      hub_scan(sm, c, tot);
-      nk = tot;
     }
-    uint32_t ntiles = 0;
-    for (uint32_t base = 0; base < nk; base += kHubThreads) {
-      const uint32_t i = base + tid;
-      const unsigned long long x = i < nk ? sm.it[i] : ~0ull;
-      const unsigned long long xp = i > 0 && i < nk ? sm.it[i - 1] : ~0ull;
-      const bool start = i < nk && (i == 0 || (x >> 40) != (xp >> 40));
-      uint32_t tot;
-      const uint32_t pos = hub_scan(sm, start ? 1u : 0u, tot);
-      const uint32_t t = ntiles + pos + (start ? 1u : 0u) - 1u;  // tile of item i
-      if (start) sm.ts[ntiles + pos] = uint16_t(i);
-      if (i < nk && out.etile) {
-        const bool first_row = start || ((x >> 36) & 15u) != ((xp >> 36) & 15u);
-        out.etile[E0 + ((x >> 16) & 0xffffu)] = t | (first_row ? 0u : kDupEntry);
-      }
-      ntiles += tot;
-    }
-    if (tid == 0) sm.ts[ntiles] = uint16_t(nk);
-    if (tid == 0) sm.bad = general_call(out, ntiles, general_seen(out)) ? 1u : 0u;
     __syncthreads();
-    const bool lite = sm.bad != 0;
-    // threads emit tiles t = tid, tid + 256, ...; chunk bases by a block scan
-    uint32_t runA = 1u + uint32_t(E0), runB = 1u + uint32_t(E0);
-    for (uint32_t t0 = 0; t0 < ntiles; t0 += kHubThreads) {
-      const uint32_t t = t0 + tid;
-      uint32_t rm[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-      uint32_t lmA = 0, lmB = 0, a = 0, b = 0, J = 0;
-      if (t < ntiles) {
-        a = sm.ts[t];
-        b = sm.ts[t + 1];
-        J = uint32_t(sm.it[a] >> 40);
-        for (uint32_t i = a; i < b; ++i) {
-          const unsigned long long x = sm.it[i];
-          const int r = int(x >> 36) & 15, cc = int(x >> 32) & 15;
-#pragma unroll
-          for (int g = 0; g < 8; ++g)
-            if (g == (r & 7)) rm[g] |= 1u << (cc + 16 * (r >> 3));
-          int L, h16;
-          slot_lane(kRoleA, r, cc, L, h16);
-          lmA |= 1u << L;
-          slot_lane(kRoleB, r, cc, L, h16);
-          lmB |= 1u << L;
-        }
-      }
-      const uint32_t nA = (roles & 1) && !lite ? __popc(lmA) : 0u, nB = (roles & 2) && !lite ? __popc(lmB) : 0u;
-      uint32_t totA, totB;
-      const uint32_t pA = hub_scan(sm, nA, totA);
-      const uint32_t pB = hub_scan(sm, nB, totB);
-      const uint32_t cbA = runA + pA, cbB = runB + pB;
-      runA += totA;
-      runB += totB;
-      if (t < ntiles) {
-        uint32_t colocc = 0, rowocc = 0;
-#pragma unroll
-        for (int g = 0; g < 8; ++g) {
-          colocc |= rm[g] | (rm[g] >> 16);
-          rowocc |= ((rm[g] & 0xffffu) != 0u ? 1u << g : 0u) | ((rm[g] >> 16) != 0u ? 1u << (g + 8) : 0u);
-        }
-        const uint32_t occ = (colocc & 0xffffu) | (rowocc << 16);
+    // (4) the tile records: tile t = the t-th set bit of the bitmap
+    for (uint32_t w = tid; w < kHubWords; w += kHubThreads) {
+      uint32_t word = sm.bits[w], t = sm.wpre[w];
+      for (; word; word &= word - 1u, ++t) {
+        const uint32_t J = jlo + w * 32u + uint32_t(__ffs(word) - 1);
+        const uint32_t o = sm.occ[t];
         mark_column(out, J);
-        if (lite) {
 #pragma unroll
-          for (int role = 0; role < 2; ++role)
-            if (roles & (1 << role)) out.rec[role][E0 + t] = make_uint4(0u, 0u, occ, J);
-        } else {
-          uint4* dst = reinterpret_cast<uint4*>(out.rm2 + size_t(E0 + t) * 8);
-          dst[0] = make_uint4(rm[0], rm[1], rm[2], rm[3]);
-          dst[1] = make_uint4(rm[4], rm[5], rm[6], rm[7]);
-#pragma unroll
-          for (int role = 0; role < 2; ++role) {
-            if (!(roles & (1 << role))) continue;
-            const uint32_t lm = role == kRoleA ? lmA : lmB, cb = role == kRoleA ? cbA : cbB;
-            out.rec[role][E0 + t] = make_uint4(lm, cb, occ, J);
-            uint32_t n = 0;
-            for (uint32_t m = lm; m; m &= m - 1u, ++n) {  // present lanes, ascending
-              const int Lw = __ffs(m) - 1;
-              uint32_t w[4] = {0, 0, 0, 0};
-              for (uint32_t i = a; i < b; ++i) {
-                const unsigned long long x = sm.it[i];
-                int L, h16;
-                slot_lane(role, int(x >> 36) & 15, int(x >> 32) & 15, L, h16);
-                if (L != Lw) continue;
-                const uint32_t hv = uint32_t(x & 0xffffu) << (16 * (h16 & 1));
-#pragma unroll
-                for (int q = 0; q < 4; ++q)
-                  if (q == (h16 >> 1)) w[q] |= hv;
-              }
-              out.chunk[role][cb + n] = make_uint4(w[0], w[1], w[2], w[3]);
-            }
-          }
-        }
+        for (int role = 0; role < 2; ++role)
+          if (roles & (1 << role)) out.rec[role][E0 + t] = make_uint4(0u, 0u, o, J);
       }
     }
     const unsigned e_or = __reduce_or_sync(kFull, err);

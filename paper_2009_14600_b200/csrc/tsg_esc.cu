@@ -1116,6 +1116,7 @@ __global__ void esc_njt_kernel(int64_t rows, const int64_t* __restrict__ rp, con
 // others test B's row occupancies.  Warp per 32 A tiles.
 __global__ void __launch_bounds__(256) esc_pairstats_kernel(TileMat A, TileMat B, uint32_t tA,
                                                            const uint32_t* __restrict__ njt,
+                                                           const int32_t* __restrict__ colB,
                                                            unsigned long long* __restrict__ out) {
   const int lane = threadIdx.x & 31;
   const uint32_t a0 = (blockIdx.x * 8 + (threadIdx.x >> 5)) * 32;
@@ -1136,14 +1137,36 @@ __global__ void __launch_bounds__(256) esc_pairstats_kernel(TileMat A, TileMat B
       multi = co != 0;
     }
   }
-  for (unsigned m = __ballot_sync(kFull, multi); m; m &= m - 1) {
-    const int src = __ffs(m) - 1;
-    const uint32_t k = __shfl_sync(kFull, K, src), c = __shfl_sync(kFull, co, src);
-    const uint32_t b0 = __ldg(B.trp + k), b1 = __ldg(B.trp + k + 1);
+  // A tile with several occupied columns kk: the B tiles it passes are the
+  // union over kk of the tiles B's CSR row 16 K + kk touches (B tile (K, J)
+  // has row kk occupied iff that row keeps an entry in tile column J).  A tile
+  // of row kk_i (its first kept entry there) counts unless an earlier row kk_j
+  // (j < i) keeps an entry in the same tile column (binary search by column).
+  if (multi) {
     uint32_t n = 0;
-    for (uint32_t b = b0 + lane; b < b1; b += 32) n += ((__ldg(&B.tco[b].y) >> 16) & c) != 0u;
-    n = __reduce_add_sync(kFull, n);
-    if (lane == src) filt += n;
+    for (uint32_t ci = co; ci; ci &= ci - 1u) {
+      const int64_t row = int64_t(K) * 16 + (__ffs(ci) - 1);
+      if (row >= B.rows) break;
+      const uint32_t e0 = uint32_t(__ldg(B.csr_rp + row)), e1 = uint32_t(__ldg(B.csr_rp + row + 1));
+      for (uint32_t e = e0; e < e1; ++e) {
+        const uint32_t et = __ldg(B.etile + e);
+        if (et == kNoTile || (et & kDupEntry)) continue;
+        const uint32_t c16 = uint32_t(__ldg(colB + e)) & ~15u;  // the tile's first column
+        bool seen = false;
+        for (uint32_t cj = co & ((ci & (0u - ci)) - 1u); cj && !seen; cj &= cj - 1u) {  // the earlier rows
+          const int64_t rj = int64_t(K) * 16 + (__ffs(cj) - 1);
+          const uint32_t q1 = uint32_t(__ldg(B.csr_rp + rj + 1));
+          for (uint32_t q = lower_col(colB, uint32_t(__ldg(B.csr_rp + rj)), q1, c16);
+               q < q1 && uint32_t(__ldg(colB + q)) < c16 + 16u; ++q)
+            if (__ldg(B.etile + q) != kNoTile) {
+              seen = true;
+              break;
+            }
+        }
+        n += seen ? 0u : 1u;
+      }
+    }
+    filt += n;
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
@@ -1276,10 +1299,10 @@ void launch_esc_copy(const EscArgs& g, const int64_t* row_ptr, int32_t* col, flo
   esc_copy_kernel<<<148 * 16, 256, 0, st>>>(g.nrec, g.piece_top, g.pool_cap, g.pieces, g.stage, row_ptr, col, val);
 }
 
-void launch_esc_pairstats(const TileMat& A, const TileMat& B, uint64_t tA, uint32_t* njt,
+void launch_esc_pairstats(const TileMat& A, const TileMat& B, const int32_t* colB, uint64_t tA, uint32_t* njt,
                           unsigned long long* out, cudaStream_t st) {
   if (B.rows > 0) esc_njt_kernel<<<2368, 256, 0, st>>>(B.rows, B.csr_rp, B.etile, njt);
-  if (tA > 0) esc_pairstats_kernel<<<unsigned((tA + 255) / 256), 256, 0, st>>>(A, B, uint32_t(tA), njt, out);
+  if (tA > 0) esc_pairstats_kernel<<<unsigned((tA + 255) / 256), 256, 0, st>>>(A, B, uint32_t(tA), njt, colB, out);
 }
 
 void launch_tiles_rowcount(const TileMat& A, int64_t* rowcnt, cudaStream_t st) {

@@ -18,3 +18,17 @@ def test_cpp_shim_acceptance():
     print(r.stdout)
     assert r.returncode == 0, r.stdout + r.stderr
     assert r.stdout.count("PASS") >= 9
+
+
+def test_cpp_reference_call_sites():
+    """The reference's CLI and test call patterns (tilemul.cpp cmd_square /
+    cmd_bench, test_kernels.cpp compact-vs-oracle) compile and pass against
+    tilemul_gpu.hpp through `namespace tilemul = tilemul_gpu`."""
+    exe = os.path.join(ROOT, "tests", "cpp", "ref_call_sites")
+    if not os.path.exists(exe):
+        import __graft_entry__
+        __graft_entry__.build()
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
+    print(r.stdout)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert r.stdout.count("PASS") == 3
