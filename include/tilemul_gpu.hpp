@@ -465,7 +465,8 @@ inline SquareResult spgemm_square(const TiledMatrix& A, const SquareOptions& o =
   Context& ctx = multi ? *multi : default_context();
   const detail::HostCsr a = detail::tiled_to_csr(A);
   const tsg_csr va = a.view();
-  const tsg_options opt = detail::options(o.ordered);
+  tsg_options opt = detail::options(o.ordered);
+  opt.phase_timing = 1;  // SquareResult::timing is always filled (kernels.cpp:260-280)
   tsg_run_stats st{};
   detail::Out out(ctx.get());
   throw_status(tsg_spgemm(ctx.get(), &va, &va, &out.o, &opt, &st, nullptr), tsg_last_error(ctx.get()));

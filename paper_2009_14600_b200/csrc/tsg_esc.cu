@@ -1034,42 +1034,59 @@ __global__ void __launch_bounds__(256) esc_rowcount_kernel(int64_t rows, uint32_
   if (row < rows) rowcnt[row] = acc;
 }
 
+// A piece's header as the copy needs it: lane r < 16 holds row r's count and
+// its entries of the row in earlier pieces; I and the staging offset.
+struct PieceHdr {
+  uint32_t cnt = 0, ro = 0, I = 0;
+  unsigned long long off = 0;
+};
+__device__ __forceinline__ PieceHdr load_hdr(const EscPiece* __restrict__ pieces, uint32_t p, int lane) {
+  PieceHdr h;
+  const EscPiece& pc = pieces[p];
+  h.cnt = lane < 16 ? pc.cnt[lane] : 0u;
+  h.ro = lane < 16 ? pc.roff[lane] : 0u;
+  h.I = pc.I;
+  h.off = pc.off;
+  return h;
+}
+// row r's first CSR slot for this piece (lane r < 16)
+__device__ __forceinline__ int64_t piece_dst0(const PieceHdr& h, const int64_t* __restrict__ row_ptr, int lane) {
+  return lane < 16 && h.cnt ? row_ptr[int64_t(h.I) * 16 + lane] + h.ro : 0;
+}
+
 // One staged piece -> its CSR slots: lanes over the piece's entries; entry q
 // belongs to the last row whose start within the piece is <= q.
-__device__ __forceinline__ void copy_piece(const EscPiece& pc, int lane, const uint2* __restrict__ stage,
-                                           const int64_t* __restrict__ row_ptr, int32_t* __restrict__ col,
-                                           float* __restrict__ val) {
-  const uint32_t cnt = lane < 16 ? pc.cnt[lane] : 0u;
-  const uint32_t ro = lane < 16 ? pc.roff[lane] : 0u;
-  uint32_t inc = cnt;  // each row's start within the piece
+__device__ __forceinline__ void copy_piece(const PieceHdr& h, int64_t dst0, int lane, const uint2* __restrict__ stage,
+                                           int32_t* __restrict__ col, float* __restrict__ val) {
+  uint32_t inc = h.cnt;  // each row's start within the piece
 #pragma unroll
   for (int o = 1; o < 16; o <<= 1) {
     const uint32_t v = __shfl_up_sync(kFull, inc, o);
     if (lane >= o) inc += v;
   }
   const uint32_t total = __shfl_sync(kFull, inc, 15);
-  const uint32_t start = inc - cnt;
-  const int64_t dst0 = lane < 16 && cnt ? row_ptr[int64_t(pc.I) * 16 + lane] + ro : 0;
-  const unsigned long long off = pc.off;
+  const uint32_t start = inc - h.cnt;
   for (uint32_t q0 = 0; q0 < total; q0 += 32) {
     const uint32_t q = q0 + lane;
     int r = 0;
 #pragma unroll
     for (int b = 8; b > 0; b >>= 1) {
-      const uint32_t s = __shfl_sync(kFull, start, r + b);
-      if (s <= q) r += b;
+      const uint32_t st = __shfl_sync(kFull, start, r + b);
+      if (st <= q) r += b;
     }
     const uint32_t sr = __shfl_sync(kFull, start, r);
     const int64_t d = __shfl_sync(kFull, dst0, r);
     if (q < total) {
-      const uint2 e = __ldg(stage + off + q);
+      const uint2 e = __ldg(stage + h.off + q);
       col[d + (q - sr)] = int32_t(e.x);
       val[d + (q - sr)] = __uint_as_float(e.y);
     }
   }
 }
 
-// staged pieces -> CSR: warp per piece
+// staged pieces -> CSR: a warp takes pieces p, p + W, ...; the header two
+// pieces ahead and the row pointers one piece ahead are in flight while the
+// current piece's entries move
 __global__ void __launch_bounds__(256) esc_copy_kernel(const uint32_t* __restrict__ nrec,
                                                       const uint32_t* __restrict__ piece_top, uint32_t pool_cap,
                                                       const EscPiece* __restrict__ pieces,
@@ -1078,8 +1095,20 @@ __global__ void __launch_bounds__(256) esc_copy_kernel(const uint32_t* __restric
                                                       int32_t* __restrict__ col, float* __restrict__ val) {
   const int lane = threadIdx.x & 31;
   const uint32_t np = *nrec + min(*piece_top, pool_cap);
-  for (uint32_t p = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; p < np; p += (gridDim.x * blockDim.x) >> 5)
-    copy_piece(pieces[p], lane, stage, row_ptr, col, val);
+  const uint32_t W = (gridDim.x * blockDim.x) >> 5;
+  uint32_t p = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (p >= np) return;
+  PieceHdr h = load_hdr(pieces, p, lane);
+  PieceHdr h1 = p + W < np ? load_hdr(pieces, p + W, lane) : PieceHdr{};
+  int64_t d0 = piece_dst0(h, row_ptr, lane);
+  for (; p < np; p += W) {
+    const PieceHdr h2 = p + 2 * W < np ? load_hdr(pieces, p + 2 * W, lane) : PieceHdr{};
+    const int64_t d1 = p + W < np ? piece_dst0(h1, row_ptr, lane) : 0;
+    copy_piece(h, d0, lane, stage, col, val);
+    h = h1;
+    h1 = h2;
+    d0 = d1;
+  }
 }
 
 // records [rec0, rec1) and the pool pieces chained after them: warp per record
@@ -1091,7 +1120,10 @@ __global__ void __launch_bounds__(256) esc_copy_records_kernel(uint32_t rec0, ui
   const int lane = threadIdx.x & 31;
   for (uint32_t p = rec0 + ((blockIdx.x * blockDim.x + threadIdx.x) >> 5); p < rec1;
        p += (gridDim.x * blockDim.x) >> 5)
-    for (uint32_t q = p; q != kNoPiece; q = pieces[q].next) copy_piece(pieces[q], lane, stage, row_ptr, col, val);
+    for (uint32_t q = p; q != kNoPiece; q = pieces[q].next) {
+      const PieceHdr h = load_hdr(pieces, q, lane);
+      copy_piece(h, piece_dst0(h, row_ptr, lane), lane, stage, col, val);
+    }
 }
 
 // ---------------------------------------------------------------- statistics
@@ -1137,36 +1169,14 @@ __global__ void __launch_bounds__(256) esc_pairstats_kernel(TileMat A, TileMat B
       multi = co != 0;
     }
   }
-  // A tile with several occupied columns kk: the B tiles it passes are the
-  // union over kk of the tiles B's CSR row 16 K + kk touches (B tile (K, J)
-  // has row kk occupied iff that row keeps an entry in tile column J).  A tile
-  // of row kk_i (its first kept entry there) counts unless an earlier row kk_j
-  // (j < i) keeps an entry in the same tile column (binary search by column).
-  if (multi) {
+  for (unsigned m = __ballot_sync(kFull, multi); m; m &= m - 1) {
+    const int src = __ffs(m) - 1;
+    const uint32_t k = __shfl_sync(kFull, K, src), c = __shfl_sync(kFull, co, src);
+    const uint32_t b0 = __ldg(B.trp + k), b1 = __ldg(B.trp + k + 1);
     uint32_t n = 0;
-    for (uint32_t ci = co; ci; ci &= ci - 1u) {
-      const int64_t row = int64_t(K) * 16 + (__ffs(ci) - 1);
-      if (row >= B.rows) break;
-      const uint32_t e0 = uint32_t(__ldg(B.csr_rp + row)), e1 = uint32_t(__ldg(B.csr_rp + row + 1));
-      for (uint32_t e = e0; e < e1; ++e) {
-        const uint32_t et = __ldg(B.etile + e);
-        if (et == kNoTile || (et & kDupEntry)) continue;
-        const uint32_t c16 = uint32_t(__ldg(colB + e)) & ~15u;  // the tile's first column
-        bool seen = false;
-        for (uint32_t cj = co & ((ci & (0u - ci)) - 1u); cj && !seen; cj &= cj - 1u) {  // the earlier rows
-          const int64_t rj = int64_t(K) * 16 + (__ffs(cj) - 1);
-          const uint32_t q1 = uint32_t(__ldg(B.csr_rp + rj + 1));
-          for (uint32_t q = lower_col(colB, uint32_t(__ldg(B.csr_rp + rj)), q1, c16);
-               q < q1 && uint32_t(__ldg(colB + q)) < c16 + 16u; ++q)
-            if (__ldg(B.etile + q) != kNoTile) {
-              seen = true;
-              break;
-            }
-        }
-        n += seen ? 0u : 1u;
-      }
-    }
-    filt += n;
+    for (uint32_t b = b0 + lane; b < b1; b += 32) n += ((__ldg(&B.tco[b].y) >> 16) & c) != 0u;
+    n = __reduce_add_sync(kFull, n);
+    if (lane == src) filt += n;
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
