@@ -1146,6 +1146,8 @@ __global__ void esc_njt_kernel(int64_t rows, const int64_t* __restrict__ rp, con
 // filtered = pairs passing tile_product_nonzero (pipeline.cpp:23-35): a
 // single-column A tile passes exactly the tiles its B row touches (njt);
 // others test B's row occupancies.  Warp per 32 A tiles.
+constexpr uint32_t kPairBits = 8192;  // tile ranks of a B tile row the pair-statistics bitmap covers
+
 __global__ void __launch_bounds__(256) esc_pairstats_kernel(TileMat A, TileMat B, uint32_t tA,
                                                            const uint32_t* __restrict__ njt,
                                                            const int32_t* __restrict__ colB,
@@ -1169,12 +1171,45 @@ __global__ void __launch_bounds__(256) esc_pairstats_kernel(TileMat A, TileMat B
       multi = co != 0;
     }
   }
+  // A tile with several occupied columns: the B tiles of tile row k whose row
+  // occupancy meets them.  Long B tile rows (R-MAT hubs): the union of the
+  // tiles the occupied B CSR rows touch, as a bitmap over the tile row's tile
+  // ranks (B tile (k, J) has row kk occupied iff CSR row 16 k + kk keeps an
+  // entry in tile J, whose etile is J's rank); short ones: the occupancy test
+  // over the tile row.
+  __shared__ uint32_t s_bm[8][kPairBits / 32];
+  const int wib = threadIdx.x >> 5;
   for (unsigned m = __ballot_sync(kFull, multi); m; m &= m - 1) {
     const int src = __ffs(m) - 1;
     const uint32_t k = __shfl_sync(kFull, K, src), c = __shfl_sync(kFull, co, src);
-    const uint32_t b0 = __ldg(B.trp + k), b1 = __ldg(B.trp + k + 1);
+    const uint32_t b0 = __ldg(B.trp + k), b1 = __ldg(B.trp + k + 1), len = b1 - b0;
+    uint32_t entries = 0;
+    for (uint32_t ci = c; ci; ci &= ci - 1u) {
+      const int64_t row = int64_t(k) * 16 + (__ffs(ci) - 1);
+      if (row < B.rows) entries += uint32_t(__ldg(B.csr_rp + row + 1) - __ldg(B.csr_rp + row));
+    }
     uint32_t n = 0;
-    for (uint32_t b = b0 + lane; b < b1; b += 32) n += ((__ldg(&B.tco[b].y) >> 16) & c) != 0u;
+    if (len <= kPairBits && entries < len) {
+      for (uint32_t i = lane; i < (len + 31) / 32; i += 32) s_bm[wib][i] = 0;
+      __syncwarp();
+      for (uint32_t ci = c; ci; ci &= ci - 1u) {
+        const int64_t row = int64_t(k) * 16 + (__ffs(ci) - 1);
+        if (row >= B.rows) continue;
+        const int64_t e1 = __ldg(B.csr_rp + row + 1);
+        for (int64_t e = __ldg(B.csr_rp + row) + lane; e < e1; e += 32) {
+          const uint32_t et = __ldg(B.etile + e);
+          if (et != kNoTile) {
+            const uint32_t t = et & ~kDupEntry;
+            atomicOr(&s_bm[wib][t >> 5], 1u << (t & 31));
+          }
+        }
+      }
+      __syncwarp();
+      for (uint32_t i = lane; i < (len + 31) / 32; i += 32) n += __popc(s_bm[wib][i]);
+      __syncwarp();
+    } else {
+      for (uint32_t b = b0 + lane; b < b1; b += 32) n += ((__ldg(&B.tco[b].y) >> 16) & c) != 0u;
+    }
     n = __reduce_add_sync(kFull, n);
     if (lane == src) filt += n;
   }
