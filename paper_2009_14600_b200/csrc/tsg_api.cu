@@ -123,15 +123,6 @@ struct Scratch {
     bytes[cat] += n * sizeof(T);
     return static_cast<T*>(p);
   }
-  // hand an allocation over to the caller (it is no longer freed at scope end)
-  void release(const void* p) {
-    for (auto& q : ptrs)
-      if (q == p) {
-        q = ptrs.back();
-        ptrs.pop_back();
-        return;
-      }
-  }
 };
 // RAII role switch for a block of allocations
 struct MemRole {
@@ -662,30 +653,17 @@ struct Call {
     const bool tc05 = opt.mode == TSG_MODE_TENSOR && tuning_variant("TSG_TC05", 0) == 1;
     unsigned* fallback = sc.alloc<unsigned>(1);
     TSG_CUDA(cudaMemsetAsync(fallback, 0, sizeof(unsigned), s));
-    // the pass writes the CSR itself (look-back row offsets, FusedOut): no
-    // row scan, no copy pass; col / val hold the staging capacity
-    const bool fused = !tc05 && TA.tile_rows > 0 && tuning_variant("TSG_FUSED_CSR", 1) == 1;
-    FusedOut fo;
-    if (fused) {
-      fo.state = sc.alloc<unsigned long long>(TA.tile_rows);
-      TSG_CUDA(cudaMemsetAsync(fo.state, 0, TA.tile_rows * sizeof(unsigned long long), s));
-      MemRole role_out(sc, kMemOutput);
-      fo.row_ptr = d_rp;
-      fo.col = sc.alloc<int32_t>(cap_slots);
-      fo.val = sc.alloc<float>(cap_slots);
-      fo.err_flag = err_flag;
-    }
     if (timing) TSG_CUDA(cudaEventRecord(ctx->kev[0], s));
     if (tc05)
       TSG_CUDA(launch_tc05_panel(TA, *TB, rows, row_stage, cap_slots, stage, rowcnt, counted_d, tot_d + 3, tot_d, dscal,
                                  work, fallback, ctx->device, s));
     else
       TSG_CUDA(launch_panel_numeric(TA, *TB, rows, row_stage, cap_slots, stage, rowcnt, counted_d, tot_d + 3, tot_d,
-                                    opt.mode, 0, TA.tile_rows, s, nullptr, dscal, work, 1, fused ? &fo : nullptr));
+                                    opt.mode, 0, TA.tile_rows, s, nullptr, dscal, work, 1));
     check_launch(ctx);
     if (timing) TSG_CUDA(cudaEventRecord(ctx->kev[1], s));
     record(ctx, timing, 5);
-    if (!fused) exclusive_sum(ctx, sc, rowcnt, d_rp, uint64_t(rows) + 1);
+    exclusive_sum(ctx, sc, rowcnt, d_rp, uint64_t(rows) + 1);
     ScalarGather g;
     const void* ps[11] = {dscal, dscal + 1, ntA_dev, ntB_dev, counted_d, d_rp + rows, tot_d, tot_d + 1, tot_d + 2,
                           tot_d + 3, fallback};
@@ -728,19 +706,6 @@ struct Call {
       raw = t[2];
     } else if (uint64_t(nnzC) >= (uint64_t(1) << 32)) {
       throw Fail{TSG_ERR_OTHER, "output beyond 2^32 elements needs row-panel batching"};
-    } else if (fused) {  // the CSR is complete: keep the pass's col / val as the output
-      d_col = fo.col;
-      d_val = fo.val;
-      sc.release(d_col);
-      sc.release(d_val);
-      owner->p[1] = d_col;
-      owner->p[2] = d_val;
-      if (timing) {
-        TSG_CUDA(cudaEventRecord(ctx->kev[2], s));
-        TSG_CUDA(cudaEventRecord(ctx->kev[3], s));
-      }
-      record(ctx, timing, 6);
-      return true;
     }
     alloc_out();
     if (timing) TSG_CUDA(cudaEventRecord(ctx->kev[2], s));

@@ -74,22 +74,11 @@ struct TileEmit {
 // `need`: device u64 total of the staging bound (the pass returns at once when
 // it exceeds stage_cap); `stats`: when non-null, {filtered pairs, segments,
 // raw pairs} are accumulated there (the element-bound flow has no count pass)
-// Fused CSR output (device output): the pass writes row_ptr / col / val
-// itself, each tile row's offset from a decoupled look-back over `state`
-// (tile_rows u64, zeroed); col / val hold the staging capacity.
-struct FusedOut {
-  unsigned long long* state = nullptr;
-  int64_t* row_ptr = nullptr;
-  int32_t* col = nullptr;
-  float* val = nullptr;
-  unsigned* err_flag = nullptr;
-};
 cudaError_t launch_panel_numeric(const TileMat& A, const TileMat& B, int64_t rows, const uint32_t* row_stage,
                                  uint64_t stage_cap, uint2* stage, int64_t* rowcnt, unsigned long long* counted,
                                  const unsigned long long* need, unsigned long long* stats, int mode, uint32_t I0,
                                  uint32_t I1, cudaStream_t st, const TileEmit* emit = nullptr,
-                                 const unsigned* gate = nullptr, unsigned* work = nullptr, int nl = 1,
-                                 const FusedOut* fused = nullptr);
+                                 const unsigned* gate = nullptr, unsigned* work = nullptr, int nl = 1);
 // The same light-row pass on tcgen05 (tsg_tc05.cu; TENSOR mode, tile rows of
 // <= 32 A tiles): persistent CTAs over panels of 8 tile rows, M = 128 MMAs
 // with TMEM accumulators.  Sets *fallback when a panel gathers more B tiles

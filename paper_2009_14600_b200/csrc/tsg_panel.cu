@@ -254,81 +254,6 @@ __device__ __forceinline__ void emit_tile(const float (&acc)[2][4], uint32_t J, 
   e_chunks += __popc(lm);
 }
 
-// Fused CSR output (device output, speculative light pass): tile rows are
-// taken in increasing order (the persistent warps' counter, or one resident
-// wave), so when tile row I is done its CSR offset comes from a decoupled
-// look-back over the rows before it -- state[I] = flag << 62 | value, flag 1:
-// the row's own count (aggregate), flag 2: the inclusive prefix -- and the
-// warp moves its just-staged (L2-resident) entries straight into the CSR and
-// writes its row pointers.  No row scan and no separate copy pass.
-// cg / cg8: this lane group's realised counts of rows g and g + 8.
-__device__ __forceinline__ void fused_csr(const FusedOut& fo, uint32_t I, int64_t rows, int lane, uint32_t cg,
-                                          uint32_t cg8, const uint32_t* __restrict__ row_stage,
-                                          const uint2* __restrict__ stage) {
-  constexpr unsigned long long kAgg = 1ull << 62, kIncl = 2ull << 62, kVal = (1ull << 62) - 1;
-  // lane r < 16: row r's count (rows g live in lane 4g, rows g + 8 in lane 4g as cg8)
-  const uint32_t c_lo = __shfl_sync(kFull, cg, (lane & 7) * 4), c_hi = __shfl_sync(kFull, cg8, (lane & 7) * 4);
-  const int64_t r0 = int64_t(I) * 16;
-  const int64_t row = r0 + (lane & 15);
-  const uint32_t cnt = lane < 16 && row < rows ? (lane < 8 ? c_lo : c_hi) : 0u;
-  uint32_t inc = cnt;  // row offsets within the tile row
-#pragma unroll
-  for (int o = 1; o < 16; o <<= 1) {
-    const uint32_t v = __shfl_up_sync(kFull, inc, o);
-    if (lane >= o) inc += v;
-  }
-  const uint32_t agg = __shfl_sync(kFull, inc, 15);
-  // look-back: lane 0 publishes the aggregate, then sums predecessors 32 at a time
-  unsigned long long excl = 0;
-  volatile unsigned long long* st = fo.state;
-  if (lane == 0) st[I] = (I == 0 ? kIncl : kAgg) | agg;
-  if (I > 0) {
-    int64_t j = int64_t(I) - 1;
-    while (true) {
-      const int64_t k = j - lane;
-      unsigned long long v = k >= 0 ? st[k] : kIncl;
-      // wait until every lane's predecessor has published something
-      while (__any_sync(kFull, (v >> 62) == 0)) {
-        if ((v >> 62) == 0) v = st[k];
-      }
-      const unsigned incl = __ballot_sync(kFull, (v >> 62) == 2);
-      const int stop = incl ? __ffs(incl) - 1 : 32;  // the nearest inclusive prefix
-      unsigned long long x = lane <= stop ? (v & kVal) : 0ull;
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(kFull, x, o);
-      excl += x;
-      if (incl) break;
-      j -= 32;
-    }
-    if (lane == 0) st[I] = kIncl | (excl + agg);
-  }
-  const int64_t base = int64_t(excl);
-  if (lane < 16 && row < rows) fo.row_ptr[row] = base + (inc - cnt);
-  if (lane == 0 && int64_t(I + 1) * 16 >= rows) fo.row_ptr[rows] = base + agg;
-  // staging rows -> CSR: lanes over the tile row's entries (the 16 rows are consecutive)
-  const uint32_t off = lane < 16 ? inc - cnt : agg;
-  const uint32_t src0 = lane < 16 && row < rows ? __ldg(row_stage + row) : 0u;
-  bool bad = false;
-  for (uint32_t q0 = 0; q0 < agg; q0 += 32) {
-    const uint32_t q = q0 + lane;
-    int r = 0;  // last row whose offset is <= q
-#pragma unroll
-    for (int b = 8; b > 0; b >>= 1) {
-      const uint32_t v = __shfl_sync(kFull, off, r + b);
-      if (v <= q) r += b;
-    }
-    const uint32_t o = __shfl_sync(kFull, off, r), sr = __shfl_sync(kFull, src0, r);
-    if (q < agg) {
-      const uint2 e = stage[sr + (q - o)];
-      const float x = __uint_as_float(e.x);
-      bad |= !isfinite(x);
-      fo.col[base + q] = int32_t(e.y);
-      fo.val[base + q] = x;
-    }
-  }
-  if (__any_sync(kFull, bad) && lane == 0) atomicOr(fo.err_flag, unsigned(kErrPrecision));
-}
-
 template <bool kOrdered, int kMinBlocks, bool kEmit, int NL>
 __global__ void __launch_bounds__(256, kMinBlocks) panel_numeric_kernel(TileMat A, TileMat B, int64_t rows,
                                                               const uint32_t* __restrict__ row_stage,
@@ -339,7 +264,7 @@ __global__ void __launch_bounds__(256, kMinBlocks) panel_numeric_kernel(TileMat 
                                                               unsigned long long* __restrict__ stats,
                                                               uint32_t I0, uint32_t I1, TileEmit em,
                                                               const unsigned* __restrict__ gate,
-                                                              unsigned* __restrict__ work, FusedOut fo) {
+                                                              unsigned* __restrict__ work) {
   // the run's pairs: {A lane mask, A chunk base, B lane mask, B chunk base}
   // (one list, TENSOR: {A tile of the row, -, B meta} with the A chunk index
   // of every lane precomputed per tile row in s_aidx)
@@ -522,8 +447,6 @@ __global__ void __launch_bounds__(256, kMinBlocks) panel_numeric_kernel(TileMat 
   }
   if (kEmit) {
     if (lane == 0) em.rtiles[I] = e_tiles;
-  } else if (fo.state) {
-    fused_csr(fo, I, rows, lane, wg - wg0, wg8 - wg80, row_stage, stage);
   } else if (L.t == 0) {
     if (rg < rows) rowcnt[rg] = int64_t(wg - wg0);
     if (rg8 < rows) rowcnt[rg8] = int64_t(wg8 - wg80);
@@ -601,7 +524,7 @@ void launch_elem_bound(const CsrView& A, const int64_t* rpB, int64_t bcols, uint
 namespace {
 using PanelK = void (*)(TileMat, TileMat, int64_t, const uint32_t*, uint64_t, uint2*, int64_t*, unsigned long long*,
                         const unsigned long long*, unsigned long long*, uint32_t, uint32_t, TileEmit, const unsigned*,
-                        unsigned*, FusedOut);
+                        unsigned*);
 template <int NL>
 PanelK pick_panel(int mode, bool emit) {
   constexpr int kB = NL == 1 ? 4 : 3;  // resident blocks per SM (registers of the NL merge lists)
@@ -614,7 +537,7 @@ cudaError_t launch_panel_numeric(const TileMat& A, const TileMat& B, int64_t row
                                  uint64_t stage_cap, uint2* stage, int64_t* rowcnt, unsigned long long* counted,
                                  const unsigned long long* need, unsigned long long* stats, int mode, uint32_t I0,
                                  uint32_t I1, cudaStream_t st, const TileEmit* emit, const unsigned* gate,
-                                 unsigned* work, int nl, const FusedOut* fused) {
+                                 unsigned* work, int nl) {
   unsigned blocks = (I1 - I0 + 7) / 8;
   if (I1 <= I0) return cudaSuccess;
   const TileEmit em = emit ? *emit : TileEmit{};
@@ -648,9 +571,8 @@ cudaError_t launch_panel_numeric(const TileMat& A, const TileMat& B, int64_t row
       if (e != cudaSuccess) return e;
     }
   }
-  const FusedOut fo = fused ? *fused : FusedOut{};
   k<<<blocks, 256, 0, st>>>(A, B, rows, row_stage, stage_cap, stage, rowcnt, counted, need, stats, I0, I1, em, gate,
-                            work, fo);
+                            work);
   return cudaSuccess;
 }
 
