@@ -351,7 +351,7 @@ def run_ours(args):
     if world == 1 and prof_name:
         kk = json.loads((Path(ROOT) / prof_name).read_text())["kernels"]
         tot = [k["dram_read_bytes"] + k["dram_write_bytes"] for name, k in kk.items()
-               if name.split("<")[0].split("#")[0] == kname]
+               if name.split("<")[0].split("#")[0].split("::")[-1] == kname]
         traffic = int(sum(tot) / len(tot)) if tot else None
 
     # ---- e2e: host CSR in (pinned), host CSR out, through the public API

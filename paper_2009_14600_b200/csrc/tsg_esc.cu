@@ -92,6 +92,20 @@ __device__ __forceinline__ uint32_t phys(uint32_t g) {
   return t * IPT + (((q + rot) & (NV - 1)) << 2) + (i & 3u);
 }
 
+// Exclusive prefix (for warp w) and total of the per-warp sums ws[0 .. kWarps):
+// every warp reads them with one lane each and scans in registers (no loop
+// over the warps in every thread).
+__device__ __forceinline__ void warp_sums(const uint32_t* ws, int w, int lane, uint32_t& pre, uint32_t& tot) {
+  uint32_t x = lane < kWarps ? ws[lane] : 0u;
+#pragma unroll
+  for (int o = 1; o < kWarps; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(kFull, x, o);
+    if (lane >= o) x += y;
+  }
+  tot = __shfl_sync(kFull, x, kWarps - 1);
+  pre = w > 0 ? __shfl_sync(kFull, x, w - 1) : 0u;
+}
+
 // exclusive block scan of two u32 (totals in ta, tb)
 __device__ __forceinline__ void block_scan2(EscSmem& sm, uint32_t& a, uint32_t& b, uint32_t& ta, uint32_t& tb) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -109,19 +123,9 @@ __device__ __forceinline__ void block_scan2(EscSmem& sm, uint32_t& a, uint32_t& 
     sm.wsum[kWarps + w] = ib;
   }
   __syncthreads();
-  uint32_t pa = 0, pb = 0;
-  ta = 0;
-  tb = 0;
-#pragma unroll
-  for (int i = 0; i < kWarps; ++i) {
-    const uint32_t x = sm.wsum[i], y = sm.wsum[kWarps + i];
-    if (i < w) {
-      pa += x;
-      pb += y;
-    }
-    ta += x;
-    tb += y;
-  }
+  uint32_t pa, pb;
+  warp_sums(sm.wsum, w, lane, pa, ta);
+  warp_sums(sm.wsum + kWarps, w, lane, pb, tb);
   a = pa + ia - a;
   b = pb + ib - b;
   __syncthreads();
@@ -152,13 +156,9 @@ __device__ __forceinline__ uint32_t digit_scan(EscSmem& sm, const uint32_t (&w8)
   }
   if (lane == 31) sm.wsum[w] = inc;
   __syncthreads();
-  uint32_t run = inc - sum, T = 0;
-#pragma unroll
-  for (int i = 0; i < kWarps; ++i) {
-    const uint32_t y = sm.wsum[i];
-    if (i < w) run += y;
-    T += y;
-  }
+  uint32_t pre, T;
+  warp_sums(sm.wsum, w, lane, pre, T);
+  uint32_t run = inc - sum + pre;
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
     sm.s.ctr[cpad(8 * tid + i)] = run;
@@ -351,6 +351,8 @@ __device__ bool build_table(EscSmem& sm, const EscArgs& g, const Unit& u, uint32
   const int nrow = 16 * int(u.nb);
   const int64_t E0 = sm.rowp[0], E1 = sm.rowp[nrow];
   const bool full = lo == 0 && int64_t(hi) >= g.colsB;
+  int bsearch0 = 128;  // the row search's first step: below the unit's row count
+  while (bsearch0 > 1 && bsearch0 >= nrow) bsearch0 >>= 1;
   P = 0;
   ne = 0;
   for (int64_t e0 = E0; e0 < E1; e0 += 2 * kNT) {
@@ -391,7 +393,7 @@ __device__ bool build_table(EscSmem& sm, const EscArgs& g, const Unit& u, uint32
       len[x] = s0[2 * x + 1] > blo[x] ? s0[2 * x + 1] - blo[x] : 0u;
       br[x] = 0;
       if (len[x])
-        for (int b = 128; b > 0; b >>= 1)  // row within the unit: last rowp <= e
+        for (int b = bsearch0; b > 0; b >>= 1)  // row within the unit: last rowp <= e
           if (int(br[x]) + b < nrow && sm.rowp[br[x] + b] <= e[x]) br[x] += b;
     }
     const uint32_t fa = len[0] > 0, fb = len[1] > 0;

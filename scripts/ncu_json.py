@@ -32,6 +32,7 @@ res = {"source": source, "kernels": {}}
 for v in rows[2:]:
     name = v[h.index("Kernel Name")]
     name = name.split("(")[0].replace("void ", "").replace("tsg::<unnamed>::", "").replace("<unnamed>::", "").strip()
+    name = name.replace("unnamed>::", "").replace("tsg::", "")
     if name.startswith("cub::"):
         name = name.split("<")[0]
     d = {}
