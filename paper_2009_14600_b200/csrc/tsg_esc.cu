@@ -1068,20 +1068,30 @@ __device__ __forceinline__ void copy_piece(const PieceHdr& h, int64_t dst0, int 
   }
   const uint32_t total = __shfl_sync(kFull, inc, 15);
   const uint32_t start = inc - h.cnt;
-  for (uint32_t q0 = 0; q0 < total; q0 += 32) {
-    const uint32_t q = q0 + lane;
-    int r = 0;
+  // four entries per lane in flight: all loads first, then the row lookups and stores
+  for (uint32_t q0 = 0; q0 < total; q0 += 128) {
+    uint2 e[4];
 #pragma unroll
-    for (int b = 8; b > 0; b >>= 1) {
-      const uint32_t st = __shfl_sync(kFull, start, r + b);
-      if (st <= q) r += b;
+    for (int u = 0; u < 4; ++u) {
+      const uint32_t q = q0 + 32 * u + lane;
+      e[u] = q < total ? __ldg(stage + h.off + q) : make_uint2(0, 0);
     }
-    const uint32_t sr = __shfl_sync(kFull, start, r);
-    const int64_t d = __shfl_sync(kFull, dst0, r);
-    if (q < total) {
-      const uint2 e = __ldg(stage + h.off + q);
-      col[d + (q - sr)] = int32_t(e.x);
-      val[d + (q - sr)] = __uint_as_float(e.y);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const uint32_t q = q0 + 32 * u + lane;
+      if (q0 + 32 * u >= total) break;
+      int r = 0;
+#pragma unroll
+      for (int b = 8; b > 0; b >>= 1) {
+        const uint32_t st = __shfl_sync(kFull, start, r + b);
+        if (st <= q) r += b;
+      }
+      const uint32_t sr = __shfl_sync(kFull, start, r);
+      const int64_t d = __shfl_sync(kFull, dst0, r);
+      if (q < total) {
+        col[d + (q - sr)] = int32_t(e[u].x);
+        val[d + (q - sr)] = __uint_as_float(e[u].y);
+      }
     }
   }
 }
@@ -1150,9 +1160,40 @@ __global__ void esc_njt_kernel(int64_t rows, const int64_t* __restrict__ rp, con
 // others test B's row occupancies.  Warp per 32 A tiles.
 constexpr uint32_t kPairBits = 8192;  // tile ranks of a B tile row the pair-statistics bitmap covers
 
+// Per B tile row k: nx[16 k + x] = its tiles whose row x is occupied, and
+// nx_single[k] = 1 when every tile occupies exactly one row (R-MAT's ~1-entry
+// tiles).  Then an A tile with column occupancy c passes sum_{x in c} nx tiles
+// of that row exactly.  Warp per tile row.
+__global__ void __launch_bounds__(256) esc_brow_bits_kernel(TileMat B, uint32_t* __restrict__ nx,
+                                                           uint8_t* __restrict__ single) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t k = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (k >= B.tile_rows) return;
+  const uint32_t b0 = B.trp[k], b1 = B.trp[k + 1];
+  uint32_t cnt[16];
+#pragma unroll
+  for (int x = 0; x < 16; ++x) cnt[x] = 0;
+  bool one = true;
+  for (uint32_t b = b0 + lane; b < b1; b += 32) {
+    const uint32_t ro = __ldg(&B.tco[b].y) >> 16;
+    one &= __popc(ro) == 1;
+#pragma unroll
+    for (int x = 0; x < 16; ++x) cnt[x] += (ro >> x) & 1u;
+  }
+#pragma unroll
+  for (int x = 0; x < 16; ++x) {
+    const uint32_t t = __reduce_add_sync(kFull, cnt[x]);
+    if (lane == x) nx[size_t(k) * 16 + x] = t;
+  }
+  const bool all = __all_sync(kFull, one);
+  if (lane == 0) single[k] = all ? 1 : 0;
+}
+
 __global__ void __launch_bounds__(256) esc_pairstats_kernel(TileMat A, TileMat B, uint32_t tA,
                                                            const uint32_t* __restrict__ njt,
                                                            const int32_t* __restrict__ colB,
+                                                           const uint32_t* __restrict__ nx,
+                                                           const uint8_t* __restrict__ single,
                                                            unsigned long long* __restrict__ out) {
   const int lane = threadIdx.x & 31;
   const uint32_t a0 = (blockIdx.x * 8 + (threadIdx.x >> 5)) * 32;
@@ -1169,6 +1210,8 @@ __global__ void __launch_bounds__(256) esc_pairstats_kernel(TileMat A, TileMat B
     if (__popc(co) == 1) {
       const int64_t row = int64_t(K) * 16 + (__ffs(co) - 1);
       filt = row < B.rows ? __ldg(njt + row) : 0u;
+    } else if (co != 0 && __ldg(single + K)) {  // every B tile of row K occupies one row
+      for (uint32_t c = co; c; c &= c - 1u) filt += __ldg(nx + size_t(K) * 16 + (__ffs(c) - 1));
     } else {
       multi = co != 0;
     }
@@ -1347,9 +1390,11 @@ void launch_esc_copy(const EscArgs& g, const int64_t* row_ptr, int32_t* col, flo
 }
 
 void launch_esc_pairstats(const TileMat& A, const TileMat& B, const int32_t* colB, uint64_t tA, uint32_t* njt,
-                          unsigned long long* out, cudaStream_t st) {
+                          uint32_t* nx, uint8_t* single, unsigned long long* out, cudaStream_t st) {
   if (B.rows > 0) esc_njt_kernel<<<2368, 256, 0, st>>>(B.rows, B.csr_rp, B.etile, njt);
-  if (tA > 0) esc_pairstats_kernel<<<unsigned((tA + 255) / 256), 256, 0, st>>>(A, B, uint32_t(tA), njt, colB, out);
+  if (B.tile_rows > 0) esc_brow_bits_kernel<<<(B.tile_rows + 7) / 8, 256, 0, st>>>(B, nx, single);
+  if (tA > 0)
+    esc_pairstats_kernel<<<unsigned((tA + 255) / 256), 256, 0, st>>>(A, B, uint32_t(tA), njt, colB, nx, single, out);
 }
 
 void launch_tiles_rowcount(const TileMat& A, int64_t* rowcnt, cudaStream_t st) {

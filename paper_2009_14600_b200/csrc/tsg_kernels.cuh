@@ -156,8 +156,9 @@ void launch_esc_copy(const EscArgs& g, const int64_t* row_ptr, int32_t* col, flo
 // the pieces of output records [rec0, rec1) and their chains (a chunk of tile rows)
 void launch_esc_copy_records(const EscArgs& g, uint32_t rec0, uint32_t rec1, const int64_t* row_ptr, int32_t* col,
                              float* val, cudaStream_t st);
+// njt: B rows + 1; nx: 16 per B tile row; single: one per B tile row (scratch)
 void launch_esc_pairstats(const TileMat& A, const TileMat& B, const int32_t* colB, uint64_t tA, uint32_t* njt,
-                          unsigned long long* out, cudaStream_t st);
+                          uint32_t* nx, uint8_t* single, unsigned long long* out, cudaStream_t st);
 // A given as A-role tiles (a chained stage) -> CSR with binary16 values
 void launch_tiles_rowcount(const TileMat& A, int64_t* rowcnt, cudaStream_t st);
 void launch_tiles_to_csr(const TileMat& A, const int64_t* rp, int32_t* col, uint16_t* h16, cudaStream_t st);

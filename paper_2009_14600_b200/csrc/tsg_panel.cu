@@ -484,21 +484,30 @@ __global__ void __launch_bounds__(256) panel_copy_kernel(int64_t rows, uint32_t 
   const uint32_t off = row < r1 ? uint32_t(row_ptr[row] - base) : T;
   const uint32_t src0 = row < r1 ? row_stage[row] : 0u;
   bool bad = false;
-  for (uint32_t q0 = 0; q0 < T; q0 += 32) {
-    const uint32_t q = q0 + lane;
-    int r = 0;  // last row whose offset is <= q (empty rows resolve to the next one)
+  // four entries per lane per step: the row lookups and loads first, then the stores
+  for (uint32_t q0 = 0; q0 < T; q0 += 128) {
+    uint2 e[4];
 #pragma unroll
-    for (int b = 8; b > 0; b >>= 1) {
-      const uint32_t v = __shfl_sync(kFull, off, r + b);
-      if (v <= q) r += b;
+    for (int u = 0; u < 4; ++u) {
+      const uint32_t q = q0 + 32 * u + lane;
+      int r = 0;  // last row whose offset is <= q (empty rows resolve to the next one)
+#pragma unroll
+      for (int b = 8; b > 0; b >>= 1) {
+        const uint32_t v = __shfl_sync(kFull, off, r + b);
+        if (v <= q) r += b;
+      }
+      const uint32_t o = __shfl_sync(kFull, off, r), sr = __shfl_sync(kFull, src0, r);
+      e[u] = q < T ? __ldg(stage + sr + (q - o)) : make_uint2(0, 0);
     }
-    const uint32_t o = __shfl_sync(kFull, off, r), sr = __shfl_sync(kFull, src0, r);
-    if (q < T) {
-      const uint2 e = __ldg(stage + sr + (q - o));
-      const float x = __uint_as_float(e.x);
-      bad |= !isfinite(x);
-      col[base + q] = int32_t(e.y);
-      val[base + q] = x;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const uint32_t q = q0 + 32 * u + lane;
+      if (q < T) {
+        const float x = __uint_as_float(e[u].x);
+        bad |= !isfinite(x);
+        col[base + q] = int32_t(e[u].y);
+        val[base + q] = x;
+      }
     }
   }
   if (__any_sync(kFull, bad) && lane == 0) atomicOr(err_flag, unsigned(kErrPrecision));

@@ -233,3 +233,18 @@ def test_rmat_full_size_t16_counters(ctx):
     st16 = port.tile_stats(A, A, 16)
     for k in ("tiles_a", "raw_pairs", "filtered_pairs", "segments", "counted_elements"):
         assert st[k] == st16[k], (k, st[k], st16[k])
+
+
+@pytest.mark.slow
+def test_rmat_full_size_against_compiled_reference(ctx):
+    """R-MAT 2^20 at full size against the compiled reference itself
+    (oracle/_ref: dense_spgemm_mixed_ordered, oracle.cpp:102-121, the
+    reference's bit-identical restatement of its pipeline; ~40 s on one host
+    core): pattern and every fp32 value bit-equal, in both numeric modes."""
+    if not ref.available():
+        pytest.skip("oracle/_ref not built")
+    A = W.make("rmat")[0]
+    want = ref.oracle(A)
+    for mode in ("tensor", "ordered"):
+        got = ctx.spgemm(A.to_device(), A.to_device(), out="device", mode=mode).C.to_numpy()
+        assert csr_bits_equal(got, want), (mode, first_diff(got, want))
