@@ -451,8 +451,8 @@ inline unsigned resolve_gpus(unsigned requested) {
 // non-square input, output Fp32Stored 8x8 tiles, the SquareResult counters.
 // Counters come from the GPU's 16x16 pipeline; counted_elements (symbolic
 // nnz(C)) is tile-size invariant and equals the reference's.  The 8x8 tiles
-// go to the GPU as CSR and come back through detail::csr_to_tiled, both
-// O(nnz) without a global sort.
+// are re-tiled on the GPU both ways (tsg_tiles8_to_csr into the pipeline's
+// CSR, tsg_csr_to_tiles8 out of it); only the tile arrays cross PCIe.
 inline SquareResult spgemm_square(const TiledMatrix& A, const SquareOptions& o = {}) {
   if (A.rows != A.cols)
     throw DimensionError("matrix squaring needs a square input, got " + std::to_string(A.rows) + "x" +
@@ -463,15 +463,65 @@ inline SquareResult spgemm_square(const TiledMatrix& A, const SquareOptions& o =
   std::unique_ptr<Context> multi;
   if (gpus > 1) multi = std::make_unique<Context>(devs);
   Context& ctx = multi ? *multi : default_context();
-  const detail::HostCsr a = detail::tiled_to_csr(A);
-  const tsg_csr va = a.view();
+  // the 8x8 tiles as a struct of arrays, to a device CSR on the GPU
+  std::vector<std::uint32_t> tr(A.tiles.size()), tc(A.tiles.size());
+  std::vector<std::uint64_t> bm(A.tiles.size()), ei(A.tiles.size());
+  for (std::size_t i = 0; i < A.tiles.size(); ++i) {
+    tr[i] = A.tiles[i].tile_row;
+    tc[i] = A.tiles[i].tile_col;
+    bm[i] = A.tiles[i].bitmap;
+    ei[i] = A.tiles[i].elem_index;
+  }
+  tsg_tiles8 t8{};
+  t8.rows = std::int64_t(A.rows);
+  t8.cols = std::int64_t(A.cols);
+  t8.ntiles = std::int64_t(A.tiles.size());
+  t8.nnz = std::int64_t(A.elements.size());
+  t8.tile_row = tr.data();
+  t8.tile_col = tc.data();
+  t8.bitmap = bm.data();
+  t8.elem_index = ei.data();
+  t8.val = A.elements.data();
+  t8.mem = TSG_MEM_HOST;
+  detail::Out ain(ctx.get());
+  ain.o.mem = TSG_MEM_DEVICE;
+  throw_status(tsg_tiles8_to_csr(ctx.get(), &t8, &ain.o), tsg_last_error(ctx.get()));
+  tsg_csr va{};
+  va.rows = ain.o.rows;
+  va.cols = ain.o.cols;
+  va.nnz = ain.o.nnz;
+  va.row_ptr = ain.o.row_ptr;
+  va.col = ain.o.col;
+  va.val = ain.o.val;
+  va.dtype = TSG_F32;
+  va.mem = TSG_MEM_DEVICE;
   tsg_options opt = detail::options(o.ordered);
   opt.phase_timing = 1;  // SquareResult::timing is always filled (kernels.cpp:260-280)
   tsg_run_stats st{};
   detail::Out out(ctx.get());
+  out.o.mem = TSG_MEM_DEVICE;
   throw_status(tsg_spgemm(ctx.get(), &va, &va, &out.o, &opt, &st, nullptr), tsg_last_error(ctx.get()));
+  // the product back to 8x8 tiles on the GPU
+  tsg_csr vc{};
+  vc.rows = out.o.rows;
+  vc.cols = out.o.cols;
+  vc.nnz = out.o.nnz;
+  vc.row_ptr = out.o.row_ptr;
+  vc.col = out.o.col;
+  vc.val = out.o.val;
+  vc.dtype = TSG_F32;
+  vc.mem = TSG_MEM_DEVICE;
+  tsg_tiles8_out t8o{};
+  throw_status(tsg_csr_to_tiles8(ctx.get(), &vc, &t8o), tsg_last_error(ctx.get()));
   SquareResult r;
-  r.output = detail::csr_to_tiled(out.o);
+  r.output.rows = A.rows;
+  r.output.cols = A.cols;
+  r.output.kind = ElementKind::Fp32Stored;
+  r.output.tiles.resize(std::size_t(t8o.ntiles));
+  for (std::size_t i = 0; i < r.output.tiles.size(); ++i)
+    r.output.tiles[i] = TileEntry{t8o.tile_row[i], t8o.tile_col[i], t8o.elem_index[i], t8o.bitmap[i]};
+  r.output.elements.assign(t8o.val, t8o.val + t8o.nnz);
+  tsg_free_tiles8(&t8o);
   r.timing = {st.task_list, st.sort, st.counting, st.multiply, st.compaction, st.total};
   r.memory = {st.mem_input_tiles, st.mem_input_elements, st.mem_task_list, st.mem_counting,
               st.mem_pre_compaction, st.mem_output, st.mem_peak};

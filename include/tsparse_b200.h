@@ -200,6 +200,40 @@ TSG_API int tsg_spgemm_chain(tsg_ctx* ctx, int n, const tsg_csr* const* X, tsg_c
 TSG_API void tsg_free_csr(tsg_ctx* ctx, tsg_csr_out* C);
 TSG_API void tsg_free_tiles(tsg_tiles_out* t);
 
+/* The reference's 8x8 TiledMatrix (proj/include/tilemul/tile_format.hpp:24-55)
+ * as a struct of arrays: tiles sorted by (tile_row, tile_col), bit 8r + c of
+ * a 64-bit bitmap marks slot (r, c), each tile's elements contiguous from
+ * elem_index in ascending bit order.  Input view (host or device). */
+typedef struct {
+  int64_t rows, cols, ntiles, nnz;
+  const uint32_t* tile_row;
+  const uint32_t* tile_col;
+  const uint64_t* bitmap;
+  const uint64_t* elem_index;
+  const float* val;
+  int32_t mem; /* tsg_mem */
+  int32_t _pad;
+} tsg_tiles8;
+
+/* Host output of tsg_csr_to_tiles8, allocated by the library. */
+typedef struct {
+  int64_t rows, cols, ntiles, nnz;
+  uint32_t* tile_row;
+  uint32_t* tile_col;
+  uint64_t* bitmap;
+  uint64_t* elem_index;
+  float* val;
+} tsg_tiles8_out;
+
+/* 8x8 tiles -> CSR on the GPU (to_element_coo, tile_format.cpp:131-154,
+ * without its global sort); C->mem chooses host or device output (fp32). */
+TSG_API int tsg_tiles8_to_csr(tsg_ctx* ctx, const tsg_tiles8* T, tsg_csr_out* C);
+/* CSR (fp32 values, host or device) -> 8x8 tiles on the GPU, equal to
+ * from_element_coo(to COO, Fp32Stored) (tile_format.cpp:61-129): zeros
+ * dropped, non-finite values raise status 3.  Host output. */
+TSG_API int tsg_csr_to_tiles8(tsg_ctx* ctx, const tsg_csr* C, tsg_tiles8_out* T);
+TSG_API void tsg_free_tiles8(tsg_tiles8_out* T);
+
 /* sum_k nnzA(:,k) * nnzB(k,:) on the device (analytics.cpp:51-65,
  * generalised to A != B): the GFLOPS denominator / 2. */
 TSG_API int tsg_cbar(tsg_ctx* ctx, const tsg_csr* A, const tsg_csr* B, uint64_t* cbar);

@@ -16,7 +16,7 @@ ROOT = PKG.parent
 CSRC = PKG / "csrc"
 BUILD = ROOT / "build" / "csrc"
 LIB = PKG / "libtsparse_b200.so"
-SOURCES = ["tsg_convert.cu", "tsg_panel.cu", "tsg_esc.cu", "tsg_tc05.cu", "tsg_api.cu"]
+SOURCES = ["tsg_convert.cu", "tsg_panel.cu", "tsg_esc.cu", "tsg_tc05.cu", "tsg_tiles8.cu", "tsg_api.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 # TSG_NVCC_FLAGS: extra nvcc flags for A/B builds (e.g. -DTSG_ESC_NT=512)

@@ -34,6 +34,18 @@ class tsg_tiles_out(C.Structure):
                 ("elem_index", C.c_void_p), ("val", C.c_void_p)]
 
 
+class tsg_tiles8(C.Structure):
+    _fields_ = [("rows", C.c_int64), ("cols", C.c_int64), ("ntiles", C.c_int64), ("nnz", C.c_int64),
+                ("tile_row", C.c_void_p), ("tile_col", C.c_void_p), ("bitmap", C.c_void_p),
+                ("elem_index", C.c_void_p), ("val", C.c_void_p), ("mem", C.c_int32), ("_pad", C.c_int32)]
+
+
+class tsg_tiles8_out(C.Structure):
+    _fields_ = [("rows", C.c_int64), ("cols", C.c_int64), ("ntiles", C.c_int64), ("nnz", C.c_int64),
+                ("tile_row", C.c_void_p), ("tile_col", C.c_void_p), ("bitmap", C.c_void_p),
+                ("elem_index", C.c_void_p), ("val", C.c_void_p)]
+
+
 class tsg_options(C.Structure):
     _fields_ = [("mode", C.c_int32), ("drop_nonfinite", C.c_int32),
                 ("phase_timing", C.c_int32), ("want_tiles", C.c_int32)]
@@ -62,7 +74,8 @@ class tsg_run_stats(C.Structure):
 # Every symbol include/tsparse_b200.h declares (checked by tests/test_abi.py).
 EXPORTS = ("tsg_default_options", "tsg_create", "tsg_destroy", "tsg_last_error", "tsg_abi_version",
            "tsg_spgemm", "tsg_spgemm_chain", "tsg_free_csr", "tsg_free_tiles", "tsg_cbar",
-           "tsg_launch_count", "tsg_last_kernel_ms", "tsg_create_multi", "tsg_last_panel_ms")
+           "tsg_launch_count", "tsg_last_kernel_ms", "tsg_create_multi", "tsg_last_panel_ms",
+           "tsg_tiles8_to_csr", "tsg_csr_to_tiles8", "tsg_free_tiles8")
 
 _lib = None
 
@@ -109,6 +122,12 @@ def load() -> C.CDLL:
     lib.tsg_cbar.restype = C.c_int
     lib.tsg_launch_count.argtypes = [P]
     lib.tsg_launch_count.restype = C.c_uint64
+    lib.tsg_tiles8_to_csr.argtypes = [P, C.POINTER(tsg_tiles8), C.POINTER(tsg_csr_out)]
+    lib.tsg_tiles8_to_csr.restype = C.c_int
+    lib.tsg_csr_to_tiles8.argtypes = [P, C.POINTER(tsg_csr), C.POINTER(tsg_tiles8_out)]
+    lib.tsg_csr_to_tiles8.restype = C.c_int
+    lib.tsg_free_tiles8.argtypes = [C.POINTER(tsg_tiles8_out)]
+    lib.tsg_free_tiles8.restype = None
     lib.tsg_last_kernel_ms.argtypes = [P, C.c_char_p]
     lib.tsg_last_kernel_ms.restype = C.c_double
     _lib = lib

@@ -2068,6 +2068,169 @@ int tsg_cbar(tsg_ctx* ctx, const tsg_csr* A, const tsg_csr* B, uint64_t* cbar) {
   }
 }
 
+int tsg_tiles8_to_csr(tsg_ctx* ctx, const tsg_tiles8* T, tsg_csr_out* C) {
+  if (!ctx || !T || !C) return TSG_ERR_OTHER;
+  if (!ctx->sub.empty()) {
+    const int rc = tsg_tiles8_to_csr(ctx->sub[0], T, C);
+    ctx->err = ctx->sub[0]->err;
+    return rc;
+  }
+  ctx->err.clear();
+  C->_owner = nullptr;
+  try {
+    TSG_CUDA(cudaSetDevice(ctx->device));
+    if (T->rows < 0 || T->cols < 0 || T->ntiles < 0 || T->nnz < 0)
+      throw Fail{TSG_ERR_INVARIANT, "tiles8: negative size"};
+    if (T->nnz >= (int64_t(1) << 32)) throw Fail{TSG_ERR_OTHER, "tiles8: more than 2^32 elements"};
+    Scratch sc(ctx);
+    cudaStream_t s = ctx->stream;
+    const int64_t rows = T->rows, nt = T->ntiles, tile_rows = (rows + 7) / 8;
+    auto dev = [&](const void* p, size_t bytes) -> const void* {  // host arrays -> device
+      if (T->mem == TSG_MEM_DEVICE || bytes == 0) return p;
+      char* d = sc.alloc<char>(bytes);
+      TSG_CUDA(cudaMemcpyAsync(d, p, bytes, cudaMemcpyHostToDevice, s));
+      return d;
+    };
+    const auto* trow = static_cast<const uint32_t*>(dev(T->tile_row, nt * 4));
+    Tiles8View v;
+    v.tile_col = static_cast<const uint32_t*>(dev(T->tile_col, nt * 4));
+    v.bitmap = static_cast<const unsigned long long*>(dev(T->bitmap, nt * 8));
+    v.elem_index = static_cast<const unsigned long long*>(dev(T->elem_index, nt * 8));
+    v.val = static_cast<const float*>(dev(T->val, T->nnz * 4));
+    auto* err = sc.alloc<unsigned>(1);
+    TSG_CUDA(cudaMemsetAsync(err, 0, sizeof(unsigned), s));
+    auto* trp = sc.alloc<uint32_t>(tile_rows + 1);
+    TSG_CUDA(cudaMemsetAsync(trp, 0, (tile_rows + 1) * sizeof(uint32_t), s));
+    launch_tiles8_trp(trow, nt, tile_rows, trp, err, s);
+    auto* rowcnt = sc.alloc<int64_t>(rows + 1);
+    TSG_CUDA(cudaMemsetAsync(rowcnt, 0, (rows + 1) * sizeof(int64_t), s));
+    launch_tiles8_to_csr(v, trp, rows, rowcnt, nullptr, nullptr, nullptr, err, true, s);
+    auto* rp = sc.alloc<int64_t>(rows + 1);
+    exclusive_sum(ctx, sc, rowcnt, rp, uint64_t(rows) + 1);
+    check_launch(ctx, 2);
+    const int64_t nnz = readback(ctx, rp + rows);
+    const unsigned ev = readback(ctx, err);
+    if (ev & kErrInvariant) throw Fail{TSG_ERR_INVARIANT, "tiles8: tiles not sorted by row"};
+    if (nnz != T->nnz) throw Fail{TSG_ERR_INVARIANT, "tiles8: bitmap population != element count"};
+    auto* col = sc.alloc<int32_t>(nnz);
+    auto* val = sc.alloc<float>(nnz);
+    launch_tiles8_to_csr(v, trp, rows, nullptr, rp, col, val, err, false, s);
+    check_launch(ctx);
+    auto* owner = new OutOwner();
+    owner->host = C->mem == TSG_MEM_HOST;
+    C->_owner = owner;
+    if (owner->host) {
+      owner->p[0] = pinned_alloc(ctx, (rows + 1) * sizeof(int64_t), &owner->sz[0]);
+      owner->p[1] = pinned_alloc(ctx, std::max<int64_t>(nnz, 1) * sizeof(int32_t), &owner->sz[1]);
+      owner->p[2] = pinned_alloc(ctx, std::max<int64_t>(nnz, 1) * sizeof(float), &owner->sz[2]);
+      TSG_CUDA(cudaMemcpyAsync(owner->p[0], rp, (rows + 1) * 8, cudaMemcpyDeviceToHost, s));
+      if (nnz) {
+        TSG_CUDA(cudaMemcpyAsync(owner->p[1], col, nnz * 4, cudaMemcpyDeviceToHost, s));
+        TSG_CUDA(cudaMemcpyAsync(owner->p[2], val, nnz * 4, cudaMemcpyDeviceToHost, s));
+      }
+    } else {  // keep the device arrays
+      owner->p[0] = rp;
+      owner->p[1] = col;
+      owner->p[2] = val;
+      sc.ptrs.erase(std::remove_if(sc.ptrs.begin(), sc.ptrs.end(),
+                                   [&](void* q) { return q == rp || q == col || q == val; }),
+                    sc.ptrs.end());
+    }
+    TSG_CUDA(cudaStreamSynchronize(s));
+    C->rows = rows;
+    C->cols = T->cols;
+    C->nnz = nnz;
+    C->row_ptr = static_cast<int64_t*>(owner->p[0]);
+    C->col = static_cast<int32_t*>(owner->p[1]);
+    C->val = static_cast<float*>(owner->p[2]);
+    return TSG_OK;
+  } catch (const Fail& f) {
+    ctx->err = f.msg;
+    cudaStreamSynchronize(ctx->stream);
+    if (C->_owner) free_out(ctx, C);
+    return f.code;
+  }
+}
+
+int tsg_csr_to_tiles8(tsg_ctx* ctx, const tsg_csr* C, tsg_tiles8_out* T) {
+  if (!ctx || !C || !T) return TSG_ERR_OTHER;
+  if (!ctx->sub.empty()) {
+    const int rc = tsg_csr_to_tiles8(ctx->sub[0], C, T);
+    ctx->err = ctx->sub[0]->err;
+    return rc;
+  }
+  ctx->err.clear();
+  std::memset(T, 0, sizeof(*T));
+  try {
+    TSG_CUDA(cudaSetDevice(ctx->device));
+    check_csr(C, "C");
+    if (C->dtype != TSG_F32) throw Fail{TSG_ERR_OTHER, "tiles8: fp32 values expected (the product's output)"};
+    Scratch sc(ctx);
+    cudaStream_t s = ctx->stream;
+    const CsrView v = stage(ctx, sc, C, nullptr);
+    const int64_t groups = (C->rows + 7) / 8;
+    auto* err = sc.alloc<unsigned>(1);
+    TSG_CUDA(cudaMemsetAsync(err, 0, sizeof(unsigned), s));
+    auto* gt = sc.alloc<uint32_t>(groups + 1);
+    auto* ge = sc.alloc<uint32_t>(groups + 1);
+    TSG_CUDA(cudaMemsetAsync(gt + groups, 0, 4, s));
+    TSG_CUDA(cudaMemsetAsync(ge + groups, 0, 4, s));
+    launch_validate_rowptr(v, err, s);
+    launch_csr_tiles8_count(v, static_cast<const float*>(v.val), gt, ge, err, s);
+    check_launch(ctx, 2);
+    auto* toff = sc.alloc<unsigned long long>(groups + 1);
+    auto* eoff = sc.alloc<unsigned long long>(groups + 1);
+    exclusive_sum(ctx, sc, gt, toff, uint64_t(groups) + 1);
+    exclusive_sum(ctx, sc, ge, eoff, uint64_t(groups) + 1);
+    const unsigned long long* src[2] = {toff + groups, eoff + groups};
+    unsigned long long tot[2];
+    readback_many(ctx, src, tot);
+    raise_flags(readback(ctx, err));
+    const int64_t nt = int64_t(tot[0]), ne = int64_t(tot[1]);
+    Tiles8Out o;
+    o.tile_row = sc.alloc<uint32_t>(nt);
+    o.tile_col = sc.alloc<uint32_t>(nt);
+    o.bitmap = sc.alloc<unsigned long long>(nt);
+    o.elem_index = sc.alloc<unsigned long long>(nt);
+    o.val = sc.alloc<float>(ne);
+    launch_csr_tiles8_write(v, static_cast<const float*>(v.val), toff, eoff, o, s);
+    check_launch(ctx);
+    T->rows = C->rows;
+    T->cols = C->cols;
+    T->ntiles = nt;
+    T->nnz = ne;
+    T->tile_row = static_cast<uint32_t*>(std::malloc(std::max<int64_t>(nt, 1) * 4));
+    T->tile_col = static_cast<uint32_t*>(std::malloc(std::max<int64_t>(nt, 1) * 4));
+    T->bitmap = static_cast<uint64_t*>(std::malloc(std::max<int64_t>(nt, 1) * 8));
+    T->elem_index = static_cast<uint64_t*>(std::malloc(std::max<int64_t>(nt, 1) * 8));
+    T->val = static_cast<float*>(std::malloc(std::max<int64_t>(ne, 1) * 4));
+    if (nt) {
+      TSG_CUDA(cudaMemcpyAsync(T->tile_row, o.tile_row, nt * 4, cudaMemcpyDeviceToHost, s));
+      TSG_CUDA(cudaMemcpyAsync(T->tile_col, o.tile_col, nt * 4, cudaMemcpyDeviceToHost, s));
+      TSG_CUDA(cudaMemcpyAsync(T->bitmap, o.bitmap, nt * 8, cudaMemcpyDeviceToHost, s));
+      TSG_CUDA(cudaMemcpyAsync(T->elem_index, o.elem_index, nt * 8, cudaMemcpyDeviceToHost, s));
+    }
+    if (ne) TSG_CUDA(cudaMemcpyAsync(T->val, o.val, ne * 4, cudaMemcpyDeviceToHost, s));
+    TSG_CUDA(cudaStreamSynchronize(s));
+    return TSG_OK;
+  } catch (const Fail& f) {
+    ctx->err = f.msg;
+    cudaStreamSynchronize(ctx->stream);
+    tsg_free_tiles8(T);
+    return f.code;
+  }
+}
+
+void tsg_free_tiles8(tsg_tiles8_out* T) {
+  if (!T) return;
+  std::free(T->tile_row);
+  std::free(T->tile_col);
+  std::free(T->bitmap);
+  std::free(T->elem_index);
+  std::free(T->val);
+  std::memset(T, 0, sizeof(*T));
+}
+
 uint64_t tsg_launch_count(const tsg_ctx* ctx) {
   if (!ctx) return 0;
   uint64_t n = ctx->launches;

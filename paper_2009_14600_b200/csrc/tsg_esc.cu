@@ -189,8 +189,21 @@ __device__ __forceinline__ uint32_t radix_pass(EscSmem& sm, uint32_t (&key)[IPT]
     }
   }
   uint32_t w8[8];
+  {
+    // nibble j of each half -> byte j (even / odd digits), then one PRMT per
+    // counter pair: w8[j] = count(j) | count(j + 8) << 16
+    const uint32_t lo = uint32_t(C), hi = uint32_t(C >> 32);
+    const uint32_t le = lo & 0x0f0f0f0fu, lod = (lo >> 4) & 0x0f0f0f0fu;
+    const uint32_t he = hi & 0x0f0f0f0fu, hod = (hi >> 4) & 0x0f0f0f0fu;
 #pragma unroll
-  for (int j = 0; j < 8; ++j) w8[j] = uint32_t((C >> (4 * j)) & 15u) | (uint32_t((C >> (4 * j + 32)) & 15u) << 16);
+    for (int j = 0; j < 8; ++j) {
+      const uint32_t a = (j & 1) ? lod : le, b = (j & 1) ? hod : he;  // compile-time selects
+      const uint32_t bj = uint32_t(j >> 1);                            // byte within the word
+      // byte bj of a -> byte 0, byte bj of b -> byte 2, zeros elsewhere (selector 4 = b byte 0 ... ; 0x7 of the
+      // zero operand): __byte_perm(x, y, s) picks bytes of {y:x} by nibbles of s
+      w8[j] = __byte_perm(a, b, (bj) | (0xcu << 4) | ((4u + bj) << 8) | (0xcu << 12)) & 0x00ff00ffu;
+    }
+  }
   if (IPT == 16 && nv == 16 && C == (d0 == 60 ? 0ull : (1ull << (d0 + 4)))) {
     // all 16 items share digit d: its count (16) carried out of the 4-bit field
     const uint32_t d = d0 >> 2;

@@ -159,6 +159,32 @@ void launch_esc_copy_records(const EscArgs& g, uint32_t rec0, uint32_t rec1, con
 // njt: B rows + 1; nx: 16 per B tile row; single: one per B tile row (scratch)
 void launch_esc_pairstats(const TileMat& A, const TileMat& B, const int32_t* colB, uint64_t tA, uint32_t* njt,
                           uint32_t* nx, uint8_t* single, unsigned long long* out, cudaStream_t st);
+// 8x8 tiles of the reference's TiledMatrix (tsg_tiles8.cu): device arrays
+struct Tiles8View {
+  const uint32_t* tile_col = nullptr;
+  const unsigned long long* bitmap = nullptr;
+  const unsigned long long* elem_index = nullptr;
+  const float* val = nullptr;
+};
+struct Tiles8Out {
+  uint32_t* tile_row = nullptr;
+  uint32_t* tile_col = nullptr;
+  unsigned long long* bitmap = nullptr;
+  unsigned long long* elem_index = nullptr;
+  float* val = nullptr;
+};
+// trp[T] = first tile of tile row T (tiles sorted by row); kErrInvariant if not
+void launch_tiles8_trp(const uint32_t* tile_row, int64_t ntiles, int64_t tile_rows, uint32_t* trp, unsigned* err,
+                       cudaStream_t st);
+// count: rowcnt[r] = elements of row r; else: the CSR at row pointers rp
+void launch_tiles8_to_csr(const Tiles8View& t, const uint32_t* trp, int64_t rows, int64_t* rowcnt, const int64_t* rp,
+                          int32_t* col, float* val, unsigned* err, bool count, cudaStream_t st);
+// per 8-row group: tiles (gt) and elements (ge); then the tiles at the scanned offsets
+void launch_csr_tiles8_count(const CsrView& C, const float* val, uint32_t* gt, uint32_t* ge, unsigned* err,
+                             cudaStream_t st);
+void launch_csr_tiles8_write(const CsrView& C, const float* val, const unsigned long long* toff,
+                             const unsigned long long* eoff, const Tiles8Out& o, cudaStream_t st);
+
 // A given as A-role tiles (a chained stage) -> CSR with binary16 values
 void launch_tiles_rowcount(const TileMat& A, int64_t* rowcnt, cudaStream_t st);
 void launch_tiles_to_csr(const TileMat& A, const int64_t* rp, int32_t* col, uint16_t* h16, cudaStream_t st);

@@ -256,6 +256,40 @@ class Context:
             self._raise(rc)
         return int(v.value)
 
+    def csr_to_tiles8(self, M: Csr) -> dict:
+        """8x8 tiles of a CSR on the GPU (from_element_coo(Fp32Stored) of it):
+        dict of numpy arrays tile_row, tile_col, bitmap, elem_index, val."""
+        keep: list = []
+        v = _view(Csr(M.rows, M.cols, M.row_ptr, M.col,
+                      M.val.to(__import__("torch").float32) if M.on_device else np.asarray(M.val, np.float32)), keep)
+        out = L.tsg_tiles8_out()
+        rc = self._lib.tsg_csr_to_tiles8(self._h, C.byref(v), C.byref(out))
+        if rc != L.TSG_OK:
+            self._raise(rc)
+        nt, nz = int(out.ntiles), int(out.nnz)
+        res = {"tile_row": _np_from(out.tile_row, nt, np.uint32), "tile_col": _np_from(out.tile_col, nt, np.uint32),
+               "bitmap": _np_from(out.bitmap, nt, np.uint64), "elem_index": _np_from(out.elem_index, nt, np.uint64),
+               "val": _np_from(out.val, nz, np.float32)}
+        self._lib.tsg_free_tiles8(C.byref(out))
+        return res
+
+    def tiles8_to_csr(self, rows: int, cols: int, t: dict, out: str = "host") -> Csr:
+        """CSR of 8x8 tiles (arrays as csr_to_tiles8 returns them) on the GPU."""
+        arr = {k: np.ascontiguousarray(t[k], dt) for k, dt in
+               (("tile_row", np.uint32), ("tile_col", np.uint32), ("bitmap", np.uint64),
+                ("elem_index", np.uint64), ("val", np.float32))}
+        v = L.tsg_tiles8()
+        v.rows, v.cols, v.ntiles, v.nnz = rows, cols, len(arr["tile_row"]), len(arr["val"])
+        for k, a in arr.items():
+            setattr(v, k, a.ctypes.data)
+        v.mem = L.TSG_MEM_HOST
+        co = L.tsg_csr_out()
+        co.mem = L.TSG_MEM_DEVICE if out == "device" else L.TSG_MEM_HOST
+        rc = self._lib.tsg_tiles8_to_csr(self._h, C.byref(v), C.byref(co))
+        if rc != L.TSG_OK:
+            self._raise(rc)
+        return self._collect(co, out == "device")
+
     def launch_count(self) -> int:
         return int(self._lib.tsg_launch_count(self._h))
 

@@ -41,7 +41,8 @@ def test_library_has_no_cpu_fallback_symbols():
 @pytest.mark.skipif(subprocess.run(["which", "gcc"], capture_output=True).returncode != 0, reason="no gcc")
 def test_struct_layouts_match_header():
     structs = {"tsg_csr": L.tsg_csr, "tsg_csr_out": L.tsg_csr_out, "tsg_tiles_out": L.tsg_tiles_out,
-               "tsg_options": L.tsg_options, "tsg_run_stats": L.tsg_run_stats}
+               "tsg_options": L.tsg_options, "tsg_run_stats": L.tsg_run_stats, "tsg_tiles8": L.tsg_tiles8,
+               "tsg_tiles8_out": L.tsg_tiles8_out}
     prog = ["#include <stdio.h>", "#include <stddef.h>", f'#include "{HEADER}"', "int main(void){"]
     for s, cls in structs.items():
         prog.append(f'printf("{s} %zu\\n", sizeof({s}));')

@@ -248,3 +248,65 @@ def test_rmat_full_size_against_compiled_reference(ctx):
     for mode in ("tensor", "ordered"):
         got = ctx.spgemm(A.to_device(), A.to_device(), out="device", mode=mode).C.to_numpy()
         assert csr_bits_equal(got, want), (mode, first_diff(got, want))
+
+
+# ---------------------------------------------------------------- 8x8 re-tiling
+def _expected_tile_vals(M, tr, tc, ei):
+    """Tile element array of from_element_coo (tile_format.cpp:61-129): each
+    tile's non-zero elements row-major (= bit order) from elem_index."""
+    rp, col = np.asarray(M.row_ptr, np.int64), np.asarray(M.col, np.int64)
+    val = np.asarray(M.val, np.float32)
+    rows = np.repeat(np.arange(M.rows, dtype=np.int64), np.diff(rp))
+    nz = val != 0
+    rows, col, val = rows[nz], col[nz], val[nz]
+    key = (rows // 8) * ((M.cols + 7) // 8) + col // 8
+    order = np.lexsort(((rows % 8) * 8 + col % 8, key))
+    return val[order]
+
+
+@pytest.mark.parametrize("case", ["random", "odd_dims", "zeros", "rmat_slice", "empty"])
+def test_tiles8_conversion_matches_reference_tiling(ctx, case):
+    rng = np.random.default_rng(7)
+    if case == "rmat_slice":
+        M = W.rmat(14, 16, seed=3)
+        M = T.Csr(M.rows, M.cols, M.row_ptr, M.col, np.asarray(M.val, np.float32) * np.float32(1.5))
+    elif case == "empty":
+        M = T.Csr(37, 29, np.zeros(38, np.int64), np.zeros(0, np.int32), np.zeros(0, np.float32))
+    else:
+        n, m = (1000, 1000) if case != "odd_dims" else (1003, 517)
+        M = ref.random_coo(11, n, m, 0.01, "signed_halves")
+        val = rng.standard_normal(len(M.col)).astype(np.float32)
+        if case == "zeros":  # explicit zeros are dropped, like from_element_coo
+            val[rng.random(len(val)) < 0.2] = 0.0
+        M = T.Csr(M.rows, M.cols, M.row_ptr, M.col, val)
+    got = ctx.csr_to_tiles8(M)
+    want = ref.tile8(T.Csr(M.rows, M.cols, M.row_ptr, M.col, np.asarray(M.val, np.float64)), kind="fp32")
+    for k in ("tile_row", "tile_col", "bitmap", "elem_index"):
+        assert np.array_equal(got[k], getattr(want, k)), k
+    exp = _expected_tile_vals(M, got["tile_row"], got["tile_col"], got["elem_index"])
+    assert np.array_equal(got["val"].view(np.uint32), exp.view(np.uint32))
+    # round trip: tiles -> CSR on the GPU is the zero-dropped input, bit-exact
+    for out in ("host", "device"):
+        back = ctx.tiles8_to_csr(M.rows, M.cols, got, out=out)
+        if out == "device":
+            back = T.Csr(back.rows, back.cols, back.row_ptr.cpu().numpy(), back.col.cpu().numpy(),
+                         back.val.cpu().numpy())
+        nz = np.asarray(M.val, np.float32) != 0
+        rp = np.concatenate([[0], np.cumsum(nz)])[np.asarray(M.row_ptr, np.int64)]
+        assert np.array_equal(np.asarray(back.row_ptr, np.int64), rp)
+        assert np.array_equal(np.asarray(back.col), np.asarray(M.col)[nz])
+        assert np.array_equal(np.asarray(back.val, np.float32).view(np.uint32),
+                              np.asarray(M.val, np.float32)[nz].view(np.uint32))
+
+
+def test_tiles8_conversion_errors(ctx):
+    M = ref.random_coo(5, 64, 64, 0.1, "signed_halves")
+    val = np.asarray(M.val, np.float32).copy()
+    val[3] = np.inf
+    with pytest.raises(T.OverflowError):
+        ctx.csr_to_tiles8(T.Csr(M.rows, M.cols, M.row_ptr, M.col, val))
+    t = ctx.csr_to_tiles8(T.Csr(M.rows, M.cols, M.row_ptr, M.col, np.asarray(M.val, np.float32)))
+    bad = dict(t)
+    bad["tile_row"] = t["tile_row"][::-1].copy()  # unsorted tile rows
+    with pytest.raises(T.InvariantError):
+        ctx.tiles8_to_csr(M.rows, M.cols, bad)
