@@ -1056,9 +1056,8 @@ struct Call {
     exclusive_sum(ctx, sc, nrec, rbase, nr);
     exclusive_sum(ctx, sc, nwk, wbase, nr);
     auto* njt = sc.alloc<uint32_t>(uint64_t(B.rows) + 1);
-    auto* nx = sc.alloc<uint32_t>(uint64_t(B.tile_rows) * 16 + 1);
-    auto* single = sc.alloc<uint8_t>(uint64_t(B.tile_rows) + 1);
-    launch_esc_pairstats(TA, B, dB.col, tA, njt, nx, single, tot + 2, s);
+    auto* rinfo = sc.alloc<uint32_t>(uint64_t(B.tile_rows) + 1);
+    launch_esc_pairstats(TA, B, tA, njt, rinfo, tot + 2, s);
     check_launch(ctx, 3);
     record(ctx, timing, 2);
     uint64_t nrecs = 0, nunits = 0, products = 0;

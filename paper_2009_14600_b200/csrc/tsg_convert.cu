@@ -183,6 +183,7 @@ struct __align__(16) FastSmem {  // 16-byte multiple: the tiles use 16-byte acce
     struct {                              // sort path
       unsigned long long items[32 * kFastU];  // (tile col, row, col, entry, fp16) sorted
       uint16_t ts[32 * kFastU + 1];       // first item of each tile
+      uint32_t bnd[kTile + 1];            // first item of each row (runs of the merge)
     };
   };
 };
@@ -190,28 +191,100 @@ struct __align__(16) FastSmem {  // 16-byte multiple: the tiles use 16-byte acce
 // Sort path for panels the bitmap cannot rank (wider than 8192 tile columns,
 // or more than kFastT tiles: R-MAT, the rectangular products): the panel's
 // kept entries, as 64-bit items (tile col << 40 | row << 36 | col & 15 << 32
-// | entry << 16 | fp16), are bitonic-sorted in shared memory; runs of equal
-// tile column are the tiles, in (row, col) order inside; lanes then emit one
-// tile each.
+// | entry << 16 | fp16), arrive in CSR order -- 16 runs (the rows), each
+// already sorted because a CSR row is -- and four levels of pairwise
+// merge-path merges in shared memory order them; runs of equal tile column
+// are the tiles, in (row, col) order inside; lanes then emit one tile each.
+//
+// One merge level: lane l produces outputs [l S, l S + S) (S = ceil(nk/32)
+// <= 16) of the runs' pairwise merges, in registers -- a merge-path search
+// finds where its first output comes from, then S sequential steps -- and
+// writes them back in place once the warp has read the level.
+__device__ __forceinline__ void merge_rows(unsigned long long* it, const uint32_t* bnd, uint32_t nk, int lane) {
+  const uint32_t S = (nk + 31u) >> 5;
+  const uint32_t q0 = min(nk, uint32_t(lane) * S), q1 = min(nk, q0 + S);
+  for (int w = 1; w < kTile; w <<= 1) {
+    unsigned long long o[kFastU];
+    uint32_t ia = 0, ib = 0, am = 0, be = 0;
+    unsigned long long va = ~0ull, vb = ~0ull;
+    if (q0 < q1) {
+      int p = 0;  // the pair of runs (p .. p+w-1, p+w .. p+2w-1) holding output q0
+      while (bnd[p + 2 * w] <= q0) p += 2 * w;
+      const uint32_t a = bnd[p];
+      am = bnd[p + w];
+      be = bnd[p + 2 * w];
+      const uint32_t d = q0 - a, la = am - a, lb = be - am;
+      uint32_t lo = d > lb ? d - lb : 0u, hi = min(d, la);
+      while (lo < hi) {  // outputs before q0 take lo items of the first run (keys are distinct)
+        const uint32_t m = (lo + hi) >> 1;
+        if (it[a + m] < it[am + d - 1u - m])
+          lo = m + 1u;
+        else
+          hi = m;
+      }
+      ia = a + lo;
+      ib = am + (d - lo);
+      va = ia < am ? it[ia] : ~0ull;
+      vb = ib < be ? it[ib] : ~0ull;
+      while (q0 == be) {  // (empty pair ends) the next non-empty pair
+        p += 2 * w;
+        ia = bnd[p];
+        am = ib = bnd[p + w];
+        be = bnd[p + 2 * w];
+        va = ia < am ? it[ia] : ~0ull;
+        vb = ib < be ? it[ib] : ~0ull;
+      }
+      int pp = p;
+#pragma unroll
+      for (int s2 = 0; s2 < kFastU; ++s2) {
+        const uint32_t q = q0 + uint32_t(s2);
+        if (q < q1) {
+          while (q == be) {  // this pair is done: the next one starts at its beginning
+            pp += 2 * w;
+            ia = bnd[pp];
+            am = ib = bnd[pp + w];
+            be = bnd[pp + 2 * w];
+            va = ia < am ? it[ia] : ~0ull;
+            vb = ib < be ? it[ib] : ~0ull;
+          }
+          if (va < vb) {
+            o[s2] = va;
+            ++ia;
+            va = ia < am ? it[ia] : ~0ull;
+          } else {
+            o[s2] = vb;
+            ++ib;
+            vb = ib < be ? it[ib] : ~0ull;
+          }
+        }
+      }
+    }
+    __syncwarp();
+#pragma unroll
+    for (int s2 = 0; s2 < kFastU; ++s2)
+      if (q0 + uint32_t(s2) < q1) it[q0 + s2] = o[s2];
+    __syncwarp();
+  }
+}
+
 __device__ __forceinline__ uint32_t sparse_panel(FastSmem& sm, const Gapped& out, int roles, int64_t E0, uint32_t E,
                                                  uint32_t nk, int lane, bool seen) {
   unsigned long long* it = sm.items;
-  uint32_t P2 = 32;
-  while (P2 < E) P2 <<= 1;
-  // bitonic sort, ascending (padding items are ~0)
-  for (uint32_t k = 2; k <= P2; k <<= 1)
-    for (uint32_t j = k >> 1; j > 0; j >>= 1) {
-      for (uint32_t pidx = lane; pidx < P2 / 2; pidx += 32) {
-        const uint32_t i = ((pidx & ~(j - 1u)) << 1) | (pidx & (j - 1u)), l = i | j;
-        const unsigned long long x = it[i], y = it[l];
-        const bool up = (i & k) == 0u;
-        if ((x > y) == up) {
-          it[i] = y;
-          it[l] = x;
-        }
-      }
-      __syncwarp();
+  // run starts: the kept items are in CSR order, so row r's run begins at the
+  // first item whose row is >= r
+  if (lane <= kTile) {
+    uint32_t lo = 0, hi = nk;
+    while (lo < hi) {
+      const uint32_t m = (lo + hi) >> 1;
+      if (((it[m] >> 36) & 15u) < uint32_t(lane))
+        lo = m + 1u;
+      else
+        hi = m;
     }
+    sm.bnd[lane] = lane == kTile ? nk : lo;
+  }
+  __syncwarp();
+  merge_rows(it, sm.bnd, nk, lane);
   // tile starts -> tile ranks; etile (first kept entry of each (row, tile))
   uint32_t ntiles = 0;
   const unsigned lt = lanemask_lt();
@@ -322,7 +395,10 @@ __device__ __forceinline__ uint32_t sparse_panel(FastSmem& sm, const Gapped& out
 // every entry stores its fp16 value at its chunk slot.  Panels outside the
 // limits go to the walk list.
 template <int kDtype>
-__global__ void __launch_bounds__(256, 4) convert_fast_kernel(CsrView in, uint32_t tile_rows, Gapped out, int roles,
+#ifndef TSG_CONV_MINB
+#define TSG_CONV_MINB 4
+#endif
+__global__ void __launch_bounds__(256, TSG_CONV_MINB) convert_fast_kernel(CsrView in, uint32_t tile_rows, Gapped out, int roles,
                                                           uint32_t* __restrict__ walk_list,
                                                           uint32_t* __restrict__ walk_count,
                                                           unsigned* __restrict__ err_flag, int drop_nonfinite,
@@ -433,18 +509,20 @@ __global__ void __launch_bounds__(256, 4) convert_fast_kernel(CsrView in, uint32
   auto sort_path = [&]() {
     uint32_t P2 = 32;
     while (P2 < E) P2 <<= 1;
-    uint32_t nk = 0;
+    uint32_t nk = 0;  // kept items, compacted in CSR order
+    const unsigned lt = lanemask_lt();
 #pragma unroll
     for (int u = 0; u < kFastU; ++u) {
       if (32u * u >= P2) break;
       const uint32_t q = 32 * u + lane;
       const bool kp = q < E && ((pk[u] >> 20) & 1u);
-      nk += __popc(__ballot_sync(kFull, kp));
-      sm.items[q] = kp ? (static_cast<unsigned long long>(uint32_t(c[u]) >> 4) << 40) |
-                             (static_cast<unsigned long long>((pk[u] >> 16) & 15u) << 36) |
-                             (static_cast<unsigned long long>(uint32_t(c[u]) & 15u) << 32) |
-                             (static_cast<unsigned long long>(q) << 16) | (pk[u] & 0xffffu)
-                       : ~0ull;
+      const unsigned kb = __ballot_sync(kFull, kp);
+      if (kp)
+        sm.items[nk + __popc(kb & lt)] = (static_cast<unsigned long long>(uint32_t(c[u]) >> 4) << 40) |
+                                         (static_cast<unsigned long long>((pk[u] >> 16) & 15u) << 36) |
+                                         (static_cast<unsigned long long>(uint32_t(c[u]) & 15u) << 32) |
+                                         (static_cast<unsigned long long>(q) << 16) | (pk[u] & 0xffffu);
+      nk += __popc(kb);
     }
     __syncwarp();
     const uint32_t nt = sparse_panel(sm, out, roles, E0, E, nk, lane, seen);

@@ -34,6 +34,8 @@
 //   esc_rowcount / scan / esc_copy   pieces -> CSR
 //   esc_njt / esc_pairstats         raw and filtered tile-pair counts
 #include <algorithm>
+#include <cstdio>
+#include <type_traits>
 
 #include "tsg_kernels.cuh"
 
@@ -79,14 +81,27 @@ struct EscSmem {
 };
 
 __device__ __forceinline__ uint32_t half_nz(uint16_t h) { return h & 0x7fffu; }
+
+#ifdef TSG_ESC_DIAG
+// build-time diagnostics (-DTSG_ESC_DIAG): leaf shapes of one esc_kernel launch
+// [0] sorted leaves [1] products [2] slots (kNT IPT) [3] pass-slots [4] nb==1 leaves
+// [5] dense leaves [6] halvings [7] units [8..12] leaves by IPT 4/8/16 and products in nb>1 leaves
+__device__ unsigned long long g_esc_diag[16];
+#define ESC_DIAG(i, v) (tid == 0 ? (void)atomicAdd(&g_esc_diag[i], (unsigned long long)(v)) : (void)0)
+#else
+#define ESC_DIAG(i, v) ((void)0)
+#endif
 __device__ __forceinline__ uint32_t cpad(uint32_t L) { return L + (L >> 5); }
 
 // Blocked layout: thread t owns items IPT t .. IPT t + IPT-1; its 16-byte
 // vectors are rotated so an LDS.128 phase of 8 lanes hits 8 bank groups.
+#ifndef TSG_ESC_ROT
+#define TSG_ESC_ROT 1
+#endif
 template <int IPT>
 __device__ __forceinline__ uint32_t phys(uint32_t g) {
   constexpr uint32_t NV = IPT / 4;
-  if (NV == 1) return g;
+  if (NV == 1 || !TSG_ESC_ROT) return g;
   const uint32_t t = g / IPT, i = g % IPT, q = i >> 2;
   const uint32_t rot = NV == 4 ? ((t >> 1) & 3u) : ((t >> 2) & 1u);
   return t * IPT + (((q + rot) & (NV - 1)) << 2) + (i & 3u);
@@ -168,6 +183,29 @@ __device__ __forceinline__ uint32_t digit_scan(EscSmem& sm, const uint32_t (&w8)
   return T;
 }
 
+// Blocked reload of the sorted items (thread t: items IPT t .. IPT t + IPT-1)
+template <int IPT>
+__device__ __forceinline__ void reload_blocked(const EscSmem& sm, uint32_t (&key)[IPT], float (&val)[IPT]) {
+  const int tid = threadIdx.x;
+  const uint4* k4 = reinterpret_cast<const uint4*>(sm.s.key) + tid * (IPT / 4);
+  const float4* v4 = reinterpret_cast<const float4*>(sm.s.val) + tid * (IPT / 4);
+#pragma unroll
+  for (int q = 0; q < IPT / 4; ++q) {
+    const uint32_t rot = !TSG_ESC_ROT ? 0u : IPT == 16 ? ((uint32_t(tid) >> 1) & 3u) : IPT == 8 ? ((uint32_t(tid) >> 2) & 1u) : 0u;
+    const uint32_t pq = (q + rot) & (IPT / 4 - 1);
+    const uint4 kk = k4[pq];
+    const float4 vv = v4[pq];
+    key[4 * q] = kk.x;
+    key[4 * q + 1] = kk.y;
+    key[4 * q + 2] = kk.z;
+    key[4 * q + 3] = kk.w;
+    val[4 * q] = vv.x;
+    val[4 * q + 1] = vv.y;
+    val[4 * q + 2] = vv.z;
+    val[4 * q + 3] = vv.w;
+  }
+}
+
 // One stable LSD pass on the 4-bit digit at `shift` over the valid items
 // (mask vm) in registers: per-thread digit counts as 4-bit fields of a u64,
 // a raking scan of the [digit][thread] counters, scatter, blocked reload.
@@ -176,14 +214,17 @@ template <int IPT>
 __device__ __forceinline__ uint32_t radix_pass(EscSmem& sm, uint32_t (&key)[IPT], float (&val)[IPT], uint32_t vm,
                                                int shift) {
   const int tid = threadIdx.x;
-  unsigned long long C = 0, rk = 0;
+  // rk: each item's rank among the thread's earlier items of its digit (4 bits each)
+  using Rk = typename std::conditional<(IPT <= 8), uint32_t, unsigned long long>::type;
+  unsigned long long C = 0;
+  Rk rk = 0;
   uint32_t nv = 0, d0 = 0;
 #pragma unroll
   for (int i = 0; i < IPT; ++i) {
     if ((vm >> i) & 1u) {
       const uint32_t s = ((key[i] >> shift) & 15u) << 2;
       if (nv == 0) d0 = s;
-      rk |= ((C >> s) & 15ull) << (4 * i);
+      rk |= Rk((C >> s) & 15ull) << (4 * i);
       C += 1ull << s;
       ++nv;
     }
@@ -224,23 +265,7 @@ __device__ __forceinline__ uint32_t radix_pass(EscSmem& sm, uint32_t (&key)[IPT]
     }
   }
   __syncthreads();
-  const uint4* k4 = reinterpret_cast<const uint4*>(sm.s.key) + tid * (IPT / 4);
-  const float4* v4 = reinterpret_cast<const float4*>(sm.s.val) + tid * (IPT / 4);
-#pragma unroll
-  for (int q = 0; q < IPT / 4; ++q) {
-    const uint32_t rot = IPT == 16 ? ((uint32_t(tid) >> 1) & 3u) : IPT == 8 ? ((uint32_t(tid) >> 2) & 1u) : 0u;
-    const uint32_t pq = (q + rot) & (IPT / 4 - 1);
-    const uint4 kk = k4[pq];
-    const float4 vv = v4[pq];
-    key[4 * q] = kk.x;
-    key[4 * q + 1] = kk.y;
-    key[4 * q + 2] = kk.z;
-    key[4 * q + 3] = kk.w;
-    val[4 * q] = vv.x;
-    val[4 * q + 1] = vv.y;
-    val[4 * q + 2] = vv.z;
-    val[4 * q + 3] = vv.w;
-  }
+  reload_blocked<IPT>(sm, key, val);
   return tlo + (T >> 16);
 }
 
@@ -548,10 +573,14 @@ __device__ void sort_leaf(EscSmem& sm, const EscArgs& g, const Unit& u, uint32_t
   float val[IPT];
   uint32_t vm = 0;
   const uint32_t g0 = uint32_t(tid) * IPT;
+  uint32_t cc[IPT];
+  uint16_t hb[IPT];
 #pragma unroll
   for (int i = 0; i < IPT; ++i) {
     key[i] = 0;
     val[i] = 0.f;
+    cc[i] = 0;
+    hb[i] = 0;
   }
   if (g0 < P) {
     uint32_t e = 0, top = ne;  // largest e with pre[e] <= g0
@@ -584,24 +613,29 @@ __device__ void sort_leaf(EscSmem& sm, const EscArgs& g, const Unit& u, uint32_t
         val[i] = av;
       }
     }
-    uint32_t cc[IPT];
-    uint16_t hb[IPT];
 #pragma unroll
     for (int i = 0; i < IPT; ++i) {
       cc[i] = g0 + i < P ? uint32_t(__ldg(g.colB + idx[i])) : 0u;
       hb[i] = g0 + i < P ? __ldg(g.hB + idx[i]) : uint16_t(0);
     }
+  }
 #pragma unroll
-    for (int i = 0; i < IPT; ++i) {
-      if (half_nz(hb[i])) {
-        const uint32_t c = cc[i], br = key[i];
-        vm |= 1u << i;
-        key[i] = ((br >> 4) << bshift) | (((c - lo) >> 4) << 8) | ((c & 15u) << 4) | (br & 15u);
-        val[i] = __fmul_rn(val[i], __half2float(__ushort_as_half(hb[i])));
-      }
+  for (int i = 0; i < IPT; ++i) {
+    if (half_nz(hb[i])) {
+      const uint32_t c = cc[i], br = key[i];
+      vm |= 1u << i;
+      key[i] = ((br >> 4) << bshift) | (((c - lo) >> 4) << 8) | ((c & 15u) << 4) | (br & 15u);
+      val[i] = __fmul_rn(val[i], __half2float(__ushort_as_half(hb[i])));
     }
   }
   __syncthreads();  // the table (aliased by the sort buffer) is consumed
+  ESC_DIAG(0, 1);
+  ESC_DIAG(1, P);
+  ESC_DIAG(2, kNT * IPT);
+  ESC_DIAG(3, uint64_t(kNT * IPT) * (1 + (bshift - 8 + 3) / 4 + (u.nb > 1 ? 2 : 0)));
+  ESC_DIAG(4, u.nb == 1);
+  ESC_DIAG(IPT == 4 ? 8 : IPT == 8 ? 9 : 10, 1);
+  if (u.nb > 1) ESC_DIAG(11, P);
   // ---- sort: cc, J digits, tile row (stable: ascending k survives)
   uint32_t n = radix_pass<IPT>(sm, key, val, vm, 4);
   for (int s = 8; s < bshift; s += 4) n = radix_pass<IPT>(sm, key, val, valid_mask<IPT>(n), s);
@@ -827,6 +861,7 @@ __global__ void __launch_bounds__(kNT, kMinBlocks) esc_kernel(EscArgs g) {
     const uint32_t ui = sm.bc[0];
     __syncthreads();
     if (ui >= nunits) break;
+    ESC_DIAG(7, 1);
     const uint4 wu = g.units[ui];
     Unit u;
     u.I = wu.x;
@@ -873,8 +908,10 @@ __global__ void __launch_bounds__(kNT, kMinBlocks) esc_kernel(EscArgs g) {
       } else if (u.nb > 1) {  // cannot happen: a group's products fit (planned exactly)
         if (tid == 0) atomicOr(g.err_flag, unsigned(kErrPool));
       } else if (hi - lo <= kDenseW) {
+        ESC_DIAG(5, 1);
         dense_leaf(sm, g, u, lo, hi, pc, segs, structural);
       } else {  // halve (16-aligned), left half first
+        ESC_DIAG(6, 1);
         if (tid == 0) {
           uint32_t mid = (lo + ((hi - lo) >> 1)) & ~15u;
           if (mid <= lo) mid = lo + 16;
@@ -1153,17 +1190,24 @@ __global__ void __launch_bounds__(256) esc_copy_records_kernel(uint32_t rec0, ui
 
 // ---------------------------------------------------------------- statistics
 
-// njt[row] = tiles touched by B's CSR row (first kept entry of each tile)
+// njt[k] = distinct tiles CSR row k of B touches (its entries that are the
+// first of their (row, tile)).  Eight lanes per row, four rows per warp step
+// (R-MAT rows hold ~16 entries).
 __global__ void esc_njt_kernel(int64_t rows, const int64_t* __restrict__ rp, const uint32_t* __restrict__ etile,
                                uint32_t* __restrict__ njt) {
-  const int lane = threadIdx.x & 31;
-  for (int64_t k = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5; k < rows;
-       k += (int64_t(gridDim.x) * blockDim.x) >> 5) {
+  const int lane = threadIdx.x & 31, sl = lane & 7;
+  for (int64_t k0 = ((blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5) * 4; k0 < rows;
+       k0 += ((int64_t(gridDim.x) * blockDim.x) >> 5) * 4) {
+    const int64_t k = k0 + (lane >> 3);
     uint32_t n = 0;
-    const int64_t e1 = rp[k + 1];
-    for (int64_t e = rp[k] + lane; e < e1; e += 32) n += (__ldg(etile + e) & kDupEntry) == 0u;
-    n = __reduce_add_sync(kFull, n);
-    if (lane == 0) njt[k] = n;
+    if (k < rows) {
+      const int64_t e1 = __ldg(rp + k + 1);
+      for (int64_t e = __ldg(rp + k) + sl; e < e1; e += 8) n += (__ldg(etile + e) & kDupEntry) == 0u;
+    }
+    n += __shfl_xor_sync(kFull, n, 1);
+    n += __shfl_xor_sync(kFull, n, 2);
+    n += __shfl_xor_sync(kFull, n, 4);
+    if (sl == 0 && k < rows) njt[k] = n;
   }
 }
 
@@ -1173,40 +1217,78 @@ __global__ void esc_njt_kernel(int64_t rows, const int64_t* __restrict__ rp, con
 // others test B's row occupancies.  Warp per 32 A tiles.
 constexpr uint32_t kPairBits = 8192;  // tile ranks of a B tile row the pair-statistics bitmap covers
 
-// Per B tile row k: nx[16 k + x] = its tiles whose row x is occupied, and
-// nx_single[k] = 1 when every tile occupies exactly one row (R-MAT's ~1-entry
-// tiles).  Then an A tile with column occupancy c passes sum_{x in c} nx tiles
-// of that row exactly.  Warp per tile row.
-__global__ void __launch_bounds__(256) esc_brow_bits_kernel(TileMat B, uint32_t* __restrict__ nx,
-                                                           uint8_t* __restrict__ single) {
+// Per B tile row k, rinfo[k] = its occupied rows (lo16: rows with a kept
+// entry) | kSingleRows when every tile occupies exactly one row (R-MAT's
+// ~1-entry tiles).  The tiles of row k with row x occupied are the distinct
+// tiles CSR row 16 k + x touches, njt[16 k + x]; so an A tile with column
+// occupancy c passes
+//   all len tiles        when c covers every occupied row,
+//   none                 when it meets none,
+//   sum_{x in c} njt     when the tiles are single-row.
+// Warp per tile row.
+constexpr uint32_t kSingleRows = 1u << 16;
+
+__global__ void __launch_bounds__(256) esc_brow_bits_kernel(TileMat B, uint32_t* __restrict__ rinfo) {
   const int lane = threadIdx.x & 31;
   const uint32_t k = blockIdx.x * 8 + (threadIdx.x >> 5);
   if (k >= B.tile_rows) return;
   const uint32_t b0 = B.trp[k], b1 = B.trp[k + 1];
-  uint32_t cnt[16];
-#pragma unroll
-  for (int x = 0; x < 16; ++x) cnt[x] = 0;
+  uint32_t rows = 0;
   bool one = true;
   for (uint32_t b = b0 + lane; b < b1; b += 32) {
     const uint32_t ro = __ldg(&B.tco[b].y) >> 16;
     one &= __popc(ro) == 1;
-#pragma unroll
-    for (int x = 0; x < 16; ++x) cnt[x] += (ro >> x) & 1u;
+    rows |= ro;
   }
-#pragma unroll
-  for (int x = 0; x < 16; ++x) {
-    const uint32_t t = __reduce_add_sync(kFull, cnt[x]);
-    if (lane == x) nx[size_t(k) * 16 + x] = t;
-  }
+  rows = __reduce_or_sync(kFull, rows);
   const bool all = __all_sync(kFull, one);
-  if (lane == 0) single[k] = all ? 1 : 0;
+  if (lane == 0) rinfo[k] = rows | (all ? kSingleRows : 0u);
 }
 
+// The B tiles of tile row k meeting column occupancy c (an A tile with several
+// occupied columns, B tiles with several occupied rows).  Long B tile rows
+// (R-MAT hubs): the union of the tiles the occupied B CSR rows touch, as a
+// bitmap over the tile row's tile ranks (B tile (k, J) has row kk occupied iff
+// CSR row 16 k + kk keeps an entry in tile J, whose etile is J's rank); short
+// ones: the occupancy test over the tile row.  Warp-collective; bm: the warp's
+// kPairBits-bit scratch.
+__device__ __forceinline__ uint32_t meets_count(const TileMat& B, uint32_t k, uint32_t c, uint32_t* bm, int lane) {
+  const uint32_t b0 = __ldg(B.trp + k), b1 = __ldg(B.trp + k + 1), len = b1 - b0;
+  uint32_t entries = 0;
+  for (uint32_t ci = c; ci; ci &= ci - 1u) {
+    const int64_t row = int64_t(k) * 16 + (__ffs(ci) - 1);
+    if (row < B.rows) entries += uint32_t(__ldg(B.csr_rp + row + 1) - __ldg(B.csr_rp + row));
+  }
+  uint32_t n = 0;
+  if (len <= kPairBits && entries < len) {
+    for (uint32_t i = lane; i < (len + 31) / 32; i += 32) bm[i] = 0;
+    __syncwarp();
+    for (uint32_t ci = c; ci; ci &= ci - 1u) {
+      const int64_t row = int64_t(k) * 16 + (__ffs(ci) - 1);
+      if (row >= B.rows) continue;
+      const int64_t e1 = __ldg(B.csr_rp + row + 1);
+      for (int64_t e = __ldg(B.csr_rp + row) + lane; e < e1; e += 32) {
+        const uint32_t et = __ldg(B.etile + e);
+        if (et != kNoTile) {
+          const uint32_t t = et & ~kDupEntry;
+          atomicOr(&bm[t >> 5], 1u << (t & 31));
+        }
+      }
+    }
+    __syncwarp();
+    for (uint32_t i = lane; i < (len + 31) / 32; i += 32) n += __popc(bm[i]);
+    __syncwarp();
+  } else {
+    for (uint32_t b = b0 + lane; b < b1; b += 32) n += ((__ldg(&B.tco[b].y) >> 16) & c) != 0u;
+  }
+  return __reduce_add_sync(kFull, n);
+}
+
+// Thread per A tile (warp per 32): raw pairs, and the filtered pairs of the
+// cheap cases; the warp counts its A tiles that need meets_count together.
 __global__ void __launch_bounds__(256) esc_pairstats_kernel(TileMat A, TileMat B, uint32_t tA,
                                                            const uint32_t* __restrict__ njt,
-                                                           const int32_t* __restrict__ colB,
-                                                           const uint32_t* __restrict__ nx,
-                                                           const uint8_t* __restrict__ single,
+                                                           const uint32_t* __restrict__ rinfo,
                                                            unsigned long long* __restrict__ out) {
   const int lane = threadIdx.x & 31;
   const uint32_t a0 = (blockIdx.x * 8 + (threadIdx.x >> 5)) * 32;
@@ -1223,52 +1305,24 @@ __global__ void __launch_bounds__(256) esc_pairstats_kernel(TileMat A, TileMat B
     if (__popc(co) == 1) {
       const int64_t row = int64_t(K) * 16 + (__ffs(co) - 1);
       filt = row < B.rows ? __ldg(njt + row) : 0u;
-    } else if (co != 0 && __ldg(single + K)) {  // every B tile of row K occupies one row
-      for (uint32_t c = co; c; c &= c - 1u) filt += __ldg(nx + size_t(K) * 16 + (__ffs(c) - 1));
-    } else {
-      multi = co != 0;
-    }
-  }
-  // A tile with several occupied columns: the B tiles of tile row k whose row
-  // occupancy meets them.  Long B tile rows (R-MAT hubs): the union of the
-  // tiles the occupied B CSR rows touch, as a bitmap over the tile row's tile
-  // ranks (B tile (k, J) has row kk occupied iff CSR row 16 k + kk keeps an
-  // entry in tile J, whose etile is J's rank); short ones: the occupancy test
-  // over the tile row.
-  __shared__ uint32_t s_bm[8][kPairBits / 32];
-  const int wib = threadIdx.x >> 5;
-  for (unsigned m = __ballot_sync(kFull, multi); m; m &= m - 1) {
-    const int src = __ffs(m) - 1;
-    const uint32_t k = __shfl_sync(kFull, K, src), c = __shfl_sync(kFull, co, src);
-    const uint32_t b0 = __ldg(B.trp + k), b1 = __ldg(B.trp + k + 1), len = b1 - b0;
-    uint32_t entries = 0;
-    for (uint32_t ci = c; ci; ci &= ci - 1u) {
-      const int64_t row = int64_t(k) * 16 + (__ffs(ci) - 1);
-      if (row < B.rows) entries += uint32_t(__ldg(B.csr_rp + row + 1) - __ldg(B.csr_rp + row));
-    }
-    uint32_t n = 0;
-    if (len <= kPairBits && entries < len) {
-      for (uint32_t i = lane; i < (len + 31) / 32; i += 32) s_bm[wib][i] = 0;
-      __syncwarp();
-      for (uint32_t ci = c; ci; ci &= ci - 1u) {
-        const int64_t row = int64_t(k) * 16 + (__ffs(ci) - 1);
-        if (row >= B.rows) continue;
-        const int64_t e1 = __ldg(B.csr_rp + row + 1);
-        for (int64_t e = __ldg(B.csr_rp + row) + lane; e < e1; e += 32) {
-          const uint32_t et = __ldg(B.etile + e);
-          if (et != kNoTile) {
-            const uint32_t t = et & ~kDupEntry;
-            atomicOr(&s_bm[wib][t >> 5], 1u << (t & 31));
-          }
+    } else if (co != 0 && raw != 0) {
+      const uint32_t info = __ldg(rinfo + K), rm = info & 0xffffu;
+      if ((co & rm) == rm) {  // every tile has an occupied row, all of them inside c
+        filt = raw;
+      } else if (co & rm) {
+        if (info & kSingleRows) {
+          for (uint32_t c = co & rm; c; c &= c - 1u) filt += __ldg(njt + size_t(K) * 16 + (__ffs(c) - 1));
+        } else {
+          multi = true;
         }
       }
-      __syncwarp();
-      for (uint32_t i = lane; i < (len + 31) / 32; i += 32) n += __popc(s_bm[wib][i]);
-      __syncwarp();
-    } else {
-      for (uint32_t b = b0 + lane; b < b1; b += 32) n += ((__ldg(&B.tco[b].y) >> 16) & c) != 0u;
     }
-    n = __reduce_add_sync(kFull, n);
+  }
+  __shared__ uint32_t s_bm[8][kPairBits / 32];
+  for (unsigned m = __ballot_sync(kFull, multi); m; m &= m - 1) {
+    const int src = __ffs(m) - 1;
+    const uint32_t n = meets_count(B, __shfl_sync(kFull, K, src), __shfl_sync(kFull, co, src),
+                                   s_bm[threadIdx.x >> 5], lane);
     if (lane == src) filt += n;
   }
 #pragma unroll
@@ -1382,6 +1436,15 @@ void launch_esc(const EscArgs& g, int device, cudaStream_t st) {
     per_sm[d][v] = std::max(1, n);
   }
   k<<<unsigned(per_sm[d][v] * sms[d]), kNT, smem, st>>>(g);
+#ifdef TSG_ESC_DIAG
+  unsigned long long h[16];
+  cudaStreamSynchronize(st);
+  cudaMemcpyFromSymbol(h, g_esc_diag, sizeof(h));
+  std::fprintf(stderr, "esc_diag leaves %llu products %llu slots %llu pass_slots %llu nb1 %llu dense %llu halve %llu units %llu ipt4 %llu ipt8 %llu ipt16 %llu grp_products %llu\n",
+               h[0], h[1], h[2], h[3], h[4], h[5], h[6], h[7], h[8], h[9], h[10], h[11]);
+  const unsigned long long z[16] = {};
+  cudaMemcpyToSymbol(g_esc_diag, z, sizeof(z));
+#endif
 }
 
 void launch_esc_rowcount(const EscArgs& g, const uint32_t* base, int64_t* rowcnt, cudaStream_t st, uint32_t I0,
@@ -1402,12 +1465,11 @@ void launch_esc_copy(const EscArgs& g, const int64_t* row_ptr, int32_t* col, flo
   esc_copy_kernel<<<148 * 16, 256, 0, st>>>(g.nrec, g.piece_top, g.pool_cap, g.pieces, g.stage, row_ptr, col, val);
 }
 
-void launch_esc_pairstats(const TileMat& A, const TileMat& B, const int32_t* colB, uint64_t tA, uint32_t* njt,
-                          uint32_t* nx, uint8_t* single, unsigned long long* out, cudaStream_t st) {
+void launch_esc_pairstats(const TileMat& A, const TileMat& B, uint64_t tA, uint32_t* njt, uint32_t* rinfo,
+                          unsigned long long* out, cudaStream_t st) {
   if (B.rows > 0) esc_njt_kernel<<<2368, 256, 0, st>>>(B.rows, B.csr_rp, B.etile, njt);
-  if (B.tile_rows > 0) esc_brow_bits_kernel<<<(B.tile_rows + 7) / 8, 256, 0, st>>>(B, nx, single);
-  if (tA > 0)
-    esc_pairstats_kernel<<<unsigned((tA + 255) / 256), 256, 0, st>>>(A, B, uint32_t(tA), njt, colB, nx, single, out);
+  if (B.tile_rows > 0) esc_brow_bits_kernel<<<(B.tile_rows + 7) / 8, 256, 0, st>>>(B, rinfo);
+  if (tA > 0) esc_pairstats_kernel<<<unsigned((tA + 255) / 256), 256, 0, st>>>(A, B, uint32_t(tA), njt, rinfo, out);
 }
 
 void launch_tiles_rowcount(const TileMat& A, int64_t* rowcnt, cudaStream_t st) {

@@ -157,8 +157,8 @@ void launch_esc_copy(const EscArgs& g, const int64_t* row_ptr, int32_t* col, flo
 void launch_esc_copy_records(const EscArgs& g, uint32_t rec0, uint32_t rec1, const int64_t* row_ptr, int32_t* col,
                              float* val, cudaStream_t st);
 // njt: B rows + 1; nx: 16 per B tile row; single: one per B tile row (scratch)
-void launch_esc_pairstats(const TileMat& A, const TileMat& B, const int32_t* colB, uint64_t tA, uint32_t* njt,
-                          uint32_t* nx, uint8_t* single, unsigned long long* out, cudaStream_t st);
+void launch_esc_pairstats(const TileMat& A, const TileMat& B, uint64_t tA, uint32_t* njt, uint32_t* rinfo,
+                          unsigned long long* out, cudaStream_t st);
 // 8x8 tiles of the reference's TiledMatrix (tsg_tiles8.cu): device arrays
 struct Tiles8View {
   const uint32_t* tile_col = nullptr;

@@ -146,6 +146,9 @@ __global__ void __launch_bounds__(256) elem_bound_kernel(CsrView A, const int64_
                                                         unsigned long long* __restrict__ total,
                                                         const unsigned* __restrict__ gate) {
   __shared__ unsigned long long s_sum[8];
+  // gate[1]: the conversion's largest A tile row; beyond 128 tiles the call
+  // is general and the speculative light pass stands down (the bound is unused)
+  if (gate[1] > 128u) return;
   const int64_t r = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
   uint64_t b = 0;
   if (r < A.rows && (*gate & kErrRowPtr)) {

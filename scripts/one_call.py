@@ -19,7 +19,15 @@ def dev(M):
     return type(D)(D.rows, D.cols, D.row_ptr, D.col, h) if torch.equal(h.to(D.val.dtype), D.val) else D
 
 
-mats = [dev(M) for M in W.make(cfg)]
+host = W.make(cfg)
+if os.environ.get("ONE_CALL_PANEL"):  # "N,p": rank p's panel of an N-GPU run (A rows), full B
+    from paper_2009_14600_b200 import distributed as Dist
+    N, p = (int(x) for x in os.environ["ONE_CALL_PANEL"].split(","))
+    A = host[0]
+    B = host[1] if len(host) > 1 else host[0]
+    r0, r1 = Dist.panel_bounds(A, B, N)[p]
+    host = [Dist.take_rows(A, r0, r1), B] + list(host[2:])
+mats = [dev(M) for M in host]
 torch.cuda.synchronize()
 if os.environ.get("ONE_CALL_WARM") == "1":  # a first call sizes the staging arena (the speculative path runs next)
     if len(mats) == 3:

@@ -49,6 +49,13 @@ def main():
         raise AssertionError("malformed row_ptr accepted")
     except T.InvariantError:
         n += 1
+    # 8x8 re-tiling both ways (tsg_tiles8.cu)
+    M = W.rmat(scale=10, edge_factor=8)
+    M = T.Csr(M.rows, M.cols, M.row_ptr, M.col, np.asarray(M.val, np.float32))
+    t8 = ctx.csr_to_tiles8(M)
+    back = ctx.tiles8_to_csr(M.rows, M.cols, t8)
+    assert np.array_equal(np.asarray(back.col), np.asarray(M.col))
+    n += 1
     multi = T.Context(devices=[0, 0, 0])
     A = W.rmat(scale=11, edge_factor=8)
     assert same(multi.spgemm(A, A).C, ctx.spgemm(A, A).C)
