@@ -251,10 +251,36 @@ def run_ours(args):
 
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
 
+    # general-row configs at N > 1: B's tile summary is split over the ranks
+    # (each summarises its row panel of B) and all-gathered, instead of every
+    # rank converting all of B (distributed.gather_b_summary; TSG_BSUM=0: off)
+    use_bsum = world > 1 and not chain and args.config in ("rmat", "rect") and \
+        os.environ.get("TSG_BSUM", "1") == "1"
+    if use_bsum:
+        bb0, bb1 = D.b_panel_bounds(Bs[0], world)[rank]
+        brp = np.asarray(Bs[0].row_ptr)
+        blo, bhi = int(brp[bb0]), int(brp[bb1])
+
+    def b_summary():
+        Bd = B_dev[0]
+        Bp = Csr(bb1 - bb0, Bd.cols, Bd.row_ptr[bb0:bb1 + 1] - blo, Bd.col[blo:bhi], Bd.val[blo:bhi])
+        part = ctx.b_summary(Bp)
+        full = D.gather_b_summary(part, dist, dev)
+        return part, full
+
     def one_step(stats=None):
         if world > 1:
             for _, flat in B_pack:
                 dist.broadcast(flat, src=0)
+        if use_bsum:
+            part, full = b_summary()
+            co = L.tsg_csr_out()
+            co.mem = L.TSG_MEM_DEVICE
+            rc = ctx.spgemm_bsum_raw(a_view, b_views[0], full, opts, co, stats)
+            part.free()
+            if rc != 0:
+                raise RuntimeError(ctx._lib.tsg_last_error(ctx.handle).decode())
+            return co
         if chain:
             import ctypes as C
             arr = (C.POINTER(L.tsg_csr) * 3)(C.pointer(a_view), C.pointer(b_views[0]), C.pointer(b_views[1]))
@@ -410,7 +436,8 @@ def run_ours(args):
         "data": "synthetic (deterministic generator, paper_2009_14600_b200/workloads.py)",
         "config": config_key(args.config, cb_total, Afull.nnz),
         "details": {"mode": args.mode,
-                    "parallelism": f"A tile-row panels x{world}, B broadcast" if world > 1 else "single GPU",
+                    "parallelism": (f"A tile-row panels x{world}, B broadcast"
+                                    + (" + B-summary all-gather" if use_bsum else "")) if world > 1 else "single GPU",
                     "l2": "flushed (256 MB write) before every timed step",
                     "values_at_boundary": "binary16 bits (TSG_F16) when exact, on the device and over PCIe",
                     "nnz_c": sd["nnz_c"], "tiles_a": sd["tiles_a"], "raw_pairs": sd["raw_pairs"],

@@ -35,7 +35,7 @@
 extern "C" {
 #endif
 
-#define TSG_ABI_VERSION 3
+#define TSG_ABI_VERSION 4
 
 /* Only the functions below are exported (the library builds with
  * -fvisibility=hidden). */
@@ -234,6 +234,46 @@ TSG_API int tsg_tiles8_to_csr(tsg_ctx* ctx, const tsg_tiles8* T, tsg_csr_out* C)
 TSG_API int tsg_csr_to_tiles8(tsg_ctx* ctx, const tsg_csr* C, tsg_tiles8_out* T);
 TSG_API void tsg_free_tiles8(tsg_tiles8_out* T);
 
+/* B's share of a general-row product, per row panel of B: the
+ * per-row and per-tile summaries the general path reads of B besides its CSR
+ * (the 16x16 tile structure behind the T = 16 pair counters, and the binary16
+ * values).  In an N-GPU run each GPU summarises its own panel of B rows and
+ * the panels are all-gathered -- concatenated in row order, array by array --
+ * instead of every GPU converting all of B.  Arrays are device memory on the
+ * context's device; tsg_bsum_create allocates them (tsg_bsum_free releases),
+ * a gathered summary passed to tsg_spgemm_bsum may live anywhere on that
+ * device (e.g. torch tensors).
+ *   njt        [rows]        distinct 16x16 tiles each row touches
+ *   tile_count [tile_rows]   tiles per 16-row tile row
+ *   rinfo      [tile_rows]   rows holding an entry (lo 16 bits) | 1 << 16
+ *                            when every tile occupies a single row
+ *   ro         [tiles]       row occupancy of each tile (tile-row order)
+ *   etile      [nnz]         per entry: its tile's rank in its tile row |
+ *                            0x80000000 unless first of its tile in its row;
+ *                            0xffffffff when the entry is dropped
+ *   h16        [nnz]         per entry: binary16 value (0 = dropped)       */
+typedef struct {
+  int64_t rows, tile_rows, tiles, nnz;
+  uint32_t* njt;
+  uint32_t* tile_count;
+  uint32_t* rinfo;
+  uint16_t* ro;
+  uint32_t* etile;
+  uint16_t* h16;
+  void* _owner;
+} tsg_bsum;
+
+/* Summary of a row panel of B given as its own CSR (row_ptr from 0; the
+ * panel's first row a multiple of 16 in B).  Validation and binary16
+ * rounding as tsg_spgemm's conversion (status 2 / 3). */
+TSG_API int tsg_bsum_create(tsg_ctx* ctx, const tsg_csr* Bpanel, tsg_bsum* out);
+TSG_API void tsg_bsum_free(tsg_ctx* ctx, tsg_bsum* s);
+/* C = A.B as tsg_spgemm, with B's summary given (all of B's rows).  Rows of A
+ * that take the general path read B only through Bsum and B's CSR; when A's
+ * rows are light the call converts B itself (as tsg_spgemm). */
+TSG_API int tsg_spgemm_bsum(tsg_ctx* ctx, const tsg_csr* A, const tsg_csr* B, const tsg_bsum* Bsum,
+                            tsg_csr_out* C, const tsg_options* opt, tsg_run_stats* stats);
+
 /* sum_k nnzA(:,k) * nnzB(k,:) on the device (analytics.cpp:51-65,
  * generalised to A != B): the GFLOPS denominator / 2. */
 TSG_API int tsg_cbar(tsg_ctx* ctx, const tsg_csr* A, const tsg_csr* B, uint64_t* cbar);
@@ -244,7 +284,8 @@ TSG_API uint64_t tsg_launch_count(const tsg_ctx* ctx);
 /* Device time (ms) of a phase ("convert", "task_list", "sort", "counting",
  * "multiply", "compaction", "total") or of a single kernel launch
  * ("numeric_kernel", "assemble_kernel") during the last call made with
- * phase_timing set -- CUDA events on the context's stream. */
+ * phase_timing set, or of the last tsg_bsum_create ("bsum") -- CUDA events
+ * on the context's stream. */
 TSG_API double tsg_last_kernel_ms(const tsg_ctx* ctx, const char* phase);
 
 #ifdef __cplusplus

@@ -46,6 +46,12 @@ class tsg_tiles8_out(C.Structure):
                 ("elem_index", C.c_void_p), ("val", C.c_void_p)]
 
 
+class tsg_bsum(C.Structure):
+    _fields_ = [("rows", C.c_int64), ("tile_rows", C.c_int64), ("tiles", C.c_int64), ("nnz", C.c_int64),
+                ("njt", C.c_void_p), ("tile_count", C.c_void_p), ("rinfo", C.c_void_p), ("ro", C.c_void_p),
+                ("etile", C.c_void_p), ("h16", C.c_void_p), ("_owner", C.c_void_p)]
+
+
 class tsg_options(C.Structure):
     _fields_ = [("mode", C.c_int32), ("drop_nonfinite", C.c_int32),
                 ("phase_timing", C.c_int32), ("want_tiles", C.c_int32)]
@@ -75,7 +81,8 @@ class tsg_run_stats(C.Structure):
 EXPORTS = ("tsg_default_options", "tsg_create", "tsg_destroy", "tsg_last_error", "tsg_abi_version",
            "tsg_spgemm", "tsg_spgemm_chain", "tsg_free_csr", "tsg_free_tiles", "tsg_cbar",
            "tsg_launch_count", "tsg_last_kernel_ms", "tsg_create_multi", "tsg_last_panel_ms",
-           "tsg_tiles8_to_csr", "tsg_csr_to_tiles8", "tsg_free_tiles8")
+           "tsg_tiles8_to_csr", "tsg_csr_to_tiles8", "tsg_free_tiles8",
+           "tsg_bsum_create", "tsg_bsum_free", "tsg_spgemm_bsum")
 
 _lib = None
 
@@ -128,6 +135,13 @@ def load() -> C.CDLL:
     lib.tsg_csr_to_tiles8.restype = C.c_int
     lib.tsg_free_tiles8.argtypes = [C.POINTER(tsg_tiles8_out)]
     lib.tsg_free_tiles8.restype = None
+    lib.tsg_bsum_create.argtypes = [P, C.POINTER(tsg_csr), C.POINTER(tsg_bsum)]
+    lib.tsg_bsum_create.restype = C.c_int
+    lib.tsg_bsum_free.argtypes = [P, C.POINTER(tsg_bsum)]
+    lib.tsg_bsum_free.restype = None
+    lib.tsg_spgemm_bsum.argtypes = [P, C.POINTER(tsg_csr), C.POINTER(tsg_csr), C.POINTER(tsg_bsum),
+                                    C.POINTER(tsg_csr_out), C.POINTER(tsg_options), C.POINTER(tsg_run_stats)]
+    lib.tsg_spgemm_bsum.restype = C.c_int
     lib.tsg_last_kernel_ms.argtypes = [P, C.c_char_p]
     lib.tsg_last_kernel_ms.restype = C.c_double
     _lib = lib

@@ -65,6 +65,7 @@ struct tsg_ctx {
   uint64_t launches = 0;
   double last_phase_ms[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   double last_numeric_kernel_ms = 0, last_assemble_kernel_ms = 0;
+  double last_bsum_ms = 0;  // device time of the last tsg_bsum_create
   // pipelined host output: a second stream for device->host slices, its events,
   // and pinned slots for the chunk ends
   cudaStream_t d2h = nullptr;
@@ -326,7 +327,6 @@ const uint32_t* convert(tsg_ctx* ctx, Scratch& sc, const CsrView& in, TileMat& T
   exclusive_sum(ctx, sc, cs.ntiles, T.trp, nr);
   T.tco = sc.alloc<uint2>(cap);
   T.rm2 = sc.alloc<uint32_t>(cap * 8);
-  T.trow = sc.alloc<uint32_t>(cap);
   for (int role = 0; role < 2; ++role) {
     if (!(roles & (1 << role))) continue;
     T.meta[role] = sc.alloc<uint2>(cap);
@@ -479,6 +479,9 @@ struct Call {
   // emitted arrays outlive this call and are listed in `keep`
   const TileMat* pre_a = nullptr;
   TileMat* emit_out = nullptr;
+  // B's summary (tsg_spgemm_bsum): the general path reads B through it and
+  // B's CSR; B is converted only if the rows turn out light
+  const tsg_bsum* bsum = nullptr;
   unsigned long long* emit_tot = nullptr;  // emit mode: P, S, raw accumulated by the numeric pass
   std::vector<void*>* keep = nullptr;
 
@@ -518,7 +521,7 @@ struct Call {
     counted_d = zblk + 1;
     work = sc.alloc<unsigned>(1);  // tile-row counter of the persistent numeric pass
     err_flag = dscal;
-    same = !pre_a && (Ain == Bin || (Ain->row_ptr == Bin->row_ptr && Ain->col == Bin->col &&
+    same = !pre_a && !bsum && (Ain == Bin || (Ain->row_ptr == Bin->row_ptr && Ain->col == Bin->col &&
                                      Ain->val == Bin->val && Ain->rows == Bin->rows && Ain->cols == Bin->cols &&
                                      Ain->mem == Bin->mem && Ain->dtype == Bin->dtype && Ain->nnz == Bin->nnz));
     const uint32_t* ntA_d;
@@ -526,7 +529,7 @@ struct Call {
     // conversion: only those are tiled (a row panel of A -- multi-GPU, or any
     // A that touches part of B -- converts its slice of B)
     uint8_t* needed = nullptr;
-    if (!same) {
+    if (!same && !bsum) {
       needed = sc.alloc<uint8_t>((Bin->rows + 15) / 16 + 1);
       TSG_CUDA(cudaMemsetAsync(needed, 0, (Bin->rows + 15) / 16 + 1, s));
     }
@@ -544,7 +547,9 @@ struct Call {
     }
     dB = same ? dA : stage(ctx, sc, Bin, st);
     const uint32_t* ntB_d = ntA_d;
-    if (!same)
+    if (bsum)
+      ntB_d = bsum_view();
+    else if (!same)
       ntB_d = convert(ctx, sc, dB, TB_own, 2, err_flag, opt.drop_nonfinite, needed, nullptr,
                       reinterpret_cast<uint32_t*>(zblk + 7), nullptr, general_flag());
     TB = same ? &TA : &TB_own;
@@ -577,6 +582,48 @@ struct Call {
     if (!owner->host) owner->p[0] = d_rp;
     rowcnt = sc.alloc<int64_t>(rows + 1);  // rowcnt[rows] = 0: written by the numeric kernels
     TSG_CUDA(cudaMemsetAsync(rowcnt + rows, 0, sizeof(int64_t), s));
+  }
+
+  // B as its summary: tile-row pointers from the tile counts, per-tile row
+  // occupancies, per-entry tile ranks and binary16 values (tsg_bsum); returns
+  // the device tile count
+  const uint32_t* bsum_view() {
+    const int64_t tr = (Bin->rows + 15) / 16;
+    if (bsum->rows != Bin->rows || bsum->nnz != Bin->nnz || bsum->tile_rows != tr)
+      throw Fail{TSG_ERR_DIMENSION, "B summary does not match B (rows " + std::to_string(bsum->rows) + ", nnz " +
+                                        std::to_string(bsum->nnz) + ", tile rows " + std::to_string(bsum->tile_rows) +
+                                        ")"};
+    if ((tr && (!bsum->tile_count || !bsum->rinfo || !bsum->njt)) ||
+        (bsum->nnz && (!bsum->etile || !bsum->h16)) || (bsum->tiles && !bsum->ro))
+      throw Fail{TSG_ERR_OTHER, "B summary arrays missing"};
+    TB_own = TileMat{};
+    TB_own.rows = Bin->rows;
+    TB_own.cols = Bin->cols;
+    TB_own.tile_rows = uint32_t(tr);
+    TB_own.tile_cols = uint32_t((Bin->cols + 15) / 16);
+    const uint64_t nr1 = uint64_t(tr) + 1;
+    auto* cnt = sc.alloc<uint32_t>(nr1);
+    if (tr) TSG_CUDA(cudaMemcpyAsync(cnt, bsum->tile_count, tr * sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
+    TSG_CUDA(cudaMemsetAsync(cnt + tr, 0, sizeof(uint32_t), s));
+    TB_own.trp = sc.alloc<uint32_t>(nr1);
+    exclusive_sum(ctx, sc, cnt, TB_own.trp, nr1);
+    TB_own.ro16 = bsum->ro;
+    TB_own.etile = bsum->etile;
+    TB_own.csr_rp = dB.row_ptr;
+    TB_own.h16 = bsum->h16;
+    return TB_own.trp + tr;
+  }
+
+  // B converted after all (a summary call whose rows are light)
+  void convert_b() {
+    const uint32_t* ntB_d = convert(ctx, sc, dB, TB_own, 2, err_flag, opt.drop_nonfinite, nullptr, nullptr,
+                                    reinterpret_cast<uint32_t*>(zblk + 7), nullptr, general_flag());
+    TB = &TB_own;
+    const unsigned* src[2] = {dscal, ntB_d};
+    unsigned v[2];
+    readback_many(ctx, src, v);
+    raise_flags(v[0]);
+    tB = v[1];
   }
 
   // realised row counts -> row_ptr; nnz(C) and counted elements to the host,
@@ -868,7 +915,6 @@ struct Call {
     const uint64_t S = std::max<uint64_t>(cap, 1);
     em.tco = sc.alloc<uint2>(S);
     em.rm2 = sc.alloc<uint32_t>(S * 8);
-    em.trow = sc.alloc<uint32_t>(S);
     em.meta = sc.alloc<uint2>(S);
     em.rec = sc.alloc<uint4>(S);
     em.chunk = kept(sc.alloc<uint4>(32 * S + 1, true));
@@ -896,7 +942,6 @@ struct Call {
     T.cap = cap;
     T.tco = kept(sc.alloc<uint2>(nt, true));
     T.rm2 = kept(sc.alloc<uint32_t>(nt * 8, true));
-    T.trow = kept(sc.alloc<uint32_t>(nt, true));
     T.meta[kRoleA] = kept(sc.alloc<uint2>(nt, true));
     T.rec[kRoleA] = kept(sc.alloc<uint4>(nt, true));
     T.chunk[kRoleA] = em.chunk;
@@ -1055,10 +1100,18 @@ struct Call {
     auto* wbase = sc.alloc<uint32_t>(nr);
     exclusive_sum(ctx, sc, nrec, rbase, nr);
     exclusive_sum(ctx, sc, nwk, wbase, nr);
-    auto* njt = sc.alloc<uint32_t>(uint64_t(B.rows) + 1);
-    auto* rinfo = sc.alloc<uint32_t>(uint64_t(B.tile_rows) + 1);
+    const uint32_t* njt = bsum ? bsum->njt : nullptr;
+    const uint32_t* rinfo = bsum ? bsum->rinfo : nullptr;
+    if (!bsum) {
+      auto* nj = sc.alloc<uint32_t>(uint64_t(B.rows) + 1);
+      auto* ri = sc.alloc<uint32_t>(uint64_t(B.tile_rows) + 1);
+      launch_esc_bsummary(B, nj, ri, s);
+      check_launch(ctx, 2);
+      njt = nj;
+      rinfo = ri;
+    }
     launch_esc_pairstats(TA, B, tA, njt, rinfo, tot + 2, s);
-    check_launch(ctx, 3);
+    check_launch(ctx);
     record(ctx, timing, 2);
     uint64_t nrecs = 0, nunits = 0, products = 0;
     // host output of a large product: the tile rows run in chunks whose CSR
@@ -1379,6 +1432,81 @@ void spgemm_impl(tsg_ctx* ctx, const tsg_csr* Ain, const tsg_csr* Bin, tsg_csr_o
     call.general_path();
   }
   call.finish(tiles);
+}
+
+// tsg_spgemm_bsum: A converted as usual, B through its summary; light rows
+// (the MMA pass reads B's operand tiles) convert B after all.
+void spgemm_bsum_impl(tsg_ctx* ctx, const tsg_csr* Ain, const tsg_csr* Bin, const tsg_bsum* bsum, tsg_csr_out* C,
+                      const tsg_options& opt, tsg_run_stats* st) {
+  if (!bsum) throw Fail{TSG_ERR_OTHER, "B summary is NULL"};
+  Call call(ctx, Ain, Bin, C, opt, st);
+  call.bsum = bsum;
+  call.convert_operands();
+  if (call.light) {
+    call.convert_b();
+    call.light_path();
+  } else {
+    call.general_path();
+  }
+  call.finish(nullptr);
+}
+
+// A panel of B -> its summary (tsg_bsum_create): B-role conversion with the
+// general flag raised (no operand chunks), then the per-row and per-tile-row
+// summaries; outputs outlive the call (pool allocations owned by the summary).
+void bsum_create_impl(tsg_ctx* ctx, const tsg_csr* Bp, tsg_bsum* out) {
+  check_csr(Bp, "B panel");
+  *out = tsg_bsum{};
+  TSG_CUDA(cudaEventRecord(ctx->kev[0], ctx->stream));
+  Scratch sc(ctx);
+  const CsrView dB = stage(ctx, sc, Bp, nullptr);
+  auto* z = sc.alloc<unsigned>(4);  // [0] error flags, [1] walk counter, [2] general flag
+  TSG_CUDA(cudaMemsetAsync(z, 0, 2 * sizeof(unsigned), ctx->stream));
+  const unsigned one = 1;
+  TSG_CUDA(cudaMemcpyAsync(z + 2, &one, sizeof(unsigned), cudaMemcpyHostToDevice, ctx->stream));
+  TileMat T;
+  const uint32_t* nt_d = convert(ctx, sc, dB, T, 2, z, 0, nullptr, nullptr, z + 1, nullptr, z + 2);
+  const unsigned* src[2] = {z, nt_d};
+  unsigned v[2];
+  readback_many(ctx, src, v);
+  raise_flags(v[0]);
+  const int64_t rows = Bp->rows, tr = (rows + 15) / 16, nnz = Bp->nnz, tiles = int64_t(v[1]);
+  auto* own = new std::vector<void*>();
+  auto keep = [&](size_t bytes) {
+    void* p = nullptr;
+    TSG_CUDA(cudaMallocFromPoolAsync(&p, std::max<size_t>(bytes, 4), ctx->pool, ctx->stream));
+    own->push_back(p);
+    return p;
+  };
+  try {
+    out->rows = rows;
+    out->tile_rows = tr;
+    out->tiles = tiles;
+    out->nnz = nnz;
+    out->njt = static_cast<uint32_t*>(keep((rows + 1) * 4));
+    out->tile_count = static_cast<uint32_t*>(keep((tr + 1) * 4));
+    out->rinfo = static_cast<uint32_t*>(keep((tr + 1) * 4));
+    out->ro = static_cast<uint16_t*>(keep(tiles * 2));
+    out->etile = static_cast<uint32_t*>(keep(nnz * 4));
+    out->h16 = static_cast<uint16_t*>(keep(nnz * 2));
+    out->_owner = own;
+    launch_esc_bsummary(T, out->njt, out->rinfo, ctx->stream);
+    launch_bsum_tiles(T, uint64_t(tiles), out->tile_count, out->ro, ctx->stream);
+    check_launch(ctx, 3);
+    if (nnz) {
+      TSG_CUDA(cudaMemcpyAsync(out->etile, T.etile, nnz * 4, cudaMemcpyDeviceToDevice, ctx->stream));
+      TSG_CUDA(cudaMemcpyAsync(out->h16, T.h16, nnz * 2, cudaMemcpyDeviceToDevice, ctx->stream));
+    }
+    TSG_CUDA(cudaEventRecord(ctx->kev[1], ctx->stream));
+    TSG_CUDA(cudaStreamSynchronize(ctx->stream));
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, ctx->kev[0], ctx->kev[1]) == cudaSuccess) ctx->last_bsum_ms = ms;
+  } catch (...) {
+    for (void* p : *own) cudaFreeAsync(p, ctx->stream);
+    delete own;
+    *out = tsg_bsum{};
+    throw;
+  }
 }
 
 // One stage of a chain (tsg_spgemm_chain).  `pre_a`: A as the previous
@@ -1917,6 +2045,65 @@ int tsg_spgemm(tsg_ctx* ctx, const tsg_csr* A, const tsg_csr* B, tsg_csr_out* C,
   }
 }
 
+int tsg_bsum_create(tsg_ctx* ctx, const tsg_csr* Bpanel, tsg_bsum* out) {
+  if (!ctx || !out) return TSG_ERR_OTHER;
+  ctx->err.clear();
+  if (!ctx->sub.empty()) {
+    ctx->err = "B summaries are per device: use a single-device context";
+    return TSG_ERR_OTHER;
+  }
+  try {
+    TSG_CUDA(cudaSetDevice(ctx->device));
+    bsum_create_impl(ctx, Bpanel, out);
+    return TSG_OK;
+  } catch (const Fail& f) {
+    ctx->err = f.msg;
+    cudaStreamSynchronize(ctx->stream);
+    return f.code;
+  } catch (const std::exception& e) {
+    ctx->err = e.what();
+    return TSG_ERR_OTHER;
+  }
+}
+
+void tsg_bsum_free(tsg_ctx* ctx, tsg_bsum* s) {
+  if (!ctx || !s || !s->_owner) return;
+  auto* own = static_cast<std::vector<void*>*>(s->_owner);
+  cudaSetDevice(ctx->device);
+  for (void* p : *own) cudaFreeAsync(p, ctx->stream);
+  cudaStreamSynchronize(ctx->stream);
+  delete own;
+  *s = tsg_bsum{};
+}
+
+int tsg_spgemm_bsum(tsg_ctx* ctx, const tsg_csr* A, const tsg_csr* B, const tsg_bsum* Bsum, tsg_csr_out* C,
+                    const tsg_options* opt, tsg_run_stats* stats) {
+  if (!ctx) return TSG_ERR_OTHER;
+  tsg_options o;
+  tsg_default_options(&o);
+  if (opt) o = *opt;
+  o.want_tiles = 0;
+  ctx->err.clear();
+  if (C) C->_owner = nullptr;
+  if (!ctx->sub.empty()) {
+    ctx->err = "tsg_spgemm_bsum runs one GPU's panel: use a single-device context";
+    return TSG_ERR_OTHER;
+  }
+  try {
+    TSG_CUDA(cudaSetDevice(ctx->device));
+    spgemm_bsum_impl(ctx, A, B, Bsum, C, o, stats);
+    return TSG_OK;
+  } catch (const Fail& f) {
+    ctx->err = f.msg;
+    cudaStreamSynchronize(ctx->stream);
+    if (C && C->_owner) free_out(ctx, C);
+    return f.code;
+  } catch (const std::exception& e) {
+    ctx->err = e.what();
+    return TSG_ERR_OTHER;
+  }
+}
+
 int tsg_spgemm_chain(tsg_ctx* ctx, int n, const tsg_csr* const* X, tsg_csr_out* C,
                      const tsg_options* opt, tsg_run_stats* stats) {
   if (!ctx) return TSG_ERR_OTHER;
@@ -2242,6 +2429,7 @@ double tsg_last_kernel_ms(const tsg_ctx* ctx, const char* phase) {
   if (!ctx->sub.empty()) return tsg_last_kernel_ms(ctx->sub[0], phase);
   if (std::strcmp(phase, "numeric_kernel") == 0) return ctx->last_numeric_kernel_ms;
   if (std::strcmp(phase, "assemble_kernel") == 0) return ctx->last_assemble_kernel_ms;
+  if (std::strcmp(phase, "bsum") == 0) return ctx->last_bsum_ms;
   static const char* names[] = {"", "convert", "task_list", "sort", "counting", "multiply",
                                 "compaction", "total"};
   for (int i = 1; i < 8; ++i)

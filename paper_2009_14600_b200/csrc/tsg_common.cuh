@@ -13,7 +13,6 @@
 //                           masks: word g = row g | row g+8 << 16 (bit c of
 //                           row r <=> slot (r,c) nonzero; reference bit 8r+c,
 //                           tile_format.hpp:20-23)
-//   trow  u32[T]            tile row of each tile (the general path's sort key)
 //   meta  uint2[T]  (per operand role)  {lane mask, first chunk}
 //   chunk uint4[]   (per operand role)  16-byte lane chunks, chunk 0 = zeros
 //   rec   uint4[T]  (per operand role)  {lane mask, first chunk, occupancy, tile col}
@@ -47,7 +46,6 @@ struct TileMat {
   uint32_t* trp = nullptr;
   uint2* tco = nullptr;
   uint32_t* rm2 = nullptr;
-  uint32_t* trow = nullptr;  // [T] tile row of each tile
   // (B-role conversions) per input CSR entry: its tile's rank within its
   // tile row (add trp[tile row]), | kDupEntry unless it
   // is the first kept entry of that tile in its row, kNoTile if dropped; and
@@ -57,6 +55,8 @@ struct TileMat {
   // per input CSR entry: its rounded binary16 value (0 when dropped) -- the
   // general path multiplies straight from the CSR
   uint16_t* h16 = nullptr;
+  // (a B summary, tsg_bsum) per tile: its row occupancy, in place of tco
+  const uint16_t* ro16 = nullptr;
   uint2* meta[2] = {nullptr, nullptr};
   uint4* rec[2] = {nullptr, nullptr};  // {lane mask, first chunk, occupancy, tile column}: one gather per tile
   uint4* chunk[2] = {nullptr, nullptr};

@@ -135,6 +135,9 @@ struct Gapped {
 
 constexpr uint32_t kLightMax = 128;  // the light path's largest tile row (tsg_api.cu decide())
 
+// the role whose records a lite (general-call) conversion writes and the compaction reads
+__device__ __forceinline__ int lite_role(int roles) { return (roles & 1) ? 0 : 1; }
+
 __device__ __forceinline__ void mark_column(const Gapped& out, uint32_t J) {
   if (out.mark && !out.mark[J]) out.mark[J] = 1;  // most tiles share their column's flag: skip the store
 }
@@ -350,10 +353,8 @@ __device__ __forceinline__ uint32_t sparse_panel(FastSmem& sm, const Gapped& out
       }
       const uint32_t occ = (colocc & 0xffffu) | (rowocc << 16);
       mark_column(out, J);
-      if (lite) {  // the general path reads only the tile column and occupancy
-#pragma unroll
-        for (int role = 0; role < 2; ++role)
-          if (roles & (1 << role)) out.rec[role][E0 + t] = make_uint4(0u, 0u, occ, J);
+      if (lite) {  // the general path reads only the tile column and occupancy (compaction: one role)
+        out.rec[lite_role(roles)][E0 + t] = make_uint4(0u, 0u, occ, J);
         continue;
       }
       uint4* dst = reinterpret_cast<uint4*>(out.rm2 + size_t(E0 + t) * 8);
@@ -689,8 +690,12 @@ __global__ void __launch_bounds__(256, TSG_CONV_MINB) convert_fast_kernel(CsrVie
       dst[1] = m1;
     }
     mark_column(out, J);
-    if (roles & 1) out.rec[kRoleA][E0 + k] = make_uint4(sm.lm[k][0], cbA[h], occ, J);
-    if (roles & 2) out.rec[kRoleB][E0 + k] = make_uint4(sm.lm[k][1], cbB[h], occ, J);
+    if (lite) {
+      out.rec[lite_role(roles)][E0 + k] = make_uint4(0u, 0u, occ, J);
+    } else {
+      if (roles & 1) out.rec[kRoleA][E0 + k] = make_uint4(sm.lm[k][0], cbA[h], occ, J);
+      if (roles & 2) out.rec[kRoleB][E0 + k] = make_uint4(sm.lm[k][1], cbB[h], occ, J);
+    }
     sm.cl[k][0] = make_uint2(cbA[h], sm.lm[k][0]);
     sm.cl[k][1] = make_uint2(cbB[h], sm.lm[k][1]);
   }
@@ -845,7 +850,7 @@ __global__ void __launch_bounds__(256) convert_walk_kernel(CsrView in, Gapped ou
       for (int role = 0; role < 2; ++role) {
         if (!(roles & (1 << role))) continue;
         if (lite) {
-          if (lane == 0) out.rec[role][t] = make_uint4(0u, 0u, occ, J);
+          if (lane == 0 && role == lite_role(roles)) out.rec[role][t] = make_uint4(0u, 0u, occ, J);
           continue;
         }
         uint32_t rg[4];
@@ -1022,9 +1027,7 @@ __global__ void __launch_bounds__(kHubThreads) convert_hub_kernel(CsrView in, Ga
         const uint32_t J = jlo + w * 32u + uint32_t(__ffs(word) - 1);
         const uint32_t o = sm.occ[t];
         mark_column(out, J);
-#pragma unroll
-        for (int role = 0; role < 2; ++role)
-          if (roles & (1 << role)) out.rec[role][E0 + t] = make_uint4(0u, 0u, o, J);
+        out.rec[lite_role(roles)][E0 + t] = make_uint4(0u, 0u, o, J);
       }
     }
     const unsigned e_or = __reduce_or_sync(kFull, err);
@@ -1049,12 +1052,11 @@ __global__ void __launch_bounds__(256) tiles_compact_kernel(CsrView in, uint32_t
   }
   if (I >= tile_rows) return;
   const uint32_t src = uint32_t(in.row_ptr[int64_t(I) * kTile]), dst = T.trp[I], n = g.ntiles[I];
-  const int r0 = (roles & 1) ? 0 : 1;
+  const int r0 = lite_role(roles);
   const bool lite = g.general && *g.general;  // final here: the conversion kernels are done
   for (uint32_t i = lane; i < n; i += 32) {
     const uint4 rec0 = g.rec[r0][src + i];
     T.tco[dst + i] = make_uint2(rec0.w, rec0.z);
-    T.trow[dst + i] = I;
     if (lite) continue;
 #pragma unroll
     for (int role = 0; role < 2; ++role) {

@@ -1228,6 +1228,11 @@ constexpr uint32_t kPairBits = 8192;  // tile ranks of a B tile row the pair-sta
 // Warp per tile row.
 constexpr uint32_t kSingleRows = 1u << 16;
 
+// row occupancy of B's tile b (a converted B's tco, or a B summary's ro)
+__device__ __forceinline__ uint32_t tile_ro(const TileMat& B, uint32_t b) {
+  return B.ro16 ? uint32_t(__ldg(B.ro16 + b)) : __ldg(&B.tco[b].y) >> 16;
+}
+
 __global__ void __launch_bounds__(256) esc_brow_bits_kernel(TileMat B, uint32_t* __restrict__ rinfo) {
   const int lane = threadIdx.x & 31;
   const uint32_t k = blockIdx.x * 8 + (threadIdx.x >> 5);
@@ -1236,7 +1241,7 @@ __global__ void __launch_bounds__(256) esc_brow_bits_kernel(TileMat B, uint32_t*
   uint32_t rows = 0;
   bool one = true;
   for (uint32_t b = b0 + lane; b < b1; b += 32) {
-    const uint32_t ro = __ldg(&B.tco[b].y) >> 16;
+    const uint32_t ro = tile_ro(B, b);
     one &= __popc(ro) == 1;
     rows |= ro;
   }
@@ -1279,7 +1284,7 @@ __device__ __forceinline__ uint32_t meets_count(const TileMat& B, uint32_t k, ui
     for (uint32_t i = lane; i < (len + 31) / 32; i += 32) n += __popc(bm[i]);
     __syncwarp();
   } else {
-    for (uint32_t b = b0 + lane; b < b1; b += 32) n += ((__ldg(&B.tco[b].y) >> 16) & c) != 0u;
+    for (uint32_t b = b0 + lane; b < b1; b += 32) n += (tile_ro(B, b) & c) != 0u;
   }
   return __reduce_add_sync(kFull, n);
 }
@@ -1334,6 +1339,16 @@ __global__ void __launch_bounds__(256) esc_pairstats_kernel(TileMat A, TileMat B
     if (raw) atomicAdd(out, raw);
     if (filt) atomicAdd(out + 1, filt);
   }
+}
+
+// A converted panel's tile counts per tile row and row occupancy per tile (tsg_bsum)
+__global__ void bsum_tiles_kernel(TileMat B, uint64_t tiles, uint32_t* __restrict__ tile_count,
+                                  uint16_t* __restrict__ ro) {
+  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < tiles; i += stride)
+    ro[i] = uint16_t(__ldg(&B.tco[i].y) >> 16);
+  for (uint64_t k = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; k < B.tile_rows; k += stride)
+    tile_count[k] = B.trp[k + 1] - B.trp[k];
 }
 
 // ---------------------------------------------------------------- chained A
@@ -1465,11 +1480,19 @@ void launch_esc_copy(const EscArgs& g, const int64_t* row_ptr, int32_t* col, flo
   esc_copy_kernel<<<148 * 16, 256, 0, st>>>(g.nrec, g.piece_top, g.pool_cap, g.pieces, g.stage, row_ptr, col, val);
 }
 
-void launch_esc_pairstats(const TileMat& A, const TileMat& B, uint64_t tA, uint32_t* njt, uint32_t* rinfo,
-                          unsigned long long* out, cudaStream_t st) {
+void launch_esc_bsummary(const TileMat& B, uint32_t* njt, uint32_t* rinfo, cudaStream_t st) {
   if (B.rows > 0) esc_njt_kernel<<<2368, 256, 0, st>>>(B.rows, B.csr_rp, B.etile, njt);
   if (B.tile_rows > 0) esc_brow_bits_kernel<<<(B.tile_rows + 7) / 8, 256, 0, st>>>(B, rinfo);
+}
+
+void launch_esc_pairstats(const TileMat& A, const TileMat& B, uint64_t tA, const uint32_t* njt, const uint32_t* rinfo,
+                          unsigned long long* out, cudaStream_t st) {
   if (tA > 0) esc_pairstats_kernel<<<unsigned((tA + 255) / 256), 256, 0, st>>>(A, B, uint32_t(tA), njt, rinfo, out);
+}
+
+void launch_bsum_tiles(const TileMat& B, uint64_t tiles, uint32_t* tile_count, uint16_t* ro, cudaStream_t st) {
+  if (tiles == 0 && B.tile_rows == 0) return;
+  bsum_tiles_kernel<<<1184, 256, 0, st>>>(B, tiles, tile_count, ro);
 }
 
 void launch_tiles_rowcount(const TileMat& A, int64_t* rowcnt, cudaStream_t st) {

@@ -61,7 +61,6 @@ void launch_panel_count(const TileMat& A, const TileMat& B, int64_t rows, uint32
 struct TileEmit {
   uint2* tco = nullptr;
   uint32_t* rm2 = nullptr;
-  uint32_t* trow = nullptr;
   uint2* meta = nullptr;
   uint4* rec = nullptr;
   uint4* chunk = nullptr;  // chunk 0 = zeros; tile row I's chunks from 1 + 32 * tile_base[I]
@@ -157,8 +156,11 @@ void launch_esc_copy(const EscArgs& g, const int64_t* row_ptr, int32_t* col, flo
 void launch_esc_copy_records(const EscArgs& g, uint32_t rec0, uint32_t rec1, const int64_t* row_ptr, int32_t* col,
                              float* val, cudaStream_t st);
 // njt: B rows + 1; nx: 16 per B tile row; single: one per B tile row (scratch)
-void launch_esc_pairstats(const TileMat& A, const TileMat& B, uint64_t tA, uint32_t* njt, uint32_t* rinfo,
+// B's per-row / per-tile-row summaries (njt, rinfo) from a converted B
+void launch_esc_bsummary(const TileMat& B, uint32_t* njt, uint32_t* rinfo, cudaStream_t st);
+void launch_esc_pairstats(const TileMat& A, const TileMat& B, uint64_t tA, const uint32_t* njt, const uint32_t* rinfo,
                           unsigned long long* out, cudaStream_t st);
+void launch_bsum_tiles(const TileMat& B, uint64_t tiles, uint32_t* tile_count, uint16_t* ro, cudaStream_t st);
 // 8x8 tiles of the reference's TiledMatrix (tsg_tiles8.cu): device arrays
 struct Tiles8View {
   const uint32_t* tile_col = nullptr;

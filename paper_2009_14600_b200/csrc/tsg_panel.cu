@@ -249,7 +249,6 @@ __device__ __forceinline__ void emit_tile(const float (&acc)[2][4], uint32_t J, 
   if (lane == 0) {
     const uint32_t occ = colocc | (rowocc << 16);
     em.tco[t] = make_uint2(J, occ);
-    em.trow[t] = I;
     em.meta[t] = make_uint2(lm, cb);
     em.rec[t] = make_uint4(lm, cb, occ, J);
   }
@@ -596,7 +595,6 @@ __global__ void emit_compact_kernel(uint32_t tile_rows, TileEmit em, const uint3
   const uint32_t src = em.tile_base[I], dst = trp[I], n = em.rtiles[I];
   for (uint32_t i = lane; i < n; i += 32) {
     T.tco[dst + i] = em.tco[src + i];
-    T.trow[dst + i] = em.trow[src + i];
     T.meta[kRoleA][dst + i] = em.meta[src + i];
     T.rec[kRoleA][dst + i] = em.rec[src + i];
   }

@@ -14,6 +14,13 @@ shards with exactly one exchange step:
     concatenation is byte-identical to the single-GPU result for any N.
 
 Each rank then runs the single-GPU C-ABI path on (A panel, B).
+
+General rows (R-MAT, the rectangular product) read B through its CSR plus a
+B summary (tsg_bsum: per-row / per-tile-row / per-tile / per-entry arrays of
+B's 16x16 tiling).  Rather than every rank converting all of B, rank p
+summarises its own row panel of B (b_panel_bounds) and the panels are
+all-gathered into the summary of B (gather_b_summary): the conversion work is
+split N ways and the exchange is one all-gather of ~6 bytes per entry.
 """
 from __future__ import annotations
 
@@ -104,3 +111,60 @@ def assemble(panels: list[Csr], cols: int) -> Csr:
     rows = sum(P.rows for P in panels)
     return Csr(rows, cols, np.concatenate(rps), np.concatenate(colsl) if colsl else np.zeros(0, np.int32),
                np.concatenate(vals) if vals else np.zeros(0, np.float32))
+
+
+def b_panel_bounds(B: Csr, world: int, tile: int = 16) -> list[tuple[int, int]]:
+    """Tile-row aligned [r0, r1) row ranges of B, one per rank, of ~equal nnz
+    (each rank summarises one, gather_b_summary)."""
+    rp = np.asarray(B.row_ptr, dtype=np.int64)
+    n_tr = (B.rows + tile - 1) // tile
+    cum = rp[np.minimum(np.arange(n_tr + 1) * tile, B.rows)]
+    cuts = [0] + [int(np.searchsorted(cum, cum[-1] * r / world, side="left")) for r in range(1, world)] + [n_tr]
+    cuts = np.maximum.accumulate(np.clip(cuts, 0, n_tr))
+    return [(min(int(cuts[i]) * tile, B.rows), min(int(cuts[i + 1]) * tile, B.rows)) for i in range(world)]
+
+
+def gather_b_summary(part, dist, device):
+    """All-gather every rank's B-panel summary (tilemul.BSummary) and
+    concatenate them in rank (= row) order: one collective on a flat byte
+    buffer per rank (its six arrays back to back, padded to the largest)."""
+    import torch
+    from .tilemul import BSUM_ARRAYS, BSummary
+    world = dist.get_world_size()
+    dims = torch.tensor([part.rows, part.tile_rows, part.tiles, part.nnz], dtype=torch.int64, device=device)
+    all_dims = [torch.zeros_like(dims) for _ in range(world)]
+    dist.all_gather(all_dims, dims)
+    all_dims = [[int(x) for x in d.tolist()] for d in all_dims]
+    field = {"rows": 0, "tile_rows": 1, "tiles": 2, "nnz": 3}
+
+    def layout(d):  # byte offsets of the arrays of a rank with dims d
+        offs, o = [], 0
+        for _, dim, ts in BSUM_ARRAYS:
+            n = d[field[dim]] * (4 if ts == "<i4" else 2)
+            offs.append((o, n))
+            o += (n + 15) // 16 * 16
+        return offs, o
+
+    sizes = [layout(d)[1] for d in all_dims]
+    maxb = max(max(sizes), 16)
+    offs, _ = layout(all_dims[dist.get_rank()])
+    flat = torch.zeros(maxb, dtype=torch.uint8, device=device)
+    for (name, _, _), (o, n) in zip(BSUM_ARRAYS, offs):
+        if n:
+            flat[o:o + n].copy_(part.arrays[name].contiguous().view(torch.uint8))
+    out = torch.empty(world * maxb, dtype=torch.uint8, device=device)
+    if flat.is_cuda and dist.get_backend() == "nccl":
+        dist.all_gather_into_tensor(out, flat)
+    else:  # gloo (CPU tests, shared-GPU runs): staged through host memory
+        host = torch.empty(world * maxb, dtype=torch.uint8)
+        dist.all_gather(list(host.view(world, maxb)), flat.cpu())
+        out.copy_(host)
+    parts = []
+    for r, d in enumerate(all_dims):
+        ro, _ = layout(d)
+        base = r * maxb
+        arrays = {}
+        for (name, _, ts), (o, n) in zip(BSUM_ARRAYS, ro):
+            arrays[name] = out[base + o:base + o + n].view(torch.int32 if ts == "<i4" else torch.int16)
+        parts.append(BSummary(d[0], d[1], d[2], d[3], arrays))
+    return BSummary.concat(parts)

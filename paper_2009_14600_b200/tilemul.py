@@ -224,6 +224,43 @@ class Context:
             self._lib.tsg_free_tiles(C.byref(to))
         return res
 
+    def b_summary(self, B: Csr) -> "BSummary":
+        """B's share of a general-row product for a row panel of B (its own
+        CSR, row_ptr from 0, first row a multiple of 16 in B): tsg_bsum_create.
+        The arrays are device tensors on this context's GPU."""
+        keep: list = []
+        b = _view(B, keep)
+        s = L.tsg_bsum()
+        rc = self._lib.tsg_bsum_create(self._h, C.byref(b), C.byref(s))
+        if rc != L.TSG_OK:
+            self._raise(rc)
+        return BSummary.from_struct(s, self)
+
+    def spgemm_bsum(self, A: Csr, B: Csr, bsum: "BSummary", *, mode: str = "tensor", out: str = "host",
+                    phase_timing: bool = False, drop_nonfinite: bool = False) -> Result:
+        """C = A.B with B's summary given (tsg_spgemm_bsum), e.g. gathered
+        from every rank's panel (distributed.gather_b_summary)."""
+        keep: list = []
+        a = _view(A, keep)
+        b = _view(B, keep)
+        sv = bsum.struct()
+        o = self._opts(mode, phase_timing, False, drop_nonfinite)
+        co = L.tsg_csr_out()
+        co.mem = L.TSG_MEM_DEVICE if out == "device" else L.TSG_MEM_HOST
+        st = L.tsg_run_stats()
+        rc = self._lib.tsg_spgemm_bsum(self._h, C.byref(a), C.byref(b), C.byref(sv), C.byref(co), C.byref(o),
+                                       C.byref(st))
+        if rc != L.TSG_OK:
+            self._raise(rc)
+        return Result(self._collect(co, out == "device"), st.as_dict())
+
+    def spgemm_bsum_raw(self, a: L.tsg_csr, b: L.tsg_csr, bsum: "BSummary", o: L.tsg_options,
+                        co: L.tsg_csr_out, st: L.tsg_run_stats | None = None) -> int:
+        """tsg_spgemm_bsum without wrapping (benchmarking; caller frees `co`)."""
+        sv = bsum.struct()
+        return self._lib.tsg_spgemm_bsum(self._h, C.byref(a), C.byref(b), C.byref(sv), C.byref(co), C.byref(o),
+                                         C.byref(st) if st is not None else None)
+
     def spgemm_raw(self, a: L.tsg_csr, b: L.tsg_csr, o: L.tsg_options, co: L.tsg_csr_out,
                    st: L.tsg_run_stats | None = None) -> int:
         """Zero-overhead call for benchmarking (caller frees `co`)."""
@@ -301,6 +338,59 @@ class Context:
         buf = (C.c_double * max(1, self.n_panels))()
         k = self._lib.tsg_last_panel_ms(self._h, buf, self.n_panels)
         return [float(buf[i]) for i in range(k)]
+
+
+# (array, its length field, element typestr): the tsg_bsum arrays (u32 / u16 carried as i4 / i2)
+BSUM_ARRAYS = (("njt", "rows", "<i4"), ("tile_count", "tile_rows", "<i4"), ("rinfo", "tile_rows", "<i4"),
+               ("ro", "tiles", "<i2"), ("etile", "nnz", "<i4"), ("h16", "nnz", "<i2"))
+
+
+class BSummary:
+    """A B summary (tsg_bsum) as device tensors: one row panel's (library
+    owned until free()) or the row-order concatenation of several panels'."""
+
+    def __init__(self, rows: int, tile_rows: int, tiles: int, nnz: int, arrays: dict, owner=None):
+        self.rows, self.tile_rows, self.tiles, self.nnz = rows, tile_rows, tiles, nnz
+        self.arrays = arrays
+        self._owner = owner  # (context, tsg_bsum) of a library-owned summary
+
+    @classmethod
+    def from_struct(cls, s: L.tsg_bsum, ctx: "Context") -> "BSummary":
+        import torch
+        dims = {"rows": s.rows, "tile_rows": s.tile_rows, "tiles": s.tiles, "nnz": s.nnz}
+        arrays = {}
+        for name, dim, ts in BSUM_ARRAYS:
+            n = int(dims[dim])
+            arrays[name] = torch.as_tensor(_CAI(getattr(s, name), n, ts), device="cuda") if n else \
+                torch.zeros(0, dtype=torch.int32 if ts == "<i4" else torch.int16, device="cuda")
+        return cls(int(s.rows), int(s.tile_rows), int(s.tiles), int(s.nnz), arrays, owner=(ctx, s))
+
+    @classmethod
+    def concat(cls, parts: list) -> "BSummary":
+        """Panels in row order -> the summary of all their rows (every array
+        is per row, per tile row, per tile or per entry, in that order)."""
+        import torch
+        arrays = {name: torch.cat([p.arrays[name] for p in parts]) for name, _, _ in BSUM_ARRAYS}
+        return cls(sum(p.rows for p in parts), sum(p.tile_rows for p in parts), sum(p.tiles for p in parts),
+                   sum(p.nnz for p in parts), arrays)
+
+    def struct(self) -> L.tsg_bsum:
+        s = L.tsg_bsum()
+        s.rows, s.tile_rows, s.tiles, s.nnz = self.rows, self.tile_rows, self.tiles, self.nnz
+        for name, _, _ in BSUM_ARRAYS:
+            t = self.arrays[name]
+            setattr(s, name, t.data_ptr() if t.numel() else None)
+        return s
+
+    def nbytes(self) -> int:
+        return sum(t.numel() * t.element_size() for t in self.arrays.values())
+
+    def free(self):
+        if self._owner is not None:
+            ctx, s = self._owner
+            self.arrays = {}
+            ctx._lib.tsg_bsum_free(ctx.handle, C.byref(s))
+            self._owner = None
 
 
 class _CAI:

@@ -89,3 +89,47 @@ def quadrants(tiles) -> tuple[np.ndarray, np.ndarray, np.ndarray]:
     rows, cols, bms = np.concatenate(rows), np.concatenate(cols), np.concatenate(bms)
     order = np.lexsort((cols, rows))
     return rows[order], cols[order], bms[order]
+
+
+def bsum_reference(M) -> dict:
+    """numpy restatement of tsg_bsum for a CSR whose values are binary16
+    (tsparse_b200.h): per row the distinct 16-column tiles it touches, per
+    16-row tile row its tile count and occupied rows (| 1 << 16 when every
+    tile occupies one row), per tile (tile row, then column order) its row
+    occupancy, per entry its tile's rank in the tile row (| 0x80000000 unless
+    the first of that tile in its row) and its binary16 bits."""
+    rp = np.asarray(M.row_ptr, np.int64)
+    col = np.asarray(M.col, np.int64)
+    h16 = np.asarray(M.val, np.float64).astype(np.float16).view(np.uint16)
+    rows = M.rows
+    tr = (rows + 15) // 16
+    row_of = np.repeat(np.arange(rows, dtype=np.int64), np.diff(rp))
+    kept = (h16 & 0x7FFF) != 0
+    J = col >> 4
+    T = row_of >> 4
+    # tiles: distinct (tile row, J) among kept entries, sorted
+    key = T[kept] * (1 << 32) + J[kept]
+    tiles, inv = np.unique(key, return_inverse=True)
+    tile_T = tiles >> 32
+    tile_count = np.bincount(tile_T, minlength=tr).astype(np.uint32)
+    first = np.concatenate([[0], np.cumsum(tile_count)])[:-1]
+    rank = np.arange(len(tiles), dtype=np.int64) - first[tile_T]
+    ro = np.zeros(len(tiles), np.int64)
+    np.bitwise_or.at(ro, inv, 1 << (row_of[kept] & 15))
+    rinfo = np.zeros(tr, np.int64)
+    np.bitwise_or.at(rinfo, tile_T, ro)
+    single = np.ones(tr, bool)
+    multi = np.array([bin(int(x)).count("1") > 1 for x in ro], bool)
+    single[np.unique(tile_T[multi])] = False
+    rinfo = rinfo | np.where(single, 1 << 16, 0)
+    etile = np.full(len(col), 0xFFFFFFFF, np.uint64)
+    et = rank[inv].astype(np.uint64)
+    # dup: not the first kept entry of its (row, tile)
+    kr, kj = row_of[kept], J[kept]
+    dup = np.zeros(len(kr), bool)
+    dup[1:] = (kr[1:] == kr[:-1]) & (kj[1:] == kj[:-1])
+    etile[kept] = et | np.where(dup, 0x80000000, 0).astype(np.uint64)
+    njt = np.bincount(kr[~dup], minlength=rows).astype(np.uint32)
+    return {"njt": njt, "tile_count": tile_count, "rinfo": rinfo.astype(np.uint32), "ro": ro.astype(np.uint16),
+            "etile": etile.astype(np.uint32), "h16": np.where(kept, h16, 0).astype(np.uint16),
+            "dims": (rows, tr, len(tiles), len(col))}

@@ -28,7 +28,7 @@ def test_library_exports_every_symbol():
     lib = L.load()
     for name in declared():
         assert hasattr(lib, name), name
-    assert lib.tsg_abi_version() == 3
+    assert lib.tsg_abi_version() == 4
 
 
 def test_library_has_no_cpu_fallback_symbols():
@@ -42,7 +42,7 @@ def test_library_has_no_cpu_fallback_symbols():
 def test_struct_layouts_match_header():
     structs = {"tsg_csr": L.tsg_csr, "tsg_csr_out": L.tsg_csr_out, "tsg_tiles_out": L.tsg_tiles_out,
                "tsg_options": L.tsg_options, "tsg_run_stats": L.tsg_run_stats, "tsg_tiles8": L.tsg_tiles8,
-               "tsg_tiles8_out": L.tsg_tiles8_out}
+               "tsg_tiles8_out": L.tsg_tiles8_out, "tsg_bsum": L.tsg_bsum}
     prog = ["#include <stdio.h>", "#include <stddef.h>", f'#include "{HEADER}"', "int main(void){"]
     for s, cls in structs.items():
         prog.append(f'printf("{s} %zu\\n", sizeof({s}));')

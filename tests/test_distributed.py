@@ -76,3 +76,52 @@ def test_panel_bounds_balance_skewed_rows():
     per = [int(work[r0:r1].sum()) for r0, r1 in b]
     assert b[0][0] == 0 and b[-1][1] == A.rows
     assert max(per) <= 1.5 * (sum(per) / 4) + int(work.max()) * 16
+
+
+def _bsum_worker(rank, world, port_no, name, q):
+    import torch
+    import torch.distributed as dist
+    from paper_2009_14600_b200.tilemul import BSUM_ARRAYS, BSummary
+    from tests.helpers import bsum_reference
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port_no))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        mats = W.make_small(name)
+        B = mats[1] if len(mats) > 1 else mats[0]
+        bounds = D.b_panel_bounds(B, world)
+        r0, r1 = bounds[rank]
+        ref = bsum_reference(D.take_rows(B, r0, r1))
+        arrays = {n: torch.from_numpy(np.ascontiguousarray(ref[n]).view(np.int32 if ts == "<i4" else np.int16))
+                  for n, _, ts in BSUM_ARRAYS}
+        full = D.gather_b_summary(BSummary(*ref["dims"], arrays), dist, "cpu")
+        q.put((rank, bounds, (full.rows, full.tile_rows, full.tiles, full.nnz),
+               {n: full.arrays[n].numpy().copy() for n, _, _ in BSUM_ARRAYS}))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("name", ["rect", "rmat"])
+def test_b_summary_all_gather_equals_whole_b(name):
+    """Every rank summarises its row panel of B; the all-gathered panels are the
+    summary of all of B (tsg_bsum, tests/helpers.bsum_reference)."""
+    from tests.helpers import bsum_reference
+    world = 3
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port_no = _free_port()
+    procs = [ctx.Process(target=_bsum_worker, args=(r, world, port_no, name, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    mats = W.make_small(name)
+    B = mats[1] if len(mats) > 1 else mats[0]
+    ref = bsum_reference(B)
+    for rank, bounds, dims, arrays in res:
+        assert bounds[0][0] == 0 and bounds[-1][1] == B.rows and all(b[0] % 16 == 0 for b in bounds)
+        assert dims == ref["dims"]
+        for n in arrays:
+            want = ref[n].view(np.int32 if ref[n].dtype == np.uint32 else np.int16)
+            assert np.array_equal(arrays[n], want), (rank, n)

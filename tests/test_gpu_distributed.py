@@ -3,7 +3,9 @@ multi-GPU step of bench.py with the real CUDA library per rank.  Rank 0
 broadcasts B, each rank multiplies its work-balanced A panel on the GPU
 (converting only the B tile rows its panel refers to), the offsets come from
 an all-gather, and the concatenated panels equal the single-call product
-bit for bit."""
+bit for bit.  General-row configs also run the B-summary
+exchange: each rank summarises its row panel of B and the panels are
+all-gathered (distributed.gather_b_summary, tsg_spgemm_bsum)."""
 import os
 import socket
 
@@ -25,7 +27,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port_no, name, q):
+def _worker(rank, world, port_no, name, q, use_bsum=False):
     import torch
     import torch.distributed as dist
     from paper_2009_14600_b200.tilemul import Context, Csr
@@ -39,7 +41,15 @@ def _worker(rank, world, port_no, name, q):
         Bh = Csr(Bb.rows, Bb.cols, Bb.row_ptr.numpy(), Bb.col.numpy(), Bb.val.numpy())
         r0, r1 = D.panel_bounds(A, Bh, world)[rank]
         ctx = Context(device=0)
-        Cp = ctx.spgemm(D.take_rows(A, r0, r1).to_device("cuda"), Bd).C
+        Ap = D.take_rows(A, r0, r1).to_device("cuda")
+        if use_bsum:  # this rank summarises its panel of B; the panels are all-gathered
+            b0, b1 = D.b_panel_bounds(Bh, world)[rank]
+            part = ctx.b_summary(D.take_rows(Bh, b0, b1).to_device("cuda"))
+            full = D.gather_b_summary(part, dist, "cuda")
+            Cp = ctx.spgemm_bsum(Ap, Bd, full).C
+            part.free()
+        else:
+            Cp = ctx.spgemm(Ap, Bd).C
         off, total = D.global_offsets(Cp.nnz, "cpu", dist)
         q.put((rank, off, total, Cp.row_ptr, Cp.col, Cp.val, r1 - r0))
         ctx.close()
@@ -47,12 +57,13 @@ def _worker(rank, world, port_no, name, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("name", ["fem27", "rect", "amg"])
-def test_two_rank_gpu_panels_equal_single_call(ctx, name):
+@pytest.mark.parametrize("name,use_bsum", [("fem27", False), ("rect", False), ("amg", False),
+                                           ("rect", True), ("rmat", True)])
+def test_two_rank_gpu_panels_equal_single_call(ctx, name, use_bsum):
     mpc = mp.get_context("spawn")
     q = mpc.Queue()
     port_no = _free_port()
-    procs = [mpc.Process(target=_worker, args=(r, 2, port_no, name, q)) for r in range(2)]
+    procs = [mpc.Process(target=_worker, args=(r, 2, port_no, name, q, use_bsum)) for r in range(2)]
     for p in procs:
         p.start()
     res = sorted((q.get(timeout=600) for _ in range(2)), key=lambda x: x[0])

@@ -310,3 +310,68 @@ def test_tiles8_conversion_errors(ctx):
     bad["tile_row"] = t["tile_row"][::-1].copy()  # unsorted tile rows
     with pytest.raises(T.InvariantError):
         ctx.tiles8_to_csr(M.rows, M.cols, bad)
+
+
+# ---------------------------------------------------------------- B summaries (multi-GPU exchange)
+def _as_np(bs):
+    return {n: bs.arrays[n].cpu().numpy() for n in bs.arrays}
+
+
+@pytest.mark.parametrize("case", ["rmat_small", "rmat14", "rect"])
+def test_b_summary_matches_restatement(ctx, case):
+    from paper_2009_14600_b200.tilemul import BSummary
+    from paper_2009_14600_b200 import distributed as D
+    from tests.helpers import bsum_reference
+    B = {"rmat_small": lambda: W.make_small("rmat")[0], "rmat14": lambda: W.rmat(14, 16, seed=5),
+         "rect": lambda: W.make_small("rect")[1]}[case]()
+    ref = bsum_reference(B)
+    whole = ctx.b_summary(B)
+    got = _as_np(whole)
+    assert (whole.rows, whole.tile_rows, whole.tiles, whole.nnz) == ref["dims"]
+    for n in got:
+        want = ref[n].view(np.int32 if ref[n].dtype == np.uint32 else np.int16)
+        assert np.array_equal(got[n], want), n
+    # panels summarised separately and concatenated = the whole
+    parts = [ctx.b_summary(D.take_rows(B, r0, r1)) for r0, r1 in D.b_panel_bounds(B, 3)]
+    cat = _as_np(BSummary.concat(parts))
+    for n in got:
+        assert np.array_equal(cat[n], got[n]), n
+    for p in parts:
+        p.free()
+    whole.free()
+
+
+@pytest.mark.parametrize("case", ["rmat14", "rect", "fem27_light"])
+def test_spgemm_with_gathered_b_summary(ctx, case):
+    """tsg_spgemm_bsum on an A panel with B's summary assembled from three row
+    panels (the N-GPU exchange) equals tsg_spgemm: CSR bits and T=16 counters."""
+    from paper_2009_14600_b200.tilemul import BSummary
+    from paper_2009_14600_b200 import distributed as D
+    if case == "rmat14":
+        A = B = W.rmat(14, 16, seed=5)
+    elif case == "rect":
+        A, B = W.make_small("rect")
+    else:
+        A = B = W.make_small("fem27")[0]
+    full = BSummary.concat([ctx.b_summary(D.take_rows(B, r0, r1)) for r0, r1 in D.b_panel_bounds(B, 3)])
+    for r0, r1 in D.panel_bounds(A, B, 2):
+        Ap = D.take_rows(A, r0, r1)
+        for mode in ("tensor", "ordered"):
+            want = ctx.spgemm(Ap, B, mode=mode)
+            got = ctx.spgemm_bsum(Ap, B, full, mode=mode)
+            assert np.array_equal(np.asarray(got.C.row_ptr), np.asarray(want.C.row_ptr))
+            assert np.array_equal(np.asarray(got.C.col), np.asarray(want.C.col))
+            assert np.array_equal(np.asarray(got.C.val, np.float32).view(np.uint32),
+                                  np.asarray(want.C.val, np.float32).view(np.uint32))
+            for k in ("raw_pairs", "filtered_pairs", "segments", "counted_elements", "nnz_c"):
+                assert got.stats[k] == want.stats[k], k
+            assert got.stats["path"] == want.stats["path"]
+
+
+def test_b_summary_mismatch_raises(ctx):
+    from paper_2009_14600_b200 import distributed as D
+    A = W.rmat(12, 8, seed=2)
+    part = ctx.b_summary(D.take_rows(A, 0, 1024))
+    with pytest.raises(T.DimensionError):
+        ctx.spgemm_bsum(A, A, part)
+    part.free()
