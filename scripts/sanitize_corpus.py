@@ -56,6 +56,13 @@ def main():
     back = ctx.tiles8_to_csr(M.rows, M.cols, t8)
     assert np.array_equal(np.asarray(back.col), np.asarray(M.col))
     n += 1
+    # B summaries of row panels, gathered, and the product through them (tsg_bsum)
+    from paper_2009_14600_b200 import distributed as D
+    from paper_2009_14600_b200.tilemul import BSummary
+    Rm = W.rmat(scale=11, edge_factor=8)
+    full = BSummary.concat([ctx.b_summary(D.take_rows(Rm, r0, r1)) for r0, r1 in D.b_panel_bounds(Rm, 3)])
+    assert same(ctx.spgemm_bsum(Rm, Rm, full).C, ctx.spgemm(Rm, Rm).C)
+    n += 1
     multi = T.Context(devices=[0, 0, 0])
     A = W.rmat(scale=11, edge_factor=8)
     assert same(multi.spgemm(A, A).C, ctx.spgemm(A, A).C)
