@@ -375,3 +375,44 @@ def test_b_summary_mismatch_raises(ctx):
     with pytest.raises(T.DimensionError):
         ctx.spgemm_bsum(A, A, part)
     part.free()
+
+
+# ---------------------------------------------------------------- exact cancellation, device output
+@pytest.mark.parametrize("mode", ["tensor", "ordered"])
+def test_light_pass_cancellation_device_output(ctx, mode):
+    """Rows whose sums cancel exactly (a B row and its negation) realise fewer
+    entries than their structural count: the device-output light pass drops
+    them like compact() and counted_elements stays structural."""
+    rng = np.random.default_rng(3)
+    n = 300
+    A = ref.random_coo(21, n, n, 0.03, "signed_halves")
+    rp, col = np.asarray(A.row_ptr), np.asarray(A.col)
+    val = np.asarray(A.val, np.float64).copy()
+    # rows 5, 17, 200: two entries k1 < k2 with B rows k1 and k2 equal up to sign
+    # -> C(r, :) = a(k1) B(k1,:) + a(k2) B(k2,:) cancels where the B rows overlap
+    dense = np.zeros((n, n))
+    for r in range(n):
+        dense[r, col[rp[r]:rp[r + 1]]] = val[rp[r]:rp[r + 1]]
+    for r in (5, 17, 200):
+        dense[r, :] = 0
+        dense[r, 10] = 1.0
+        dense[r, 11] = 1.0
+    dense[11, :] = -dense[10, :]
+    dense[10, 3] = 2.0
+    dense[11, 3] = -2.0
+    M = T.Csr(n, n, *(lambda d: (np.concatenate([[0], np.cumsum((d != 0).sum(1))]).astype(np.int64),
+                               np.nonzero(d)[1].astype(np.int32), d[d != 0]))(dense))
+    got = ctx.spgemm(M.to_device(), M.to_device(), mode=mode, out="device")
+    want = ref.spgemm(M)  # the compiled reference: compact() drops the cancelled slots
+    C = got.C.to_numpy()
+    assert np.array_equal(np.asarray(C.row_ptr), want.row_ptr)
+    assert np.array_equal(np.asarray(C.col), want.col)
+    if mode == "ordered":
+        assert np.array_equal(np.asarray(C.val, np.float32).view(np.uint32),
+                              want.val.astype(np.float32).view(np.uint32))
+    assert got.stats["counted_elements"] == want.counted
+    assert got.stats["nnz_c"] == len(want.col) < got.stats["counted_elements"]
+    assert got.stats["mem_output"] == (n + 1) * 8 + got.stats["nnz_c"] * 8
+    # host output agrees
+    host = ctx.spgemm(M, M, mode=mode)
+    assert np.array_equal(np.asarray(host.C.col), np.asarray(C.col))
