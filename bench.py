@@ -229,13 +229,14 @@ def run_ours(args):
         parts = [torch.from_numpy(np.ascontiguousarray(M.row_ptr, dtype=np.int64)),
                  torch.from_numpy(np.ascontiguousarray(M.col, dtype=np.int32)), val]
         sizes = [t.numel() * t.element_size() for t in parts]
-        flat = torch.empty(sum(sizes), dtype=torch.uint8, device=dev)
+        pads = [(n + 7) // 8 * 8 for n in sizes]  # every part 8-byte aligned (f64 values)
+        flat = torch.empty(sum(pads), dtype=torch.uint8, device=dev)
         views, o = [], 0
-        for t, n in zip(parts, sizes):
+        for t, n, pn in zip(parts, sizes, pads):
             v = flat[o:o + n].view(t.dtype)
             v.copy_(t.to(dev))
             views.append(v)
-            o += n
+            o += pn
         return Csr(M.rows, M.cols, *views), flat
 
     A_dev, _ = dev_csr(Apanel)

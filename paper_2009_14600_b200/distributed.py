@@ -74,11 +74,11 @@ def broadcast_csr(M: Csr | None, src: int, device, dist) -> Csr:
     vdt = {0: torch.float16, 1: torch.float32, 2: torch.float64}[dt]
     # one collective: row_ptr | col | val in a flat byte buffer
     esz = torch.empty(0, dtype=vdt).element_size()
-    sizes = [8 * (rows + 1), 4 * nnz, esz * nnz]
+    sizes = [8 * (rows + 1), (4 * nnz + 7) // 8 * 8, esz * nnz]  # col padded: f64 values stay 8-byte aligned
     flat = torch.empty(sum(sizes), dtype=torch.uint8, device=device)
     o = [0, sizes[0], sizes[0] + sizes[1], sum(sizes)]
     rp = flat[o[0]:o[1]].view(torch.int64)
-    col = flat[o[1]:o[2]].view(torch.int32)
+    col = flat[o[1]:o[1] + 4 * nnz].view(torch.int32)
     val = flat[o[2]:o[3]].view(vdt)
     if rank == src:
         rp.copy_(torch.from_numpy(np.ascontiguousarray(M.row_ptr, np.int64)))
