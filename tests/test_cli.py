@@ -80,6 +80,38 @@ def test_stats_matches_reference_counters(tmp_path):
     assert s["nnzCbarTilesRaw"] == st8["raw_pairs"] and s["nnzCbarTilesFiltered"] == st8["filtered_pairs"]
 
 
+def _advise_rules(s: dict, raw: bool) -> dict:
+    """advise (analytics.cpp:93-118): the published thresholds on the stats."""
+    pairs = s["nnzCbarTilesRaw"] if raw else s["nnzCbarTilesFiltered"]
+    ratio = s["nnzCbar"] / pairs if pairs else 0.0
+    nnz, avg = s["nnzA"], s["avgRow"]
+    return {"cuSPARSE": nnz > 200000, "CUSP": ratio >= 1.0, "RMerge2": avg > 42 and nnz > 100000,
+            "Nsparse": avg > 42 and nnz > 100000, "AC-SpGEMM": ratio > 9.0, "spECK": avg > 42 and nnz > 300000,
+            "global": nnz > 300000 and avg > 42, "globalRelaxed": nnz > 300000 and avg > 21}
+
+
+@pytest.mark.parametrize("raw", [False, True])
+def test_advise_evaluates_thresholds_on_stats(tmp_path, raw):
+    """`advise --json` (tilemul.cpp:146-162): the eight approaches in the
+    reference's order with their conditions, recommended per the thresholds
+    on the same statistics `stats` prints."""
+    import json
+    d = G.load("cli_5150")
+    A = G.csr(d, "A")
+    write_mtx(tmp_path / "a.mtx", A)
+    s = json.loads(run("stats", "--input", str(tmp_path / "a.mtx"), "--json").stdout)
+    args = ["advise", "--input", str(tmp_path / "a.mtx"), "--json"] + (["--raw-tile-ratio"] if raw else [])
+    r = run(*args)
+    assert r.returncode == 0, r.stderr
+    adv = json.loads(r.stdout)
+    want = _advise_rules(s, raw)
+    assert [e["approach"] for e in adv] == list(want)
+    assert {e["approach"]: e["recommended"] for e in adv} == want
+    assert all(e["condition"] for e in adv)
+    table = run("advise", "--input", str(tmp_path / "a.mtx")).stdout.splitlines()
+    assert table[0].startswith("approach") and len(table) == 9
+
+
 def test_exit_codes(tmp_path):
     """tilemul.cpp:285-306 / acceptance criterion 10 (acceptance.cpp:489-515)."""
     (tmp_path / "bad.mtx").write_text("not a banner\n")

@@ -6,6 +6,7 @@
 //                       [--pairing on|off] [--threads N] [--numerics ordered|tensor]
 //   tilemul_gpu compare --input A.mtx [--mode fp64|mixed] [--numerics ...]
 //   tilemul_gpu stats   --input A.{mtx,tspz} [--json]
+//   tilemul_gpu advise  --input A.{mtx,tspz} [--json] [--raw-tile-ratio]
 //   tilemul_gpu bench   --input A.{mtx,tspz} [--iters K] [--threads N] [--csv out.csv]
 //                       [--numerics ...]
 //
@@ -17,8 +18,8 @@
 // .tspz bytes and `bench` the same FNV-1a output hash; `--numerics tensor`
 // uses the tensor-core path (pattern-exact, values within DESIGN.md 5).
 // `--pairing` and `--threads` are accepted for compatibility (16x16 tiles
-// need no pairing; the GPU grid replaces the thread pool).  `advise` is the
-// paper-analysis advisor (analytics.cpp:93-118), out of scope here.
+// need no pairing; the GPU grid replaces the thread pool).  `stats` and
+// `advise` (analytics.cpp:16-118) are host analyses at the reference's T = 8.
 #include <algorithm>
 #include <chrono>
 #include <cstdint>
@@ -242,35 +243,40 @@ int cmd_compare(const Args& a) {
 }
 
 // Table-1 statistics (analytics.cpp:16-84) at the reference's T = 8.
-int cmd_stats(const Args& a) {
-  const std::filesystem::path in(a.get("--input"));
-  const TiledMatrix A = load_matrix(in, ElementKind::Fp32Stored);
+struct Stats {
+  std::uint64_t dims = 0, nnz_a = 0, nnz_c = 0, cbar = 0, c_tiles = 0, raw = 0, filt = 0;
+  double avg = 0, med = 0, mean = 0, sd = 0;
+};
+
+Stats compute_stats(const TiledMatrix& A) {
   if (A.rows != A.cols)
     throw DimensionError("statistics for A*A need a square matrix, got " + std::to_string(A.rows) + "x" +
                          std::to_string(A.cols));
-  std::uint64_t nnzc = 0, ctiles = 0, cbar = 0, raw = 0, filt = 0;
-  double med = 0, mean = 0, sd = 0;
+  Stats st;
+  st.dims = A.rows;
+  st.nnz_a = A.elements.size();
+  st.avg = A.rows ? double(A.elements.size()) / double(A.rows) : 0.0;
   if (!A.tiles.empty()) {
     std::vector<int> pops;
     for (const auto& t : A.tiles) pops.push_back(std::popcount(t.bitmap));
     std::sort(pops.begin(), pops.end());
-    med = pops[(pops.size() - 1) / 2];
-    for (int p : pops) mean += p;
-    mean /= double(pops.size());
-    for (int p : pops) sd += (p - mean) * (p - mean);
-    sd = std::sqrt(sd / double(pops.size()));
+    st.med = pops[(pops.size() - 1) / 2];
+    for (int p : pops) st.mean += p;
+    st.mean /= double(pops.size());
+    for (int p : pops) st.sd += (p - st.mean) * (p - st.mean);
+    st.sd = std::sqrt(st.sd / double(pops.size()));
   }
   const ElementCoo coo = to_element_coo(A);
   {
     std::vector<std::uint64_t> rn(A.rows, 0), cn(A.cols, 0);
     for (const auto& e : coo.entries) rn[e.row]++, cn[e.col]++;
-    for (std::uint64_t k = 0; k < A.rows; ++k) cbar += cn[k] * rn[k];
+    for (std::uint64_t k = 0; k < A.rows; ++k) st.cbar += cn[k] * rn[k];
     const ElementCoo C = host_product<double>(coo, coo, false);
-    nnzc = C.entries.size();
+    st.nnz_c = C.entries.size();
     std::vector<std::uint64_t> keys;
     for (const auto& e : C.entries) keys.push_back((e.row / 8) * ((A.cols / 8) + 1) + e.col / 8);
     std::sort(keys.begin(), keys.end());
-    ctiles = std::uint64_t(std::unique(keys.begin(), keys.end()) - keys.begin());
+    st.c_tiles = std::uint64_t(std::unique(keys.begin(), keys.end()) - keys.begin());
   }
   {  // tile pairs (pipeline.cpp:23-60): row starts of B's tile rows, O(1) filter
     std::vector<std::uint64_t> rs(A.tile_rows() + 1, 0);
@@ -288,24 +294,74 @@ int cmd_stats(const Args& a) {
     };
     for (const auto& ta : A.tiles)
       for (std::uint64_t j = rs[ta.tile_col]; j < rs[ta.tile_col + 1]; ++j) {
-        ++raw;
-        filt += (colocc(ta.bitmap) & rowocc(A.tiles[j].bitmap)) != 0;
+        ++st.raw;
+        st.filt += (colocc(ta.bitmap) & rowocc(A.tiles[j].bitmap)) != 0;
       }
   }
+  return st;
+}
+
+int cmd_stats(const Args& a) {
+  const std::filesystem::path in(a.get("--input"));
+  const TiledMatrix A = load_matrix(in, ElementKind::Fp32Stored);
+  const Stats st = compute_stats(A);
   const std::string name = in.stem().string();
-  const double avg = A.rows ? double(A.elements.size()) / double(A.rows) : 0.0;
   if (a.has("--json")) {
-    std::cout << "{\"matrixName\": \"" << name << "\", \"dims\": " << A.rows << ", \"nnzA\": " << A.elements.size()
-              << ", \"nnzC\": " << nnzc << ", \"nnzCbar\": " << cbar << ", \"nnzCTiles\": " << ctiles
-              << ", \"nnzCbarTilesRaw\": " << raw << ", \"nnzCbarTilesFiltered\": " << filt
-              << ", \"avgRow\": " << num(avg) << ", \"densityMedian\": " << num(med)
-              << ", \"densityMean\": " << num(mean) << ", \"densityStd\": " << num(sd) << "}\n";
+    std::cout << "{\"matrixName\": \"" << name << "\", \"dims\": " << st.dims << ", \"nnzA\": " << st.nnz_a
+              << ", \"nnzC\": " << st.nnz_c << ", \"nnzCbar\": " << st.cbar << ", \"nnzCTiles\": " << st.c_tiles
+              << ", \"nnzCbarTilesRaw\": " << st.raw << ", \"nnzCbarTilesFiltered\": " << st.filt
+              << ", \"avgRow\": " << num(st.avg) << ", \"densityMedian\": " << num(st.med)
+              << ", \"densityMean\": " << num(st.mean) << ", \"densityStd\": " << num(st.sd) << "}\n";
   } else {
     std::cout << "matrixName,dims,nnzA,nnzC,nnzCbar,nnzCTiles,nnzCbarTilesRaw,nnzCbarTilesFiltered,avgRow,"
                  "densityMedian,densityMean,densityStd\n"
-              << name << ',' << A.rows << ',' << A.elements.size() << ',' << nnzc << ',' << cbar << ',' << ctiles
-              << ',' << raw << ',' << filt << ',' << num(avg) << ',' << num(med) << ',' << num(mean) << ','
-              << num(sd) << "\n";
+              << name << ',' << st.dims << ',' << st.nnz_a << ',' << st.nnz_c << ',' << st.cbar << ',' << st.c_tiles
+              << ',' << st.raw << ',' << st.filt << ',' << num(st.avg) << ',' << num(st.med) << ','
+              << num(st.mean) << ',' << num(st.sd) << "\n";
+  }
+  return kExitOk;
+}
+
+// The paper's approach-selection thresholds evaluated on the statistics
+// (advise, analytics.cpp:93-118; output as cmd_advise, tilemul.cpp:146-162).
+// The intermediate ratio is C-bar over the filtered tile pairs, or the raw
+// ones with --raw-tile-ratio.
+int cmd_advise(const Args& a) {
+  const std::filesystem::path in(a.get("--input"));
+  const Stats st = compute_stats(load_matrix(in, ElementKind::Fp32Stored));
+  const std::uint64_t pairs = a.has("--raw-tile-ratio") ? st.raw : st.filt;
+  const double ratio = pairs ? double(st.cbar) / double(pairs) : 0.0;
+  struct Rule {
+    const char* approach;
+    const char* condition;
+    bool yes;
+  };
+  const Rule rules[] = {
+      {"cuSPARSE", "NNZ(A) > 200000", st.nnz_a > 200000},
+      {"CUSP", "NNZ(Cbar) / NNZ(Cbar_tiles) >= 1", ratio >= 1.0},
+      {"RMerge2", "avgRowA > 42 AND NNZ(A) > 100000", st.avg > 42.0 && st.nnz_a > 100000},
+      {"Nsparse", "avgRowA > 42 AND NNZ(A) > 100000", st.avg > 42.0 && st.nnz_a > 100000},
+      {"AC-SpGEMM", "NNZ(Cbar) / NNZ(Cbar_tiles) > 9", ratio > 9.0},
+      {"spECK", "avgRowA > 42 AND NNZ(A) > 300000", st.avg > 42.0 && st.nnz_a > 300000},
+      {"global", "NNZ(A) > 300000 AND avgRowA > 42", st.nnz_a > 300000 && st.avg > 42.0},
+      {"globalRelaxed", "NNZ(A) > 300000 AND avgRowA > 21", st.nnz_a > 300000 && st.avg > 21.0},
+  };
+  if (a.has("--json")) {
+    std::cout << "[";
+    bool first = true;
+    for (const auto& r : rules) {
+      std::cout << (first ? "\n" : ",\n") << "  {\n    \"approach\": \"" << r.approach << "\",\n    \"condition\": \""
+                << r.condition << "\",\n    \"recommended\": " << (r.yes ? "true" : "false") << "\n  }";
+      first = false;
+    }
+    std::cout << "\n]\n";
+    return kExitOk;
+  }
+  std::cout << "approach        recommended  condition\n";
+  for (const auto& r : rules) {
+    const std::string ap(r.approach);
+    std::cout << ap << std::string(16 - std::min<std::size_t>(16, ap.size()), ' ') << (r.yes ? "yes" : "no ")
+              << "          " << r.condition << "\n";
   }
   return kExitOk;
 }
@@ -361,9 +417,7 @@ int main(int argc, char** argv) {
     if (a.cmd == "compare") return cmd_compare(a);
     if (a.cmd == "stats") return cmd_stats(a);
     if (a.cmd == "bench") return cmd_bench(a);
-    load_matrix(std::filesystem::path(a.get("--input")), ElementKind::Fp32Stored);
-    std::cerr << "error: advise (the paper's approach advisor) is not part of the GPU build\n";
-    return kExitOther;
+    return cmd_advise(a);
   } catch (const UsageError& e) {
     std::cerr << "usage error: " << e.what() << "\n";
     return kExitOther;
