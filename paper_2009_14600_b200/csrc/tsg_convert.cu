@@ -16,11 +16,13 @@
 // than entries), so tile row I writes its tiles at gapped slots starting at
 // row_ptr[16 I]; a scan of the per-tile-row counts and tiles_compact_kernel
 // give the dense CSR-of-tiles afterwards.  Per tile row: the fast path ranks
-// tile columns with a shared-memory bitmap (or bitonic-sorts the entries when
-// the panel is wide or has many tiles), builds the 256-bit masks with
-// shared-memory atomics and stores each fp16 value straight into its
-// lane-dense operand chunk (A order and/or B order, tsg_common.cuh); panels
-// of more than 512 entries take the 16-way merge walk, one tile at a time.
+// tile columns with a shared-memory bitmap (or, when the panel is wide or has
+// many tiles, merges its 16 already-sorted row runs), builds the 256-bit
+// masks with shared-memory atomics and stores each fp16 value straight into
+// its lane-dense operand chunk (A order and/or B order, tsg_common.cuh);
+// panels of 512-8192 entries in a general call take convert_hub_kernel (a CTA
+// bitmap over the tile columns), the rest the 16-way merge walk, one tile at
+// a time.
 #include <algorithm>
 #include <type_traits>
 
