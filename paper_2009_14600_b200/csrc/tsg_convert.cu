@@ -310,6 +310,21 @@ __device__ __forceinline__ uint32_t sparse_panel(FastSmem& sm, const Gapped& out
   if (lane == 0) sm.ts[ntiles] = uint16_t(nk);
   const bool lite = __shfl_sync(kFull, lane == 0 ? general_call(out, ntiles, seen) : false, 0);
   __syncwarp();
+  if (lite) {  // the general path reads only each tile's column and occupancy
+    for (uint32_t t = lane; t < ntiles; t += 32) {
+      const uint32_t a = sm.ts[t], b = sm.ts[t + 1];
+      const uint32_t J = uint32_t(it[a] >> 40);
+      uint32_t co = 0, ro = 0;
+      for (uint32_t i = a; i < b; ++i) {
+        const unsigned long long x = it[i];
+        ro |= 1u << uint32_t((x >> 36) & 15u);
+        co |= 1u << uint32_t((x >> 32) & 15u);
+      }
+      mark_column(out, J);
+      out.rec[lite_role(roles)][E0 + t] = make_uint4(0u, 0u, co | (ro << 16), J);
+    }
+    return ntiles;
+  }
   // lanes emit tiles t = lane, lane + 32, ...; chunk bases by a warp scan
   uint32_t runA = 1u + uint32_t(E0), runB = 1u + uint32_t(E0);
   for (uint32_t t0 = 0; t0 < ntiles; t0 += 32) {
@@ -333,7 +348,7 @@ __device__ __forceinline__ uint32_t sparse_panel(FastSmem& sm, const Gapped& out
         lmB |= 1u << L;
       }
     }
-    const uint32_t nA = (roles & 1) && !lite ? __popc(lmA) : 0u, nB = (roles & 2) && !lite ? __popc(lmB) : 0u;
+    const uint32_t nA = (roles & 1) ? __popc(lmA) : 0u, nB = (roles & 2) ? __popc(lmB) : 0u;
     uint32_t iA = nA, iB = nB;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -355,10 +370,6 @@ __device__ __forceinline__ uint32_t sparse_panel(FastSmem& sm, const Gapped& out
       }
       const uint32_t occ = (colocc & 0xffffu) | (rowocc << 16);
       mark_column(out, J);
-      if (lite) {  // the general path reads only the tile column and occupancy (compaction: one role)
-        out.rec[lite_role(roles)][E0 + t] = make_uint4(0u, 0u, occ, J);
-        continue;
-      }
       uint4* dst = reinterpret_cast<uint4*>(out.rm2 + size_t(E0 + t) * 8);
       dst[0] = make_uint4(rm[0], rm[1], rm[2], rm[3]);
       dst[1] = make_uint4(rm[4], rm[5], rm[6], rm[7]);

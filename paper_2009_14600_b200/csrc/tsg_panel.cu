@@ -467,6 +467,11 @@ __global__ void __launch_bounds__(256, kMinBlocks) panel_numeric_kernel(TileMat 
 // positions (the 16 rows are consecutive in the CSR), each taken from its
 // row's staging region.  Non-finite values raise kErrPrecision
 // (finalize_segment, kernels.cpp:115-127).
+#ifndef TSG_COPY_U
+#define TSG_COPY_U 4
+#endif
+constexpr int kCopyU = TSG_COPY_U;  // staged entries per lane in flight
+
 __global__ void __launch_bounds__(256) panel_copy_kernel(int64_t rows, uint32_t tile_rows,
                                                         const uint32_t* __restrict__ row_stage,
                                                         const int64_t* __restrict__ row_ptr,
@@ -486,11 +491,11 @@ __global__ void __launch_bounds__(256) panel_copy_kernel(int64_t rows, uint32_t 
   const uint32_t off = row < r1 ? uint32_t(row_ptr[row] - base) : T;
   const uint32_t src0 = row < r1 ? row_stage[row] : 0u;
   bool bad = false;
-  // four entries per lane per step: the row lookups and loads first, then the stores
-  for (uint32_t q0 = 0; q0 < T; q0 += 128) {
-    uint2 e[4];
+  // kCopyU entries per lane per step: the row lookups and loads first, then the stores
+  for (uint32_t q0 = 0; q0 < T; q0 += 32 * kCopyU) {
+    uint2 e[kCopyU];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int u = 0; u < kCopyU; ++u) {
       const uint32_t q = q0 + 32 * u + lane;
       int r = 0;  // last row whose offset is <= q (empty rows resolve to the next one)
 #pragma unroll
@@ -502,7 +507,7 @@ __global__ void __launch_bounds__(256) panel_copy_kernel(int64_t rows, uint32_t 
       e[u] = q < T ? __ldg(stage + sr + (q - o)) : make_uint2(0, 0);
     }
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int u = 0; u < kCopyU; ++u) {
       const uint32_t q = q0 + 32 * u + lane;
       if (q < T) {
         const float x = __uint_as_float(e[u].x);
