@@ -1557,7 +1557,16 @@ void free_out(tsg_ctx* ctx, tsg_csr_out* C) {
 // in row order (byte-identical to one device: a C tile row depends only on
 // X0's tile row and the other operands).
 
-// work[I] = sum over X0's entries (r, k) in tile row I of nnz(X1 row k)
+// A tile row's cost for the panel split: its intermediate products w plus,
+// for the general path, the range searches of its work units (each unit of
+// ~kEscTarget products searches the B rows of all the tile row's entries)
+__host__ __device__ inline unsigned long long panel_cost(unsigned long long w, int64_t entries) {
+  constexpr double kSearchWeight = 0.6;  // one (entry, unit) search, in products (distributed.py SEARCH_WEIGHT)
+  const double units = w ? double((w + kEscTarget - 1) / kEscTarget) : 0.0;
+  return w + (unsigned long long)(kSearchWeight * units * double(entries));
+}
+
+// work[I] = panel_cost(sum over X0's entries (r, k) in tile row I of nnz(X1 row k), entries)
 __global__ void tile_row_work_kernel(CsrView A, const int64_t* __restrict__ rpB, unsigned long long* __restrict__ work) {
   const int lane = threadIdx.x & 31;
   const int64_t I = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5;
@@ -1571,7 +1580,7 @@ __global__ void tile_row_work_kernel(CsrView A, const int64_t* __restrict__ rpB,
     if (c >= 0 && c < A.cols) w += (unsigned long long)(rpB[c + 1] - rpB[c]);
   }
   for (int o = 16; o > 0; o >>= 1) w += __shfl_xor_sync(0xffffffffu, w, o);
-  if (lane == 0) work[I] = w;
+  if (lane == 0) work[I] = panel_cost(w, e1 - e0);
 }
 
 // dst[i] = src[i] - src[0] + add, i < n (a row-pointer slice rebased)
@@ -1602,7 +1611,7 @@ void rebase(const int64_t* src, int64_t n, int64_t add, int64_t* dst, cudaStream
 }
 
 // Panel boundaries (rows, 16-aligned): cut p = the first tile row whose
-// exclusive work prefix reaches p/n of the total (paper_2009_14600_b200/
+// exclusive cost prefix reaches p/n of the total (paper_2009_14600_b200/
 // distributed.py panel_bounds restates the same rule).
 std::vector<int64_t> panel_cuts(tsg_ctx* ctx, const tsg_csr* A, const tsg_csr* B, int n) {
   const int64_t T = (A->rows + 15) / 16;
@@ -1619,7 +1628,7 @@ std::vector<int64_t> panel_cuts(tsg_ctx* ctx, const tsg_csr* A, const tsg_csr* B
             const int32_t c = A->col[e];
             if (c >= 0 && c < A->cols) w += (unsigned long long)(B->row_ptr[c + 1] - B->row_ptr[c]);
           }
-          cum[I + 1] = w;
+          cum[I + 1] = panel_cost(w, A->row_ptr[r1] - A->row_ptr[I * 16]);
         }
       });
     for (auto& x : th) x.join();

@@ -468,7 +468,7 @@ __global__ void __launch_bounds__(256, kMinBlocks) panel_numeric_kernel(TileMat 
 // row's staging region.  Non-finite values raise kErrPrecision
 // (finalize_segment, kernels.cpp:115-127).
 #ifndef TSG_COPY_U
-#define TSG_COPY_U 4
+#define TSG_COPY_U 8
 #endif
 constexpr int kCopyU = TSG_COPY_U;  // staged entries per lane in flight
 
