@@ -34,7 +34,7 @@
 #include "tsg_kernels.cuh"
 
 namespace tsg {
-constexpr int kGatherMax = 32;  // scalars per gathered readback
+constexpr int kGatherMax = 48;  // scalars per gathered readback (3 + 2 (kPipeChunks + 1) at most)
 constexpr int kPipeChunks = 16;  // max tile-row chunks of the pipelined host-output path (TSG_PIPE, default 8)
 // Tuning switches for A/B runs: read from the environment once
 // per name and process; the defaults are the measured best.

@@ -1,4 +1,5 @@
 cd /root/repo
-TSG_DIST_BACKEND=gloo timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29555 bench.py --gpus 2 --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/bench_2rank_gloo.log 2>&1; echo "rc=$?" >> gpurun_out/bench_2rank_gloo.log
-TSG_DIST_BACKEND=gloo timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29556 bench.py --gpus 2 --steps 3 --warmup 3 --config rect --no-cpu-baseline > gpurun_out/bench_2rank_gloo_rect.log 2>&1; echo "rc=$?" >> gpurun_out/bench_2rank_gloo_rect.log
-timeout 900 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_ref.log 2>&1; echo "rc=$?" >> gpurun_out/bench_ref.log
+: > gpurun_out/pos_ab.log
+for v in 0 1; do echo "TSG_ESC_POS=$v" >> gpurun_out/pos_ab.log; TSG_ESC_POS=$v timeout 600 python scripts/cfg_time.py rmat rect --reps 5 >> gpurun_out/pos_ab.log 2>&1; done
+timeout 1200 python -m pytest tests -m gpu -x -q -p no:cacheprovider -k "rmat or rect or general or r02 or counters or summary or corpus" > gpurun_out/pytest_pos.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_pos.log
+bash scripts/launch_list.sh rmat
