@@ -353,14 +353,6 @@ __device__ __forceinline__ unsigned long long piece_base(const EscSmem& sm) {
 // Lockstep lower bounds: for each k, the first index of [b0[k], b1[k]) whose
 // column is >= c[k] (returned in b0).  The K searches issue their loads
 // together, so their latency chains overlap.
-// Binary steps until every range holds at most kLin entries, then one round
-// that loads them all and counts those below c (R-MAT's B rows hold ~16
-// entries: two dependent load rounds instead of four or five).
-#ifndef TSG_ESC_LIN
-#define TSG_ESC_LIN 8
-#endif
-constexpr uint32_t kLin = TSG_ESC_LIN;
-
 template <int K>
 __device__ __forceinline__ void lower_cols(const int32_t* __restrict__ colB, uint32_t (&b0)[K], uint32_t (&b1)[K],
                                            const uint32_t (&c)[K]) {
@@ -371,7 +363,7 @@ __device__ __forceinline__ void lower_cols(const int32_t* __restrict__ colB, uin
 #pragma unroll
     for (int k = 0; k < K; ++k) {
       m[k] = (b0[k] + b1[k]) >> 1;
-      if (b1[k] - b0[k] > kLin) {
+      if (b0[k] < b1[k]) {
         v[k] = uint32_t(__ldg(colB + m[k]));
         any = true;
       }
@@ -379,24 +371,12 @@ __device__ __forceinline__ void lower_cols(const int32_t* __restrict__ colB, uin
     if (!any) break;
 #pragma unroll
     for (int k = 0; k < K; ++k)
-      if (b1[k] - b0[k] > kLin) {
+      if (b0[k] < b1[k]) {
         if (v[k] < c[k])
           b0[k] = m[k] + 1;
         else
           b1[k] = m[k];
       }
-  }
-  if (kLin > 0) {
-    uint32_t cnt[K];
-#pragma unroll
-    for (int k = 0; k < K; ++k) {
-      cnt[k] = 0;
-#pragma unroll
-      for (uint32_t i = 0; i < kLin; ++i)
-        if (b0[k] + i < b1[k]) cnt[k] += uint32_t(__ldg(colB + b0[k] + i)) < c[k] ? 1u : 0u;  // sorted: a prefix
-    }
-#pragma unroll
-    for (int k = 0; k < K; ++k) b0[k] += cnt[k];
   }
 }
 
