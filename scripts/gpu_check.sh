@@ -14,3 +14,7 @@ if [ -n "$NCU" ]; then
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:"${KREGEX}" -s ${NSKIP:-2} -c ${NCAP:-1} \
       -o gpurun_out/prof_${TAG} -f python bench.py --steps 1 --warmup 1 --no-cpu-baseline > gpurun_out/ncu_full.log 2>&1
 fi
+# compute-sanitizer memcheck / racecheck / synccheck over the parity corpus
+# (summaries: gpurun_out/sanitizer_<tool>.txt, kept as profiles/r02_sanitizer_*)
+[ -n "$SANITIZE" ] && bash scripts/sanitize.sh
+true
