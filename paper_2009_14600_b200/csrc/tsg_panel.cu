@@ -467,6 +467,9 @@ __global__ void __launch_bounds__(256, kMinBlocks) panel_numeric_kernel(TileMat 
 // positions (the 16 rows are consecutive in the CSR), each taken from its
 // row's staging region.  Non-finite values raise kErrPrecision
 // (finalize_segment, kernels.cpp:115-127).
+#ifndef TSG_PANEL_KB
+#define TSG_PANEL_KB 4
+#endif
 #ifndef TSG_COPY_U
 #define TSG_COPY_U 8
 #endif
@@ -543,7 +546,7 @@ using PanelK = void (*)(TileMat, TileMat, int64_t, const uint32_t*, uint64_t, ui
                         unsigned*);
 template <int NL>
 PanelK pick_panel(int mode, bool emit) {
-  constexpr int kB = NL == 1 ? 4 : 3;  // resident blocks per SM (registers of the NL merge lists)
+  constexpr int kB = NL == 1 ? TSG_PANEL_KB : 3;  // resident blocks per SM (registers of the NL merge lists)
   if (mode == 1) return emit ? panel_numeric_kernel<true, kB, true, NL> : panel_numeric_kernel<true, kB, false, NL>;
   return emit ? panel_numeric_kernel<false, kB, true, NL> : panel_numeric_kernel<false, kB, false, NL>;
 }
