@@ -1276,7 +1276,7 @@ __device__ __forceinline__ uint32_t meets_count(const TileMat& B, uint32_t k, ui
         const uint32_t et = __ldg(B.etile + e);
         if (et != kNoTile) {
           const uint32_t t = et & ~kDupEntry;
-          atomicOr(&bm[t >> 5], 1u << (t & 31));
+          if (t < len) atomicOr(&bm[t >> 5], 1u << (t & 31));  // (a summary from another B cannot write past bm)
         }
       }
     }
