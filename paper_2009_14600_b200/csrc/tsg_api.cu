@@ -566,6 +566,9 @@ struct Call {
       raise_flags(v[0]);
       tA = v[2];
       tB = v[3];
+      if (bsum && tB != uint64_t(bsum->tiles))
+        throw Fail{TSG_ERR_DIMENSION, "B summary: tile counts sum to " + std::to_string(tB) + ", not its " +
+                                          std::to_string(bsum->tiles) + " tiles"};
       decide(v[1]);
     }
     record(ctx, timing, 1);
