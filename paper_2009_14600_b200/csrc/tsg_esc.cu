@@ -1108,6 +1108,11 @@ __device__ __forceinline__ int64_t piece_dst0(const PieceHdr& h, const int64_t* 
 
 // One staged piece -> its CSR slots: lanes over the piece's entries; entry q
 // belongs to the last row whose start within the piece is <= q.
+#ifndef TSG_ESC_COPY_U
+#define TSG_ESC_COPY_U 8
+#endif
+constexpr int kEscCopyU = TSG_ESC_COPY_U;
+
 __device__ __forceinline__ void copy_piece(const PieceHdr& h, int64_t dst0, int lane, const uint2* __restrict__ stage,
                                            int32_t* __restrict__ col, float* __restrict__ val) {
   uint32_t inc = h.cnt;  // each row's start within the piece
@@ -1118,16 +1123,16 @@ __device__ __forceinline__ void copy_piece(const PieceHdr& h, int64_t dst0, int 
   }
   const uint32_t total = __shfl_sync(kFull, inc, 15);
   const uint32_t start = inc - h.cnt;
-  // four entries per lane in flight: all loads first, then the row lookups and stores
-  for (uint32_t q0 = 0; q0 < total; q0 += 128) {
-    uint2 e[4];
+  // kEscCopyU entries per lane in flight: all loads first, then the row lookups and stores
+  for (uint32_t q0 = 0; q0 < total; q0 += 32 * kEscCopyU) {
+    uint2 e[kEscCopyU];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int u = 0; u < kEscCopyU; ++u) {
       const uint32_t q = q0 + 32 * u + lane;
       e[u] = q < total ? __ldg(stage + h.off + q) : make_uint2(0, 0);
     }
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int u = 0; u < kEscCopyU; ++u) {
       const uint32_t q = q0 + 32 * u + lane;
       if (q0 + 32 * u >= total) break;
       int r = 0;
