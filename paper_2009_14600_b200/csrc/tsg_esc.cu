@@ -1109,7 +1109,7 @@ __device__ __forceinline__ int64_t piece_dst0(const PieceHdr& h, const int64_t* 
 // One staged piece -> its CSR slots: lanes over the piece's entries; entry q
 // belongs to the last row whose start within the piece is <= q.
 #ifndef TSG_ESC_COPY_U
-#define TSG_ESC_COPY_U 8
+#define TSG_ESC_COPY_U 16
 #endif
 constexpr int kEscCopyU = TSG_ESC_COPY_U;
 

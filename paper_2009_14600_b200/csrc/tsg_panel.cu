@@ -471,7 +471,7 @@ __global__ void __launch_bounds__(256, kMinBlocks) panel_numeric_kernel(TileMat 
 #define TSG_PANEL_KB 4
 #endif
 #ifndef TSG_COPY_U
-#define TSG_COPY_U 8
+#define TSG_COPY_U 16
 #endif
 constexpr int kCopyU = TSG_COPY_U;  // staged entries per lane in flight
 
