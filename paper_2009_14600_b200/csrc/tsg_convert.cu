@@ -1067,10 +1067,21 @@ __global__ void __launch_bounds__(256) tiles_compact_kernel(CsrView in, uint32_t
   const uint32_t src = uint32_t(in.row_ptr[int64_t(I) * kTile]), dst = T.trp[I], n = g.ntiles[I];
   const int r0 = lite_role(roles);
   const bool lite = g.general && *g.general;  // final here: the conversion kernels are done
+  if (lite) {  // tile column + occupancy only; four records per lane in flight
+    for (uint32_t i0 = lane; i0 < n; i0 += 128) {
+      uint4 r[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (i0 + 32u * u < n) r[u] = g.rec[r0][src + i0 + 32u * u];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (i0 + 32u * u < n) T.tco[dst + i0 + 32u * u] = make_uint2(r[u].w, r[u].z);
+    }
+    return;
+  }
   for (uint32_t i = lane; i < n; i += 32) {
     const uint4 rec0 = g.rec[r0][src + i];
     T.tco[dst + i] = make_uint2(rec0.w, rec0.z);
-    if (lite) continue;
 #pragma unroll
     for (int role = 0; role < 2; ++role) {
       if (!(roles & (1 << role))) continue;
@@ -1079,7 +1090,6 @@ __global__ void __launch_bounds__(256) tiles_compact_kernel(CsrView in, uint32_t
       T.rec[role][dst + i] = rc;
     }
   }
-  if (lite) return;
   const uint4* s4 = reinterpret_cast<const uint4*>(g.rm2 + size_t(src) * 8);
   uint4* d4 = reinterpret_cast<uint4*>(T.rm2 + size_t(dst) * 8);
   for (uint32_t i = lane; i < 2 * n; i += 32) d4[i] = s4[i];
