@@ -125,3 +125,32 @@ def test_b_summary_all_gather_equals_whole_b(name):
         for n in arrays:
             want = ref[n].view(np.int32 if ref[n].dtype == np.uint32 else np.int16)
             assert np.array_equal(arrays[n], want), (rank, n)
+
+
+def _bcast_worker(rank, world, port_no, q):
+    import torch.distributed as dist
+    from paper_2009_14600_b200.tilemul import Csr
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port_no))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        rp = np.array([0, 2, 3, 5], np.int64)  # odd nnz with float64 values: the val section must stay aligned
+        M = Csr(3, 4, rp, np.array([0, 3, 1, 0, 2], np.int32), np.array([1.5, -2.0, 3.25, 4.0, -0.5]))
+        B = D.broadcast_csr(M if rank == 0 else None, 0, "cpu", dist)
+        q.put((rank, B.row_ptr.numpy().tolist(), B.col.numpy().tolist(), B.val.numpy().tolist()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_broadcast_csr_float64_odd_nnz():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port_no = _free_port()
+    procs = [ctx.Process(target=_bcast_worker, args=(r, 2, port_no, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(2)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for _, rp, col, val in res:
+        assert rp == [0, 2, 3, 5] and col == [0, 3, 1, 0, 2] and val == [1.5, -2.0, 3.25, 4.0, -0.5]
