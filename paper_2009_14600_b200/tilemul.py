@@ -311,15 +311,29 @@ class Context:
         return res
 
     def tiles8_to_csr(self, rows: int, cols: int, t: dict, out: str = "host") -> Csr:
-        """CSR of 8x8 tiles (arrays as csr_to_tiles8 returns them) on the GPU."""
-        arr = {k: np.ascontiguousarray(t[k], dt) for k, dt in
-               (("tile_row", np.uint32), ("tile_col", np.uint32), ("bitmap", np.uint64),
-                ("elem_index", np.uint64), ("val", np.float32))}
+        """CSR of 8x8 tiles (arrays as csr_to_tiles8 returns them: numpy, or
+        torch CUDA tensors of the same element sizes) on the GPU."""
+        names = (("tile_row", np.uint32), ("tile_col", np.uint32), ("bitmap", np.uint64),
+                 ("elem_index", np.uint64), ("val", np.float32))
+        device = hasattr(t["val"], "is_cuda") and t["val"].is_cuda
         v = L.tsg_tiles8()
-        v.rows, v.cols, v.ntiles, v.nnz = rows, cols, len(arr["tile_row"]), len(arr["val"])
-        for k, a in arr.items():
-            setattr(v, k, a.ctypes.data)
-        v.mem = L.TSG_MEM_HOST
+        if device:
+            import torch
+            torch.cuda.current_stream(t["val"].device).synchronize()  # the library's stream reads after torch's writes
+            arr = {k: t[k].contiguous() for k, _ in names}
+            for k, dt in names:
+                assert arr[k].element_size() == np.dtype(dt).itemsize, k
+            ptr = {k: a.data_ptr() for k, a in arr.items()}
+            n_t, n_e = arr["tile_row"].numel(), arr["val"].numel()
+            v.mem = L.TSG_MEM_DEVICE
+        else:
+            arr = {k: np.ascontiguousarray(t[k], dt) for k, dt in names}
+            ptr = {k: a.ctypes.data for k, a in arr.items()}
+            n_t, n_e = len(arr["tile_row"]), len(arr["val"])
+            v.mem = L.TSG_MEM_HOST
+        v.rows, v.cols, v.ntiles, v.nnz = rows, cols, n_t, n_e
+        for k, _ in names:
+            setattr(v, k, ptr[k])
         co = L.tsg_csr_out()
         co.mem = L.TSG_MEM_DEVICE if out == "device" else L.TSG_MEM_HOST
         rc = self._lib.tsg_tiles8_to_csr(self._h, C.byref(v), C.byref(co))

@@ -416,3 +416,22 @@ def test_light_pass_cancellation_device_output(ctx, mode):
     # host output agrees
     host = ctx.spgemm(M, M, mode=mode)
     assert np.array_equal(np.asarray(host.C.col), np.asarray(C.col))
+
+
+def test_tiles8_device_inputs(ctx):
+    """tsg_tiles8_to_csr from device arrays (TSG_MEM_DEVICE) equals the host-input call."""
+    import torch
+    M = ref.random_coo(13, 700, 500, 0.02, "signed_halves")
+    M = T.Csr(M.rows, M.cols, M.row_ptr, M.col, np.asarray(M.val, np.float32))
+    t = ctx.csr_to_tiles8(M)
+    dt = {"tile_row": torch.from_numpy(t["tile_row"].view(np.int32)).cuda(),
+          "tile_col": torch.from_numpy(t["tile_col"].view(np.int32)).cuda(),
+          "bitmap": torch.from_numpy(t["bitmap"].view(np.int64)).cuda(),
+          "elem_index": torch.from_numpy(t["elem_index"].view(np.int64)).cuda(),
+          "val": torch.from_numpy(t["val"]).cuda()}
+    a = ctx.tiles8_to_csr(M.rows, M.cols, t)
+    b = ctx.tiles8_to_csr(M.rows, M.cols, dt, out="device").to_numpy()
+    for x, y in ((a.row_ptr, b.row_ptr), (a.col, b.col)):
+        assert np.array_equal(np.asarray(x), np.asarray(y))
+    assert np.array_equal(np.asarray(a.val, np.float32).view(np.uint32), np.asarray(b.val, np.float32).view(np.uint32))
+    assert np.array_equal(np.asarray(a.col), np.asarray(M.col))
