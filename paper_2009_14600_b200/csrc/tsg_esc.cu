@@ -1296,44 +1296,71 @@ __device__ __forceinline__ uint32_t meets_count(const TileMat& B, uint32_t k, ui
 
 // Thread per A tile (warp per 32): raw pairs, and the filtered pairs of the
 // cheap cases; the warp counts its A tiles that need meets_count together.
+#ifndef TSG_PS_TILES
+#define TSG_PS_TILES 2
+#endif
+constexpr int kPsTiles = TSG_PS_TILES;  // A tiles per lane (their gathers in flight together)
+
 __global__ void __launch_bounds__(256) esc_pairstats_kernel(TileMat A, TileMat B, uint32_t tA,
                                                            const uint32_t* __restrict__ njt,
                                                            const uint32_t* __restrict__ rinfo,
                                                            unsigned long long* __restrict__ out) {
   const int lane = threadIdx.x & 31;
-  const uint32_t a0 = (blockIdx.x * 8 + (threadIdx.x >> 5)) * 32;
+  const uint32_t a0 = (blockIdx.x * 8 + (threadIdx.x >> 5)) * 32 * kPsTiles;
   if (a0 >= tA) return;
-  const uint32_t a = a0 + lane;
   unsigned long long raw = 0, filt = 0;
-  uint32_t K = 0, co = 0;
-  bool multi = false;
-  if (a < tA) {
-    const uint2 t = __ldg(A.tco + a);
-    K = t.x;
-    co = t.y & 0xffffu;
-    raw = __ldg(B.trp + K + 1) - __ldg(B.trp + K);
-    if (__popc(co) == 1) {
-      const int64_t row = int64_t(K) * 16 + (__ffs(co) - 1);
-      filt = row < B.rows ? __ldg(njt + row) : 0u;
-    } else if (co != 0 && raw != 0) {
-      const uint32_t info = __ldg(rinfo + K), rm = info & 0xffffu;
-      if ((co & rm) == rm) {  // every tile has an occupied row, all of them inside c
-        filt = raw;
-      } else if (co & rm) {
-        if (info & kSingleRows) {
-          for (uint32_t c = co & rm; c; c &= c - 1u) filt += __ldg(njt + size_t(K) * 16 + (__ffs(c) - 1));
+  uint32_t K[kPsTiles], co[kPsTiles], b0[kPsTiles], b1[kPsTiles], info[kPsTiles];
+  unsigned multi = 0;  // bit q: tile q of this lane needs meets_count
+  // (1) every gather of the lane's tiles in flight together
+#pragma unroll
+  for (int q = 0; q < kPsTiles; ++q) {
+    const uint32_t a = a0 + 32u * q + lane;
+    K[q] = 0;
+    co[q] = 0;
+    if (a < tA) {
+      const uint2 t = __ldg(A.tco + a);
+      K[q] = t.x;
+      co[q] = t.y & 0xffffu;
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < kPsTiles; ++q) {
+    const bool in = co[q] != 0u;
+    b0[q] = in ? __ldg(B.trp + K[q]) : 0u;
+    b1[q] = in ? __ldg(B.trp + K[q] + 1) : 0u;
+    info[q] = in && __popc(co[q]) > 1 ? __ldg(rinfo + K[q]) : 0u;
+  }
+  // (2) raw pairs and the cheap filtered cases
+#pragma unroll
+  for (int q = 0; q < kPsTiles; ++q) {
+    const uint32_t r = b1[q] - b0[q];
+    raw += r;
+    if (co[q] == 0u || r == 0u) continue;
+    if (__popc(co[q]) == 1) {
+      const int64_t row = int64_t(K[q]) * 16 + (__ffs(co[q]) - 1);
+      filt += row < B.rows ? __ldg(njt + row) : 0u;
+    } else {
+      const uint32_t rm = info[q] & 0xffffu;
+      if ((co[q] & rm) == rm) {  // every tile has an occupied row, all of them inside c
+        filt += r;
+      } else if (co[q] & rm) {
+        if (info[q] & kSingleRows) {
+          for (uint32_t c = co[q] & rm; c; c &= c - 1u) filt += __ldg(njt + size_t(K[q]) * 16 + (__ffs(c) - 1));
         } else {
-          multi = true;
+          multi |= 1u << q;
         }
       }
     }
   }
   __shared__ uint32_t s_bm[8][kPairBits / 32];
-  for (unsigned m = __ballot_sync(kFull, multi); m; m &= m - 1) {
-    const int src = __ffs(m) - 1;
-    const uint32_t n = meets_count(B, __shfl_sync(kFull, K, src), __shfl_sync(kFull, co, src),
-                                   s_bm[threadIdx.x >> 5], lane);
-    if (lane == src) filt += n;
+#pragma unroll
+  for (int q = 0; q < kPsTiles; ++q) {
+    for (unsigned m = __ballot_sync(kFull, (multi >> q) & 1u); m; m &= m - 1) {
+      const int src = __ffs(m) - 1;
+      const uint32_t n = meets_count(B, __shfl_sync(kFull, K[q], src), __shfl_sync(kFull, co[q], src),
+                                     s_bm[threadIdx.x >> 5], lane);
+      if (lane == src) filt += n;
+    }
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
@@ -1492,7 +1519,9 @@ void launch_esc_bsummary(const TileMat& B, uint32_t* njt, uint32_t* rinfo, cudaS
 
 void launch_esc_pairstats(const TileMat& A, const TileMat& B, uint64_t tA, const uint32_t* njt, const uint32_t* rinfo,
                           unsigned long long* out, cudaStream_t st) {
-  if (tA > 0) esc_pairstats_kernel<<<unsigned((tA + 255) / 256), 256, 0, st>>>(A, B, uint32_t(tA), njt, rinfo, out);
+  if (tA > 0)
+    esc_pairstats_kernel<<<unsigned((tA + 256 * kPsTiles - 1) / (256 * kPsTiles)), 256, 0, st>>>(A, B, uint32_t(tA), njt,
+                                                                                                rinfo, out);
 }
 
 void launch_bsum_tiles(const TileMat& B, uint64_t tiles, uint32_t* tile_count, uint16_t* ro, cudaStream_t st) {
