@@ -953,13 +953,15 @@ __global__ void esc_colcount_kernel(int64_t nnz, const int32_t* __restrict__ col
 __global__ void esc_colhist_kernel(int64_t rowsB, const int64_t* __restrict__ rpB, const int32_t* __restrict__ colB,
                                    const uint16_t* __restrict__ hB, const uint32_t* __restrict__ colcnt,
                                    unsigned long long* __restrict__ hist) {
-  const int lane = threadIdx.x & 31;
-  for (int64_t k = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5; k < rowsB;
-       k += (int64_t(gridDim.x) * blockDim.x) >> 5) {
-    const uint32_t w = __ldg(colcnt + k);
+  // eight lanes per B row, four rows per warp step (R-MAT rows hold ~16 entries)
+  const int lane = threadIdx.x & 31, sl = lane & 7;
+  for (int64_t k0 = ((blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5) * 4; k0 < rowsB;
+       k0 += ((int64_t(gridDim.x) * blockDim.x) >> 5) * 4) {
+    const int64_t k = k0 + (lane >> 3);
+    const uint32_t w = k < rowsB ? __ldg(colcnt + k) : 0u;
     if (!w) continue;
     const int64_t b1 = __ldg(rpB + k + 1);
-    for (int64_t e = __ldg(rpB + k) + lane; e < b1; e += 32)
+    for (int64_t e = __ldg(rpB + k) + sl; e < b1; e += 8)
       if (half_nz(__ldg(hB + e))) atomicAdd(hist + __ldg(colB + e), (unsigned long long)w);
   }
 }
