@@ -1564,7 +1564,7 @@ void free_out(tsg_ctx* ctx, tsg_csr_out* C) {
 // for the general path, the range searches of its work units (each unit of
 // ~kEscTarget products searches the B rows of all the tile row's entries)
 __host__ __device__ inline unsigned long long panel_cost(unsigned long long w, int64_t entries) {
-  constexpr double kSearchWeight = 0.6;  // one (entry, unit) search, in products (distributed.py SEARCH_WEIGHT)
+  constexpr double kSearchWeight = 0.9;  // one (entry, unit) search, in products (distributed.py SEARCH_WEIGHT)
   const double units = w ? double((w + kEscTarget - 1) / kEscTarget) : 0.0;
   return w + (unsigned long long)(kSearchWeight * units * double(entries));
 }

@@ -39,7 +39,7 @@ def row_work(A: Csr, B: Csr) -> np.ndarray:
 
 
 UNIT_PRODUCTS = 3584  # products per general-path work unit (tsg_kernels.cuh kEscTarget)
-SEARCH_WEIGHT = 0.6   # cost of one (A entry, work unit) range search, in products
+SEARCH_WEIGHT = 0.9   # cost of one (A entry, work unit) range search, in products
 
 
 def panel_bounds(A: Csr, B: Csr, world: int, tile: int = 16) -> list[tuple[int, int]]:
